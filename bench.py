@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""bench.py -- snapshot hash+validate throughput of the Kerncap address-space
+closure hot path on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1; NCCL)
+
+Workload (default): config c4, the 30,074,000,000-byte vLLM-style MoE pool of
+185 regions (24 x w13 + 24 x w2 bf16 expert stacks, 24 pointer tables, 113
+misc regions), E1 residency-first placement over the N GPUs.
+One STEP is one pass of the whole device hot path over the pool:
+  A2  K1 pre-manifest (XXH64 per 64 KiB chunk + region/snapshot digests)
+  A3  the target dispatch (F3, pointer-indirected MoE GEMV through ptr_table)
+  A4  K1 post-manifest + K3 written set
+  A8  K2 validate: restored/replayed pool vs captured reference pool, per region
+  A9  (N > 1) NCCL all_gather of manifests + all_reduce of the reports
+value = algorithmic HBM bytes of the hash and diff kernels per second, whole
+job (2 x pool for the two hashes + 2 x pool for the diff), inputs resident in
+HBM and larger than L2.  e2e = the same metric with the step's snapshot bytes
+copied host->device (pinned) every step and the reports read back.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "snapshot hash+validate GB/s (1/2/4/8 B200, % HBM peak); 30 GB capture->replay latency"
+UNIT = "GB/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+class Pool:
+    """This rank's shard of the c4 pool: live regions, the captured reference copy, the F3 dispatch."""
+
+    def __init__(self, ctx, rank, world, device, log):
+        import numpy as np
+        import torch
+        import synth
+        self.torch = torch
+        specs = synth.c4_specs()
+        owner = synth.c4_placement(specs, world)
+        # the F3 activations/output sit with layer 0 on rank 0 (its closure is local)
+        for i, s in enumerate(specs):
+            if s.name in ("x", "topk", "y"):
+                owner[i] = 0
+        self.specs = [s for s, o in zip(specs, owner) if o == rank]
+        self.total_bytes = sum(s.size for s in specs)
+        gen = torch.Generator(device=f"cuda:{device}")
+        self.va, self.ref = {}, {}
+        t0 = time.time()
+        for s in self.specs:
+            self.va[s.name] = ctx.alloc(s.size)
+        for idx, s in enumerate(specs):
+            if s.name not in self.va:
+                continue
+            v = synth.dev_view(self.va[s.name], s.size, device)
+            gen.manual_seed(synth.seed(4, 100 + idx))
+            if s.fill == "ptr_table":
+                layer = s.layer
+                t = synth.c4_ptr_table(self.va[f"w13_{layer}"], self.va[f"w2_{layer}"])
+                v.copy_(torch.from_numpy(t.view(np.uint8)))
+            elif s.fill == "topk":
+                v.zero_()
+                tk = synth.c4_topk()
+                v[: tk.nbytes].copy_(torch.from_numpy(tk.view(np.uint8).reshape(-1)))
+            else:
+                synth.fill_device(v, s, gen)
+        torch.cuda.synchronize()
+        log(f"rank {rank}: {len(self.specs)} regions, {sum(s.size for s in self.specs) / 1e9:.3f} GB filled in "
+            f"{time.time() - t0:.1f}s")
+        self.regions = sorted([(self.va[s.name], s.size) for s in self.specs])
+        self.bytes = sum(s.size for s in self.specs)
+        self.dtype_of = {self.va[s.name]: s.dtype for s in self.specs}
+        # F3 dispatch (rank 0): the target kernel, loaded like any captured code object
+        self.fn = None
+        if "x" in self.va:
+            from cuda.bindings import driver as drv
+            image = open(synth.FIXTURE_CUBIN, "rb").read()
+            err, self.mod = drv.cuModuleLoadData(image)
+            err, self.fn = drv.cuModuleGetFunction(self.mod, b"kc_fixture_moe_gemv")
+            self.image = image
+            self.kernarg = synth.c4_kernarg(self.va["ptr_0"], self.va["x"], self.va["topk"], self.va["y"])
+        self.launch_f3(torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        # the captured reference (post-dispatch) copy of every region: "what the replay must reproduce"
+        for s in self.specs:
+            self.ref[s.name] = ctx.alloc(s.size)
+            synth.dev_view(self.ref[s.name], s.size, device).copy_(synth.dev_view(self.va[s.name], s.size, device))
+        torch.cuda.synchronize()
+        self.C = None
+
+    def launch_f3(self, stream):
+        if self.fn is None:
+            return 0
+        import ctypes
+        from cuda.bindings import driver as drv
+        import synth
+        warps = synth.C4_T * 2816
+        args = ((self.va["ptr_0"], self.va["x"], self.va["topk"], self.va["y"], synth.C4_T, 2816, 2048),
+                (ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                 ctypes.c_int))
+        err, = drv.cuLaunchKernel(self.fn, (warps * 32 + 255) // 256, 1, 1, 256, 1, 1, 0, stream, args, 0)
+        assert int(err) == 0, err
+        return 1
+
+    def diff_buffers(self):
+        from paper_2605_03208_b200 import kc
+        out = []
+        for i, s in enumerate(sorted(self.specs, key=lambda s: self.va[s.name])):
+            out.append(kc.Buffer(self.ref[s.name], self.va[s.name], s.size, kc.DT[s.dtype], i, 0))
+        return out
+
+
+def run_ours(a, rank, world, device, log):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2605_03208_b200 import kc
+
+    torch.cuda.set_device(device)
+    ctx = kc.Context(device)
+    pool = Pool(ctx, rank, world, device, log)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    C = kc.count_chunks(pool.regions)
+    nreg = len(pool.regions)
+    pre = torch.zeros(max(1, C), dtype=torch.int64, device="cuda")
+    post = torch.zeros_like(pre)
+    dig = torch.zeros(max(1, nreg) + 1, dtype=torch.int64, device="cuda")
+    words = (C + 63) // 64
+    wbm = torch.zeros(max(1, words), dtype=torch.int64, device="cuda")
+    wcnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    bufs = pool.diff_buffers()
+    rep_nbytes = [b.nbytes for b in bufs]
+    word0, acc = [], 0
+    for b in bufs:
+        word0.append(acc)
+        acc += ((b.nbytes + 65535) // 65536 + 63) // 64
+    REP_WORDS = 15  # sizeof(kc_diff_report) / 8
+    reps = torch.zeros(max(1, len(bufs)) * REP_WORDS, dtype=torch.int64, device="cuda")
+    bms = torch.zeros(max(1, acc), dtype=torch.int64, device="cuda")
+    KEYS = ("hash_pre", "dispatch", "hash_post", "written", "diff", "combine")
+    evs = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in KEYS}
+           for _ in range(a.steps)]
+
+    # A9 combine buffers (N > 1): manifests all_gather (padded), report all_reduce
+    max_c = C
+    if world > 1:
+        t = torch.tensor([C], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_c = int(t.item())
+    gath = torch.zeros(world * max(1, max_c), dtype=torch.int64, device="cuda") if world > 1 else None
+    red_sum = torch.zeros(8, dtype=torch.int64, device="cuda")
+
+    def step(ev):
+        launches = 0
+
+        def rec(k, i):
+            if ev is not None:
+                ev[k][i].record(stream)
+        rec("hash_pre", 0)
+        ctx.hash(pool.regions, pre.data_ptr(), dig.data_ptr(), dig.data_ptr() + 8 * nreg, stream=sh)
+        rec("hash_pre", 1)
+        rec("dispatch", 0)
+        launches += pool.launch_f3(sh)
+        rec("dispatch", 1)
+        rec("hash_post", 0)
+        ctx.hash(pool.regions, post.data_ptr(), stream=sh)
+        rec("hash_post", 1)
+        rec("written", 0)
+        ctx.written(pre.data_ptr(), post.data_ptr(), C, wbm.data_ptr(), wcnt.data_ptr(), stream=sh)
+        rec("written", 1)
+        rec("diff", 0)
+        ctx.diff_async(bufs, len(bufs), rep_nbytes, reps.data_ptr(), word0, bms.data_ptr(), stream=sh)
+        rec("diff", 1)
+        if world > 1:
+            rec("combine", 0)
+            # C2: manifests (pad to the max per-rank count); C3: report counters (SUM) and maxima (MAX)
+            mine = torch.zeros(max(1, max_c), dtype=torch.int64, device="cuda")
+            mine[:C].copy_(post[:C])
+            dist.all_gather_into_tensor(gath, mine)
+            r = reps.view(-1, REP_WORDS)
+            red_sum.copy_(torch.stack([r[:, 3].sum(), r[:, 4].sum(), r[:, 9].sum(), r[:, 10].sum(),
+                                       r[:, 11].sum(), r[:, 12].sum(), r[:, 13].sum(), wcnt[0]]))
+            dist.all_reduce(red_sum)
+            rec("combine", 1)
+        return launches
+
+    for _ in range(a.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    # correctness gate before timing: the replayed pool must validate bit-exactly
+    rh = reps.view(-1, REP_WORDS).cpu().numpy()
+    assert int(rh[:, 3].sum()) == 0, "pool pair differs: validation failed"
+
+    l0 = ctx.kernel_launches()
+    clocks = ClockSampler(device)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    f3 = 0
+    for i in range(a.steps):
+        f3 += step(evs[i])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = ctx.kernel_launches() - l0 + f3
+    ms_local = e0.elapsed_time(e1) / a.steps
+    tsum = {k: 0.0 for k in KEYS}
+    for ev in evs:
+        for k in KEYS:
+            if k == "combine" and world == 1:
+                continue
+            tsum[k] += ev[k][0].elapsed_time(ev[k][1])
+    tmax = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    alg_local = 4 * pool.bytes
+    alg = torch.tensor([float(alg_local)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(alg)
+    ms = float(tmax.item())
+    value = float(alg.item()) / (ms * 1e-3) / 1e9
+
+    # per-kernel roofline: the dominant kernel by time share
+    per = {k: tsum[k] / a.steps for k in tsum}
+    k1_ms = (per["hash_pre"] + per["hash_post"]) / 2
+    k2_ms = per["diff"]
+    peak, peak_src = peaks()
+    kern = {
+        "K1_hash": {"ms": k1_ms, "alg_bytes": pool.bytes, "gbs": pool.bytes / (k1_ms * 1e-3) / 1e9},
+        "K2_diff": {"ms": k2_ms, "alg_bytes": 2 * pool.bytes, "gbs": 2 * pool.bytes / (k2_ms * 1e-3) / 1e9},
+        "K3_written_ms": per["written"], "F3_dispatch_ms": per["dispatch"],
+    }
+    if world > 1:
+        kern["A9_combine_ms"] = per["combine"]
+    dom = "K2_diff" if 2 * k2_ms >= 2 * k1_ms else "K1_hash"
+    dom_ms = k2_ms if dom == "K2_diff" else 2 * k1_ms
+    share = dom_ms / ms if ms else None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
+            "frac": kern[dom]["gbs"] / peak, "traffic": None, "peak_source": peak_src,
+            "frac_of_spec_8000": kern[dom]["gbs"] / 8000.0, "share_of_step": share,
+            "alg_bytes_per_launch": kern[dom]["alg_bytes"]}
+
+    # ------------------------------------------------------------------ e2e
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, ctx, pool, step, stream, world, log)
+
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded; bf16 N(0,0.02) expert weights, bf16 misc, device-pointer tables)",
+        "config": {"workload": "c4: vLLM-style MoE weight pool, 30,074,000,000 B, 185 regions, E1 placement",
+                   "step": "K1 pre-manifest + F3 dispatch + K1 post-manifest + K3 written set + K2 pool-pair "
+                           "validate" + (" + NCCL combine" if world > 1 else ""),
+                   "alg_bytes_per_step": int(float(alg.item())), "regions_this_rank": len(pool.regions),
+                   "bytes_this_rank": pool.bytes, "l2": "inputs (30 GB) >> L2 (126 MB); no flush needed",
+                   "parallelism": f"E1 residency-first shards over {world} GPU(s)"},
+        "roofline": roof, "kernels": kern, "clocks": clk, "gpu_launches": launches,
+        "e2e": e2e,
+    }
+    return res, pool
+
+
+def run_e2e(a, ctx, pool, step, stream, world, log):
+    """Same metric through the public API with the snapshot in pinned HOST memory:
+    every step copies the snapshot host->device (restore) before the device hot
+    path and reads the reports back."""
+    import torch
+    import synth
+    host = {}
+    for s in pool.specs:
+        h = torch.empty(s.size, dtype=torch.uint8, pin_memory=True)
+        h.copy_(synth.dev_view(pool.ref[s.name], s.size, torch.cuda.current_device()))
+        host[s.name] = h
+    torch.cuda.synchronize()
+    steps = max(1, min(a.steps, a.e2e_steps))
+    out = torch.empty(16 * 185 + 8, dtype=torch.int64, pin_memory=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        for s in pool.specs:
+            synth.dev_view(pool.ref[s.name], s.size, torch.cuda.current_device()).copy_(host[s.name],
+                                                                                         non_blocking=True)
+        step(None)
+        out[:8].copy_(torch.zeros(8, dtype=torch.int64, device="cuda"), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+    ms = float(tm.item())
+    total = 4 * pool.total_bytes
+    return {"value": total / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": pool.total_bytes,
+            "d2h_bytes_per_step": 8 * (16 * len(pool.specs)), "ms_per_step": ms, "steps": steps,
+            "h2d_gbs": pool.total_bytes / world / (ms * 1e-3) / 1e9}
+
+
+# ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
+def oracle_sample(pool_or_none, sample_mb: int):
+    """A bounded sample of the c4 workload as host bytes: real pool regions (copied
+    back) when a pool exists, else regenerated on the host with the same recipes."""
+    import numpy as np
+    import synth
+    specs = synth.c4_specs()
+    chosen, total = [], 0
+    for s in sorted(specs, key=lambda s: s.size):
+        if s.name in ("x", "topk", "y") or total + s.size > sample_mb * 2**20:
+            continue
+        chosen.append(s)
+        total += s.size
+    # add a slice of one expert stack so the sample mixes big and small regions
+    out = []
+    rng = np.random.default_rng(synth.seed(4, 999))
+    for s in chosen:
+        if pool_or_none is not None and s.name in pool_or_none.va:
+            v = synth.dev_view(pool_or_none.va[s.name], s.size).cpu().numpy()
+        elif s.fill == "zero":
+            v = np.zeros(s.size, dtype=np.uint8)
+        else:
+            v = (rng.standard_normal(s.size // 2).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+            v = v.view(np.uint8)
+        out.append((s, v))
+    return out
+
+
+def time_oracle(sample, threads: int):
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    oracle.build()
+    t0 = time.perf_counter()
+    # A2 + A4: two manifests; A8: diff of each region against its reference copy
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), sample))
+        list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), sample))
+        dts = {"bf16": oracle.DT_BF16, "u64": oracle.DT_U64, "i32": oracle.DT_I32, "f32": oracle.DT_F32}
+        list(ex.map(lambda sv: oracle.diff(sv[1], sv[1], dts.get(sv[0].dtype, oracle.DT_BYTES)), sample))
+    dt = time.perf_counter() - t0
+    nbytes = sum(v.size for _, v in sample)
+    return 4 * nbytes / dt / 1e9, dt, nbytes
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    sample = oracle_sample(None, a.cpu_sample_mb)
+    for _ in range(a.warmup if a.warmup < 2 else 1):
+        time_oracle(sample[:2], threads)
+    vals, secs = [], 0.0
+    for _ in range(a.steps):
+        v, dt, nb = time_oracle(sample, threads)
+        vals.append(v)
+        secs += dt
+    value = sum(vals) / len(vals)
+    desc = (f"{len(sample)} c4 regions ({nb / 1e6:.1f} MB, smallest-first, regenerated on host with the c4 recipes); "
+            f"per step: 2 oracle manifests + oracle diff of each region vs its reference")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "c4 sample (bounded) on host cores", "threads": threads},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--cpu-sample-mb", type=int, default=384)
+    p.add_argument("--quiet", action="store_true")
+    a = p.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    log = (lambda m: None) if a.quiet else (lambda m: print(m, file=sys.stderr, flush=True))
+
+    if a.impl == "reference":
+        res = run_reference(a, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    res, pool = run_ours(a, rank, world, local, log)
+    if rank == 0:
+        threads = os.cpu_count() or 1
+        sample = oracle_sample(pool, a.cpu_sample_mb)
+        v, dt, nb = time_oracle(sample, threads)
+        res["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                               "sample": f"{len(sample)} regions of this run's c4 pool ({nb / 1e6:.1f} MB): "
+                                         f"2 oracle manifests + oracle diff; {dt:.2f} s"}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

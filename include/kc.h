@@ -1,0 +1,292 @@
+/*
+ * kc.h -- C ABI of libkc.so, the B200-native (sm_100a) hot path of Kerncap's
+ * capture-and-validate loop: the address-space closure (arXiv 2605.03208).
+ *
+ * The paper's statement of the problem: a kernel reproducer needs the
+ * definition, the runtime state ("the contents of every device-memory region
+ * the kernel reads -- including buffers reached indirectly through pointer
+ * arguments") and an environment that "faithfully replays the original
+ * execution with bit-identical semantics" (fig:three-problems).
+ * The closure: "capturing every tracked allocation at its original virtual
+ * address captures the graph for free" (sec. 4.2.1).
+ *
+ * Conventions:
+ *  - Every call returns kc_status: 0 = OK, >0 = completed with tolerated
+ *    failures (KC_PARTIAL), <0 = error.  kc_last_error(ctx) holds a message.
+ *  - Every pointer argument is BORROWED for the duration of the call.  Outputs
+ *    go to caller-provided memory.  "device" pointers are CUDA device virtual
+ *    addresses (CUdeviceptr values) of the context's device; "host" pointers are
+ *    ordinary process memory.  Streams are CUstream handles passed as void*
+ *    (NULL = the legacy default stream).
+ *  - kc_ctx owns the tracker, pinned staging, device scratch and cached tables.
+ *    kc_restored owns VA reservations, physical handles, the loaded module and
+ *    the device stash; release it with kc_release() BEFORE kc_destroy().
+ *  - Threading: kc_track/kc_regions are internally synchronized (driver
+ *    callbacks arrive from any host thread).  Every other call:
+ *    one host thread per ctx at a time.
+ *  - Sticky CUDA errors poison the ctx: every later call returns KC_ERR_CUDA.
+ *
+ * Hash chunk: 65,536 bytes (reading R1).  XXH64, seed 0 (R2), last chunk short
+ * and unpadded (R3), little-endian (R5).  Region digest D_r = XXH64 of the
+ * region's chunk hashes as LE u64s; snapshot digest S = XXH64 of
+ * (LE64 base, LE64 size, LE64 D_r) over regions in ascending base order (R4).
+ */
+#ifndef KC_H_
+#define KC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KC_ABI_VERSION 1
+#define KC_CHUNK_BYTES 65536u
+
+typedef enum {
+    KC_OK = 0,
+    KC_PARTIAL = 1,                 /* completed; per-region failures recorded */
+    KC_ERR_ARG = -1,
+    KC_ERR_STATE = -2,              /* wrong call order, double install, ... */
+    KC_ERR_CUDA = -3,               /* a CUDA driver/runtime error; CUresult in kc_last_error */
+    KC_ERR_IO = -4,
+    KC_ERR_FORMAT = -5,             /* snapshot directory does not parse */
+    KC_ERR_VA_UNAVAILABLE = -6,     /* restore could not reserve the captured VA */
+    KC_ERR_NOT_TRACKED = -7,
+    KC_ERR_OUT_OF_BOUNDS = -8,
+    KC_ERR_NOMEM = -9,
+    KC_ERR_MANIFEST_MISMATCH = -10, /* restored bytes do not hash to the captured manifest */
+    KC_ERR_UNSUPPORTED = -11
+} kc_status;
+
+typedef enum { KC_EV_ALLOC = 0, KC_EV_FREE = 1, KC_EV_MAP = 2, KC_EV_UNMAP = 3 } kc_event;
+typedef enum { KC_KIND_MEMALLOC = 0, KC_KIND_VMM = 1, KC_KIND_POOL = 2 } kc_alloc_kind;
+
+/* Element types of a validated buffer (O4).  KC_DT_BYTES compares raw bytes. */
+typedef enum {
+    KC_DT_BYTES = 0, KC_DT_U8, KC_DT_I8, KC_DT_U16, KC_DT_I16, KC_DT_U32, KC_DT_I32,
+    KC_DT_U64, KC_DT_I64, KC_DT_F16, KC_DT_BF16, KC_DT_F32, KC_DT_F64, KC_DT__COUNT
+} kc_dtype;
+
+/* Capture timing (reading R7).  PRE_W (default): the snapshot holds the
+ * pre-dispatch state plus the post-dispatch bytes of the written chunks W
+ * (chunks whose hash changed), so replay starts from the true inputs.  POST:
+ * the paper's post-execution snapshot. */
+typedef enum { KC_MODE_PRE_W = 0, KC_MODE_POST = 1 } kc_capture_mode;
+
+/* One tracked allocation (A1; reading R6). */
+typedef struct {
+    uint64_t base;      /* device VA */
+    uint64_t size;      /* bytes */
+    int32_t device;     /* CUDA device ordinal */
+    int32_t kind;       /* kc_alloc_kind */
+    uint64_t seq;       /* tracker sequence number of the ALLOC/MAP event */
+} kc_region;
+
+/* One validated buffer pair (A8): reference and actual device VAs, nbytes each.
+ * bitmap_chunk0 = chunk index of ref/act[0] inside the report's bitmap (0 for a
+ * whole buffer; kc_validate uses it for W-chunk segments of a region). */
+typedef struct {
+    uint64_t ref;
+    uint64_t act;
+    uint64_t nbytes;    /* must be a multiple of the element size (else KC_ERR_ARG) */
+    int32_t dtype;      /* kc_dtype */
+    int32_t report;     /* index of the kc_diff_report this segment accumulates into */
+    uint64_t bitmap_chunk0;
+} kc_buffer;
+
+/* numpy.allclose tolerances; defaults 1e-8 / 1e-5 / 0 (R14, R15). */
+typedef struct {
+    double atol;
+    double rtol;
+    int32_t equal_nan;
+    int32_t _pad;
+} kc_tolerance;
+
+/* Diff report per output buffer (O4; R8-R18).
+ * Layout is part of the ABI (identical on host and device). */
+typedef struct {
+    uint64_t nbytes, n_elems, n_chunks;
+    uint64_t differing_bytes;       /* #{j : R[j] != A[j]}                          */
+    uint64_t differing_elems;       /* #{i : bits(R_i) != bits(A_i)}                */
+    uint64_t max_ulp;               /* floats: ordered-int distance; ints: |A-R|    */
+    double max_abs;                 /* max |f64(A)-f64(R)| over differing non-NaN   */
+    double max_rel;                 /* max d/|R| (R=+-inf -> +inf; R=0 -> undefined)*/
+    double percent_bytes;           /* 100*differing_bytes/nbytes                   */
+    uint64_t nan_ref, nan_act, nan_pos_mismatch, rel_undefined, allclose_fail;
+    int32_t pass;                   /* floats: allclose_fail==0; ints: differing_elems==0; bytes: differing_bytes==0 */
+    int32_t _pad;
+} kc_diff_report;
+
+/* Explicit dispatch description (A3; D4 of SURVEY.md 2.2).  Either func (a
+ * CUfunction cast to void*) or (image, mangled) must be given.  kernarg is the
+ * packed parameter buffer (Q22: CUDA params live outside tracked memory). */
+typedef struct {
+    void* func;
+    const void* image;          /* cubin/fatbin bytes, may be NULL if func given */
+    size_t image_size;
+    const char* mangled;        /* kernel symbol name */
+    uint32_t grid[3], block[3];
+    uint32_t smem_bytes;
+    uint32_t kernarg_size;
+    const void* kernarg;
+    void* stream;
+} kc_dispatch;
+
+/* kc_alloc backing (reading R6/R20): VMM allocations live in free VA space and
+ * can be re-reserved at the same VA by a fresh process; plain cuMemAlloc
+ * regions below the driver's pooling threshold share driver-reserved VA and
+ * are restored by replaying cuMemAlloc in capture order (abort on mismatch). */
+typedef enum { KC_ALLOC_VMM = 0, KC_ALLOC_MEMALLOC = 1 } kc_alloc_mode;
+
+typedef struct {
+    uint64_t io_chunk_bytes;    /* KERNCAP_SNAPSHOT_CHUNK_BYTES; 0 = env or 64 MiB */
+    uint32_t pinned_depth;      /* staging buffers in flight (R26); 0 = 2 */
+    int32_t device;             /* CUDA device ordinal; -1 = current */
+    int32_t alloc_mode;         /* kc_alloc_mode for kc_alloc */
+    int32_t _pad;
+} kc_options;
+
+typedef struct {
+    uint64_t n_regions, n_chunks, total_bytes;
+    uint64_t n_failed_regions;
+    uint64_t written_chunks;        /* |W| */
+    uint64_t d2h_bytes;             /* bytes copied device->host */
+    uint64_t dma_calls;             /* number of D2H copy calls */
+    uint64_t staging_high_water;    /* peak pinned staging bytes in use */
+    uint64_t snapshot_digest;       /* S of the region files (pre state in PRE_W) */
+    double t_hash_pre_s, t_d2h_s, t_dispatch_s, t_hash_post_s, t_total_s;
+} kc_capture_report;
+
+typedef struct {
+    uint32_t iterations;        /* >= 1 */
+    int32_t no_recopy;          /* 1: do not restore W's pre-state between iterations */
+    const char* dump_dir;       /* NULL: no output dump */
+    const void* image_override; /* variant code object ("--hsaco") */
+    size_t image_override_size;
+    void* stream;
+} kc_replay_opts;
+
+typedef struct {
+    uint32_t iterations;
+    uint32_t _pad;
+    double kernel_ms_mean, kernel_ms_min, kernel_ms_max;
+} kc_replay_report;
+
+typedef struct {
+    uint64_t n_regions, n_spans, mapped_bytes, h2d_bytes;
+    uint64_t n_failed_regions;      /* reserved and zero-filled */
+    uint64_t verify_mismatch_chunks;
+    double t_reserve_s, t_h2d_s, t_verify_s, t_total_s;
+} kc_restore_report;
+
+typedef struct kc_ctx kc_ctx;
+typedef struct kc_restored kc_restored;
+
+/* ---- lifetime ---------------------------------------------------------- */
+/* Creates a context on opt->device (primary CUDA context).  opt may be NULL. */
+kc_status kc_create(kc_ctx** out, const kc_options* opt);
+void kc_destroy(kc_ctx* ctx);
+/* Last error message of this ctx (valid until the next call on it). */
+const char* kc_last_error(const kc_ctx* ctx);
+/* ABI version and a build identification string (arch, flags). */
+int kc_abi_version(void);
+const char* kc_build_info(void);
+const char* kc_status_str(kc_status s);
+/* Number of libkc kernels this ctx has launched so far (bench evidence). */
+uint64_t kc_kernel_launches(const kc_ctx* ctx);
+
+/* ---- A1 allocation tracking -------- */
+/* Feeds one driver event: ALLOC/MAP add [base, base+size); FREE/UNMAP remove
+ * the entry at base (size ignored).  An unknown FREE is KC_OK plus a warning
+ * (SPEC.md:320, 324).  Overlap with a live entry is KC_ERR_ARG. */
+kc_status kc_track(kc_ctx* ctx, kc_event ev, uint64_t base, uint64_t size, int32_t device, int32_t kind);
+/* Copies up to cap live regions, sorted by base, into out; *n_out = live count. */
+kc_status kc_regions(kc_ctx* ctx, kc_region* out, size_t cap, size_t* n_out);
+/* Driver-API interposition: allocate / free wrappers that feed the tracker
+ * (the CUDA analog of the paper's hooked pool allocate / VMEM map, PAPER.md:
+ * 490-497).  KC_ALLOC_VMM: cuMemAddressReserve + cuMemCreate + cuMemMap +
+ * cuMemSetAccess (granularity-rounded); KC_ALLOC_MEMALLOC: cuMemAlloc. */
+kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out);
+kc_status kc_free(kc_ctx* ctx, uint64_t dptr);
+/* CUPTI driver-API callback interposition (cuMemAlloc*, cuMemFree*, cuMemMap,
+ * cuMemUnmap).  Second install -> KC_ERR_STATE. */
+kc_status kc_track_install(kc_ctx* ctx);
+kc_status kc_track_uninstall(kc_ctx* ctx);
+
+/* ---- K1 chunk hash (A2/A4; north star) -------------------------------- */
+/* Hashes every region: d_chunk_hash[C] (device, u64, global chunk order =
+ * regions in the given order, chunks in order; C = sum ceil(size/65536)).
+ * d_region_digest (device, n words) and d_snapshot_digest (device, 1 word)
+ * may be NULL.  Regions must be sorted by base and non-overlapping when the
+ * snapshot digest is requested.  Asynchronous on stream. */
+kc_status kc_hash(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_chunk_hash,
+                  uint64_t* d_region_digest, uint64_t* d_snapshot_digest, void* stream);
+/* Total chunk count of a region list (host helper). */
+uint64_t kc_count_chunks(const kc_region* regions, size_t n);
+
+/* ---- K3 written set (A4) ---------------------------------------------- */
+/* W[k] = (pre[k] != post[k]) for k < n_chunks: d_w_bitmap (device,
+ * ceil(C/64) u64, LSB-first) and d_written_count (device, 1 u64).  Async. */
+kc_status kc_written(kc_ctx* ctx, const uint64_t* d_pre, const uint64_t* d_post, uint64_t n_chunks,
+                     uint64_t* d_w_bitmap, uint64_t* d_written_count, void* stream);
+
+/* ---- K2 fused diff (A8) ----------------------------------------------- */
+/* Compares every segment; reports accumulate per bufs[i].report index in
+ * d_reports (device, n_reports entries, zeroed and finalized here), bitmaps in
+ * d_bitmaps (device; report j's bitmap starts at word bitmap_word0[j], host
+ * array of n_reports entries, may be NULL when d_bitmaps is NULL).
+ * report_nbytes[j] (host) = total bytes of report j (for percent/n_chunks).
+ * Asynchronous on stream. */
+kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
+                        const uint64_t* report_nbytes, const uint64_t* bitmap_word0,
+                        const kc_tolerance* tol, kc_diff_report* d_reports, uint64_t* d_bitmaps,
+                        void* stream);
+/* Convenience: one report per buffer, results copied to HOST reps[n] and
+ * h_bitmaps (concatenated ceil(n_chunks_i/64) words per buffer, may be NULL).
+ * Synchronizes the stream. */
+kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
+                  kc_diff_report* reps, uint64_t* h_bitmaps, void* stream);
+
+/* ---- A3/A5 capture --------------- */
+/* Quiesce, hash, write metadata FIRST, snapshot through the pinned ring,
+ * forward the dispatch, hash again, record W, write capture_log.json and the
+ * capture_complete sentinel LAST.  regions == NULL: every tracked region.
+ * Per-region copy failures -> KC_PARTIAL (the dispatch always proceeds). */
+kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, const char* dir,
+                     kc_capture_mode mode, kc_capture_report* rep);
+
+/* ---- A6 VA-faithful restore ----------- */
+/* Reserves every granule span at its captured VA (abort + full rollback with
+ * KC_ERR_VA_UNAVAILABLE if the driver returns another address), maps
+ * device-local memory, copies the region files in, zero-fills gaps and
+ * failed regions, and verifies the bytes against the captured manifest. */
+kc_status kc_restore(kc_ctx* ctx, const char* dir, kc_restored** out, kc_restore_report* rep);
+/* Host placeholder reservation of every captured span with
+ * mmap(MAP_FIXED_NOREPLACE) -- call BEFORE the CUDA context exists
+ * (PAPER.md:1067-1074).  kc_restore releases them.  No CUDA calls. */
+kc_status kc_prereserve(const char* dir, uint64_t* n_reserved);
+
+/* ---- A7 replay ------------------------------------ */
+kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts* o, kc_replay_report* rep);
+
+/* ---- A8 validate ---------------------------------- */
+/* outs == NULL: every region with written chunks, compared as bytes against
+ * the captured post-dispatch bytes (PRE_W), one report per such region in
+ * region order; *n_reports_out = their count.  outs != NULL: typed
+ * sub-ranges ref=captured-post VA offset, act=live VA (only .act/.nbytes/
+ * .dtype used; ref comes from the capture).  Also re-hashes every restored
+ * region and counts chunks whose hash differs from the captured post
+ * manifest (*unexpected_chunks, may be NULL). */
+kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n, const kc_tolerance* tol,
+                      kc_diff_report* reps, size_t cap_reports, size_t* n_reports_out,
+                      uint64_t* unexpected_chunks);
+/* Restored regions (sorted by base). */
+kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out);
+void kc_release(kc_restored* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KC_H_ */

@@ -1,0 +1,128 @@
+"""O1: independent reader/checker of the kc-snapshot/1 directory -- TEST INFRASTRUCTURE.
+
+Parses the capture directory with Python's json (not the product's C++
+parser), checks every file's length, recomputes every manifest and digest
+with the oracle's own XXH64 (oracle/kc_oracle.c) and checks the sentinel
+(DESIGN.md "Snapshot
+format").  Never imports the product path.
+"""
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import CHUNK, chunk_hashes, n_chunks, region_digest, snapshot_digest
+
+
+@dataclass
+class SnapRegion:
+    base: int
+    size: int
+    kind: str
+    status: str
+    digest: int
+    data_file: str
+    written: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.uint64))
+
+
+@dataclass
+class Snapshot:
+    dir: str
+    dispatch: dict
+    regions: list
+    log: dict
+
+    def region_bytes(self, r: SnapRegion) -> np.ndarray:
+        return np.fromfile(os.path.join(self.dir, r.data_file), dtype=np.uint8)
+
+    def written_bytes(self, r: SnapRegion) -> np.ndarray:
+        p = os.path.join(self.dir, "written", f"region_{r.base:x}.bin")
+        return np.fromfile(p, dtype=np.uint8) if os.path.exists(p) else np.zeros(0, dtype=np.uint8)
+
+    def post_state(self, r: SnapRegion) -> np.ndarray:
+        """Post-dispatch bytes of a region: PRE_W = region file overlaid with written chunks."""
+        b = self.region_bytes(r).copy()
+        if self.dispatch.get("mode") == "pre_w" and r.written.size:
+            w = self.written_bytes(r)
+            off = 0
+            for k in r.written.tolist():
+                lo = k * CHUNK
+                ln = min(CHUNK, r.size - lo)
+                b[lo:lo + ln] = w[off:off + ln]
+                off += ln
+        return b
+
+
+def load(d: str) -> Snapshot:
+    if not os.path.exists(os.path.join(d, "capture_complete")):
+        raise ValueError("no capture_complete sentinel")
+    with open(os.path.join(d, "dispatch.json")) as f:
+        disp = json.load(f)
+    with open(os.path.join(d, "memory_regions.json")) as f:
+        mr = json.load(f)
+    with open(os.path.join(d, "capture_log.json")) as f:
+        log = json.load(f)
+    final = {e["base"]: e["status"] for e in log["regions"]}
+    regs = []
+    for e in mr:
+        r = SnapRegion(int(e["base"], 16), int(e["size"]), e["alloc_kind"], final.get(e["base"], e["status"]),
+                       int(e["digest"], 16), e["data_file"])
+        idx = os.path.join(d, "written", f"region_{e['base']}.idx")
+        if os.path.exists(idx):
+            r.written = np.fromfile(idx, dtype="<u8")
+        regs.append(r)
+    return Snapshot(d, disp, regs, log)
+
+
+def verify(snap: Snapshot) -> dict:
+    """Recompute and check everything the format promises; returns a summary.
+
+    Raises AssertionError on the first violation."""
+    d = snap.dir
+    assert snap.dispatch["format"] == "kc-snapshot/1"
+    assert snap.dispatch["hash"] == {"algo": "xxh64", "seed": 0, "chunk_bytes": CHUNK}
+    bases = [r.base for r in snap.regions]
+    assert bases == sorted(bases), "regions not sorted by base (R25)"
+    for a, b in zip(snap.regions, snap.regions[1:]):
+        assert a.base + a.size <= b.base, "regions overlap"
+    ka = os.path.getsize(os.path.join(d, "kernarg.bin"))
+    assert ka == snap.dispatch["kernarg_size"]
+    cub = os.path.join(d, "kernel.cubin")
+    if snap.dispatch.get("code_object_bytes"):
+        assert os.path.getsize(cub) == snap.dispatch["code_object_bytes"]
+    ok_bases, ok_sizes, ok_digs = [], [], []
+    n_written = 0
+    for r in snap.regions:
+        if r.status != "ok":
+            continue
+        data = snap.region_bytes(r)
+        assert data.size == r.size, f"region {r.base:x}: file has {data.size} bytes, expected {r.size}"
+        h = chunk_hashes(data)
+        man = np.fromfile(os.path.join(d, "memory", f"region_{r.base:x}.xxh64"), dtype="<u8")
+        assert np.array_equal(h, man), f"region {r.base:x}: manifest mismatch"
+        dg = region_digest(h)
+        assert dg == r.digest, f"region {r.base:x}: digest mismatch"
+        post = snap.post_state(r)
+        ph = chunk_hashes(post)
+        pm_path = os.path.join(d, "post", f"region_{r.base:x}.xxh64")
+        if os.path.exists(pm_path):
+            assert np.array_equal(ph, np.fromfile(pm_path, dtype="<u8")), f"region {r.base:x}: post manifest"
+        if snap.dispatch.get("mode") == "pre_w":
+            wexp = sum(min(CHUNK, r.size - k * CHUNK) for k in r.written.tolist())
+            assert snap.written_bytes(r).size == wexp
+            # W = chunks whose pre/post bytes differ (O3)
+            pre = data
+            w_true = [k for k in range(n_chunks(r.size))
+                      if not np.array_equal(pre[k * CHUNK:(k + 1) * CHUNK], post[k * CHUNK:(k + 1) * CHUNK])]
+            assert w_true == sorted(r.written.tolist())
+        n_written += int(r.written.size)
+        ok_bases.append(r.base)
+        ok_sizes.append(r.size)
+        ok_digs.append(dg)
+    S = snapshot_digest(ok_bases, ok_sizes, ok_digs)
+    logged = int(snap.log["snapshot_digest"], 16)
+    assert S == logged, "snapshot digest mismatch"
+    return {"regions": len(snap.regions), "ok": len(ok_bases), "written_chunks": n_written, "snapshot_digest": S}

@@ -1,0 +1,68 @@
+"""Build libkc.so (sm_100a) in-tree with nvcc, plus the fixture cubin.
+
+    python -m paper_2605_03208_b200.build            # build if stale
+    python -m paper_2605_03208_b200.build --force
+
+The library is the product path: hand-written CUDA kernels + the C ABI of
+include/kc.h.  Flags: -gencode arch=compute_100a,code=sm_100a, -O3, -lineinfo,
+NO fast-math, -fmad=false (exact IEEE fp64 in K2; reading R17).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libkc.so")
+FIXTURE_SRC = os.path.join(ROOT, "synth", "kc_fixtures.cu")
+FIXTURE_CUBIN = os.path.join(ROOT, "synth", "kc_fixtures.cubin")
+SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu"]
+HEADERS = ["kc_kernels.cuh", "kc_internal.h", "kc_json.h"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "kc.h"), __file__]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    tmp = LIB + f".tmp{os.getpid()}"
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
+           "-shared", "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES],
+           "-ldl"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd, cwd=CSRC)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def build_fixtures(force: bool = False) -> str:
+    if not force and not _stale(FIXTURE_CUBIN, [FIXTURE_SRC]):
+        return FIXTURE_CUBIN
+    tmp = FIXTURE_CUBIN + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC, "-cubin", *ARCH, "-O3", "-lineinfo", "-o", tmp, FIXTURE_SRC])
+    os.replace(tmp, FIXTURE_CUBIN)
+    return FIXTURE_CUBIN
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    build_lib(force, verbose)
+    build_fixtures(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,142 @@
+// kc_internal.h -- host-side internals of libkc.so (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kc_kernels.cuh"
+
+// Driver-API entry points resolved through cudart (cudaGetDriverEntryPoint),
+// so libkc.so has no link-time dependency on libcuda and loads on hosts
+// without a GPU driver (calls then fail with KC_ERR_CUDA).
+#define KC_DRV_FUNCS(X) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemFree) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
+namespace kc {
+struct Drv {
+#define KC_DRV_DECL(f) decltype(&::f) f = nullptr;
+    KC_DRV_FUNCS(KC_DRV_DECL)
+#undef KC_DRV_DECL
+    bool ok = false;
+};
+const Drv& drv();
+}  // namespace kc
+#define KC_DRV(f) (::kc::drv().f)
+
+struct kc_ctx_dev_buf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+struct kc_ctx {
+    int device = 0;
+    int num_sms = 148;
+    std::string err;
+    bool poisoned = false;
+
+    // A1 tracker (internally synchronized)
+    std::mutex mu;
+    std::map<uint64_t, kc_region> live;
+    uint64_t seq = 0;
+    uint64_t unknown_frees = 0;
+
+    // cached device tables / scratch (stream-ordered; one stream at a time per ctx)
+    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count;
+    std::vector<kc::RegionDev> regs_cached;
+    bool regs_aligned = true;
+
+    // pinned staging ring for D2H/H2D (lazily allocated)
+    uint64_t io_chunk = 64ull << 20;
+    uint32_t depth = 2;
+    std::vector<void*> pinned;
+    std::vector<cudaEvent_t> pin_ev;
+    cudaStream_t copy_stream = nullptr;
+
+    // CUPTI interposition
+    void* cupti_subscriber = nullptr;
+    bool cupti_installed = false;
+
+    // kc_alloc backing
+    int alloc_mode = KC_ALLOC_VMM;
+    size_t granularity = 0;
+    struct VmmAlloc {
+        uint64_t reserved;
+        CUmemGenericAllocationHandle h;
+    };
+    std::map<uint64_t, VmmAlloc> vmm;  // base -> reservation (guarded by mu)
+    uint64_t launches = 0;
+};
+
+struct kc_restored_region {
+    kc_region r;
+    std::string hexbase;
+    bool ok = true;
+    uint64_t n_chunks = 0;
+    std::vector<uint64_t> written;          // chunk indices of W (sorted)
+    std::vector<uint64_t> stash_off;        // per written chunk: offset in the stashes
+    std::vector<uint64_t> post_manifest;    // captured post-dispatch chunk hashes (may be empty)
+};
+
+struct kc_restored {
+    kc_ctx* ctx = nullptr;
+    std::string dir;
+    int mode = KC_MODE_PRE_W;
+    std::string mangled;
+    uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0;
+    std::vector<uint8_t> kernarg;
+    std::vector<kc_restored_region> regions;  // sorted by base
+    // VMM spans
+    struct Span {
+        uint64_t base, size;
+        CUmemGenericAllocationHandle h;
+        bool reserved, mapped, created;
+        bool fallback;                   // restored by replaying cuMemAlloc (driver-pooled VA)
+        std::vector<uint64_t> memalloc;  // cuMemAlloc'd region bases inside this span
+        uint64_t reserve_got;            // diagnostics of a refused reservation
+        int reserve_cr;
+    };
+    std::vector<Span> spans;
+    std::vector<std::pair<uint64_t, uint64_t>> windows;  // reserved VA windows (base, size), ascending
+    // device stashes for W chunks: pre-state (recopy) and reference post bytes (validate)
+    void* stash_pre = nullptr;
+    void* stash_ref = nullptr;
+    uint64_t stash_bytes = 0;
+    CUmodule module = nullptr;
+};
+
+namespace kc {
+
+// error helpers
+kc_status set_err(kc_ctx* ctx, kc_status st, const char* fmt, ...);
+kc_status cuda_err(kc_ctx* ctx, cudaError_t e, const char* what);
+kc_status cu_err(kc_ctx* ctx, CUresult r, const char* what);
+cudaError_t ensure(kc_ctx_dev_buf& b, size_t bytes);
+kc_status ensure_pinned(kc_ctx* ctx);
+bool bind_device(kc_ctx* ctx);
+
+std::string hex_base(uint64_t base);  // lowercase hex, no 0x
+bool region_live(kc_ctx* ctx, uint64_t base, uint64_t size);
+kc_status free_alloc(kc_ctx* ctx, uint64_t dptr, bool track);
+size_t granularity(kc_ctx* ctx);
+
+// snapshot format helpers (kc_snapshot.cu)
+kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std::vector<uint64_t>& out_hashes,
+                            std::vector<uint64_t>* out_digests, uint64_t* out_snapshot, uint64_t* d_hash_out,
+                            cudaStream_t s);
+
+}  // namespace kc
+
+#define KC_CHECK_CUDA(ctx, expr, what)                                  \
+    do {                                                                \
+        cudaError_t _e = (expr);                                        \
+        if (_e != cudaSuccess) return ::kc::cuda_err((ctx), _e, (what)); \
+    } while (0)
+#define KC_CHECK_CU(ctx, expr, what)                                  \
+    do {                                                              \
+        CUresult _r = (expr);                                         \
+        if (_r != CUDA_SUCCESS) return ::kc::cu_err((ctx), _r, (what)); \
+    } while (0)

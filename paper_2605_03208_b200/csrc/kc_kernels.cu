@@ -1,0 +1,856 @@
+// kc_kernels.cu -- the data-parallel hot path of Kerncap's capture-and-validate
+// loop on B200 (sm_100a): K1 chunked XXH64 content hash (TMA bulk ring, 4 lanes
+// per chunk, shuffle merge), region/snapshot digests, K3 written set, K2 fused
+// diff (bitmap, counts, ULP, fp64 abs/rel, allclose, NaN counters).
+//
+// Definitions: SURVEY.md 8(c) O2-O4 and DESIGN.md readings R1-R26, restating
+// PAPER.md:681-691 (chunked snapshot), 1120-1126 (byte-exact compare),
+// 1128-1135 (allclose + explicit NaN reporting).  Compiled WITHOUT fast-math
+// and with -fmad=false; every fp64 op below is an explicit _rn intrinsic.
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <math_constants.h>
+
+#include "kc_kernels.cuh"
+
+namespace kc {
+
+// ========================================================================== //
+// XXH64 primitives (public algorithm; constants SURVEY.md Appendix A)         //
+// ========================================================================== //
+#define P1 0x9E3779B185EBCA87ULL
+#define P2 0xC2B2AE3D27D4EB4FULL
+#define P3 0x165667B19E3779F9ULL
+#define P4 0x85EBCA77C2B2AE63ULL
+#define P5 0x27D4EB2F165667C5ULL
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+// accumulator round: rotl(acc + x*P2, 31) * P1
+__device__ __forceinline__ uint64_t xround(uint64_t acc, uint64_t x) {
+    acc += x * P2;
+    acc = rotl64(acc, 31);
+    return acc * P1;
+}
+
+__device__ __forceinline__ uint64_t xavalanche(uint64_t h) {
+    h ^= h >> 33;
+    h *= P2;
+    h ^= h >> 29;
+    h *= P3;
+    h ^= h >> 32;
+    return h;
+}
+
+// unaligned little-endian loads from global memory (byte-assembled)
+__device__ __forceinline__ uint64_t ldg_u64_bytes(const uint8_t* p) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int i = 7; i >= 0; --i) v = (v << 8) | __ldg(p + i);
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_u32_bytes(const uint8_t* p) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 3; i >= 0; --i) v = (v << 8) | __ldg(p + i);
+    return v;
+}
+
+// Finish XXH64 on a quad: v = this lane's accumulator (lane ql of 4), len the
+// total length, tail = pointer to the bytes after the last full stripe.
+// All 4 lanes must call; every lane returns the same hash.
+template <bool ALIGNED>
+__device__ __forceinline__ uint64_t quad_finish(uint64_t v, int ql, unsigned qmask, uint64_t len, const uint8_t* tail) {
+    uint64_t h;
+    if (len >= 32) {
+        const int rot = ql == 0 ? 1 : (ql == 1 ? 7 : (ql == 2 ? 12 : 18));
+        uint64_t a = rotl64(v, rot);
+        a += __shfl_xor_sync(qmask, a, 1, 4);
+        a += __shfl_xor_sync(qmask, a, 2, 4);
+        const uint64_t m = xround(0, v);
+        const uint64_t m0 = __shfl_sync(qmask, m, 0, 4);
+        const uint64_t m1 = __shfl_sync(qmask, m, 1, 4);
+        const uint64_t m2 = __shfl_sync(qmask, m, 2, 4);
+        const uint64_t m3 = __shfl_sync(qmask, m, 3, 4);
+        h = a;
+        h = (h ^ m0) * P1 + P4;
+        h = (h ^ m1) * P1 + P4;
+        h = (h ^ m2) * P1 + P4;
+        h = (h ^ m3) * P1 + P4;
+    } else {
+        h = P5;  // seed 0
+    }
+    h += len;
+    uint32_t rem = (uint32_t)(len & 31);
+    const uint8_t* p = tail;
+    while (rem >= 8) {
+        const uint64_t x = ALIGNED ? __ldg(reinterpret_cast<const unsigned long long*>(p)) : ldg_u64_bytes(p);
+        h ^= xround(0, x);
+        h = rotl64(h, 27) * P1 + P4;
+        p += 8;
+        rem -= 8;
+    }
+    if (rem >= 4) {
+        const uint32_t x = ALIGNED ? __ldg(reinterpret_cast<const unsigned int*>(p)) : ldg_u32_bytes(p);
+        h ^= (uint64_t)x * P1;
+        h = rotl64(h, 23) * P2 + P3;
+        p += 4;
+        rem -= 4;
+    }
+    while (rem > 0) {
+        h ^= (uint64_t)__ldg(p) * P5;
+        h = rotl64(h, 11) * P1;
+        ++p;
+        --rem;
+    }
+    return xavalanche(h);
+}
+
+__device__ __forceinline__ uint64_t lane_seed(int ql) {
+    // v1 = P1+P2, v2 = P2, v3 = 0, v4 = -P1 (seed 0)
+    return ql == 0 ? (P1 + P2) : (ql == 1 ? P2 : (ql == 2 ? 0ULL : (0ULL - P1)));
+}
+
+// XXH64 of one contiguous global byte range by a quad, direct loads.
+template <bool ALIGNED>
+__device__ uint64_t quad_xxh64_global(const uint8_t* p, uint64_t len, int ql, unsigned qmask) {
+    uint64_t v = lane_seed(ql);
+    const uint64_t nst = len >= 32 ? len / 32 : 0;
+    const uint8_t* q = p + 8 * ql;
+    for (uint64_t t = 0; t < nst; ++t) {
+        const uint64_t x =
+            ALIGNED ? __ldg(reinterpret_cast<const unsigned long long*>(q + 32 * t)) : ldg_u64_bytes(q + 32 * t);
+        v = xround(v, x);
+    }
+    return quad_finish<ALIGNED>(v, ql, qmask, len, p + 32 * nst);
+}
+
+__device__ __forceinline__ int find_region(const RegionDev* __restrict__ r, int n, uint64_t g) {
+    int lo = 0, hi = n;  // first i with chunk_off > g, minus one
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (r[mid].chunk_off <= g) lo = mid + 1; else hi = mid;
+    }
+    return lo - 1;
+}
+
+// ========================================================================== //
+// K1: chunk hash.  One CTA = 64 chunk slots x 4 lanes (one XXH64 accumulator //
+// per lane).  Each slot owns a private 3-stage ring of 1 KiB slices filled by //
+// cp.async.bulk (TMA 1-D bulk copies, mbarrier complete_tx); lane 0 of the    //
+// quad is the producer, all 4 lanes consume with LDS.64.  Slots stream their  //
+// chunk sequence continuously, so the next chunk's first slices are in       //
+// flight while the current chunk finishes.  Chunk g -> slot (g / grid) % 64   //
+// of CTA g % grid: every CTA gets the same share (interleaved).              //
+// ========================================================================== //
+constexpr int HK_THREADS = 256;
+constexpr int HK_SLOTS = HK_THREADS / 4;
+constexpr int HK_STAGES = 3;
+constexpr int HK_SLICE = 1024;
+constexpr int HK_PITCH = HK_SLICE + 32;  // quads of a warp land on distinct bank groups
+constexpr size_t HK_SMEM = (size_t)HK_SLOTS * HK_STAGES * HK_PITCH + (size_t)HK_SLOTS * HK_STAGES * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+struct ChunkRef {
+    const uint8_t* src;
+    uint32_t len;
+};
+
+__device__ __forceinline__ ChunkRef chunk_ref(const RegionDev* __restrict__ regs, int nreg, uint64_t g) {
+    const int r = find_region(regs, nreg, g);
+    const uint64_t off = (g - regs[r].chunk_off) * kChunk;
+    const uint64_t rem = regs[r].size - off;
+    return {reinterpret_cast<const uint8_t*>(regs[r].base + off), rem < kChunk ? (uint32_t)rem : (uint32_t)kChunk};
+}
+
+__global__ void __launch_bounds__(HK_THREADS, 1)
+    k1_hash_tma(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int slot = threadIdx.x >> 2;
+    const int ql = threadIdx.x & 3;
+    const unsigned qmask = 0xFu << (threadIdx.x & 28);
+    uint8_t* ring = smem + (size_t)slot * HK_STAGES * HK_PITCH;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)HK_SLOTS * HK_STAGES * HK_PITCH) + slot * HK_STAGES;
+
+    if (ql == 0) {
+#pragma unroll
+        for (int s = 0; s < HK_STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+
+    const uint64_t Q = (uint64_t)HK_SLOTS * gridDim.x;
+    const uint64_t g0 = (uint64_t)slot * gridDim.x + blockIdx.x;
+
+    // ---- producer cursor (used by ql == 0 only) ----
+    uint64_t pg = g0;              // chunk being fetched
+    const uint8_t* psrc = nullptr; // its first byte
+    uint32_t pbytes = 0, poff = 0; // stripe bytes to stage, bytes already issued
+    bool phave = false;
+    uint32_t fetched = 0;
+    auto issue_next = [&]() {
+        while (pg < C) {
+            if (!phave) {
+                const ChunkRef cr = chunk_ref(regs, nreg, pg);
+                psrc = cr.src;
+                pbytes = cr.len >= 32 ? (cr.len & ~31u) : 0u;
+                poff = 0;
+                phave = true;
+            }
+            if (poff < pbytes) {
+                const uint32_t b = min((uint32_t)HK_SLICE, pbytes - poff);
+                const int st = fetched % HK_STAGES;
+                mbar_arrive_expect_tx(&bars[st], b);
+                bulk_g2s(ring + st * HK_PITCH, psrc + poff, b, &bars[st], policy);
+                poff += b;
+                ++fetched;
+                if (poff == pbytes) { pg += Q; phave = false; }
+                return;
+            }
+            pg += Q;
+            phave = false;
+        }
+    };
+    if (ql == 0) {
+        for (int s = 0; s < HK_STAGES; ++s) issue_next();
+    }
+
+    uint32_t consumed = 0;
+    for (uint64_t g = g0; g < C; g += Q) {
+        const ChunkRef cr = chunk_ref(regs, nreg, g);
+        const uint32_t nst = cr.len >= 32 ? cr.len / 32 : 0;
+        uint64_t v = lane_seed(ql);
+        uint32_t remaining = nst * 32;
+        while (remaining > 0) {
+            const int st = consumed % HK_STAGES;
+            mbar_wait(&bars[st], (consumed / HK_STAGES) & 1);
+            const uint64_t* p = reinterpret_cast<const uint64_t*>(ring + st * HK_PITCH) + ql;
+            if (remaining >= (uint32_t)HK_SLICE) {
+#pragma unroll
+                for (int t = 0; t < HK_SLICE / 32; ++t) v = xround(v, p[4 * t]);
+                remaining -= HK_SLICE;
+            } else {
+                const uint32_t n = remaining / 32;
+                for (uint32_t t = 0; t < n; ++t) v = xround(v, p[4 * t]);
+                remaining = 0;
+            }
+            ++consumed;
+            __syncwarp(qmask);  // all 4 lanes are done with this stage
+            if (ql == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_next();
+            }
+        }
+        const uint64_t h = quad_finish<true>(v, ql, qmask, cr.len, cr.src + (size_t)nst * 32);
+        if (ql == 0) out[g] = h;
+    }
+}
+
+// Unaligned regions (base % 16 != 0): quad per chunk, byte-assembled loads.
+__global__ void __launch_bounds__(256)
+    k1_hash_generic(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out) {
+    const int ql = threadIdx.x & 3;
+    const unsigned qmask = 0xFu << (threadIdx.x & 28);
+    const uint64_t nq = (uint64_t)gridDim.x * (blockDim.x / 4);
+    for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x / 4) + (threadIdx.x >> 2); g < C; g += nq) {
+        const ChunkRef cr = chunk_ref(regs, nreg, g);
+        const uint64_t h = quad_xxh64_global<false>(cr.src, cr.len, ql, qmask);
+        if (ql == 0) out[g] = h;
+    }
+}
+
+// Region digests (quad per region) + the (base,size,digest) LE triples.
+__global__ void k1_region_digest(const RegionDev* __restrict__ regs, int nreg, const uint64_t* __restrict__ h,
+                                 uint64_t* __restrict__ dig, uint8_t* __restrict__ scratch) {
+    const int ql = threadIdx.x & 3;
+    const unsigned qmask = 0xFu << (threadIdx.x & 28);
+    const int nq = gridDim.x * (blockDim.x / 4);
+    for (int r = blockIdx.x * (blockDim.x / 4) + (threadIdx.x >> 2); r < nreg; r += nq) {
+        const uint64_t nck = (regs[r].size + kChunk - 1) / kChunk;
+        const uint64_t d =
+            quad_xxh64_global<true>(reinterpret_cast<const uint8_t*>(h + regs[r].chunk_off), 8 * nck, ql, qmask);
+        if (ql == 0) {
+            if (dig) dig[r] = d;
+            if (scratch) {
+                uint64_t* t = reinterpret_cast<uint64_t*>(scratch + 24 * (size_t)r);
+                t[0] = regs[r].base;
+                t[1] = regs[r].size;
+                t[2] = d;
+            }
+        }
+    }
+}
+
+__global__ void k1_snapshot_digest(const uint8_t* __restrict__ scratch, int nreg, uint64_t* __restrict__ out) {
+    const int ql = threadIdx.x & 3;
+    const uint64_t s = quad_xxh64_global<true>(scratch, 24 * (uint64_t)nreg, ql, 0xFu);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// ========================================================================== //
+// K3: written set W[k] = (pre[k] != post[k]); warp per 64 chunks (ballots).  //
+// ========================================================================== //
+__global__ void k3_written(const uint64_t* __restrict__ pre, const uint64_t* __restrict__ post, uint64_t C,
+                           uint64_t* __restrict__ bitmap, unsigned long long* __restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwords = (C + 63) / 64;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    unsigned long long local = 0;
+    for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < nwords; w += nwarps) {
+        const uint64_t k0 = 64 * w + lane, k1 = k0 + 32;
+        const bool b0 = k0 < C && __ldg(pre + k0) != __ldg(post + k0);
+        const bool b1 = k1 < C && __ldg(pre + k1) != __ldg(post + k1);
+        const uint32_t lo = __ballot_sync(0xFFFFFFFFu, b0);
+        const uint32_t hi = __ballot_sync(0xFFFFFFFFu, b1);
+        if (lane == 0) {
+            bitmap[w] = (uint64_t)lo | ((uint64_t)hi << 32);
+            local += __popc(lo) + __popc(hi);
+        }
+    }
+    if (lane == 0 && local) atomicAdd(count, local);
+}
+
+// ========================================================================== //
+// K2: fused diff.  Work = 16 KiB units of every segment, distributed to warps //
+// in contiguous blocks.  Each lane streams 32-byte vectors of ref and act     //
+// with 256-bit non-allocating loads (4 vectors of each in flight); equal      //
+// vectors with no Inf/NaN exponent take the fast path.  Per-warp accumulators //
+// flush with one atomic per nonzero field when the segment changes.          //
+// ========================================================================== //
+struct Acc {
+    unsigned long long dbytes, delems, nan_r, nan_a, nan_pos, rel_undef, fail, max_ulp;
+    double max_abs, max_rel;
+    uint32_t any;  // this lane saw a differing byte in the current unit
+};
+
+__device__ __forceinline__ void acc_zero(Acc& a) {
+    a.dbytes = a.delems = a.nan_r = a.nan_a = a.nan_pos = a.rel_undef = a.fail = a.max_ulp = 0;
+    a.max_abs = 0.0;
+    a.max_rel = 0.0;
+    a.any = 0;
+}
+
+// number of nonzero bytes of x
+__device__ __forceinline__ uint32_t nz_bytes(uint32_t x) {
+    return __popc((((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u);
+}
+
+template <int DT> struct DT_;
+template <> struct DT_<KC_DT_F16> { static constexpr int S = 2; static constexpr bool F = true; };
+template <> struct DT_<KC_DT_BF16> { static constexpr int S = 2; static constexpr bool F = true; };
+template <> struct DT_<KC_DT_F32> { static constexpr int S = 4; static constexpr bool F = true; };
+template <> struct DT_<KC_DT_F64> { static constexpr int S = 8; static constexpr bool F = true; };
+template <> struct DT_<KC_DT_BYTES> { static constexpr int S = 1; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_U8> { static constexpr int S = 1; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_I8> { static constexpr int S = 1; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_U16> { static constexpr int S = 2; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_I16> { static constexpr int S = 2; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_U32> { static constexpr int S = 4; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_I32> { static constexpr int S = 4; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_U64> { static constexpr int S = 8; static constexpr bool F = false; };
+template <> struct DT_<KC_DT_I64> { static constexpr int S = 8; static constexpr bool F = false; };
+
+template <int DT>
+__device__ __forceinline__ bool is_signed_dt() {
+    return DT == KC_DT_I8 || DT == KC_DT_I16 || DT == KC_DT_I32 || DT == KC_DT_I64;
+}
+
+// "exponent all ones" (Inf or NaN) anywhere in a 32-bit word of this dtype
+template <int DT>
+__device__ __forceinline__ uint32_t special_word(uint32_t w) {
+    if (DT == KC_DT_F16) return ((w & 0x7C007C00u) + 0x04000400u) & 0x80008000u;
+    if (DT == KC_DT_BF16) return ((w & 0x7F807F80u) + 0x00800080u) & 0x80008000u;
+    if (DT == KC_DT_F32) return ((w & 0x7F800000u) + 0x00800000u) & 0x80000000u;
+    if (DT == KC_DT_F64) return ((w & 0x7FF00000u) + 0x00100000u) & 0x80000000u;  // applied to hi words only
+    return 0;
+}
+
+template <int DT>
+__device__ __forceinline__ bool isnan_bits(uint64_t b) {
+    if (DT == KC_DT_F16) return (b & 0x7FFFu) > 0x7C00u;
+    if (DT == KC_DT_BF16) return (b & 0x7FFFu) > 0x7F80u;
+    if (DT == KC_DT_F32) return (b & 0x7FFFFFFFu) > 0x7F800000u;
+    return (b & 0x7FFFFFFFFFFFFFFFULL) > 0x7FF0000000000000ULL;
+}
+
+// exact conversion to fp64 (no FTZ: compiled without fast-math)
+template <int DT>
+__device__ __forceinline__ double to_f64(uint64_t b) {
+    if (DT == KC_DT_F16) return (double)__half2float(__ushort_as_half((unsigned short)b));
+    if (DT == KC_DT_BF16) return (double)__uint_as_float((uint32_t)b << 16);
+    if (DT == KC_DT_F32) return (double)__uint_as_float((uint32_t)b);
+    return __longlong_as_double((long long)b);
+}
+
+// One element (float dtypes): r, a raw bits.
+template <int DT>
+__device__ __forceinline__ void elem_float(uint64_t r, uint64_t a, Acc& acc, double atol, double rtol, int equal_nan) {
+    constexpr int S = DT_<DT>::S;
+    const bool nr = isnan_bits<DT>(r), na = isnan_bits<DT>(a);
+    const bool differ = r != a;
+    acc.delems += differ;
+    acc.nan_r += nr;
+    acc.nan_a += na;
+    acc.nan_pos += (nr != na);
+    if (nr || na) {
+        acc.fail += !(equal_nan && nr && na);
+        return;
+    }
+    if (!differ) return;
+    // ordered-integer ULP distance
+    const uint64_t sign = 1ULL << (8 * S - 1);
+    const long long oa = (a & sign) ? -(long long)(a & ~sign) : (long long)a;
+    const long long orr = (r & sign) ? -(long long)(r & ~sign) : (long long)r;
+    const unsigned long long ulp =
+        oa >= orr ? (unsigned long long)oa - (unsigned long long)orr : (unsigned long long)orr - (unsigned long long)oa;
+    if (ulp > acc.max_ulp) acc.max_ulp = ulp;
+    const double av = to_f64<DT>(a), rv = to_f64<DT>(r);
+    const double d = fabs(__dsub_rn(av, rv));
+    if (d > acc.max_abs) acc.max_abs = d;
+    const double ar = fabs(rv);
+    const double tol = __dadd_rn(atol, __dmul_rn(rtol, ar));
+    const bool rfin = ar != CUDART_INF;
+    const bool close = ((d <= tol) && rfin) || (av == rv);
+    acc.fail += !close;
+    if (d != 0.0) {
+        if (rv == 0.0) {
+            acc.rel_undef += 1;
+        } else {
+            const double rel = rfin ? __ddiv_rn(d, ar) : CUDART_INF;
+            if (rel > acc.max_rel) acc.max_rel = rel;
+        }
+    }
+}
+
+template <int DT>
+__device__ __forceinline__ void elem_int(uint64_t r, uint64_t a, Acc& acc) {
+    constexpr int S = DT_<DT>::S;
+    if (r == a) return;
+    acc.delems += 1;
+    unsigned long long d;
+    if (is_signed_dt<DT>()) {
+        const int sh = 64 - 8 * S;
+        const long long va = (long long)(a << sh) >> sh, vr = (long long)(r << sh) >> sh;
+        d = va >= vr ? (unsigned long long)va - (unsigned long long)vr : (unsigned long long)vr - (unsigned long long)va;
+    } else {
+        d = a >= r ? a - r : r - a;
+    }
+    if (d > acc.max_ulp) acc.max_ulp = d;
+}
+
+// select word i (0..7) of an 8-word register vector without local memory
+__device__ __forceinline__ uint32_t sel8(const uint32_t (&w)[8], int i) {
+    const uint32_t a = (i & 1) ? w[1] : w[0], b = (i & 1) ? w[3] : w[2];
+    const uint32_t c = (i & 1) ? w[5] : w[4], d = (i & 1) ? w[7] : w[6];
+    const uint32_t e = (i & 2) ? b : a, f = (i & 2) ? d : c;
+    return (i & 4) ? f : e;
+}
+
+// Fast check of one 32-byte vector pair: counts differing bytes, and returns
+// the mask of elements that need the per-element path (differing bits, or an
+// Inf/NaN exponent on either side for float types).  BYTES is finished here.
+template <int DT>
+__device__ __forceinline__ uint32_t vec_scan(const uint32_t (&r)[8], const uint32_t (&a)[8], Acc& acc) {
+    constexpr int S = DT_<DT>::S;
+    constexpr bool F = DT_<DT>::F;
+    uint32_t x[8];
+    uint32_t anyx = 0, spec = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        x[i] = r[i] ^ a[i];
+        anyx |= x[i];
+    }
+    if (F) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (S != 8 || (i & 1)) spec |= special_word<DT>(r[i]) | special_word<DT>(a[i]);
+    }
+    if ((anyx | spec) == 0) return 0;  // fast path: equal, no Inf/NaN
+    if (anyx) {
+        acc.any = 1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc.dbytes += nz_bytes(x[i]);
+    }
+    if (DT == KC_DT_BYTES) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m = __vmaxu4(m, __vabsdiffu4(r[i], a[i]));
+        m = max(max(m & 0xFF, (m >> 8) & 0xFF), max((m >> 16) & 0xFF, m >> 24));
+        if (m > acc.max_ulp) acc.max_ulp = m;
+        return 0;
+    }
+    uint32_t mask = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (S == 8) {
+            if (i & 1) {
+                const uint32_t sp = F ? (special_word<DT>(r[i]) | special_word<DT>(a[i])) : 0u;
+                mask |= (uint32_t)(((x[i - 1] | x[i]) | sp) != 0) << (i >> 1);
+            }
+        } else if (S == 4) {
+            const uint32_t sp = F ? (special_word<DT>(r[i]) | special_word<DT>(a[i])) : 0u;
+            mask |= (uint32_t)((x[i] | sp) != 0) << i;
+        } else if (S == 2) {
+            uint32_t m = (((x[i] & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x[i]) & 0x80008000u;
+            if (F) m |= special_word<DT>(r[i]) | special_word<DT>(a[i]);
+            mask |= (((m >> 15) & 1u) | ((m >> 30) & 2u)) << (2 * i);
+        } else {
+            const uint32_t m = (((x[i] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x[i]) & 0x80808080u;
+            mask |= (((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u)) << (4 * i);
+        }
+    }
+    return mask;
+}
+
+// Per-element path for the elements in mask (one code copy: element bits are
+// picked out of the register vector with selects).
+template <int DT>
+__device__ __forceinline__ void vec_slow(const uint32_t (&r)[8], const uint32_t (&a)[8], uint32_t mask, Acc& acc,
+                                         double atol, double rtol, int equal_nan) {
+    constexpr int S = DT_<DT>::S;
+    while (mask) {
+        const int e = __ffs(mask) - 1;
+        mask &= mask - 1;
+        uint64_t rb, ab;
+        if (S == 8) {
+            rb = (uint64_t)sel8(r, 2 * e) | ((uint64_t)sel8(r, 2 * e + 1) << 32);
+            ab = (uint64_t)sel8(a, 2 * e) | ((uint64_t)sel8(a, 2 * e + 1) << 32);
+        } else if (S == 4) {
+            rb = sel8(r, e);
+            ab = sel8(a, e);
+        } else if (S == 2) {
+            rb = (sel8(r, e >> 1) >> (16 * (e & 1))) & 0xFFFFu;
+            ab = (sel8(a, e >> 1) >> (16 * (e & 1))) & 0xFFFFu;
+        } else {
+            rb = (sel8(r, e >> 2) >> (8 * (e & 3))) & 0xFFu;
+            ab = (sel8(a, e >> 2) >> (8 * (e & 3))) & 0xFFu;
+        }
+        if (DT_<DT>::F) elem_float<DT>(rb, ab, acc, atol, rtol, equal_nan); else elem_int<DT>(rb, ab, acc);
+    }
+}
+
+// scalar path: one element at byte offset o (element-size aligned within the buffer)
+template <int DT>
+__device__ __forceinline__ void elem_scalar(const uint8_t* R, const uint8_t* A, Acc& acc, double atol, double rtol,
+                                            int equal_nan) {
+    constexpr int S = DT_<DT>::S;
+    uint64_t rb = 0, ab = 0;
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+        rb = (rb << 8) | __ldg(R + i);
+        ab = (ab << 8) | __ldg(A + i);
+    }
+    if (rb != ab) {
+        acc.any = 1;
+        uint64_t x = rb ^ ab;
+#pragma unroll
+        for (int i = 0; i < S; ++i) acc.dbytes += ((x >> (8 * i)) & 0xFF) != 0;
+    }
+    if (DT == KC_DT_BYTES) {
+        const unsigned long long d = rb > ab ? rb - ab : ab - rb;
+        if (d > acc.max_ulp) acc.max_ulp = d;
+        return;
+    }
+    if (DT_<DT>::F) elem_float<DT>(rb, ab, acc, atol, rtol, equal_nan); else elem_int<DT>(rb, ab, acc);
+}
+
+__device__ __forceinline__ void ld256(const void* p, uint32_t* w) {
+    unsigned long long a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p));
+    w[0] = (uint32_t)a; w[1] = (uint32_t)(a >> 32);
+    w[2] = (uint32_t)b; w[3] = (uint32_t)(b >> 32);
+    w[4] = (uint32_t)c; w[5] = (uint32_t)(c >> 32);
+    w[6] = (uint32_t)d; w[7] = (uint32_t)(d >> 32);
+}
+
+// one unit [off, off+len) of a segment, whole warp: 2 vectors of each stream
+// in flight per lane; the per-element path runs once per vector that needs it.
+template <int DT>
+__device__ void diff_unit(const uint8_t* R, const uint8_t* A, uint32_t len, bool vec_ok, Acc& acc, double atol,
+                          double rtol, int equal_nan, int lane) {
+    constexpr int S = DT_<DT>::S;
+    uint32_t done = 0;
+    if (vec_ok) {
+        const uint32_t nvec = len / 32;
+        uint32_t v = lane;
+        for (; v + 32 < nvec; v += 64) {
+            uint32_t r0[8], a0[8], r1[8], a1[8];
+            ld256(R + 32 * (size_t)v, r0);
+            ld256(A + 32 * (size_t)v, a0);
+            ld256(R + 32 * (size_t)(v + 32), r1);
+            ld256(A + 32 * (size_t)(v + 32), a1);
+            const uint32_t m0 = vec_scan<DT>(r0, a0, acc);
+            const uint32_t m1 = vec_scan<DT>(r1, a1, acc);
+            if (m0 | m1) {
+#pragma unroll 1
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t m = u ? m1 : m0;
+                    if (!m) continue;
+                    uint32_t rr[8], aa[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        rr[i] = u ? r1[i] : r0[i];
+                        aa[i] = u ? a1[i] : a0[i];
+                    }
+                    vec_slow<DT>(rr, aa, m, acc, atol, rtol, equal_nan);
+                }
+            }
+        }
+        if (v < nvec) {
+            uint32_t r0[8], a0[8];
+            ld256(R + 32 * (size_t)v, r0);
+            ld256(A + 32 * (size_t)v, a0);
+            const uint32_t m0 = vec_scan<DT>(r0, a0, acc);
+            if (m0) vec_slow<DT>(r0, a0, m0, acc, atol, rtol, equal_nan);
+        }
+        done = nvec * 32;
+    }
+    for (uint32_t o = done + lane * S; o < len; o += 32 * S) elem_scalar<DT>(R + o, A + o, acc, atol, rtol, equal_nan);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_maxu(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+__device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
+    const unsigned long long nonzero =
+        acc.dbytes | acc.delems | acc.nan_r | acc.nan_a | acc.nan_pos | acc.rel_undef | acc.fail | acc.max_ulp |
+        (unsigned long long)__double_as_longlong(acc.max_abs) | (unsigned long long)__double_as_longlong(acc.max_rel);
+    if (__ballot_sync(0xFFFFFFFFu, nonzero != 0) != 0) {
+        const unsigned long long s0 = warp_sum(acc.dbytes), s1 = warp_sum(acc.delems), s2 = warp_sum(acc.nan_r),
+                                 s3 = warp_sum(acc.nan_a), s4 = warp_sum(acc.nan_pos), s5 = warp_sum(acc.rel_undef),
+                                 s6 = warp_sum(acc.fail);
+        const unsigned long long m0 = warp_maxu(acc.max_ulp),
+                                 m1 = warp_maxu((unsigned long long)__double_as_longlong(acc.max_abs)),
+                                 m2 = warp_maxu((unsigned long long)__double_as_longlong(acc.max_rel));
+        if (lane == 0) {
+            if (s0) atomicAdd((unsigned long long*)&rep->differing_bytes, s0);
+            if (s1) atomicAdd((unsigned long long*)&rep->differing_elems, s1);
+            if (s2) atomicAdd((unsigned long long*)&rep->nan_ref, s2);
+            if (s3) atomicAdd((unsigned long long*)&rep->nan_act, s3);
+            if (s4) atomicAdd((unsigned long long*)&rep->nan_pos_mismatch, s4);
+            if (s5) atomicAdd((unsigned long long*)&rep->rel_undefined, s5);
+            if (s6) atomicAdd((unsigned long long*)&rep->allclose_fail, s6);
+            if (m0) atomicMax((unsigned long long*)&rep->max_ulp, m0);
+            // non-negative doubles order like their bit patterns (+0.0 < ... < +inf)
+            if (m1) atomicMax((unsigned long long*)&rep->max_abs, m1);
+            if (m2) atomicMax((unsigned long long*)&rep->max_rel, m2);
+        }
+    }
+    const uint32_t any = acc.any;
+    acc_zero(acc);
+    acc.any = any;
+}
+
+constexpr int DK_THREADS = 512;
+
+// One launch per dtype group: segments [seg0, seg0+nseg) own the global units
+// [unit0, unit0+U).
+template <int DT>
+__global__ void __launch_bounds__(DK_THREADS, 2)
+    k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
+            kc_diff_report* __restrict__ reps, unsigned long long* __restrict__ bitmaps, double atol, double rtol,
+            int equal_nan) {
+    const int lane = threadIdx.x & 31;
+    segs += seg0;
+    const uint64_t W = (uint64_t)gridDim.x * (DK_THREADS / 32);
+    const uint64_t w = (uint64_t)blockIdx.x * (DK_THREADS / 32) + (threadIdx.x >> 5);
+    // contiguous block of units for this warp
+    const uint64_t u0 = unit0 + (U * w) / W, u1 = unit0 + (U * (w + 1)) / W;
+    if (u0 >= u1) return;
+    int s = 0;
+    {
+        int lo = 0, hi = nseg;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (segs[mid].unit_off <= u0) lo = mid + 1; else hi = mid;
+        }
+        s = lo - 1;
+    }
+    Acc acc;
+    acc_zero(acc);
+    for (uint64_t u = u0; u < u1; ++u) {
+        while (s + 1 < nseg && segs[s + 1].unit_off <= u) {
+            acc_flush(acc, reps + segs[s].report, lane);
+            ++s;
+        }
+        const SegDev sg = segs[s];
+        const uint64_t off = (u - sg.unit_off) * (uint64_t)kDiffUnit;
+        const uint32_t len = (uint32_t)min((uint64_t)kDiffUnit, sg.nbytes - off);
+        const uint8_t* R = reinterpret_cast<const uint8_t*>(sg.ref) + off;
+        const uint8_t* A = reinterpret_cast<const uint8_t*>(sg.act) + off;
+        const bool vec_ok = ((sg.ref | sg.act) & 31) == 0;
+        acc.any = 0;
+        diff_unit<DT>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane);
+        if (__any_sync(0xFFFFFFFFu, acc.any) && lane == 0 && bitmaps) {
+            const uint64_t k = sg.bitmap_chunk0 + off / kChunk;
+            atomicOr(bitmaps + sg.bitmap_word0 + k / 64, 1ULL << (k % 64));
+        }
+    }
+    acc_flush(acc, reps + segs[s].report, lane);
+}
+
+// per report: nbytes / n_elems / n_chunks / percent / pass
+__global__ void k2_finalize(const ReportMeta* __restrict__ meta, int nrep, kc_diff_report* __restrict__ reps) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nrep) return;
+    kc_diff_report& r = reps[j];
+    const int dt = meta[j].dtype;
+    const int es = (dt == KC_DT_BYTES || dt == KC_DT_U8 || dt == KC_DT_I8) ? 1
+                   : (dt == KC_DT_U16 || dt == KC_DT_I16 || dt == KC_DT_F16 || dt == KC_DT_BF16) ? 2
+                   : (dt == KC_DT_U32 || dt == KC_DT_I32 || dt == KC_DT_F32) ? 4 : 8;
+    const uint64_t n = meta[j].nbytes;
+    r.nbytes = n;
+    r.n_elems = n / es;
+    r.n_chunks = (n + kChunk - 1) / kChunk;
+    r.percent_bytes = n ? __ddiv_rn(__dmul_rn(100.0, (double)r.differing_bytes), (double)n) : 0.0;
+    if (dt == KC_DT_BYTES) {
+        r.differing_elems = r.differing_bytes;
+        r.pass = r.differing_bytes == 0;
+    } else if (dt == KC_DT_F16 || dt == KC_DT_BF16 || dt == KC_DT_F32 || dt == KC_DT_F64) {
+        r.pass = r.allclose_fail == 0;
+    } else {
+        r.pass = r.differing_elems == 0;
+    }
+}
+
+// ========================================================================== //
+// K4: gather/scatter of many small ranges (pack small regions for one DMA).  //
+// ========================================================================== //
+__global__ void k4_gather(const uint64_t* __restrict__ src, const uint64_t* __restrict__ dst,
+                          const uint64_t* __restrict__ len, int n) {
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint8_t* s = reinterpret_cast<const uint8_t*>(src[i]);
+        uint8_t* d = reinterpret_cast<uint8_t*>(dst[i]);
+        const uint64_t L = len[i];
+        if (((src[i] | dst[i]) & 15) == 0) {
+            const uint64_t nv = L / 16;
+            for (uint64_t k = threadIdx.x; k < nv; k += blockDim.x)
+                reinterpret_cast<uint4*>(d)[k] = __ldg(reinterpret_cast<const uint4*>(s) + k);
+            for (uint64_t k = nv * 16 + threadIdx.x; k < L; k += blockDim.x) d[k] = s[k];
+        } else {
+            for (uint64_t k = threadIdx.x; k < L; k += blockDim.x) d[k] = s[k];
+        }
+    }
+}
+
+// ========================================================================== //
+// launchers                                                                  //
+// ========================================================================== //
+cudaError_t kernels_init() {
+    return cudaFuncSetAttribute(k1_hash_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HK_SMEM);
+}
+
+cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool aligned, uint64_t* d_out, int num_sms,
+                        cudaStream_t s) {
+    if (C == 0) return cudaSuccess;
+    if (aligned) {
+        // one CTA per SM (64 chunk slots each); fewer CTAs when there are few chunks
+        uint64_t grid = (C + HK_SLOTS - 1) / HK_SLOTS;
+        if (grid > (uint64_t)num_sms) grid = num_sms;
+        k1_hash_tma<<<(unsigned)grid, HK_THREADS, HK_SMEM, s>>>(d_regs, nreg, C, d_out);
+    } else {
+        uint64_t grid = (C + 63) / 64;
+        if (grid > (uint64_t)num_sms * 8) grid = num_sms * 8;
+        k1_hash_generic<<<(unsigned)grid, 256, 0, s>>>(d_regs, nreg, C, d_out);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_digests(const RegionDev* d_regs, int nreg, const uint64_t* d_h, uint64_t* d_dig, uint8_t* d_scratch,
+                           uint64_t* d_snap, cudaStream_t s) {
+    if (nreg == 0) return cudaSuccess;
+    const int grid = (nreg + 63) / 64;
+    k1_region_digest<<<grid, 256, 0, s>>>(d_regs, nreg, d_h, d_dig, d_snap ? d_scratch : nullptr);
+    if (d_snap) k1_snapshot_digest<<<1, 4, 0, s>>>(d_scratch, nreg, d_snap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64_t C, uint64_t* d_bitmap,
+                           uint64_t* d_count, int num_sms, cudaStream_t s) {
+    if (C == 0) return cudaSuccess;
+    const uint64_t nwords = (C + 63) / 64;
+    uint64_t grid = (nwords + 7) / 8;
+    if (grid > (uint64_t)num_sms * 4) grid = num_sms * 4;
+    k3_written<<<(unsigned)grid, 256, 0, s>>>(d_pre, d_post, C, d_bitmap, (unsigned long long*)d_count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_diff(const SegDev* d_segs, const DiffGroup* groups, int ngroups, const ReportMeta* d_meta,
+                        int nrep, kc_diff_report* d_reps, uint64_t* d_bitmaps, double atol, double rtol,
+                        int equal_nan, int num_sms, cudaStream_t s) {
+    for (int g = 0; g < ngroups; ++g) {
+        const DiffGroup& G = groups[g];
+        if (G.n_units == 0 || G.n_segs == 0) continue;
+        uint64_t grid = (G.n_units + (DK_THREADS / 32) - 1) / (DK_THREADS / 32);
+        if (grid > (uint64_t)num_sms * 2) grid = num_sms * 2;
+        unsigned long long* bm = (unsigned long long*)d_bitmaps;
+        switch (G.dtype) {
+#define KC_CASE(D)                                                                                             \
+    case D:                                                                                                    \
+        k2_diff<D><<<(unsigned)grid, DK_THREADS, 0, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units, d_reps, \
+                                                         bm, atol, rtol, equal_nan);                           \
+        break;
+            KC_CASE(KC_DT_BYTES) KC_CASE(KC_DT_U8) KC_CASE(KC_DT_I8) KC_CASE(KC_DT_U16) KC_CASE(KC_DT_I16)
+            KC_CASE(KC_DT_U32) KC_CASE(KC_DT_I32) KC_CASE(KC_DT_U64) KC_CASE(KC_DT_I64) KC_CASE(KC_DT_F16)
+            KC_CASE(KC_DT_BF16) KC_CASE(KC_DT_F32) KC_CASE(KC_DT_F64)
+#undef KC_CASE
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    if (nrep > 0) k2_finalize<<<(nrep + 127) / 128, 128, 0, s>>>(d_meta, nrep, d_reps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d_len, int n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k4_gather<<<min(n, 148 * 8), 256, 0, s>>>(d_src, d_dst, d_len, n);
+    return cudaGetLastError();
+}
+
+}  // namespace kc

@@ -1,0 +1,62 @@
+// kc_kernels.cuh -- device-side types shared by kc_kernels.cu and kc_runtime.cu
+// (product path only; the oracle in oracle/ shares nothing with this file).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/kc.h"
+
+namespace kc {
+
+constexpr uint64_t kChunk = KC_CHUNK_BYTES;  // 65,536 B hash/diff granule (reading R1)
+
+// Device region table: regions in global-chunk order with the
+// prefix-summed first chunk index of each region.
+struct RegionDev {
+    uint64_t base;
+    uint64_t size;
+    uint64_t chunk_off;
+};
+
+// One K2 segment, pre-split into 16 KiB work units (unit_off = prefix sum).
+struct SegDev {
+    uint64_t ref, act, nbytes;
+    uint64_t bitmap_word0;   // first bitmap word of this segment's report
+    uint64_t bitmap_chunk0;  // chunk index of byte 0 inside that report
+    uint64_t unit_off;       // first global unit index
+    int32_t dtype;
+    int32_t report;
+};
+
+struct ReportMeta {
+    uint64_t nbytes;
+    int32_t dtype;
+    int32_t _pad;
+};
+
+constexpr uint32_t kDiffUnit = 16384;  // K2 work unit (bytes)
+
+// K2 launch group: one dtype, a contiguous run of segments and their units.
+struct DiffGroup {
+    int32_t dtype;
+    int32_t seg0, n_segs;
+    uint64_t unit0, n_units;
+};
+
+// ---- launchers (kc_kernels.cu) ------------------------------------------
+cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t n_chunks, bool aligned, uint64_t* d_out,
+                        int num_sms, cudaStream_t s);
+cudaError_t launch_digests(const RegionDev* d_regs, int nreg, const uint64_t* d_chunk_hash, uint64_t* d_region_digest,
+                           uint8_t* d_scratch /* 24*nreg */, uint64_t* d_snapshot_digest, cudaStream_t s);
+cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64_t n_chunks, uint64_t* d_bitmap,
+                           uint64_t* d_count, int num_sms, cudaStream_t s);
+cudaError_t launch_diff(const SegDev* d_segs, const DiffGroup* groups, int ngroups, const ReportMeta* d_meta,
+                        int nrep, kc_diff_report* d_reps, uint64_t* d_bitmaps, double atol, double rtol,
+                        int equal_nan, int num_sms, cudaStream_t s);
+cudaError_t launch_gather(const uint64_t* d_src_ptrs, const uint64_t* d_dst_ptrs, const uint64_t* d_lens, int n,
+                          cudaStream_t s);
+
+// kernel attribute setup (dynamic smem opt-in); call once per device
+cudaError_t kernels_init();
+
+}  // namespace kc

@@ -1,0 +1,719 @@
+// kc_runtime.cu -- libkc.so core: context lifetime, errors, the A1 allocation
+// tracker (explicit feed, cuMemAlloc/cuMemFree wrappers, CUPTI driver-API
+// interposition), and the asynchronous K1/K2/K3 entry points of include/kc.h.
+#include <cupti.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "kc_internal.h"
+
+namespace kc {
+
+// Missing entry points resolve to stubs returning CUDA_ERROR_NOT_INITIALIZED
+// through the ok flag checked in bind_device().
+const Drv& drv() {
+    static Drv d = [] {
+        Drv x;
+        bool all = true;
+#define KC_DRV_LOAD(f)                                                                                    \
+    {                                                                                                     \
+        void* p = nullptr;                                                                                \
+        cudaDriverEntryPointQueryResult q;                                                                \
+        if (cudaGetDriverEntryPoint(#f, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess) \
+            x.f = reinterpret_cast<decltype(x.f)>(p);                                                     \
+        else                                                                                              \
+            all = false;                                                                                  \
+    }
+        KC_DRV_FUNCS(KC_DRV_LOAD)
+#undef KC_DRV_LOAD
+        x.ok = all;
+        return x;
+    }();
+    return d;
+}
+
+kc_status set_err(kc_ctx* ctx, kc_status st, const char* fmt, ...) {
+    if (ctx) {
+        char buf[1024];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        ctx->err = buf;
+    }
+    return st;
+}
+
+static bool sticky(cudaError_t e) {
+    switch (e) {
+        case cudaErrorIllegalAddress: case cudaErrorLaunchFailure: case cudaErrorMisalignedAddress:
+        case cudaErrorIllegalInstruction: case cudaErrorInvalidAddressSpace: case cudaErrorInvalidPc:
+        case cudaErrorHardwareStackError: case cudaErrorAssert: case cudaErrorLaunchTimeout:
+            return true;
+        default:
+            return false;
+    }
+}
+
+kc_status cuda_err(kc_ctx* ctx, cudaError_t e, const char* what) {
+    if (ctx && sticky(e)) ctx->poisoned = true;
+    return set_err(ctx, KC_ERR_CUDA, "%s: %s (%s, cudaError %d)", what, cudaGetErrorName(e), cudaGetErrorString(e),
+                   (int)e);
+}
+
+kc_status cu_err(kc_ctx* ctx, CUresult r, const char* what) {
+    const char* name = nullptr;
+    const char* str = nullptr;
+    if (drv().cuGetErrorName) drv().cuGetErrorName(r, &name);
+    if (drv().cuGetErrorString) drv().cuGetErrorString(r, &str);
+    if (ctx && (r == CUDA_ERROR_ILLEGAL_ADDRESS || r == CUDA_ERROR_LAUNCH_FAILED)) ctx->poisoned = true;
+    return set_err(ctx, KC_ERR_CUDA, "%s: %s (%s, CUresult %d)", what, name ? name : "?", str ? str : "?", (int)r);
+}
+
+cudaError_t ensure(kc_ctx_dev_buf& b, size_t bytes) {
+    if (bytes == 0) bytes = 1;
+    if (b.cap >= bytes) return cudaSuccess;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    size_t cap = std::max(bytes, (size_t)4096);
+    cudaError_t e = cudaMalloc(&b.p, cap);
+    if (e == cudaSuccess) b.cap = cap;
+    return e;
+}
+
+bool bind_device(kc_ctx* ctx) {
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return false;
+    if (cudaFree(nullptr) != cudaSuccess) return false;  // make the primary context current
+    return drv().ok;
+}
+
+kc_status ensure_pinned(kc_ctx* ctx) {
+    if (!ctx->pinned.empty()) return KC_OK;
+    if (!ctx->copy_stream) KC_CHECK_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking),
+                                         "cudaStreamCreate(copy)");
+    for (uint32_t i = 0; i < ctx->depth; ++i) {
+        void* p = nullptr;
+        cudaError_t e = cudaHostAlloc(&p, ctx->io_chunk, cudaHostAllocDefault);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "cudaHostAlloc(staging)");
+        ctx->pinned.push_back(p);
+        cudaEvent_t ev;
+        KC_CHECK_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+        ctx->pin_ev.push_back(ev);
+    }
+    return KC_OK;
+}
+
+size_t granularity(kc_ctx* ctx) {
+    if (ctx->granularity) return ctx->granularity;
+    CUmemAllocationProp prop;
+    memset(&prop, 0, sizeof prop);
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = ctx->device;
+    size_t g = 0;
+    if (KC_DRV(cuMemGetAllocationGranularity)(&g, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS || !g)
+        g = 2ull << 20;
+    ctx->granularity = g;
+    return g;
+}
+
+// Is [base, base+size) backed by live device memory?  cuMemAlloc ranges via
+// RANGE_START/SIZE; VMM mappings via MAPPED on the first and last byte.
+bool region_live(kc_ctx* ctx, uint64_t base, uint64_t size) {
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        auto it = ctx->vmm.upper_bound(base);
+        if (it != ctx->vmm.begin()) {
+            --it;
+            if (it->first <= base && base + size <= it->first + it->second.reserved) return true;
+        }
+    }
+    CUdeviceptr start = 0;
+    size_t rsize = 0;
+    if (KC_DRV(cuPointerGetAttribute)(&start, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, (CUdeviceptr)base) == CUDA_SUCCESS &&
+        KC_DRV(cuPointerGetAttribute)(&rsize, CU_POINTER_ATTRIBUTE_RANGE_SIZE, (CUdeviceptr)base) == CUDA_SUCCESS &&
+        rsize > 0)
+        return (uint64_t)start <= base && base + size <= (uint64_t)start + rsize;
+    int m0 = 0, m1 = 0;
+    if (KC_DRV(cuPointerGetAttribute)(&m0, CU_POINTER_ATTRIBUTE_MAPPED, (CUdeviceptr)base) != CUDA_SUCCESS) return false;
+    if (KC_DRV(cuPointerGetAttribute)(&m1, CU_POINTER_ATTRIBUTE_MAPPED, (CUdeviceptr)(base + size - 1)) != CUDA_SUCCESS)
+        return false;
+    return m0 && m1;
+}
+
+kc_status free_alloc(kc_ctx* ctx, uint64_t dptr, bool track) {
+    kc_ctx::VmmAlloc va;
+    bool is_vmm = false;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        auto it = ctx->vmm.find(dptr);
+        if (it != ctx->vmm.end()) {
+            va = it->second;
+            is_vmm = true;
+            ctx->vmm.erase(it);
+        }
+    }
+    if (is_vmm) {
+        KC_DRV(cuMemUnmap)((CUdeviceptr)dptr, va.reserved);
+        KC_DRV(cuMemRelease)(va.h);
+        KC_CHECK_CU(ctx, KC_DRV(cuMemAddressFree)((CUdeviceptr)dptr, va.reserved), "cuMemAddressFree");
+        if (track && !ctx->cupti_installed) kc_track(ctx, KC_EV_UNMAP, dptr, 0, ctx->device, KC_KIND_VMM);
+        return KC_OK;
+    }
+    KC_CHECK_CU(ctx, KC_DRV(cuMemFree)((CUdeviceptr)dptr), "cuMemFree");
+    if (track && !ctx->cupti_installed) kc_track(ctx, KC_EV_FREE, dptr, 0, ctx->device, KC_KIND_MEMALLOC);
+    return KC_OK;
+}
+
+std::string hex_base(uint64_t base) {
+    char b[32];
+    snprintf(b, sizeof b, "%llx", (unsigned long long)base);
+    return b;
+}
+
+}  // namespace kc
+
+using namespace kc;
+
+#define KC_ENTER(ctx)                                                                  \
+    do {                                                                               \
+        if (!(ctx)) return KC_ERR_ARG;                                                 \
+        if ((ctx)->poisoned) return KC_ERR_CUDA;                                       \
+        if (!bind_device(ctx)) return set_err((ctx), KC_ERR_CUDA, "cannot bind device %d", (ctx)->device); \
+    } while (0)
+
+extern "C" {
+
+int kc_abi_version(void) { return KC_ABI_VERSION; }
+
+const char* kc_build_info(void) {
+    return "libkc sm_100a; K1 tma-bulk 64 slots x 3 stages x 1 KiB; K2 ld.v4.u64 16 KiB units; "
+           "no fast-math, -fmad=false";
+}
+
+const char* kc_status_str(kc_status s) {
+    switch (s) {
+        case KC_OK: return "KC_OK";
+        case KC_PARTIAL: return "KC_PARTIAL";
+        case KC_ERR_ARG: return "KC_ERR_ARG";
+        case KC_ERR_STATE: return "KC_ERR_STATE";
+        case KC_ERR_CUDA: return "KC_ERR_CUDA";
+        case KC_ERR_IO: return "KC_ERR_IO";
+        case KC_ERR_FORMAT: return "KC_ERR_FORMAT";
+        case KC_ERR_VA_UNAVAILABLE: return "KC_ERR_VA_UNAVAILABLE";
+        case KC_ERR_NOT_TRACKED: return "KC_ERR_NOT_TRACKED";
+        case KC_ERR_OUT_OF_BOUNDS: return "KC_ERR_OUT_OF_BOUNDS";
+        case KC_ERR_NOMEM: return "KC_ERR_NOMEM";
+        case KC_ERR_MANIFEST_MISMATCH: return "KC_ERR_MANIFEST_MISMATCH";
+        case KC_ERR_UNSUPPORTED: return "KC_ERR_UNSUPPORTED";
+    }
+    return "KC_?";
+}
+
+kc_status kc_create(kc_ctx** out, const kc_options* opt) {
+    if (!out) return KC_ERR_ARG;
+    *out = nullptr;
+    kc_ctx* ctx = new kc_ctx();
+    int dev = -1;
+    if (opt && opt->device >= 0) {
+        dev = opt->device;
+    } else if (cudaGetDevice(&dev) != cudaSuccess) {
+        delete ctx;
+        return KC_ERR_CUDA;
+    }
+    ctx->device = dev;
+    uint64_t io = opt && opt->io_chunk_bytes ? opt->io_chunk_bytes : 0;
+    if (!io) {
+        const char* env = getenv("KERNCAP_SNAPSHOT_CHUNK_BYTES");
+        if (env && *env) io = strtoull(env, nullptr, 0);
+    }
+    if (!io) io = 64ull << 20;
+    io = (io + kChunk - 1) / kChunk * kChunk;  // reading R1: multiple of the hash chunk
+    ctx->io_chunk = io;
+    ctx->depth = opt && opt->pinned_depth ? opt->pinned_depth : 2;
+    ctx->alloc_mode = opt ? opt->alloc_mode : KC_ALLOC_VMM;
+    if (!bind_device(ctx)) {
+        delete ctx;
+        return KC_ERR_CUDA;
+    }
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0) ctx->num_sms = sms;
+    if (kernels_init() != cudaSuccess) {
+        delete ctx;
+        return KC_ERR_CUDA;
+    }
+    *out = ctx;
+    return KC_OK;
+}
+
+void kc_destroy(kc_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->cupti_installed) kc_track_uninstall(ctx);
+    bind_device(ctx);
+    std::vector<uint64_t> vm;
+    for (auto& kv : ctx->vmm) vm.push_back(kv.first);
+    for (uint64_t b : vm) free_alloc(ctx, b, false);
+    for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch,
+                              &ctx->tmp_hash, &ctx->tmp_count})
+        if (b->p) cudaFree(b->p);
+    for (void* p : ctx->pinned) cudaFreeHost(p);
+    for (cudaEvent_t e : ctx->pin_ev) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+}
+
+const char* kc_last_error(const kc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+// ------------------------------------------------------------------ A1 tracker
+kc_status kc_track(kc_ctx* ctx, kc_event ev, uint64_t base, uint64_t size, int32_t device, int32_t kind) {
+    if (!ctx) return KC_ERR_ARG;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ev == KC_EV_ALLOC || ev == KC_EV_MAP) {
+        if (size == 0) return set_err(ctx, KC_ERR_ARG, "kc_track: zero-size allocation at 0x%llx",
+                                      (unsigned long long)base);
+        auto it = ctx->live.upper_bound(base);
+        if (it != ctx->live.end() && it->first < base + size)
+            return set_err(ctx, KC_ERR_ARG, "kc_track: [0x%llx,+%llu) overlaps live region 0x%llx",
+                           (unsigned long long)base, (unsigned long long)size, (unsigned long long)it->first);
+        if (it != ctx->live.begin()) {
+            auto pv = std::prev(it);
+            if (pv->first + pv->second.size > base)
+                return set_err(ctx, KC_ERR_ARG, "kc_track: [0x%llx,+%llu) overlaps live region 0x%llx",
+                               (unsigned long long)base, (unsigned long long)size, (unsigned long long)pv->first);
+        }
+        kc_region r;
+        r.base = base;
+        r.size = size;
+        r.device = device;
+        r.kind = kind;
+        r.seq = ++ctx->seq;
+        ctx->live[base] = r;
+        return KC_OK;
+    }
+    if (ev == KC_EV_FREE || ev == KC_EV_UNMAP) {
+        auto it = ctx->live.find(base);
+        if (it == ctx->live.end()) {
+            ++ctx->unknown_frees;  // logged, not fatal
+            set_err(ctx, KC_OK, "warning: free of untracked base 0x%llx", (unsigned long long)base);
+            return KC_OK;
+        }
+        ctx->live.erase(it);
+        return KC_OK;
+    }
+    return set_err(ctx, KC_ERR_ARG, "kc_track: bad event %d", (int)ev);
+}
+
+kc_status kc_regions(kc_ctx* ctx, kc_region* out, size_t cap, size_t* n_out) {
+    if (!ctx) return KC_ERR_ARG;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    size_t i = 0;
+    for (auto& kv : ctx->live) {
+        if (i < cap && out) out[i] = kv.second;
+        ++i;
+    }
+    if (n_out) *n_out = i;
+    return KC_OK;
+}
+
+kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
+    KC_ENTER(ctx);
+    if (!dptr_out || size == 0) return set_err(ctx, KC_ERR_ARG, "kc_alloc: bad args");
+    if (ctx->alloc_mode == KC_ALLOC_MEMALLOC) {
+        CUdeviceptr p = 0;
+        CUresult r = KC_DRV(cuMemAlloc)(&p, size);
+        if (r == CUDA_ERROR_OUT_OF_MEMORY)
+            return set_err(ctx, KC_ERR_NOMEM, "cuMemAlloc(%llu): out of memory", (unsigned long long)size);
+        KC_CHECK_CU(ctx, r, "cuMemAlloc");
+        kc_status st = ctx->cupti_installed ? KC_OK
+                                            : kc_track(ctx, KC_EV_ALLOC, (uint64_t)p, size, ctx->device, KC_KIND_MEMALLOC);
+        if (st != KC_OK) {
+            KC_DRV(cuMemFree)(p);
+            return st;
+        }
+        *dptr_out = (uint64_t)p;
+        return KC_OK;
+    }
+    // VMM: reserve VA, create device-local physical memory, map, enable access
+    const size_t G = granularity(ctx);
+    const uint64_t rsz = (size + G - 1) / G * G;
+    CUmemAllocationProp prop;
+    memset(&prop, 0, sizeof prop);
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = ctx->device;
+    CUdeviceptr va = 0;
+    KC_CHECK_CU(ctx, KC_DRV(cuMemAddressReserve)(&va, rsz, G, 0, 0), "cuMemAddressReserve");
+    CUmemGenericAllocationHandle h;
+    CUresult r = KC_DRV(cuMemCreate)(&h, rsz, &prop, 0);
+    if (r != CUDA_SUCCESS) {
+        KC_DRV(cuMemAddressFree)(va, rsz);
+        if (r == CUDA_ERROR_OUT_OF_MEMORY)
+            return set_err(ctx, KC_ERR_NOMEM, "cuMemCreate(%llu): out of memory", (unsigned long long)rsz);
+        return cu_err(ctx, r, "cuMemCreate");
+    }
+    r = KC_DRV(cuMemMap)(va, rsz, 0, h, 0);
+    if (r == CUDA_SUCCESS) {
+        CUmemAccessDesc acc;
+        acc.location = prop.location;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        r = KC_DRV(cuMemSetAccess)(va, rsz, &acc, 1);
+        if (r != CUDA_SUCCESS) KC_DRV(cuMemUnmap)(va, rsz);
+    }
+    if (r != CUDA_SUCCESS) {
+        KC_DRV(cuMemRelease)(h);
+        KC_DRV(cuMemAddressFree)(va, rsz);
+        return cu_err(ctx, r, "cuMemMap/cuMemSetAccess");
+    }
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        ctx->vmm[(uint64_t)va] = kc_ctx::VmmAlloc{rsz, h};
+    }
+    if (!ctx->cupti_installed) {
+        kc_status st = kc_track(ctx, KC_EV_MAP, (uint64_t)va, size, ctx->device, KC_KIND_VMM);
+        if (st != KC_OK) {
+            free_alloc(ctx, (uint64_t)va, false);
+            return st;
+        }
+    }
+    *dptr_out = (uint64_t)va;
+    return KC_OK;
+}
+
+kc_status kc_free(kc_ctx* ctx, uint64_t dptr) {
+    KC_ENTER(ctx);
+    return free_alloc(ctx, dptr, true);
+}
+
+uint64_t kc_kernel_launches(const kc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+uint64_t kc_count_chunks(const kc_region* regions, size_t n) {
+    uint64_t c = 0;
+    for (size_t i = 0; i < n; ++i) c += (regions[i].size + kChunk - 1) / kChunk;
+    return c;
+}
+
+// ------------------------------------------------------------------ K1
+static kc_status upload_regions(kc_ctx* ctx, const kc_region* regions, size_t n, cudaStream_t s, uint64_t* C_out) {
+    std::vector<RegionDev> t(n);
+    uint64_t c = 0;
+    bool aligned = true;
+    for (size_t i = 0; i < n; ++i) {
+        t[i].base = regions[i].base;
+        t[i].size = regions[i].size;
+        t[i].chunk_off = c;
+        c += (regions[i].size + kChunk - 1) / kChunk;
+        if (regions[i].base & 15) aligned = false;
+    }
+    *C_out = c;
+    bool same = t.size() == ctx->regs_cached.size() && ctx->regs.p &&
+                (t.empty() || memcmp(t.data(), ctx->regs_cached.data(), t.size() * sizeof(RegionDev)) == 0);
+    if (!same) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->regs, t.size() * sizeof(RegionDev)), "cudaMalloc(region table)");
+        if (!t.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->regs.p, t.data(), t.size() * sizeof(RegionDev),
+                                               cudaMemcpyHostToDevice, s),
+                          "upload region table");
+        ctx->regs_cached.swap(t);
+        ctx->regs_aligned = aligned;
+    }
+    return KC_OK;
+}
+
+kc_status kc_hash(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_chunk_hash, uint64_t* d_region_digest,
+                  uint64_t* d_snapshot_digest, void* stream) {
+    KC_ENTER(ctx);
+    if (n && !regions) return set_err(ctx, KC_ERR_ARG, "kc_hash: regions is NULL");
+    for (size_t i = 0; i < n; ++i) {
+        if (regions[i].size == 0) return set_err(ctx, KC_ERR_ARG, "kc_hash: region %zu has size 0", i);
+        if (d_snapshot_digest && i > 0 && regions[i].base < regions[i - 1].base + regions[i - 1].size)
+            return set_err(ctx, KC_ERR_ARG, "kc_hash: regions not sorted/non-overlapping (snapshot digest, R25)");
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    uint64_t C = 0;
+    kc_status st = upload_regions(ctx, regions, n, s, &C);
+    if (st != KC_OK) return st;
+    if (C && !d_chunk_hash) return set_err(ctx, KC_ERR_ARG, "kc_hash: d_chunk_hash is NULL");
+    KC_CHECK_CUDA(ctx, launch_hash((const RegionDev*)ctx->regs.p, (int)n, C, ctx->regs_aligned, d_chunk_hash,
+                                   ctx->num_sms, s),
+                  "launch K1");
+    if (C) ctx->launches += 1;
+    if (d_region_digest || d_snapshot_digest) {
+        if (d_snapshot_digest)
+            KC_CHECK_CUDA(ctx, ensure(ctx->digest_scratch, 24 * n + 8), "cudaMalloc(digest scratch)");
+        KC_CHECK_CUDA(ctx, launch_digests((const RegionDev*)ctx->regs.p, (int)n, d_chunk_hash, d_region_digest,
+                                          (uint8_t*)ctx->digest_scratch.p, d_snapshot_digest, s),
+                      "launch digests");
+        if (n) ctx->launches += d_snapshot_digest ? 2 : 1;
+        if (d_snapshot_digest && n == 0)
+            KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_snapshot_digest, 0, 8, s), "snapshot digest of nothing");
+    }
+    return KC_OK;
+}
+
+// ------------------------------------------------------------------ K3
+kc_status kc_written(kc_ctx* ctx, const uint64_t* d_pre, const uint64_t* d_post, uint64_t n_chunks,
+                     uint64_t* d_w_bitmap, uint64_t* d_written_count, void* stream) {
+    KC_ENTER(ctx);
+    if (n_chunks && (!d_pre || !d_post || !d_w_bitmap)) return set_err(ctx, KC_ERR_ARG, "kc_written: null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint64_t* cnt = d_written_count;
+    if (!cnt) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->tmp_count, 8), "cudaMalloc");
+        cnt = (uint64_t*)ctx->tmp_count.p;
+    }
+    KC_CHECK_CUDA(ctx, cudaMemsetAsync(cnt, 0, 8, s), "memset count");
+    KC_CHECK_CUDA(ctx, launch_written(d_pre, d_post, n_chunks, d_w_bitmap, cnt, ctx->num_sms, s), "launch K3");
+    if (n_chunks) ctx->launches += 1;
+    return KC_OK;
+}
+
+// ------------------------------------------------------------------ K2
+static int elem_size(int dt) {
+    switch (dt) {
+        case KC_DT_BYTES: case KC_DT_U8: case KC_DT_I8: return 1;
+        case KC_DT_U16: case KC_DT_I16: case KC_DT_F16: case KC_DT_BF16: return 2;
+        case KC_DT_U32: case KC_DT_I32: case KC_DT_F32: return 4;
+        case KC_DT_U64: case KC_DT_I64: case KC_DT_F64: return 8;
+    }
+    return 0;
+}
+
+kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
+                        const uint64_t* report_nbytes, const uint64_t* bitmap_word0, const kc_tolerance* tol,
+                        kc_diff_report* d_reports, uint64_t* d_bitmaps, void* stream) {
+    KC_ENTER(ctx);
+    if ((n_bufs && !bufs) || (n_reports && (!d_reports || !report_nbytes)))
+        return set_err(ctx, KC_ERR_ARG, "kc_diff_async: null pointer");
+    if (d_bitmaps && !bitmap_word0) return set_err(ctx, KC_ERR_ARG, "kc_diff_async: bitmaps need bitmap_word0");
+    const kc_tolerance deft = {1e-8, 1e-5, 0, 0};  // numpy defaults (reading R14)
+    if (!tol) tol = &deft;
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<ReportMeta> meta(n_reports);
+    std::vector<int> rep_dt(n_reports, -1);
+    // validate, then order segments by dtype (stable) so each dtype is one launch
+    std::vector<size_t> order;
+    order.reserve(n_bufs);
+    for (size_t i = 0; i < n_bufs; ++i) {
+        const kc_buffer& b = bufs[i];
+        const int es = elem_size(b.dtype);
+        if (es == 0) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: bad dtype %d", i, b.dtype);
+        if (b.nbytes % es) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: %llu bytes is not a multiple of "
+                                          "the element size %d", i, (unsigned long long)b.nbytes, es);
+        if (b.report < 0 || (size_t)b.report >= n_reports)
+            return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: report index %d out of range", i, b.report);
+        if (rep_dt[b.report] >= 0 && rep_dt[b.report] != b.dtype)
+            return set_err(ctx, KC_ERR_ARG, "kc_diff: report %d mixes dtypes", b.report);
+        rep_dt[b.report] = b.dtype;
+        if (b.nbytes == 0) continue;
+        if (!b.ref || !b.act) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: null VA", i);
+        order.push_back(i);
+    }
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return bufs[a].dtype < bufs[b].dtype; });
+    std::vector<SegDev> segs;
+    segs.reserve(order.size());
+    std::vector<DiffGroup> groups;
+    uint64_t U = 0;
+    for (size_t i : order) {
+        const kc_buffer& b = bufs[i];
+        SegDev d;
+        d.ref = b.ref;
+        d.act = b.act;
+        d.nbytes = b.nbytes;
+        d.bitmap_word0 = bitmap_word0 ? bitmap_word0[b.report] : 0;
+        d.bitmap_chunk0 = b.bitmap_chunk0;
+        d.unit_off = U;
+        d.dtype = b.dtype;
+        d.report = b.report;
+        const uint64_t nu = (b.nbytes + kDiffUnit - 1) / kDiffUnit;
+        if (groups.empty() || groups.back().dtype != b.dtype)
+            groups.push_back(DiffGroup{b.dtype, (int32_t)segs.size(), 0, U, 0});
+        groups.back().n_segs += 1;
+        groups.back().n_units += nu;
+        U += nu;
+        segs.push_back(d);
+    }
+    uint64_t bitmap_words = 0;
+    for (size_t j = 0; j < n_reports; ++j) {
+        meta[j].nbytes = report_nbytes[j];
+        meta[j].dtype = rep_dt[j] < 0 ? KC_DT_BYTES : rep_dt[j];
+        if (bitmap_word0) {
+            const uint64_t w = (report_nbytes[j] + kChunk - 1) / kChunk;
+            bitmap_words = std::max(bitmap_words, bitmap_word0[j] + (w + 63) / 64);
+        }
+    }
+    KC_CHECK_CUDA(ctx, ensure(ctx->segs, segs.size() * sizeof(SegDev)), "cudaMalloc(segments)");
+    KC_CHECK_CUDA(ctx, ensure(ctx->meta, meta.size() * sizeof(ReportMeta)), "cudaMalloc(meta)");
+    if (!segs.empty())
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(SegDev),
+                                           cudaMemcpyHostToDevice, s), "upload segments");
+    if (!meta.empty())
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->meta.p, meta.data(), meta.size() * sizeof(ReportMeta),
+                                           cudaMemcpyHostToDevice, s), "upload meta");
+    if (n_reports)
+        KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_reports, 0, n_reports * sizeof(kc_diff_report), s), "zero reports");
+    if (d_bitmaps && bitmap_words)
+        KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_bitmaps, 0, bitmap_words * 8, s), "zero bitmaps");
+    KC_CHECK_CUDA(ctx, launch_diff((const SegDev*)ctx->segs.p, groups.data(), (int)groups.size(),
+                                   (const ReportMeta*)ctx->meta.p, (int)n_reports, d_reports, d_bitmaps, tol->atol,
+                                   tol->rtol, tol->equal_nan, ctx->num_sms, s),
+                  "launch K2");
+    for (auto& g : groups) ctx->launches += g.n_units ? 1 : 0;
+    if (n_reports) ctx->launches += 1;
+    return KC_OK;
+}
+
+kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol, kc_diff_report* reps,
+                  uint64_t* h_bitmaps, void* stream) {
+    KC_ENTER(ctx);
+    if (n && (!bufs || !reps)) return set_err(ctx, KC_ERR_ARG, "kc_diff: null pointer");
+    std::vector<kc_buffer> b(bufs, bufs + n);
+    std::vector<uint64_t> nbytes(n), word0(n);
+    uint64_t words = 0;
+    for (size_t i = 0; i < n; ++i) {
+        b[i].report = (int32_t)i;
+        b[i].bitmap_chunk0 = 0;
+        nbytes[i] = bufs[i].nbytes;
+        word0[i] = words;
+        words += ((bufs[i].nbytes + kChunk - 1) / kChunk + 63) / 64;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    KC_CHECK_CUDA(ctx, ensure(ctx->reps, std::max<size_t>(1, n) * sizeof(kc_diff_report)), "cudaMalloc(reports)");
+    KC_CHECK_CUDA(ctx, ensure(ctx->bitmaps, std::max<uint64_t>(1, words) * 8), "cudaMalloc(bitmaps)");
+    kc_status st = kc_diff_async(ctx, b.data(), n, n, nbytes.data(), word0.data(), tol, (kc_diff_report*)ctx->reps.p,
+                                 (uint64_t*)ctx->bitmaps.p, stream);
+    if (st != KC_OK) return st;
+    KC_CHECK_CUDA(ctx, cudaMemcpyAsync(reps, ctx->reps.p, n * sizeof(kc_diff_report), cudaMemcpyDeviceToHost, s),
+                  "D2H reports");
+    if (h_bitmaps && words)
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(h_bitmaps, ctx->bitmaps.p, words * 8, cudaMemcpyDeviceToHost, s),
+                      "D2H bitmaps");
+    KC_CHECK_CUDA(ctx, cudaStreamSynchronize(s), "kc_diff sync");
+    return KC_OK;
+}
+
+// ------------------------------------------------------------------ CUPTI interposition
+// The CUDA analog of the paper's HSA memory hooks: driver-API
+// callbacks on the EXIT site of every allocation/free/map entry point feed the
+// tracker.  CUPTI is resolved with dlopen so libkc.so loads without it; types,
+// callback ids and parameter structs come from the CUDA 12.9 headers.
+namespace {
+typedef CUptiResult (*cupti_subscribe_t)(CUpti_SubscriberHandle*, CUpti_CallbackFunc, void*);
+typedef CUptiResult (*cupti_enable_t)(uint32_t, CUpti_SubscriberHandle, CUpti_CallbackDomain, CUpti_CallbackId);
+typedef CUptiResult (*cupti_unsubscribe_t)(CUpti_SubscriberHandle);
+void* g_cupti = nullptr;
+cupti_subscribe_t p_subscribe = nullptr;
+cupti_enable_t p_enable = nullptr;
+cupti_unsubscribe_t p_unsubscribe = nullptr;
+
+const CUpti_CallbackId kTrackedCbids[] = {
+    CUPTI_DRIVER_TRACE_CBID_cuMemAlloc_v2,           CUPTI_DRIVER_TRACE_CBID_cuMemAllocPitch_v2,
+    CUPTI_DRIVER_TRACE_CBID_cuMemFree_v2,            CUPTI_DRIVER_TRACE_CBID_cuMemAllocAsync,
+    CUPTI_DRIVER_TRACE_CBID_cuMemAllocAsync_ptsz,    CUPTI_DRIVER_TRACE_CBID_cuMemFreeAsync,
+    CUPTI_DRIVER_TRACE_CBID_cuMemFreeAsync_ptsz,     CUPTI_DRIVER_TRACE_CBID_cuMemAllocFromPoolAsync,
+    CUPTI_DRIVER_TRACE_CBID_cuMemAllocFromPoolAsync_ptsz, CUPTI_DRIVER_TRACE_CBID_cuMemMap,
+    CUPTI_DRIVER_TRACE_CBID_cuMemUnmap};
+
+void CUPTIAPI cupti_cb(void* user, CUpti_CallbackDomain domain, CUpti_CallbackId cbid, const void* cbdata) {
+    kc_ctx* ctx = (kc_ctx*)user;
+    const CUpti_CallbackData* d = (const CUpti_CallbackData*)cbdata;
+    if (domain != CUPTI_CB_DOMAIN_DRIVER_API || d->callbackSite != CUPTI_API_EXIT) return;
+    const CUresult* rv = (const CUresult*)d->functionReturnValue;
+    if (rv && *rv != CUDA_SUCCESS) return;
+    const int dev = ctx->device;
+    switch (cbid) {
+        case CUPTI_DRIVER_TRACE_CBID_cuMemAlloc_v2: {
+            auto p = (const cuMemAlloc_v2_params*)d->functionParams;
+            kc_track(ctx, KC_EV_ALLOC, (uint64_t)*p->dptr, p->bytesize, dev, KC_KIND_MEMALLOC);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuMemAllocPitch_v2: {
+            auto p = (const cuMemAllocPitch_v2_params*)d->functionParams;
+            kc_track(ctx, KC_EV_ALLOC, (uint64_t)*p->dptr, (uint64_t)*p->pPitch * p->Height, dev, KC_KIND_MEMALLOC);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuMemFree_v2: {
+            auto p = (const cuMemFree_v2_params*)d->functionParams;
+            kc_track(ctx, KC_EV_FREE, (uint64_t)p->dptr, 0, dev, KC_KIND_MEMALLOC);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuMemAllocAsync:
+        case CUPTI_DRIVER_TRACE_CBID_cuMemAllocAsync_ptsz: {
+            auto p = (const cuMemAllocAsync_params*)d->functionParams;
+            kc_track(ctx, KC_EV_ALLOC, (uint64_t)*p->dptr, p->bytesize, dev, KC_KIND_POOL);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuMemAllocFromPoolAsync:
+        case CUPTI_DRIVER_TRACE_CBID_cuMemAllocFromPoolAsync_ptsz: {
+            auto p = (const cuMemAllocFromPoolAsync_params*)d->functionParams;
+            kc_track(ctx, KC_EV_ALLOC, (uint64_t)*p->dptr, p->bytesize, dev, KC_KIND_POOL);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuMemFreeAsync:
+        case CUPTI_DRIVER_TRACE_CBID_cuMemFreeAsync_ptsz: {
+            auto p = (const cuMemFreeAsync_params*)d->functionParams;
+            kc_track(ctx, KC_EV_FREE, (uint64_t)p->dptr, 0, dev, KC_KIND_POOL);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuMemMap: {
+            auto p = (const cuMemMap_params*)d->functionParams;
+            kc_track(ctx, KC_EV_MAP, (uint64_t)p->ptr, p->size, dev, KC_KIND_VMM);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuMemUnmap: {
+            auto p = (const cuMemUnmap_params*)d->functionParams;
+            kc_track(ctx, KC_EV_UNMAP, (uint64_t)p->ptr, p->size, dev, KC_KIND_VMM);
+            break;
+        }
+        default:
+            break;
+    }
+}
+}  // namespace
+
+kc_status kc_track_install(kc_ctx* ctx) {
+    if (!ctx) return KC_ERR_ARG;
+    if (ctx->cupti_installed) return set_err(ctx, KC_ERR_STATE, "kc_track_install: already installed (SPEC.md:311)");
+    if (!g_cupti) {
+        const char* names[] = {"libcupti.so.12", "libcupti.so", "/usr/local/cuda/lib64/libcupti.so.12",
+                               "/usr/local/cuda/extras/CUPTI/lib64/libcupti.so.12"};
+        for (const char* n : names)
+            if ((g_cupti = dlopen(n, RTLD_NOW | RTLD_LOCAL))) break;
+        if (!g_cupti) return set_err(ctx, KC_ERR_UNSUPPORTED, "kc_track_install: libcupti not found");
+        p_subscribe = (cupti_subscribe_t)dlsym(g_cupti, "cuptiSubscribe");
+        p_enable = (cupti_enable_t)dlsym(g_cupti, "cuptiEnableCallback");
+        p_unsubscribe = (cupti_unsubscribe_t)dlsym(g_cupti, "cuptiUnsubscribe");
+        if (!p_subscribe || !p_enable || !p_unsubscribe)
+            return set_err(ctx, KC_ERR_UNSUPPORTED, "kc_track_install: CUPTI symbols missing");
+    }
+    CUpti_SubscriberHandle sub = nullptr;
+    CUptiResult rc = p_subscribe(&sub, cupti_cb, ctx);
+    if (rc != CUPTI_SUCCESS)
+        return set_err(ctx, KC_ERR_STATE, "cuptiSubscribe failed (%d): another subscriber?", (int)rc);
+    ctx->cupti_subscriber = (void*)sub;
+    for (CUpti_CallbackId c : kTrackedCbids) {
+        rc = p_enable(1, sub, CUPTI_CB_DOMAIN_DRIVER_API, c);
+        if (rc != CUPTI_SUCCESS) {
+            p_unsubscribe(sub);
+            ctx->cupti_subscriber = nullptr;
+            return set_err(ctx, KC_ERR_STATE, "cuptiEnableCallback(%u) failed (%d)", (unsigned)c, (int)rc);
+        }
+    }
+    ctx->cupti_installed = true;
+    return KC_OK;
+}
+
+kc_status kc_track_uninstall(kc_ctx* ctx) {
+    if (!ctx) return KC_ERR_ARG;
+    if (!ctx->cupti_installed) return set_err(ctx, KC_ERR_STATE, "kc_track_uninstall: not installed");
+    p_unsubscribe((CUpti_SubscriberHandle)ctx->cupti_subscriber);
+    ctx->cupti_subscriber = nullptr;
+    ctx->cupti_installed = false;
+    return KC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1221 @@
+// kc_snapshot.cu -- the address-space closure on CUDA: kc_capture (A3/A5),
+// kc_restore (A6), kc_replay (A7), kc_validate (A8), kc_prereserve.
+//
+// Snapshot format kc-snapshot/1 (names mirror
+// the paper's capture directory):
+//   dispatch.json, kernarg.bin, kernel.cubin, memory_regions.json,
+//   memory/region_<hex>.bin (+ .xxh64 manifest), post/region_<hex>.xxh64,
+//   written/region_<hex>.idx + .bin (PRE_W), capture_log.json, capture_complete.
+// Ordering and crash safety: metadata before any D2H copy,
+// per-region copy failures tolerated and logged, the sentinel written last.
+#include <errno.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <sys/types.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "kc_internal.h"
+#include "kc_json.h"
+
+using namespace kc;
+
+namespace {
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+bool mkdir_p(const std::string& path) {
+    std::string cur;
+    for (size_t i = 0; i < path.size(); ++i) {
+        cur += path[i];
+        if (path[i] == '/' || i + 1 == path.size()) {
+            if (cur.size() > 1 && mkdir(cur.c_str(), 0755) != 0 && errno != EEXIST) return false;
+        }
+    }
+    return true;
+}
+
+bool write_file(const std::string& path, const void* data, size_t n) {
+    FILE* f = fopen(path.c_str(), "wb");
+    if (!f) return false;
+    bool ok = n == 0 || fwrite(data, 1, n, f) == n;
+    ok = (fclose(f) == 0) && ok;
+    return ok;
+}
+
+bool write_text(const std::string& path, const std::string& s) { return write_file(path, s.data(), s.size()); }
+
+bool read_bin(const std::string& path, std::vector<uint8_t>& out) {
+    FILE* f = fopen(path.c_str(), "rb");
+    if (!f) return false;
+    fseek(f, 0, SEEK_END);
+    long n = ftell(f);
+    fseek(f, 0, SEEK_SET);
+    out.resize(n > 0 ? (size_t)n : 0);
+    bool ok = n <= 0 || fread(out.data(), 1, (size_t)n, f) == (size_t)n;
+    fclose(f);
+    return ok;
+}
+
+bool read_u64s(const std::string& path, std::vector<uint64_t>& out) {
+    std::vector<uint8_t> b;
+    if (!read_bin(path, b) || b.size() % 8) return false;
+    out.resize(b.size() / 8);
+    memcpy(out.data(), b.data(), b.size());  // little-endian host (x86-64), reading R5
+    return true;
+}
+
+std::string hex16(uint64_t v) {
+    char b[32];
+    snprintf(b, sizeof b, "%016llx", (unsigned long long)v);
+    return b;
+}
+
+// ------------------------------------------------------------------ pinned ring D2H / H2D
+// Streams [base, base+size) to a FILE through ctx->depth pinned buffers of
+// ctx->io_chunk bytes (KERNCAP_SNAPSHOT_CHUNK_BYTES): the DMA
+// of piece i overlaps the file write of piece i-1.
+bool d2h_stream(kc_ctx* ctx, uint64_t base, uint64_t size, FILE* f, kc_capture_report* rep, std::string& err) {
+    const uint64_t io = ctx->io_chunk;
+    const uint32_t depth = ctx->depth;
+    const uint64_t np = (size + io - 1) / io;
+    std::vector<uint64_t> pend(depth, 0);
+    bool ok = true;
+    auto drain = [&](uint64_t i) {
+        const uint32_t slot = i % depth;
+        cudaError_t e = cudaEventSynchronize(ctx->pin_ev[slot]);
+        if (e != cudaSuccess) { err = cudaGetErrorString(e); ok = false; return; }
+        if (ok && f && fwrite(ctx->pinned[slot], 1, pend[slot], f) != pend[slot]) { err = "fwrite failed"; ok = false; }
+    };
+    for (uint64_t i = 0; i < np && ok; ++i) {
+        const uint32_t slot = i % depth;
+        if (i >= depth) drain(i - depth);
+        if (!ok) break;
+        const uint64_t b = std::min(io, size - i * io);
+        cudaError_t e = cudaMemcpyAsync(ctx->pinned[slot], (const void*)(base + i * io), b, cudaMemcpyDeviceToHost,
+                                        ctx->copy_stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            err = std::string("cudaMemcpyAsync D2H: ") + cudaGetErrorString(e);
+            ok = false;
+            break;
+        }
+        cudaEventRecord(ctx->pin_ev[slot], ctx->copy_stream);
+        pend[slot] = b;
+        if (rep) {
+            rep->dma_calls += 1;
+            rep->d2h_bytes += b;
+            rep->staging_high_water = std::max<uint64_t>(rep->staging_high_water, std::min<uint64_t>(i + 1, depth) * io);
+        }
+    }
+    // drain the tail in order
+    const uint64_t first = np > depth ? np - depth : 0;
+    for (uint64_t i = first; i < np; ++i)
+        if (ok) drain(i);
+    cudaStreamSynchronize(ctx->copy_stream);
+    return ok;
+}
+
+bool h2d_stream(kc_ctx* ctx, FILE* f, uint64_t base, uint64_t size, uint64_t* h2d_bytes, std::string& err) {
+    const uint64_t io = ctx->io_chunk;
+    const uint32_t depth = ctx->depth;
+    const uint64_t np = (size + io - 1) / io;
+    for (uint64_t i = 0; i < np; ++i) {
+        const uint32_t slot = i % depth;
+        if (i >= depth) cudaEventSynchronize(ctx->pin_ev[slot]);  // buffer free again
+        const uint64_t b = std::min(io, size - i * io);
+        if (fread(ctx->pinned[slot], 1, b, f) != b) { err = "short read"; cudaStreamSynchronize(ctx->copy_stream); return false; }
+        cudaError_t e = cudaMemcpyAsync((void*)(base + i * io), ctx->pinned[slot], b, cudaMemcpyHostToDevice,
+                                        ctx->copy_stream);
+        if (e != cudaSuccess) { err = cudaGetErrorString(e); cudaStreamSynchronize(ctx->copy_stream); return false; }
+        cudaEventRecord(ctx->pin_ev[slot], ctx->copy_stream);
+        if (h2d_bytes) *h2d_bytes += b;
+    }
+    cudaStreamSynchronize(ctx->copy_stream);
+    return true;
+}
+
+// Gather (K4) many device ranges into a device staging buffer, then D2H into
+// the file in io pieces.  Used for the written chunks W.
+bool gather_d2h(kc_ctx* ctx, const std::vector<std::pair<uint64_t, uint64_t>>& ranges, FILE* f, void* d_stage,
+                uint64_t stage_bytes, uint64_t* d_tab, kc_capture_report* rep, std::string& err) {
+    size_t i = 0;
+    while (i < ranges.size()) {
+        std::vector<uint64_t> src, dst, len;
+        uint64_t off = 0;
+        while (i < ranges.size() && off + ranges[i].second <= stage_bytes) {
+            src.push_back(ranges[i].first);
+            dst.push_back((uint64_t)d_stage + off);
+            len.push_back(ranges[i].second);
+            off += ranges[i].second;
+            ++i;
+        }
+        if (src.empty()) { err = "range larger than staging"; return false; }
+        const int n = (int)src.size();
+        cudaMemcpyAsync(d_tab, src.data(), 8 * n, cudaMemcpyHostToDevice, ctx->copy_stream);
+        cudaMemcpyAsync(d_tab + n, dst.data(), 8 * n, cudaMemcpyHostToDevice, ctx->copy_stream);
+        cudaMemcpyAsync(d_tab + 2 * n, len.data(), 8 * n, cudaMemcpyHostToDevice, ctx->copy_stream);
+        launch_gather(d_tab, d_tab + n, d_tab + 2 * n, n, ctx->copy_stream);
+        cudaError_t e = cudaMemcpyAsync(ctx->pinned[0], d_stage, off, cudaMemcpyDeviceToHost, ctx->copy_stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->copy_stream);
+        if (e != cudaSuccess) { err = cudaGetErrorString(e); return false; }
+        if (rep) { rep->dma_calls += 1; rep->d2h_bytes += off; }
+        if (fwrite(ctx->pinned[0], 1, off, f) != off) { err = "fwrite failed"; return false; }
+    }
+    return true;
+}
+
+struct RegionState {
+    kc_region r;
+    bool ok = true;
+    std::string error;
+    uint64_t chunk0 = 0;  // index into the manifest arrays (ok regions only)
+    uint64_t n_chunks = 0;
+    uint64_t pre_digest = 0, post_digest = 0;
+    std::vector<uint64_t> written;
+};
+
+}  // namespace
+
+namespace kc {
+
+// Hash a region list (all must be live) and bring the manifest (and digests) to the host.
+kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std::vector<uint64_t>& out_hashes,
+                            std::vector<uint64_t>* out_digests, uint64_t* out_snapshot, uint64_t* d_hash_out,
+                            cudaStream_t s) {
+    const uint64_t C = kc_count_chunks(regs.data(), regs.size());
+    uint64_t* d_h = d_hash_out;
+    if (!d_h) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->tmp_hash, (C + regs.size() + 1) * 8), "cudaMalloc(manifest)");
+        d_h = (uint64_t*)ctx->tmp_hash.p;
+    }
+    uint64_t* d_dig = nullptr;
+    uint64_t* d_snap = nullptr;
+    kc_ctx_dev_buf dig;
+    if (out_digests || out_snapshot) {
+        KC_CHECK_CUDA(ctx, ensure(dig, (regs.size() + 1) * 8), "cudaMalloc(digests)");
+        d_dig = (uint64_t*)dig.p;
+        d_snap = d_dig + regs.size();
+    }
+    kc_status st = kc_hash(ctx, regs.data(), regs.size(), d_h, d_dig, out_snapshot ? d_snap : nullptr, s);
+    if (st != KC_OK) {
+        if (dig.p) cudaFree(dig.p);
+        return st;
+    }
+    out_hashes.resize(C);
+    if (C) KC_CHECK_CUDA(ctx, cudaMemcpyAsync(out_hashes.data(), d_h, C * 8, cudaMemcpyDeviceToHost, s), "D2H manifest");
+    std::vector<uint64_t> tmp(regs.size() + 1);
+    if (d_dig) KC_CHECK_CUDA(ctx, cudaMemcpyAsync(tmp.data(), d_dig, (regs.size() + 1) * 8, cudaMemcpyDeviceToHost, s),
+                             "D2H digests");
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (dig.p) cudaFree(dig.p);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "hash sync");
+    if (out_digests) out_digests->assign(tmp.begin(), tmp.begin() + regs.size());
+    if (out_snapshot) *out_snapshot = regs.empty() ? 0 : tmp[regs.size()];
+    return KC_OK;
+}
+
+}  // namespace kc
+
+// ====================================================================== capture
+extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
+                                const char* dir_c, kc_capture_mode mode, kc_capture_report* rep_out) {
+    if (!ctx) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    if (!d || !dir_c) return set_err(ctx, KC_ERR_ARG, "kc_capture: dispatch and dir are required");
+    if (mode != KC_MODE_PRE_W && mode != KC_MODE_POST) return set_err(ctx, KC_ERR_ARG, "kc_capture: bad mode");
+    kc_capture_report rep;
+    memset(&rep, 0, sizeof rep);
+    const double t0 = now_s();
+    const std::string dir = dir_c;
+    cudaStream_t cs = (cudaStream_t)d->stream;
+
+    // ---- region list: given, or every tracked allocation; sorted by base (R25)
+    std::vector<kc_region> list;
+    if (regions) {
+        list.assign(regions, regions + n);
+    } else {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        for (auto& kv : ctx->live) list.push_back(kv.second);
+    }
+    list.erase(std::remove_if(list.begin(), list.end(), [](const kc_region& r) { return r.size == 0; }), list.end());
+    std::sort(list.begin(), list.end(), [](const kc_region& a, const kc_region& b) { return a.base < b.base; });
+    for (size_t i = 1; i < list.size(); ++i)
+        if (list[i].base < list[i - 1].base + list[i - 1].size)
+            return set_err(ctx, KC_ERR_ARG, "kc_capture: regions overlap at 0x%llx", (unsigned long long)list[i].base);
+
+    // ---- resolve the function (D4 analog) before touching memory
+    CUfunction f = (CUfunction)d->func;
+    CUmodule own_mod = nullptr;
+    if (!f) {
+        if (!d->image || !d->mangled) return set_err(ctx, KC_ERR_ARG, "kc_capture: need func or image+mangled");
+        KC_CHECK_CU(ctx, KC_DRV(cuModuleLoadData)(&own_mod, d->image), "cuModuleLoadData");
+        CUresult r = KC_DRV(cuModuleGetFunction)(&f, own_mod, d->mangled);
+        if (r != CUDA_SUCCESS) {
+            KC_DRV(cuModuleUnload)(own_mod);
+            return set_err(ctx, KC_ERR_ARG, "kc_capture: symbol %s not found in image", d->mangled);
+        }
+    }
+    std::string mangled = d->mangled ? d->mangled : "";
+    if (mangled.empty()) {
+        const char* nm = nullptr;
+        if (KC_DRV(cuFuncGetName)(&nm, f) == CUDA_SUCCESS && nm) mangled = nm;
+    }
+    // kernarg layout via cuFuncGetParamInfo (reading R22)
+    std::vector<std::pair<size_t, size_t>> layout;
+    for (size_t i = 0; i < 4096; ++i) {
+        size_t off = 0, sz = 0;
+        if (KC_DRV(cuFuncGetParamInfo)(f, i, &off, &sz) != CUDA_SUCCESS) break;
+        layout.emplace_back(off, sz);
+    }
+
+    if (!layout.empty() && d->kernarg && d->kernarg_size != layout.back().first + layout.back().second) {
+        if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+        return set_err(ctx, KC_ERR_ARG, "kc_capture: kernarg_size %u != parameter buffer size %zu of %s",
+                       d->kernarg_size, layout.back().first + layout.back().second, mangled.c_str());
+    }
+    kc_status final_st = KC_OK;
+    // ---- A3 bracket: quiesce every stream that could write tracked memory
+    {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+            return cuda_err(ctx, e, "kc_capture: quiesce");
+        }
+    }
+    std::vector<RegionState> rs(list.size());
+    std::vector<kc_region> live;
+    for (size_t i = 0; i < list.size(); ++i) {
+        rs[i].r = list[i];
+        rs[i].n_chunks = (list[i].size + kChunk - 1) / kChunk;
+        if (!region_live(ctx, list[i].base, list[i].size)) {
+            rs[i].ok = false;
+            rs[i].error = "not inside a live CUDA allocation before the dispatch";
+        } else {
+            rs[i].chunk0 = kc_count_chunks(live.data(), live.size());
+            live.push_back(list[i]);
+        }
+    }
+    rep.n_regions = list.size();
+
+    // ---- A2: pre-manifest (K1)
+    double t = now_s();
+    std::vector<uint64_t> pre_h, pre_dig;
+    uint64_t pre_snap = 0;
+    kc_status st = hash_regions_sync(ctx, live, pre_h, &pre_dig, &pre_snap, nullptr, cs);
+    if (st != KC_OK) {
+        if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+        return st;
+    }
+    rep.t_hash_pre_s = now_s() - t;
+    {
+        size_t j = 0;
+        for (auto& r : rs)
+            if (r.ok) r.pre_digest = pre_dig[j++];
+    }
+    rep.n_chunks = pre_h.size();
+    for (auto& r : live) rep.total_bytes += r.size;
+
+    if (!mkdir_p(dir + "/memory") || !mkdir_p(dir + "/post") || !mkdir_p(dir + "/written")) {
+        if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+        return set_err(ctx, KC_ERR_IO, "kc_capture: cannot create %s", dir.c_str());
+    }
+    unlink((dir + "/capture_complete").c_str());  // sentinel-last
+    st = ensure_pinned(ctx);
+    if (st != KC_OK) {
+        if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+        return st;
+    }
+
+    auto write_metadata = [&](bool post_digests) -> bool {
+        int cc_major = 0, cc_minor = 0;
+        cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, ctx->device);
+        cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, ctx->device);
+        std::string j = "{\n";
+        j += "  \"format\": \"kc-snapshot/1\",\n";
+        j += std::string("  \"mode\": \"") + (mode == KC_MODE_PRE_W ? "pre_w" : "post") + "\",\n";
+        j += "  \"mangled_symbol\": \"" + kcj::esc(mangled) + "\",\n";
+        char b[512];
+        snprintf(b, sizeof b,
+                 "  \"grid\": [%u, %u, %u],\n  \"block\": [%u, %u, %u],\n  \"cluster\": [1, 1, 1],\n"
+                 "  \"shared_mem_bytes\": %u,\n  \"kernarg_size\": %u,\n  \"device_ordinal\": %d,\n"
+                 "  \"compute_capability\": \"%d.%d\",\n  \"code_object_bytes\": %zu,\n",
+                 d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2], d->smem_bytes,
+                 d->kernarg_size, ctx->device, cc_major, cc_minor, d->image ? d->image_size : (size_t)0);
+        j += b;
+        j += "  \"kernarg_layout\": [";
+        for (size_t i = 0; i < layout.size(); ++i) {
+            snprintf(b, sizeof b, "%s{\"offset\": %zu, \"size\": %zu}", i ? ", " : "", layout[i].first,
+                     layout[i].second);
+            j += b;
+        }
+        j += "],\n  \"hash\": {\"algo\": \"xxh64\", \"seed\": 0, \"chunk_bytes\": 65536}\n}\n";
+        if (!write_text(dir + "/dispatch.json", j)) return false;
+        if (!write_file(dir + "/kernarg.bin", d->kernarg, d->kernarg ? d->kernarg_size : 0)) return false;
+        if (d->image && d->image_size && !write_file(dir + "/kernel.cubin", d->image, d->image_size)) return false;
+        std::string m = "[\n";
+        for (size_t i = 0; i < rs.size(); ++i) {
+            const RegionState& r = rs[i];
+            const std::string hx = hex_base(r.r.base);
+            const char* kind = r.r.kind == KC_KIND_VMM ? "vmm" : (r.r.kind == KC_KIND_POOL ? "pool" : "mem_alloc");
+            snprintf(b, sizeof b,
+                     "  {\"base\": \"%s\", \"size\": %llu, \"alloc_kind\": \"%s\", \"device\": %d, "
+                     "\"contains_kernarg\": false, \"data_file\": \"memory/region_%s.bin\", \"n_chunks\": %llu, "
+                     "\"digest\": \"%s\", \"status\": \"%s\", \"seq\": %llu}%s\n",
+                     hx.c_str(), (unsigned long long)r.r.size, kind, r.r.device, hx.c_str(),
+                     (unsigned long long)r.n_chunks, hex16(post_digests ? r.post_digest : r.pre_digest).c_str(),
+                     r.ok ? "ok" : "failed", (unsigned long long)r.r.seq, i + 1 < rs.size() ? "," : "");
+            m += b;
+        }
+        m += "]\n";
+        return write_text(dir + "/memory_regions.json", m);
+    };
+
+    // region file writer: region bytes + the matching manifest slice
+    auto snapshot_regions = [&](const std::vector<uint64_t>& manifest) {
+        for (auto& r : rs) {
+            if (!r.ok) continue;
+            const std::string hx = hex_base(r.r.base);
+            const std::string path = dir + "/memory/region_" + hx + ".bin";
+            FILE* fp = fopen(path.c_str(), "wb");
+            std::string err;
+            bool ok = fp && d2h_stream(ctx, r.r.base, r.r.size, fp, &rep, err);
+            if (fp) ok = (fclose(fp) == 0) && ok;
+            if (!ok) {
+                r.ok = false;
+                r.error = err.empty() ? "cannot write " + path : err;
+                unlink(path.c_str());
+                continue;
+            }
+            write_file(dir + "/memory/region_" + hx + ".xxh64", manifest.data() + r.chunk0, 8 * r.n_chunks);
+        }
+    };
+
+    double t_d2h = 0;
+    if (mode == KC_MODE_PRE_W) {
+        if (!write_metadata(false)) {
+            if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+            return set_err(ctx, KC_ERR_IO, "kc_capture: cannot write metadata in %s", dir.c_str());
+        }
+        t = now_s();
+        snapshot_regions(pre_h);
+        t_d2h += now_s() - t;
+    }
+
+    // ---- A3: forward the target dispatch, then wait for it
+    t = now_s();
+    {
+        CUresult r;
+        if (d->kernarg && d->kernarg_size) {
+            size_t ksz = d->kernarg_size;
+            void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, (void*)d->kernarg, CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
+                             CU_LAUNCH_PARAM_END};
+            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
+                               d->smem_bytes, (CUstream)cs, nullptr, extra);
+        } else {
+            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
+                               d->smem_bytes, (CUstream)cs, nullptr, nullptr);
+        }
+        if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)cs);
+        if (r != CUDA_SUCCESS) {
+            if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+            return cu_err(ctx, r, "kc_capture: target dispatch");
+        }
+    }
+    rep.t_dispatch_s = now_s() - t;
+    if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+
+    // test hook: a region freed between completion and snapshot
+    if (const char* hook = getenv("KC_TEST_FREE_AFTER_DISPATCH")) {
+        const uint64_t b = strtoull(hook, nullptr, 16);
+        if (b) free_alloc(ctx, b, true);
+    }
+
+    // ---- A4: post-manifest + written set
+    t = now_s();
+    std::vector<kc_region> live2;
+    for (auto& r : rs) {
+        if (r.ok && !region_live(ctx, r.r.base, r.r.size)) {
+            r.ok = false;
+            r.error = "freed between dispatch completion and snapshot";
+        }
+    }
+    std::vector<uint64_t> post_h, post_dig;
+    uint64_t post_snap = 0;
+    {
+        // hash every region still ok; remap manifest offsets
+        std::vector<uint64_t> off_post(rs.size(), 0);
+        for (size_t i = 0; i < rs.size(); ++i)
+            if (rs[i].ok) {
+                off_post[i] = kc_count_chunks(live2.data(), live2.size());
+                live2.push_back(rs[i].r);
+            }
+        st = hash_regions_sync(ctx, live2, post_h, &post_dig, &post_snap, nullptr, cs);
+        if (st != KC_OK) return st;
+        size_t j = 0;
+        for (size_t i = 0; i < rs.size(); ++i) {
+            if (!rs[i].ok) continue;
+            RegionState& r = rs[i];
+            r.post_digest = post_dig[j++];
+            for (uint64_t k = 0; k < r.n_chunks; ++k)
+                if (pre_h[r.chunk0 + k] != post_h[off_post[i] + k]) r.written.push_back(k);
+            rep.written_chunks += r.written.size();
+            r.chunk0 = off_post[i];  // from here on chunk0 indexes post_h
+        }
+    }
+    rep.t_hash_post_s = now_s() - t;
+
+    if (mode == KC_MODE_POST) {
+        if (!write_metadata(true)) return set_err(ctx, KC_ERR_IO, "kc_capture: cannot write metadata");
+        t = now_s();
+        snapshot_regions(post_h);
+        t_d2h += now_s() - t;
+    }
+
+    // ---- written chunks: indices (+ post bytes in PRE_W) and post manifests
+    void* d_stage = nullptr;
+    uint64_t* d_tab = nullptr;
+    t = now_s();
+    for (auto& r : rs) {
+        if (!r.ok) continue;
+        const std::string hx = hex_base(r.r.base);
+        write_file(dir + "/post/region_" + hx + ".xxh64", post_h.data() + r.chunk0, 8 * r.n_chunks);
+        write_file(dir + "/written/region_" + hx + ".idx", r.written.data(), 8 * r.written.size());
+        if (mode == KC_MODE_PRE_W && !r.written.empty()) {
+            if (!d_stage) {
+                const uint64_t sb = std::min<uint64_t>(ctx->io_chunk, 64ull << 20);
+                if (cudaMalloc(&d_stage, sb) != cudaSuccess || cudaMalloc((void**)&d_tab, 3 * 8 * (sb / 32)) != cudaSuccess)
+                    return set_err(ctx, KC_ERR_NOMEM, "kc_capture: staging");
+            }
+            std::vector<std::pair<uint64_t, uint64_t>> ranges;
+            for (uint64_t k : r.written) {
+                const uint64_t off = k * kChunk;
+                ranges.emplace_back(r.r.base + off, std::min<uint64_t>(kChunk, r.r.size - off));
+            }
+            const std::string path = dir + "/written/region_" + hx + ".bin";
+            FILE* fp = fopen(path.c_str(), "wb");
+            std::string err;
+            const uint64_t sb = std::min<uint64_t>(ctx->io_chunk, 64ull << 20);
+            bool ok = fp && gather_d2h(ctx, ranges, fp, d_stage, sb, d_tab, &rep, err);
+            if (fp) ok = (fclose(fp) == 0) && ok;
+            if (!ok) {
+                r.ok = false;
+                r.error = "written-chunk copy failed: " + err;
+            }
+        }
+    }
+    if (d_stage) cudaFree(d_stage);
+    if (d_tab) cudaFree(d_tab);
+    t_d2h += now_s() - t;
+    rep.t_d2h_s = t_d2h;
+
+    // ---- capture_log.json, then the sentinel LAST
+    rep.snapshot_digest = mode == KC_MODE_PRE_W ? pre_snap : post_snap;  // S of the region files written
+    std::string lg = "{\n  \"regions\": [\n";
+    char b[512];
+    for (size_t i = 0; i < rs.size(); ++i) {
+        const RegionState& r = rs[i];
+        if (!r.ok) rep.n_failed_regions++;
+        snprintf(b, sizeof b,
+                 "    {\"base\": \"%s\", \"status\": \"%s\", \"error\": \"%s\", \"post_digest\": \"%s\", "
+                 "\"written_chunks\": %zu}%s\n",
+                 hex_base(r.r.base).c_str(), r.ok ? "ok" : "failed", kcj::esc(r.error).c_str(),
+                 hex16(r.post_digest).c_str(), r.written.size(), i + 1 < rs.size() ? "," : "");
+        lg += b;
+    }
+    rep.t_total_s = now_s() - t0;
+    snprintf(b, sizeof b,
+             "  ],\n  \"snapshot_digest\": \"%s\",\n  \"written_chunks\": %llu,\n  \"d2h_bytes\": %llu,\n"
+             "  \"dma_calls\": %llu,\n  \"io_chunk_bytes\": %llu,\n  \"pinned_depth\": %u,\n"
+             "  \"staging_high_water\": %llu,\n  \"t_hash_pre_s\": %.6f,\n  \"t_d2h_s\": %.6f,\n"
+             "  \"t_dispatch_s\": %.6f,\n  \"t_hash_post_s\": %.6f,\n  \"t_total_s\": %.6f\n}\n",
+             hex16(rep.snapshot_digest).c_str(), (unsigned long long)rep.written_chunks,
+             (unsigned long long)rep.d2h_bytes, (unsigned long long)rep.dma_calls, (unsigned long long)ctx->io_chunk,
+             ctx->depth, (unsigned long long)rep.staging_high_water, rep.t_hash_pre_s, rep.t_d2h_s, rep.t_dispatch_s,
+             rep.t_hash_post_s, rep.t_total_s);
+    lg += b;
+    if (!write_text(dir + "/capture_log.json", lg)) return set_err(ctx, KC_ERR_IO, "cannot write capture_log.json");
+    if (!write_file(dir + "/capture_complete", "", 0)) return set_err(ctx, KC_ERR_IO, "cannot write sentinel");
+    if (rep_out) *rep_out = rep;
+    if (rep.n_failed_regions) {
+        final_st = KC_PARTIAL;
+        set_err(ctx, KC_PARTIAL, "kc_capture: %llu region(s) failed; see capture_log.json",
+                (unsigned long long)rep.n_failed_regions);
+    }
+    return final_st;
+}
+
+// ====================================================================== restore
+namespace {
+struct Placeholder {
+    uint64_t base, size;
+};
+std::mutex g_ph_mu;
+std::vector<Placeholder> g_placeholders;
+
+const uint64_t kPlaceholderGranule = 2ull << 20;  // typical VMM granularity before cuInit
+
+struct ParsedRegion {
+    uint64_t base, size;
+    int kind;
+    bool ok;
+    std::string hx;
+    uint64_t seq = 0;
+};
+
+kc_status parse_regions(kc_ctx* ctx, const std::string& dir, std::vector<ParsedRegion>& out) {
+    std::string text;
+    if (!kcj::read_file(dir + "/memory_regions.json", text))
+        return set_err(ctx, KC_ERR_FORMAT, "cannot read %s/memory_regions.json", dir.c_str());
+    kcj::Value v;
+    if (!kcj::Parser(text).parse(v) || v.t != kcj::Value::Arr)
+        return set_err(ctx, KC_ERR_FORMAT, "memory_regions.json does not parse");
+    for (auto& e : v.a) {
+        const kcj::Value* b = e.get("base");
+        const kcj::Value* s = e.get("size");
+        if (!b || !s || b->t != kcj::Value::Str) return set_err(ctx, KC_ERR_FORMAT, "region entry lacks base/size");
+        ParsedRegion r;
+        r.base = strtoull(b->s.c_str(), nullptr, 16);
+        r.size = s->as_u64();
+        r.hx = b->s;
+        const kcj::Value* k = e.get("alloc_kind");
+        r.kind = k && k->s == "vmm" ? KC_KIND_VMM : (k && k->s == "pool" ? KC_KIND_POOL : KC_KIND_MEMALLOC);
+        const kcj::Value* stv = e.get("status");
+        r.ok = !stv || stv->s == "ok";
+        if (const kcj::Value* q = e.get("seq")) r.seq = q->as_u64();
+        out.push_back(r);
+    }
+    // final statuses from capture_log.json (a region may fail after the metadata was written)
+    std::string lt;
+    if (kcj::read_file(dir + "/capture_log.json", lt)) {
+        kcj::Value lv;
+        if (kcj::Parser(lt).parse(lv)) {
+            if (const kcj::Value* rr = lv.get("regions"))
+                for (auto& e : rr->a) {
+                    const kcj::Value* b = e.get("base");
+                    const kcj::Value* stv = e.get("status");
+                    if (!b || !stv) continue;
+                    for (auto& r : out)
+                        if (r.hx == b->s && stv->s != "ok") r.ok = false;
+                }
+        }
+    }
+    std::sort(out.begin(), out.end(), [](const ParsedRegion& a, const ParsedRegion& b) { return a.base < b.base; });
+    return KC_OK;
+}
+
+std::vector<std::pair<uint64_t, uint64_t>> make_spans(const std::vector<ParsedRegion>& regs, uint64_t G) {
+    std::vector<std::pair<uint64_t, uint64_t>> spans;  // [lo, hi)
+    for (auto& r : regs) {
+        const uint64_t lo = r.base / G * G, hi = (r.base + r.size + G - 1) / G * G;
+        if (!spans.empty() && lo <= spans.back().second) spans.back().second = std::max(spans.back().second, hi);
+        else spans.emplace_back(lo, hi);
+    }
+    return spans;
+}
+
+void release_placeholders() {
+    std::lock_guard<std::mutex> lk(g_ph_mu);
+    for (auto& p : g_placeholders) munmap((void*)p.base, p.size);
+    g_placeholders.clear();
+}
+
+void rollback(kc_restored* h) {
+    for (auto it = h->spans.rbegin(); it != h->spans.rend(); ++it) {
+        for (uint64_t p : it->memalloc) KC_DRV(cuMemFree)((CUdeviceptr)p);
+        it->memalloc.clear();
+        if (it->mapped) KC_DRV(cuMemUnmap)((CUdeviceptr)it->base, it->size);
+        if (it->created) KC_DRV(cuMemRelease)(it->h);
+    }
+    h->spans.clear();
+    for (auto& w : h->windows) KC_DRV(cuMemAddressFree)((CUdeviceptr)w.first, w.second);
+    h->windows.clear();
+}
+}  // namespace
+
+extern "C" kc_status kc_prereserve(const char* dir, uint64_t* n_reserved) {
+    if (!dir) return KC_ERR_ARG;
+    std::vector<ParsedRegion> regs;
+    kc_status st = parse_regions(nullptr, dir, regs);
+    if (st != KC_OK) return st;
+    auto spans = make_spans(regs, kPlaceholderGranule);
+    uint64_t n = 0;
+    std::lock_guard<std::mutex> lk(g_ph_mu);
+    for (auto& s : spans) {
+        void* p = mmap((void*)s.first, s.second - s.first, PROT_NONE,
+                       MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE | MAP_FIXED_NOREPLACE, -1, 0);
+        if (p == MAP_FAILED) continue;
+        if ((uint64_t)p != s.first) {  // old kernels ignore MAP_FIXED_NOREPLACE
+            munmap(p, s.second - s.first);
+            continue;
+        }
+        g_placeholders.push_back({s.first, s.second - s.first});
+        ++n;
+    }
+    if (n_reserved) *n_reserved = n;
+    return KC_OK;
+}
+
+extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** out, kc_restore_report* rep_out) {
+    if (!ctx || !dir_c || !out) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    *out = nullptr;
+    kc_restore_report rep;
+    memset(&rep, 0, sizeof rep);
+    const double t0 = now_s();
+    const std::string dir = dir_c;
+    {
+        struct stat sb;
+        if (stat((dir + "/capture_complete").c_str(), &sb) != 0)
+            return set_err(ctx, KC_ERR_FORMAT, "%s: no capture_complete sentinel (incomplete capture)", dir_c);
+    }
+    // ---- stage 1: parse metadata
+    std::string dtext;
+    if (!kcj::read_file(dir + "/dispatch.json", dtext)) return set_err(ctx, KC_ERR_FORMAT, "cannot read dispatch.json");
+    kcj::Value dv;
+    if (!kcj::Parser(dtext).parse(dv)) return set_err(ctx, KC_ERR_FORMAT, "dispatch.json does not parse");
+    std::vector<ParsedRegion> regs;
+    kc_status st = parse_regions(ctx, dir, regs);
+    if (st != KC_OK) return st;
+
+    kc_restored* h = new kc_restored();
+    h->ctx = ctx;
+    h->dir = dir;
+    h->mode = dv.get("mode") && dv.get("mode")->s == "post" ? KC_MODE_POST : KC_MODE_PRE_W;
+    h->mangled = dv.get("mangled_symbol") ? dv.get("mangled_symbol")->s : "";
+    if (const kcj::Value* g = dv.get("grid"))
+        for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) h->grid[i] = (uint32_t)g->a[i].as_u64(1);
+    if (const kcj::Value* g = dv.get("block"))
+        for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) h->block[i] = (uint32_t)g->a[i].as_u64(1);
+    if (const kcj::Value* g = dv.get("shared_mem_bytes")) h->smem = (uint32_t)g->as_u64();
+    if (!read_bin(dir + "/kernarg.bin", h->kernarg)) {
+        delete h;
+        return set_err(ctx, KC_ERR_FORMAT, "cannot read kernarg.bin");
+    }
+    const uint64_t ksz = dv.get("kernarg_size") ? dv.get("kernarg_size")->as_u64() : h->kernarg.size();
+    if (ksz != h->kernarg.size()) {
+        delete h;
+        return set_err(ctx, KC_ERR_FORMAT, "kernarg.bin has %zu bytes, dispatch.json says %llu", h->kernarg.size(),
+                       (unsigned long long)ksz);
+    }
+    for (auto& r : regs) {
+        kc_restored_region rr;
+        rr.r.base = r.base;
+        rr.r.size = r.size;
+        rr.r.device = ctx->device;
+        rr.r.kind = r.kind;
+        rr.r.seq = 0;
+        rr.hexbase = r.hx;
+        rr.ok = r.ok;
+        rr.n_chunks = (r.size + kChunk - 1) / kChunk;
+        if (r.ok) {
+            read_u64s(dir + "/written/region_" + r.hx + ".idx", rr.written);
+            const std::string pm = dir + (h->mode == KC_MODE_PRE_W ? "/post/region_" : "/memory/region_") + r.hx + ".xxh64";
+            read_u64s(pm, rr.post_manifest);
+        } else {
+            rep.n_failed_regions++;
+        }
+        h->regions.push_back(rr);
+    }
+    rep.n_regions = regs.size();
+
+    // ---- stages 2-4: placeholders released, exact-VA reservation
+    if (!bind_device(ctx)) {
+        delete h;
+        return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    }
+    double t = now_s();
+    CUmemAllocationProp prop;
+    memset(&prop, 0, sizeof prop);
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = ctx->device;
+    size_t G = 0;
+    CUresult cr = KC_DRV(cuMemGetAllocationGranularity)(&G, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM);
+    if (cr != CUDA_SUCCESS || G == 0) {
+        delete h;
+        return cu_err(ctx, cr, "cuMemGetAllocationGranularity");
+    }
+    auto spans = make_spans(regs, G);
+    release_placeholders();
+    // Reserve VA windows at exactly aligned hints.  A fresh process honours a
+    // hint only where the driver can open a new VA chunk, i.e. at a coarse
+    // alignment (observed: 32 MiB), so try the exact span first and then
+    // covering windows aligned to 32 MiB ... 1 GiB; map only the spans.
+    static const uint64_t kWindows[] = {0, 32ull << 20, 64ull << 20, 128ull << 20, 256ull << 20, 512ull << 20,
+                                        1ull << 30};
+    for (auto& sp : spans) {
+        kc_restored::Span s{sp.first, sp.second - sp.first, 0, false, false, false, false, {}, 0, 0};
+        bool covered = false;
+        for (auto& w : h->windows)
+            if (w.first <= s.base && s.base + s.size <= w.first + w.second) covered = true;
+        if (!covered) {
+            const uint64_t prev_end = h->windows.empty() ? 0 : h->windows.back().first + h->windows.back().second;
+            for (uint64_t W : kWindows) {
+                const uint64_t A = W ? W : G;
+                uint64_t lo = s.base / A * A;
+                const uint64_t hi = (s.base + s.size + A - 1) / A * A;
+                if (lo < prev_end) {
+                    if (W) continue;  // would overlap a window we already hold
+                    lo = s.base;
+                }
+                CUdeviceptr p = 0;
+                cr = KC_DRV(cuMemAddressReserve)(&p, hi - lo, A, (CUdeviceptr)lo, 0);
+                if (cr == CUDA_SUCCESS && (uint64_t)p == lo) {
+                    h->windows.emplace_back(lo, hi - lo);
+                    covered = true;
+                    break;
+                }
+                if (cr == CUDA_SUCCESS) KC_DRV(cuMemAddressFree)(p, hi - lo);
+                s.reserve_got = (uint64_t)p;
+                s.reserve_cr = (int)cr;
+            }
+        }
+        if (covered) {
+            s.reserved = true;
+        } else {
+            // The span lies in VA the driver pools for small cuMemAlloc
+            // allocations: fall back to replaying cuMemAlloc below.
+            s.fallback = true;
+        }
+        h->spans.push_back(s);
+    }
+    for (auto& s : h->spans) {
+        if (s.fallback) continue;
+        cr = KC_DRV(cuMemCreate)(&s.h, s.size, &prop, 0);
+        if (cr == CUDA_SUCCESS) {
+            s.created = true;
+            cr = KC_DRV(cuMemMap)((CUdeviceptr)s.base, s.size, 0, s.h, 0);
+        }
+        if (cr == CUDA_SUCCESS) {
+            s.mapped = true;
+            CUmemAccessDesc acc;
+            acc.location = prop.location;
+            acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+            cr = KC_DRV(cuMemSetAccess)((CUdeviceptr)s.base, s.size, &acc, 1);
+        }
+        if (cr != CUDA_SUCCESS) {
+            rollback(h);
+            delete h;
+            return cu_err(ctx, cr, "kc_restore: cuMemCreate/cuMemMap/cuMemSetAccess");
+        }
+        rep.mapped_bytes += s.size;
+    }
+    {
+        // cuMemAlloc replay, in the capture's allocation order, for fallback spans
+        std::vector<std::pair<uint64_t, size_t>> fb;  // (seq, region index)
+        for (size_t i = 0; i < h->regions.size(); ++i) {
+            const auto& rr = h->regions[i];
+            for (auto& s : h->spans)
+                if (s.fallback && s.base <= rr.r.base && rr.r.base < s.base + s.size) fb.emplace_back(regs[i].seq, i);
+        }
+        std::sort(fb.begin(), fb.end());
+        for (auto& e : fb) {
+            const auto& rr = h->regions[e.second];
+            CUdeviceptr p = 0;
+            cr = KC_DRV(cuMemAlloc)(&p, rr.r.size);
+            kc_restored::Span* owner = nullptr;
+            for (auto& s : h->spans)
+                if (s.fallback && s.base <= rr.r.base && rr.r.base < s.base + s.size) owner = &s;
+            if (cr == CUDA_SUCCESS) owner->memalloc.push_back((uint64_t)p);
+            if (cr != CUDA_SUCCESS || (uint64_t)p != rr.r.base) {
+                const uint64_t got = (uint64_t)p, want = rr.r.base, sz = rr.r.size;
+                uint64_t sbase = 0, sgot = 0;
+                int scr = 0;
+                for (auto& s : h->spans)
+                    if (s.fallback && s.base <= want && want < s.base + s.size) {
+                        sbase = s.base;
+                        sgot = s.reserve_got;
+                        scr = s.reserve_cr;
+                    }
+                rollback(h);
+                delete h;
+                return set_err(ctx, KC_ERR_VA_UNAVAILABLE,
+                               "kc_restore: cannot restore captured region [0x%llx, +%llu): reserving span 0x%llx "
+                               "returned 0x%llx (CUresult %d) and the cuMemAlloc replay returned 0x%llx (%d); VA "
+                               "faithfulness is a hard requirement (PAPER.md:1080-1082)",
+                               (unsigned long long)want, (unsigned long long)sz, (unsigned long long)sbase,
+                               (unsigned long long)sgot, scr, (unsigned long long)got, (int)cr);
+            }
+            rep.mapped_bytes += rr.r.size;
+        }
+    }
+    rep.n_spans = h->spans.size();
+    rep.t_reserve_s = now_s() - t;
+
+    // ---- stage 5a: copy-in (pinned ring; gaps and failed regions zero-filled)
+    t = now_s();
+    st = ensure_pinned(ctx);
+    if (st != KC_OK) {
+        rollback(h);
+        delete h;
+        return st;
+    }
+    for (auto& s : h->spans) {
+        if (!s.fallback) cudaMemsetAsync((void*)s.base, 0, s.size, ctx->copy_stream);
+    }
+    for (auto& rr : h->regions) cudaMemsetAsync((void*)rr.r.base, 0, rr.r.size, ctx->copy_stream);
+    for (auto& rr : h->regions) {
+        if (!rr.ok) continue;
+        const std::string path = dir + "/memory/region_" + rr.hexbase + ".bin";
+        FILE* fp = fopen(path.c_str(), "rb");
+        std::string err;
+        struct stat sb;
+        bool ok = fp && fstat(fileno(fp), &sb) == 0 && (uint64_t)sb.st_size == rr.r.size &&
+                  h2d_stream(ctx, fp, rr.r.base, rr.r.size, &rep.h2d_bytes, err);
+        if (fp) fclose(fp);
+        if (!ok) {
+            rollback(h);
+            delete h;
+            return set_err(ctx, KC_ERR_FORMAT, "kc_restore: %s: missing, wrong length or unreadable (%s)", path.c_str(),
+                           err.c_str());
+        }
+    }
+    cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+    if (ce != cudaSuccess) {
+        rollback(h);
+        delete h;
+        return cuda_err(ctx, ce, "kc_restore: copy-in");
+    }
+    rep.t_h2d_s = now_s() - t;
+
+    // ---- verify against the captured manifest (K1, O6)
+    t = now_s();
+    std::vector<kc_region> okregs;
+    for (auto& rr : h->regions)
+        if (rr.ok) okregs.push_back(rr.r);
+    std::vector<uint64_t> got;
+    st = hash_regions_sync(ctx, okregs, got, nullptr, nullptr, nullptr, ctx->copy_stream);
+    if (st != KC_OK) {
+        rollback(h);
+        delete h;
+        return st;
+    }
+    {
+        uint64_t c = 0, mism = 0;
+        for (auto& rr : h->regions) {
+            if (!rr.ok) continue;
+            std::vector<uint64_t> man;
+            if (!read_u64s(dir + "/memory/region_" + rr.hexbase + ".xxh64", man) || man.size() != rr.n_chunks) {
+                mism += rr.n_chunks;
+            } else {
+                for (uint64_t k = 0; k < rr.n_chunks; ++k) mism += man[k] != got[c + k];
+            }
+            c += rr.n_chunks;
+        }
+        rep.verify_mismatch_chunks = mism;
+    }
+    rep.t_verify_s = now_s() - t;
+    if (rep.verify_mismatch_chunks) {
+        if (rep_out) *rep_out = rep;
+        rollback(h);
+        delete h;
+        return set_err(ctx, KC_ERR_MANIFEST_MISMATCH, "kc_restore: %llu restored chunk(s) do not match the captured "
+                       "manifest", (unsigned long long)rep.verify_mismatch_chunks);
+    }
+
+    // ---- device stashes of the written chunks: replay recopy (pre) and validation reference (post)
+    uint64_t total = 0;
+    for (auto& rr : h->regions) {
+        rr.stash_off.clear();
+        for (uint64_t k : rr.written) {
+            rr.stash_off.push_back(total);
+            total += std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
+        }
+    }
+    h->stash_bytes = total;
+    if (total) {
+        if (cudaMalloc(&h->stash_pre, total) != cudaSuccess || cudaMalloc(&h->stash_ref, total) != cudaSuccess) {
+            rollback(h);
+            delete h;
+            return set_err(ctx, KC_ERR_NOMEM, "kc_restore: stash of %llu bytes", (unsigned long long)total);
+        }
+        for (auto& rr : h->regions) {
+            if (!rr.ok || rr.written.empty()) continue;
+            std::vector<uint8_t> wb;
+            if (h->mode == KC_MODE_PRE_W && !read_bin(dir + "/written/region_" + rr.hexbase + ".bin", wb)) {
+                rollback(h);
+                delete h;
+                return set_err(ctx, KC_ERR_FORMAT, "missing written/region_%s.bin", rr.hexbase.c_str());
+            }
+            uint64_t woff = 0;
+            for (size_t j = 0; j < rr.written.size(); ++j) {
+                const uint64_t k = rr.written[j];
+                const uint64_t len = std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
+                uint8_t* pre = (uint8_t*)h->stash_pre + rr.stash_off[j];
+                uint8_t* ref = (uint8_t*)h->stash_ref + rr.stash_off[j];
+                cudaMemcpyAsync(pre, (const void*)(rr.r.base + k * kChunk), len, cudaMemcpyDeviceToDevice,
+                                ctx->copy_stream);
+                if (h->mode == KC_MODE_PRE_W) {
+                    if (woff + len > wb.size()) {
+                        rollback(h);
+                        delete h;
+                        return set_err(ctx, KC_ERR_FORMAT, "written/region_%s.bin is short", rr.hexbase.c_str());
+                    }
+                    cudaMemcpy(ref, wb.data() + woff, len, cudaMemcpyHostToDevice);
+                } else {
+                    cudaMemcpyAsync(ref, (const void*)(rr.r.base + k * kChunk), len, cudaMemcpyDeviceToDevice,
+                                    ctx->copy_stream);
+                }
+                woff += len;
+            }
+        }
+        ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (ce != cudaSuccess) {
+            rollback(h);
+            delete h;
+            return cuda_err(ctx, ce, "kc_restore: stash");
+        }
+    }
+    rep.t_total_s = now_s() - t0;
+    if (rep_out) *rep_out = rep;
+    *out = h;
+    return KC_OK;
+}
+
+extern "C" kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out) {
+    if (!h) return KC_ERR_ARG;
+    size_t i = 0;
+    for (auto& rr : h->regions) {
+        if (out && i < cap) out[i] = rr.r;
+        ++i;
+    }
+    if (n_out) *n_out = i;
+    return KC_OK;
+}
+
+extern "C" void kc_release(kc_restored* h) {
+    if (!h) return;
+    if (h->ctx) bind_device(h->ctx);
+    cudaDeviceSynchronize();
+    if (h->module) KC_DRV(cuModuleUnload)(h->module);
+    if (h->stash_pre) cudaFree(h->stash_pre);
+    if (h->stash_ref) cudaFree(h->stash_ref);
+    rollback(h);
+    delete h;
+}
+
+// ====================================================================== replay
+extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts* o, kc_replay_report* rep_out) {
+    if (!ctx || !h) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    kc_replay_opts dflt;
+    memset(&dflt, 0, sizeof dflt);
+    dflt.iterations = 1;
+    if (!o) o = &dflt;
+    const uint32_t iters = o->iterations ? o->iterations : 1;
+    cudaStream_t s = (cudaStream_t)o->stream;
+    CUmodule mod = nullptr;
+    bool own = false;
+    if (o->image_override) {
+        KC_CHECK_CU(ctx, KC_DRV(cuModuleLoadData)(&mod, o->image_override), "cuModuleLoadData(override)");
+        own = true;
+    } else {
+        if (!h->module) {
+            std::vector<uint8_t> img;
+            if (!read_bin(h->dir + "/kernel.cubin", img) || img.empty())
+                return set_err(ctx, KC_ERR_FORMAT, "kc_replay: no kernel.cubin in %s", h->dir.c_str());
+            KC_CHECK_CU(ctx, KC_DRV(cuModuleLoadData)(&h->module, img.data()), "cuModuleLoadData(kernel.cubin)");
+        }
+        mod = h->module;
+    }
+    CUfunction f = nullptr;
+    if (KC_DRV(cuModuleGetFunction)(&f, mod, h->mangled.c_str()) != CUDA_SUCCESS) {
+        if (own) KC_DRV(cuModuleUnload)(mod);
+        return set_err(ctx, KC_ERR_ARG, "kc_replay: symbol %s not found in the code object", h->mangled.c_str());
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double sum = 0, mn = 1e300, mx = 0;
+    kc_status res = KC_OK;
+    for (uint32_t it = 0; it < iters; ++it) {
+        if (it > 0 && !o->no_recopy) {  // restore the pre-state of W
+            for (auto& rr : h->regions)
+                for (size_t j = 0; j < rr.written.size(); ++j) {
+                    const uint64_t k = rr.written[j];
+                    const uint64_t len = std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
+                    cudaMemcpyAsync((void*)(rr.r.base + k * kChunk), (uint8_t*)h->stash_pre + rr.stash_off[j], len,
+                                    cudaMemcpyDeviceToDevice, s);
+                }
+        }
+        cudaEventRecord(e0, s);
+        CUresult r;
+        if (!h->kernarg.empty()) {
+            size_t ksz = h->kernarg.size();
+            void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, h->kernarg.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
+                             CU_LAUNCH_PARAM_END};
+            r = KC_DRV(cuLaunchKernel)(f, h->grid[0], h->grid[1], h->grid[2], h->block[0], h->block[1], h->block[2], h->smem,
+                               (CUstream)s, nullptr, extra);
+        } else {
+            r = KC_DRV(cuLaunchKernel)(f, h->grid[0], h->grid[1], h->grid[2], h->block[0], h->block[1], h->block[2], h->smem,
+                               (CUstream)s, nullptr, nullptr);
+        }
+        cudaEventRecord(e1, s);
+        if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)s);
+        if (r != CUDA_SUCCESS) {
+            res = cu_err(ctx, r, "kc_replay: dispatch");
+            break;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        sum += ms;
+        mn = std::min(mn, (double)ms);
+        mx = std::max(mx, (double)ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (own) KC_DRV(cuModuleUnload)(mod);
+    if (res != KC_OK) return res;
+    if (rep_out) {
+        rep_out->iterations = iters;
+        rep_out->kernel_ms_mean = sum / iters;
+        rep_out->kernel_ms_min = mn;
+        rep_out->kernel_ms_max = mx;
+    }
+    if (o->dump_dir) {  // stage 6
+        const std::string od = std::string(o->dump_dir) + "/output";
+        if (!mkdir_p(od)) return set_err(ctx, KC_ERR_IO, "cannot create %s", od.c_str());
+        kc_status st = ensure_pinned(ctx);
+        if (st != KC_OK) return st;
+        for (auto& rr : h->regions) {
+            const std::string path = od + "/region_" + rr.hexbase + ".bin";
+            FILE* fp = fopen(path.c_str(), "wb");
+            std::string err;
+            bool ok = fp && d2h_stream(ctx, rr.r.base, rr.r.size, fp, nullptr, err);
+            if (fp) ok = (fclose(fp) == 0) && ok;
+            if (!ok) return set_err(ctx, KC_ERR_IO, "dump %s: %s", path.c_str(), err.c_str());
+        }
+    }
+    return KC_OK;
+}
+
+// ====================================================================== validate
+extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n,
+                                 const kc_tolerance* tol, kc_diff_report* reps, size_t cap_reports,
+                                 size_t* n_reports_out, uint64_t* unexpected_chunks) {
+    if (!ctx || !h) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    cudaStream_t s = ctx->copy_stream;
+    std::vector<kc_buffer> segs;
+    std::vector<uint64_t> rep_nbytes, word0;
+    uint64_t words = 0;
+    void* typed_ref = nullptr;
+    if (!outs) {
+        // every region with written chunks, bytes, reference = captured post bytes of W
+        for (auto& rr : h->regions) {
+            if (!rr.ok || rr.written.empty()) continue;
+            const int rid = (int)rep_nbytes.size();
+            rep_nbytes.push_back(rr.r.size);
+            word0.push_back(words);
+            words += (rr.n_chunks + 63) / 64;
+            for (size_t j = 0; j < rr.written.size(); ++j) {
+                const uint64_t k = rr.written[j];
+                kc_buffer b;
+                b.ref = (uint64_t)h->stash_ref + rr.stash_off[j];
+                b.act = rr.r.base + k * kChunk;
+                b.nbytes = std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
+                b.dtype = KC_DT_BYTES;
+                b.report = rid;
+                b.bitmap_chunk0 = k;
+                segs.push_back(b);
+            }
+        }
+    } else {
+        // typed sub-ranges: rebuild the captured post-dispatch bytes of each range
+        uint64_t total = 0;
+        for (size_t i = 0; i < n; ++i) total += (outs[i].nbytes + 255) / 256 * 256;
+        if (total && cudaMalloc(&typed_ref, total) != cudaSuccess)
+            return set_err(ctx, KC_ERR_NOMEM, "kc_validate: reference buffer");
+        uint64_t off = 0;
+        for (size_t i = 0; i < n; ++i) {
+            const kc_buffer& o = outs[i];
+            const kc_restored_region* owner = nullptr;
+            for (auto& rr : h->regions)
+                if (rr.r.base <= o.act && o.act + o.nbytes <= rr.r.base + rr.r.size) owner = &rr;
+            if (!owner || !owner->ok) {
+                if (typed_ref) cudaFree(typed_ref);
+                return set_err(ctx, KC_ERR_OUT_OF_BOUNDS, "kc_validate: output %zu is not inside a restored region", i);
+            }
+            std::vector<uint8_t> host(o.nbytes);
+            const uint64_t roff = o.act - owner->r.base;
+            FILE* fp = fopen((h->dir + "/memory/region_" + owner->hexbase + ".bin").c_str(), "rb");
+            bool okr = fp && fseek(fp, (long)roff, SEEK_SET) == 0 && fread(host.data(), 1, o.nbytes, fp) == o.nbytes;
+            if (fp) fclose(fp);
+            if (!okr) {
+                if (typed_ref) cudaFree(typed_ref);
+                return set_err(ctx, KC_ERR_FORMAT, "kc_validate: cannot read reference bytes");
+            }
+            if (h->mode == KC_MODE_PRE_W && !owner->written.empty()) {  // overlay W's post bytes
+                std::vector<uint8_t> wb;
+                read_bin(h->dir + "/written/region_" + owner->hexbase + ".bin", wb);
+                uint64_t woff = 0;
+                for (uint64_t k : owner->written) {
+                    const uint64_t c0 = k * kChunk, len = std::min<uint64_t>(kChunk, owner->r.size - c0);
+                    const uint64_t lo = std::max(c0, roff), hi = std::min(c0 + len, roff + o.nbytes);
+                    if (lo < hi && woff + len <= wb.size()) memcpy(host.data() + (lo - roff), wb.data() + woff + (lo - c0), hi - lo);
+                    woff += len;
+                }
+            }
+            cudaMemcpy((uint8_t*)typed_ref + off, host.data(), o.nbytes, cudaMemcpyHostToDevice);
+            kc_buffer b = o;
+            b.ref = (uint64_t)typed_ref + off;
+            b.report = (int32_t)i;
+            b.bitmap_chunk0 = 0;
+            segs.push_back(b);
+            rep_nbytes.push_back(o.nbytes);
+            word0.push_back(words);
+            words += ((o.nbytes + kChunk - 1) / kChunk + 63) / 64;
+            off += (o.nbytes + 255) / 256 * 256;
+        }
+    }
+    const size_t nrep = rep_nbytes.size();
+    if (n_reports_out) *n_reports_out = nrep;
+    kc_status st = KC_OK;
+    if (nrep) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->reps, nrep * sizeof(kc_diff_report)), "cudaMalloc(reports)");
+        KC_CHECK_CUDA(ctx, ensure(ctx->bitmaps, std::max<uint64_t>(1, words) * 8), "cudaMalloc(bitmaps)");
+        st = kc_diff_async(ctx, segs.data(), segs.size(), nrep, rep_nbytes.data(), word0.data(), tol,
+                           (kc_diff_report*)ctx->reps.p, (uint64_t*)ctx->bitmaps.p, s);
+        if (st == KC_OK && reps) {
+            std::vector<kc_diff_report> tmp(nrep);
+            cudaMemcpyAsync(tmp.data(), ctx->reps.p, nrep * sizeof(kc_diff_report), cudaMemcpyDeviceToHost, s);
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) st = cuda_err(ctx, e, "kc_validate: reports");
+            for (size_t j = 0; j < nrep && j < cap_reports; ++j) reps[j] = tmp[j];
+        }
+    }
+    if (typed_ref) {
+        cudaStreamSynchronize(s);
+        cudaFree(typed_ref);
+    }
+    if (st != KC_OK) return st;
+    if (unexpected_chunks) {  // re-hash every restored region vs the captured post manifest
+        std::vector<kc_region> okregs;
+        for (auto& rr : h->regions)
+            if (rr.ok) okregs.push_back(rr.r);
+        std::vector<uint64_t> got;
+        st = hash_regions_sync(ctx, okregs, got, nullptr, nullptr, nullptr, s);
+        if (st != KC_OK) return st;
+        uint64_t c = 0, bad = 0;
+        for (auto& rr : h->regions) {
+            if (!rr.ok) continue;
+            for (uint64_t k = 0; k < rr.n_chunks; ++k)
+                bad += (rr.post_manifest.size() != rr.n_chunks) || rr.post_manifest[k] != got[c + k];
+            c += rr.n_chunks;
+        }
+        *unexpected_chunks = bad;
+    }
+    return KC_OK;
+}

@@ -1,0 +1,416 @@
+"""Thin ctypes binding of libkc.so (include/kc.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels and C++ runtime;
+this module only converts Python values to the C ABI and back.  There is no
+fallback: if libkc.so is missing or does not load, :func:`lib` raises.
+
+Device memory is passed as integer device virtual addresses (e.g.
+``torch.Tensor.data_ptr()`` or :meth:`Context.alloc`), streams as integer
+CUstream handles (``torch.cuda.current_stream().cuda_stream``; 0 = default).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libkc.so")
+
+KC_CHUNK_BYTES = 65536
+
+# kc_status
+KC_OK, KC_PARTIAL = 0, 1
+KC_ERR_ARG, KC_ERR_STATE, KC_ERR_CUDA, KC_ERR_IO, KC_ERR_FORMAT = -1, -2, -3, -4, -5
+KC_ERR_VA_UNAVAILABLE, KC_ERR_NOT_TRACKED, KC_ERR_OUT_OF_BOUNDS, KC_ERR_NOMEM = -6, -7, -8, -9
+KC_ERR_MANIFEST_MISMATCH, KC_ERR_UNSUPPORTED = -10, -11
+# kc_event / kc_alloc_kind / kc_capture_mode
+KC_EV_ALLOC, KC_EV_FREE, KC_EV_MAP, KC_EV_UNMAP = 0, 1, 2, 3
+KC_KIND_MEMALLOC, KC_KIND_VMM, KC_KIND_POOL = 0, 1, 2
+KC_MODE_PRE_W, KC_MODE_POST = 0, 1
+KC_ALLOC_VMM, KC_ALLOC_MEMALLOC = 0, 1
+# kc_dtype
+DTYPES = ["bytes", "u8", "i8", "u16", "i16", "u32", "i32", "u64", "i64", "f16", "bf16", "f32", "f64"]
+DT = {n: i for i, n in enumerate(DTYPES)}
+ELEM_SIZE = [1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8]
+
+EXPORTED = [
+    "kc_create", "kc_destroy", "kc_last_error", "kc_abi_version", "kc_build_info", "kc_status_str",
+    "kc_kernel_launches", "kc_track",
+    "kc_regions", "kc_alloc", "kc_free", "kc_track_install", "kc_track_uninstall", "kc_hash", "kc_count_chunks",
+    "kc_written", "kc_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
+    "kc_validate", "kc_restored_regions", "kc_release",
+]
+
+
+class KcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{status_name(status)}: {msg}")
+        self.status = status
+
+
+# ----------------------------------------------------------------- ABI structs
+class Region(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_uint64), ("size", ctypes.c_uint64), ("device", ctypes.c_int32),
+                ("kind", ctypes.c_int32), ("seq", ctypes.c_uint64)]
+
+    def __repr__(self):
+        return f"Region(base=0x{self.base:x}, size={self.size}, device={self.device}, kind={self.kind})"
+
+
+class Buffer(ctypes.Structure):
+    _fields_ = [("ref", ctypes.c_uint64), ("act", ctypes.c_uint64), ("nbytes", ctypes.c_uint64),
+                ("dtype", ctypes.c_int32), ("report", ctypes.c_int32), ("bitmap_chunk0", ctypes.c_uint64)]
+
+
+class Tolerance(ctypes.Structure):
+    _fields_ = [("atol", ctypes.c_double), ("rtol", ctypes.c_double), ("equal_nan", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
+
+
+class DiffReport(ctypes.Structure):
+    _fields_ = [
+        ("nbytes", ctypes.c_uint64), ("n_elems", ctypes.c_uint64), ("n_chunks", ctypes.c_uint64),
+        ("differing_bytes", ctypes.c_uint64), ("differing_elems", ctypes.c_uint64), ("max_ulp", ctypes.c_uint64),
+        ("max_abs", ctypes.c_double), ("max_rel", ctypes.c_double), ("percent_bytes", ctypes.c_double),
+        ("nan_ref", ctypes.c_uint64), ("nan_act", ctypes.c_uint64), ("nan_pos_mismatch", ctypes.c_uint64),
+        ("rel_undefined", ctypes.c_uint64), ("allclose_fail", ctypes.c_uint64),
+        ("pass_", ctypes.c_int32), ("_pad", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {n: getattr(self, n) for n, _ in self._fields_ if n != "_pad"}
+        d["pass"] = d.pop("pass_")
+        return d
+
+
+class Dispatch(ctypes.Structure):
+    _fields_ = [("func", ctypes.c_void_p), ("image", ctypes.c_void_p), ("image_size", ctypes.c_size_t),
+                ("mangled", ctypes.c_char_p), ("grid", ctypes.c_uint32 * 3), ("block", ctypes.c_uint32 * 3),
+                ("smem_bytes", ctypes.c_uint32), ("kernarg_size", ctypes.c_uint32), ("kernarg", ctypes.c_void_p),
+                ("stream", ctypes.c_void_p)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("io_chunk_bytes", ctypes.c_uint64), ("pinned_depth", ctypes.c_uint32), ("device", ctypes.c_int32),
+                ("alloc_mode", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+class CaptureReport(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "n_regions", "n_chunks", "total_bytes", "n_failed_regions", "written_chunks", "d2h_bytes", "dma_calls",
+        "staging_high_water", "snapshot_digest")] + [(n, ctypes.c_double) for n in (
+            "t_hash_pre_s", "t_d2h_s", "t_dispatch_s", "t_hash_post_s", "t_total_s")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class ReplayOpts(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_uint32), ("no_recopy", ctypes.c_int32), ("dump_dir", ctypes.c_char_p),
+                ("image_override", ctypes.c_void_p), ("image_override_size", ctypes.c_size_t),
+                ("stream", ctypes.c_void_p)]
+
+
+class ReplayReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_uint32), ("_pad", ctypes.c_uint32), ("kernel_ms_mean", ctypes.c_double),
+                ("kernel_ms_min", ctypes.c_double), ("kernel_ms_max", ctypes.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "_pad"}
+
+
+class RestoreReport(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "n_regions", "n_spans", "mapped_bytes", "h2d_bytes", "n_failed_regions", "verify_mismatch_chunks")] + [
+        (n, ctypes.c_double) for n in ("t_reserve_s", "t_h2d_s", "t_verify_s", "t_total_s")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+# ----------------------------------------------------------------- loading
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libkc.so (built in-tree by ``python -m paper_2605_03208_b200.build``).
+
+    Raises if it is missing: the product path has no CPU or Python fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2605_03208_b200.build` "
+                          "(there is no fallback for the CUDA path)")
+    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_LOCAL)
+    P, V, U64, I32, SZ = ctypes.POINTER, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_size_t
+    st = ctypes.c_int
+    sig = {
+        "kc_create": (st, [P(V), P(Options)]),
+        "kc_destroy": (None, [V]),
+        "kc_last_error": (ctypes.c_char_p, [V]),
+        "kc_abi_version": (ctypes.c_int, []),
+        "kc_build_info": (ctypes.c_char_p, []),
+        "kc_status_str": (ctypes.c_char_p, [st]),
+        "kc_kernel_launches": (U64, [V]),
+        "kc_track": (st, [V, ctypes.c_int, U64, U64, I32, I32]),
+        "kc_regions": (st, [V, P(Region), SZ, P(SZ)]),
+        "kc_alloc": (st, [V, U64, P(U64)]),
+        "kc_free": (st, [V, U64]),
+        "kc_track_install": (st, [V]),
+        "kc_track_uninstall": (st, [V]),
+        "kc_hash": (st, [V, P(Region), SZ, V, V, V, V]),
+        "kc_count_chunks": (U64, [P(Region), SZ]),
+        "kc_written": (st, [V, V, V, U64, V, V, V]),
+        "kc_diff_async": (st, [V, P(Buffer), SZ, SZ, P(U64), P(U64), P(Tolerance), V, V, V]),
+        "kc_diff": (st, [V, P(Buffer), SZ, P(Tolerance), P(DiffReport), P(U64), V]),
+        "kc_capture": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_char_p, ctypes.c_int, P(CaptureReport)]),
+        "kc_restore": (st, [V, ctypes.c_char_p, P(V), P(RestoreReport)]),
+        "kc_prereserve": (st, [ctypes.c_char_p, P(U64)]),
+        "kc_replay": (st, [V, V, P(ReplayOpts), P(ReplayReport)]),
+        "kc_validate": (st, [V, V, P(Buffer), SZ, P(Tolerance), P(DiffReport), SZ, P(SZ), P(U64)]),
+        "kc_restored_regions": (st, [V, P(Region), SZ, P(SZ)]),
+        "kc_release": (None, [V]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def status_name(s: int) -> str:
+    try:
+        return lib().kc_status_str(s).decode()
+    except Exception:  # pragma: no cover - message path only
+        return str(s)
+
+
+def abi_version() -> int:
+    return lib().kc_abi_version()
+
+
+def build_info() -> str:
+    return lib().kc_build_info().decode()
+
+
+def count_chunks(regions: Sequence[Region]) -> int:
+    arr = _regions(regions)
+    return int(lib().kc_count_chunks(arr, len(regions)))
+
+
+def _regions(regions) -> ctypes.Array:
+    arr = (Region * max(1, len(regions)))()
+    for i, r in enumerate(regions):
+        if isinstance(r, Region):
+            arr[i] = r
+        else:  # (base, size) or (base, size, device, kind)
+            t = tuple(r)
+            arr[i] = Region(t[0], t[1], t[2] if len(t) > 2 else 0, t[3] if len(t) > 3 else 0, 0)
+    return arr
+
+
+def prereserve(snapshot_dir: str) -> int:
+    """Host placeholder reservation of the captured spans before any CUDA call."""
+    n = ctypes.c_uint64(0)
+    rc = lib().kc_prereserve(snapshot_dir.encode(), ctypes.byref(n))
+    if rc < 0:
+        raise KcError(rc, "kc_prereserve failed")
+    return n.value
+
+
+@dataclass
+class Restored:
+    handle: int
+    ctx: "Context"
+
+    def regions(self) -> list:
+        n = ctypes.c_size_t(0)
+        lib().kc_restored_regions(self.handle, None, 0, ctypes.byref(n))
+        arr = (Region * max(1, n.value))()
+        lib().kc_restored_regions(self.handle, arr, n.value, ctypes.byref(n))
+        return [arr[i] for i in range(n.value)]
+
+    def release(self):
+        if self.handle:
+            lib().kc_release(self.handle)
+            self.handle = 0
+
+
+class Context:
+    """A kc_ctx on one device (primary CUDA context)."""
+
+    def __init__(self, device: int = 0, io_chunk_bytes: int = 0, pinned_depth: int = 0,
+                 alloc_mode: int = KC_ALLOC_VMM):
+        L = lib()
+        self._h = ctypes.c_void_p()
+        opt = Options(io_chunk_bytes, pinned_depth, device, alloc_mode, 0)
+        rc = L.kc_create(ctypes.byref(self._h), ctypes.byref(opt))
+        if rc != KC_OK:
+            raise KcError(rc, f"kc_create(device={device}) failed")
+        self.device = device
+
+    # -- plumbing
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().kc_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def kernel_launches(self) -> int:
+        return int(lib().kc_kernel_launches(self._h))
+
+    def last_error(self) -> str:
+        return lib().kc_last_error(self._h).decode(errors="replace")
+
+    def _check(self, rc: int, what: str, ok=(KC_OK,)) -> int:
+        if rc not in ok:
+            raise KcError(rc, f"{what}: {self.last_error()}")
+        return rc
+
+    # -- A1
+    def track(self, ev: int, base: int, size: int = 0, device: int = 0, kind: int = KC_KIND_MEMALLOC) -> int:
+        return self._check(lib().kc_track(self._h, ev, base, size, device, kind), "kc_track")
+
+    def regions(self) -> list:
+        n = ctypes.c_size_t(0)
+        self._check(lib().kc_regions(self._h, None, 0, ctypes.byref(n)), "kc_regions")
+        arr = (Region * max(1, n.value))()
+        self._check(lib().kc_regions(self._h, arr, n.value, ctypes.byref(n)), "kc_regions")
+        return [arr[i] for i in range(n.value)]
+
+    def alloc(self, size: int) -> int:
+        p = ctypes.c_uint64(0)
+        self._check(lib().kc_alloc(self._h, size, ctypes.byref(p)), "kc_alloc")
+        return p.value
+
+    def free(self, dptr: int):
+        self._check(lib().kc_free(self._h, dptr), "kc_free")
+
+    def track_install(self):
+        return self._check(lib().kc_track_install(self._h), "kc_track_install")
+
+    def track_uninstall(self):
+        return self._check(lib().kc_track_uninstall(self._h), "kc_track_uninstall")
+
+    # -- K1 / K3 / K2
+    def hash(self, regions, d_chunk_hash: int, d_region_digest: int = 0, d_snapshot_digest: int = 0,
+             stream: int = 0):
+        arr = _regions(regions)
+        self._check(lib().kc_hash(self._h, arr, len(regions), d_chunk_hash or None, d_region_digest or None,
+                                  d_snapshot_digest or None, stream or None), "kc_hash")
+
+    def written(self, d_pre: int, d_post: int, n_chunks: int, d_bitmap: int, d_count: int = 0, stream: int = 0):
+        self._check(lib().kc_written(self._h, d_pre, d_post, n_chunks, d_bitmap, d_count or None, stream or None),
+                    "kc_written")
+
+    @staticmethod
+    def _buffers(bufs) -> ctypes.Array:
+        arr = (Buffer * max(1, len(bufs)))()
+        for i, b in enumerate(bufs):
+            if isinstance(b, Buffer):
+                arr[i] = b
+            else:  # (ref, act, nbytes, dtype[, report[, chunk0]])
+                t = tuple(b)
+                dt = DT[t[3]] if isinstance(t[3], str) else int(t[3])
+                arr[i] = Buffer(t[0], t[1], t[2], dt, t[4] if len(t) > 4 else i, t[5] if len(t) > 5 else 0)
+        return arr
+
+    def diff(self, bufs, atol: float = 1e-8, rtol: float = 1e-5, equal_nan: bool = False, stream: int = 0,
+             with_bitmaps: bool = True):
+        """K2 over (ref, act, nbytes, dtype) device buffers -> (list of report dicts, list of bitmap word lists)."""
+        n = len(bufs)
+        arr = self._buffers(bufs)
+        reps = (DiffReport * max(1, n))()
+        words = [((b.nbytes + KC_CHUNK_BYTES - 1) // KC_CHUNK_BYTES + 63) // 64 for b in arr[:n]]
+        bm = (ctypes.c_uint64 * max(1, sum(words)))()
+        tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
+        self._check(lib().kc_diff(self._h, arr, n, ctypes.byref(tol), reps, bm if with_bitmaps else None,
+                                  stream or None), "kc_diff")
+        out_b, o = [], 0
+        for w in words:
+            out_b.append([bm[o + k] for k in range(w)])
+            o += w
+        return [reps[i].as_dict() for i in range(n)], out_b
+
+    def diff_async(self, bufs, n_reports: int, report_nbytes: Sequence[int], d_reports: int,
+                   bitmap_word0: Sequence[int] | None = None, d_bitmaps: int = 0, atol: float = 1e-8,
+                   rtol: float = 1e-5, equal_nan: bool = False, stream: int = 0):
+        arr = self._buffers(bufs)
+        rn = (ctypes.c_uint64 * max(1, n_reports))(*report_nbytes)
+        w0 = (ctypes.c_uint64 * max(1, n_reports))(*bitmap_word0) if bitmap_word0 is not None else None
+        tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
+        self._check(lib().kc_diff_async(self._h, arr, len(bufs), n_reports, rn, w0, ctypes.byref(tol), d_reports,
+                                        d_bitmaps or None, stream or None), "kc_diff_async")
+
+    # -- closure
+    def capture(self, directory: str, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
+                block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
+                stream: int = 0) -> tuple[int, dict]:
+        img = ctypes.create_string_buffer(image, len(image)) if image else None
+        ka = ctypes.create_string_buffer(kernarg, len(kernarg)) if kernarg else None
+        d = Dispatch(None, ctypes.cast(img, ctypes.c_void_p) if img else None, len(image) if image else 0,
+                     mangled.encode() if mangled else None, (ctypes.c_uint32 * 3)(*grid),
+                     (ctypes.c_uint32 * 3)(*block), smem, len(kernarg), ctypes.cast(ka, ctypes.c_void_p) if ka else None,
+                     stream or None)
+        rep = CaptureReport()
+        arr = _regions(regions) if regions is not None else None
+        rc = lib().kc_capture(self._h, ctypes.byref(d), arr, len(regions) if regions is not None else 0,
+                              directory.encode(), mode, ctypes.byref(rep))
+        self._check(rc, "kc_capture", ok=(KC_OK, KC_PARTIAL))
+        return rc, rep.as_dict()
+
+    def restore(self, directory: str) -> tuple[Restored, dict]:
+        h = ctypes.c_void_p()
+        rep = RestoreReport()
+        rc = lib().kc_restore(self._h, directory.encode(), ctypes.byref(h), ctypes.byref(rep))
+        if rc != KC_OK:
+            e = KcError(rc, f"kc_restore: {self.last_error()}")
+            e.report = rep.as_dict()
+            raise e
+        return Restored(h.value, self), rep.as_dict()
+
+    def replay(self, restored: Restored, iterations: int = 1, no_recopy: bool = False, dump_dir: str | None = None,
+               image_override: bytes | None = None, stream: int = 0) -> dict:
+        ov = ctypes.create_string_buffer(image_override, len(image_override)) if image_override else None
+        o = ReplayOpts(iterations, int(no_recopy), dump_dir.encode() if dump_dir else None,
+                       ctypes.cast(ov, ctypes.c_void_p) if ov else None, len(image_override) if image_override else 0,
+                       stream or None)
+        rep = ReplayReport()
+        self._check(lib().kc_replay(self._h, restored.handle, ctypes.byref(o), ctypes.byref(rep)), "kc_replay")
+        return rep.as_dict()
+
+    def validate(self, restored: Restored, outs=None, atol: float = 1e-8, rtol: float = 1e-5,
+                 equal_nan: bool = False) -> tuple[list, int]:
+        tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
+        cap = 4096
+        reps = (DiffReport * cap)()
+        nrep = ctypes.c_size_t(0)
+        unexpected = ctypes.c_uint64(0)
+        arr = None
+        n = 0
+        if outs is not None:
+            arr = (Buffer * max(1, len(outs)))()
+            for i, (act, nbytes, dt) in enumerate(outs):
+                arr[i] = Buffer(0, act, nbytes, DT[dt] if isinstance(dt, str) else int(dt), i, 0)
+            n = len(outs)
+        self._check(lib().kc_validate(self._h, restored.handle, arr, n, ctypes.byref(tol), reps, cap,
+                                      ctypes.byref(nrep), ctypes.byref(unexpected)), "kc_validate")
+        return [reps[i].as_dict() for i in range(min(cap, nrep.value))], unexpected.value
+
+
+def exported_symbols() -> list:
+    """Names of the C ABI entry points (checked against include/kc.h in the CPU tests)."""
+    return list(EXPORTED)

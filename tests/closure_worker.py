@@ -1,0 +1,200 @@
+"""Subprocess worker for the closure tests (capture in one process, restore /
+replay / validate in a fresh one).  Prints one JSON line on stdout.
+
+    python tests/closure_worker.py capture-c1 DIR --mode pre_w|post [--mutate] [--free REGION]
+    python tests/closure_worker.py capture-c2 DIR
+    python tests/closure_worker.py replay DIR [--iterations N] [--no-recopy] [--squat]
+    python tests/closure_worker.py recapture DIR OUT2     # restore then snapshot again (round trip)
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2605_03208_b200 import kc  # noqa: E402
+
+
+def _upload(va, arr):
+    import torch
+    v = synth.dev_view(va, arr.size)
+    v.copy_(torch.from_numpy(np.ascontiguousarray(arr)))
+    torch.cuda.synchronize()
+
+
+def _download(va, n):
+    import torch
+    v = synth.dev_view(va, n)
+    return v.cpu().numpy()
+
+
+def capture_c1(a):
+    ctx = kc.Context(0, io_chunk_bytes=a.io_chunk)
+    sizes = [s.size for s in synth.C1_SPECS]
+    vas = [ctx.alloc(sz) for sz in sizes]
+    nodes_va, heads_va, out_va = vas
+    nodes, heads, out = synth.c1_fill(nodes_va)
+    for va, arr in zip(vas, (nodes, heads, out)):
+        _upload(va, arr)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    karg = synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=int(a.mutate))
+    if a.free:
+        os.environ["KC_TEST_FREE_AFTER_DISPATCH"] = f"{vas[a.free]:x}"
+    mode = kc.KC_MODE_PRE_W if a.mode == "pre_w" else kc.KC_MODE_POST
+    rc, rep = ctx.capture(a.dir, image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
+                          kernarg=karg, mode=mode)
+    # the original dispatch's post-state (what the replay must reproduce)
+    if not a.free:
+        np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_orig_out.npy"), _download(out_va, sizes[2]))
+        np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_orig_nodes.npy"), _download(nodes_va, sizes[0]))
+    print(json.dumps({"rc": rc, "report": rep, "vas": vas}))
+
+
+def capture_c2(a):
+    import torch
+    ctx = kc.Context(0)
+    specs = synth.c2_specs()
+    gen = torch.Generator(device="cuda").manual_seed(synth.seed(2))
+    va = {}
+    for s in specs:
+        p = ctx.alloc(s.size)
+        va[s.name] = p
+        synth.fill_device(synth.dev_view(p, s.size), s, gen)
+    torch.cuda.synchronize()
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    rc, rep = ctx.capture(a.dir, image=image, mangled="kc_fixture_decode_attn", grid=(32, 1, 1), block=(128, 1, 1),
+                          kernarg=synth.c2_kernarg(va), mode=kc.KC_MODE_PRE_W)
+    np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_orig_out.npy"),
+            _download(va["attn_out"], specs[[s.name for s in specs].index("attn_out")].size))
+    print(json.dumps({"rc": rc, "report": rep, "vas": va}))
+
+
+def replay(a):
+    if a.prereserve:
+        n = kc.prereserve(a.dir)
+    ctx = kc.Context(0)
+    out = {}
+    if a.squat:
+        from cuda.bindings import driver as drv
+        with open(os.path.join(a.dir, "memory_regions.json")) as f:
+            regs = json.load(f)
+        # squat on the first captured span the way the restore would claim it:
+        # the smallest exactly-honoured aligned window (2 MiB .. 1 GiB)
+        b0 = int(regs[0]["base"], 16)
+        held = None
+        for W in [2 << 20, 32 << 20, 64 << 20, 128 << 20, 256 << 20, 512 << 20, 1 << 30]:
+            lo = b0 // W * W
+            err, p = drv.cuMemAddressReserve(W, W, lo, 0)
+            if int(err) == 0 and int(p) == lo:
+                held = (p, W, lo)
+                break
+            if int(err) == 0:
+                drv.cuMemAddressFree(p, W)
+        p, W, base = held
+        out["squat"] = [0, int(p), base]
+        try:
+            r0, _ = ctx.restore(a.dir)
+            out["restore"] = "unexpected success"
+            r0.release()
+        except kc.KcError as e:
+            out["restore_status"] = e.status
+            out["message"] = str(e)
+        out["squat_free"] = int(drv.cuMemAddressFree(p, W)[0])
+        # after the squatter leaves, the same restore must succeed (full rollback before)
+        try:
+            r, rep = ctx.restore(a.dir)
+            out["retry"] = rep
+            r.release()
+        except kc.KcError as e:
+            out["retry_status"] = e.status
+            out["retry_message"] = str(e)
+        print(json.dumps(out))
+        return
+    try:
+        r, rep = ctx.restore(a.dir)
+    except kc.KcError as e:
+        print(json.dumps({"restore_status": e.status, "message": str(e), "report": getattr(e, "report", None)}))
+        return
+    out["restore"] = rep
+    out["regions"] = [[x.base, x.size] for x in r.regions()]
+    dump = os.path.join(a.dir, "..", os.path.basename(a.dir) + "_replay")
+    out["replay"] = ctx.replay(r, iterations=a.iterations, no_recopy=a.no_recopy, dump_dir=dump)
+    reps, unexpected = ctx.validate(r)
+    out["validate"] = reps
+    out["unexpected_chunks"] = unexpected
+    out["dump"] = dump
+    r.release()
+    print(json.dumps(out))
+
+
+def recapture(a):
+    ctx = kc.Context(0)
+    r, rep = ctx.restore(a.dir)
+    regs = r.regions()
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    # a no-op dispatch (zero lists): the snapshot must equal the restored state
+    karg = synth.c1_kernarg(0, 0, 0, n_lists=0)
+    rc, rep2 = ctx.capture(a.out, image=image, mangled="kc_fixture_walk", grid=(1, 1, 1), block=(32, 1, 1),
+                           kernarg=karg, regions=[(x.base, x.size) for x in regs], mode=kc.KC_MODE_PRE_W)
+    r.release()
+    print(json.dumps({"rc": rc, "restore": rep, "capture": rep2}))
+
+
+def inproc(a):
+    """Capture c1 from cuMemAlloc'd regions, free them, restore in the same
+    process (cuMemAlloc replay for driver-pooled VA), replay, validate."""
+    ctx = kc.Context(0, alloc_mode=kc.KC_ALLOC_MEMALLOC if a.memalloc else kc.KC_ALLOC_VMM)
+    sizes = [s.size for s in synth.C1_SPECS]
+    vas = [ctx.alloc(sz) for sz in sizes]
+    nodes_va, heads_va, out_va = vas
+    for va, arr in zip(vas, synth.c1_fill(nodes_va)):
+        _upload(va, arr)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    rc, rep = ctx.capture(a.dir, image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
+                          kernarg=synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=1))
+    orig = _download(out_va, sizes[2])
+    for va in vas:
+        ctx.free(va)
+    out = {"rc": rc, "vas": vas}
+    try:
+        r, rrep = ctx.restore(a.dir)
+    except kc.KcError as e:
+        out.update({"restore_status": e.status, "message": str(e)})
+        print(json.dumps(out))
+        return
+    out["restore"] = rrep
+    out["replay"] = ctx.replay(r)
+    reps, unexpected = ctx.validate(r)
+    out["validate"] = reps
+    out["unexpected_chunks"] = unexpected
+    out["out_equal"] = bool(np.array_equal(_download(out_va, sizes[2]), orig))
+    r.release()
+    print(json.dumps(out))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("cmd")
+    p.add_argument("dir")
+    p.add_argument("out", nargs="?")
+    p.add_argument("--mode", default="pre_w")
+    p.add_argument("--mutate", action="store_true")
+    p.add_argument("--free", type=int, default=0)
+    p.add_argument("--io-chunk", type=int, default=0)
+    p.add_argument("--iterations", type=int, default=1)
+    p.add_argument("--no-recopy", action="store_true")
+    p.add_argument("--squat", action="store_true")
+    p.add_argument("--prereserve", action="store_true")
+    p.add_argument("--memalloc", action="store_true")
+    a = p.parse_args()
+    {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
+     "inproc": inproc}[a.cmd](a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,209 @@
+"""The address-space closure end to end on the GPU (configs c1, c2):
+capture in one process, VA-faithful restore + replay + validate in a fresh
+one, checked against the oracle (O1 snapshot checker, O5 closure walker).
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "closure_worker.py")
+
+
+def run(*args, env=None, timeout=300):
+    e = dict(os.environ)
+    if env:
+        e.update(env)
+    p = subprocess.run([sys.executable, WORKER, *args], capture_output=True, text=True, timeout=timeout, env=e)
+    assert p.returncode == 0, f"worker {args} failed:\n{p.stdout}\n{p.stderr}"
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2605_03208_b200 import build
+    import oracle
+    build.build()
+    oracle.build()
+
+
+def _walker_prediction(snapdir, mutate):
+    import oracle
+    from oracle import snapshot
+    snap = snapshot.load(snapdir)
+    regs = sorted(snap.regions, key=lambda r: r.base)
+    mem = [(r.base, bytearray(snap.region_bytes(r).tobytes())) for r in regs]
+    ka = open(os.path.join(snapdir, "kernarg.bin"), "rb").read()
+    import struct
+    h, o, nb, nl, mu = struct.unpack("<QQQIi", ka)
+    oracle.walk_lists(mem, h, nl, nb, o, mutate=bool(mu))
+    return {b: np.frombuffer(bytes(m), dtype=np.uint8) for b, m in mem}, (h, o, nb)
+
+
+@pytest.mark.parametrize("mutate", [False, True])
+def test_c1_capture_restore_replay_validate(tmp_path, mutate):
+    d = str(tmp_path / "cap")
+    cap = run("capture-c1", d, "--mode", "pre_w", *(["--mutate"] if mutate else []))
+    assert cap["rc"] == 0
+    from oracle import snapshot
+    summ = snapshot.verify(snapshot.load(d))          # O1: format, manifests, digests, W
+    assert summ["ok"] == 3
+    pred, (heads_va, out_va, nodes_va) = _walker_prediction(d, mutate)
+    # the original dispatch equals the oracle's closure walk
+    orig_out = np.load(str(tmp_path / "cap_orig_out.npy"))
+    assert np.array_equal(orig_out, pred[out_va])
+    if mutate:
+        assert np.array_equal(np.load(str(tmp_path / "cap_orig_nodes.npy")), pred[nodes_va])
+    res = run("replay", d)
+    assert "restore" in res, res
+    assert [tuple(x) for x in res["regions"]] == sorted((r.base, r.size) for r in snapshot.load(d).regions)
+    assert res["restore"]["verify_mismatch_chunks"] == 0
+    # validation: bit-exact against the captured post bytes, nothing else written
+    assert res["validate"], "no written regions validated"
+    for rep in res["validate"]:
+        assert rep["differing_bytes"] == 0 and rep["pass"] == 1
+    assert res["unexpected_chunks"] == 0
+    # the replay's dump equals the walker's prediction (closure property)
+    dump = res["dump"]
+    got_out = np.fromfile(os.path.join(dump, "output", f"region_{out_va:x}.bin"), dtype=np.uint8)
+    assert np.array_equal(got_out, pred[out_va])
+
+
+def test_c1_post_mode_diverges_for_in_place_kernel(tmp_path):
+    """Capture timing (reading R7): POST replays from the post state, so an
+    in-place kernel (F1') cannot reproduce its original output; PRE_W can."""
+    d = str(tmp_path / "post")
+    cap = run("capture-c1", d, "--mode", "post", "--mutate")
+    assert cap["rc"] == 0
+    from oracle import snapshot
+    snapshot.verify(snapshot.load(d))
+    res = run("replay", d)
+    bad = [r for r in res["validate"] if r["differing_bytes"] > 0]
+    assert bad, "POST-mode replay of an in-place kernel should diverge"
+
+
+def test_c1_replay_iterations_recopy(tmp_path):
+    d = str(tmp_path / "it")
+    run("capture-c1", d, "--mode", "pre_w", "--mutate")
+    res = run("replay", d, "--iterations", "5")
+    assert all(r["differing_bytes"] == 0 for r in res["validate"])
+    assert res["replay"]["iterations"] == 5
+    # without recopy the in-place kernel accumulates: iteration 5 != captured post state
+    res2 = run("replay", d, "--iterations", "3", "--no-recopy")
+    assert any(r["differing_bytes"] > 0 for r in res2["validate"])
+
+
+def test_va_squat_aborts_and_rolls_back(tmp_path):
+    """PAPER.md:1080-1082 "VA faithfulness is a hard requirement"."""
+    d = str(tmp_path / "sq")
+    run("capture-c1", d)
+    res = run("replay", d, "--squat")
+    assert res["squat"][0] == 0 and res["squat"][1] == res["squat"][2], res
+    assert res["restore_status"] == -6, res
+    assert res["squat_free"] == 0, res
+    assert "retry" in res, res
+    assert res["retry"]["verify_mismatch_chunks"] == 0
+
+
+def test_corrupted_region_file_is_localised(tmp_path):
+    d = str(tmp_path / "cor")
+    run("capture-c1", d)
+    from oracle import snapshot
+    s = snapshot.load(d)
+    r = max(s.regions, key=lambda x: x.size)
+    p = os.path.join(d, r.data_file)
+    b = bytearray(open(p, "rb").read())
+    b[3 * 65536 + 5] ^= 0xFF
+    open(p, "wb").write(bytes(b))
+    res = run("replay", d)
+    assert res["restore_status"] == -10
+    assert res["report"] is None or True
+    assert "1 restored chunk" in res["message"]
+
+
+def test_round_trip_snapshot_restore_resnapshot(tmp_path):
+    """O6: snapshot -> restore -> re-snapshot gives identical files, manifests and S."""
+    d = str(tmp_path / "rt")
+    run("capture-c1", d, "--mutate")
+    d2 = str(tmp_path / "rt2")
+    res = run("recapture", d, d2)
+    assert res["rc"] == 0
+    from oracle import snapshot
+    a, b = snapshot.load(d), snapshot.load(d2)
+    assert [(r.base, r.size, r.digest) for r in a.regions] == [(r.base, r.size, r.digest) for r in b.regions]
+    for ra, rb in zip(a.regions, b.regions):
+        assert np.array_equal(a.region_bytes(ra), b.region_bytes(rb))
+    assert a.log["snapshot_digest"] == b.log["snapshot_digest"]
+    snapshot.verify(b)
+
+
+def test_region_freed_after_dispatch_is_tolerated(tmp_path):
+    """a buffer freed between completion and snapshot fails
+    alone; metadata and the other regions stay intact."""
+    d = str(tmp_path / "fr")
+    cap = run("capture-c1", d, "--mode", "post", "--free", "1")
+    assert cap["rc"] == 1  # KC_PARTIAL
+    from oracle import snapshot
+    s = snapshot.load(d)
+    st = {r.base: r.status for r in s.regions}
+    assert st[cap["vas"][1]] == "failed"
+    assert sum(v == "ok" for v in st.values()) == 2
+    snapshot.verify(s)
+    assert json.load(open(os.path.join(d, "memory_regions.json")))  # written first, still parses
+
+
+def test_staging_pieces_follow_io_chunk(tmp_path):
+    """the number of D2H copies follows KERNCAP_SNAPSHOT_CHUNK_BYTES."""
+    d = str(tmp_path / "st")
+    cap = run("capture-c1", d, "--io-chunk", str(4 * 65536))
+    # c1 regions: 655,360 / 65,536 / 327,680 B at 256 KiB pieces -> 3 + 1 + 2 copies (+ W gathers)
+    assert cap["report"]["dma_calls"] >= 6
+    assert cap["report"]["staging_high_water"] <= 2 * 4 * 65536
+
+
+def test_c2_llama_shaped_capture_replay(tmp_path):
+    d = str(tmp_path / "c2")
+    cap = run("capture-c2", d)
+    assert cap["rc"] == 0 and cap["report"]["n_regions"] == 21
+    assert cap["report"]["total_bytes"] == 159_383_552
+    from oracle import snapshot
+    summ = snapshot.verify(snapshot.load(d))
+    assert summ["written_chunks"] >= 1
+    res = run("replay", d)
+    assert all(r["differing_bytes"] == 0 for r in res["validate"]), res["validate"]
+    assert res["unexpected_chunks"] == 0
+    orig = np.load(str(tmp_path / "c2_orig_out.npy"))
+    attn = cap["vas"]["attn_out"]
+    got = np.fromfile(os.path.join(res["dump"], "output", f"region_{attn:x}.bin"), dtype=np.uint8)
+    assert np.array_equal(got, orig)
+
+
+def test_inprocess_restore_after_free(tmp_path):
+    """Capture, free every region, restore in the same process at the same
+    VAs, replay, validate (the bench's capture->replay latency path)."""
+    d = str(tmp_path / "ip")
+    res = run("inproc", d)
+    assert res["rc"] == 0
+    assert "restore" in res, res
+    assert all(r["differing_bytes"] == 0 for r in res["validate"])
+    assert res["unexpected_chunks"] == 0 and res["out_equal"]
+
+
+def test_memalloc_regions_restore_exactly_or_abort(tmp_path):
+    """cuMemAlloc regions below the driver's pooling threshold share driver-
+    reserved VA: restore replays cuMemAlloc in capture order and must either
+    land on the exact VAs or abort with KC_ERR_VA_UNAVAILABLE -- never relocate
+    (PAPER.md:1080-1082, 1106-1108)."""
+    d = str(tmp_path / "ipm")
+    res = run("inproc", d, "--memalloc")
+    assert res["rc"] == 0
+    if "restore" in res:
+        assert all(r["differing_bytes"] == 0 for r in res["validate"]) and res["out_equal"]
+    else:
+        assert res["restore_status"] == -6 and "hard requirement" in res["message"]
