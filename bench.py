@@ -138,7 +138,15 @@ class Pool:
         torch.cuda.synchronize()
         log(f"rank {rank}: {len(self.specs)} regions, {sum(s.size for s in self.specs) / 1e9:.3f} GB filled in "
             f"{time.time() - t0:.1f}s")
-        self.regions = sorted([(self.va[s.name], s.size) for s in self.specs])
+        # hashing order: ascending VA at N = 1 (so the snapshot digest is defined);
+        # global spec order at N > 1 (VAs of different processes are not comparable)
+        self.gidx = {s.name: i for i, s in enumerate(specs)}
+        self.all_specs, self.owner = specs, owner
+        if world == 1:
+            self.specs.sort(key=lambda s: self.va[s.name])
+        else:
+            self.specs.sort(key=lambda s: self.gidx[s.name])
+        self.regions = [(self.va[s.name], s.size) for s in self.specs]
         self.bytes = sum(s.size for s in self.specs)
         self.dtype_of = {self.va[s.name]: s.dtype for s in self.specs}
         # F3 dispatch (rank 0): the target kernel, loaded like any captured code object
@@ -176,7 +184,7 @@ class Pool:
     def diff_buffers(self):
         from paper_2605_03208_b200 import kc
         out = []
-        for i, s in enumerate(sorted(self.specs, key=lambda s: self.va[s.name])):
+        for i, s in enumerate(self.specs):
             out.append(kc.Buffer(self.ref[s.name], self.va[s.name], s.size, kc.DT[s.dtype], i, 0))
         return out
 
@@ -213,14 +221,18 @@ def run_ours(a, rank, world, device, log):
     evs = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in KEYS}
            for _ in range(a.steps)]
 
-    # A9 combine buffers (N > 1): manifests all_gather (padded), report all_reduce
-    max_c = C
+    # A9 combine (N > 1): C1 plan broadcast once; per step C2 manifests all-gather, C3 reports all-reduce
+    plan = perm = None
+    glob_reps = None
     if world > 1:
-        t = torch.tensor([C], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        max_c = int(t.item())
-    gath = torch.zeros(world * max(1, max_c), dtype=torch.int64, device="cuda") if world > 1 else None
-    red_sum = torch.zeros(8, dtype=torch.int64, device="cuda")
+        from paper_2605_03208_b200 import dist as kd
+        specs_all = pool.all_specs
+        plan = kd.Plan.from_rank0(list(range(len(specs_all))) if rank == 0 else None,
+                                  [s.size for s in specs_all] if rank == 0 else None,
+                                  pool.owner if rank == 0 else None, device="cuda")
+        perm = plan.manifest_permutation().cuda()
+        rows = torch.tensor([pool.gidx[s.name] for s in pool.specs], dtype=torch.int64, device="cuda")
+        glob_reps = torch.zeros(len(specs_all), REP_WORDS, dtype=torch.int64, device="cuda")
 
     def step(ev):
         launches = 0
@@ -229,7 +241,8 @@ def run_ours(a, rank, world, device, log):
             if ev is not None:
                 ev[k][i].record(stream)
         rec("hash_pre", 0)
-        ctx.hash(pool.regions, pre.data_ptr(), dig.data_ptr(), dig.data_ptr() + 8 * nreg, stream=sh)
+        ctx.hash(pool.regions, pre.data_ptr(), dig.data_ptr(), dig.data_ptr() + 8 * nreg if world == 1 else 0,
+                 stream=sh)
         rec("hash_pre", 1)
         rec("dispatch", 0)
         launches += pool.launch_f3(sh)
@@ -245,14 +258,10 @@ def run_ours(a, rank, world, device, log):
         rec("diff", 1)
         if world > 1:
             rec("combine", 0)
-            # C2: manifests (pad to the max per-rank count); C3: report counters (SUM) and maxima (MAX)
-            mine = torch.zeros(max(1, max_c), dtype=torch.int64, device="cuda")
-            mine[:C].copy_(post[:C])
-            dist.all_gather_into_tensor(gath, mine)
-            r = reps.view(-1, REP_WORDS)
-            red_sum.copy_(torch.stack([r[:, 3].sum(), r[:, 4].sum(), r[:, 9].sum(), r[:, 10].sum(),
-                                       r[:, 11].sum(), r[:, 12].sum(), r[:, 13].sum(), wcnt[0]]))
-            dist.all_reduce(red_sum)
+            kd.Plan.gather_manifest(plan, post, perm)
+            glob_reps.zero_()
+            glob_reps.index_copy_(0, rows, reps.view(-1, REP_WORDS))
+            kd.combine_reports(glob_reps)
             rec("combine", 1)
         return launches
 
@@ -321,6 +330,12 @@ def run_ours(a, rank, world, device, log):
     e2e = None
     if not a.no_e2e:
         e2e = run_e2e(a, ctx, pool, step, stream, world, log)
+    lat = None
+    if world == 1 and not a.no_latency:
+        try:
+            lat = run_latency(a, ctx, pool, log)
+        except Exception as ex:  # reported, never hidden
+            lat = {"error": repr(ex)[:300]}
 
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
@@ -333,7 +348,7 @@ def run_ours(a, rank, world, device, log):
                    "bytes_this_rank": pool.bytes, "l2": "inputs (30 GB) >> L2 (126 MB); no flush needed",
                    "parallelism": f"E1 residency-first shards over {world} GPU(s)"},
         "roofline": roof, "kernels": kern, "clocks": clk, "gpu_launches": launches,
-        "e2e": e2e,
+        "e2e": e2e, "capture_replay": lat,
     }
     return res, pool
 
@@ -371,10 +386,59 @@ def run_e2e(a, ctx, pool, step, stream, world, log):
     if world > 1:
         torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
     ms = float(tm.item())
+    host.clear()
     total = 4 * pool.total_bytes
     return {"value": total / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": pool.total_bytes,
             "d2h_bytes_per_step": 8 * (16 * len(pool.specs)), "ms_per_step": ms, "steps": steps,
             "h2d_gbs": pool.total_bytes / world / (ms * 1e-3) / 1e9}
+
+
+def run_latency(a, ctx, pool, log):
+    """The metric's second half: 30 GB capture -> replay latency through the public
+    C ABI, per stage.  kc_capture (PRE_W: K1 pre-manifest, metadata, pinned D2H of
+    every region to files on /dev/shm, the F3 dispatch, K1 post-manifest, W), then
+    the live regions are freed, kc_restore maps them back at the captured VAs and
+    verifies them against the manifest, kc_replay re-dispatches F3 and
+    kc_validate diffs the written chunks and re-hashes everything."""
+    import shutil
+    import torch
+    import synth
+    from paper_2605_03208_b200 import kc
+    d = a.latency_dir
+    shutil.rmtree(d, ignore_errors=True)
+    regions = [(b, n) for b, n in pool.regions]
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    warps = synth.C4_T * 2816
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rc, cap = ctx.capture(d, image=image, mangled="kc_fixture_moe_gemv", grid=((warps * 32 + 255) // 256, 1, 1),
+                          block=(256, 1, 1), kernarg=pool.kernarg, regions=regions, mode=kc.KC_MODE_PRE_W)
+    t1 = time.perf_counter()
+    for s in pool.specs:
+        ctx.free(pool.va[s.name])
+    t2 = time.perf_counter()
+    r, rst = ctx.restore(d)
+    t3 = time.perf_counter()
+    rep = ctx.replay(r)
+    t4 = time.perf_counter()
+    reps, unexpected = ctx.validate(r)
+    t5 = time.perf_counter()
+    ok = all(x["differing_bytes"] == 0 for x in reps) and unexpected == 0 and rst["verify_mismatch_chunks"] == 0
+    restored = sorted((x.base, x.size) for x in r.regions()) == sorted(regions)
+    r.release()
+    shutil.rmtree(d, ignore_errors=True)
+    total = (t1 - t0) + (t3 - t2) + (t4 - t3) + (t5 - t4)
+    log(f"capture->replay: capture {t1 - t0:.2f}s restore {t3 - t2:.2f}s replay {t4 - t3:.3f}s "
+        f"validate {t5 - t4:.3f}s ok={ok}")
+    return {"latency_s": total, "bytes": pool.bytes, "validated_bit_exact": bool(ok), "same_vas": bool(restored),
+            "sink": d, "written_chunks": cap["written_chunks"],
+            "stages_s": {"capture_total": t1 - t0, "capture_hash_pre": cap["t_hash_pre_s"],
+                         "capture_d2h_and_files": cap["t_d2h_s"], "capture_dispatch": cap["t_dispatch_s"],
+                         "capture_hash_post": cap["t_hash_post_s"], "restore_total": t3 - t2,
+                         "restore_reserve_map": rst["t_reserve_s"], "restore_files_h2d": rst["t_h2d_s"],
+                         "restore_verify": rst["t_verify_s"], "replay": t4 - t3, "validate": t5 - t4},
+            "d2h_gbs_incl_files": pool.bytes / max(cap["t_d2h_s"], 1e-9) / 1e9,
+            "h2d_gbs_incl_files": rst["h2d_bytes"] / max(rst["t_h2d_s"], 1e-9) / 1e9}
 
 
 # ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
@@ -394,8 +458,8 @@ def oracle_sample(pool_or_none, sample_mb: int):
     out = []
     rng = np.random.default_rng(synth.seed(4, 999))
     for s in chosen:
-        if pool_or_none is not None and s.name in pool_or_none.va:
-            v = synth.dev_view(pool_or_none.va[s.name], s.size).cpu().numpy()
+        if pool_or_none is not None and s.name in pool_or_none.ref:
+            v = synth.dev_view(pool_or_none.ref[s.name], s.size).cpu().numpy()
         elif s.fill == "zero":
             v = np.zeros(s.size, dtype=np.uint8)
         else:
@@ -405,20 +469,28 @@ def oracle_sample(pool_or_none, sample_mb: int):
     return out
 
 
-def time_oracle(sample, threads: int):
+def time_oracle(sample, threads: int, min_seconds: float = 0.0):
+    """The oracle as it stands on the host cores: per pass, two manifests (A2, A4)
+    and the diff of every sampled region against its reference copy (A8); passes
+    repeat until min_seconds of work.  Returns (GB/s in the metric's unit, s, bytes)."""
     import oracle
     from concurrent.futures import ThreadPoolExecutor
     oracle.build()
-    t0 = time.perf_counter()
-    # A2 + A4: two manifests; A8: diff of each region against its reference copy
-    with ThreadPoolExecutor(threads) as ex:
-        list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), sample))
-        list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), sample))
-        dts = {"bf16": oracle.DT_BF16, "u64": oracle.DT_U64, "i32": oracle.DT_I32, "f32": oracle.DT_F32}
-        list(ex.map(lambda sv: oracle.diff(sv[1], sv[1], dts.get(sv[0].dtype, oracle.DT_BYTES)), sample))
-    dt = time.perf_counter() - t0
+    dts = {"bf16": oracle.DT_BF16, "u64": oracle.DT_U64, "i32": oracle.DT_I32, "f32": oracle.DT_F32}
+    refs = [(s, v, v.copy()) for s, v in sample]
     nbytes = sum(v.size for _, v in sample)
-    return 4 * nbytes / dt / 1e9, dt, nbytes
+    passes = 0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        while True:
+            list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), refs))
+            list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), refs))
+            list(ex.map(lambda sv: oracle.diff(sv[2], sv[1], dts.get(sv[0].dtype, oracle.DT_BYTES)), refs))
+            passes += 1
+            if time.perf_counter() - t0 >= min_seconds:
+                break
+    dt = time.perf_counter() - t0
+    return 4 * nbytes * passes / dt / 1e9, dt, nbytes * passes
 
 
 def run_reference(a, rank, world):
@@ -426,16 +498,17 @@ def run_reference(a, rank, world):
         return None
     threads = os.cpu_count() or 1
     sample = oracle_sample(None, a.cpu_sample_mb)
-    for _ in range(a.warmup if a.warmup < 2 else 1):
+    for _ in range(min(a.warmup, 1)):
         time_oracle(sample[:2], threads)
     vals, secs = [], 0.0
     for _ in range(a.steps):
-        v, dt, nb = time_oracle(sample, threads)
+        v, dt, nb = time_oracle(sample, threads, a.ref_step_seconds)
         vals.append(v)
         secs += dt
     value = sum(vals) / len(vals)
-    desc = (f"{len(sample)} c4 regions ({nb / 1e6:.1f} MB, smallest-first, regenerated on host with the c4 recipes); "
-            f"per step: 2 oracle manifests + oracle diff of each region vs its reference")
+    desc = (f"{len(sample)} smallest c4 regions ({sum(v.size for _, v in sample) / 1e6:.1f} MB, regenerated on the "
+            f"host with the c4 recipes), repeated for >= {a.ref_step_seconds:.0f} s per step: 2 oracle manifests + "
+            f"oracle diff of each region vs its reference per pass")
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
@@ -453,6 +526,10 @@ def main():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-sample-mb", type=int, default=384)
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--ref-step-seconds", type=float, default=5.0)
+    p.add_argument("--no-latency", action="store_true")
+    p.add_argument("--latency-dir", default="/dev/shm/kc_bench_capture")
     p.add_argument("--quiet", action="store_true")
     a = p.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -475,10 +552,12 @@ def main():
     if rank == 0:
         threads = os.cpu_count() or 1
         sample = oracle_sample(pool, a.cpu_sample_mb)
-        v, dt, nb = time_oracle(sample, threads)
+        v, dt, nb = time_oracle(sample, threads, a.cpu_seconds)
         res["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                               "sample": f"{len(sample)} regions of this run's c4 pool ({nb / 1e6:.1f} MB): "
-                                         f"2 oracle manifests + oracle diff; {dt:.2f} s"}
+                               "sample": f"{len(sample)} smallest regions of this run's c4 pool "
+                                         f"({sum(x.size for _, x in sample) / 1e6:.1f} MB) repeated to "
+                                         f"{nb / 1e9:.2f} GB: 2 oracle manifests + oracle diff per pass; "
+                                         f"{dt:.1f} s on {threads} threads"}
         print(json.dumps(res), flush=True)
     if world > 1:
         torch.distributed.barrier()

@@ -11,6 +11,9 @@
 #include <cuda_fp16.h>
 #include <math_constants.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kc_kernels.cuh"
 
 namespace kc {
@@ -31,6 +34,22 @@ __device__ __forceinline__ uint64_t xround(uint64_t acc, uint64_t x) {
     acc += x * P2;
     acc = rotl64(acc, 31);
     return acc * P1;
+}
+
+// Same round with an explicit 32-bit schedule: acc + x*P2 as one mad.wide plus
+// two off-chain IMADs, the 64-bit rotate as two funnel shifts, *P1 as one
+// mad.wide + two IMADs (10 SASS instead of 13; the chain is what bounds K1).
+__device__ __forceinline__ uint64_t xround_fast(uint64_t acc, uint64_t x) {
+    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    uint64_t w;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(xl), "r"((uint32_t)P2), "l"(acc));
+    const uint32_t t = xl * (uint32_t)(P2 >> 32) + xh * (uint32_t)P2;
+    const uint32_t sl = (uint32_t)w, sh = (uint32_t)(w >> 32) + t;
+    const uint32_t rh = __funnelshift_l(sl, sh, 31), rl = __funnelshift_l(sh, sl, 31);
+    uint64_t w2;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(w2) : "r"(rl), "r"((uint32_t)P1));
+    const uint32_t t2 = rl * (uint32_t)(P1 >> 32) + rh * (uint32_t)P1;
+    return (w2 & 0xFFFFFFFFull) | ((uint64_t)((uint32_t)(w2 >> 32) + t2) << 32);
 }
 
 __device__ __forceinline__ uint64_t xavalanche(uint64_t h) {
@@ -120,7 +139,7 @@ __device__ uint64_t quad_xxh64_global(const uint8_t* p, uint64_t len, int ql, un
     for (uint64_t t = 0; t < nst; ++t) {
         const uint64_t x =
             ALIGNED ? __ldg(reinterpret_cast<const unsigned long long*>(q + 32 * t)) : ldg_u64_bytes(q + 32 * t);
-        v = xround(v, x);
+        v = xround_fast(v, x);
     }
     return quad_finish<ALIGNED>(v, ql, qmask, len, p + 32 * nst);
 }
@@ -135,20 +154,27 @@ __device__ __forceinline__ int find_region(const RegionDev* __restrict__ r, int 
 }
 
 // ========================================================================== //
-// K1: chunk hash.  One CTA = 64 chunk slots x 4 lanes (one XXH64 accumulator //
-// per lane).  Each slot owns a private 3-stage ring of 1 KiB slices filled by //
-// cp.async.bulk (TMA 1-D bulk copies, mbarrier complete_tx); lane 0 of the    //
-// quad is the producer, all 4 lanes consume with LDS.64.  Slots stream their  //
-// chunk sequence continuously, so the next chunk's first slices are in       //
-// flight while the current chunk finishes.  Chunk g -> slot (g / grid) % 64   //
-// of CTA g % grid: every CTA gets the same share (interleaved).              //
+// K1: chunk hash.  XXH64 of a 64 KiB chunk is four serial 2,048-step chains //
+// (one per accumulator), so K1 is latency-bound per chunk and HBM-bound only //
+// with >= ~64 chunks in flight per SM.  A quad of lanes hashes one chunk (one //
+// accumulator per lane, shuffle merge).  Two staging designs share the body: //
+//  * k1_hash_tma: per-quad 3-stage ring filled by cp.async.bulk (TMA 1-D     //
+//    bulk copies + mbarrier complete_tx), lane 0 of the quad the producer;   //
+//  * k1_hash_cpasync (default): a warp stages its 8 quads' next slices with  //
+//    coalesced 16-byte cp.async (512 B per warp instruction) into padded,    //
+//    bank-conflict-free rings.                                               //
+// Measured on B200: the per-request cost of 1 KiB bulk copies    //
+// caps the TMA ring at ~5.0 TB/s, the cp.async ring reaches the HBM peak.    //
 // ========================================================================== //
-constexpr int HK_THREADS = 256;
-constexpr int HK_SLOTS = HK_THREADS / 4;
-constexpr int HK_STAGES = 3;
-constexpr int HK_SLICE = 1024;
-constexpr int HK_PITCH = HK_SLICE + 32;  // quads of a warp land on distinct bank groups
-constexpr size_t HK_SMEM = (size_t)HK_SLOTS * HK_STAGES * HK_PITCH + (size_t)HK_SLOTS * HK_STAGES * 8;
+template <int THREADS, int STAGES, int SLICE>
+struct HkCfg {
+    static constexpr int kThreads = THREADS;
+    static constexpr int kSlots = THREADS / 4;
+    static constexpr int kStages = STAGES;
+    static constexpr int kSlice = SLICE;
+    static constexpr int kPitch = SLICE + 32;  // quads of a warp land on distinct bank groups
+    static constexpr size_t kSmem = (size_t)kSlots * STAGES * kPitch + (size_t)kSlots * STAGES * 8;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -193,18 +219,19 @@ __device__ __forceinline__ ChunkRef chunk_ref(const RegionDev* __restrict__ regs
     return {reinterpret_cast<const uint8_t*>(regs[r].base + off), rem < kChunk ? (uint32_t)rem : (uint32_t)kChunk};
 }
 
-__global__ void __launch_bounds__(HK_THREADS, 1)
+template <class CFG>
+__global__ void __launch_bounds__(CFG::kThreads, 1)
     k1_hash_tma(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int slot = threadIdx.x >> 2;
     const int ql = threadIdx.x & 3;
     const unsigned qmask = 0xFu << (threadIdx.x & 28);
-    uint8_t* ring = smem + (size_t)slot * HK_STAGES * HK_PITCH;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)HK_SLOTS * HK_STAGES * HK_PITCH) + slot * HK_STAGES;
+    uint8_t* ring = smem + (size_t)slot * CFG::kStages * CFG::kPitch;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)CFG::kSlots * CFG::kStages * CFG::kPitch) + slot * CFG::kStages;
 
     if (ql == 0) {
 #pragma unroll
-        for (int s = 0; s < HK_STAGES; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < CFG::kStages; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -212,7 +239,7 @@ __global__ void __launch_bounds__(HK_THREADS, 1)
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
 
-    const uint64_t Q = (uint64_t)HK_SLOTS * gridDim.x;
+    const uint64_t Q = (uint64_t)CFG::kSlots * gridDim.x;
     const uint64_t g0 = (uint64_t)slot * gridDim.x + blockIdx.x;
 
     // ---- producer cursor (used by ql == 0 only) ----
@@ -231,10 +258,10 @@ __global__ void __launch_bounds__(HK_THREADS, 1)
                 phave = true;
             }
             if (poff < pbytes) {
-                const uint32_t b = min((uint32_t)HK_SLICE, pbytes - poff);
-                const int st = fetched % HK_STAGES;
+                const uint32_t b = min((uint32_t)CFG::kSlice, pbytes - poff);
+                const int st = fetched % CFG::kStages;
                 mbar_arrive_expect_tx(&bars[st], b);
-                bulk_g2s(ring + st * HK_PITCH, psrc + poff, b, &bars[st], policy);
+                bulk_g2s(ring + st * CFG::kPitch, psrc + poff, b, &bars[st], policy);
                 poff += b;
                 ++fetched;
                 if (poff == pbytes) { pg += Q; phave = false; }
@@ -245,7 +272,7 @@ __global__ void __launch_bounds__(HK_THREADS, 1)
         }
     };
     if (ql == 0) {
-        for (int s = 0; s < HK_STAGES; ++s) issue_next();
+        for (int s = 0; s < CFG::kStages; ++s) issue_next();
     }
 
     uint32_t consumed = 0;
@@ -255,16 +282,16 @@ __global__ void __launch_bounds__(HK_THREADS, 1)
         uint64_t v = lane_seed(ql);
         uint32_t remaining = nst * 32;
         while (remaining > 0) {
-            const int st = consumed % HK_STAGES;
-            mbar_wait(&bars[st], (consumed / HK_STAGES) & 1);
-            const uint64_t* p = reinterpret_cast<const uint64_t*>(ring + st * HK_PITCH) + ql;
-            if (remaining >= (uint32_t)HK_SLICE) {
+            const int st = consumed % CFG::kStages;
+            mbar_wait(&bars[st], (consumed / CFG::kStages) & 1);
+            const uint64_t* p = reinterpret_cast<const uint64_t*>(ring + st * CFG::kPitch) + ql;
+            if (remaining >= (uint32_t)CFG::kSlice) {
 #pragma unroll
-                for (int t = 0; t < HK_SLICE / 32; ++t) v = xround(v, p[4 * t]);
-                remaining -= HK_SLICE;
+                for (int t = 0; t < CFG::kSlice / 32; ++t) v = xround_fast(v, p[4 * t]);
+                remaining -= CFG::kSlice;
             } else {
                 const uint32_t n = remaining / 32;
-                for (uint32_t t = 0; t < n; ++t) v = xround(v, p[4 * t]);
+                for (uint32_t t = 0; t < n; ++t) v = xround_fast(v, p[4 * t]);
                 remaining = 0;
             }
             ++consumed;
@@ -277,6 +304,133 @@ __global__ void __launch_bounds__(HK_THREADS, 1)
         const uint64_t h = quad_finish<true>(v, ql, qmask, cr.len, cr.src + (size_t)nst * 32);
         if (ql == 0) out[g] = h;
     }
+}
+
+// V_CPASYNC: warp-cooperative cp.async staging.  A warp hashes 8 consecutive
+// chunks (one per quad); per pipeline step every lane copies 16-byte pieces of
+// all 8 chunks' next 1 KiB slices (coalesced 512-byte rows), so 64 chunks per
+// SM are in compute while STAGES-1 steps are in flight.  Slices are padded by
+// 32 bytes so the 8 quads of a warp read distinct bank groups.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int WARPS, int STAGES, int SL>
+struct CpCfg {
+    static constexpr int kWarps = WARPS, kStages = STAGES, kSlice = SL;
+    static constexpr int kPitch = SL + 32;      // quads of a warp on distinct bank groups
+    static constexpr int kWStage = 8 * kPitch;  // one warp's stage: 8 chunk slices
+    static constexpr int kUPC = SL / 16;        // 16-byte copy units per chunk slice
+    static constexpr int kUPL = (8 * kUPC + 31) / 32;  // copy units per lane per step
+    static constexpr size_t kSmem = (size_t)WARPS * STAGES * kWStage;
+};
+
+template <class CFG>
+__global__ void __launch_bounds__(CFG::kWarps * 32, 1)
+    k1_hash_cpasync(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out) {
+    constexpr int WARPS = CFG::kWarps, STAGES = CFG::kStages, SL = CFG::kSlice, PITCH = CFG::kPitch;
+    constexpr int WSTAGE = CFG::kWStage, UPC = CFG::kUPC, UPL = CFG::kUPL;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q = lane >> 2, ql = lane & 3;
+    const unsigned qmask = 0xFu << (lane & 28);
+    uint8_t* wring = smem + (size_t)w * STAGES * WSTAGE;
+    const uint64_t ngroups = (C + 7) / 8;
+    const uint64_t W = (uint64_t)gridDim.x * WARPS;
+    const uint64_t j0 = (uint64_t)w * gridDim.x + blockIdx.x;  // interleaved over CTAs
+
+    // fetch cursor (warp-uniform): group jf, slice sf.  Per lane: the chunk of
+    // each of its UPL copy units (unit u = lane + 32k -> chunk u / UPC).
+    uint64_t jf = j0;
+    uint32_t sf = 0, f_nsl = 0;
+    unsigned long long u_src[UPL];
+    uint32_t u_bytes[UPL];
+    auto load_group = [&](uint64_t j) {
+        const uint64_t g = 8 * j + q;
+        unsigned long long src = 0;
+        uint32_t bytes = 0;
+        if (g < C) {
+            const ChunkRef cr = chunk_ref(regs, nreg, g);
+            src = (unsigned long long)cr.src;
+            bytes = cr.len >= 32 ? (cr.len & ~31u) : 0u;
+        }
+        f_nsl = __reduce_max_sync(0xFFFFFFFFu, (bytes + SL - 1) / SL);
+#pragma unroll
+        for (int k = 0; k < UPL; ++k) {
+            const int u = lane + 32 * k;
+            const int qq = u < 8 * UPC ? u / UPC : 0;
+            u_src[k] = __shfl_sync(0xFFFFFFFFu, src, 4 * qq);
+            u_bytes[k] = __shfl_sync(0xFFFFFFFFu, bytes, 4 * qq);
+        }
+    };
+    auto issue = [&](int stage) {
+        uint8_t* dst = wring + stage * WSTAGE;
+#pragma unroll
+        for (int k = 0; k < UPL; ++k) {
+            const int u = lane + 32 * k;
+            if (u < 8 * UPC) {
+                const int qq = u / UPC, off = (u % UPC) * 16;
+                const uint32_t g_off = sf * SL + off;
+                if (g_off < u_bytes[k])
+                    cp_async16(dst + qq * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+            }
+        }
+    };
+    auto advance = [&]() {
+        if (++sf >= f_nsl) {
+            sf = 0;
+            jf += W;
+            if (jf < ngroups) load_group(jf); else f_nsl = 0;
+        }
+    };
+    auto fetch = [&](int stage) {  // next step of the sequence (skips groups with no full stripe)
+        while (jf < ngroups && f_nsl == 0) {
+            jf += W;
+            if (jf < ngroups) load_group(jf);
+        }
+        if (jf < ngroups) {
+            issue(stage);
+            advance();
+        }
+        cp_async_commit();
+    };
+    if (j0 < ngroups) load_group(jf);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) fetch(s);
+    uint32_t step = 0;
+    for (uint64_t j = j0; j < ngroups; j += W) {
+        const uint64_t g = 8 * j + q;
+        ChunkRef cr = {nullptr, 0};
+        if (g < C) cr = chunk_ref(regs, nreg, g);
+        const uint32_t nst = cr.len >= 32 ? cr.len / 32 : 0;
+        const uint32_t nsl = __reduce_max_sync(0xFFFFFFFFu, (nst * 32 + SL - 1) / SL);
+        uint64_t v = lane_seed(ql);
+        for (uint32_t s = 0; s < nsl; ++s, ++step) {
+            cp_async_wait<STAGES - 2>();
+            __syncwarp();
+            const int st = step % STAGES;
+            const uint64_t* p = reinterpret_cast<const uint64_t*>(wring + st * WSTAGE + q * PITCH) + ql;
+            const uint32_t done = s * (SL / 32);
+            const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
+            if (n == SL / 32) {
+#pragma unroll
+                for (int t = 0; t < SL / 32; ++t) v = xround_fast(v, p[4 * t]);
+            } else {
+                for (uint32_t t = 0; t < n; ++t) v = xround_fast(v, p[4 * t]);
+            }
+            __syncwarp();
+            fetch((step + STAGES - 1) % STAGES);
+        }
+        if (g < C) {
+            const uint64_t h = quad_finish<true>(v, ql, qmask, cr.len, cr.src + (size_t)nst * 32);
+            if (ql == 0) out[g] = h;
+        } else {
+            quad_finish<true>(v, ql, qmask, 0, nullptr);
+        }
+    }
+    cp_async_wait<0>();
 }
 
 // Unaligned regions (base % 16 != 0): quad per chunk, byte-assembled loads.
@@ -782,22 +936,61 @@ __global__ void k4_gather(const uint64_t* __restrict__ src, const uint64_t* __re
 // ========================================================================== //
 // launchers                                                                  //
 // ========================================================================== //
+using TmaA = HkCfg<256, 3, 1024>;  // 64 slots x 3 x 1 KiB
+using TmaB = HkCfg<128, 3, 2048>;  // 32 slots x 3 x 2 KiB
+using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bound)
+using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
+
 cudaError_t kernels_init() {
-    return cudaFuncSetAttribute(k1_hash_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HK_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k1_hash_tma<TmaA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaA::kSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k1_hash_tma<TmaB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaB::kSmem);
+#define KC_CP_ATTR(CFG)                                                                                      \
+    if (e == cudaSuccess)                                                                                    \
+        e = cudaFuncSetAttribute(k1_hash_cpasync<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
+    KC_CP_ATTR(CpA) KC_CP_ATTR(CpD)
+#undef KC_CP_ATTR
+    return e;
+}
+
+template <class CFG>
+static void launch_tma(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, int num_sms, cudaStream_t s) {
+    uint64_t grid = (C + CFG::kSlots - 1) / CFG::kSlots;
+    if (grid > (uint64_t)num_sms) grid = num_sms;
+    k1_hash_tma<CFG><<<(unsigned)grid, CFG::kThreads, CFG::kSmem, s>>>(d_regs, nreg, C, d_out);
+}
+
+template <class CFG>
+static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, int num_sms, cudaStream_t s) {
+    const uint64_t groups = (C + 7) / 8;
+    const uint64_t grid = std::min<uint64_t>((groups + CFG::kWarps - 1) / CFG::kWarps, (uint64_t)num_sms);
+    k1_hash_cpasync<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out);
+}
+
+// K1 variant selection (KC_K1_VARIANT, tuning knob; default = the measured best)
+static int k1_variant() {
+    static int v = [] {
+        const char* e = getenv("KC_K1_VARIANT");
+        return e && *e ? atoi(e) : 0;
+    }();
+    return v;
 }
 
 cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool aligned, uint64_t* d_out, int num_sms,
                         cudaStream_t s) {
     if (C == 0) return cudaSuccess;
-    if (aligned) {
-        // one CTA per SM (64 chunk slots each); fewer CTAs when there are few chunks
-        uint64_t grid = (C + HK_SLOTS - 1) / HK_SLOTS;
-        if (grid > (uint64_t)num_sms) grid = num_sms;
-        k1_hash_tma<<<(unsigned)grid, HK_THREADS, HK_SMEM, s>>>(d_regs, nreg, C, d_out);
-    } else {
+    if (!aligned) {
         uint64_t grid = (C + 63) / 64;
         if (grid > (uint64_t)num_sms * 8) grid = num_sms * 8;
         k1_hash_generic<<<(unsigned)grid, 256, 0, s>>>(d_regs, nreg, C, d_out);
+        return cudaGetLastError();
+    }
+    // measured on B200: cp.async 64 chunks x 3 x 1 KiB is HBM-bound
+    switch (k1_variant()) {
+        case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, num_sms, s); break;
+        case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, num_sms, s); break;
+        case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, num_sms, s); break;
+        default: launch_cp<CpA>(d_regs, nreg, C, d_out, num_sms, s); break;
     }
     return cudaGetLastError();
 }

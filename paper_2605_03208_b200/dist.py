@@ -1,0 +1,160 @@
+"""A9: multi-GPU combine of manifests and diff reports over torch.distributed.
+
+SURVEY.md 8(e): chunks are independent for K1 and K2 and every combine is a
+concatenation, a SUM or a MAX, so the N-GPU result equals the 1-GPU result bit
+for bit (O7).  Placement is residency-first (E1): each rank hashes/diffs the
+regions resident in its own HBM.  Collectives (NCCL on GPUs, gloo on CPU):
+
+  C1  broadcast of the global region table + owner map (Plan.from_rank0)
+  C2  all_gather of per-rank chunk manifests, reordered into global chunk order
+  C3  all_reduce SUM of report counters and MAX of report maxima
+  C4  all_gather (bitwise OR) of mismatch-bitmap words
+
+Host logic only: every byte of hashing and diffing happened in libkc.so.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+CHUNK = 65536
+REP_WORDS = 15  # sizeof(kc_diff_report) / 8
+# kc_diff_report word offsets (include/kc.h)
+NBYTES, N_ELEMS, N_CHUNKS, DIFF_BYTES, DIFF_ELEMS, MAX_ULP, MAX_ABS, MAX_REL, PERCENT = range(9)
+NAN_REF, NAN_ACT, NAN_POS, REL_UNDEF, ALLCLOSE_FAIL, PASS = range(9, 15)
+SUM_FIELDS = [DIFF_BYTES, DIFF_ELEMS, NAN_REF, NAN_ACT, NAN_POS, REL_UNDEF, ALLCLOSE_FAIL]
+MAX_FIELDS = [MAX_ULP, MAX_ABS, MAX_REL]
+_SIGN = -(1 << 63)
+
+
+def _nchunks(size: int) -> int:
+    return (size + CHUNK - 1) // CHUNK
+
+
+@dataclass
+class Plan:
+    """Global region table (sorted by base) with the owning rank of each region."""
+    bases: list
+    sizes: list
+    owner: list
+    world: int
+    rank: int
+
+    @staticmethod
+    def from_rank0(bases, sizes, owner, group=None, device="cpu") -> "Plan":
+        """C1: rank 0's table is broadcast to every rank (other ranks may pass None)."""
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        n = torch.tensor([len(bases) if rank == 0 else 0], dtype=torch.int64, device=device)
+        dist.broadcast(n, 0, group=group)
+        t = torch.zeros(3, int(n.item()), dtype=torch.int64, device=device)
+        if rank == 0:
+            t[0] = torch.tensor(list(bases), dtype=torch.int64)
+            t[1] = torch.tensor(list(sizes), dtype=torch.int64)
+            t[2] = torch.tensor(list(owner), dtype=torch.int64)
+        dist.broadcast(t, 0, group=group)
+        order = torch.argsort(t[0].cpu(), stable=True)
+        tc = t.cpu()[:, order]
+        return Plan(tc[0].tolist(), tc[1].tolist(), tc[2].tolist(), world, rank)
+
+    # -- per-rank views
+    def local_regions(self, r=None):
+        r = self.rank if r is None else r
+        return [(b, s) for b, s, o in zip(self.bases, self.sizes, self.owner) if o == r]
+
+    def local_chunks(self, r=None) -> int:
+        return sum(_nchunks(s) for _, s in self.local_regions(r))
+
+    def max_local_chunks(self) -> int:
+        return max(self.local_chunks(r) for r in range(self.world))
+
+    def global_chunks(self) -> int:
+        return sum(_nchunks(s) for s in self.sizes)
+
+    def manifest_permutation(self) -> torch.Tensor:
+        """Index into the gathered [world, max_local] manifest that yields global chunk order."""
+        pad = self.max_local_chunks()
+        offs = [0] * self.world
+        idx = []
+        for s, o in zip(self.sizes, self.owner):
+            n = _nchunks(s)
+            idx.extend(range(o * pad + offs[o], o * pad + offs[o] + n))
+            offs[o] += n
+        return torch.tensor(idx, dtype=torch.int64)
+
+    # -- C2
+    def gather_manifest(self, local_h: torch.Tensor, perm: torch.Tensor | None = None, group=None) -> torch.Tensor:
+        """All-gather the per-rank manifests (int64 views of the u64 hashes, local
+        regions in ascending base) and return the global manifest."""
+        pad = self.max_local_chunks()
+        mine = torch.zeros(max(1, pad), dtype=torch.int64, device=local_h.device)
+        n = self.local_chunks()
+        mine[:n].copy_(local_h[:n])
+        out = torch.empty(self.world * max(1, pad), dtype=torch.int64, device=local_h.device)
+        dist.all_gather_into_tensor(out, mine, group=group)
+        if perm is None:
+            perm = self.manifest_permutation()
+        return out.index_select(0, perm.to(local_h.device))
+
+
+# ------------------------------------------------------------------ C3
+def combine_reports(reps: torch.Tensor, group=None) -> torch.Tensor:
+    """All-reduce per-buffer reports ([R, 15] int64 view of kc_diff_report):
+    SUM of the counters, MAX of max_ulp (unsigned, order-preserving sign flip)
+    and of max_abs / max_rel (non-negative doubles order like their bits).
+    nbytes/n_elems/n_chunks/percent/pass are recomputed by :func:`finalize`."""
+    out = reps.clone()
+    s = reps[:, SUM_FIELDS].contiguous()
+    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+    m = reps[:, MAX_FIELDS].contiguous()
+    m[:, 0] ^= _SIGN
+    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    m[:, 0] ^= _SIGN
+    out[:, SUM_FIELDS] = s
+    out[:, MAX_FIELDS] = m
+    return out
+
+
+_ELEM = {"bytes": 1, "u8": 1, "i8": 1, "u16": 2, "i16": 2, "u32": 4, "i32": 4, "u64": 8, "i64": 8,
+         "f16": 2, "bf16": 2, "f32": 4, "f64": 8}
+_FLOATS = ("f16", "bf16", "f32", "f64")
+
+
+def finalize(combined: torch.Tensor, nbytes: list, dtypes: list) -> list:
+    """Host-side report dicts of a combined report table (same rules as K2's finalize)."""
+    rows = combined.cpu()
+    out = []
+    for i, (n, dt) in enumerate(zip(nbytes, dtypes)):
+        r = rows[i]
+        u = lambda k: int(r[k].item()) & 0xFFFFFFFFFFFFFFFF
+        d = lambda k: float(torch.tensor([int(r[k].item())], dtype=torch.int64).view(torch.float64).item())
+        db = u(DIFF_BYTES)
+        rep = {"nbytes": n, "n_elems": n // _ELEM[dt], "n_chunks": _nchunks(n), "differing_bytes": db,
+               "differing_elems": db if dt == "bytes" else u(DIFF_ELEMS), "max_ulp": u(MAX_ULP),
+               "max_abs": d(MAX_ABS), "max_rel": d(MAX_REL),
+               "percent_bytes": (100.0 * float(db)) / float(n) if n else 0.0,
+               "nan_ref": u(NAN_REF), "nan_act": u(NAN_ACT), "nan_pos_mismatch": u(NAN_POS),
+               "rel_undefined": u(REL_UNDEF), "allclose_fail": u(ALLCLOSE_FAIL)}
+        if dt == "bytes":
+            rep["pass"] = int(db == 0)
+        elif dt in _FLOATS:
+            rep["pass"] = int(rep["allclose_fail"] == 0)
+        else:
+            rep["pass"] = int(rep["differing_elems"] == 0)
+        out.append(rep)
+    return out
+
+
+# ------------------------------------------------------------------ C4
+def gather_bitmaps(local_words: torch.Tensor, group=None) -> torch.Tensor:
+    """Bitwise OR of every rank's bitmap words (ranks hold disjoint chunks under
+    E1, so the OR is a concatenation; split buffers OR their bits)."""
+    world = dist.get_world_size(group)
+    out = torch.empty(world * local_words.numel(), dtype=local_words.dtype, device=local_words.device)
+    dist.all_gather_into_tensor(out, local_words.contiguous(), group=group)
+    acc = out.view(world, -1)[0].clone()
+    for r in range(1, world):
+        acc |= out.view(world, -1)[r]
+    return acc

@@ -52,12 +52,31 @@ def test_sm100a_code_in_library(kclib):
     assert "sm_100a" in out
 
 
-def test_tma_bulk_copy_in_k1_sass(kclib):
-    # K1 stages chunk slices with cp.async.bulk (SASS UBLKCP) and mbarriers (SYNCS)
-    out = subprocess.check_output(["cuobjdump", "-sass", "-fun", "_ZN2kc11k1_hash_tmaEPKNS_9RegionDevEimPm",
-                                   kclib.LIB_PATH], text=True)
-    assert "UBLKCP" in out
-    assert "SYNCS" in out
+def _sass_of(lib_path, needle):
+    out = subprocess.check_output(["cuobjdump", "-sass", lib_path], text=True)
+    funcs, cur = {}, None
+    for line in out.splitlines():
+        if "Function :" in line:
+            cur = line.split("Function :")[1].strip()
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    return {k: "\n".join(v) for k, v in funcs.items() if needle in k}
+
+
+def test_k1_staging_instructions_in_sass(kclib):
+    # default K1 stages slices with cp.async (SASS LDGSTS); the TMA ring variant
+    # uses cp.async.bulk (UBLKCP) + mbarriers (SYNCS); both use the fast round
+    cp = _sass_of(kclib.LIB_PATH, "k1_hash_cpasync")
+    tma = _sass_of(kclib.LIB_PATH, "k1_hash_tma")
+    assert cp and all("LDGSTS" in s for s in cp.values())
+    assert tma and all("UBLKCP" in s and "SYNCS" in s for s in tma.values())
+    assert all("SHF.L.W" in s for s in cp.values())  # funnel-shift rotate of the XXH64 round
+
+
+def test_k2_uses_256bit_loads(kclib):
+    k2 = _sass_of(kclib.LIB_PATH, "k2_diff")
+    assert k2 and all(".256" in s for s in k2.values())
 
 
 def test_abi_version_and_status_strings(kclib):
