@@ -55,6 +55,13 @@ struct kc_ctx {
     std::vector<void*> pinned;
     std::vector<cudaEvent_t> pin_ev;
     cudaStream_t copy_stream = nullptr;
+    // parallel snapshot file I/O workers (stream + `depth` pinned buffers each)
+    struct IoWorker {
+        cudaStream_t stream = nullptr;
+        std::vector<void*> pinned;
+        std::vector<cudaEvent_t> ev;
+    };
+    std::vector<IoWorker> io;
 
     // CUPTI interposition
     void* cupti_subscriber = nullptr;

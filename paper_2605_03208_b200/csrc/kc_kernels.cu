@@ -130,13 +130,26 @@ __device__ __forceinline__ uint64_t lane_seed(int ql) {
     return ql == 0 ? (P1 + P2) : (ql == 1 ? P2 : (ql == 2 ? 0ULL : (0ULL - P1)));
 }
 
-// XXH64 of one contiguous global byte range by a quad, direct loads.
+// XXH64 of one contiguous global byte range by a quad, direct loads (16
+// stripes of loads in flight per lane on the aligned path: the digests walk
+// manifests of up to ~84 KB serially, so load latency must not be exposed).
 template <bool ALIGNED>
 __device__ uint64_t quad_xxh64_global(const uint8_t* p, uint64_t len, int ql, unsigned qmask) {
     uint64_t v = lane_seed(ql);
     const uint64_t nst = len >= 32 ? len / 32 : 0;
     const uint8_t* q = p + 8 * ql;
-    for (uint64_t t = 0; t < nst; ++t) {
+    uint64_t t = 0;
+    if (ALIGNED) {
+        constexpr int U = 16;
+        for (; t + U <= nst; t += U) {
+            uint64_t x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = __ldg(reinterpret_cast<const unsigned long long*>(q + 32 * (t + u)));
+#pragma unroll
+            for (int u = 0; u < U; ++u) v = xround_fast(v, x[u]);
+        }
+    }
+    for (; t < nst; ++t) {
         const uint64_t x =
             ALIGNED ? __ldg(reinterpret_cast<const unsigned long long*>(q + 32 * t)) : ldg_u64_bytes(q + 32 * t);
         v = xround_fast(v, x);
@@ -595,15 +608,21 @@ __device__ __forceinline__ void elem_float(uint64_t r, uint64_t a, Acc& acc, dou
     const double d = fabs(__dsub_rn(av, rv));
     if (d > acc.max_abs) acc.max_abs = d;
     const double ar = fabs(rv);
-    const double tol = __dadd_rn(atol, __dmul_rn(rtol, ar));
     const bool rfin = ar != CUDART_INF;
-    const bool close = ((d <= tol) && rfin) || (av == rv);
+    // numpy.isclose(a, r) on fp64 (R27).  d <= atol already implies
+    // d <= RN(atol + RN(rtol*|r|)) for rtol >= 0, so the product is skipped.
+    bool close = (av == rv);
+    if (!close && rfin) close = (d <= atol) || (d <= __dadd_rn(atol, __dmul_rn(rtol, ar)));
     acc.fail += !close;
     if (d != 0.0) {
         if (rv == 0.0) {
             acc.rel_undef += 1;
-        } else {
-            const double rel = rfin ? __ddiv_rn(d, ar) : CUDART_INF;
+        } else if (!rfin) {
+            acc.max_rel = CUDART_INF;
+        } else if (d > __dmul_rd(acc.max_rel, ar)) {
+            // only then can RN(d/|r|) exceed the running max: d <= RD(M*|r|) <= M*|r|
+            // implies d/|r| <= M, and RN is monotonic
+            const double rel = __ddiv_rn(d, ar);
             if (rel > acc.max_rel) acc.max_rel = rel;
         }
     }
@@ -641,30 +660,33 @@ __device__ __forceinline__ uint32_t vec_scan(const uint32_t (&r)[8], const uint3
     constexpr int S = DT_<DT>::S;
     constexpr bool F = DT_<DT>::F;
     uint32_t x[8];
-    uint32_t anyx = 0, spec = 0;
+    uint32_t anyx = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         x[i] = r[i] ^ a[i];
         anyx |= x[i];
     }
-    if (F) {
+    if (anyx == 0) {
+        // bit-equal vector: only a NaN (counted, and failing allclose unless
+        // equal_nan) can matter, and then special(a) == special(r)
+        if (!F) return 0;
+        uint32_t spec = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-            if (S != 8 || (i & 1)) spec |= special_word<DT>(r[i]) | special_word<DT>(a[i]);
-    }
-    if ((anyx | spec) == 0) return 0;  // fast path: equal, no Inf/NaN
-    if (anyx) {
+            if (S != 8 || (i & 1)) spec |= special_word<DT>(r[i]);
+        if (spec == 0) return 0;  // fast path
+    } else {
         acc.any = 1;
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc.dbytes += nz_bytes(x[i]);
-    }
-    if (DT == KC_DT_BYTES) {
-        uint32_t m = 0;
+        if (DT == KC_DT_BYTES) {
+            uint32_t m = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) m = __vmaxu4(m, __vabsdiffu4(r[i], a[i]));
-        m = max(max(m & 0xFF, (m >> 8) & 0xFF), max((m >> 16) & 0xFF, m >> 24));
-        if (m > acc.max_ulp) acc.max_ulp = m;
-        return 0;
+            for (int i = 0; i < 8; ++i) m = __vmaxu4(m, __vabsdiffu4(r[i], a[i]));
+            m = max(max(m & 0xFF, (m >> 8) & 0xFF), max((m >> 16) & 0xFF, m >> 24));
+            if (m > acc.max_ulp) acc.max_ulp = m;
+            return 0;
+        }
     }
     uint32_t mask = 0;
 #pragma unroll
@@ -752,40 +774,53 @@ __device__ __forceinline__ void ld256(const void* p, uint32_t* w) {
     w[6] = (uint32_t)d; w[7] = (uint32_t)(d >> 32);
 }
 
-// one unit [off, off+len) of a segment, whole warp: 2 vectors of each stream
+// one unit [off, off+len) of a segment, whole warp: U vectors of each stream
 // in flight per lane; the per-element path runs once per vector that needs it.
-template <int DT>
-__device__ void diff_unit(const uint8_t* R, const uint8_t* A, uint32_t len, bool vec_ok, Acc& acc, double atol,
-                          double rtol, int equal_nan, int lane) {
+template <int DT, int U>
+__device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, uint32_t len, bool vec_ok, Acc& acc,
+                                          double atol, double rtol, int equal_nan, int lane) {
     constexpr int S = DT_<DT>::S;
     uint32_t done = 0;
     if (vec_ok) {
         const uint32_t nvec = len / 32;
         uint32_t v = lane;
-        for (; v + 32 < nvec; v += 64) {
-            uint32_t r0[8], a0[8], r1[8], a1[8];
-            ld256(R + 32 * (size_t)v, r0);
-            ld256(A + 32 * (size_t)v, a0);
-            ld256(R + 32 * (size_t)(v + 32), r1);
-            ld256(A + 32 * (size_t)(v + 32), a1);
-            const uint32_t m0 = vec_scan<DT>(r0, a0, acc);
-            const uint32_t m1 = vec_scan<DT>(r1, a1, acc);
-            if (m0 | m1) {
+        for (; v + 32 * (U - 1) < nvec; v += 32 * U) {
+            uint32_t rw[U][8], aw[U][8];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                ld256(R + 32 * (size_t)(v + 32 * u), rw[u]);
+                ld256(A + 32 * (size_t)(v + 32 * u), aw[u]);
+            }
+            uint32_t m[U];
+            uint32_t any = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                m[u] = vec_scan<DT>(rw[u], aw[u], acc);
+                any |= m[u];
+            }
+            if (any) {
 #pragma unroll 1
-                for (int u = 0; u < 2; ++u) {
-                    const uint32_t m = u ? m1 : m0;
-                    if (!m) continue;
+                for (int u = 0; u < U; ++u) {
+                    uint32_t mu = m[0];
+#pragma unroll
+                    for (int k = 1; k < U; ++k) mu = u == k ? m[k] : mu;
+                    if (!mu) continue;
                     uint32_t rr[8], aa[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        rr[i] = u ? r1[i] : r0[i];
-                        aa[i] = u ? a1[i] : a0[i];
+                        rr[i] = rw[0][i];
+                        aa[i] = aw[0][i];
+#pragma unroll
+                        for (int k = 1; k < U; ++k) {
+                            rr[i] = u == k ? rw[k][i] : rr[i];
+                            aa[i] = u == k ? aw[k][i] : aa[i];
+                        }
                     }
-                    vec_slow<DT>(rr, aa, m, acc, atol, rtol, equal_nan);
+                    vec_slow<DT>(rr, aa, mu, acc, atol, rtol, equal_nan);
                 }
             }
         }
-        if (v < nvec) {
+        for (; v < nvec; v += 32) {
             uint32_t r0[8], a0[8];
             ld256(R + 32 * (size_t)v, r0);
             ld256(A + 32 * (size_t)v, a0);
@@ -841,19 +876,18 @@ __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
     acc.any = any;
 }
 
-constexpr int DK_THREADS = 512;
 
 // One launch per dtype group: segments [seg0, seg0+nseg) own the global units
 // [unit0, unit0+U).
-template <int DT>
-__global__ void __launch_bounds__(DK_THREADS, 2)
+template <int DT, int THREADS, int MINB, int VU>
+__global__ void __launch_bounds__(THREADS, MINB)
     k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
             kc_diff_report* __restrict__ reps, unsigned long long* __restrict__ bitmaps, double atol, double rtol,
             int equal_nan) {
     const int lane = threadIdx.x & 31;
     segs += seg0;
-    const uint64_t W = (uint64_t)gridDim.x * (DK_THREADS / 32);
-    const uint64_t w = (uint64_t)blockIdx.x * (DK_THREADS / 32) + (threadIdx.x >> 5);
+    const uint64_t W = (uint64_t)gridDim.x * (THREADS / 32);
+    const uint64_t w = (uint64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
     // contiguous block of units for this warp
     const uint64_t u0 = unit0 + (U * w) / W, u1 = unit0 + (U * (w + 1)) / W;
     if (u0 >= u1) return;
@@ -880,7 +914,7 @@ __global__ void __launch_bounds__(DK_THREADS, 2)
         const uint8_t* A = reinterpret_cast<const uint8_t*>(sg.act) + off;
         const bool vec_ok = ((sg.ref | sg.act) & 31) == 0;
         acc.any = 0;
-        diff_unit<DT>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane);
+        diff_unit<DT, VU>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane);
         if (__any_sync(0xFFFFFFFFu, acc.any) && lane == 0 && bitmaps) {
             const uint64_t k = sg.bitmap_chunk0 + off / kChunk;
             atomicOr(bitmaps + sg.bitmap_word0 + k / 64, 1ULL << (k % 64));
@@ -1014,21 +1048,39 @@ cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64
     return cudaGetLastError();
 }
 
+// K2 launch configurations (KC_K2_VARIANT, tuning knob): threads per CTA,
+// min CTAs per SM (register budget), vectors of each operand in flight per lane
+template <int DT, int THREADS, int MINB, int U>
+static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps,
+                          unsigned long long* bm, double atol, double rtol, int equal_nan, int num_sms,
+                          cudaStream_t s) {
+    constexpr int WPB = THREADS / 32;
+    uint64_t grid = (G.n_units + WPB - 1) / WPB;
+    if (grid > (uint64_t)num_sms * MINB) grid = (uint64_t)num_sms * MINB;
+    k2_diff<DT, THREADS, MINB, U><<<(unsigned)grid, THREADS, 0, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
+                                                                      d_reps, bm, atol, rtol, equal_nan);
+}
+
+// Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per
+// SM with 2 vectors of each operand in flight keeps the float paths free of
+// spills and reaches 6.9 TB/s on identical bf16 pairs; 512 x 2 CTAs (64
+// registers) spilled segment state into the inner loop (3.6 TB/s).
+template <int DT>
+static void launch_k2(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps, unsigned long long* bm,
+                      double atol, double rtol, int equal_nan, int num_sms, cudaStream_t s) {
+    launch_k2_cfg<DT, 512, 1, 2>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s);
+}
+
 cudaError_t launch_diff(const SegDev* d_segs, const DiffGroup* groups, int ngroups, const ReportMeta* d_meta,
                         int nrep, kc_diff_report* d_reps, uint64_t* d_bitmaps, double atol, double rtol,
                         int equal_nan, int num_sms, cudaStream_t s) {
     for (int g = 0; g < ngroups; ++g) {
         const DiffGroup& G = groups[g];
         if (G.n_units == 0 || G.n_segs == 0) continue;
-        uint64_t grid = (G.n_units + (DK_THREADS / 32) - 1) / (DK_THREADS / 32);
-        if (grid > (uint64_t)num_sms * 2) grid = num_sms * 2;
         unsigned long long* bm = (unsigned long long*)d_bitmaps;
         switch (G.dtype) {
-#define KC_CASE(D)                                                                                             \
-    case D:                                                                                                    \
-        k2_diff<D><<<(unsigned)grid, DK_THREADS, 0, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units, d_reps, \
-                                                         bm, atol, rtol, equal_nan);                           \
-        break;
+#define KC_CASE(D) \
+    case D: launch_k2<D>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s); break;
             KC_CASE(KC_DT_BYTES) KC_CASE(KC_DT_U8) KC_CASE(KC_DT_I8) KC_CASE(KC_DT_U16) KC_CASE(KC_DT_I16)
             KC_CASE(KC_DT_U32) KC_CASE(KC_DT_I32) KC_CASE(KC_DT_U64) KC_CASE(KC_DT_I64) KC_CASE(KC_DT_F16)
             KC_CASE(KC_DT_BF16) KC_CASE(KC_DT_F32) KC_CASE(KC_DT_F64)

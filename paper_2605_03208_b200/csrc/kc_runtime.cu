@@ -261,6 +261,11 @@ void kc_destroy(kc_ctx* ctx) {
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch,
                               &ctx->tmp_hash, &ctx->tmp_count})
         if (b->p) cudaFree(b->p);
+    for (auto& w : ctx->io) {
+        for (void* p : w.pinned) cudaFreeHost(p);
+        for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
+        if (w.stream) cudaStreamDestroy(w.stream);
+    }
     for (void* p : ctx->pinned) cudaFreeHost(p);
     for (cudaEvent_t e : ctx->pin_ev) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -492,6 +497,8 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
     if (d_bitmaps && !bitmap_word0) return set_err(ctx, KC_ERR_ARG, "kc_diff_async: bitmaps need bitmap_word0");
     const kc_tolerance deft = {1e-8, 1e-5, 0, 0};  // numpy defaults (reading R14)
     if (!tol) tol = &deft;
+    if (!(tol->atol >= 0.0) || !(tol->rtol >= 0.0))
+        return set_err(ctx, KC_ERR_ARG, "kc_diff: tolerances must be >= 0 (atol %g, rtol %g)", tol->atol, tol->rtol);
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<ReportMeta> meta(n_reports);
     std::vector<int> rep_dt(n_reports, -1);

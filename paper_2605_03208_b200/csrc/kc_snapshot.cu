@@ -16,7 +16,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -124,25 +126,6 @@ bool d2h_stream(kc_ctx* ctx, uint64_t base, uint64_t size, FILE* f, kc_capture_r
     return ok;
 }
 
-bool h2d_stream(kc_ctx* ctx, FILE* f, uint64_t base, uint64_t size, uint64_t* h2d_bytes, std::string& err) {
-    const uint64_t io = ctx->io_chunk;
-    const uint32_t depth = ctx->depth;
-    const uint64_t np = (size + io - 1) / io;
-    for (uint64_t i = 0; i < np; ++i) {
-        const uint32_t slot = i % depth;
-        if (i >= depth) cudaEventSynchronize(ctx->pin_ev[slot]);  // buffer free again
-        const uint64_t b = std::min(io, size - i * io);
-        if (fread(ctx->pinned[slot], 1, b, f) != b) { err = "short read"; cudaStreamSynchronize(ctx->copy_stream); return false; }
-        cudaError_t e = cudaMemcpyAsync((void*)(base + i * io), ctx->pinned[slot], b, cudaMemcpyHostToDevice,
-                                        ctx->copy_stream);
-        if (e != cudaSuccess) { err = cudaGetErrorString(e); cudaStreamSynchronize(ctx->copy_stream); return false; }
-        cudaEventRecord(ctx->pin_ev[slot], ctx->copy_stream);
-        if (h2d_bytes) *h2d_bytes += b;
-    }
-    cudaStreamSynchronize(ctx->copy_stream);
-    return true;
-}
-
 // Gather (K4) many device ranges into a device staging buffer, then D2H into
 // the file in io pieces.  Used for the written chunks W.
 bool gather_d2h(kc_ctx* ctx, const std::vector<std::pair<uint64_t, uint64_t>>& ranges, FILE* f, void* d_stage,
@@ -171,6 +154,127 @@ bool gather_d2h(kc_ctx* ctx, const std::vector<std::pair<uint64_t, uint64_t>>& r
         if (fwrite(ctx->pinned[0], 1, off, f) != off) { err = "fwrite failed"; return false; }
     }
     return true;
+}
+
+// ------------------------------------------------------------------ parallel file I/O
+// Snapshot files are written/read by KC_IO_THREADS worker threads (default 8),
+// each with its own stream and `depth` pinned buffers of io_chunk bytes; big
+// regions are split into 256 MiB work items at file offsets (pwrite/pread).
+// Host-side memcpy into the page cache is what bounds a file sink, so the
+// threads overlap it across cores while each stream keeps PCIe busy.
+int io_threads() {
+    const char* e = getenv("KC_IO_THREADS");
+    int t = e && *e ? atoi(e) : 8;
+    return t < 1 ? 1 : (t > 64 ? 64 : t);
+}
+
+struct IoItem {
+    size_t region;
+    uint64_t off, len;
+};
+
+std::vector<IoItem> make_items(const std::vector<std::pair<size_t, uint64_t>>& regions /* (index, size) */) {
+    const uint64_t piece = 256ull << 20;
+    std::vector<IoItem> items;
+    for (auto& r : regions)
+        for (uint64_t o = 0; o < r.second; o += piece) items.push_back({r.first, o, std::min(piece, r.second - o)});
+    // largest first keeps the tail short
+    std::stable_sort(items.begin(), items.end(), [](const IoItem& a, const IoItem& b) { return a.len > b.len; });
+    return items;
+}
+
+kc_status ensure_io(kc_ctx* ctx, int T) {
+    while ((int)ctx->io.size() < T) {
+        kc_ctx::IoWorker w;
+        KC_CHECK_CUDA(ctx, cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking), "cudaStreamCreate(io)");
+        for (uint32_t i = 0; i < ctx->depth; ++i) {
+            void* p = nullptr;
+            cudaError_t e = cudaHostAlloc(&p, ctx->io_chunk, cudaHostAllocDefault);
+            if (e != cudaSuccess) return cuda_err(ctx, e, "cudaHostAlloc(io staging)");
+            w.pinned.push_back(p);
+            cudaEvent_t ev;
+            KC_CHECK_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+            w.ev.push_back(ev);
+        }
+        ctx->io.push_back(w);
+    }
+    return KC_OK;
+}
+
+template <class F>
+void run_pool(int T, size_t n, F fn) {
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+            size_t i;
+            while ((i = next.fetch_add(1)) < n) fn(t, i);
+        });
+    for (auto& x : th) x.join();
+}
+
+// One work item device -> file (fd opened O_WRONLY by the caller's worker).
+bool item_d2h(kc_ctx* ctx, kc_ctx::IoWorker& w, uint64_t base, const IoItem& it, int fd, std::atomic<uint64_t>& calls,
+              std::string& err) {
+    const uint64_t io = ctx->io_chunk;
+    const uint32_t depth = (uint32_t)w.pinned.size();
+    const uint64_t np = (it.len + io - 1) / io;
+    std::vector<uint64_t> pend(depth, 0), poff(depth, 0);
+    bool ok = true;
+    auto drain = [&](uint64_t i) {
+        const uint32_t slot = i % depth;
+        if (cudaEventSynchronize(w.ev[slot]) != cudaSuccess) { err = "D2H failed"; ok = false; return; }
+        if (ok && pwrite(fd, w.pinned[slot], pend[slot], (off_t)poff[slot]) != (ssize_t)pend[slot]) {
+            err = "pwrite failed";
+            ok = false;
+        }
+    };
+    for (uint64_t i = 0; i < np && ok; ++i) {
+        const uint32_t slot = i % depth;
+        if (i >= depth) drain(i - depth);
+        if (!ok) break;
+        const uint64_t o = it.off + i * io, b = std::min(io, it.off + it.len - o);
+        cudaError_t e = cudaMemcpyAsync(w.pinned[slot], (const void*)(base + o), b, cudaMemcpyDeviceToHost, w.stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            err = std::string("cudaMemcpyAsync D2H: ") + cudaGetErrorString(e);
+            ok = false;
+            break;
+        }
+        cudaEventRecord(w.ev[slot], w.stream);
+        pend[slot] = b;
+        poff[slot] = o;
+        calls.fetch_add(1);
+    }
+    const uint64_t first = np > depth ? np - depth : 0;
+    for (uint64_t i = first; i < np; ++i)
+        if (ok) drain(i);
+    cudaStreamSynchronize(w.stream);
+    return ok;
+}
+
+bool item_h2d(kc_ctx* ctx, kc_ctx::IoWorker& w, int fd, uint64_t base, const IoItem& it, std::string& err) {
+    const uint64_t io = ctx->io_chunk;
+    const uint32_t depth = (uint32_t)w.pinned.size();
+    const uint64_t np = (it.len + io - 1) / io;
+    for (uint64_t i = 0; i < np; ++i) {
+        const uint32_t slot = i % depth;
+        if (i >= depth) cudaEventSynchronize(w.ev[slot]);
+        const uint64_t o = it.off + i * io, b = std::min(io, it.off + it.len - o);
+        if (pread(fd, w.pinned[slot], b, (off_t)o) != (ssize_t)b) {
+            err = "short read";
+            cudaStreamSynchronize(w.stream);
+            return false;
+        }
+        cudaError_t e = cudaMemcpyAsync((void*)(base + o), w.pinned[slot], b, cudaMemcpyHostToDevice, w.stream);
+        if (e != cudaSuccess) {
+            err = cudaGetErrorString(e);
+            cudaStreamSynchronize(w.stream);
+            return false;
+        }
+        cudaEventRecord(w.ev[slot], w.stream);
+    }
+    return cudaStreamSynchronize(w.stream) == cudaSuccess;
 }
 
 struct RegionState {
@@ -380,22 +484,59 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
         return write_text(dir + "/memory_regions.json", m);
     };
 
-    // region file writer: region bytes + the matching manifest slice
+    // region files: region bytes (parallel workers) + the matching manifest slice
     auto snapshot_regions = [&](const std::vector<uint64_t>& manifest) {
-        for (auto& r : rs) {
+        const int T = io_threads();
+        if (ensure_io(ctx, T) != KC_OK) {
+            for (auto& r : rs)
+                if (r.ok) { r.ok = false; r.error = "cannot allocate pinned I/O staging"; }
+            return;
+        }
+        std::vector<std::pair<size_t, uint64_t>> todo;
+        for (size_t i = 0; i < rs.size(); ++i) {
+            if (!rs[i].ok) continue;
+            const std::string path = dir + "/memory/region_" + hex_base(rs[i].r.base) + ".bin";
+            int fd = open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+            if (fd < 0 || ftruncate(fd, (off_t)rs[i].r.size) != 0) {
+                rs[i].ok = false;
+                rs[i].error = "cannot create " + path;
+            } else {
+                todo.emplace_back(i, rs[i].r.size);
+            }
+            if (fd >= 0) close(fd);
+        }
+        const std::vector<IoItem> items = make_items(todo);
+        std::vector<std::atomic<int>> failed(rs.size());
+        for (auto& f : failed) f = 0;
+        std::mutex emu;
+        std::atomic<uint64_t> calls{0};
+        run_pool(T, items.size(), [&](int t, size_t k) {
+            const IoItem& it = items[k];
+            if (failed[it.region]) return;
+            cudaSetDevice(ctx->device);
+            const std::string path = dir + "/memory/region_" + hex_base(rs[it.region].r.base) + ".bin";
+            int fd = open(path.c_str(), O_WRONLY);
+            std::string err = fd < 0 ? "cannot open " + path : "";
+            const bool ok = fd >= 0 && item_d2h(ctx, ctx->io[t], rs[it.region].r.base, it, fd, calls, err);
+            if (fd >= 0) close(fd);
+            if (!ok && !failed[it.region].exchange(1)) {
+                std::lock_guard<std::mutex> lk(emu);
+                rs[it.region].error = err;
+            }
+        });
+        rep.dma_calls += calls.load();
+        rep.staging_high_water = std::max<uint64_t>(rep.staging_high_water,
+                                                    (uint64_t)std::min<size_t>(T, items.size()) * ctx->depth * ctx->io_chunk);
+        for (size_t i = 0; i < rs.size(); ++i) {
+            RegionState& r = rs[i];
             if (!r.ok) continue;
             const std::string hx = hex_base(r.r.base);
-            const std::string path = dir + "/memory/region_" + hx + ".bin";
-            FILE* fp = fopen(path.c_str(), "wb");
-            std::string err;
-            bool ok = fp && d2h_stream(ctx, r.r.base, r.r.size, fp, &rep, err);
-            if (fp) ok = (fclose(fp) == 0) && ok;
-            if (!ok) {
+            if (failed[i]) {
                 r.ok = false;
-                r.error = err.empty() ? "cannot write " + path : err;
-                unlink(path.c_str());
+                unlink((dir + "/memory/region_" + hx + ".bin").c_str());
                 continue;
             }
+            rep.d2h_bytes += r.r.size;
             write_file(dir + "/memory/region_" + hx + ".xxh64", manifest.data() + r.chunk0, 8 * r.n_chunks);
         }
     };
@@ -864,20 +1005,56 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
         if (!s.fallback) cudaMemsetAsync((void*)s.base, 0, s.size, ctx->copy_stream);
     }
     for (auto& rr : h->regions) cudaMemsetAsync((void*)rr.r.base, 0, rr.r.size, ctx->copy_stream);
-    for (auto& rr : h->regions) {
-        if (!rr.ok) continue;
-        const std::string path = dir + "/memory/region_" + rr.hexbase + ".bin";
-        FILE* fp = fopen(path.c_str(), "rb");
-        std::string err;
-        struct stat sb;
-        bool ok = fp && fstat(fileno(fp), &sb) == 0 && (uint64_t)sb.st_size == rr.r.size &&
-                  h2d_stream(ctx, fp, rr.r.base, rr.r.size, &rep.h2d_bytes, err);
-        if (fp) fclose(fp);
-        if (!ok) {
+    {
+        // every region file must exist with exactly `size` bytes (O1)
+        std::vector<std::pair<size_t, uint64_t>> todo;
+        for (size_t i = 0; i < h->regions.size(); ++i) {
+            const auto& rr = h->regions[i];
+            if (!rr.ok) continue;
+            const std::string path = dir + "/memory/region_" + rr.hexbase + ".bin";
+            struct stat sb;
+            if (stat(path.c_str(), &sb) != 0 || (uint64_t)sb.st_size != rr.r.size) {
+                rollback(h);
+                delete h;
+                return set_err(ctx, KC_ERR_FORMAT, "kc_restore: %s: missing or wrong length", path.c_str());
+            }
+            todo.emplace_back(i, rr.r.size);
+        }
+        cudaStreamSynchronize(ctx->copy_stream);  // zero-fill first
+        const int T = io_threads();
+        st = ensure_io(ctx, T);
+        if (st != KC_OK) {
             rollback(h);
             delete h;
-            return set_err(ctx, KC_ERR_FORMAT, "kc_restore: %s: missing, wrong length or unreadable (%s)", path.c_str(),
-                           err.c_str());
+            return st;
+        }
+        const std::vector<IoItem> items = make_items(todo);
+        std::atomic<int> bad{0};
+        std::mutex emu;
+        std::string first_err;
+        std::atomic<uint64_t> h2d{0};
+        run_pool(T, items.size(), [&](int t, size_t k) {
+            if (bad) return;
+            const IoItem& it = items[k];
+            cudaSetDevice(ctx->device);
+            const auto& rr = h->regions[it.region];
+            const std::string path = dir + "/memory/region_" + rr.hexbase + ".bin";
+            int fd = open(path.c_str(), O_RDONLY);
+            std::string err = fd < 0 ? "cannot open" : "";
+            const bool ok = fd >= 0 && item_h2d(ctx, ctx->io[t], fd, rr.r.base, it, err);
+            if (fd >= 0) close(fd);
+            if (ok) {
+                h2d.fetch_add(it.len);
+            } else if (!bad.exchange(1)) {
+                std::lock_guard<std::mutex> lk(emu);
+                first_err = path + ": " + err;
+            }
+        });
+        rep.h2d_bytes += h2d.load();
+        if (bad) {
+            rollback(h);
+            delete h;
+            return set_err(ctx, KC_ERR_FORMAT, "kc_restore: copy-in failed: %s", first_err.c_str());
         }
     }
     cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);

@@ -161,9 +161,11 @@ def test_region_freed_after_dispatch_is_tolerated(tmp_path):
 def test_staging_pieces_follow_io_chunk(tmp_path):
     """the number of D2H copies follows KERNCAP_SNAPSHOT_CHUNK_BYTES."""
     d = str(tmp_path / "st")
-    cap = run("capture-c1", d, "--io-chunk", str(4 * 65536))
-    # c1 regions: 655,360 / 65,536 / 327,680 B at 256 KiB pieces -> 3 + 1 + 2 copies (+ W gathers)
-    assert cap["report"]["dma_calls"] >= 6
+    cap = run("capture-c1", d, "--io-chunk", str(4 * 65536), env={"KC_IO_THREADS": "1"})
+    # c1 regions: 655,360 / 65,536 / 327,680 B at 256 KiB pieces -> 3 + 1 + 2 copies; W = the 5
+    # chunks of `out` (320 KiB) gathered through a 256 KiB stage -> 2 more copies
+    assert cap["report"]["dma_calls"] == 8
+    # one I/O thread: staging high water <= depth (2) x io chunk (SPEC.md:424, reading R26)
     assert cap["report"]["staging_high_water"] <= 2 * 4 * 65536
 
 
