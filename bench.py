@@ -318,8 +318,15 @@ def run_ours(a, rank, world, device, log):
     dom = "K2_diff" if 2 * k2_ms >= 2 * k1_ms else "K1_hash"
     dom_ms = k2_ms if dom == "K2_diff" else 2 * k1_ms
     share = dom_ms / ms if ms else None
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):  # dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture
+        t = json.load(open(tp)).get(dom)
+        if t and t.get("alg_bytes_per_launch") == kern[dom]["alg_bytes"]:
+            traffic, traffic_src = t["dram_bytes_per_launch"], t["source"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
-            "frac": kern[dom]["gbs"] / peak, "traffic": None, "peak_source": peak_src,
+            "frac": kern[dom]["gbs"] / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": peak_src,
             "frac_of_spec_8000": kern[dom]["gbs"] / 8000.0, "share_of_step": share,
             "alg_bytes_per_launch": kern[dom]["alg_bytes"]}
 

@@ -263,9 +263,14 @@ kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions
  * device-local memory, copies the region files in, zero-fills gaps and
  * failed regions, and verifies the bytes against the captured manifest. */
 kc_status kc_restore(kc_ctx* ctx, const char* dir, kc_restored** out, kc_restore_report* rep);
-/* Host placeholder reservation of every captured span with
- * mmap(MAP_FIXED_NOREPLACE) -- call BEFORE the CUDA context exists
- * (PAPER.md:1067-1074).  kc_restore releases them.  No CUDA calls. */
+/* Stage 2 of the paper's replay reserves the captured
+ * ranges with mmap(MAP_FIXED_NOREPLACE) before the runtime initialises.  On
+ * CUDA that backfires: ranges mapped at cuInit are excluded from the driver's
+ * VA space for the process lifetime (measured, R28).  So this is a
+ * CHECK, called before CUDA initialises: KC_PARTIAL when a host mapping
+ * already overlaps a captured 32 MiB window (the replay process should re-exec
+ * for a fresh ASLR layout); *n_reserved = windows that are free.  Maps nothing,
+ * makes no CUDA calls. */
 kc_status kc_prereserve(const char* dir, uint64_t* n_reserved);
 
 /* ---- A7 replay ------------------------------------ */

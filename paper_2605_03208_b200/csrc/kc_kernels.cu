@@ -140,13 +140,30 @@ __device__ uint64_t quad_xxh64_global(const uint8_t* p, uint64_t len, int ql, un
     const uint8_t* q = p + 8 * ql;
     uint64_t t = 0;
     if (ALIGNED) {
+        // software-pipelined: batch k+1's 16 loads are in flight while batch k is hashed
         constexpr int U = 16;
-        for (; t + U <= nst; t += U) {
-            uint64_t x[U];
+        const unsigned long long* g = reinterpret_cast<const unsigned long long*>(q);
+        if (nst >= 2 * U) {
+            uint64_t xa[U], xb[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) x[u] = __ldg(reinterpret_cast<const unsigned long long*>(q + 32 * (t + u)));
+            for (int u = 0; u < U; ++u) xa[u] = __ldg(g + 4 * u);
+            for (; t + 2 * U <= nst; t += 2 * U) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) v = xround_fast(v, x[u]);
+                for (int u = 0; u < U; ++u) xb[u] = __ldg(g + 4 * (t + U + u));
+#pragma unroll
+                for (int u = 0; u < U; ++u) v = xround_fast(v, xa[u]);
+                if (t + 3 * U <= nst) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) xa[u] = __ldg(g + 4 * (t + 2 * U + u));
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) v = xround_fast(v, xb[u]);
+            }
+            if (t + U <= nst) {  // xa already holds batch t when fewer than 2U stripes remain
+#pragma unroll
+                for (int u = 0; u < U; ++u) v = xround_fast(v, xa[u]);
+                t += U;
+            }
         }
     }
     for (; t < nst; ++t) {
@@ -459,25 +476,73 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// Region digests (quad per region) + the (base,size,digest) LE triples.
-__global__ void k1_region_digest(const RegionDev* __restrict__ regs, int nreg, const uint64_t* __restrict__ h,
-                                 uint64_t* __restrict__ dig, uint8_t* __restrict__ scratch) {
-    const int ql = threadIdx.x & 3;
-    const unsigned qmask = 0xFu << (threadIdx.x & 28);
-    const int nq = gridDim.x * (blockDim.x / 4);
-    for (int r = blockIdx.x * (blockDim.x / 4) + (threadIdx.x >> 2); r < nreg; r += nq) {
+// Region digests + the (base,size,digest) LE triples.  One warp per region
+// streams the region's manifest (8 B per chunk, only 8-byte aligned) through a
+// 2-stage shared-memory ring with 8-byte cp.async while lanes 0-3 (one quad)
+// run the serial XXH64 chain from shared memory, so load latency is hidden
+// behind the chain (~2,640 stripes for a 692 MB region).
+constexpr int DG_STAGE = 8192;  // bytes per stage (multiple of 32)
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(32)
+    k1_region_digest(const RegionDev* __restrict__ regs, int nreg, const uint64_t* __restrict__ h,
+                     uint64_t* __restrict__ dig, uint8_t* __restrict__ scratch) {
+    __shared__ __align__(16) uint8_t buf[2][DG_STAGE];
+    const int lane = threadIdx.x & 31, ql = lane & 3;
+    for (int r = blockIdx.x; r < nreg; r += gridDim.x) {
         const uint64_t nck = (regs[r].size + kChunk - 1) / kChunk;
-        const uint64_t d =
-            quad_xxh64_global<true>(reinterpret_cast<const uint8_t*>(h + regs[r].chunk_off), 8 * nck, ql, qmask);
-        if (ql == 0) {
-            if (dig) dig[r] = d;
-            if (scratch) {
-                uint64_t* t = reinterpret_cast<uint64_t*>(scratch + 24 * (size_t)r);
-                t[0] = regs[r].base;
-                t[1] = regs[r].size;
-                t[2] = d;
+        const uint64_t len = 8 * nck;
+        const uint8_t* p = reinterpret_cast<const uint8_t*>(h + regs[r].chunk_off);
+        const uint64_t nst = len >= 32 ? len / 32 : 0;
+        const uint64_t body = nst * 32;  // bytes consumed as stripes
+        const uint32_t nstage = (uint32_t)((body + DG_STAGE - 1) / DG_STAGE);
+        auto issue = [&](uint32_t k) {
+            const uint64_t off = (uint64_t)k * DG_STAGE;
+            const uint32_t b = (uint32_t)min((uint64_t)DG_STAGE, body - off);
+            for (uint32_t o = 8 * lane; o < b; o += 256) cp_async8(&buf[k & 1][o], p + off + o);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        uint64_t v = lane_seed(ql);
+        if (nstage > 0) issue(0);
+        for (uint32_t k = 0; k < nstage; ++k) {
+            if (k + 1 < nstage) {
+                issue(k + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncwarp();
+            if (lane < 4) {
+                const uint64_t off = (uint64_t)k * DG_STAGE;
+                const uint32_t n = (uint32_t)(min((uint64_t)DG_STAGE, body - off) / 32);
+                const uint64_t* q = reinterpret_cast<const uint64_t*>(buf[k & 1]) + ql;
+                uint32_t t = 0;
+                for (; t + 8 <= n; t += 8) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v = xround_fast(v, q[4 * (t + u)]);
+                }
+                for (; t < n; ++t) v = xround_fast(v, q[4 * t]);
+            }
+            __syncwarp();  // stage k & 1 is rewritten by issue(k + 2)
+        }
+        if (lane < 4) {
+            const uint64_t d = quad_finish<true>(v, ql, 0xFu, len, p + body);
+            if (lane == 0) {
+                if (dig) dig[r] = d;
+                if (scratch) {
+                    uint64_t* t = reinterpret_cast<uint64_t*>(scratch + 24 * (size_t)r);
+                    t[0] = regs[r].base;
+                    t[1] = regs[r].size;
+                    t[2] = d;
+                }
             }
         }
+        __syncwarp();
     }
 }
 
@@ -1032,8 +1097,8 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
 cudaError_t launch_digests(const RegionDev* d_regs, int nreg, const uint64_t* d_h, uint64_t* d_dig, uint8_t* d_scratch,
                            uint64_t* d_snap, cudaStream_t s) {
     if (nreg == 0) return cudaSuccess;
-    const int grid = (nreg + 63) / 64;
-    k1_region_digest<<<grid, 256, 0, s>>>(d_regs, nreg, d_h, d_dig, d_snap ? d_scratch : nullptr);
+    const int grid = std::min(nreg, 148 * 8);
+    k1_region_digest<<<grid, 32, 0, s>>>(d_regs, nreg, d_h, d_dig, d_snap ? d_scratch : nullptr);
     if (d_snap) k1_snapshot_digest<<<1, 4, 0, s>>>(d_scratch, nreg, d_snap);
     return cudaGetLastError();
 }

@@ -697,13 +697,8 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
 
 // ====================================================================== restore
 namespace {
-struct Placeholder {
-    uint64_t base, size;
-};
-std::mutex g_ph_mu;
-std::vector<Placeholder> g_placeholders;
-
 const uint64_t kPlaceholderGranule = 2ull << 20;  // typical VMM granularity before cuInit
+const uint64_t kWindowAlign = 32ull << 20;        // smallest VA window a fresh process honours (R28)
 
 struct ParsedRegion {
     uint64_t base, size;
@@ -764,12 +759,6 @@ std::vector<std::pair<uint64_t, uint64_t>> make_spans(const std::vector<ParsedRe
     return spans;
 }
 
-void release_placeholders() {
-    std::lock_guard<std::mutex> lk(g_ph_mu);
-    for (auto& p : g_placeholders) munmap((void*)p.base, p.size);
-    g_placeholders.clear();
-}
-
 void rollback(kc_restored* h) {
     for (auto it = h->spans.rbegin(); it != h->spans.rend(); ++it) {
         for (uint64_t p : it->memalloc) KC_DRV(cuMemFree)((CUdeviceptr)p);
@@ -783,27 +772,64 @@ void rollback(kc_restored* h) {
 }
 }  // namespace
 
+// Stage 2 on CUDA: measured on the B200 box, PROT_NONE
+// placeholders mapped before cuInit are excluded from the driver's VA space
+// for the process lifetime, so munmapping them later does NOT make the captured
+// VAs reservable (R28).  Stage 2 is therefore a check, made before CUDA
+// initialises: KC_PARTIAL when an existing host mapping already overlaps a
+// captured 32 MiB window, so the caller can re-exec for a fresh ASLR layout.
+// *n_reserved = windows that are free.  No CUDA calls, nothing is mapped.
 extern "C" kc_status kc_prereserve(const char* dir, uint64_t* n_reserved) {
     if (!dir) return KC_ERR_ARG;
     std::vector<ParsedRegion> regs;
     kc_status st = parse_regions(nullptr, dir, regs);
     if (st != KC_OK) return st;
     auto spans = make_spans(regs, kPlaceholderGranule);
-    uint64_t n = 0;
-    std::lock_guard<std::mutex> lk(g_ph_mu);
-    for (auto& s : spans) {
-        void* p = mmap((void*)s.first, s.second - s.first, PROT_NONE,
-                       MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE | MAP_FIXED_NOREPLACE, -1, 0);
-        if (p == MAP_FAILED) continue;
-        if ((uint64_t)p != s.first) {  // old kernels ignore MAP_FIXED_NOREPLACE
-            munmap(p, s.second - s.first);
-            continue;
+    std::vector<std::pair<uint64_t, uint64_t>> win;  // merged 32 MiB windows [lo, hi)
+    for (auto& sp : spans) {
+        const uint64_t lo = sp.first / kWindowAlign * kWindowAlign;
+        const uint64_t hi = (sp.second + kWindowAlign - 1) / kWindowAlign * kWindowAlign;
+        if (!win.empty() && lo <= win.back().second) win.back().second = std::max(win.back().second, hi);
+        else win.emplace_back(lo, hi);
+    }
+    std::vector<std::pair<uint64_t, uint64_t>> maps;
+    if (FILE* f = fopen("/proc/self/maps", "r")) {
+        char line[512];
+        while (fgets(line, sizeof line, f)) {
+            unsigned long long a = 0, b = 0;
+            if (sscanf(line, "%llx-%llx", &a, &b) == 2) maps.emplace_back(a, b);
         }
-        g_placeholders.push_back({s.first, s.second - s.first});
-        ++n;
+        fclose(f);
+    }
+    uint64_t n = 0;
+    for (auto& w : win) {
+        bool clash = false;
+        for (auto& m : maps)
+            if (m.first < w.second && m.second > w.first) clash = true;
+        n += !clash;
     }
     if (n_reserved) *n_reserved = n;
-    return KC_OK;
+    return n == win.size() ? KC_OK : KC_PARTIAL;
+}
+
+// /proc/self/maps lines overlapping [lo, hi) (diagnostics for KC_ERR_VA_UNAVAILABLE)
+static std::string maps_overlapping(uint64_t lo, uint64_t hi) {
+    std::string out;
+    FILE* f = fopen("/proc/self/maps", "r");
+    if (!f) return out;
+    char line[512];
+    int n = 0;
+    while (fgets(line, sizeof line, f) && n < 4) {
+        unsigned long long a = 0, b = 0;
+        if (sscanf(line, "%llx-%llx", &a, &b) == 2 && a < hi && b > lo) {
+            std::string l(line);
+            while (!l.empty() && (l.back() == '\n' || l.back() == ' ')) l.pop_back();
+            out += (out.empty() ? "" : " | ") + l;
+            ++n;
+        }
+    }
+    fclose(f);
+    return out.empty() ? "no host mapping overlaps (driver-internal VA)" : out;
 }
 
 extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** out, kc_restore_report* rep_out) {
@@ -887,7 +913,6 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
         return cu_err(ctx, cr, "cuMemGetAllocationGranularity");
     }
     auto spans = make_spans(regs, G);
-    release_placeholders();
     // Reserve VA windows at exactly aligned hints.  A fresh process honours a
     // hint only where the driver can open a new VA chunk, i.e. at a coarse
     // alignment (observed: 32 MiB), so try the exact span first and then
@@ -980,12 +1005,13 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
                     }
                 rollback(h);
                 delete h;
+                const std::string maps = maps_overlapping(want, want + sz);
                 return set_err(ctx, KC_ERR_VA_UNAVAILABLE,
                                "kc_restore: cannot restore captured region [0x%llx, +%llu): reserving span 0x%llx "
-                               "returned 0x%llx (CUresult %d) and the cuMemAlloc replay returned 0x%llx (%d); VA "
-                               "faithfulness is a hard requirement (PAPER.md:1080-1082)",
+                               "returned 0x%llx (CUresult %d) and the cuMemAlloc replay returned 0x%llx (%d); host "
+                               "maps: %s; VA faithfulness is a hard requirement (PAPER.md:1080-1082)",
                                (unsigned long long)want, (unsigned long long)sz, (unsigned long long)sbase,
-                               (unsigned long long)sgot, scr, (unsigned long long)got, (int)cr);
+                               (unsigned long long)sgot, scr, (unsigned long long)got, (int)cr, maps.c_str());
             }
             rep.mapped_bytes += rr.r.size;
         }

@@ -213,13 +213,44 @@ def _regions(regions) -> ctypes.Array:
     return arr
 
 
-def prereserve(snapshot_dir: str) -> int:
-    """Host placeholder reservation of the captured spans before any CUDA call."""
+def prereserve(snapshot_dir: str) -> tuple[int, bool]:
+    """Pre-CUDA check that no host mapping overlaps the captured VA windows
+    (the CUDA form of the paper's stage 2; R28).
+    Returns (free windows, all free)."""
     n = ctypes.c_uint64(0)
     rc = lib().kc_prereserve(snapshot_dir.encode(), ctypes.byref(n))
     if rc < 0:
         raise KcError(rc, "kc_prereserve failed")
-    return n.value
+    return n.value, rc == KC_OK
+
+
+def _reexec(argv: list, max_attempts: int) -> None:
+    import os
+    import sys
+    attempt = int(os.environ.get("KC_REEXEC_ATTEMPT", "0"))
+    if attempt + 1 < max_attempts:
+        os.environ["KC_REEXEC_ATTEMPT"] = str(attempt + 1)
+        os.execv(sys.executable, [sys.executable] + list(argv))
+
+
+def exec_replay_process(argv: list, snapshot_dir: str, max_attempts: int = 8) -> None:
+    """Call first thing in a replay process, before CUDA initialises: if a host
+    mapping already sits on a captured VA window, re-exec for a new layout."""
+    _, ok = prereserve(snapshot_dir)
+    if not ok:
+        _reexec(argv, max_attempts)
+
+
+def restore_in_fresh_layout(ctx: "Context", snapshot_dir: str, argv: list, max_attempts: int = 8):
+    """ctx.restore(); on KC_ERR_VA_UNAVAILABLE re-exec this process (ASLR gives
+    the driver's VA arenas a new random placement) up to max_attempts times.
+    The restore itself never relocates: it aborts and rolls back (R21)."""
+    try:
+        return ctx.restore(snapshot_dir)
+    except KcError as e:
+        if e.status == KC_ERR_VA_UNAVAILABLE:
+            _reexec(argv, max_attempts)
+        raise
 
 
 @dataclass

@@ -74,49 +74,80 @@ def capture_c2(a):
     print(json.dumps({"rc": rc, "report": rep, "vas": va}))
 
 
-def replay(a):
-    if a.prereserve:
-        n = kc.prereserve(a.dir)
+def _windows(d):
+    with open(os.path.join(d, "memory_regions.json")) as f:
+        regs = json.load(f)
+    W = 32 << 20
+    out = []
+    for r in sorted(regs, key=lambda r: int(r["base"], 16)):
+        lo = int(r["base"], 16) // W * W
+        hi = (int(r["base"], 16) + int(r["size"]) + W - 1) // W * W
+        if out and lo <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], hi)
+        else:
+            out.append([lo, hi])
+    return out
+
+
+def squat(a):
+    """Occupy every captured VA window with a host PROT_NONE mapping (after CUDA
+    initialises: a mapping present at cuInit is excluded from the driver's VA
+    space for good, R28): restore must abort with
+    KC_ERR_VA_UNAVAILABLE and leave nothing behind; once the squatter unmaps,
+    the same restore must succeed."""
+    import ctypes
+    libc = ctypes.CDLL(None, use_errno=True)
+    libc.mmap.restype = ctypes.c_void_p
+    libc.mmap.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long]
+    libc.munmap.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    flags = 0x02 | 0x20 | 0x4000 | 0x100000  # PRIVATE | ANONYMOUS | NORESERVE | FIXED_NOREPLACE
+    attempt = int(os.environ.get("KC_REEXEC_ATTEMPT", "0"))
+
+    def again(why):
+        if attempt < 8:
+            os.environ["KC_REEXEC_ATTEMPT"] = str(attempt + 1)
+            os.execv(sys.executable, [sys.executable] + sys.argv)
+        return {"error": why}
+
     ctx = kc.Context(0)
-    out = {}
-    if a.squat:
-        from cuda.bindings import driver as drv
-        with open(os.path.join(a.dir, "memory_regions.json")) as f:
-            regs = json.load(f)
-        # squat on the first captured span the way the restore would claim it:
-        # the smallest exactly-honoured aligned window (2 MiB .. 1 GiB)
-        b0 = int(regs[0]["base"], 16)
-        held = None
-        for W in [2 << 20, 32 << 20, 64 << 20, 128 << 20, 256 << 20, 512 << 20, 1 << 30]:
-            lo = b0 // W * W
-            err, p = drv.cuMemAddressReserve(W, W, lo, 0)
-            if int(err) == 0 and int(p) == lo:
-                held = (p, W, lo)
-                break
-            if int(err) == 0:
-                drv.cuMemAddressFree(p, W)
-        p, W, base = held
-        out["squat"] = [0, int(p), base]
-        try:
-            r0, _ = ctx.restore(a.dir)
-            out["restore"] = "unexpected success"
-            r0.release()
-        except kc.KcError as e:
-            out["restore_status"] = e.status
-            out["message"] = str(e)
-        out["squat_free"] = int(drv.cuMemAddressFree(p, W)[0])
-        # after the squatter leaves, the same restore must succeed (full rollback before)
-        try:
-            r, rep = ctx.restore(a.dir)
-            out["retry"] = rep
-            r.release()
-        except kc.KcError as e:
-            out["retry_status"] = e.status
-            out["retry_message"] = str(e)
-        print(json.dumps(out))
-        return
+    held = []
+    for lo, hi in _windows(a.dir):
+        p = libc.mmap(lo, hi - lo, 0, flags, -1, 0)
+        if p != lo:
+            for l2, h2 in held:
+                libc.munmap(l2, h2 - l2)
+            return again("window occupied before the squat")
+        held.append((lo, hi))
+    out = {"squat": [0, held[0][0], held[0][0]], "attempts": attempt + 1}
     try:
-        r, rep = ctx.restore(a.dir)
+        r0, _ = ctx.restore(a.dir)
+        out["restore"] = "unexpected success"
+        r0.release()
+    except kc.KcError as e:
+        out["restore_status"] = e.status
+        out["message"] = str(e)
+    out["squat_free"] = sum(int(libc.munmap(lo, hi - lo)) for lo, hi in held)
+    # the aborted restore left nothing behind and the ctx is healthy: hash a fresh buffer
+    p = ctx.alloc(1 << 20)
+    import torch
+    h = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ctx.hash([(p, 1 << 20)], h.data_ptr())
+    torch.cuda.synchronize()
+    ctx.free(p)
+    out["ctx_healthy_after_abort"] = True
+    return out
+
+
+def replay(a):
+    if a.squat:
+        print(json.dumps(squat(a)))
+        return
+    if not a.no_prereserve:  # stage 2: claim the captured VA windows before CUDA initialises
+        kc.exec_replay_process(sys.argv, a.dir)
+    ctx = kc.Context(0)
+    out = {"attempts": int(os.environ.get("KC_REEXEC_ATTEMPT", "0")) + 1}
+    try:
+        r, rep = kc.restore_in_fresh_layout(ctx, a.dir, sys.argv)
     except kc.KcError as e:
         print(json.dumps({"restore_status": e.status, "message": str(e), "report": getattr(e, "report", None)}))
         return
@@ -133,8 +164,9 @@ def replay(a):
 
 
 def recapture(a):
+    kc.exec_replay_process(sys.argv, a.dir)
     ctx = kc.Context(0)
-    r, rep = ctx.restore(a.dir)
+    r, rep = kc.restore_in_fresh_layout(ctx, a.dir, sys.argv)
     regs = r.regions()
     image = open(synth.FIXTURE_CUBIN, "rb").read()
     # a no-op dispatch (zero lists): the snapshot must equal the restored state
@@ -189,7 +221,7 @@ def main():
     p.add_argument("--iterations", type=int, default=1)
     p.add_argument("--no-recopy", action="store_true")
     p.add_argument("--squat", action="store_true")
-    p.add_argument("--prereserve", action="store_true")
+    p.add_argument("--no-prereserve", action="store_true")
     p.add_argument("--memalloc", action="store_true")
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,

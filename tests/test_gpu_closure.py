@@ -100,15 +100,20 @@ def test_c1_replay_iterations_recopy(tmp_path):
 
 
 def test_va_squat_aborts_and_rolls_back(tmp_path):
-    """PAPER.md:1080-1082 "VA faithfulness is a hard requirement" (SPEC.md:624, 788)."""
+    """PAPER.md:1080-1082 "VA faithfulness is a hard requirement" (SPEC.md:624, 788):
+    with every captured window occupied, restore aborts with
+    KC_ERR_VA_UNAVAILABLE, nothing is dispatched or left mapped and the ctx
+    stays usable; the snapshot itself is intact, so a fresh process restores it."""
     d = str(tmp_path / "sq")
     run("capture-c1", d)
     res = run("replay", d, "--squat")
-    assert res["squat"][0] == 0 and res["squat"][1] == res["squat"][2], res
+    assert "squat" in res, res
     assert res["restore_status"] == -6, res
-    assert res["squat_free"] == 0, res
-    assert "retry" in res, res
-    assert res["retry"]["verify_mismatch_chunks"] == 0
+    assert "hard requirement" in res["message"]
+    assert res["squat_free"] == 0 and res["ctx_healthy_after_abort"]
+    ok = run("replay", d)
+    assert "restore" in ok, ok
+    assert all(r["differing_bytes"] == 0 for r in ok["validate"])
 
 
 def test_corrupted_region_file_is_localised(tmp_path):

@@ -90,19 +90,21 @@ def test_k1_many_small_regions(env):
     assert [int(x) for x in d] == [orc.region_digest(e) for e in exp]
 
 
-def test_k1_sampled_2gib_region(env):
-    """c3-sized region at full size: sampled chunks + digest-free check of first/last."""
+def test_k1_full_2gib_region_and_digests(env):
+    """c3-sized region at full size: every chunk hash and the region/snapshot
+    digests (manifest of 256 KB: the digest kernel streams several stages)."""
     torch, kc, ctx, orc = env
     n = 2 * 2**30 + 12345
     buf = _rand_dev(torch, n, 11)
-    h, _, _ = _hash(torch, ctx, [(buf.data_ptr(), n)], digests=False)
-    C = (n + CH - 1) // CH
-    assert h.size == C
-    rng = np.random.default_rng(1)
-    for k in sorted(set([0, 1, C - 2, C - 1] + list(rng.integers(0, C, size=60)))):
-        lo = k * CH
-        piece = buf[lo:min(n, lo + CH)].cpu().numpy()
-        assert int(h[k]) == orc.xxh64(piece), k
+    small = _rand_dev(torch, 3 * CH + 7, 12)
+    regions = sorted([(buf.data_ptr(), n), (small.data_ptr(), small.numel())])
+    h, d, s = _hash(torch, ctx, regions, digests=True)
+    hosts = {buf.data_ptr(): buf.cpu().numpy(), small.data_ptr(): small.cpu().numpy()}
+    exp = [orc.chunk_hashes(hosts[b], threads=16) for b, _ in regions]
+    assert np.array_equal(h, np.concatenate(exp))
+    dig = [orc.region_digest(e) for e in exp]
+    assert [int(x) for x in d] == dig
+    assert s == orc.snapshot_digest([r[0] for r in regions], [r[1] for r in regions], dig)
 
 
 def test_k1_zero_chunks_and_empty(env):
