@@ -303,6 +303,37 @@ def run_ours(a, rank, world, device, log):
     ms = float(tmax.item())
     value = float(alg.item()) / (ms * 1e-3) / 1e9
 
+    # cross-N fingerprint (O7: N-GPU results equal the 1-GPU ones bit for bit): SHA-256 of the
+    # post-manifest in global spec order (pointer tables excluded: they hold this process's
+    # VAs) and the combined report counters
+    import hashlib
+    import numpy as np
+    specs_all = pool.all_specs
+    if world > 1:
+        gm = kd.Plan.gather_manifest(plan, post, perm).cpu().numpy()
+        cr = kd.combine_reports(torch.zeros_like(glob_reps).index_copy_(0, rows, reps.view(-1, REP_WORDS)))
+        counters = cr.cpu().numpy()[:, [3, 4, 9, 10, 13]].sum(axis=0)
+        starts, o = [], 0
+        for s in specs_all:
+            starts.append(o)
+            o += (s.size + 65535) // 65536
+        pieces = [gm[starts[g]:starts[g] + (s.size + 65535) // 65536] for g, s in enumerate(specs_all)]
+    else:
+        hp = post.cpu().numpy()
+        byg, o = {}, 0
+        for s in pool.specs:
+            n = (s.size + 65535) // 65536
+            byg[pool.gidx[s.name]] = hp[o:o + n]
+            o += n
+        pieces = [byg[g] for g in range(len(specs_all))]
+        counters = reps.view(-1, REP_WORDS).cpu().numpy()[:, [3, 4, 9, 10, 13]].sum(axis=0)
+    fp = hashlib.sha256()
+    for s, pc in zip(specs_all, pieces):
+        if not s.name.startswith("ptr_"):
+            fp.update(pc.tobytes())
+    fingerprint = {"post_manifest_sha256_excl_ptr_tables": fp.hexdigest(),
+                   "chunks": int(sum(p.size for p in pieces)), "report_counter_sums": [int(x) for x in counters]}
+
     # per-kernel roofline: the dominant kernel by time share
     per = {k: tsum[k] / a.steps for k in tsum}
     k1_ms = (per["hash_pre"] + per["hash_post"]) / 2
@@ -352,7 +383,7 @@ def run_ours(a, rank, world, device, log):
                    "bytes_this_rank": pool.bytes, "l2": "inputs (30 GB) >> L2 (126 MB); no flush needed",
                    "parallelism": f"E1 residency-first shards over {world} GPU(s)"},
         "roofline": roof, "kernels": kern, "clocks": clk, "gpu_launches": launches,
-        "e2e": e2e, "capture_replay": lat,
+        "e2e": e2e, "capture_replay": lat, "fingerprint": fingerprint,
     }
     return res, pool
 
@@ -552,11 +583,20 @@ def main():
         return
 
     import torch
+    # KC_BENCH_ONE_GPU=1 + KC_BENCH_BACKEND=gloo: every rank on cuda:0, collectives through
+    # host memory -- a functional check of the N > 1 path on a single-GPU box, never a number
+    device = 0 if os.environ.get("KC_BENCH_ONE_GPU") else local
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    res, pool = run_ours(a, rank, world, local, log)
+        torch.cuda.set_device(device)
+        backend = os.environ.get("KC_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
+        else:
+            dist.init_process_group(backend)
+    res, pool = run_ours(a, rank, world, device, log)
+    if os.environ.get("KC_BENCH_ONE_GPU") and world > 1:
+        res["config"]["functional_check_only"] = "all ranks on cuda:0 (KC_BENCH_ONE_GPU)"
     if rank == 0:
         threads = os.cpu_count() or 1
         sample = oracle_sample(pool, a.cpu_sample_mb)

@@ -45,8 +45,11 @@ struct kc_ctx {
     uint64_t unknown_frees = 0;
 
     // cached device tables / scratch (stream-ordered; one stream at a time per ctx)
-    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count;
+    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map;
     std::vector<kc::RegionDev> regs_cached;
+    std::vector<uint8_t> diff_key;  // K2 plan cache (raw inputs of the last kc_diff_async)
+    std::vector<kc::DiffGroup> diff_groups;
+    uint64_t diff_bitmap_words = 0;
     bool regs_aligned = true;
 
     // pinned staging ring for D2H/H2D (lazily allocated)

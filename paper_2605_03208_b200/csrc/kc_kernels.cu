@@ -242,8 +242,11 @@ struct ChunkRef {
     uint32_t len;
 };
 
-__device__ __forceinline__ ChunkRef chunk_ref(const RegionDev* __restrict__ regs, int nreg, uint64_t g) {
-    const int r = find_region(regs, nreg, g);
+// chunk -> region: one load from the host-built map when given (uploaded once
+// with the cached region table), else binary search over the chunk offsets
+__device__ __forceinline__ ChunkRef chunk_ref(const RegionDev* __restrict__ regs, int nreg, uint64_t g,
+                                             const uint32_t* __restrict__ map) {
+    const int r = map ? (int)__ldg(map + g) : find_region(regs, nreg, g);
     const uint64_t off = (g - regs[r].chunk_off) * kChunk;
     const uint64_t rem = regs[r].size - off;
     return {reinterpret_cast<const uint8_t*>(regs[r].base + off), rem < kChunk ? (uint32_t)rem : (uint32_t)kChunk};
@@ -251,7 +254,8 @@ __device__ __forceinline__ ChunkRef chunk_ref(const RegionDev* __restrict__ regs
 
 template <class CFG>
 __global__ void __launch_bounds__(CFG::kThreads, 1)
-    k1_hash_tma(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out) {
+    k1_hash_tma(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out,
+                const uint32_t* __restrict__ map) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int slot = threadIdx.x >> 2;
     const int ql = threadIdx.x & 3;
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(CFG::kThreads, 1)
     auto issue_next = [&]() {
         while (pg < C) {
             if (!phave) {
-                const ChunkRef cr = chunk_ref(regs, nreg, pg);
+                const ChunkRef cr = chunk_ref(regs, nreg, pg, map);
                 psrc = cr.src;
                 pbytes = cr.len >= 32 ? (cr.len & ~31u) : 0u;
                 poff = 0;
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(CFG::kThreads, 1)
 
     uint32_t consumed = 0;
     for (uint64_t g = g0; g < C; g += Q) {
-        const ChunkRef cr = chunk_ref(regs, nreg, g);
+        const ChunkRef cr = chunk_ref(regs, nreg, g, map);
         const uint32_t nst = cr.len >= 32 ? cr.len / 32 : 0;
         uint64_t v = lane_seed(ql);
         uint32_t remaining = nst * 32;
@@ -360,7 +364,8 @@ struct CpCfg {
 
 template <class CFG>
 __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
-    k1_hash_cpasync(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out) {
+    k1_hash_cpasync(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out,
+                    const uint32_t* __restrict__ map) {
     constexpr int WARPS = CFG::kWarps, STAGES = CFG::kStages, SL = CFG::kSlice, PITCH = CFG::kPitch;
     constexpr int WSTAGE = CFG::kWStage, UPC = CFG::kUPC, UPL = CFG::kUPL;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -382,7 +387,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         unsigned long long src = 0;
         uint32_t bytes = 0;
         if (g < C) {
-            const ChunkRef cr = chunk_ref(regs, nreg, g);
+            const ChunkRef cr = chunk_ref(regs, nreg, g, map);
             src = (unsigned long long)cr.src;
             bytes = cr.len >= 32 ? (cr.len & ~31u) : 0u;
         }
@@ -433,7 +438,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     for (uint64_t j = j0; j < ngroups; j += W) {
         const uint64_t g = 8 * j + q;
         ChunkRef cr = {nullptr, 0};
-        if (g < C) cr = chunk_ref(regs, nreg, g);
+        if (g < C) cr = chunk_ref(regs, nreg, g, map);
         const uint32_t nst = cr.len >= 32 ? cr.len / 32 : 0;
         const uint32_t nsl = __reduce_max_sync(0xFFFFFFFFu, (nst * 32 + SL - 1) / SL);
         uint64_t v = lane_seed(ql);
@@ -465,12 +470,13 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
 
 // Unaligned regions (base % 16 != 0): quad per chunk, byte-assembled loads.
 __global__ void __launch_bounds__(256)
-    k1_hash_generic(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out) {
+    k1_hash_generic(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out,
+                    const uint32_t* __restrict__ map) {
     const int ql = threadIdx.x & 3;
     const unsigned qmask = 0xFu << (threadIdx.x & 28);
     const uint64_t nq = (uint64_t)gridDim.x * (blockDim.x / 4);
     for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x / 4) + (threadIdx.x >> 2); g < C; g += nq) {
-        const ChunkRef cr = chunk_ref(regs, nreg, g);
+        const ChunkRef cr = chunk_ref(regs, nreg, g, map);
         const uint64_t h = quad_xxh64_global<false>(cr.src, cr.len, ql, qmask);
         if (ql == 0) out[g] = h;
     }
@@ -897,31 +903,38 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
     for (uint32_t o = done + lane * S; o < len; o += 32 * S) elem_scalar<DT>(R + o, A + o, acc, atol, rtol, equal_nan);
 }
 
+// Warp reductions with the REDUX unit (one instruction each): 64-bit sums as
+// two 32-bit partial sums (valid while every lane's value is < 2^48, i.e. for
+// any segment < 256 TiB), 64-bit maxima as max of the high words, then of the
+// low words among the lanes holding that high word.
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    return v;
+    const uint32_t lo = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(v & 0xFFFFu));
+    const uint32_t hi = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(v >> 16));
+    return ((unsigned long long)hi << 16) + lo;
 }
 __device__ __forceinline__ unsigned long long warp_maxu(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
-        v = w > v ? w : v;
-    }
-    return v;
+    const uint32_t hi = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)(v >> 32));
+    const uint32_t lo = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)(v >> 32) == hi ? (uint32_t)v : 0u);
+    return ((unsigned long long)hi << 32) | lo;
 }
 
 __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
-    const unsigned long long nonzero =
-        acc.dbytes | acc.delems | acc.nan_r | acc.nan_a | acc.nan_pos | acc.rel_undef | acc.fail | acc.max_ulp |
-        (unsigned long long)__double_as_longlong(acc.max_abs) | (unsigned long long)__double_as_longlong(acc.max_rel);
-    if (__ballot_sync(0xFFFFFFFFu, nonzero != 0) != 0) {
-        const unsigned long long s0 = warp_sum(acc.dbytes), s1 = warp_sum(acc.delems), s2 = warp_sum(acc.nan_r),
-                                 s3 = warp_sum(acc.nan_a), s4 = warp_sum(acc.nan_pos), s5 = warp_sum(acc.rel_undef),
-                                 s6 = warp_sum(acc.fail);
-        const unsigned long long m0 = warp_maxu(acc.max_ulp),
-                                 m1 = warp_maxu((unsigned long long)__double_as_longlong(acc.max_abs)),
-                                 m2 = warp_maxu((unsigned long long)__double_as_longlong(acc.max_rel));
+    const unsigned FULL = 0xFFFFFFFFu;
+    const unsigned long long mabs = (unsigned long long)__double_as_longlong(acc.max_abs);
+    const unsigned long long mrel = (unsigned long long)__double_as_longlong(acc.max_rel);
+    // one ballot per field: only fields nonzero somewhere in the warp are reduced
+    const unsigned b0 = __ballot_sync(FULL, acc.dbytes != 0), b1 = __ballot_sync(FULL, acc.delems != 0);
+    const unsigned b2 = __ballot_sync(FULL, acc.nan_r != 0), b3 = __ballot_sync(FULL, acc.nan_a != 0);
+    const unsigned b4 = __ballot_sync(FULL, acc.nan_pos != 0), b5 = __ballot_sync(FULL, acc.rel_undef != 0);
+    const unsigned b6 = __ballot_sync(FULL, acc.fail != 0), b7 = __ballot_sync(FULL, acc.max_ulp != 0);
+    const unsigned b8 = __ballot_sync(FULL, mabs != 0), b9 = __ballot_sync(FULL, mrel != 0);
+    if (b0 | b1 | b2 | b3 | b4 | b5 | b6 | b7 | b8 | b9) {
+        const unsigned long long s0 = b0 ? warp_sum(acc.dbytes) : 0, s1 = b1 ? warp_sum(acc.delems) : 0,
+                                 s2 = b2 ? warp_sum(acc.nan_r) : 0, s3 = b3 ? warp_sum(acc.nan_a) : 0,
+                                 s4 = b4 ? warp_sum(acc.nan_pos) : 0, s5 = b5 ? warp_sum(acc.rel_undef) : 0,
+                                 s6 = b6 ? warp_sum(acc.fail) : 0;
+        const unsigned long long m0 = b7 ? warp_maxu(acc.max_ulp) : 0, m1 = b8 ? warp_maxu(mabs) : 0,
+                                 m2 = b9 ? warp_maxu(mrel) : 0;
         if (lane == 0) {
             if (s0) atomicAdd((unsigned long long*)&rep->differing_bytes, s0);
             if (s1) atomicAdd((unsigned long long*)&rep->differing_elems, s1);
@@ -940,7 +953,6 @@ __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
     acc_zero(acc);
     acc.any = any;
 }
-
 
 // One launch per dtype group: segments [seg0, seg0+nseg) own the global units
 // [unit0, unit0+U).
@@ -1053,17 +1065,19 @@ cudaError_t kernels_init() {
 }
 
 template <class CFG>
-static void launch_tma(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, int num_sms, cudaStream_t s) {
+static void launch_tma(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
+                       int num_sms, cudaStream_t s) {
     uint64_t grid = (C + CFG::kSlots - 1) / CFG::kSlots;
     if (grid > (uint64_t)num_sms) grid = num_sms;
-    k1_hash_tma<CFG><<<(unsigned)grid, CFG::kThreads, CFG::kSmem, s>>>(d_regs, nreg, C, d_out);
+    k1_hash_tma<CFG><<<(unsigned)grid, CFG::kThreads, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map);
 }
 
 template <class CFG>
-static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, int num_sms, cudaStream_t s) {
+static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
+                      int num_sms, cudaStream_t s) {
     const uint64_t groups = (C + 7) / 8;
     const uint64_t grid = std::min<uint64_t>((groups + CFG::kWarps - 1) / CFG::kWarps, (uint64_t)num_sms);
-    k1_hash_cpasync<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out);
+    k1_hash_cpasync<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map);
 }
 
 // K1 variant selection (KC_K1_VARIANT, tuning knob; default = the measured best)
@@ -1075,21 +1089,21 @@ static int k1_variant() {
     return v;
 }
 
-cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool aligned, uint64_t* d_out, int num_sms,
-                        cudaStream_t s) {
+cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool aligned, uint64_t* d_out,
+                        const uint32_t* map, int num_sms, cudaStream_t s) {
     if (C == 0) return cudaSuccess;
     if (!aligned) {
         uint64_t grid = (C + 63) / 64;
         if (grid > (uint64_t)num_sms * 8) grid = num_sms * 8;
-        k1_hash_generic<<<(unsigned)grid, 256, 0, s>>>(d_regs, nreg, C, d_out);
+        k1_hash_generic<<<(unsigned)grid, 256, 0, s>>>(d_regs, nreg, C, d_out, map);
         return cudaGetLastError();
     }
     // measured on B200: cp.async 64 chunks x 3 x 1 KiB is HBM-bound
     switch (k1_variant()) {
-        case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, num_sms, s); break;
-        case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, num_sms, s); break;
-        case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, num_sms, s); break;
-        default: launch_cp<CpA>(d_regs, nreg, C, d_out, num_sms, s); break;
+        case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
+        case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, map, num_sms, s); break;
+        case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s); break;
+        default: launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
     }
     return cudaGetLastError();
 }

@@ -259,7 +259,7 @@ void kc_destroy(kc_ctx* ctx) {
     for (auto& kv : ctx->vmm) vm.push_back(kv.first);
     for (uint64_t b : vm) free_alloc(ctx, b, false);
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch,
-                              &ctx->tmp_hash, &ctx->tmp_count})
+                              &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map})
         if (b->p) cudaFree(b->p);
     for (auto& w : ctx->io) {
         for (void* p : w.pinned) cudaFreeHost(p);
@@ -423,6 +423,16 @@ static kc_status upload_regions(kc_ctx* ctx, const kc_region* regions, size_t n,
             KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->regs.p, t.data(), t.size() * sizeof(RegionDev),
                                                cudaMemcpyHostToDevice, s),
                           "upload region table");
+        // chunk -> region map (4 B per 64 KiB chunk): one load instead of a binary search per chunk
+        std::vector<uint32_t> map(c);
+        for (size_t i = 0; i < t.size(); ++i) {
+            const uint64_t n_i = (i + 1 < t.size() ? t[i + 1].chunk_off : c) - t[i].chunk_off;
+            std::fill(map.begin() + t[i].chunk_off, map.begin() + t[i].chunk_off + n_i, (uint32_t)i);
+        }
+        KC_CHECK_CUDA(ctx, ensure(ctx->chunk_map, std::max<size_t>(1, map.size()) * 4), "cudaMalloc(chunk map)");
+        if (!map.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->chunk_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
+                          "upload chunk map");
         ctx->regs_cached.swap(t);
         ctx->regs_aligned = aligned;
     }
@@ -444,7 +454,7 @@ kc_status kc_hash(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_c
     if (st != KC_OK) return st;
     if (C && !d_chunk_hash) return set_err(ctx, KC_ERR_ARG, "kc_hash: d_chunk_hash is NULL");
     KC_CHECK_CUDA(ctx, launch_hash((const RegionDev*)ctx->regs.p, (int)n, C, ctx->regs_aligned, d_chunk_hash,
-                                   ctx->num_sms, s),
+                                   (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s),
                   "launch K1");
     if (C) ctx->launches += 1;
     if (d_region_digest || d_snapshot_digest) {
@@ -500,67 +510,92 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
     if (!(tol->atol >= 0.0) || !(tol->rtol >= 0.0))
         return set_err(ctx, KC_ERR_ARG, "kc_diff: tolerances must be >= 0 (atol %g, rtol %g)", tol->atol, tol->rtol);
     cudaStream_t s = (cudaStream_t)stream;
-    std::vector<ReportMeta> meta(n_reports);
-    std::vector<int> rep_dt(n_reports, -1);
-    // validate, then order segments by dtype (stable) so each dtype is one launch
-    std::vector<size_t> order;
-    order.reserve(n_bufs);
-    for (size_t i = 0; i < n_bufs; ++i) {
-        const kc_buffer& b = bufs[i];
-        const int es = elem_size(b.dtype);
-        if (es == 0) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: bad dtype %d", i, b.dtype);
-        if (b.nbytes % es) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: %llu bytes is not a multiple of "
-                                          "the element size %d", i, (unsigned long long)b.nbytes, es);
-        if (b.report < 0 || (size_t)b.report >= n_reports)
-            return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: report index %d out of range", i, b.report);
-        if (rep_dt[b.report] >= 0 && rep_dt[b.report] != b.dtype)
-            return set_err(ctx, KC_ERR_ARG, "kc_diff: report %d mixes dtypes", b.report);
-        rep_dt[b.report] = b.dtype;
-        if (b.nbytes == 0) continue;
-        if (!b.ref || !b.act) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: null VA", i);
-        order.push_back(i);
+    // plan cache: identical inputs to the previous call reuse the uploaded
+    // segment/meta tables (validation of the same buffer set every replay)
+    const size_t key_bytes = n_bufs * sizeof(kc_buffer) + n_reports * 8 * (bitmap_word0 ? 2 : 1) + 8;
+    std::vector<uint8_t> key(key_bytes);
+    {
+        uint8_t* k = key.data();
+        if (n_bufs) memcpy(k, bufs, n_bufs * sizeof(kc_buffer));
+        k += n_bufs * sizeof(kc_buffer);
+        if (n_reports) memcpy(k, report_nbytes, n_reports * 8);
+        k += n_reports * 8;
+        if (bitmap_word0 && n_reports) memcpy(k, bitmap_word0, n_reports * 8);
+        k += bitmap_word0 ? n_reports * 8 : 0;
+        const uint64_t nr = n_reports;
+        memcpy(k, &nr, 8);
     }
-    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return bufs[a].dtype < bufs[b].dtype; });
-    std::vector<SegDev> segs;
-    segs.reserve(order.size());
+    const bool cached = ctx->diff_key.size() == key.size() && ctx->segs.p && ctx->meta.p &&
+                        memcmp(ctx->diff_key.data(), key.data(), key.size()) == 0;
     std::vector<DiffGroup> groups;
-    uint64_t U = 0;
-    for (size_t i : order) {
-        const kc_buffer& b = bufs[i];
-        SegDev d;
-        d.ref = b.ref;
-        d.act = b.act;
-        d.nbytes = b.nbytes;
-        d.bitmap_word0 = bitmap_word0 ? bitmap_word0[b.report] : 0;
-        d.bitmap_chunk0 = b.bitmap_chunk0;
-        d.unit_off = U;
-        d.dtype = b.dtype;
-        d.report = b.report;
-        const uint64_t nu = (b.nbytes + kDiffUnit - 1) / kDiffUnit;
-        if (groups.empty() || groups.back().dtype != b.dtype)
-            groups.push_back(DiffGroup{b.dtype, (int32_t)segs.size(), 0, U, 0});
-        groups.back().n_segs += 1;
-        groups.back().n_units += nu;
-        U += nu;
-        segs.push_back(d);
-    }
     uint64_t bitmap_words = 0;
-    for (size_t j = 0; j < n_reports; ++j) {
-        meta[j].nbytes = report_nbytes[j];
-        meta[j].dtype = rep_dt[j] < 0 ? KC_DT_BYTES : rep_dt[j];
-        if (bitmap_word0) {
-            const uint64_t w = (report_nbytes[j] + kChunk - 1) / kChunk;
-            bitmap_words = std::max(bitmap_words, bitmap_word0[j] + (w + 63) / 64);
+    if (cached) {
+        groups = ctx->diff_groups;
+        bitmap_words = ctx->diff_bitmap_words;
+    } else {
+        std::vector<ReportMeta> meta(n_reports);
+        std::vector<int> rep_dt(n_reports, -1);
+        // validate, then order segments by dtype (stable) so each dtype is one launch
+        std::vector<size_t> order;
+        order.reserve(n_bufs);
+        for (size_t i = 0; i < n_bufs; ++i) {
+            const kc_buffer& b = bufs[i];
+            const int es = elem_size(b.dtype);
+            if (es == 0) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: bad dtype %d", i, b.dtype);
+            if (b.nbytes % es) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: %llu bytes is not a multiple of "
+                                              "the element size %d", i, (unsigned long long)b.nbytes, es);
+            if (b.report < 0 || (size_t)b.report >= n_reports)
+                return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: report index %d out of range", i, b.report);
+            if (rep_dt[b.report] >= 0 && rep_dt[b.report] != b.dtype)
+                return set_err(ctx, KC_ERR_ARG, "kc_diff: report %d mixes dtypes", b.report);
+            rep_dt[b.report] = b.dtype;
+            if (b.nbytes == 0) continue;
+            if (!b.ref || !b.act) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: null VA", i);
+            order.push_back(i);
         }
+        std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return bufs[a].dtype < bufs[b].dtype; });
+        std::vector<SegDev> segs;
+        segs.reserve(order.size());
+        uint64_t U = 0;
+        for (size_t i : order) {
+            const kc_buffer& b = bufs[i];
+            SegDev d;
+            d.ref = b.ref;
+            d.act = b.act;
+            d.nbytes = b.nbytes;
+            d.bitmap_word0 = bitmap_word0 ? bitmap_word0[b.report] : 0;
+            d.bitmap_chunk0 = b.bitmap_chunk0;
+            d.unit_off = U;
+            d.dtype = b.dtype;
+            d.report = b.report;
+            const uint64_t nu = (b.nbytes + kDiffUnit - 1) / kDiffUnit;
+            if (groups.empty() || groups.back().dtype != b.dtype)
+                groups.push_back(DiffGroup{b.dtype, (int32_t)segs.size(), 0, U, 0});
+            groups.back().n_segs += 1;
+            groups.back().n_units += nu;
+            U += nu;
+            segs.push_back(d);
+        }
+        for (size_t j = 0; j < n_reports; ++j) {
+            meta[j].nbytes = report_nbytes[j];
+            meta[j].dtype = rep_dt[j] < 0 ? KC_DT_BYTES : rep_dt[j];
+            if (bitmap_word0) {
+                const uint64_t w = (report_nbytes[j] + kChunk - 1) / kChunk;
+                bitmap_words = std::max(bitmap_words, bitmap_word0[j] + (w + 63) / 64);
+            }
+        }
+        KC_CHECK_CUDA(ctx, ensure(ctx->segs, segs.size() * sizeof(SegDev)), "cudaMalloc(segments)");
+        KC_CHECK_CUDA(ctx, ensure(ctx->meta, meta.size() * sizeof(ReportMeta)), "cudaMalloc(meta)");
+        if (!segs.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(SegDev),
+                                               cudaMemcpyHostToDevice, s), "upload segments");
+        if (!meta.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->meta.p, meta.data(), meta.size() * sizeof(ReportMeta),
+                                               cudaMemcpyHostToDevice, s), "upload meta");
+        ctx->diff_key.swap(key);
+        ctx->diff_groups = groups;
+        ctx->diff_bitmap_words = bitmap_words;
     }
-    KC_CHECK_CUDA(ctx, ensure(ctx->segs, segs.size() * sizeof(SegDev)), "cudaMalloc(segments)");
-    KC_CHECK_CUDA(ctx, ensure(ctx->meta, meta.size() * sizeof(ReportMeta)), "cudaMalloc(meta)");
-    if (!segs.empty())
-        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(SegDev),
-                                           cudaMemcpyHostToDevice, s), "upload segments");
-    if (!meta.empty())
-        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->meta.p, meta.data(), meta.size() * sizeof(ReportMeta),
-                                           cudaMemcpyHostToDevice, s), "upload meta");
     if (n_reports)
         KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_reports, 0, n_reports * sizeof(kc_diff_report), s), "zero reports");
     if (d_bitmaps && bitmap_words)

@@ -33,6 +33,29 @@ def _nchunks(size: int) -> int:
     return (size + CHUNK - 1) // CHUNK
 
 
+def _host_staged(group) -> bool:
+    """gloo cannot run these collectives on CUDA tensors: stage through host memory."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None) -> None:
+    if _host_staged(group) and inp.is_cuda:
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def _all_reduce(t: torch.Tensor, op, group=None) -> None:
+    if _host_staged(group) and t.is_cuda:
+        c = t.cpu()
+        dist.all_reduce(c, op=op, group=group)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
 @dataclass
 class Plan:
     """Global region table (sorted by base) with the owning rank of each region."""
@@ -47,6 +70,8 @@ class Plan:
         """C1: rank 0's table is broadcast to every rank (other ranks may pass None)."""
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
+        if _host_staged(group):
+            device = "cpu"
         n = torch.tensor([len(bases) if rank == 0 else 0], dtype=torch.int64, device=device)
         dist.broadcast(n, 0, group=group)
         t = torch.zeros(3, int(n.item()), dtype=torch.int64, device=device)
@@ -93,7 +118,7 @@ class Plan:
         n = self.local_chunks()
         mine[:n].copy_(local_h[:n])
         out = torch.empty(self.world * max(1, pad), dtype=torch.int64, device=local_h.device)
-        dist.all_gather_into_tensor(out, mine, group=group)
+        _all_gather_into(out, mine, group)
         if perm is None:
             perm = self.manifest_permutation()
         return out.index_select(0, perm.to(local_h.device))
@@ -107,10 +132,10 @@ def combine_reports(reps: torch.Tensor, group=None) -> torch.Tensor:
     nbytes/n_elems/n_chunks/percent/pass are recomputed by :func:`finalize`."""
     out = reps.clone()
     s = reps[:, SUM_FIELDS].contiguous()
-    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+    _all_reduce(s, dist.ReduceOp.SUM, group)
     m = reps[:, MAX_FIELDS].contiguous()
     m[:, 0] ^= _SIGN
-    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    _all_reduce(m, dist.ReduceOp.MAX, group)
     m[:, 0] ^= _SIGN
     out[:, SUM_FIELDS] = s
     out[:, MAX_FIELDS] = m
@@ -153,7 +178,7 @@ def gather_bitmaps(local_words: torch.Tensor, group=None) -> torch.Tensor:
     E1, so the OR is a concatenation; split buffers OR their bits)."""
     world = dist.get_world_size(group)
     out = torch.empty(world * local_words.numel(), dtype=local_words.dtype, device=local_words.device)
-    dist.all_gather_into_tensor(out, local_words.contiguous(), group=group)
+    _all_gather_into(out, local_words.contiguous(), group)
     acc = out.view(world, -1)[0].clone()
     for r in range(1, world):
         acc |= out.view(world, -1)[r]

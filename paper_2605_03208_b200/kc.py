@@ -202,7 +202,19 @@ def count_chunks(regions: Sequence[Region]) -> int:
     return int(lib().kc_count_chunks(arr, len(regions)))
 
 
+def region_array(regions) -> ctypes.Array:
+    """Prebuilt kc_region array (reuse it across calls to keep marshalling off the hot path)."""
+    return _regions(regions)
+
+
+def buffer_array(bufs) -> ctypes.Array:
+    """Prebuilt kc_buffer array (reuse it across calls)."""
+    return Context._buffers(bufs)
+
+
 def _regions(regions) -> ctypes.Array:
+    if isinstance(regions, ctypes.Array) and regions._type_ is Region:
+        return regions
     arr = (Region * max(1, len(regions)))()
     for i, r in enumerate(regions):
         if isinstance(r, Region):
@@ -338,9 +350,10 @@ class Context:
 
     # -- K1 / K3 / K2
     def hash(self, regions, d_chunk_hash: int, d_region_digest: int = 0, d_snapshot_digest: int = 0,
-             stream: int = 0):
+             stream: int = 0, n: int | None = None):
         arr = _regions(regions)
-        self._check(lib().kc_hash(self._h, arr, len(regions), d_chunk_hash or None, d_region_digest or None,
+        n = len(regions) if n is None else n
+        self._check(lib().kc_hash(self._h, arr, n, d_chunk_hash or None, d_region_digest or None,
                                   d_snapshot_digest or None, stream or None), "kc_hash")
 
     def written(self, d_pre: int, d_post: int, n_chunks: int, d_bitmap: int, d_count: int = 0, stream: int = 0):
@@ -349,6 +362,8 @@ class Context:
 
     @staticmethod
     def _buffers(bufs) -> ctypes.Array:
+        if isinstance(bufs, ctypes.Array) and bufs._type_ is Buffer:
+            return bufs
         arr = (Buffer * max(1, len(bufs)))()
         for i, b in enumerate(bufs):
             if isinstance(b, Buffer):
@@ -380,8 +395,12 @@ class Context:
                    bitmap_word0: Sequence[int] | None = None, d_bitmaps: int = 0, atol: float = 1e-8,
                    rtol: float = 1e-5, equal_nan: bool = False, stream: int = 0):
         arr = self._buffers(bufs)
-        rn = (ctypes.c_uint64 * max(1, n_reports))(*report_nbytes)
-        w0 = (ctypes.c_uint64 * max(1, n_reports))(*bitmap_word0) if bitmap_word0 is not None else None
+        rn = report_nbytes if isinstance(report_nbytes, ctypes.Array) else \
+            (ctypes.c_uint64 * max(1, n_reports))(*report_nbytes)
+        w0 = None
+        if bitmap_word0 is not None:
+            w0 = bitmap_word0 if isinstance(bitmap_word0, ctypes.Array) else \
+                (ctypes.c_uint64 * max(1, n_reports))(*bitmap_word0)
         tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
         self._check(lib().kc_diff_async(self._h, arr, len(bufs), n_reports, rn, w0, ctypes.byref(tol), d_reports,
                                         d_bitmaps or None, stream or None), "kc_diff_async")

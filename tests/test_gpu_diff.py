@@ -199,3 +199,21 @@ def test_k2_c3_full_size(env, kind):
         _same(reps[i], exp.report, f"c3 full {kind} #{i}")
         assert [int(w) for w in bms[i]] == [int(w) for w in exp.bitmap]
     assert reps[1]["differing_bytes"] == 1 and reps[0]["differing_bytes"] == 0
+
+
+def test_k2_plan_cache_sees_new_contents_and_new_sets(env):
+    """Identical buffer sets reuse the uploaded tables; contents are always re-read."""
+    torch, kc, ctx, orc = env
+    r, a = _pair_host(orc.DT_F16, 200000, 77, orc)
+    tr, pr = _dev(torch, r)
+    ta, pa = _dev(torch, a)
+    bufs = [(pr, pa, r.size, "f16")]
+    first, _ = ctx.diff(bufs)
+    _same(first[0], orc.diff(r, a, orc.DT_F16).report, "first")
+    a2 = a.copy()
+    a2[1000:1100] ^= 0x55
+    ta[:a2.size].copy_(torch.from_numpy(a2))
+    second, _ = ctx.diff(bufs)                      # same set, new contents
+    _same(second[0], orc.diff(r, a2, orc.DT_F16).report, "second")
+    third, _ = ctx.diff([(pr, pa, r.size // 2, "f16")])   # a different set
+    _same(third[0], orc.diff(r[:r.size // 2], a2[:a2.size // 2], orc.DT_F16).report, "third")
