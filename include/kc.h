@@ -183,6 +183,7 @@ typedef struct {
 
 typedef struct kc_ctx kc_ctx;
 typedef struct kc_restored kc_restored;
+typedef struct kc_snapshot kc_snapshot;   /* device-resident snapshot (F1) */
 
 /* ---- lifetime ---------------------------------------------------------- */
 /* Creates a context on opt->device (primary CUDA context).  opt may be NULL. */
@@ -272,6 +273,27 @@ kc_status kc_restore(kc_ctx* ctx, const char* dir, kc_restored** out, kc_restore
  * for a fresh ASLR layout); *n_reserved = windows that are free.  Maps nothing,
  * makes no CUDA calls. */
 kc_status kc_prereserve(const char* dir, uint64_t* n_reserved);
+
+/* ---- F1 device-resident snapshot --------------------
+ * The same capture with the region bytes kept in a device arena in this GPU's
+ * HBM (D2D copies at HBM bandwidth instead of PCIe + files): PRE_W keeps the
+ * pre-dispatch bytes of every region plus the post bytes of W, POST the
+ * post-dispatch bytes.  Manifests, W and the dispatch description stay in host
+ * memory inside the kc_snapshot.  The arena (sum of region sizes, 256 B
+ * aligned per region, + |W| chunks) is allocated with cudaMalloc and owned by
+ * the snapshot; KC_ERR_NOMEM if it does not fit.  The dispatch is forwarded
+ * exactly as in kc_capture (it always proceeds). */
+kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
+                         kc_snapshot** out, kc_capture_report* rep);
+/* Same-VA restore from a device snapshot (the originals must be freed first,
+ * or this is another process sharing nothing: the arena lives in this ctx's
+ * device): VA windows as kc_restore, then D2D copy-in and the K1 verify. */
+kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep);
+/* Persist a device snapshot as a kc-snapshot/1 directory (parallel D2H). */
+kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
+/* Bytes held in the device arena. */
+uint64_t kc_snapshot_bytes(const kc_snapshot* s);
+void kc_snapshot_free(kc_snapshot* s);
 
 /* ---- A7 replay ------------------------------------ */
 kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts* o, kc_replay_report* rep);

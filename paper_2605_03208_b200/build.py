@@ -19,6 +19,10 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libkc.so")
 FIXTURE_SRC = os.path.join(ROOT, "synth", "kc_fixtures.cu")
 FIXTURE_CUBIN = os.path.join(ROOT, "synth", "kc_fixtures.cubin")
+# variant code objects for the replay-override tests: an unmodified recompile
+# (different optimisation level) and a modified kernel (KC_VARIANT_DELTA=1)
+FIXTURE_VARIANTS = {os.path.join(ROOT, "synth", "kc_fixtures_recompiled.cubin"): ["-O1"],
+                    os.path.join(ROOT, "synth", "kc_fixtures_modified.cubin"): ["-O3", "-DKC_VARIANT_DELTA=1"]}
 SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu"]
 HEADERS = ["kc_kernels.cuh", "kc_internal.h", "kc_json.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -50,11 +54,11 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
 
 
 def build_fixtures(force: bool = False) -> str:
-    if not force and not _stale(FIXTURE_CUBIN, [FIXTURE_SRC]):
-        return FIXTURE_CUBIN
-    tmp = FIXTURE_CUBIN + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, "-cubin", *ARCH, "-O3", "-lineinfo", "-o", tmp, FIXTURE_SRC])
-    os.replace(tmp, FIXTURE_CUBIN)
+    for out, flags in [(FIXTURE_CUBIN, ["-O3"])] + list(FIXTURE_VARIANTS.items()):
+        if force or _stale(out, [FIXTURE_SRC]):
+            tmp = out + f".tmp{os.getpid()}"
+            subprocess.check_call([NVCC, "-cubin", *ARCH, *flags, "-lineinfo", "-o", tmp, FIXTURE_SRC])
+            os.replace(tmp, out)
     return FIXTURE_CUBIN
 
 

@@ -116,6 +116,8 @@ struct kc_restored {
     void* stash_ref = nullptr;
     uint64_t stash_bytes = 0;
     CUmodule module = nullptr;
+    std::vector<uint8_t> image;  // code object (kernel.cubin or the device snapshot's copy)
+    const kc_snapshot* dev_snap = nullptr;  // restored from a device snapshot (kc_restore_dev)
 };
 
 namespace kc {

@@ -16,6 +16,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <thread>
@@ -277,6 +278,89 @@ bool item_h2d(kc_ctx* ctx, kc_ctx::IoWorker& w, int fd, uint64_t base, const IoI
     return cudaStreamSynchronize(w.stream) == cudaSuccess;
 }
 
+// ------------------------------------------------------------------ kc-snapshot/1 writers
+// Shared by kc_capture (file sink) and kc_snapshot_save (device snapshot).
+struct MetaRegion {
+    uint64_t base, size, n_chunks, digest, seq;
+    int kind, device;
+    bool ok;
+};
+struct LogRegion {
+    uint64_t base, post_digest, written;
+    bool ok;
+    std::string error;
+};
+
+std::string dispatch_json(int mode, const std::string& mangled, const uint32_t grid[3], const uint32_t block[3],
+                          uint32_t smem, uint32_t kernarg_size, int device, size_t image_size,
+                          const std::vector<std::pair<size_t, size_t>>& layout) {
+    int cc_major = 0, cc_minor = 0;
+    cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+    std::string j = "{\n";
+    j += "  \"format\": \"kc-snapshot/1\",\n";
+    j += std::string("  \"mode\": \"") + (mode == KC_MODE_PRE_W ? "pre_w" : "post") + "\",\n";
+    j += "  \"mangled_symbol\": \"" + kcj::esc(mangled) + "\",\n";
+    char b[512];
+    snprintf(b, sizeof b,
+             "  \"grid\": [%u, %u, %u],\n  \"block\": [%u, %u, %u],\n  \"cluster\": [1, 1, 1],\n"
+             "  \"shared_mem_bytes\": %u,\n  \"kernarg_size\": %u,\n  \"device_ordinal\": %d,\n"
+             "  \"compute_capability\": \"%d.%d\",\n  \"code_object_bytes\": %zu,\n",
+             grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, kernarg_size, device, cc_major, cc_minor,
+             image_size);
+    j += b;
+    j += "  \"kernarg_layout\": [";
+    for (size_t i = 0; i < layout.size(); ++i) {
+        snprintf(b, sizeof b, "%s{\"offset\": %zu, \"size\": %zu}", i ? ", " : "", layout[i].first, layout[i].second);
+        j += b;
+    }
+    j += "],\n  \"hash\": {\"algo\": \"xxh64\", \"seed\": 0, \"chunk_bytes\": 65536}\n}\n";
+    return j;
+}
+
+std::string regions_json(const std::vector<MetaRegion>& rs) {
+    std::string m = "[\n";
+    char b[512];
+    for (size_t i = 0; i < rs.size(); ++i) {
+        const MetaRegion& r = rs[i];
+        const std::string hx = hex_base(r.base);
+        const char* kind = r.kind == KC_KIND_VMM ? "vmm" : (r.kind == KC_KIND_POOL ? "pool" : "mem_alloc");
+        snprintf(b, sizeof b,
+                 "  {\"base\": \"%s\", \"size\": %llu, \"alloc_kind\": \"%s\", \"device\": %d, "
+                 "\"contains_kernarg\": false, \"data_file\": \"memory/region_%s.bin\", \"n_chunks\": %llu, "
+                 "\"digest\": \"%s\", \"status\": \"%s\", \"seq\": %llu}%s\n",
+                 hx.c_str(), (unsigned long long)r.size, kind, r.device, hx.c_str(), (unsigned long long)r.n_chunks,
+                 hex16(r.digest).c_str(), r.ok ? "ok" : "failed", (unsigned long long)r.seq,
+                 i + 1 < rs.size() ? "," : "");
+        m += b;
+    }
+    return m + "]\n";
+}
+
+std::string capture_log_json(const std::vector<LogRegion>& rs, const kc_capture_report& rep, uint64_t io_chunk,
+                             uint32_t depth, const char* sink) {
+    std::string out = "{\n  \"regions\": [\n";
+    char b[768];
+    for (size_t i = 0; i < rs.size(); ++i) {
+        snprintf(b, sizeof b,
+                 "    {\"base\": \"%s\", \"status\": \"%s\", \"error\": \"%s\", \"post_digest\": \"%s\", "
+                 "\"written_chunks\": %llu}%s\n",
+                 hex_base(rs[i].base).c_str(), rs[i].ok ? "ok" : "failed", kcj::esc(rs[i].error).c_str(),
+                 hex16(rs[i].post_digest).c_str(), (unsigned long long)rs[i].written, i + 1 < rs.size() ? "," : "");
+        out += b;
+    }
+    snprintf(b, sizeof b,
+             "  ],\n  \"sink\": \"%s\",\n  \"snapshot_digest\": \"%s\",\n  \"written_chunks\": %llu,\n"
+             "  \"d2h_bytes\": %llu,\n  \"dma_calls\": %llu,\n  \"io_chunk_bytes\": %llu,\n  \"pinned_depth\": %u,\n"
+             "  \"staging_high_water\": %llu,\n  \"t_hash_pre_s\": %.6f,\n  \"t_d2h_s\": %.6f,\n"
+             "  \"t_dispatch_s\": %.6f,\n  \"t_hash_post_s\": %.6f,\n  \"t_total_s\": %.6f\n}\n",
+             sink, hex16(rep.snapshot_digest).c_str(), (unsigned long long)rep.written_chunks,
+             (unsigned long long)rep.d2h_bytes, (unsigned long long)rep.dma_calls, (unsigned long long)io_chunk, depth,
+             (unsigned long long)rep.staging_high_water, rep.t_hash_pre_s, rep.t_d2h_s, rep.t_dispatch_s,
+             rep.t_hash_post_s, rep.t_total_s);
+    return out + b;
+}
+
 struct RegionState {
     kc_region r;
     bool ok = true;
@@ -441,47 +525,16 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
     }
 
     auto write_metadata = [&](bool post_digests) -> bool {
-        int cc_major = 0, cc_minor = 0;
-        cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, ctx->device);
-        cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, ctx->device);
-        std::string j = "{\n";
-        j += "  \"format\": \"kc-snapshot/1\",\n";
-        j += std::string("  \"mode\": \"") + (mode == KC_MODE_PRE_W ? "pre_w" : "post") + "\",\n";
-        j += "  \"mangled_symbol\": \"" + kcj::esc(mangled) + "\",\n";
-        char b[512];
-        snprintf(b, sizeof b,
-                 "  \"grid\": [%u, %u, %u],\n  \"block\": [%u, %u, %u],\n  \"cluster\": [1, 1, 1],\n"
-                 "  \"shared_mem_bytes\": %u,\n  \"kernarg_size\": %u,\n  \"device_ordinal\": %d,\n"
-                 "  \"compute_capability\": \"%d.%d\",\n  \"code_object_bytes\": %zu,\n",
-                 d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2], d->smem_bytes,
-                 d->kernarg_size, ctx->device, cc_major, cc_minor, d->image ? d->image_size : (size_t)0);
-        j += b;
-        j += "  \"kernarg_layout\": [";
-        for (size_t i = 0; i < layout.size(); ++i) {
-            snprintf(b, sizeof b, "%s{\"offset\": %zu, \"size\": %zu}", i ? ", " : "", layout[i].first,
-                     layout[i].second);
-            j += b;
-        }
-        j += "],\n  \"hash\": {\"algo\": \"xxh64\", \"seed\": 0, \"chunk_bytes\": 65536}\n}\n";
+        const std::string j = dispatch_json(mode, mangled, d->grid, d->block, d->smem_bytes, d->kernarg_size,
+                                            ctx->device, d->image ? d->image_size : (size_t)0, layout);
         if (!write_text(dir + "/dispatch.json", j)) return false;
         if (!write_file(dir + "/kernarg.bin", d->kernarg, d->kernarg ? d->kernarg_size : 0)) return false;
         if (d->image && d->image_size && !write_file(dir + "/kernel.cubin", d->image, d->image_size)) return false;
-        std::string m = "[\n";
-        for (size_t i = 0; i < rs.size(); ++i) {
-            const RegionState& r = rs[i];
-            const std::string hx = hex_base(r.r.base);
-            const char* kind = r.r.kind == KC_KIND_VMM ? "vmm" : (r.r.kind == KC_KIND_POOL ? "pool" : "mem_alloc");
-            snprintf(b, sizeof b,
-                     "  {\"base\": \"%s\", \"size\": %llu, \"alloc_kind\": \"%s\", \"device\": %d, "
-                     "\"contains_kernarg\": false, \"data_file\": \"memory/region_%s.bin\", \"n_chunks\": %llu, "
-                     "\"digest\": \"%s\", \"status\": \"%s\", \"seq\": %llu}%s\n",
-                     hx.c_str(), (unsigned long long)r.r.size, kind, r.r.device, hx.c_str(),
-                     (unsigned long long)r.n_chunks, hex16(post_digests ? r.post_digest : r.pre_digest).c_str(),
-                     r.ok ? "ok" : "failed", (unsigned long long)r.r.seq, i + 1 < rs.size() ? "," : "");
-            m += b;
-        }
-        m += "]\n";
-        return write_text(dir + "/memory_regions.json", m);
+        std::vector<MetaRegion> mr;
+        for (const RegionState& r : rs)
+            mr.push_back({r.r.base, r.r.size, r.n_chunks, post_digests ? r.post_digest : r.pre_digest, r.r.seq,
+                          r.r.kind, r.r.device, r.ok});
+        return write_text(dir + "/memory_regions.json", regions_json(mr));
     };
 
     // region files: region bytes (parallel workers) + the matching manifest slice
@@ -661,29 +714,13 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
 
     // ---- capture_log.json, then the sentinel LAST
     rep.snapshot_digest = mode == KC_MODE_PRE_W ? pre_snap : post_snap;  // S of the region files written
-    std::string lg = "{\n  \"regions\": [\n";
-    char b[512];
-    for (size_t i = 0; i < rs.size(); ++i) {
-        const RegionState& r = rs[i];
+    std::vector<LogRegion> lr;
+    for (const RegionState& r : rs) {
         if (!r.ok) rep.n_failed_regions++;
-        snprintf(b, sizeof b,
-                 "    {\"base\": \"%s\", \"status\": \"%s\", \"error\": \"%s\", \"post_digest\": \"%s\", "
-                 "\"written_chunks\": %zu}%s\n",
-                 hex_base(r.r.base).c_str(), r.ok ? "ok" : "failed", kcj::esc(r.error).c_str(),
-                 hex16(r.post_digest).c_str(), r.written.size(), i + 1 < rs.size() ? "," : "");
-        lg += b;
+        lr.push_back({r.r.base, r.post_digest, (uint64_t)r.written.size(), r.ok, r.error});
     }
     rep.t_total_s = now_s() - t0;
-    snprintf(b, sizeof b,
-             "  ],\n  \"snapshot_digest\": \"%s\",\n  \"written_chunks\": %llu,\n  \"d2h_bytes\": %llu,\n"
-             "  \"dma_calls\": %llu,\n  \"io_chunk_bytes\": %llu,\n  \"pinned_depth\": %u,\n"
-             "  \"staging_high_water\": %llu,\n  \"t_hash_pre_s\": %.6f,\n  \"t_d2h_s\": %.6f,\n"
-             "  \"t_dispatch_s\": %.6f,\n  \"t_hash_post_s\": %.6f,\n  \"t_total_s\": %.6f\n}\n",
-             hex16(rep.snapshot_digest).c_str(), (unsigned long long)rep.written_chunks,
-             (unsigned long long)rep.d2h_bytes, (unsigned long long)rep.dma_calls, (unsigned long long)ctx->io_chunk,
-             ctx->depth, (unsigned long long)rep.staging_high_water, rep.t_hash_pre_s, rep.t_d2h_s, rep.t_dispatch_s,
-             rep.t_hash_post_s, rep.t_total_s);
-    lg += b;
+    const std::string lg = capture_log_json(lr, rep, ctx->io_chunk, ctx->depth, "files");
     if (!write_text(dir + "/capture_log.json", lg)) return set_err(ctx, KC_ERR_IO, "cannot write capture_log.json");
     if (!write_file(dir + "/capture_complete", "", 0)) return set_err(ctx, KC_ERR_IO, "cannot write sentinel");
     if (rep_out) *rep_out = rep;
@@ -832,20 +869,46 @@ static std::string maps_overlapping(uint64_t lo, uint64_t hi) {
     return out.empty() ? "no host mapping overlaps (driver-internal VA)" : out;
 }
 
-extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** out, kc_restore_report* rep_out) {
-    if (!ctx || !dir_c || !out) return KC_ERR_ARG;
-    if (ctx->poisoned) return KC_ERR_CUDA;
-    *out = nullptr;
-    kc_restore_report rep;
-    memset(&rep, 0, sizeof rep);
-    const double t0 = now_s();
-    const std::string dir = dir_c;
-    {
-        struct stat sb;
-        if (stat((dir + "/capture_complete").c_str(), &sb) != 0)
-            return set_err(ctx, KC_ERR_FORMAT, "%s: no capture_complete sentinel (incomplete capture)", dir_c);
-    }
-    // ---- stage 1: parse metadata
+// ====================================================================== restore core
+// A snapshot's contents independent of where the bytes live (files or a
+// device arena); restore_core maps the captured VAs and pulls the bytes
+// through a RestoreSource.
+struct SnapRegion {
+    kc_region r;
+    std::string hx;
+    bool ok = true;
+    uint64_t n_chunks = 0;
+    uint64_t digest = 0, post_digest = 0;
+    std::vector<uint64_t> manifest;       // manifest of the stored bytes
+    std::vector<uint64_t> post_manifest;  // post-dispatch manifest
+    std::vector<uint64_t> written;        // W chunk indices
+};
+
+struct SnapDesc {
+    int mode = KC_MODE_PRE_W;
+    std::string mangled;
+    uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0;
+    std::vector<uint8_t> kernarg, image;
+    std::vector<std::pair<size_t, size_t>> layout;  // kernarg (offset, size)
+    std::vector<SnapRegion> regions;                 // ascending base
+    uint64_t snapshot_digest = 0;
+};
+
+struct RestoreSource {
+    virtual ~RestoreSource() {}
+    // stored bytes of every ok region -> its (mapped, zero-filled) VA
+    virtual kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) = 0;
+    // PRE_W: the captured post-dispatch bytes of region i's W chunks, concatenated, -> device dst
+    virtual kc_status written_ref(kc_ctx* ctx, const SnapDesc& d, size_t i, void* dst, uint64_t bytes) = 0;
+};
+
+namespace {
+
+kc_status load_desc_files(kc_ctx* ctx, const std::string& dir, SnapDesc& d, kc_restore_report& rep) {
+    struct stat sb;
+    if (stat((dir + "/capture_complete").c_str(), &sb) != 0)
+        return set_err(ctx, KC_ERR_FORMAT, "%s: no capture_complete sentinel (incomplete capture)", dir.c_str());
+    // stage 1: parse metadata
     std::string dtext;
     if (!kcj::read_file(dir + "/dispatch.json", dtext)) return set_err(ctx, KC_ERR_FORMAT, "cannot read dispatch.json");
     kcj::Value dv;
@@ -853,49 +916,133 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
     std::vector<ParsedRegion> regs;
     kc_status st = parse_regions(ctx, dir, regs);
     if (st != KC_OK) return st;
-
-    kc_restored* h = new kc_restored();
-    h->ctx = ctx;
-    h->dir = dir;
-    h->mode = dv.get("mode") && dv.get("mode")->s == "post" ? KC_MODE_POST : KC_MODE_PRE_W;
-    h->mangled = dv.get("mangled_symbol") ? dv.get("mangled_symbol")->s : "";
+    d.mode = dv.get("mode") && dv.get("mode")->s == "post" ? KC_MODE_POST : KC_MODE_PRE_W;
+    d.mangled = dv.get("mangled_symbol") ? dv.get("mangled_symbol")->s : "";
     if (const kcj::Value* g = dv.get("grid"))
-        for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) h->grid[i] = (uint32_t)g->a[i].as_u64(1);
+        for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) d.grid[i] = (uint32_t)g->a[i].as_u64(1);
     if (const kcj::Value* g = dv.get("block"))
-        for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) h->block[i] = (uint32_t)g->a[i].as_u64(1);
-    if (const kcj::Value* g = dv.get("shared_mem_bytes")) h->smem = (uint32_t)g->as_u64();
-    if (!read_bin(dir + "/kernarg.bin", h->kernarg)) {
-        delete h;
-        return set_err(ctx, KC_ERR_FORMAT, "cannot read kernarg.bin");
-    }
-    const uint64_t ksz = dv.get("kernarg_size") ? dv.get("kernarg_size")->as_u64() : h->kernarg.size();
-    if (ksz != h->kernarg.size()) {
-        delete h;
-        return set_err(ctx, KC_ERR_FORMAT, "kernarg.bin has %zu bytes, dispatch.json says %llu", h->kernarg.size(),
+        for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) d.block[i] = (uint32_t)g->a[i].as_u64(1);
+    if (const kcj::Value* g = dv.get("shared_mem_bytes")) d.smem = (uint32_t)g->as_u64();
+    if (!read_bin(dir + "/kernarg.bin", d.kernarg)) return set_err(ctx, KC_ERR_FORMAT, "cannot read kernarg.bin");
+    const uint64_t ksz = dv.get("kernarg_size") ? dv.get("kernarg_size")->as_u64() : d.kernarg.size();
+    if (ksz != d.kernarg.size())
+        return set_err(ctx, KC_ERR_FORMAT, "kernarg.bin has %zu bytes, dispatch.json says %llu", d.kernarg.size(),
                        (unsigned long long)ksz);
-    }
+    read_bin(dir + "/kernel.cubin", d.image);
     for (auto& r : regs) {
-        kc_restored_region rr;
-        rr.r.base = r.base;
-        rr.r.size = r.size;
-        rr.r.device = ctx->device;
-        rr.r.kind = r.kind;
-        rr.r.seq = 0;
-        rr.hexbase = r.hx;
-        rr.ok = r.ok;
-        rr.n_chunks = (r.size + kChunk - 1) / kChunk;
+        SnapRegion sr;
+        sr.r.base = r.base;
+        sr.r.size = r.size;
+        sr.r.device = ctx->device;
+        sr.r.kind = r.kind;
+        sr.r.seq = r.seq;
+        sr.hx = r.hx;
+        sr.ok = r.ok;
+        sr.n_chunks = (r.size + kChunk - 1) / kChunk;
         if (r.ok) {
-            read_u64s(dir + "/written/region_" + r.hx + ".idx", rr.written);
-            const std::string pm = dir + (h->mode == KC_MODE_PRE_W ? "/post/region_" : "/memory/region_") + r.hx + ".xxh64";
-            read_u64s(pm, rr.post_manifest);
+            read_u64s(dir + "/written/region_" + r.hx + ".idx", sr.written);
+            read_u64s(dir + "/memory/region_" + r.hx + ".xxh64", sr.manifest);
+            const std::string pm = dir + (d.mode == KC_MODE_PRE_W ? "/post/region_" : "/memory/region_") + r.hx + ".xxh64";
+            read_u64s(pm, sr.post_manifest);
         } else {
             rep.n_failed_regions++;
         }
-        h->regions.push_back(rr);
+        d.regions.push_back(std::move(sr));
     }
-    rep.n_regions = regs.size();
+    return KC_OK;
+}
 
-    // ---- stages 2-4: placeholders released, exact-VA reservation
+struct FileSource : RestoreSource {
+    std::string dir;
+    explicit FileSource(std::string d) : dir(std::move(d)) {}
+    kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) override {
+        // every region file must exist with exactly `size` bytes (O1)
+        std::vector<std::pair<size_t, uint64_t>> todo;
+        for (size_t i = 0; i < d.regions.size(); ++i) {
+            const auto& sr = d.regions[i];
+            if (!sr.ok) continue;
+            const std::string path = dir + "/memory/region_" + sr.hx + ".bin";
+            struct stat sb;
+            if (stat(path.c_str(), &sb) != 0 || (uint64_t)sb.st_size != sr.r.size)
+                return set_err(ctx, KC_ERR_FORMAT, "kc_restore: %s: missing or wrong length", path.c_str());
+            todo.emplace_back(i, sr.r.size);
+        }
+        const int T = io_threads();
+        kc_status st = ensure_io(ctx, T);
+        if (st != KC_OK) return st;
+        const std::vector<IoItem> items = make_items(todo);
+        std::atomic<int> bad{0};
+        std::mutex emu;
+        std::string first_err;
+        std::atomic<uint64_t> h2d{0};
+        run_pool(T, items.size(), [&](int t, size_t k) {
+            if (bad) return;
+            const IoItem& it = items[k];
+            cudaSetDevice(ctx->device);
+            const auto& sr = d.regions[it.region];
+            const std::string path = dir + "/memory/region_" + sr.hx + ".bin";
+            int fd = open(path.c_str(), O_RDONLY);
+            std::string err = fd < 0 ? "cannot open" : "";
+            const bool ok = fd >= 0 && item_h2d(ctx, ctx->io[t], fd, sr.r.base, it, err);
+            if (fd >= 0) close(fd);
+            if (ok) {
+                h2d.fetch_add(it.len);
+            } else if (!bad.exchange(1)) {
+                std::lock_guard<std::mutex> lk(emu);
+                first_err = path + ": " + err;
+            }
+        });
+        rep.h2d_bytes += h2d.load();
+        if (bad) return set_err(ctx, KC_ERR_FORMAT, "kc_restore: copy-in failed: %s", first_err.c_str());
+        return KC_OK;
+    }
+    kc_status written_ref(kc_ctx* ctx, const SnapDesc& d, size_t i, void* dst, uint64_t bytes) override {
+        std::vector<uint8_t> wb;
+        if (!read_bin(dir + "/written/region_" + d.regions[i].hx + ".bin", wb) || wb.size() != bytes)
+            return set_err(ctx, KC_ERR_FORMAT, "written/region_%s.bin is missing or has the wrong length",
+                           d.regions[i].hx.c_str());
+        KC_CHECK_CUDA(ctx, cudaMemcpy(dst, wb.data(), bytes, cudaMemcpyHostToDevice), "H2D written reference");
+        return KC_OK;
+    }
+};
+
+}  // namespace
+
+static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src, kc_restored** out,
+                              kc_restore_report* rep_out, kc_restore_report& rep, double t0) {
+    kc_restored* h = new kc_restored();
+    h->ctx = ctx;
+    h->mode = d.mode;
+    h->mangled = d.mangled;
+    for (int i = 0; i < 3; ++i) {
+        h->grid[i] = d.grid[i];
+        h->block[i] = d.block[i];
+    }
+    h->smem = d.smem;
+    h->kernarg = d.kernarg;
+    h->image = d.image;
+    std::vector<ParsedRegion> regs;
+    for (auto& sr : d.regions) {
+        kc_restored_region rr;
+        rr.r = sr.r;
+        rr.hexbase = sr.hx;
+        rr.ok = sr.ok;
+        rr.n_chunks = sr.n_chunks;
+        rr.written = sr.written;
+        rr.post_manifest = sr.post_manifest;
+        h->regions.push_back(rr);
+        ParsedRegion p;
+        p.base = sr.r.base;
+        p.size = sr.r.size;
+        p.kind = sr.r.kind;
+        p.ok = sr.ok;
+        p.hx = sr.hx;
+        p.seq = sr.r.seq;
+        regs.push_back(p);
+    }
+    rep.n_regions = d.regions.size();
+
+    // ---- stages 2-4: exact-VA reservation (R28)
     if (!bind_device(ctx)) {
         delete h;
         return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -1019,75 +1166,25 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
     rep.n_spans = h->spans.size();
     rep.t_reserve_s = now_s() - t;
 
-    // ---- stage 5a: copy-in (pinned ring; gaps and failed regions zero-filled)
+    // ---- stage 5a: copy-in (gaps and failed regions zero-filled)
     t = now_s();
-    st = ensure_pinned(ctx);
+    kc_status st = ensure_pinned(ctx);
     if (st != KC_OK) {
         rollback(h);
         delete h;
         return st;
     }
-    for (auto& s : h->spans) {
+    for (auto& s : h->spans)
         if (!s.fallback) cudaMemsetAsync((void*)s.base, 0, s.size, ctx->copy_stream);
-    }
     for (auto& rr : h->regions) cudaMemsetAsync((void*)rr.r.base, 0, rr.r.size, ctx->copy_stream);
-    {
-        // every region file must exist with exactly `size` bytes (O1)
-        std::vector<std::pair<size_t, uint64_t>> todo;
-        for (size_t i = 0; i < h->regions.size(); ++i) {
-            const auto& rr = h->regions[i];
-            if (!rr.ok) continue;
-            const std::string path = dir + "/memory/region_" + rr.hexbase + ".bin";
-            struct stat sb;
-            if (stat(path.c_str(), &sb) != 0 || (uint64_t)sb.st_size != rr.r.size) {
-                rollback(h);
-                delete h;
-                return set_err(ctx, KC_ERR_FORMAT, "kc_restore: %s: missing or wrong length", path.c_str());
-            }
-            todo.emplace_back(i, rr.r.size);
-        }
-        cudaStreamSynchronize(ctx->copy_stream);  // zero-fill first
-        const int T = io_threads();
-        st = ensure_io(ctx, T);
-        if (st != KC_OK) {
-            rollback(h);
-            delete h;
-            return st;
-        }
-        const std::vector<IoItem> items = make_items(todo);
-        std::atomic<int> bad{0};
-        std::mutex emu;
-        std::string first_err;
-        std::atomic<uint64_t> h2d{0};
-        run_pool(T, items.size(), [&](int t, size_t k) {
-            if (bad) return;
-            const IoItem& it = items[k];
-            cudaSetDevice(ctx->device);
-            const auto& rr = h->regions[it.region];
-            const std::string path = dir + "/memory/region_" + rr.hexbase + ".bin";
-            int fd = open(path.c_str(), O_RDONLY);
-            std::string err = fd < 0 ? "cannot open" : "";
-            const bool ok = fd >= 0 && item_h2d(ctx, ctx->io[t], fd, rr.r.base, it, err);
-            if (fd >= 0) close(fd);
-            if (ok) {
-                h2d.fetch_add(it.len);
-            } else if (!bad.exchange(1)) {
-                std::lock_guard<std::mutex> lk(emu);
-                first_err = path + ": " + err;
-            }
-        });
-        rep.h2d_bytes += h2d.load();
-        if (bad) {
-            rollback(h);
-            delete h;
-            return set_err(ctx, KC_ERR_FORMAT, "kc_restore: copy-in failed: %s", first_err.c_str());
-        }
-    }
+    cudaStreamSynchronize(ctx->copy_stream);  // zero-fill before the copy-in streams
+    st = src.copy_in(ctx, d, rep);
     cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
-    if (ce != cudaSuccess) {
+    if (st == KC_OK && ce != cudaSuccess) st = cuda_err(ctx, ce, "kc_restore: copy-in");
+    if (st != KC_OK) {
         rollback(h);
         delete h;
-        return cuda_err(ctx, ce, "kc_restore: copy-in");
+        return st;
     }
     rep.t_h2d_s = now_s() - t;
 
@@ -1105,15 +1202,14 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
     }
     {
         uint64_t c = 0, mism = 0;
-        for (auto& rr : h->regions) {
-            if (!rr.ok) continue;
-            std::vector<uint64_t> man;
-            if (!read_u64s(dir + "/memory/region_" + rr.hexbase + ".xxh64", man) || man.size() != rr.n_chunks) {
-                mism += rr.n_chunks;
+        for (auto& sr : d.regions) {
+            if (!sr.ok) continue;
+            if (sr.manifest.size() != sr.n_chunks) {
+                mism += sr.n_chunks;
             } else {
-                for (uint64_t k = 0; k < rr.n_chunks; ++k) mism += man[k] != got[c + k];
+                for (uint64_t k = 0; k < sr.n_chunks; ++k) mism += sr.manifest[k] != got[c + k];
             }
-            c += rr.n_chunks;
+            c += sr.n_chunks;
         }
         rep.verify_mismatch_chunks = mism;
     }
@@ -1142,34 +1238,28 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
             delete h;
             return set_err(ctx, KC_ERR_NOMEM, "kc_restore: stash of %llu bytes", (unsigned long long)total);
         }
-        for (auto& rr : h->regions) {
+        for (size_t i = 0; i < h->regions.size(); ++i) {
+            auto& rr = h->regions[i];
             if (!rr.ok || rr.written.empty()) continue;
-            std::vector<uint8_t> wb;
-            if (h->mode == KC_MODE_PRE_W && !read_bin(dir + "/written/region_" + rr.hexbase + ".bin", wb)) {
-                rollback(h);
-                delete h;
-                return set_err(ctx, KC_ERR_FORMAT, "missing written/region_%s.bin", rr.hexbase.c_str());
-            }
-            uint64_t woff = 0;
+            uint64_t wbytes = 0;
             for (size_t j = 0; j < rr.written.size(); ++j) {
                 const uint64_t k = rr.written[j];
                 const uint64_t len = std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
-                uint8_t* pre = (uint8_t*)h->stash_pre + rr.stash_off[j];
-                uint8_t* ref = (uint8_t*)h->stash_ref + rr.stash_off[j];
-                cudaMemcpyAsync(pre, (const void*)(rr.r.base + k * kChunk), len, cudaMemcpyDeviceToDevice,
-                                ctx->copy_stream);
-                if (h->mode == KC_MODE_PRE_W) {
-                    if (woff + len > wb.size()) {
-                        rollback(h);
-                        delete h;
-                        return set_err(ctx, KC_ERR_FORMAT, "written/region_%s.bin is short", rr.hexbase.c_str());
-                    }
-                    cudaMemcpy(ref, wb.data() + woff, len, cudaMemcpyHostToDevice);
-                } else {
-                    cudaMemcpyAsync(ref, (const void*)(rr.r.base + k * kChunk), len, cudaMemcpyDeviceToDevice,
-                                    ctx->copy_stream);
+                cudaMemcpyAsync((uint8_t*)h->stash_pre + rr.stash_off[j], (const void*)(rr.r.base + k * kChunk), len,
+                                cudaMemcpyDeviceToDevice, ctx->copy_stream);
+                if (h->mode != KC_MODE_PRE_W)
+                    cudaMemcpyAsync((uint8_t*)h->stash_ref + rr.stash_off[j], (const void*)(rr.r.base + k * kChunk),
+                                    len, cudaMemcpyDeviceToDevice, ctx->copy_stream);
+                wbytes += len;
+            }
+            if (h->mode == KC_MODE_PRE_W) {
+                cudaStreamSynchronize(ctx->copy_stream);
+                st = src.written_ref(ctx, d, i, (uint8_t*)h->stash_ref + rr.stash_off[0], wbytes);
+                if (st != KC_OK) {
+                    rollback(h);
+                    delete h;
+                    return st;
                 }
-                woff += len;
             }
         }
         ce = cudaStreamSynchronize(ctx->copy_stream);
@@ -1183,6 +1273,417 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
     if (rep_out) *rep_out = rep;
     *out = h;
     return KC_OK;
+}
+
+extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** out, kc_restore_report* rep_out) {
+    if (!ctx || !dir_c || !out) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    *out = nullptr;
+    kc_restore_report rep;
+    memset(&rep, 0, sizeof rep);
+    const double t0 = now_s();
+    SnapDesc d;
+    kc_status st = load_desc_files(ctx, dir_c, d, rep);
+    if (st != KC_OK) return st;
+    FileSource src(dir_c);
+    st = restore_core(ctx, d, src, out, rep_out, rep, t0);
+    if (st == KC_OK) (*out)->dir = dir_c;
+    return st;
+}
+
+// ====================================================================== F1 device-resident snapshot
+// kc_capture with the region bytes kept in an HBM arena: D2D copies at HBM
+// bandwidth replace PCIe + files.  Big regions go through
+// cudaMemcpyAsync, regions and W chunks under 1 MiB through the K4 gather.
+struct kc_snapshot {
+    kc_ctx* ctx = nullptr;
+    SnapDesc desc;
+    void* arena = nullptr;  // stored bytes, region i at off[i] (256 B aligned)
+    uint64_t arena_bytes = 0;
+    std::vector<uint64_t> off;
+    void* warena = nullptr;  // PRE_W: post bytes of W, region i at w_off[i]
+    uint64_t w_bytes = 0;
+    std::vector<uint64_t> w_off;
+    kc_capture_report rep;
+};
+
+namespace {
+
+// device copies of (src, dst, len) ranges: >= 1 MiB by cudaMemcpyAsync, smaller ones batched through K4
+kc_status copy_ranges_d2d(kc_ctx* ctx, const std::vector<std::array<uint64_t, 3>>& ranges, cudaStream_t s,
+                          uint64_t* calls) {
+    std::vector<uint64_t> src, dst, len;
+    for (auto& r : ranges) {
+        if (r[2] == 0) continue;
+        if (r[2] >= (1ull << 20)) {
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync((void*)r[1], (const void*)r[0], r[2], cudaMemcpyDeviceToDevice, s),
+                          "D2D copy");
+            if (calls) ++*calls;
+        } else {
+            src.push_back(r[0]);
+            dst.push_back(r[1]);
+            len.push_back(r[2]);
+        }
+    }
+    if (!src.empty()) {
+        const size_t n = src.size();
+        kc_ctx_dev_buf tab;
+        KC_CHECK_CUDA(ctx, ensure(tab, 3 * 8 * n), "cudaMalloc(gather table)");
+        uint64_t* t = (uint64_t*)tab.p;
+        cudaMemcpyAsync(t, src.data(), 8 * n, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(t + n, dst.data(), 8 * n, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(t + 2 * n, len.data(), 8 * n, cudaMemcpyHostToDevice, s);
+        KC_CHECK_CUDA(ctx, launch_gather(t, t + n, t + 2 * n, (int)n, s), "launch K4");
+        ctx->launches += 1;
+        if (calls) ++*calls;
+        cudaError_t e = cudaStreamSynchronize(s);
+        cudaFree(tab.p);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "K4 gather");
+    }
+    return KC_OK;
+}
+
+struct DevSource : RestoreSource {
+    const kc_snapshot* sn;
+    explicit DevSource(const kc_snapshot* s) : sn(s) {}
+    kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) override {
+        std::vector<std::array<uint64_t, 3>> ranges;
+        for (size_t i = 0; i < d.regions.size(); ++i) {
+            if (!d.regions[i].ok) continue;
+            ranges.push_back({(uint64_t)sn->arena + sn->off[i], d.regions[i].r.base, d.regions[i].r.size});
+            rep.h2d_bytes += d.regions[i].r.size;  // bytes copied in (device to device here)
+        }
+        return copy_ranges_d2d(ctx, ranges, ctx->copy_stream, nullptr);
+    }
+    kc_status written_ref(kc_ctx* ctx, const SnapDesc&, size_t i, void* dst, uint64_t bytes) override {
+        KC_CHECK_CUDA(ctx, cudaMemcpy(dst, (const uint8_t*)sn->warena + sn->w_off[i], bytes, cudaMemcpyDeviceToDevice),
+                      "D2D written reference");
+        return KC_OK;
+    }
+};
+
+}  // namespace
+
+extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
+                                    kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
+    if (!ctx) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    if (!d || !out) return set_err(ctx, KC_ERR_ARG, "kc_capture_dev: dispatch and out are required");
+    if (mode != KC_MODE_PRE_W && mode != KC_MODE_POST) return set_err(ctx, KC_ERR_ARG, "kc_capture_dev: bad mode");
+    *out = nullptr;
+    kc_capture_report rep;
+    memset(&rep, 0, sizeof rep);
+    const double t0 = now_s();
+    cudaStream_t cs = (cudaStream_t)d->stream;
+    std::vector<kc_region> list;
+    if (regions) {
+        list.assign(regions, regions + n);
+    } else {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        for (auto& kv : ctx->live) list.push_back(kv.second);
+    }
+    list.erase(std::remove_if(list.begin(), list.end(), [](const kc_region& r) { return r.size == 0; }), list.end());
+    std::sort(list.begin(), list.end(), [](const kc_region& a, const kc_region& b) { return a.base < b.base; });
+    for (size_t i = 1; i < list.size(); ++i)
+        if (list[i].base < list[i - 1].base + list[i - 1].size)
+            return set_err(ctx, KC_ERR_ARG, "kc_capture_dev: regions overlap at 0x%llx",
+                           (unsigned long long)list[i].base);
+    // ---- resolve the function
+    CUfunction f = (CUfunction)d->func;
+    CUmodule own_mod = nullptr;
+    if (!f) {
+        if (!d->image || !d->mangled) return set_err(ctx, KC_ERR_ARG, "kc_capture_dev: need func or image+mangled");
+        KC_CHECK_CU(ctx, KC_DRV(cuModuleLoadData)(&own_mod, d->image), "cuModuleLoadData");
+        if (KC_DRV(cuModuleGetFunction)(&f, own_mod, d->mangled) != CUDA_SUCCESS) {
+            KC_DRV(cuModuleUnload)(own_mod);
+            return set_err(ctx, KC_ERR_ARG, "kc_capture_dev: symbol %s not found in image", d->mangled);
+        }
+    }
+    kc_snapshot* sn = new kc_snapshot();
+    sn->ctx = ctx;
+    SnapDesc& D = sn->desc;
+    D.mode = mode;
+    D.mangled = d->mangled ? d->mangled : "";
+    if (D.mangled.empty()) {
+        const char* nm = nullptr;
+        if (KC_DRV(cuFuncGetName)(&nm, f) == CUDA_SUCCESS && nm) D.mangled = nm;
+    }
+    for (size_t i = 0; i < 4096; ++i) {
+        size_t o = 0, z = 0;
+        if (KC_DRV(cuFuncGetParamInfo)(f, i, &o, &z) != CUDA_SUCCESS) break;
+        D.layout.emplace_back(o, z);
+    }
+    auto fail = [&](kc_status st) {
+        if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+        kc_snapshot_free(sn);
+        return st;
+    };
+    if (!D.layout.empty() && d->kernarg && d->kernarg_size != D.layout.back().first + D.layout.back().second)
+        return fail(set_err(ctx, KC_ERR_ARG, "kc_capture_dev: kernarg_size %u != parameter buffer size %zu",
+                            d->kernarg_size, D.layout.back().first + D.layout.back().second));
+    for (int i = 0; i < 3; ++i) {
+        D.grid[i] = d->grid[i];
+        D.block[i] = d->block[i];
+    }
+    D.smem = d->smem_bytes;
+    if (d->kernarg && d->kernarg_size)
+        D.kernarg.assign((const uint8_t*)d->kernarg, (const uint8_t*)d->kernarg + d->kernarg_size);
+    if (d->image && d->image_size) D.image.assign((const uint8_t*)d->image, (const uint8_t*)d->image + d->image_size);
+
+    // ---- A3 bracket: quiesce, liveness, K1 pre-manifest
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return fail(cuda_err(ctx, e, "kc_capture_dev: quiesce"));
+    std::vector<kc_region> live;
+    std::vector<uint64_t> pre_off;  // manifest offset per region (ok regions)
+    for (auto& r : list) {
+        SnapRegion sr;
+        sr.r = r;
+        sr.hx = hex_base(r.base);
+        sr.n_chunks = (r.size + kChunk - 1) / kChunk;
+        sr.ok = region_live(ctx, r.base, r.size);
+        pre_off.push_back(kc_count_chunks(live.data(), live.size()));
+        if (sr.ok) live.push_back(r);
+        D.regions.push_back(std::move(sr));
+    }
+    rep.n_regions = D.regions.size();
+    double t = now_s();
+    std::vector<uint64_t> pre_h, pre_dig, post_h, post_dig;
+    uint64_t pre_snap = 0, post_snap = 0;
+    kc_status st = hash_regions_sync(ctx, live, pre_h, &pre_dig, &pre_snap, nullptr, cs);
+    if (st != KC_OK) return fail(st);
+    rep.t_hash_pre_s = now_s() - t;
+    rep.n_chunks = pre_h.size();
+    for (auto& r : live) rep.total_bytes += r.size;
+
+    // ---- the arena
+    uint64_t total = 0;
+    for (auto& sr : D.regions) {
+        sn->off.push_back(total);
+        if (sr.ok) total += (sr.r.size + 255) / 256 * 256;
+    }
+    sn->arena_bytes = total;
+    if (total && cudaMalloc(&sn->arena, total) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: cannot allocate a %llu-byte device arena",
+                            (unsigned long long)total));
+    }
+    auto snapshot_regions = [&]() -> kc_status {
+        std::vector<std::array<uint64_t, 3>> ranges;
+        for (size_t i = 0; i < D.regions.size(); ++i)
+            if (D.regions[i].ok) ranges.push_back({D.regions[i].r.base, (uint64_t)sn->arena + sn->off[i],
+                                                   D.regions[i].r.size});
+        kc_status s2 = copy_ranges_d2d(ctx, ranges, ctx->copy_stream ? ctx->copy_stream : cs, &rep.dma_calls);
+        cudaStreamSynchronize(ctx->copy_stream);
+        return s2;
+    };
+    st = ensure_pinned(ctx);  // creates the copy stream
+    if (st != KC_OK) return fail(st);
+    double t_copy = 0;
+    if (mode == KC_MODE_PRE_W) {
+        t = now_s();
+        st = snapshot_regions();
+        if (st != KC_OK) return fail(st);
+        t_copy += now_s() - t;
+    }
+    // ---- forward the dispatch
+    t = now_s();
+    {
+        CUresult r;
+        if (d->kernarg && d->kernarg_size) {
+            size_t ksz = d->kernarg_size;
+            void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, (void*)d->kernarg, CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
+                             CU_LAUNCH_PARAM_END};
+            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
+                                       d->smem_bytes, (CUstream)cs, nullptr, extra);
+        } else {
+            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
+                                       d->smem_bytes, (CUstream)cs, nullptr, nullptr);
+        }
+        if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)cs);
+        if (r != CUDA_SUCCESS) return fail(cu_err(ctx, r, "kc_capture_dev: target dispatch"));
+    }
+    rep.t_dispatch_s = now_s() - t;
+    if (own_mod) {
+        KC_DRV(cuModuleUnload)(own_mod);
+        own_mod = nullptr;
+    }
+    // ---- K1 post-manifest + W
+    t = now_s();
+    st = hash_regions_sync(ctx, live, post_h, &post_dig, &post_snap, nullptr, cs);
+    if (st != KC_OK) return fail(st);
+    rep.t_hash_post_s = now_s() - t;
+    {
+        size_t j = 0;
+        for (size_t i = 0; i < D.regions.size(); ++i) {
+            SnapRegion& sr = D.regions[i];
+            if (!sr.ok) continue;
+            const uint64_t c0 = pre_off[i];
+            sr.post_manifest.assign(post_h.begin() + c0, post_h.begin() + c0 + sr.n_chunks);
+            std::vector<uint64_t> pm(pre_h.begin() + c0, pre_h.begin() + c0 + sr.n_chunks);
+            for (uint64_t k = 0; k < sr.n_chunks; ++k)
+                if (pm[k] != sr.post_manifest[k]) sr.written.push_back(k);
+            rep.written_chunks += sr.written.size();
+            sr.post_digest = post_dig[j];
+            if (mode == KC_MODE_PRE_W) {
+                sr.manifest = std::move(pm);
+                sr.digest = pre_dig[j];
+            } else {
+                sr.manifest = sr.post_manifest;
+                sr.digest = post_dig[j];
+            }
+            ++j;
+        }
+    }
+    D.snapshot_digest = mode == KC_MODE_PRE_W ? pre_snap : post_snap;
+    t = now_s();
+    if (mode == KC_MODE_POST) {
+        st = snapshot_regions();
+        if (st != KC_OK) return fail(st);
+    } else if (rep.written_chunks) {
+        uint64_t wtot = 0;
+        for (auto& sr : D.regions) {
+            sn->w_off.push_back(wtot);
+            for (uint64_t k : sr.written) wtot += std::min<uint64_t>(kChunk, sr.r.size - k * kChunk);
+        }
+        sn->w_bytes = wtot;
+        if (cudaMalloc(&sn->warena, wtot) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: W arena of %llu bytes", (unsigned long long)wtot));
+        }
+        std::vector<std::array<uint64_t, 3>> ranges;
+        for (size_t i = 0; i < D.regions.size(); ++i) {
+            uint64_t o = sn->w_off[i];
+            for (uint64_t k : D.regions[i].written) {
+                const uint64_t len = std::min<uint64_t>(kChunk, D.regions[i].r.size - k * kChunk);
+                ranges.push_back({D.regions[i].r.base + k * kChunk, (uint64_t)sn->warena + o, len});
+                o += len;
+            }
+        }
+        st = copy_ranges_d2d(ctx, ranges, ctx->copy_stream, &rep.dma_calls);
+        cudaStreamSynchronize(ctx->copy_stream);
+        if (st != KC_OK) return fail(st);
+    }
+    if (sn->w_off.empty()) sn->w_off.assign(D.regions.size(), 0);
+    t_copy += now_s() - t;
+    rep.t_d2h_s = t_copy;  // device-to-device here
+    for (auto& sr : D.regions)
+        if (!sr.ok) rep.n_failed_regions++;
+    rep.snapshot_digest = D.snapshot_digest;
+    rep.t_total_s = now_s() - t0;
+    sn->rep = rep;
+    if (rep_out) *rep_out = rep;
+    *out = sn;
+    if (rep.n_failed_regions) {
+        set_err(ctx, KC_PARTIAL, "kc_capture_dev: %llu region(s) were not live", (unsigned long long)rep.n_failed_regions);
+        return KC_PARTIAL;
+    }
+    return KC_OK;
+}
+
+extern "C" kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep_out) {
+    if (!ctx || !s || !out) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (s->ctx != ctx || ctx->device != s->ctx->device)
+        return set_err(ctx, KC_ERR_ARG, "kc_restore_dev: the snapshot lives on another ctx/device");
+    *out = nullptr;
+    kc_restore_report rep;
+    memset(&rep, 0, sizeof rep);
+    const double t0 = now_s();
+    for (auto& sr : s->desc.regions)
+        if (!sr.ok) rep.n_failed_regions++;
+    DevSource src(s);
+    kc_status st = restore_core(ctx, s->desc, src, out, rep_out, rep, t0);
+    if (st == KC_OK) (*out)->dev_snap = s;
+    return st;
+}
+
+extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
+    if (!ctx || !s || !dir_c) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    const std::string dir = dir_c;
+    const SnapDesc& D = s->desc;
+    if (!mkdir_p(dir + "/memory") || !mkdir_p(dir + "/post") || !mkdir_p(dir + "/written"))
+        return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot create %s", dir_c);
+    unlink((dir + "/capture_complete").c_str());
+    // metadata first
+    if (!write_text(dir + "/dispatch.json", dispatch_json(D.mode, D.mangled, D.grid, D.block, D.smem,
+                                                          (uint32_t)D.kernarg.size(), ctx->device, D.image.size(),
+                                                          D.layout)) ||
+        !write_file(dir + "/kernarg.bin", D.kernarg.data(), D.kernarg.size()) ||
+        (!D.image.empty() && !write_file(dir + "/kernel.cubin", D.image.data(), D.image.size())))
+        return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write metadata in %s", dir_c);
+    std::vector<MetaRegion> mr;
+    for (auto& sr : D.regions)
+        mr.push_back({sr.r.base, sr.r.size, sr.n_chunks, sr.digest, sr.r.seq, sr.r.kind, sr.r.device, sr.ok});
+    if (!write_text(dir + "/memory_regions.json", regions_json(mr)))
+        return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write memory_regions.json");
+    // region files from the arena (parallel workers)
+    const int T = io_threads();
+    kc_status st = ensure_io(ctx, T);
+    if (st != KC_OK) return st;
+    std::vector<std::pair<size_t, uint64_t>> todo;
+    for (size_t i = 0; i < D.regions.size(); ++i) {
+        if (!D.regions[i].ok) continue;
+        const std::string path = dir + "/memory/region_" + D.regions[i].hx + ".bin";
+        int fd = open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        const bool ok = fd >= 0 && ftruncate(fd, (off_t)D.regions[i].r.size) == 0;
+        if (fd >= 0) close(fd);
+        if (!ok) return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot create %s", path.c_str());
+        todo.emplace_back(i, D.regions[i].r.size);
+    }
+    const std::vector<IoItem> items = make_items(todo);
+    std::atomic<int> bad{0};
+    std::atomic<uint64_t> calls{0};
+    run_pool(T, items.size(), [&](int t, size_t k) {
+        if (bad) return;
+        const IoItem& it = items[k];
+        cudaSetDevice(ctx->device);
+        const std::string path = dir + "/memory/region_" + D.regions[it.region].hx + ".bin";
+        int fd = open(path.c_str(), O_WRONLY);
+        std::string err;
+        // item_d2h copies [base + off, +len) -> file offset off: base = this region's arena slot
+        const bool ok = fd >= 0 && item_d2h(ctx, ctx->io[t], (uint64_t)s->arena + s->off[it.region], it, fd, calls, err);
+        if (fd >= 0) close(fd);
+        if (!ok) bad = 1;
+    });
+    if (bad) return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: region copy failed");
+    std::vector<LogRegion> lr;
+    for (size_t i = 0; i < D.regions.size(); ++i) {
+        const SnapRegion& sr = D.regions[i];
+        lr.push_back({sr.r.base, sr.post_digest, (uint64_t)sr.written.size(), sr.ok,
+                      sr.ok ? "" : "not inside a live CUDA allocation before the dispatch"});
+        if (!sr.ok) continue;
+        write_file(dir + "/memory/region_" + sr.hx + ".xxh64", sr.manifest.data(), 8 * sr.manifest.size());
+        write_file(dir + "/post/region_" + sr.hx + ".xxh64", sr.post_manifest.data(), 8 * sr.post_manifest.size());
+        write_file(dir + "/written/region_" + sr.hx + ".idx", sr.written.data(), 8 * sr.written.size());
+        if (D.mode == KC_MODE_PRE_W && !sr.written.empty()) {
+            uint64_t wb = 0;
+            for (uint64_t k : sr.written) wb += std::min<uint64_t>(kChunk, sr.r.size - k * kChunk);
+            std::vector<uint8_t> host(wb);
+            KC_CHECK_CUDA(ctx, cudaMemcpy(host.data(), (const uint8_t*)s->warena + s->w_off[i], wb,
+                                          cudaMemcpyDeviceToHost), "D2H written chunks");
+            if (!write_file(dir + "/written/region_" + sr.hx + ".bin", host.data(), wb))
+                return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write written chunks");
+        }
+    }
+    kc_capture_report rep = s->rep;
+    rep.dma_calls += calls.load();
+    if (!write_text(dir + "/capture_log.json", capture_log_json(lr, rep, ctx->io_chunk, ctx->depth, "device")) ||
+        !write_file(dir + "/capture_complete", "", 0))
+        return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write capture_log.json / sentinel");
+    return KC_OK;
+}
+
+extern "C" uint64_t kc_snapshot_bytes(const kc_snapshot* s) { return s ? s->arena_bytes + s->w_bytes : 0; }
+
+extern "C" void kc_snapshot_free(kc_snapshot* s) {
+    if (!s) return;
+    if (s->ctx) bind_device(s->ctx);
+    if (s->arena) cudaFree(s->arena);
+    if (s->warena) cudaFree(s->warena);
+    delete s;
 }
 
 extern "C" kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out) {
@@ -1225,10 +1726,9 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
         own = true;
     } else {
         if (!h->module) {
-            std::vector<uint8_t> img;
-            if (!read_bin(h->dir + "/kernel.cubin", img) || img.empty())
-                return set_err(ctx, KC_ERR_FORMAT, "kc_replay: no kernel.cubin in %s", h->dir.c_str());
-            KC_CHECK_CU(ctx, KC_DRV(cuModuleLoadData)(&h->module, img.data()), "cuModuleLoadData(kernel.cubin)");
+            if (h->image.empty())
+                return set_err(ctx, KC_ERR_FORMAT, "kc_replay: the snapshot holds no code object (kernel.cubin)");
+            KC_CHECK_CU(ctx, KC_DRV(cuModuleLoadData)(&h->module, h->image.data()), "cuModuleLoadData(kernel.cubin)");
         }
         mod = h->module;
     }
@@ -1351,27 +1851,45 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
                 if (typed_ref) cudaFree(typed_ref);
                 return set_err(ctx, KC_ERR_OUT_OF_BOUNDS, "kc_validate: output %zu is not inside a restored region", i);
             }
-            std::vector<uint8_t> host(o.nbytes);
             const uint64_t roff = o.act - owner->r.base;
-            FILE* fp = fopen((h->dir + "/memory/region_" + owner->hexbase + ".bin").c_str(), "rb");
-            bool okr = fp && fseek(fp, (long)roff, SEEK_SET) == 0 && fread(host.data(), 1, o.nbytes, fp) == o.nbytes;
-            if (fp) fclose(fp);
-            if (!okr) {
-                if (typed_ref) cudaFree(typed_ref);
-                return set_err(ctx, KC_ERR_FORMAT, "kc_validate: cannot read reference bytes");
-            }
-            if (h->mode == KC_MODE_PRE_W && !owner->written.empty()) {  // overlay W's post bytes
-                std::vector<uint8_t> wb;
-                read_bin(h->dir + "/written/region_" + owner->hexbase + ".bin", wb);
-                uint64_t woff = 0;
-                for (uint64_t k : owner->written) {
-                    const uint64_t c0 = k * kChunk, len = std::min<uint64_t>(kChunk, owner->r.size - c0);
-                    const uint64_t lo = std::max(c0, roff), hi = std::min(c0 + len, roff + o.nbytes);
-                    if (lo < hi && woff + len <= wb.size()) memcpy(host.data() + (lo - roff), wb.data() + woff + (lo - c0), hi - lo);
-                    woff += len;
+            if (h->dev_snap) {  // device snapshot: stored bytes from the arena, W's post bytes from the W arena
+                const kc_snapshot* sn = h->dev_snap;
+                const size_t ri = (size_t)(owner - h->regions.data());
+                cudaMemcpy((uint8_t*)typed_ref + off, (const uint8_t*)sn->arena + sn->off[ri] + roff, o.nbytes,
+                           cudaMemcpyDeviceToDevice);
+                if (h->mode == KC_MODE_PRE_W) {
+                    uint64_t woff = sn->w_off[ri];
+                    for (uint64_t k : owner->written) {
+                        const uint64_t c0 = k * kChunk, len = std::min<uint64_t>(kChunk, owner->r.size - c0);
+                        const uint64_t lo = std::max(c0, roff), hi = std::min(c0 + len, roff + o.nbytes);
+                        if (lo < hi)
+                            cudaMemcpy((uint8_t*)typed_ref + off + (lo - roff),
+                                       (const uint8_t*)sn->warena + woff + (lo - c0), hi - lo, cudaMemcpyDeviceToDevice);
+                        woff += len;
+                    }
                 }
+            } else {
+                std::vector<uint8_t> host(o.nbytes);
+                FILE* fp = fopen((h->dir + "/memory/region_" + owner->hexbase + ".bin").c_str(), "rb");
+                bool okr = fp && fseek(fp, (long)roff, SEEK_SET) == 0 && fread(host.data(), 1, o.nbytes, fp) == o.nbytes;
+                if (fp) fclose(fp);
+                if (!okr) {
+                    if (typed_ref) cudaFree(typed_ref);
+                    return set_err(ctx, KC_ERR_FORMAT, "kc_validate: cannot read reference bytes");
+                }
+                if (h->mode == KC_MODE_PRE_W && !owner->written.empty()) {  // overlay W's post bytes
+                    std::vector<uint8_t> wb;
+                    read_bin(h->dir + "/written/region_" + owner->hexbase + ".bin", wb);
+                    uint64_t woff = 0;
+                    for (uint64_t k : owner->written) {
+                        const uint64_t c0 = k * kChunk, len = std::min<uint64_t>(kChunk, owner->r.size - c0);
+                        const uint64_t lo = std::max(c0, roff), hi = std::min(c0 + len, roff + o.nbytes);
+                        if (lo < hi && woff + len <= wb.size()) memcpy(host.data() + (lo - roff), wb.data() + woff + (lo - c0), hi - lo);
+                        woff += len;
+                    }
+                }
+                cudaMemcpy((uint8_t*)typed_ref + off, host.data(), o.nbytes, cudaMemcpyHostToDevice);
             }
-            cudaMemcpy((uint8_t*)typed_ref + off, host.data(), o.nbytes, cudaMemcpyHostToDevice);
             kc_buffer b = o;
             b.ref = (uint64_t)typed_ref + off;
             b.report = (int32_t)i;

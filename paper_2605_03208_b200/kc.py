@@ -40,7 +40,8 @@ EXPORTED = [
     "kc_kernel_launches", "kc_track",
     "kc_regions", "kc_alloc", "kc_free", "kc_track_install", "kc_track_uninstall", "kc_hash", "kc_count_chunks",
     "kc_written", "kc_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
-    "kc_validate", "kc_restored_regions", "kc_release",
+    "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
+    "kc_snapshot_bytes", "kc_snapshot_free",
 ]
 
 
@@ -173,6 +174,11 @@ def lib() -> ctypes.CDLL:
         "kc_validate": (st, [V, V, P(Buffer), SZ, P(Tolerance), P(DiffReport), SZ, P(SZ), P(U64)]),
         "kc_restored_regions": (st, [V, P(Region), SZ, P(SZ)]),
         "kc_release": (None, [V]),
+        "kc_capture_dev": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
+        "kc_restore_dev": (st, [V, V, P(V), P(RestoreReport)]),
+        "kc_snapshot_save": (st, [V, V, ctypes.c_char_p]),
+        "kc_snapshot_bytes": (U64, [V]),
+        "kc_snapshot_free": (None, [V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -280,6 +286,24 @@ class Restored:
     def release(self):
         if self.handle:
             lib().kc_release(self.handle)
+            self.handle = 0
+
+
+@dataclass
+class DevSnapshot:
+    """A device-resident snapshot (F1): region bytes in an HBM arena."""
+    handle: int
+    ctx: "Context"
+
+    def nbytes(self) -> int:
+        return int(lib().kc_snapshot_bytes(self.handle))
+
+    def save(self, directory: str) -> None:
+        self.ctx._check(lib().kc_snapshot_save(self.ctx.handle, self.handle, directory.encode()), "kc_snapshot_save")
+
+    def free(self):
+        if self.handle:
+            lib().kc_snapshot_free(self.handle)
             self.handle = 0
 
 
@@ -421,6 +445,38 @@ class Context:
                               directory.encode(), mode, ctypes.byref(rep))
         self._check(rc, "kc_capture", ok=(KC_OK, KC_PARTIAL))
         return rc, rep.as_dict()
+
+    def _dispatch(self, image, mangled, grid, block, smem, kernarg, stream):
+        img = ctypes.create_string_buffer(image, len(image)) if image else None
+        ka = ctypes.create_string_buffer(kernarg, len(kernarg)) if kernarg else None
+        d = Dispatch(None, ctypes.cast(img, ctypes.c_void_p) if img else None, len(image) if image else 0,
+                     mangled.encode() if mangled else None, (ctypes.c_uint32 * 3)(*grid),
+                     (ctypes.c_uint32 * 3)(*block), smem, len(kernarg), ctypes.cast(ka, ctypes.c_void_p) if ka else None,
+                     stream or None)
+        return d, (img, ka)
+
+    def capture_dev(self, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
+                    block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
+                    stream: int = 0) -> tuple[DevSnapshot, dict]:
+        """kc_capture into a device arena (F1)."""
+        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream)
+        rep = CaptureReport()
+        h = ctypes.c_void_p()
+        arr = _regions(regions) if regions is not None else None
+        rc = lib().kc_capture_dev(self._h, ctypes.byref(d), arr, len(regions) if regions is not None else 0, mode,
+                                  ctypes.byref(h), ctypes.byref(rep))
+        self._check(rc, "kc_capture_dev", ok=(KC_OK, KC_PARTIAL))
+        return DevSnapshot(h.value, self), rep.as_dict()
+
+    def restore_dev(self, snap: DevSnapshot) -> tuple[Restored, dict]:
+        h = ctypes.c_void_p()
+        rep = RestoreReport()
+        rc = lib().kc_restore_dev(self._h, snap.handle, ctypes.byref(h), ctypes.byref(rep))
+        if rc != KC_OK:
+            e = KcError(rc, f"kc_restore_dev: {self.last_error()}")
+            e.report = rep.as_dict()
+            raise e
+        return Restored(h.value, self), rep.as_dict()
 
     def restore(self, directory: str) -> tuple[Restored, dict]:
         h = ctypes.c_void_p()

@@ -7,6 +7,12 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+// KC_VARIANT_DELTA: a "modified kernel" for the validate-variant workflow
+// (PAPER.md:1120-1126); 0 = the captured kernel.
+#ifndef KC_VARIANT_DELTA
+#define KC_VARIANT_DELTA 0
+#endif
+
 struct KcNode {
     unsigned long long next;  // device VA of the next node, 0 ends the list
     unsigned int value;
@@ -25,7 +31,7 @@ extern "C" __global__ void kc_fixture_walk(const unsigned long long* __restrict_
     while (va != 0) {
         KcNode* nd = reinterpret_cast<KcNode*>(va);
         const unsigned int v = nd->value;
-        acc += v;
+        acc += v + KC_VARIANT_DELTA;
         out[(va - nodes_base) / 16] = acc;
         if (mutate) nd->value = v * 3u + 1u;
         va = nd->next;

@@ -154,7 +154,13 @@ def replay(a):
     out["restore"] = rep
     out["regions"] = [[x.base, x.size] for x in r.regions()]
     dump = os.path.join(a.dir, "..", os.path.basename(a.dir) + "_replay")
-    out["replay"] = ctx.replay(r, iterations=a.iterations, no_recopy=a.no_recopy, dump_dir=dump)
+    override = open(a.override, "rb").read() if a.override else None
+    out["replay"] = ctx.replay(r, iterations=a.iterations, no_recopy=a.no_recopy, dump_dir=dump,
+                               image_override=override)
+    if a.typed:  # typed validation of one output range: "<hex va>:<nbytes>:<dtype>"
+        va, nb, dt = a.typed.split(":")
+        treps, _ = ctx.validate(r, outs=[(int(va, 16), int(nb), dt)])
+        out["typed"] = treps
     reps, unexpected = ctx.validate(r)
     out["validate"] = reps
     out["unexpected_chunks"] = unexpected
@@ -209,6 +215,41 @@ def inproc(a):
     print(json.dumps(out))
 
 
+def devsnap(a):
+    """F1: capture c1 into a device arena, persist it (for the oracle), free the
+    live regions, restore from the arena at the same VAs, replay, validate."""
+    ctx = kc.Context(0)
+    sizes = [s.size for s in synth.C1_SPECS]
+    vas = [ctx.alloc(sz) for sz in sizes]
+    nodes_va, heads_va, out_va = vas
+    for va, arr in zip(vas, synth.c1_fill(nodes_va)):
+        _upload(va, arr)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    mode = kc.KC_MODE_PRE_W if a.mode == "pre_w" else kc.KC_MODE_POST
+    snap, rep = ctx.capture_dev(image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
+                                kernarg=synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=int(a.mutate)),
+                                mode=mode)
+    orig_out = _download(out_va, sizes[2])
+    np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_orig_out.npy"), orig_out)
+    snap.save(a.dir)
+    out = {"capture": rep, "vas": vas, "arena_bytes": snap.nbytes()}
+    for va in vas:
+        ctx.free(va)
+    r, rrep = ctx.restore_dev(snap)
+    out["restore"] = rrep
+    out["regions"] = [[x.base, x.size] for x in r.regions()]
+    out["replay"] = ctx.replay(r)
+    out["out_equal"] = bool(np.array_equal(_download(out_va, sizes[2]), orig_out))
+    treps, _ = ctx.validate(r, outs=[(out_va, sizes[2], "u64")])
+    out["typed"] = treps
+    reps, unexpected = ctx.validate(r)
+    out["validate"] = reps
+    out["unexpected_chunks"] = unexpected
+    r.release()
+    snap.free()
+    print(json.dumps(out))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -223,9 +264,11 @@ def main():
     p.add_argument("--squat", action="store_true")
     p.add_argument("--no-prereserve", action="store_true")
     p.add_argument("--memalloc", action="store_true")
+    p.add_argument("--override", default=None)
+    p.add_argument("--typed", default=None)
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
-     "inproc": inproc}[a.cmd](a)
+     "inproc": inproc, "devsnap": devsnap}[a.cmd](a)
 
 
 if __name__ == "__main__":

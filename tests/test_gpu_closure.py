@@ -214,3 +214,56 @@ def test_memalloc_regions_restore_exactly_or_abort(tmp_path):
         assert all(r["differing_bytes"] == 0 for r in res["validate"]) and res["out_equal"]
     else:
         assert res["restore_status"] == -6 and "hard requirement" in res["message"]
+
+
+def test_replay_override_validate_variant(tmp_path):
+    """The paper's validate-variant workflow:
+    an unmodified recompile replays to zero differing bytes, a modified kernel to a
+    nonzero diff localised to the output region; the original snapshot is intact."""
+    import synth
+    d = str(tmp_path / "var")
+    cap = run("capture-c1", d)
+    out_va = cap["vas"][2]
+    same = run("replay", d, "--override", os.path.join(ROOT, "synth", "kc_fixtures_recompiled.cubin"))
+    assert all(r["differing_bytes"] == 0 for r in same["validate"]) and same["unexpected_chunks"] == 0
+    mod = run("replay", d, "--override", os.path.join(ROOT, "synth", "kc_fixtures_modified.cubin"),
+              "--typed", f"{out_va:x}:{synth.C1_N_NODES * 8}:u64")
+    bad = [r for r in mod["validate"] if r["differing_bytes"] > 0]
+    assert len(bad) == 1 and bad[0]["nbytes"] == synth.C1_N_NODES * 8   # only `out` differs
+    assert mod["unexpected_chunks"] > 0
+    typed = mod["typed"][0]
+    # every node's running sum is off by its position j+1 (delta 1 per node): max |A-R| = list length
+    assert typed["differing_elems"] == synth.C1_N_NODES and typed["max_ulp"] == synth.C1_LIST_LEN
+    assert typed["pass"] == 0
+
+
+def test_typed_validation_of_a_float_output(tmp_path):
+    """kc_validate with a typed f32 sub-range (F2 decode-attention output): exact replay -> pass."""
+    d = str(tmp_path / "c2t")
+    cap = run("capture-c2", d)
+    attn = cap["vas"]["attn_out"]
+    res = run("replay", d, "--typed", f"{attn:x}:{32 * 64 * 4}:f32")
+    t = res["typed"][0]
+    assert t["n_elems"] == 32 * 64 and t["differing_elems"] == 0 and t["pass"] == 1 and t["max_abs"] == 0.0
+
+
+@pytest.mark.parametrize("mode,mutate", [("pre_w", True), ("post", False)])
+def test_device_snapshot_capture_restore_replay(tmp_path, mode, mutate):
+    """F1: the snapshot lives in an HBM arena; persisted with
+    kc_snapshot_save it is a valid kc-snapshot/1 directory (oracle O1); restored
+    at the same VAs from the arena, the replay reproduces the original output."""
+    d = str(tmp_path / "dev")
+    os.makedirs(d, exist_ok=True)
+    res = run("devsnap", d, "--mode", mode, *(["--mutate"] if mutate else []))
+    from oracle import snapshot
+    summ = snapshot.verify(snapshot.load(d))
+    assert summ["ok"] == 3
+    assert res["arena_bytes"] >= sum(s for _, s in res["regions"])
+    assert [tuple(x) for x in res["regions"]] == sorted((v, s) for v, s in zip(res["vas"], [655360, 65536, 327680]))
+    assert res["restore"]["verify_mismatch_chunks"] == 0
+    assert res["out_equal"]
+    assert all(r["differing_bytes"] == 0 for r in res["validate"]) and res["unexpected_chunks"] == 0
+    assert res["typed"][0]["differing_elems"] == 0 and res["typed"][0]["pass"] == 1
+    pred, (heads_va, out_va, nodes_va) = _walker_prediction(d, mutate)
+    if mode == "pre_w":   # the PRE_W snapshot holds the inputs: the oracle's walk reproduces the output
+        assert np.array_equal(np.load(str(tmp_path / "dev_orig_out.npy")), pred[out_va])
