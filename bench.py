@@ -430,54 +430,83 @@ def run_e2e(a, ctx, pool, step, stream, world, log):
 
 def run_latency(a, ctx, pool, log):
     """The metric's second half: 30 GB capture -> replay latency through the public
-    C ABI, per stage.  kc_capture (PRE_W: K1 pre-manifest, metadata, pinned D2H of
-    every region to files on /dev/shm, the F3 dispatch, K1 post-manifest, W), then
-    the live regions are freed, kc_restore maps them back at the captured VAs and
-    verifies them against the manifest, kc_replay re-dispatches F3 and
-    kc_validate diffs the written chunks and re-hashes everything."""
+    C ABI, per stage, for both snapshot sinks.
+      device (F1): kc_capture_dev (K1 pre-manifest, D2D copy of every region into an
+        HBM arena, the F3 dispatch, K1 post-manifest, W) -> the live regions are
+        freed -> kc_restore_dev maps them back at the captured VAs, copies the arena
+        in and verifies the manifest -> kc_replay -> kc_validate.
+      files: kc_capture (PRE_W, pinned D2H by 8 I/O threads into /dev/shm) ->
+        kc_restore from the files -> kc_replay -> kc_validate.
+    The device run's restored memory serves as the live state of the file run."""
     import shutil
     import torch
     import synth
     from paper_2605_03208_b200 import kc
-    d = a.latency_dir
-    shutil.rmtree(d, ignore_errors=True)
     regions = [(b, n) for b, n in pool.regions]
     image = open(synth.FIXTURE_CUBIN, "rb").read()
     warps = synth.C4_T * 2816
-    # the capture sees y as a fresh output buffer (zeroed), so the dispatch writes W != {}
+    disp = dict(image=image, mangled="kc_fixture_moe_gemv", grid=((warps * 32 + 255) // 256, 1, 1),
+                block=(256, 1, 1), kernarg=pool.kernarg, regions=regions, mode=kc.KC_MODE_PRE_W)
     ys = [s for s in pool.specs if s.name == "y"][0]
-    synth.dev_view(pool.va["y"], ys.size).zero_()
+    out = {}
+
+    def finish(name, cap, rst, r, times):
+        rep = ctx.replay(r)
+        t4 = time.perf_counter()
+        reps, unexpected = ctx.validate(r)
+        t5 = time.perf_counter()
+        ok = (all(x["differing_bytes"] == 0 for x in reps) and unexpected == 0
+              and rst["verify_mismatch_chunks"] == 0 and cap["written_chunks"] > 0 and len(reps) > 0)
+        same = sorted((x.base, x.size) for x in r.regions()) == sorted(regions)
+        t0, t1, t2, t3 = times
+        total = (t1 - t0) + (t3 - t2) + (t4 - t3) + (t5 - t4)
+        log(f"capture->replay [{name}]: capture {t1 - t0:.3f}s restore {t3 - t2:.3f}s replay {t4 - t3:.4f}s "
+            f"validate {t5 - t4:.4f}s ok={ok}")
+        return {"latency_s": total, "validated_bit_exact": bool(ok), "same_vas": bool(same),
+                "written_chunks": cap["written_chunks"],
+                "stages_s": {"capture_total": t1 - t0, "capture_hash_pre": cap["t_hash_pre_s"],
+                             "capture_copy": cap["t_d2h_s"], "capture_dispatch": cap["t_dispatch_s"],
+                             "capture_hash_post": cap["t_hash_post_s"], "restore_total": t3 - t2,
+                             "restore_reserve_map": rst["t_reserve_s"], "restore_copy_in": rst["t_h2d_s"],
+                             "restore_verify": rst["t_verify_s"], "replay": t4 - t3, "validate": t5 - t4},
+                "copy_out_gbs": pool.bytes / max(cap["t_d2h_s"], 1e-9) / 1e9,
+                "copy_in_gbs": rst["h2d_bytes"] / max(rst["t_h2d_s"], 1e-9) / 1e9}
+
+    # ---- device sink (F1)
+    synth.dev_view(pool.va["y"], ys.size).zero_()   # a fresh output buffer: the dispatch writes W != {}
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rc, cap = ctx.capture(d, image=image, mangled="kc_fixture_moe_gemv", grid=((warps * 32 + 255) // 256, 1, 1),
-                          block=(256, 1, 1), kernarg=pool.kernarg, regions=regions, mode=kc.KC_MODE_PRE_W)
+    snap, cap = ctx.capture_dev(**disp)
     t1 = time.perf_counter()
     for s in pool.specs:
         ctx.free(pool.va[s.name])
     t2 = time.perf_counter()
+    r_dev, rst = ctx.restore_dev(snap)
+    t3 = time.perf_counter()
+    out["device"] = finish("device", cap, rst, r_dev, (t0, t1, t2, t3))
+    out["device"]["arena_bytes"] = snap.nbytes()
+    snap.free()
+
+    # ---- file sink (the restored memory is now the live state)
+    d = a.latency_dir
+    shutil.rmtree(d, ignore_errors=True)
+    synth.dev_view(pool.va["y"], ys.size).zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rc, cap = ctx.capture(d, **disp)
+    t1 = time.perf_counter()
+    r_dev.release()
+    t2 = time.perf_counter()
     r, rst = ctx.restore(d)
     t3 = time.perf_counter()
-    rep = ctx.replay(r)
-    t4 = time.perf_counter()
-    reps, unexpected = ctx.validate(r)
-    t5 = time.perf_counter()
-    ok = (all(x["differing_bytes"] == 0 for x in reps) and unexpected == 0 and rst["verify_mismatch_chunks"] == 0
-          and cap["written_chunks"] > 0 and len(reps) > 0)
-    restored = sorted((x.base, x.size) for x in r.regions()) == sorted(regions)
+    out["files"] = finish("files", cap, rst, r, (t0, t1, t2, t3))
+    out["files"]["sink"] = d
     r.release()
     shutil.rmtree(d, ignore_errors=True)
-    total = (t1 - t0) + (t3 - t2) + (t4 - t3) + (t5 - t4)
-    log(f"capture->replay: capture {t1 - t0:.2f}s restore {t3 - t2:.2f}s replay {t4 - t3:.3f}s "
-        f"validate {t5 - t4:.3f}s ok={ok}")
-    return {"latency_s": total, "bytes": pool.bytes, "validated_bit_exact": bool(ok), "same_vas": bool(restored),
-            "sink": d, "written_chunks": cap["written_chunks"],
-            "stages_s": {"capture_total": t1 - t0, "capture_hash_pre": cap["t_hash_pre_s"],
-                         "capture_d2h_and_files": cap["t_d2h_s"], "capture_dispatch": cap["t_dispatch_s"],
-                         "capture_hash_post": cap["t_hash_post_s"], "restore_total": t3 - t2,
-                         "restore_reserve_map": rst["t_reserve_s"], "restore_files_h2d": rst["t_h2d_s"],
-                         "restore_verify": rst["t_verify_s"], "replay": t4 - t3, "validate": t5 - t4},
-            "d2h_gbs_incl_files": pool.bytes / max(cap["t_d2h_s"], 1e-9) / 1e9,
-            "h2d_gbs_incl_files": rst["h2d_bytes"] / max(rst["t_h2d_s"], 1e-9) / 1e9}
+    out["bytes"] = pool.bytes
+    out["latency_s"] = out["device"]["latency_s"]
+    out["validated_bit_exact"] = out["device"]["validated_bit_exact"] and out["files"]["validated_bit_exact"]
+    return out
 
 
 # ------------------------------------------------------------------ oracle (CPU baseline / reference arm)

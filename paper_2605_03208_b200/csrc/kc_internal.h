@@ -78,6 +78,11 @@ struct kc_ctx {
         CUmemGenericAllocationHandle h;
     };
     std::map<uint64_t, VmmAlloc> vmm;  // base -> reservation (guarded by mu)
+    // ctx-owned VA heap for KC_ALLOC_VMM (reserved once, never returned to the
+    // driver): freed ranges stay ours, so a same-process restore maps back at
+    // the exact VAs (R28d).  heap_free: base -> size of free ranges (mu).
+    uint64_t heap_base = 0, heap_size = 0;
+    std::map<uint64_t, uint64_t> heap_free;
     uint64_t launches = 0;
 };
 
@@ -104,6 +109,7 @@ struct kc_restored {
         uint64_t base, size;
         CUmemGenericAllocationHandle h;
         bool reserved, mapped, created;
+        bool heap;                       // claimed from the ctx VA heap (not a driver reservation)
         bool fallback;                   // restored by replaying cuMemAlloc (driver-pooled VA)
         std::vector<uint64_t> memalloc;  // cuMemAlloc'd region bases inside this span
         uint64_t reserve_got;            // diagnostics of a refused reservation
@@ -134,6 +140,10 @@ std::string hex_base(uint64_t base);  // lowercase hex, no 0x (PAPER.md:685, 944
 bool region_live(kc_ctx* ctx, uint64_t base, uint64_t size);
 kc_status free_alloc(kc_ctx* ctx, uint64_t dptr, bool track);
 size_t granularity(kc_ctx* ctx);
+// ctx VA heap: claim an exact free range / allocate / give back (coalescing)
+bool heap_take(kc_ctx* ctx, uint64_t base, uint64_t size);
+uint64_t heap_alloc(kc_ctx* ctx, uint64_t size);
+void heap_put(kc_ctx* ctx, uint64_t base, uint64_t size);
 
 // snapshot format helpers (kc_snapshot.cu)
 kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std::vector<uint64_t>& out_hashes,

@@ -122,6 +122,64 @@ size_t granularity(kc_ctx* ctx) {
     return g;
 }
 
+// ---- ctx VA heap (KC_ALLOC_VMM) ----------------------------------------
+static bool heap_init(kc_ctx* ctx) {
+    if (ctx->heap_base) return true;
+    uint64_t gb = 1024;  // 1 TiB of VA by default (47-bit space; costs no memory)
+    if (const char* e = getenv("KC_VA_HEAP_GB")) gb = strtoull(e, nullptr, 0);
+    const size_t G = granularity(ctx);
+    const uint64_t size = gb << 30;
+    CUdeviceptr p = 0;
+    if (KC_DRV(cuMemAddressReserve)(&p, size, std::max<size_t>(G, 1ull << 30), 0, 0) != CUDA_SUCCESS) return false;
+    ctx->heap_base = (uint64_t)p;
+    ctx->heap_size = size;
+    ctx->heap_free[(uint64_t)p] = size;
+    return true;
+}
+
+bool heap_take(kc_ctx* ctx, uint64_t base, uint64_t size) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ctx->heap_base || base < ctx->heap_base || base + size > ctx->heap_base + ctx->heap_size) return false;
+    auto it = ctx->heap_free.upper_bound(base);
+    if (it == ctx->heap_free.begin()) return false;
+    --it;
+    const uint64_t fb = it->first, fs = it->second;
+    if (base < fb || base + size > fb + fs) return false;  // not entirely free
+    ctx->heap_free.erase(it);
+    if (base > fb) ctx->heap_free[fb] = base - fb;
+    if (base + size < fb + fs) ctx->heap_free[base + size] = fb + fs - (base + size);
+    return true;
+}
+
+uint64_t heap_alloc(kc_ctx* ctx, uint64_t size) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    for (auto it = ctx->heap_free.begin(); it != ctx->heap_free.end(); ++it) {
+        if (it->second < size) continue;
+        const uint64_t b = it->first, s = it->second;
+        ctx->heap_free.erase(it);
+        if (s > size) ctx->heap_free[b + size] = s - size;
+        return b;
+    }
+    return 0;
+}
+
+void heap_put(kc_ctx* ctx, uint64_t base, uint64_t size) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    auto it = ctx->heap_free.emplace(base, size).first;
+    auto nx = std::next(it);
+    if (nx != ctx->heap_free.end() && it->first + it->second == nx->first) {
+        it->second += nx->second;
+        ctx->heap_free.erase(nx);
+    }
+    if (it != ctx->heap_free.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) {
+            pv->second += it->second;
+            ctx->heap_free.erase(it);
+        }
+    }
+}
+
 // Is [base, base+size) backed by live device memory?  cuMemAlloc ranges via
 // RANGE_START/SIZE; VMM mappings via MAPPED on the first and last byte.
 bool region_live(kc_ctx* ctx, uint64_t base, uint64_t size) {
@@ -159,9 +217,9 @@ kc_status free_alloc(kc_ctx* ctx, uint64_t dptr, bool track) {
         }
     }
     if (is_vmm) {
-        KC_DRV(cuMemUnmap)((CUdeviceptr)dptr, va.reserved);
+        KC_CHECK_CU(ctx, KC_DRV(cuMemUnmap)((CUdeviceptr)dptr, va.reserved), "cuMemUnmap");
         KC_DRV(cuMemRelease)(va.h);
-        KC_CHECK_CU(ctx, KC_DRV(cuMemAddressFree)((CUdeviceptr)dptr, va.reserved), "cuMemAddressFree");
+        heap_put(ctx, dptr, va.reserved);  // the VA stays in the ctx heap
         if (track && !ctx->cupti_installed) kc_track(ctx, KC_EV_UNMAP, dptr, 0, ctx->device, KC_KIND_VMM);
         return KC_OK;
     }
@@ -258,6 +316,7 @@ void kc_destroy(kc_ctx* ctx) {
     std::vector<uint64_t> vm;
     for (auto& kv : ctx->vmm) vm.push_back(kv.first);
     for (uint64_t b : vm) free_alloc(ctx, b, false);
+    if (ctx->heap_base) KC_DRV(cuMemAddressFree)((CUdeviceptr)ctx->heap_base, ctx->heap_size);
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch,
                               &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map})
         if (b->p) cudaFree(b->p);
@@ -351,12 +410,13 @@ kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = ctx->device;
-    CUdeviceptr va = 0;
-    KC_CHECK_CU(ctx, KC_DRV(cuMemAddressReserve)(&va, rsz, G, 0, 0), "cuMemAddressReserve");
+    if (!heap_init(ctx)) return set_err(ctx, KC_ERR_CUDA, "kc_alloc: cannot reserve the VA heap");
+    const CUdeviceptr va = (CUdeviceptr)heap_alloc(ctx, rsz);
+    if (!va) return set_err(ctx, KC_ERR_NOMEM, "kc_alloc: VA heap exhausted (KC_VA_HEAP_GB)");
     CUmemGenericAllocationHandle h;
     CUresult r = KC_DRV(cuMemCreate)(&h, rsz, &prop, 0);
     if (r != CUDA_SUCCESS) {
-        KC_DRV(cuMemAddressFree)(va, rsz);
+        heap_put(ctx, (uint64_t)va, rsz);
         if (r == CUDA_ERROR_OUT_OF_MEMORY)
             return set_err(ctx, KC_ERR_NOMEM, "cuMemCreate(%llu): out of memory", (unsigned long long)rsz);
         return cu_err(ctx, r, "cuMemCreate");
@@ -371,7 +431,7 @@ kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
     }
     if (r != CUDA_SUCCESS) {
         KC_DRV(cuMemRelease)(h);
-        KC_DRV(cuMemAddressFree)(va, rsz);
+        heap_put(ctx, (uint64_t)va, rsz);
         return cu_err(ctx, r, "cuMemMap/cuMemSetAccess");
     }
     {

@@ -802,6 +802,7 @@ void rollback(kc_restored* h) {
         it->memalloc.clear();
         if (it->mapped) KC_DRV(cuMemUnmap)((CUdeviceptr)it->base, it->size);
         if (it->created) KC_DRV(cuMemRelease)(it->h);
+        if (it->heap) heap_put(h->ctx, it->base, it->size);
     }
     h->spans.clear();
     for (auto& w : h->windows) KC_DRV(cuMemAddressFree)((CUdeviceptr)w.first, w.second);
@@ -1011,7 +1012,7 @@ struct FileSource : RestoreSource {
 static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src, kc_restored** out,
                               kc_restore_report* rep_out, kc_restore_report& rep, double t0) {
     kc_restored* h = new kc_restored();
-    h->ctx = ctx;
+    h->ctx = ctx;  // rollback() returns heap spans to this ctx
     h->mode = d.mode;
     h->mangled = d.mangled;
     for (int i = 0; i < 3; ++i) {
@@ -1067,7 +1068,15 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     static const uint64_t kWindows[] = {0, 32ull << 20, 64ull << 20, 128ull << 20, 256ull << 20, 512ull << 20,
                                         1ull << 30};
     for (auto& sp : spans) {
-        kc_restored::Span s{sp.first, sp.second - sp.first, 0, false, false, false, false, {}, 0, 0};
+        kc_restored::Span s{sp.first, sp.second - sp.first, 0, false, false, false, false, false, {}, 0, 0};
+        // a span inside this ctx's VA heap that is free (its allocation was released
+        // with kc_free) is mapped straight back at the exact VA (R28d)
+        if (heap_take(ctx, s.base, s.size)) {
+            s.reserved = true;
+            s.heap = true;
+            h->spans.push_back(s);
+            continue;
+        }
         bool covered = false;
         for (auto& w : h->windows)
             if (w.first <= s.base && s.base + s.size <= w.first + w.second) covered = true;
