@@ -435,9 +435,11 @@ def run_latency(a, ctx, pool, log):
         HBM arena, the F3 dispatch, K1 post-manifest, W) -> the live regions are
         freed -> kc_restore_dev maps them back at the captured VAs, copies the arena
         in and verifies the manifest -> kc_replay -> kc_validate.
+      host_pinned: kc_capture_host (the same, D2H into a pinned host arena at PCIe
+        rate) -> kc_restore_dev (H2D) -> kc_replay -> kc_validate.
       files: kc_capture (PRE_W, pinned D2H by 8 I/O threads into /dev/shm) ->
         kc_restore from the files -> kc_replay -> kc_validate.
-    The device run's restored memory serves as the live state of the file run."""
+    Each run's restored memory serves as the live state of the next."""
     import shutil
     import torch
     import synth
@@ -487,7 +489,28 @@ def run_latency(a, ctx, pool, log):
     out["device"]["arena_bytes"] = snap.nbytes()
     snap.free()
 
-    # ---- file sink (the restored memory is now the live state)
+    # ---- pinned host sink (the restored memory is now the live state); the arena
+    # is pinned ahead of time like the staging ring, its cost reported apart
+    tp = time.perf_counter()
+    ctx.host_arena_reserve(pool.bytes + 256 * len(regions))
+    pin_s = time.perf_counter() - tp
+    synth.dev_view(pool.va["y"], ys.size).zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    snap, cap = ctx.capture_host(**disp)
+    t1 = time.perf_counter()
+    r_dev.release()
+    t2 = time.perf_counter()
+    r_host, rst = ctx.restore_dev(snap)
+    t3 = time.perf_counter()
+    out["host_pinned"] = finish("host_pinned", cap, rst, r_host, (t0, t1, t2, t3))
+    out["host_pinned"]["arena_bytes"] = snap.nbytes()
+    out["host_pinned"]["arena_pin_s"] = pin_s
+    out["host_pinned"]["pcie"] = pcie_peak(log)
+    snap.free()
+    ctx.host_arena_reserve(0)
+
+    # ---- file sink
     d = a.latency_dir
     shutil.rmtree(d, ignore_errors=True)
     synth.dev_view(pool.va["y"], ys.size).zero_()
@@ -495,7 +518,7 @@ def run_latency(a, ctx, pool, log):
     t0 = time.perf_counter()
     rc, cap = ctx.capture(d, **disp)
     t1 = time.perf_counter()
-    r_dev.release()
+    r_host.release()
     t2 = time.perf_counter()
     r, rst = ctx.restore(d)
     t3 = time.perf_counter()
@@ -505,7 +528,30 @@ def run_latency(a, ctx, pool, log):
     shutil.rmtree(d, ignore_errors=True)
     out["bytes"] = pool.bytes
     out["latency_s"] = out["device"]["latency_s"]
-    out["validated_bit_exact"] = out["device"]["validated_bit_exact"] and out["files"]["validated_bit_exact"]
+    out["validated_bit_exact"] = all(out[k]["validated_bit_exact"] for k in ("device", "host_pinned", "files"))
+    return out
+
+
+def pcie_peak(log, nbytes: int = 1 << 30, reps: int = 5) -> dict:
+    """Measured pinned-host <-> device copy rate (best of `reps` 1 GiB copies per
+    direction, CUDA events): the PCIe roofline the host-sink copies are quoted against."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, dst, src in (("d2h_gbs", h, d), ("h2d_gbs", d, h)):
+        best = 0.0
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out[name] = best
+    out["spec_gbs_per_dir"] = 64.0
+    log(f"pcie measured: d2h {out['d2h_gbs']:.1f} GB/s h2d {out['h2d_gbs']:.1f} GB/s")
+    del h, d
     return out
 
 

@@ -285,14 +285,30 @@ kc_status kc_prereserve(const char* dir, uint64_t* n_reserved);
  * exactly as in kc_capture (it always proceeds). */
 kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
                          kc_snapshot** out, kc_capture_report* rep);
-/* Same-VA restore from a device snapshot (the originals must be freed first,
- * or this is another process sharing nothing: the arena lives in this ctx's
- * device): VA windows as kc_restore, then D2D copy-in and the K1 verify. */
+/* The same capture into a PINNED HOST arena (cudaHostAlloc): the region bytes
+ * leave the GPU at PCIe rate (A5's D2H without the file sink; SURVEY.md 8(d)
+ * D.4 "the latency benchmark uses a pinned in-memory arena").  Small regions
+ * (< 1 MiB) are packed by one K4 launch writing through the mapped pinned
+ * pages.  The arena is taken from the ctx's pinned-arena cache when one of
+ * sufficient size is parked there (kc_host_arena_reserve, or a freed host
+ * snapshot), else allocated (pinning costs ~0.2-0.3 s per 10 GB). */
+kc_status kc_capture_host(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
+                          kc_snapshot** out, kc_capture_report* rep);
+/* Pin `bytes` of host memory ahead of time and park it in the ctx's cache (one
+ * arena; a larger request replaces a smaller parked one).  0 frees the cache. */
+kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes);
+/* Same-VA restore from an in-memory snapshot (device or pinned host arena; the
+ * originals must be freed first): VA windows as kc_restore (or the ctx VA
+ * heap), then copy-in (D2D or H2D) and the K1 verify. */
 kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep);
-/* Persist a device snapshot as a kc-snapshot/1 directory (parallel D2H). */
+/* Persist an in-memory snapshot as a kc-snapshot/1 directory (parallel). */
 kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
-/* Bytes held in the device arena. */
+/* Bytes held in the snapshot's arenas. */
 uint64_t kc_snapshot_bytes(const kc_snapshot* s);
+/* 1 = pinned host arena (kc_capture_host), 0 = device arena. */
+int kc_snapshot_is_host(const kc_snapshot* s);
+/* Frees the arenas; a host arena is parked in the ctx's cache instead when it
+ * is at least as large as the one parked there. */
 void kc_snapshot_free(kc_snapshot* s);
 
 /* ---- A7 replay ------------------------------------ */

@@ -82,6 +82,9 @@ struct kc_ctx {
     // driver): freed ranges stay ours, so a same-process restore maps back at
     // the exact VAs (R28d).  heap_free: base -> size of free ranges (mu).
     uint64_t heap_base = 0, heap_size = 0;
+    // parked pinned host arena for kc_capture_host (kc_host_arena_reserve)
+    void* host_arena = nullptr;
+    uint64_t host_arena_bytes = 0;
     std::map<uint64_t, uint64_t> heap_free;
     uint64_t launches = 0;
 };

@@ -317,6 +317,7 @@ void kc_destroy(kc_ctx* ctx) {
     for (auto& kv : ctx->vmm) vm.push_back(kv.first);
     for (uint64_t b : vm) free_alloc(ctx, b, false);
     if (ctx->heap_base) KC_DRV(cuMemAddressFree)((CUdeviceptr)ctx->heap_base, ctx->heap_size);
+    if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch,
                               &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map})
         if (b->p) cudaFree(b->p);

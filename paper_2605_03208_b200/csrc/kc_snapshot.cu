@@ -235,7 +235,7 @@ bool item_d2h(kc_ctx* ctx, kc_ctx::IoWorker& w, uint64_t base, const IoItem& it,
         if (i >= depth) drain(i - depth);
         if (!ok) break;
         const uint64_t o = it.off + i * io, b = std::min(io, it.off + it.len - o);
-        cudaError_t e = cudaMemcpyAsync(w.pinned[slot], (const void*)(base + o), b, cudaMemcpyDeviceToHost, w.stream);
+        cudaError_t e = cudaMemcpyAsync(w.pinned[slot], (const void*)(base + o), b, cudaMemcpyDefault, w.stream);
         if (e != cudaSuccess) {
             cudaGetLastError();
             err = std::string("cudaMemcpyAsync D2H: ") + cudaGetErrorString(e);
@@ -1306,9 +1306,11 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
 // cudaMemcpyAsync, regions and W chunks under 1 MiB through the K4 gather.
 struct kc_snapshot {
     kc_ctx* ctx = nullptr;
+    bool host = false;      // arenas in pinned host memory (kc_capture_host)
     SnapDesc desc;
     void* arena = nullptr;  // stored bytes, region i at off[i] (256 B aligned)
     uint64_t arena_bytes = 0;
+    uint64_t arena_cap = 0;  // allocated bytes (>= arena_bytes when a parked host arena was reused)
     std::vector<uint64_t> off;
     void* warena = nullptr;  // PRE_W: post bytes of W, region i at w_off[i]
     uint64_t w_bytes = 0;
@@ -1318,15 +1320,16 @@ struct kc_snapshot {
 
 namespace {
 
-// device copies of (src, dst, len) ranges: >= 1 MiB by cudaMemcpyAsync, smaller ones batched through K4
+// copies of (src, dst, len) ranges between device memory and the device or pinned
+// host arena (UVA): >= 1 MiB by cudaMemcpyAsync, smaller ones batched through K4
 kc_status copy_ranges_d2d(kc_ctx* ctx, const std::vector<std::array<uint64_t, 3>>& ranges, cudaStream_t s,
                           uint64_t* calls) {
     std::vector<uint64_t> src, dst, len;
     for (auto& r : ranges) {
         if (r[2] == 0) continue;
         if (r[2] >= (1ull << 20)) {
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync((void*)r[1], (const void*)r[0], r[2], cudaMemcpyDeviceToDevice, s),
-                          "D2D copy");
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync((void*)r[1], (const void*)r[0], r[2], cudaMemcpyDefault, s),
+                          "arena copy");
             if (calls) ++*calls;
         } else {
             src.push_back(r[0]);
@@ -1360,21 +1363,73 @@ struct DevSource : RestoreSource {
         for (size_t i = 0; i < d.regions.size(); ++i) {
             if (!d.regions[i].ok) continue;
             ranges.push_back({(uint64_t)sn->arena + sn->off[i], d.regions[i].r.base, d.regions[i].r.size});
-            rep.h2d_bytes += d.regions[i].r.size;  // bytes copied in (device to device here)
+            rep.h2d_bytes += d.regions[i].r.size;  // bytes copied in (D2D or H2D)
         }
         return copy_ranges_d2d(ctx, ranges, ctx->copy_stream, nullptr);
     }
     kc_status written_ref(kc_ctx* ctx, const SnapDesc&, size_t i, void* dst, uint64_t bytes) override {
-        KC_CHECK_CUDA(ctx, cudaMemcpy(dst, (const uint8_t*)sn->warena + sn->w_off[i], bytes, cudaMemcpyDeviceToDevice),
-                      "D2D written reference");
+        KC_CHECK_CUDA(ctx, cudaMemcpy(dst, (const uint8_t*)sn->warena + sn->w_off[i], bytes, cudaMemcpyDefault),
+                      "written reference from the arena");
         return KC_OK;
     }
 };
 
 }  // namespace
 
+namespace {
+// arena allocation for in-memory snapshots: device (cudaMalloc) or pinned host,
+// the latter from the ctx's parked arena when it is large enough
+cudaError_t arena_alloc(kc_ctx* ctx, bool host, void** p, uint64_t bytes, uint64_t* cap) {
+    *cap = bytes;
+    if (!host) return cudaMalloc(p, bytes);
+    if (ctx->host_arena && ctx->host_arena_bytes >= bytes) {
+        *p = ctx->host_arena;
+        *cap = ctx->host_arena_bytes;
+        ctx->host_arena = nullptr;
+        ctx->host_arena_bytes = 0;
+        return cudaSuccess;
+    }
+    return cudaHostAlloc(p, bytes, cudaHostAllocPortable);
+}
+
+kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
+                      kc_snapshot** out, kc_capture_report* rep_out, bool host);
+}  // namespace
+
 extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                     kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
+    return capture_mem(ctx, d, regions, n, mode, out, rep_out, false);
+}
+
+extern "C" kc_status kc_capture_host(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
+                                     kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
+    return capture_mem(ctx, d, regions, n, mode, out, rep_out, true);
+}
+
+extern "C" kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
+    if (!ctx) return KC_ERR_ARG;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    if (bytes == 0) {
+        if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+        ctx->host_arena = nullptr;
+        ctx->host_arena_bytes = 0;
+        return KC_OK;
+    }
+    if (ctx->host_arena_bytes >= bytes) return KC_OK;
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(ctx, KC_ERR_NOMEM, "kc_host_arena_reserve: cannot pin %llu bytes", (unsigned long long)bytes);
+    }
+    if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+    ctx->host_arena = p;
+    ctx->host_arena_bytes = bytes;
+    return KC_OK;
+}
+
+namespace {
+kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
+                      kc_snapshot** out, kc_capture_report* rep_out, bool host) {
     if (!ctx) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -1411,6 +1466,7 @@ extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_
     }
     kc_snapshot* sn = new kc_snapshot();
     sn->ctx = ctx;
+    sn->host = host;
     SnapDesc& D = sn->desc;
     D.mode = mode;
     D.mangled = d->mangled ? d->mangled : "";
@@ -1472,9 +1528,10 @@ extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_
         if (sr.ok) total += (sr.r.size + 255) / 256 * 256;
     }
     sn->arena_bytes = total;
-    if (total && cudaMalloc(&sn->arena, total) != cudaSuccess) {
+    if (total && arena_alloc(ctx, host, &sn->arena, total, &sn->arena_cap) != cudaSuccess) {
         cudaGetLastError();
-        return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: cannot allocate a %llu-byte device arena",
+        sn->arena = nullptr;
+        return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_%s: cannot allocate a %llu-byte arena", host ? "host" : "dev",
                             (unsigned long long)total));
     }
     auto snapshot_regions = [&]() -> kc_status {
@@ -1556,8 +1613,10 @@ extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_
             for (uint64_t k : sr.written) wtot += std::min<uint64_t>(kChunk, sr.r.size - k * kChunk);
         }
         sn->w_bytes = wtot;
-        if (cudaMalloc(&sn->warena, wtot) != cudaSuccess) {
+        if ((host ? cudaHostAlloc(&sn->warena, wtot, cudaHostAllocPortable) : cudaMalloc(&sn->warena, wtot)) !=
+            cudaSuccess) {
             cudaGetLastError();
+            sn->warena = nullptr;
             return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: W arena of %llu bytes", (unsigned long long)wtot));
         }
         std::vector<std::array<uint64_t, 3>> ranges;
@@ -1575,7 +1634,8 @@ extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_
     }
     if (sn->w_off.empty()) sn->w_off.assign(D.regions.size(), 0);
     t_copy += now_s() - t;
-    rep.t_d2h_s = t_copy;  // device-to-device here
+    rep.t_d2h_s = t_copy;  // device-to-device for a device arena
+    if (host) rep.d2h_bytes = sn->arena_bytes + sn->w_bytes;
     for (auto& sr : D.regions)
         if (!sr.ok) rep.n_failed_regions++;
     rep.snapshot_digest = D.snapshot_digest;
@@ -1589,6 +1649,7 @@ extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_
     }
     return KC_OK;
 }
+}  // namespace
 
 extern "C" kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep_out) {
     if (!ctx || !s || !out) return KC_ERR_ARG;
@@ -1672,14 +1733,14 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
             for (uint64_t k : sr.written) wb += std::min<uint64_t>(kChunk, sr.r.size - k * kChunk);
             std::vector<uint8_t> host(wb);
             KC_CHECK_CUDA(ctx, cudaMemcpy(host.data(), (const uint8_t*)s->warena + s->w_off[i], wb,
-                                          cudaMemcpyDeviceToHost), "D2H written chunks");
+                                          cudaMemcpyDefault), "D2H written chunks");
             if (!write_file(dir + "/written/region_" + sr.hx + ".bin", host.data(), wb))
                 return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write written chunks");
         }
     }
     kc_capture_report rep = s->rep;
     rep.dma_calls += calls.load();
-    if (!write_text(dir + "/capture_log.json", capture_log_json(lr, rep, ctx->io_chunk, ctx->depth, "device")) ||
+    if (!write_text(dir + "/capture_log.json", capture_log_json(lr, rep, ctx->io_chunk, ctx->depth, s->host ? "host" : "device")) ||
         !write_file(dir + "/capture_complete", "", 0))
         return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write capture_log.json / sentinel");
     return KC_OK;
@@ -1687,11 +1748,25 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
 
 extern "C" uint64_t kc_snapshot_bytes(const kc_snapshot* s) { return s ? s->arena_bytes + s->w_bytes : 0; }
 
+extern "C" int kc_snapshot_is_host(const kc_snapshot* s) { return s && s->host ? 1 : 0; }
+
 extern "C" void kc_snapshot_free(kc_snapshot* s) {
     if (!s) return;
     if (s->ctx) bind_device(s->ctx);
-    if (s->arena) cudaFree(s->arena);
-    if (s->warena) cudaFree(s->warena);
+    if (s->host) {
+        kc_ctx* ctx = s->ctx;
+        if (s->arena && ctx && s->arena_cap >= ctx->host_arena_bytes) {  // park the larger arena
+            if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+            ctx->host_arena = s->arena;
+            ctx->host_arena_bytes = s->arena_cap;
+        } else if (s->arena) {
+            cudaFreeHost(s->arena);
+        }
+        if (s->warena) cudaFreeHost(s->warena);
+    } else {
+        if (s->arena) cudaFree(s->arena);
+        if (s->warena) cudaFree(s->warena);
+    }
     delete s;
 }
 
@@ -1865,7 +1940,7 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
                 const kc_snapshot* sn = h->dev_snap;
                 const size_t ri = (size_t)(owner - h->regions.data());
                 cudaMemcpy((uint8_t*)typed_ref + off, (const uint8_t*)sn->arena + sn->off[ri] + roff, o.nbytes,
-                           cudaMemcpyDeviceToDevice);
+                           cudaMemcpyDefault);
                 if (h->mode == KC_MODE_PRE_W) {
                     uint64_t woff = sn->w_off[ri];
                     for (uint64_t k : owner->written) {
@@ -1873,7 +1948,7 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
                         const uint64_t lo = std::max(c0, roff), hi = std::min(c0 + len, roff + o.nbytes);
                         if (lo < hi)
                             cudaMemcpy((uint8_t*)typed_ref + off + (lo - roff),
-                                       (const uint8_t*)sn->warena + woff + (lo - c0), hi - lo, cudaMemcpyDeviceToDevice);
+                                       (const uint8_t*)sn->warena + woff + (lo - c0), hi - lo, cudaMemcpyDefault);
                         woff += len;
                     }
                 }

@@ -41,7 +41,7 @@ EXPORTED = [
     "kc_regions", "kc_alloc", "kc_free", "kc_track_install", "kc_track_uninstall", "kc_hash", "kc_count_chunks",
     "kc_written", "kc_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
-    "kc_snapshot_bytes", "kc_snapshot_free",
+    "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
 ]
 
 
@@ -179,6 +179,9 @@ def lib() -> ctypes.CDLL:
         "kc_snapshot_save": (st, [V, V, ctypes.c_char_p]),
         "kc_snapshot_bytes": (U64, [V]),
         "kc_snapshot_free": (None, [V]),
+        "kc_capture_host": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
+        "kc_host_arena_reserve": (st, [V, U64]),
+        "kc_snapshot_is_host": (ctypes.c_int, [V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -291,12 +294,16 @@ class Restored:
 
 @dataclass
 class DevSnapshot:
-    """A device-resident snapshot (F1): region bytes in an HBM arena."""
+    """An in-memory snapshot (F1): region bytes in an HBM arena (capture_dev) or
+    a pinned host arena (capture_host)."""
     handle: int
     ctx: "Context"
 
     def nbytes(self) -> int:
         return int(lib().kc_snapshot_bytes(self.handle))
+
+    def is_host(self) -> bool:
+        return bool(lib().kc_snapshot_is_host(self.handle))
 
     def save(self, directory: str) -> None:
         self.ctx._check(lib().kc_snapshot_save(self.ctx.handle, self.handle, directory.encode()), "kc_snapshot_save")
@@ -457,16 +464,25 @@ class Context:
 
     def capture_dev(self, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
                     block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
-                    stream: int = 0) -> tuple[DevSnapshot, dict]:
-        """kc_capture into a device arena (F1)."""
+                    stream: int = 0, host: bool = False) -> tuple[DevSnapshot, dict]:
+        """kc_capture into a device arena (F1), or a pinned host arena (host=True: kc_capture_host)."""
         d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream)
         rep = CaptureReport()
         h = ctypes.c_void_p()
         arr = _regions(regions) if regions is not None else None
-        rc = lib().kc_capture_dev(self._h, ctypes.byref(d), arr, len(regions) if regions is not None else 0, mode,
-                                  ctypes.byref(h), ctypes.byref(rep))
-        self._check(rc, "kc_capture_dev", ok=(KC_OK, KC_PARTIAL))
+        fn = lib().kc_capture_host if host else lib().kc_capture_dev
+        rc = fn(self._h, ctypes.byref(d), arr, len(regions) if regions is not None else 0, mode,
+                ctypes.byref(h), ctypes.byref(rep))
+        self._check(rc, "kc_capture_host" if host else "kc_capture_dev", ok=(KC_OK, KC_PARTIAL))
         return DevSnapshot(h.value, self), rep.as_dict()
+
+    def capture_host(self, **kw) -> tuple[DevSnapshot, dict]:
+        """kc_capture_host: the capture into a pinned host arena."""
+        return self.capture_dev(host=True, **kw)
+
+    def host_arena_reserve(self, nbytes: int) -> None:
+        """kc_host_arena_reserve: pin a host arena ahead of time (0 frees the parked one)."""
+        self._check(lib().kc_host_arena_reserve(self._h, nbytes), "kc_host_arena_reserve")
 
     def restore_dev(self, snap: DevSnapshot) -> tuple[Restored, dict]:
         h = ctypes.c_void_p()

@@ -228,24 +228,25 @@ def devsnap(a):
     mode = kc.KC_MODE_PRE_W if a.mode == "pre_w" else kc.KC_MODE_POST
     snap, rep = ctx.capture_dev(image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
                                 kernarg=synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=int(a.mutate)),
-                                mode=mode)
+                                mode=mode, host=a.host)
     orig_out = _download(out_va, sizes[2])
     np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_orig_out.npy"), orig_out)
     snap.save(a.dir)
-    out = {"capture": rep, "vas": vas, "arena_bytes": snap.nbytes()}
+    out = {"capture": rep, "vas": vas, "arena_bytes": snap.nbytes(), "is_host": snap.is_host()}
     for va in vas:
         ctx.free(va)
-    r, rrep = ctx.restore_dev(snap)
-    out["restore"] = rrep
-    out["regions"] = [[x.base, x.size] for x in r.regions()]
-    out["replay"] = ctx.replay(r)
-    out["out_equal"] = bool(np.array_equal(_download(out_va, sizes[2]), orig_out))
-    treps, _ = ctx.validate(r, outs=[(out_va, sizes[2], "u64")])
-    out["typed"] = treps
-    reps, unexpected = ctx.validate(r)
-    out["validate"] = reps
-    out["unexpected_chunks"] = unexpected
-    r.release()
+    # restore -> replay -> validate -> release, `cycles` times in this process:
+    # every cycle must land on the captured VAs (the ctx VA heap, R28d)
+    out["cycles"] = []
+    for c in range(a.cycles):
+        r, rrep = ctx.restore_dev(snap)
+        cyc = {"restore": rrep, "regions": [[x.base, x.size] for x in r.regions()], "replay": ctx.replay(r),
+               "out_equal": bool(np.array_equal(_download(out_va, sizes[2]), orig_out))}
+        cyc["typed"], _ = ctx.validate(r, outs=[(out_va, sizes[2], "u64")])
+        cyc["validate"], cyc["unexpected_chunks"] = ctx.validate(r)
+        r.release()
+        out["cycles"].append(cyc)
+    out.update(out["cycles"][0])
     snap.free()
     print(json.dumps(out))
 
@@ -266,6 +267,8 @@ def main():
     p.add_argument("--memalloc", action="store_true")
     p.add_argument("--override", default=None)
     p.add_argument("--typed", default=None)
+    p.add_argument("--host", action="store_true")
+    p.add_argument("--cycles", type=int, default=1)
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
      "inproc": inproc, "devsnap": devsnap}[a.cmd](a)

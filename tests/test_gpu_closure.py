@@ -247,14 +247,23 @@ def test_typed_validation_of_a_float_output(tmp_path):
     assert t["n_elems"] == 32 * 64 and t["differing_elems"] == 0 and t["pass"] == 1 and t["max_abs"] == 0.0
 
 
-@pytest.mark.parametrize("mode,mutate", [("pre_w", True), ("post", False)])
-def test_device_snapshot_capture_restore_replay(tmp_path, mode, mutate):
-    """F1: the snapshot lives in an HBM arena; persisted with
-    kc_snapshot_save it is a valid kc-snapshot/1 directory (oracle O1); restored
-    at the same VAs from the arena, the replay reproduces the original output."""
+@pytest.mark.parametrize("mode,mutate,host", [("pre_w", True, False), ("post", False, False),
+                                               ("pre_w", True, True), ("post", False, True)])
+def test_device_snapshot_capture_restore_replay(tmp_path, mode, mutate, host):
+    """F1: the snapshot lives in an HBM arena (or a pinned host
+    arena, kc_capture_host); persisted with kc_snapshot_save it is a valid
+    kc-snapshot/1 directory (oracle O1); restored at the same VAs from the arena
+    three times in one process (R28d), the replay reproduces the original output."""
     d = str(tmp_path / "dev")
     os.makedirs(d, exist_ok=True)
-    res = run("devsnap", d, "--mode", mode, *(["--mutate"] if mutate else []))
+    res = run("devsnap", d, "--mode", mode, "--cycles", "3", *(["--mutate"] if mutate else []),
+              *(["--host"] if host else []))
+    assert res["is_host"] == host
+    for cyc in res["cycles"]:
+        assert cyc["regions"] == res["cycles"][0]["regions"]
+        assert cyc["out_equal"] and cyc["restore"]["verify_mismatch_chunks"] == 0
+        assert all(r["differing_bytes"] == 0 for r in cyc["validate"]) and cyc["unexpected_chunks"] == 0
+        assert cyc["typed"][0]["pass"] == 1
     from oracle import snapshot
     summ = snapshot.verify(snapshot.load(d))
     assert summ["ok"] == 3
