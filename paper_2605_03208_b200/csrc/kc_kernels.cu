@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kc_kernels.cuh"
 
@@ -588,11 +589,15 @@ __global__ void k3_written(const uint64_t* __restrict__ pre, const uint64_t* __r
 // vectors with no Inf/NaN exponent take the fast path.  Per-warp accumulators //
 // flush with one atomic per nonzero field when the segment changes.          //
 // ========================================================================== //
+// Per-lane accumulators.  Counters are 32-bit: a warp flushes at least every
+// kFlushUnits units (1 GiB), so one lane counts < 2^25 bytes between flushes.
 struct Acc {
-    unsigned long long dbytes, delems, nan_r, nan_a, nan_pos, rel_undef, fail, max_ulp;
+    uint32_t dbytes, delems, nan_r, nan_a, nan_pos, rel_undef, fail;
+    unsigned long long max_ulp;
     double max_abs, max_rel;
     uint32_t any;  // this lane saw a differing byte in the current unit
 };
+constexpr uint64_t kFlushUnits = 65536;
 
 __device__ __forceinline__ void acc_zero(Acc& a) {
     a.dbytes = a.delems = a.nan_r = a.nan_a = a.nan_pos = a.rel_undef = a.fail = a.max_ulp = 0;
@@ -636,8 +641,8 @@ __device__ __forceinline__ uint32_t special_word(uint32_t w) {
     return 0;
 }
 
-template <int DT>
-__device__ __forceinline__ bool isnan_bits(uint64_t b) {
+template <int DT, typename B>
+__device__ __forceinline__ bool isnan_bits(B b) {
     if (DT == KC_DT_F16) return (b & 0x7FFFu) > 0x7C00u;
     if (DT == KC_DT_BF16) return (b & 0x7FFFu) > 0x7F80u;
     if (DT == KC_DT_F32) return (b & 0x7FFFFFFFu) > 0x7F800000u;
@@ -645,18 +650,22 @@ __device__ __forceinline__ bool isnan_bits(uint64_t b) {
 }
 
 // exact conversion to fp64 (no FTZ: compiled without fast-math)
-template <int DT>
-__device__ __forceinline__ double to_f64(uint64_t b) {
+template <int DT, typename B>
+__device__ __forceinline__ double to_f64(B b) {
     if (DT == KC_DT_F16) return (double)__half2float(__ushort_as_half((unsigned short)b));
     if (DT == KC_DT_BF16) return (double)__uint_as_float((uint32_t)b << 16);
     if (DT == KC_DT_F32) return (double)__uint_as_float((uint32_t)b);
     return __longlong_as_double((long long)b);
 }
 
-// One element (float dtypes): r, a raw bits.
+// One element (float dtypes): r, a raw bits (32-bit arithmetic below 8-byte types).
 template <int DT>
-__device__ __forceinline__ void elem_float(uint64_t r, uint64_t a, Acc& acc, double atol, double rtol, int equal_nan) {
+__device__ __forceinline__ void elem_float(typename std::conditional<DT_<DT>::S == 8, uint64_t, uint32_t>::type r,
+                                           typename std::conditional<DT_<DT>::S == 8, uint64_t, uint32_t>::type a,
+                                           Acc& acc, double atol, double rtol, int equal_nan) {
     constexpr int S = DT_<DT>::S;
+    using B = typename std::conditional<S == 8, uint64_t, uint32_t>::type;
+    using SI = typename std::conditional<S == 8, long long, int>::type;
     const bool nr = isnan_bits<DT>(r), na = isnan_bits<DT>(a);
     const bool differ = r != a;
     acc.delems += differ;
@@ -668,12 +677,11 @@ __device__ __forceinline__ void elem_float(uint64_t r, uint64_t a, Acc& acc, dou
         return;
     }
     if (!differ) return;
-    // ordered-integer ULP distance
-    const uint64_t sign = 1ULL << (8 * S - 1);
-    const long long oa = (a & sign) ? -(long long)(a & ~sign) : (long long)a;
-    const long long orr = (r & sign) ? -(long long)(r & ~sign) : (long long)r;
-    const unsigned long long ulp =
-        oa >= orr ? (unsigned long long)oa - (unsigned long long)orr : (unsigned long long)orr - (unsigned long long)oa;
+    // ordered-integer ULP distance (|oa - orr| < 2^(8S), exact in B)
+    const B sign = (B)1 << (8 * S - 1);
+    const SI oa = (a & sign) ? -(SI)(a & ~sign) : (SI)a;
+    const SI orr = (r & sign) ? -(SI)(r & ~sign) : (SI)r;
+    const B ulp = oa >= orr ? (B)oa - (B)orr : (B)orr - (B)oa;
     if (ulp > acc.max_ulp) acc.max_ulp = ulp;
     const double av = to_f64<DT>(a), rv = to_f64<DT>(r);
     const double d = fabs(__dsub_rn(av, rv));
@@ -809,6 +817,77 @@ __device__ __forceinline__ void vec_slow(const uint32_t (&r)[8], const uint32_t 
     }
 }
 
+// ---- compacted per-element path for float dtypes: every lane appends the
+// (ref, act) bits of its flagged elements to a per-warp shared-memory queue
+// (warp prefix sum for the slots); full rounds of 32 elements are then
+// processed with every lane busy, instead of each lane looping over its own
+// mask (SIMT runs the longest lane's loop: ~12 of 32 lanes were active at
+// 11% mismatch density).  All accumulations are sums and maxima, so the order
+// in which elements are processed does not change a report bit.
+template <int DT> struct QT_ { using T = uint32_t; };  // 2-byte types: r | a << 16
+template <> struct QT_<KC_DT_F32> { using T = uint2; };
+template <> struct QT_<KC_DT_F64> { using T = ulonglong2; };
+template <int DT, int U>
+struct KQ {  // queue capacity: < 32 carried + the most one step can append
+    static constexpr int kCap = 32 + 32 * U * (32 / DT_<DT>::S);
+    static constexpr int kBytes = kCap * (int)sizeof(typename QT_<DT>::T);
+};
+
+template <int DT>
+__device__ __forceinline__ void q_push(const uint32_t (&r)[8], const uint32_t (&a)[8], uint32_t mask,
+                                       typename QT_<DT>::T* q, uint32_t& pos) {
+    constexpr int S = DT_<DT>::S;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if constexpr (S == 2) {
+            if (mask & (1u << (2 * i))) q[pos++] = __byte_perm(r[i], a[i], 0x5410);
+            if (mask & (2u << (2 * i))) q[pos++] = __byte_perm(r[i], a[i], 0x7632);
+        } else if constexpr (S == 4) {
+            if (mask & (1u << i)) q[pos++] = make_uint2(r[i], a[i]);
+        } else {
+            if ((i & 1) && (mask & (1u << (i >> 1))))
+                q[pos++] = make_ulonglong2((unsigned long long)r[i - 1] | ((unsigned long long)r[i] << 32),
+                                           (unsigned long long)a[i - 1] | ((unsigned long long)a[i] << 32));
+        }
+    }
+}
+
+template <int DT>
+__device__ __forceinline__ void q_item(typename QT_<DT>::T t, Acc& acc, double atol, double rtol, int equal_nan) {
+    if constexpr (DT_<DT>::S == 2)
+        elem_float<DT>(t & 0xFFFFu, t >> 16, acc, atol, rtol, equal_nan);
+    else
+        elem_float<DT>(t.x, t.y, acc, atol, rtol, equal_nan);
+}
+
+// process floor(qn/32) full rounds, move the remainder to the front
+template <int DT>
+__device__ __forceinline__ void q_drain(typename QT_<DT>::T* q, uint32_t& qn, Acc& acc, double atol, double rtol,
+                                        int equal_nan, int lane) {
+    __syncwarp();
+    const uint32_t full = qn & ~31u, rem = qn - full;
+    for (uint32_t i = lane; i < full; i += 32) q_item<DT>(q[i], acc, atol, rtol, equal_nan);
+    typename QT_<DT>::T t;
+    if (lane < rem) t = q[full + lane];
+    __syncwarp();
+    if (lane < rem) q[lane] = t;
+    __syncwarp();
+    qn = rem;
+}
+
+// process everything left (before a report flush)
+template <int DT>
+__device__ __forceinline__ void q_finish(typename QT_<DT>::T* q, uint32_t& qn, Acc& acc, double atol, double rtol,
+                                         int equal_nan, int lane) {
+    if constexpr (DT_<DT>::F) {
+        if (qn == 0) return;
+        __syncwarp();
+        if (lane < qn) q_item<DT>(q[lane], acc, atol, rtol, equal_nan);
+        __syncwarp();
+        qn = 0;
+    }
+}
+
 // scalar path: one element at byte offset o (element-size aligned within the buffer)
 template <int DT>
 __device__ __forceinline__ void elem_scalar(const uint8_t* R, const uint8_t* A, Acc& acc, double atol, double rtol,
@@ -849,13 +928,16 @@ __device__ __forceinline__ void ld256(const void* p, uint32_t* w) {
 // in flight per lane; the per-element path runs once per vector that needs it.
 template <int DT, int U>
 __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, uint32_t len, bool vec_ok, Acc& acc,
-                                          double atol, double rtol, int equal_nan, int lane) {
+                                          double atol, double rtol, int equal_nan, int lane,
+                                          typename QT_<DT>::T* q, uint32_t& qn) {
     constexpr int S = DT_<DT>::S;
     uint32_t done = 0;
     if (vec_ok) {
         const uint32_t nvec = len / 32;
         uint32_t v = lane;
-        for (; v + 32 * (U - 1) < nvec; v += 32 * U) {
+        // every lane runs the same number of U-steps (nvec is warp-uniform), so
+        // the warp-wide queue operations below see all 32 lanes
+        for (; v - lane + 32 * U <= nvec; v += 32 * U) {
             uint32_t rw[U][8], aw[U][8];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -868,6 +950,26 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
             for (int u = 0; u < U; ++u) {
                 m[u] = vec_scan<DT>(rw[u], aw[u], acc);
                 any |= m[u];
+            }
+            if constexpr (DT_<DT>::F) {
+                if (__any_sync(0xFFFFFFFFu, any != 0)) {
+                    uint32_t c = 0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) c += __popc(m[u]);
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                        if (lane >= d) incl += t;
+                    }
+                    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    uint32_t pos = qn + incl - c;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) q_push<DT>(rw[u], aw[u], m[u], q, pos);
+                    qn += total;
+                    if (qn >= 32) q_drain<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+                }
+                continue;
             }
             if (any) {
 #pragma unroll 1
@@ -979,24 +1081,35 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
     Acc acc;
     acc_zero(acc);
+    extern __shared__ __align__(16) uint8_t k2_smem[];
+    typename QT_<DT>::T* q =
+        reinterpret_cast<typename QT_<DT>::T*>(k2_smem + (size_t)(threadIdx.x >> 5) * KQ<DT, VU>::kBytes);
+    uint32_t qn = 0;  // warp-uniform queue length
     for (uint64_t u = u0; u < u1; ++u) {
         while (s + 1 < nseg && segs[s + 1].unit_off <= u) {
+            q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
             acc_flush(acc, reps + segs[s].report, lane);
             ++s;
         }
         const SegDev sg = segs[s];
+        const uint32_t s_rep = sg.report;
         const uint64_t off = (u - sg.unit_off) * (uint64_t)kDiffUnit;
         const uint32_t len = (uint32_t)min((uint64_t)kDiffUnit, sg.nbytes - off);
         const uint8_t* R = reinterpret_cast<const uint8_t*>(sg.ref) + off;
         const uint8_t* A = reinterpret_cast<const uint8_t*>(sg.act) + off;
         const bool vec_ok = ((sg.ref | sg.act) & 31) == 0;
         acc.any = 0;
-        diff_unit<DT, VU>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane);
+        diff_unit<DT, VU>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane, q, qn);
         if (__any_sync(0xFFFFFFFFu, acc.any) && lane == 0 && bitmaps) {
             const uint64_t k = sg.bitmap_chunk0 + off / kChunk;
             atomicOr(bitmaps + sg.bitmap_word0 + k / 64, 1ULL << (k % 64));
         }
+        if ((u - u0) % kFlushUnits == kFlushUnits - 1) {  // keeps the 32-bit lane counters in range
+            q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+            acc_flush(acc, reps + s_rep, lane);
+        }
     }
+    q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
     acc_flush(acc, reps + segs[s].report, lane);
 }
 
@@ -1136,8 +1249,14 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
     constexpr int WPB = THREADS / 32;
     uint64_t grid = (G.n_units + WPB - 1) / WPB;
     if (grid > (uint64_t)num_sms * MINB) grid = (uint64_t)num_sms * MINB;
-    k2_diff<DT, THREADS, MINB, U><<<(unsigned)grid, THREADS, 0, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
-                                                                      d_reps, bm, atol, rtol, equal_nan);
+    const int smem = DT_<DT>::F ? WPB * KQ<DT, U>::kBytes : 0;
+    static bool attr = [] {
+        return cudaFuncSetAttribute(k2_diff<DT, THREADS, MINB, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    DT_<DT>::F ? WPB * KQ<DT, U>::kBytes : 0) == cudaSuccess;
+    }();
+    (void)attr;
+    k2_diff<DT, THREADS, MINB, U><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
+                                                                         d_reps, bm, atol, rtol, equal_nan);
 }
 
 // Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per

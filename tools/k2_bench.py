@@ -26,7 +26,10 @@ ctx = kc.Context(0)
 g = torch.Generator(device="cuda").manual_seed(3)
 res = {}
 n = 2 * 2**30  # elements of bf16 per buffer: 4 GiB
-for name in ["identical_bf16", "c3_planted_bf16", "c3_planted_f16", "identical_bytes"]:
+cases = ["identical_bf16", "c3_planted_bf16", "c3_planted_f16", "identical_bytes"]
+if os.environ.get("KC_K2_CASES"):
+    cases = os.environ["KC_K2_CASES"].split(",")
+for name in cases:
     tdt = torch.float16 if "f16" in name and "bf16" not in name else torch.bfloat16
     ref = (torch.randn(n // 2, device="cuda", generator=g) * 0.5).to(tdt)
     act = ref.clone()
