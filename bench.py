@@ -361,10 +361,15 @@ def run_ours(a, rank, world, device, log):
             "frac_of_spec_8000": kern[dom]["gbs"] / 8000.0, "share_of_step": share,
             "alg_bytes_per_launch": kern[dom]["alg_bytes"]}
 
+    # ------------------------------------------------------------------ F2 fused step
+    fused = None
+    if not a.no_fused:
+        fused = run_fused(a, ctx, pool, stream, pre, post, dig, wbm, wcnt, bufs, reps, C, nreg, world, log)
+
     # ------------------------------------------------------------------ e2e
     e2e = None
     if not a.no_e2e:
-        e2e = run_e2e(a, ctx, pool, step, stream, world, log)
+        e2e = run_e2e(a, ctx, pool, step, stream, world, log, reps)
     lat = None
     if world == 1 and not a.no_latency:
         try:
@@ -383,12 +388,69 @@ def run_ours(a, rank, world, device, log):
                    "bytes_this_rank": pool.bytes, "l2": "inputs (30 GB) >> L2 (126 MB); no flush needed",
                    "parallelism": f"E1 residency-first shards over {world} GPU(s)"},
         "roofline": roof, "kernels": kern, "clocks": clk, "gpu_launches": launches,
-        "e2e": e2e, "capture_replay": lat, "fingerprint": fingerprint,
+        "e2e": e2e, "capture_replay": lat, "fingerprint": fingerprint, "fused_step": fused,
     }
     return res, pool
 
 
-def run_e2e(a, ctx, pool, step, stream, world, log):
+def run_fused(a, ctx, pool, stream, pre, post, dig, wbm, wcnt, bufs, reps, C, nreg, world, log):
+    """F2: the same step with the post-manifest and the pool-pair validation fused
+    (kc_hash_diff_async: K5 reads pool and reference once, hashing the pool while
+    comparing; K2 then reads only dirty chunks).  Same algorithmic work as the
+    headline step (hash 2N, validate 2N); the post-manifest and the reports must
+    equal the unfused step's bit for bit."""
+    import torch
+    sh = stream.cuda_stream
+    post_ref = post.clone()
+    reps_ref = reps.clone()
+    reps_f = torch.zeros_like(reps)
+    dirty = torch.zeros((C + 63) // 64 + 1, dtype=torch.int64, device="cuda")
+    bms = torch.zeros(sum(((b.nbytes + 65535) // 65536 + 63) // 64 for b in bufs) + 1, dtype=torch.int64,
+                      device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+
+    def step(ev):
+        ctx.hash(pool.regions, pre.data_ptr(), dig.data_ptr(), dig.data_ptr() + 8 * nreg if world == 1 else 0,
+                 stream=sh)
+        n = pool.launch_f3(sh)
+        if ev is not None:
+            ev[0].record(stream)
+        ctx.hash_diff_async(bufs, post.data_ptr(), reps_f.data_ptr(), bms.data_ptr(), dirty.data_ptr(), stream=sh)
+        if ev is not None:
+            ev[1].record(stream)
+        ctx.written(pre.data_ptr(), post.data_ptr(), C, wbm.data_ptr(), wcnt.data_ptr(), stream=sh)
+        return n
+    for _ in range(a.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(post, post_ref)) and bool(torch.equal(reps_f, reps_ref))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(a.steps):
+        step(evs[i])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+    ms = float(tm.item())
+    k5_ms = sum(x[0].elapsed_time(x[1]) for x in evs) / a.steps
+    n_dirty = int(sum(bin(int(w) & 0xFFFFFFFFFFFFFFFF).count("1") for w in dirty.cpu().tolist()))
+    log(f"fused step: {ms:.3f} ms (K5 + filtered K2 {k5_ms:.3f} ms, {n_dirty} dirty chunks), "
+        f"bit-identical to the unfused step: {same}")
+    return {"ms_per_step": ms, "value_same_metric": 4 * pool.bytes * world / (ms * 1e-3) / 1e9,
+            "identical_to_unfused": same, "dirty_chunks": n_dirty,
+            "K5_plus_filtered_K2": {"ms": k5_ms, "hbm_bytes": 2 * pool.bytes,
+                                    "gbs": 2 * pool.bytes / (k5_ms * 1e-3) / 1e9},
+            "step": "K1 pre-manifest + F3 dispatch + K5 fused post-manifest/compare + K2 over dirty chunks + "
+                    "K3 written set"}
+
+
+def run_e2e(a, ctx, pool, step, stream, world, log, reps):
     """Same metric through the public API with the snapshot in pinned HOST memory:
     every step copies the snapshot host->device (restore) before the device hot
     path and reads the reports back."""
@@ -401,7 +463,7 @@ def run_e2e(a, ctx, pool, step, stream, world, log):
         host[s.name] = h
     torch.cuda.synchronize()
     steps = max(1, min(a.steps, a.e2e_steps))
-    out = torch.empty(16 * 185 + 8, dtype=torch.int64, pin_memory=True)
+    out = torch.empty(reps.numel(), dtype=torch.int64, pin_memory=True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -413,7 +475,7 @@ def run_e2e(a, ctx, pool, step, stream, world, log):
             synth.dev_view(pool.ref[s.name], s.size, torch.cuda.current_device()).copy_(host[s.name],
                                                                                          non_blocking=True)
         step(None)
-        out[:8].copy_(torch.zeros(8, dtype=torch.int64, device="cuda"), non_blocking=True)
+        out.copy_(reps, non_blocking=True)  # the step's result: every validation report
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
@@ -424,7 +486,7 @@ def run_e2e(a, ctx, pool, step, stream, world, log):
     host.clear()
     total = 4 * pool.total_bytes
     return {"value": total / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": pool.total_bytes,
-            "d2h_bytes_per_step": 8 * (16 * len(pool.specs)), "ms_per_step": ms, "steps": steps,
+            "d2h_bytes_per_step": 8 * reps.numel(), "ms_per_step": ms, "steps": steps,
             "h2d_gbs": pool.total_bytes / world / (ms * 1e-3) / 1e9}
 
 
@@ -638,6 +700,7 @@ def main():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-fused", action="store_true", help="skip the F2 fused-step measurement")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-sample-mb", type=int, default=384)
     p.add_argument("--cpu-seconds", type=float, default=10.0)

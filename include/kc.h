@@ -250,6 +250,24 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
 kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
                   kc_diff_report* reps, uint64_t* h_bitmaps, void* stream);
 
+/* ---- F2 fused hash + validate ----------------------
+ * One pass (K5) over every buffer pair hashes the ACTUAL bytes (the chunk
+ * manifest of the regions {act, nbytes} in the given order: bit-identical to
+ * kc_hash over them) while comparing them with the reference.  A chunk whose
+ * bits all agree and whose reference holds no Inf/NaN (float dtypes)
+ * contributes nothing to any report field; K2 then reads only the other
+ * ("dirty") chunks.  Results equal kc_diff's: one report per buffer (the
+ * .report and .bitmap_chunk0 fields are ignored) in d_reports (device, n),
+ * bitmaps (device, may be NULL) concatenated per buffer at ceil(n_chunks_i/64)
+ * words each.  d_chunk_hash: device, sum of n_chunks_i words.  d_dirty:
+ * device ceil(C/64) words receiving the dirty-chunk bitmap, or NULL (ctx
+ * scratch).  Buffers not 16-byte aligned run K1 + an unfiltered K2 instead
+ * (every chunk reported dirty).
+ * Asynchronous on stream. */
+kc_status kc_hash_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
+                             uint64_t* d_chunk_hash, kc_diff_report* d_reports, uint64_t* d_bitmaps,
+                             uint64_t* d_dirty, void* stream);
+
 /* ---- A3/A5 capture --------------- */
 /* Quiesce, hash, write metadata FIRST, snapshot through the pinned ring,
  * forward the dispatch, hash again, record W, write capture_log.json and the

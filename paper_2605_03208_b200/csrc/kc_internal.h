@@ -47,6 +47,8 @@ struct kc_ctx {
     // cached device tables / scratch (stream-ordered; one stream at a time per ctx)
     kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map;
     std::vector<kc::RegionDev> regs_cached;
+    kc_ctx_dev_buf pairs, pair_map, dirty;  // F2 (K5) pair table, chunk -> pair map, dirty bitmap
+    std::vector<kc::PairDev> pairs_cached;
     std::vector<uint8_t> diff_key;  // K2 plan cache (raw inputs of the last kc_diff_async)
     std::vector<kc::DiffGroup> diff_groups;
     uint64_t diff_bitmap_words = 0;

@@ -469,6 +469,179 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     cp_async_wait<0>();
 }
 
+// ========================================================================== //
+// K5 (F2 fused hash + compare): K1's cp.async ring staging BOTH the actual    //
+// and the reference slice of 8 chunks per warp; each quad lane hashes its     //
+// actual words (the post-manifest, bit-identical to K1) and ORs act ^ ref and //
+// the reference's Inf/NaN exponent flags (float dtypes) into per-lane flags.  //
+// A chunk is CLEAN when every bit agrees and the reference holds no Inf/NaN:  //
+// it then contributes nothing to any report field, and K2 skips it.  Chunks   //
+// with a sub-32-byte tail are marked dirty (K2 decides them exactly).         //
+// ========================================================================== //
+template <int WARPS, int STAGES, int SL>
+struct CmpCfg {
+    static constexpr int kWarps = WARPS, kStages = STAGES, kSlice = SL;
+    static constexpr int kPitch = SL + 32;
+    static constexpr int kWStage = 16 * kPitch;          // 8 actual + 8 reference slices
+    static constexpr int kUPC = SL / 16;                 // 16-byte units per slice
+    static constexpr int kUPL = (16 * kUPC + 31) / 32;   // units per lane per step
+    static constexpr size_t kSmem = (size_t)WARPS * STAGES * kWStage;
+};
+
+// special-exponent masks per dtype on the low / high 32-bit word of 8 bytes:
+// ((w & M) + A) has bit H set exactly where an element's exponent is all ones
+struct SpecMask { uint32_t m_lo, a_lo, m_hi, a_hi, h_lo, h_hi; };
+__device__ __forceinline__ SpecMask spec_mask(int dt) {
+    switch (dt) {
+        case KC_DT_F16: return {0x7C007C00u, 0x04000400u, 0x7C007C00u, 0x04000400u, 0x80008000u, 0x80008000u};
+        case KC_DT_BF16: return {0x7F807F80u, 0x00800080u, 0x7F807F80u, 0x00800080u, 0x80008000u, 0x80008000u};
+        case KC_DT_F32: return {0x7F800000u, 0x00800000u, 0x7F800000u, 0x00800000u, 0x80000000u, 0x80000000u};
+        case KC_DT_F64: return {0u, 0u, 0x7FF00000u, 0x00100000u, 0u, 0x80000000u};
+        default: return {0u, 0u, 0u, 0u, 0u, 0u};
+    }
+}
+
+template <class CFG>
+__global__ void __launch_bounds__(CFG::kWarps * 32, 1)
+    k5_hash_cmp(const PairDev* __restrict__ pairs, int npair, uint64_t C, uint64_t* __restrict__ out,
+                unsigned long long* __restrict__ dirty, const uint32_t* __restrict__ map) {
+    constexpr int WARPS = CFG::kWarps, STAGES = CFG::kStages, SL = CFG::kSlice, PITCH = CFG::kPitch;
+    constexpr int WSTAGE = CFG::kWStage, UPC = CFG::kUPC, UPL = CFG::kUPL;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q = lane >> 2, ql = lane & 3;
+    const unsigned qmask = 0xFu << (lane & 28);
+    uint8_t* wring = smem + (size_t)w * STAGES * WSTAGE;
+    const uint64_t ngroups = (C + 7) / 8;
+    const uint64_t W = (uint64_t)gridDim.x * WARPS;
+    const uint64_t j0 = (uint64_t)w * gridDim.x + blockIdx.x;
+    auto pair_of = [&](uint64_t g) -> int {
+        if (map) return (int)__ldg(map + g);
+        int lo = 0, hi = npair;  // last pair with chunk_off <= g
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pairs[mid].chunk_off <= g) lo = mid; else hi = mid;
+        }
+        return lo;
+    };
+
+    uint64_t jf = j0;
+    uint32_t sf = 0, f_nsl = 0;
+    unsigned long long u_src[UPL];
+    uint32_t u_bytes[UPL];
+    auto load_group = [&](uint64_t j) {
+        const uint64_t g = 8 * j + q;
+        unsigned long long sa = 0, sr = 0;
+        uint32_t bytes = 0;
+        if (g < C) {
+            const PairDev& P = pairs[pair_of(g)];
+            const uint64_t off = (g - P.chunk_off) * kChunk, rem = P.size - off;
+            const uint32_t len = rem < kChunk ? (uint32_t)rem : (uint32_t)kChunk;
+            sa = P.act + off;
+            sr = P.ref + off;
+            bytes = len >= 32 ? (len & ~31u) : 0u;
+        }
+        f_nsl = __reduce_max_sync(0xFFFFFFFFu, (bytes + SL - 1) / SL);
+#pragma unroll
+        for (int k = 0; k < UPL; ++k) {
+            const int u = lane + 32 * k;
+            const int qq = (u / UPC) & 7;
+            const unsigned long long a = __shfl_sync(0xFFFFFFFFu, sa, 4 * qq);
+            const unsigned long long r = __shfl_sync(0xFFFFFFFFu, sr, 4 * qq);
+            u_src[k] = u < 8 * UPC ? a : r;
+            u_bytes[k] = __shfl_sync(0xFFFFFFFFu, bytes, 4 * qq);
+        }
+    };
+    auto issue = [&](int stage) {
+        uint8_t* dst = wring + stage * WSTAGE;
+#pragma unroll
+        for (int k = 0; k < UPL; ++k) {
+            const int u = lane + 32 * k;
+            if (u < 16 * UPC) {
+                const int slot = u / UPC, off = (u % UPC) * 16;  // slot 0-7 actual, 8-15 reference
+                const uint32_t g_off = sf * SL + off;
+                if (g_off < u_bytes[k])
+                    cp_async16(dst + slot * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+            }
+        }
+    };
+    auto advance = [&]() {
+        if (++sf >= f_nsl) {
+            sf = 0;
+            jf += W;
+            if (jf < ngroups) load_group(jf); else f_nsl = 0;
+        }
+    };
+    auto fetch = [&](int stage) {
+        while (jf < ngroups && f_nsl == 0) {
+            jf += W;
+            if (jf < ngroups) load_group(jf);
+        }
+        if (jf < ngroups) {
+            issue(stage);
+            advance();
+        }
+        cp_async_commit();
+    };
+    if (j0 < ngroups) load_group(jf);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) fetch(s);
+    uint32_t step = 0;
+    for (uint64_t j = j0; j < ngroups; j += W) {
+        const uint64_t g = 8 * j + q;
+        const uint8_t* src = nullptr;
+        uint32_t len = 0;
+        SpecMask sm = {0u, 0u, 0u, 0u, 0u, 0u};
+        if (g < C) {
+            const PairDev& P = pairs[pair_of(g)];
+            const uint64_t off = (g - P.chunk_off) * kChunk, rem = P.size - off;
+            len = rem < kChunk ? (uint32_t)rem : (uint32_t)kChunk;
+            src = reinterpret_cast<const uint8_t*>(P.act + off);
+            sm = spec_mask(P.dtype);
+        }
+        const uint32_t nst = len >= 32 ? len / 32 : 0;
+        const uint32_t nsl = __reduce_max_sync(0xFFFFFFFFu, (nst * 32 + SL - 1) / SL);
+        uint64_t v = lane_seed(ql);
+        unsigned long long x = 0;
+        uint32_t sp_lo = 0, sp_hi = 0;
+        for (uint32_t s = 0; s < nsl; ++s, ++step) {
+            cp_async_wait<STAGES - 2>();
+            __syncwarp();
+            const int st = step % STAGES;
+            const uint64_t* pa = reinterpret_cast<const uint64_t*>(wring + st * WSTAGE + q * PITCH) + ql;
+            const uint64_t* pr = reinterpret_cast<const uint64_t*>(wring + st * WSTAGE + (8 + q) * PITCH) + ql;
+            const uint32_t done = s * (SL / 32);
+            const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
+            auto word = [&](int t) {
+                const uint64_t a = pa[4 * t], r = pr[4 * t];
+                v = xround_fast(v, a);
+                x |= a ^ r;
+                sp_lo |= ((uint32_t)r & sm.m_lo) + sm.a_lo;
+                sp_hi |= ((uint32_t)(r >> 32) & sm.m_hi) + sm.a_hi;
+            };
+            if (n == SL / 32) {
+#pragma unroll
+                for (int t = 0; t < SL / 32; ++t) word(t);
+            } else {
+                for (uint32_t t = 0; t < n; ++t) word(t);
+            }
+            __syncwarp();
+            fetch((step + STAGES - 1) % STAGES);
+        }
+        const bool mine = x != 0 || ((sp_lo & sm.h_lo) | (sp_hi & sm.h_hi)) != 0 || (len & 31u) != 0;
+        const bool d = __ballot_sync(0xFFFFFFFFu, mine) & qmask;
+        if (g < C) {
+            const uint64_t h = quad_finish<true>(v, ql, qmask, len, src + (size_t)nst * 32);
+            if (ql == 0) {
+                out[g] = h;
+                if (d) atomicOr(dirty + (g >> 6), 1ULL << (g & 63));
+            }
+        } else {
+            quad_finish<true>(v, ql, qmask, 0, nullptr);
+        }
+    }
+    cp_async_wait<0>();
+}
+
 // Unaligned regions (base % 16 != 0): quad per chunk, byte-assembled loads.
 __global__ void __launch_bounds__(256)
     k1_hash_generic(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out,
@@ -767,20 +940,23 @@ __device__ __forceinline__ uint32_t vec_scan(const uint32_t (&r)[8], const uint3
             return 0;
         }
     }
+    // an element is flagged when its bits differ, or (float types) when the
+    // reference is Inf/NaN: an element with equal bits has special(a) ==
+    // special(r), and one with differing bits is flagged already
     uint32_t mask = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         if (S == 8) {
             if (i & 1) {
-                const uint32_t sp = F ? (special_word<DT>(r[i]) | special_word<DT>(a[i])) : 0u;
+                const uint32_t sp = F ? special_word<DT>(r[i]) : 0u;
                 mask |= (uint32_t)(((x[i - 1] | x[i]) | sp) != 0) << (i >> 1);
             }
         } else if (S == 4) {
-            const uint32_t sp = F ? (special_word<DT>(r[i]) | special_word<DT>(a[i])) : 0u;
+            const uint32_t sp = F ? special_word<DT>(r[i]) : 0u;
             mask |= (uint32_t)((x[i] | sp) != 0) << i;
         } else if (S == 2) {
             uint32_t m = (((x[i] & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x[i]) & 0x80008000u;
-            if (F) m |= special_word<DT>(r[i]) | special_word<DT>(a[i]);
+            if (F) m |= special_word<DT>(r[i]);
             mask |= (((m >> 15) & 1u) | ((m >> 30) & 2u)) << (2 * i);
         } else {
             const uint32_t m = (((x[i] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x[i]) & 0x80808080u;
@@ -1058,17 +1234,22 @@ __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
 
 // One launch per dtype group: segments [seg0, seg0+nseg) own the global units
 // [unit0, unit0+U).
+// Unfiltered: each warp takes a contiguous block of units.  Filtered (K5 ran
+// first): units are interleaved over warps (u = unit0 + w + k*W) so the dirty
+// chunks, wherever they cluster, spread evenly; a unit whose chunk is clean is
+// skipped without reading it.
 template <int DT, int THREADS, int MINB, int VU>
 __global__ void __launch_bounds__(THREADS, MINB)
     k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
             kc_diff_report* __restrict__ reps, unsigned long long* __restrict__ bitmaps, double atol, double rtol,
-            int equal_nan) {
+            int equal_nan, const unsigned long long* __restrict__ filter) {
     const int lane = threadIdx.x & 31;
     segs += seg0;
     const uint64_t W = (uint64_t)gridDim.x * (THREADS / 32);
     const uint64_t w = (uint64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
-    // contiguous block of units for this warp
-    const uint64_t u0 = unit0 + (U * w) / W, u1 = unit0 + (U * (w + 1)) / W;
+    const uint64_t u0 = filter ? unit0 + w : unit0 + (U * w) / W;
+    const uint64_t u1 = filter ? unit0 + U : unit0 + (U * (w + 1)) / W;
+    const uint64_t ustep = filter ? W : 1;
     if (u0 >= u1) return;
     int s = 0;
     {
@@ -1085,7 +1266,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     typename QT_<DT>::T* q =
         reinterpret_cast<typename QT_<DT>::T*>(k2_smem + (size_t)(threadIdx.x >> 5) * KQ<DT, VU>::kBytes);
     uint32_t qn = 0;  // warp-uniform queue length
-    for (uint64_t u = u0; u < u1; ++u) {
+    uint64_t since_flush = 0;
+    for (uint64_t u = u0; u < u1; u += ustep) {
         while (s + 1 < nseg && segs[s + 1].unit_off <= u) {
             q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
             acc_flush(acc, reps + segs[s].report, lane);
@@ -1094,6 +1276,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
         const SegDev sg = segs[s];
         const uint32_t s_rep = sg.report;
         const uint64_t off = (u - sg.unit_off) * (uint64_t)kDiffUnit;
+        if (filter) {
+            const uint64_t c = sg.filter_chunk0 + off / kChunk;
+            if (!((__ldg(filter + (c >> 6)) >> (c & 63)) & 1ULL)) continue;  // clean chunk
+        }
         const uint32_t len = (uint32_t)min((uint64_t)kDiffUnit, sg.nbytes - off);
         const uint8_t* R = reinterpret_cast<const uint8_t*>(sg.ref) + off;
         const uint8_t* A = reinterpret_cast<const uint8_t*>(sg.act) + off;
@@ -1104,7 +1290,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
             const uint64_t k = sg.bitmap_chunk0 + off / kChunk;
             atomicOr(bitmaps + sg.bitmap_word0 + k / 64, 1ULL << (k % 64));
         }
-        if ((u - u0) % kFlushUnits == kFlushUnits - 1) {  // keeps the 32-bit lane counters in range
+        if (++since_flush == kFlushUnits) {  // keeps the 32-bit lane counters in range
+            since_flush = 0;
             q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
             acc_flush(acc, reps + s_rep, lane);
         }
@@ -1164,6 +1351,7 @@ using TmaA = HkCfg<256, 3, 1024>;  // 64 slots x 3 x 1 KiB
 using TmaB = HkCfg<128, 3, 2048>;  // 32 slots x 3 x 2 KiB
 using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bound)
 using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
+using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
 
 cudaError_t kernels_init() {
     cudaError_t e = cudaFuncSetAttribute(k1_hash_tma<TmaA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaA::kSmem);
@@ -1174,7 +1362,19 @@ cudaError_t kernels_init() {
         e = cudaFuncSetAttribute(k1_hash_cpasync<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
     KC_CP_ATTR(CpA) KC_CP_ATTR(CpD)
 #undef KC_CP_ATTR
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
     return e;
+}
+
+cudaError_t launch_hash_cmp(const PairDev* d_pairs, int npair, uint64_t C, uint64_t* d_out, uint64_t* d_dirty,
+                            const uint32_t* map, int num_sms, cudaStream_t s) {
+    if (C == 0) return cudaSuccess;
+    const uint64_t groups = (C + 7) / 8;
+    const uint64_t grid = std::min<uint64_t>((groups + CmpA::kWarps - 1) / CmpA::kWarps, (uint64_t)num_sms);
+    k5_hash_cmp<CmpA><<<(unsigned)grid, CmpA::kWarps * 32, CmpA::kSmem, s>>>(
+        d_pairs, npair, C, d_out, reinterpret_cast<unsigned long long*>(d_dirty), map);
+    return cudaGetLastError();
 }
 
 template <class CFG>
@@ -1245,7 +1445,7 @@ cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64
 template <int DT, int THREADS, int MINB, int U>
 static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps,
                           unsigned long long* bm, double atol, double rtol, int equal_nan, int num_sms,
-                          cudaStream_t s) {
+                          cudaStream_t s, const unsigned long long* filter) {
     constexpr int WPB = THREADS / 32;
     uint64_t grid = (G.n_units + WPB - 1) / WPB;
     if (grid > (uint64_t)num_sms * MINB) grid = (uint64_t)num_sms * MINB;
@@ -1256,7 +1456,7 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
     }();
     (void)attr;
     k2_diff<DT, THREADS, MINB, U><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
-                                                                         d_reps, bm, atol, rtol, equal_nan);
+                                                                         d_reps, bm, atol, rtol, equal_nan, filter);
 }
 
 // Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per
@@ -1265,20 +1465,22 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
 // registers) spilled segment state into the inner loop (3.6 TB/s).
 template <int DT>
 static void launch_k2(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps, unsigned long long* bm,
-                      double atol, double rtol, int equal_nan, int num_sms, cudaStream_t s) {
-    launch_k2_cfg<DT, 512, 1, 2>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s);
+                      double atol, double rtol, int equal_nan, int num_sms, cudaStream_t s,
+                      const unsigned long long* filter) {
+    launch_k2_cfg<DT, 512, 1, 2>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
 }
 
 cudaError_t launch_diff(const SegDev* d_segs, const DiffGroup* groups, int ngroups, const ReportMeta* d_meta,
                         int nrep, kc_diff_report* d_reps, uint64_t* d_bitmaps, double atol, double rtol,
-                        int equal_nan, int num_sms, cudaStream_t s) {
+                        int equal_nan, int num_sms, cudaStream_t s, const uint64_t* d_filter) {
+    const unsigned long long* filter = reinterpret_cast<const unsigned long long*>(d_filter);
     for (int g = 0; g < ngroups; ++g) {
         const DiffGroup& G = groups[g];
         if (G.n_units == 0 || G.n_segs == 0) continue;
         unsigned long long* bm = (unsigned long long*)d_bitmaps;
         switch (G.dtype) {
 #define KC_CASE(D) \
-    case D: launch_k2<D>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s); break;
+    case D: launch_k2<D>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter); break;
             KC_CASE(KC_DT_BYTES) KC_CASE(KC_DT_U8) KC_CASE(KC_DT_I8) KC_CASE(KC_DT_U16) KC_CASE(KC_DT_I16)
             KC_CASE(KC_DT_U32) KC_CASE(KC_DT_I32) KC_CASE(KC_DT_U64) KC_CASE(KC_DT_I64) KC_CASE(KC_DT_F16)
             KC_CASE(KC_DT_BF16) KC_CASE(KC_DT_F32) KC_CASE(KC_DT_F64)

@@ -24,8 +24,17 @@ struct SegDev {
     uint64_t bitmap_word0;   // first bitmap word of this segment's report
     uint64_t bitmap_chunk0;  // chunk index of byte 0 inside that report
     uint64_t unit_off;       // first global unit index
+    uint64_t filter_chunk0;  // filtered launches: index of the segment's first chunk in the dirty bitmap
     int32_t dtype;
     int32_t report;
+};
+
+// K5 (F2): one buffer pair whose actual bytes are hashed while compared.
+struct PairDev {
+    uint64_t act, ref, size;
+    uint64_t chunk_off;  // first chunk index (buffers in the given order)
+    int32_t dtype;
+    int32_t _pad;
 };
 
 struct ReportMeta {
@@ -50,9 +59,13 @@ cudaError_t launch_digests(const RegionDev* d_regs, int nreg, const uint64_t* d_
                            uint8_t* d_scratch /* 24*nreg */, uint64_t* d_snapshot_digest, cudaStream_t s);
 cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64_t n_chunks, uint64_t* d_bitmap,
                            uint64_t* d_count, int num_sms, cudaStream_t s);
+// d_filter (may be nullptr): dirty-chunk bitmap; units of clean chunks are skipped
 cudaError_t launch_diff(const SegDev* d_segs, const DiffGroup* groups, int ngroups, const ReportMeta* d_meta,
                         int nrep, kc_diff_report* d_reps, uint64_t* d_bitmaps, double atol, double rtol,
-                        int equal_nan, int num_sms, cudaStream_t s);
+                        int equal_nan, int num_sms, cudaStream_t s, const uint64_t* d_filter = nullptr);
+// K5: chunk hashes of every pair's act bytes + dirty bits (OR-ed into the zeroed d_dirty)
+cudaError_t launch_hash_cmp(const PairDev* d_pairs, int npair, uint64_t n_chunks, uint64_t* d_out, uint64_t* d_dirty,
+                            const uint32_t* d_chunk_pair, int num_sms, cudaStream_t s);
 cudaError_t launch_gather(const uint64_t* d_src_ptrs, const uint64_t* d_dst_ptrs, const uint64_t* d_lens, int n,
                           cudaStream_t s);
 

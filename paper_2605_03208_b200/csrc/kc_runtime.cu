@@ -318,7 +318,7 @@ void kc_destroy(kc_ctx* ctx) {
     for (uint64_t b : vm) free_alloc(ctx, b, false);
     if (ctx->heap_base) KC_DRV(cuMemAddressFree)((CUdeviceptr)ctx->heap_base, ctx->heap_size);
     if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
-    for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch,
+    for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch, &ctx->pairs, &ctx->pair_map, &ctx->dirty,
                               &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map})
         if (b->p) cudaFree(b->p);
     for (auto& w : ctx->io) {
@@ -559,10 +559,12 @@ static int elem_size(int dt) {
     return 0;
 }
 
-kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
-                        const uint64_t* report_nbytes, const uint64_t* bitmap_word0, const kc_tolerance* tol,
-                        kc_diff_report* d_reports, uint64_t* d_bitmaps, void* stream) {
-    KC_ENTER(ctx);
+// K2 planning + launch.  filter_chunk0 (host, per buffer) and d_filter (device
+// dirty bitmap) select the filtered mode that skips clean chunks (F2).
+static kc_status diff_launch(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
+                             const uint64_t* report_nbytes, const uint64_t* bitmap_word0, const kc_tolerance* tol,
+                             kc_diff_report* d_reports, uint64_t* d_bitmaps, void* stream,
+                             const uint64_t* filter_chunk0, const uint64_t* d_filter) {
     if ((n_bufs && !bufs) || (n_reports && (!d_reports || !report_nbytes)))
         return set_err(ctx, KC_ERR_ARG, "kc_diff_async: null pointer");
     if (d_bitmaps && !bitmap_word0) return set_err(ctx, KC_ERR_ARG, "kc_diff_async: bitmaps need bitmap_word0");
@@ -573,10 +575,16 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
     cudaStream_t s = (cudaStream_t)stream;
     // plan cache: identical inputs to the previous call reuse the uploaded
     // segment/meta tables (validation of the same buffer set every replay)
-    const size_t key_bytes = n_bufs * sizeof(kc_buffer) + n_reports * 8 * (bitmap_word0 ? 2 : 1) + 8;
+    const size_t key_bytes = n_bufs * sizeof(kc_buffer) + n_reports * 8 * (bitmap_word0 ? 2 : 1) + 8 +
+                             (filter_chunk0 ? n_bufs * 8 : 0) + 1;
     std::vector<uint8_t> key(key_bytes);
     {
         uint8_t* k = key.data();
+        *k++ = filter_chunk0 ? 1 : 0;
+        if (filter_chunk0 && n_bufs) {
+            memcpy(k, filter_chunk0, n_bufs * 8);
+            k += n_bufs * 8;
+        }
         if (n_bufs) memcpy(k, bufs, n_bufs * sizeof(kc_buffer));
         k += n_bufs * sizeof(kc_buffer);
         if (n_reports) memcpy(k, report_nbytes, n_reports * 8);
@@ -627,6 +635,7 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
             d.bitmap_word0 = bitmap_word0 ? bitmap_word0[b.report] : 0;
             d.bitmap_chunk0 = b.bitmap_chunk0;
             d.unit_off = U;
+            d.filter_chunk0 = filter_chunk0 ? filter_chunk0[i] : 0;
             d.dtype = b.dtype;
             d.report = b.report;
             const uint64_t nu = (b.nbytes + kDiffUnit - 1) / kDiffUnit;
@@ -663,11 +672,87 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
         KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_bitmaps, 0, bitmap_words * 8, s), "zero bitmaps");
     KC_CHECK_CUDA(ctx, launch_diff((const SegDev*)ctx->segs.p, groups.data(), (int)groups.size(),
                                    (const ReportMeta*)ctx->meta.p, (int)n_reports, d_reports, d_bitmaps, tol->atol,
-                                   tol->rtol, tol->equal_nan, ctx->num_sms, s),
+                                   tol->rtol, tol->equal_nan, ctx->num_sms, s, filter_chunk0 ? d_filter : nullptr),
                   "launch K2");
     for (auto& g : groups) ctx->launches += g.n_units ? 1 : 0;
     if (n_reports) ctx->launches += 1;
     return KC_OK;
+}
+
+kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
+                        const uint64_t* report_nbytes, const uint64_t* bitmap_word0, const kc_tolerance* tol,
+                        kc_diff_report* d_reports, uint64_t* d_bitmaps, void* stream) {
+    KC_ENTER(ctx);
+    return diff_launch(ctx, bufs, n_bufs, n_reports, report_nbytes, bitmap_word0, tol, d_reports, d_bitmaps, stream,
+                       nullptr, nullptr);
+}
+
+// ------------------------------------------------------------------ F2: K5 fused hash + compare, then filtered K2
+kc_status kc_hash_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
+                             uint64_t* d_chunk_hash, kc_diff_report* d_reports, uint64_t* d_bitmaps,
+                             uint64_t* d_dirty, void* stream) {
+    KC_ENTER(ctx);
+    if (n && (!bufs || !d_chunk_hash || !d_reports))
+        return set_err(ctx, KC_ERR_ARG, "kc_hash_diff_async: null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<kc_buffer> b(bufs, bufs + n);
+    std::vector<PairDev> t(n);
+    std::vector<uint64_t> nbytes(n), word0(n), chunk0(n);
+    uint64_t C = 0, words = 0;
+    bool aligned = true;
+    for (size_t i = 0; i < n; ++i) {
+        if (bufs[i].nbytes == 0) return set_err(ctx, KC_ERR_ARG, "kc_hash_diff_async: buffer %zu is empty", i);
+        b[i].report = (int32_t)i;
+        b[i].bitmap_chunk0 = 0;
+        nbytes[i] = bufs[i].nbytes;
+        word0[i] = words;
+        chunk0[i] = C;
+        const uint64_t nc = (bufs[i].nbytes + kChunk - 1) / kChunk;
+        words += (nc + 63) / 64;
+        t[i] = PairDev{bufs[i].act, bufs[i].ref, bufs[i].nbytes, C, bufs[i].dtype, 0};
+        C += nc;
+        if ((bufs[i].act | bufs[i].ref) & 15) aligned = false;
+    }
+    if (!aligned) {  // K5 stages 16-byte pieces: unaligned sets run K1 + an unfiltered K2
+        std::vector<kc_region> regs(n);
+        for (size_t i = 0; i < n; ++i) regs[i] = kc_region{bufs[i].act, bufs[i].nbytes, ctx->device, KC_KIND_MEMALLOC, 0};
+        kc_status st = kc_hash(ctx, regs.data(), n, d_chunk_hash, nullptr, nullptr, stream);
+        if (st != KC_OK) return st;
+        if (d_dirty && C)  // every chunk is dirty: the whole set is diffed
+            KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_dirty, 0xFF, (C + 63) / 64 * 8, s), "dirty bitmap (fallback)");
+        return diff_launch(ctx, b.data(), n, n, nbytes.data(), word0.data(), tol, d_reports, d_bitmaps, stream,
+                           nullptr, nullptr);
+    }
+    // pair table + chunk -> pair map, cached like the K1 region table
+    const bool same = t.size() == ctx->pairs_cached.size() && ctx->pairs.p &&
+                      (t.empty() || memcmp(t.data(), ctx->pairs_cached.data(), t.size() * sizeof(PairDev)) == 0);
+    if (!same) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->pairs, std::max<size_t>(1, t.size()) * sizeof(PairDev)), "cudaMalloc(pairs)");
+        if (!t.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pairs.p, t.data(), t.size() * sizeof(PairDev),
+                                               cudaMemcpyHostToDevice, s), "upload pairs");
+        std::vector<uint32_t> map(C);
+        for (size_t i = 0; i < n; ++i)
+            std::fill(map.begin() + chunk0[i], map.begin() + chunk0[i] + (bufs[i].nbytes + kChunk - 1) / kChunk,
+                      (uint32_t)i);
+        KC_CHECK_CUDA(ctx, ensure(ctx->pair_map, std::max<size_t>(1, map.size()) * 4), "cudaMalloc(pair map)");
+        if (!map.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pair_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
+                          "upload pair map");
+        ctx->pairs_cached.swap(t);
+    }
+    uint64_t* dirty = d_dirty;
+    if (!dirty) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->dirty, std::max<uint64_t>(1, (C + 63) / 64) * 8), "cudaMalloc(dirty bitmap)");
+        dirty = (uint64_t*)ctx->dirty.p;
+    }
+    if (C) KC_CHECK_CUDA(ctx, cudaMemsetAsync(dirty, 0, (C + 63) / 64 * 8, s), "zero dirty bitmap");
+    KC_CHECK_CUDA(ctx, launch_hash_cmp((const PairDev*)ctx->pairs.p, (int)n, C, d_chunk_hash, dirty,
+                                       (const uint32_t*)ctx->pair_map.p, ctx->num_sms, s),
+                  "launch K5");
+    if (C) ctx->launches += 1;
+    return diff_launch(ctx, b.data(), n, n, nbytes.data(), word0.data(), tol, d_reports, d_bitmaps, stream,
+                       chunk0.data(), dirty);
 }
 
 kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol, kc_diff_report* reps,

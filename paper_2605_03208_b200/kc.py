@@ -39,7 +39,7 @@ EXPORTED = [
     "kc_create", "kc_destroy", "kc_last_error", "kc_abi_version", "kc_build_info", "kc_status_str",
     "kc_kernel_launches", "kc_track",
     "kc_regions", "kc_alloc", "kc_free", "kc_track_install", "kc_track_uninstall", "kc_hash", "kc_count_chunks",
-    "kc_written", "kc_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
+    "kc_written", "kc_diff_async", "kc_hash_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
 ]
@@ -166,6 +166,7 @@ def lib() -> ctypes.CDLL:
         "kc_count_chunks": (U64, [P(Region), SZ]),
         "kc_written": (st, [V, V, V, U64, V, V, V]),
         "kc_diff_async": (st, [V, P(Buffer), SZ, SZ, P(U64), P(U64), P(Tolerance), V, V, V]),
+        "kc_hash_diff_async": (st, [V, P(Buffer), SZ, P(Tolerance), V, V, V, V, V]),
         "kc_diff": (st, [V, P(Buffer), SZ, P(Tolerance), P(DiffReport), P(U64), V]),
         "kc_capture": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_char_p, ctypes.c_int, P(CaptureReport)]),
         "kc_restore": (st, [V, ctypes.c_char_p, P(V), P(RestoreReport)]),
@@ -435,6 +436,15 @@ class Context:
         tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
         self._check(lib().kc_diff_async(self._h, arr, len(bufs), n_reports, rn, w0, ctypes.byref(tol), d_reports,
                                         d_bitmaps or None, stream or None), "kc_diff_async")
+
+    def hash_diff_async(self, bufs, d_chunk_hash: int, d_reports: int, d_bitmaps: int = 0, d_dirty: int = 0,
+                        atol: float = 1e-8, rtol: float = 1e-5, equal_nan: bool = False, stream: int = 0):
+        """kc_hash_diff_async (F2): K5 hashes every act buffer while comparing it with its
+        ref; K2 then diffs only the dirty chunks.  One report per buffer."""
+        arr = self._buffers(bufs)
+        tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
+        self._check(lib().kc_hash_diff_async(self._h, arr, len(bufs), ctypes.byref(tol), d_chunk_hash, d_reports,
+                                             d_bitmaps or None, d_dirty or None, stream or None), "kc_hash_diff_async")
 
     # -- closure
     def capture(self, directory: str, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
