@@ -499,6 +499,8 @@ def run_latency(a, ctx, pool, log):
         in and verifies the manifest -> kc_replay -> kc_validate.
       host_pinned: kc_capture_host (the same, D2H into a pinned host arena at PCIe
         rate) -> kc_restore_dev (H2D) -> kc_replay -> kc_validate.
+      host_pinned_incremental: kc_capture_incr against that snapshot (only chunks
+        whose hash changed cross PCIe) -> kc_restore_dev -> kc_replay -> kc_validate.
       files: kc_capture (PRE_W, pinned D2H by 8 I/O threads into /dev/shm) ->
         kc_restore from the files -> kc_replay -> kc_validate.
     Each run's restored memory serves as the live state of the next."""
@@ -533,7 +535,8 @@ def run_latency(a, ctx, pool, log):
                              "capture_hash_post": cap["t_hash_post_s"], "restore_total": t3 - t2,
                              "restore_reserve_map": rst["t_reserve_s"], "restore_copy_in": rst["t_h2d_s"],
                              "restore_verify": rst["t_verify_s"], "replay": t4 - t3, "validate": t5 - t4},
-                "copy_out_gbs": pool.bytes / max(cap["t_d2h_s"], 1e-9) / 1e9,
+                "copy_out_gbs": (cap["d2h_bytes"] or pool.bytes) / max(cap["t_d2h_s"], 1e-9) / 1e9,
+                "copy_out_bytes": cap["d2h_bytes"] or pool.bytes,
                 "copy_in_gbs": rst["h2d_bytes"] / max(rst["t_h2d_s"], 1e-9) / 1e9}
 
     # ---- device sink (F1)
@@ -569,6 +572,21 @@ def run_latency(a, ctx, pool, log):
     out["host_pinned"]["arena_bytes"] = snap.nbytes()
     out["host_pinned"]["arena_pin_s"] = pin_s
     out["host_pinned"]["pcie"] = pcie_peak(log)
+
+    # ---- F2 incremental capture against that snapshot: only chunks whose hash changed are copied
+    synth.dev_view(pool.va["y"], ys.size).zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    snap_i, cap = ctx.capture_host(base=snap, **disp)
+    t1 = time.perf_counter()
+    r_host.release()
+    t2 = time.perf_counter()
+    r_host, rst = ctx.restore_dev(snap_i)
+    t3 = time.perf_counter()
+    out["host_pinned_incremental"] = finish("host_pinned_incremental", cap, rst, r_host, (t0, t1, t2, t3))
+    out["host_pinned_incremental"]["copied_bytes"] = snap_i.nbytes()
+    out["host_pinned_incremental"]["shared_bytes"] = snap_i.shared_bytes()
+    snap_i.free()
     snap.free()
     ctx.host_arena_reserve(0)
 
@@ -590,7 +608,8 @@ def run_latency(a, ctx, pool, log):
     shutil.rmtree(d, ignore_errors=True)
     out["bytes"] = pool.bytes
     out["latency_s"] = out["device"]["latency_s"]
-    out["validated_bit_exact"] = all(out[k]["validated_bit_exact"] for k in ("device", "host_pinned", "files"))
+    out["validated_bit_exact"] = all(out[k]["validated_bit_exact"]
+                                     for k in ("device", "host_pinned", "host_pinned_incremental", "files"))
     return out
 
 

@@ -312,6 +312,16 @@ kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* reg
  * snapshot), else allocated (pinning costs ~0.2-0.3 s per 10 GB). */
 kc_status kc_capture_host(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
                           kc_snapshot** out, kc_capture_report* rep);
+/* F2 incremental capture: the capture of kc_capture_dev
+ * (host = 0) / kc_capture_host (host != 0) that copies only the chunks whose
+ * stored-state hash (pre-dispatch in PRE_W, post in POST) differs from
+ * `base`'s stored manifest at the same region base, size and chunk index;
+ * every other chunk references the base's bytes (hash equality is the same
+ * "unchanged" test the written set W uses).  The new snapshot shares
+ * ownership of the base's arenas: the base may be freed first.  base = NULL
+ * is a full capture.  rep->d2h_bytes = bytes actually copied. */
+kc_status kc_capture_incr(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
+                          const kc_snapshot* base, int host, kc_snapshot** out, kc_capture_report* rep);
 /* Pin `bytes` of host memory ahead of time and park it in the ctx's cache (one
  * arena; a larger request replaces a smaller parked one).  0 frees the cache. */
 kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes);
@@ -321,8 +331,10 @@ kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes);
 kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep);
 /* Persist an in-memory snapshot as a kc-snapshot/1 directory (parallel). */
 kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
-/* Bytes held in the snapshot's arenas. */
+/* Bytes this snapshot copied into its own arenas. */
 uint64_t kc_snapshot_bytes(const kc_snapshot* s);
+/* Stored bytes referenced from base snapshots (kc_capture_incr), not copied. */
+uint64_t kc_snapshot_shared_bytes(const kc_snapshot* s);
 /* 1 = pinned host arena (kc_capture_host), 0 = device arena. */
 int kc_snapshot_is_host(const kc_snapshot* s);
 /* Frees the arenas; a host arena is parked in the ctx's cache instead when it

@@ -19,6 +19,8 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <map>
+#include <memory>
 #include <thread>
 #include <cstdio>
 #include <cstdlib>
@@ -1304,15 +1306,49 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
 // kc_capture with the region bytes kept in an HBM arena: D2D copies at HBM
 // bandwidth replace PCIe + files.  Big regions go through
 // cudaMemcpyAsync, regions and W chunks under 1 MiB through the K4 gather.
+//
+// F2 incremental capture (kc_capture_incr): a chunk whose stored-state hash
+// equals the base snapshot's at the same region and chunk index is not copied;
+// the new snapshot references the base's bytes (shared ownership of the base
+// arenas, so a base may be freed first).  Hash equality as "unchanged" is the
+// method's own reading: W (A4) declares a chunk unwritten on the same test.
+
+// One arena allocation, freed (or, pinned host, parked in the ctx cache) when
+// the last snapshot referencing it goes.
+struct ArenaBuf {
+    kc_ctx* ctx = nullptr;
+    void* p = nullptr;
+    uint64_t cap = 0;
+    bool host = false;
+    ~ArenaBuf() {
+        if (!p) return;
+        if (ctx) bind_device(ctx);
+        if (!host) {
+            cudaFree(p);
+        } else if (ctx && cap >= ctx->host_arena_bytes) {  // park the larger arena
+            if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+            ctx->host_arena = p;
+            ctx->host_arena_bytes = cap;
+        } else {
+            cudaFreeHost(p);
+        }
+    }
+};
+
 struct kc_snapshot {
     kc_ctx* ctx = nullptr;
-    bool host = false;      // arenas in pinned host memory (kc_capture_host)
+    bool host = false;  // arenas in pinned host memory (kc_capture_host)
     SnapDesc desc;
-    void* arena = nullptr;  // stored bytes, region i at off[i] (256 B aligned)
-    uint64_t arena_bytes = 0;
-    uint64_t arena_cap = 0;  // allocated bytes (>= arena_bytes when a parked host arena was reused)
-    std::vector<uint64_t> off;
-    void* warena = nullptr;  // PRE_W: post bytes of W, region i at w_off[i]
+    std::shared_ptr<ArenaBuf> arena;                // this snapshot's own stored bytes
+    uint64_t arena_bytes = 0;                       // bytes used in it
+    std::vector<std::shared_ptr<ArenaBuf>> deps;    // base arenas referenced by runs
+    struct Run {
+        uint64_t roff, len;  // region byte range (chunk aligned)
+        uint64_t src;        // where its stored bytes are (own arena or a base's)
+    };
+    std::vector<std::vector<Run>> runs;  // per region, ascending roff, covering ok regions
+    uint64_t shared_bytes = 0;           // stored bytes referenced from base snapshots
+    void* warena = nullptr;              // PRE_W: post bytes of W, region i at w_off[i]
     uint64_t w_bytes = 0;
     std::vector<uint64_t> w_off;
     kc_capture_report rep;
@@ -1362,7 +1398,7 @@ struct DevSource : RestoreSource {
         std::vector<std::array<uint64_t, 3>> ranges;
         for (size_t i = 0; i < d.regions.size(); ++i) {
             if (!d.regions[i].ok) continue;
-            ranges.push_back({(uint64_t)sn->arena + sn->off[i], d.regions[i].r.base, d.regions[i].r.size});
+            for (const auto& ru : sn->runs[i]) ranges.push_back({ru.src, d.regions[i].r.base + ru.roff, ru.len});
             rep.h2d_bytes += d.regions[i].r.size;  // bytes copied in (D2D or H2D)
         }
         return copy_ranges_d2d(ctx, ranges, ctx->copy_stream, nullptr);
@@ -1393,17 +1429,24 @@ cudaError_t arena_alloc(kc_ctx* ctx, bool host, void** p, uint64_t bytes, uint64
 }
 
 kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
-                      kc_snapshot** out, kc_capture_report* rep_out, bool host);
+                      kc_snapshot** out, kc_capture_report* rep_out, bool host, const kc_snapshot* base);
 }  // namespace
 
 extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                     kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
-    return capture_mem(ctx, d, regions, n, mode, out, rep_out, false);
+    return capture_mem(ctx, d, regions, n, mode, out, rep_out, false, nullptr);
 }
 
 extern "C" kc_status kc_capture_host(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                      kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
-    return capture_mem(ctx, d, regions, n, mode, out, rep_out, true);
+    return capture_mem(ctx, d, regions, n, mode, out, rep_out, true, nullptr);
+}
+
+extern "C" kc_status kc_capture_incr(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
+                                     kc_capture_mode mode, const kc_snapshot* base, int host, kc_snapshot** out,
+                                     kc_capture_report* rep_out) {
+    if (base && base->ctx != ctx) return set_err(ctx, KC_ERR_ARG, "kc_capture_incr: base snapshot of another ctx");
+    return capture_mem(ctx, d, regions, n, mode, out, rep_out, host != 0, base);
 }
 
 extern "C" kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
@@ -1429,7 +1472,7 @@ extern "C" kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
 
 namespace {
 kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
-                      kc_snapshot** out, kc_capture_report* rep_out, bool host) {
+                      kc_snapshot** out, kc_capture_report* rep_out, bool host, const kc_snapshot* base) {
     if (!ctx) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -1521,36 +1564,96 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     rep.n_chunks = pre_h.size();
     for (auto& r : live) rep.total_bytes += r.size;
 
-    // ---- the arena
-    uint64_t total = 0;
-    for (auto& sr : D.regions) {
-        sn->off.push_back(total);
-        if (sr.ok) total += (sr.r.size + 255) / 256 * 256;
+    // ---- the stored bytes: runs per region; chunks whose stored-state hash equals
+    // the base's at the same (region, chunk) reference the base, the rest are
+    // copied into this snapshot's own arena (256 B aligned runs)
+    double t_copy = 0;
+    std::map<uint64_t, size_t> base_idx;
+    if (base)
+        for (size_t j = 0; j < base->desc.regions.size(); ++j)
+            if (base->desc.regions[j].ok) base_idx[base->desc.regions[j].r.base] = j;
+    if (base) {
+        sn->deps = base->deps;
+        if (base->arena) sn->deps.push_back(base->arena);
     }
-    sn->arena_bytes = total;
-    if (total && arena_alloc(ctx, host, &sn->arena, total, &sn->arena_cap) != cudaSuccess) {
-        cudaGetLastError();
-        sn->arena = nullptr;
-        return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_%s: cannot allocate a %llu-byte arena", host ? "host" : "dev",
-                            (unsigned long long)total));
-    }
-    auto snapshot_regions = [&]() -> kc_status {
+    auto snapshot_regions = [&](const std::vector<uint64_t>& h /* stored-state manifest, live-region order */)
+        -> kc_status {
+        struct OwnRun { size_t i, r; uint64_t aoff; };
+        std::vector<OwnRun> own;
+        sn->runs.assign(D.regions.size(), {});
+        uint64_t total = 0;
+        for (size_t i = 0; i < D.regions.size(); ++i) {
+            const SnapRegion& sr = D.regions[i];
+            if (!sr.ok) continue;
+            const SnapRegion* bsr = nullptr;
+            const std::vector<kc_snapshot::Run>* bruns = nullptr;
+            if (base) {
+                auto it = base_idx.find(sr.r.base);
+                if (it != base_idx.end() && base->desc.regions[it->second].r.size == sr.r.size) {
+                    bsr = &base->desc.regions[it->second];
+                    bruns = &base->runs[it->second];
+                }
+            }
+            size_t bj = 0;
+            auto& runs = sn->runs[i];
+            for (uint64_t kc = 0; kc < sr.n_chunks; ++kc) {
+                const uint64_t roff = kc * kChunk, len = std::min<uint64_t>(kChunk, sr.r.size - roff);
+                uint64_t bsrc = 0;
+                if (bsr && bsr->manifest[kc] == h[pre_off[i] + kc]) {
+                    while ((*bruns)[bj].roff + (*bruns)[bj].len <= roff) ++bj;
+                    bsrc = (*bruns)[bj].src + (roff - (*bruns)[bj].roff);
+                    sn->shared_bytes += len;
+                }
+                if (bsrc) {
+                    if (!runs.empty() && runs.back().roff + runs.back().len == roff &&
+                        runs.back().src + runs.back().len == bsrc &&
+                        (own.empty() || own.back().i != i || own.back().r != runs.size() - 1))
+                        runs.back().len += len;
+                    else
+                        runs.push_back({roff, len, bsrc});
+                } else {
+                    if (!own.empty() && own.back().i == i && own.back().r == runs.size() - 1 &&
+                        runs.back().roff + runs.back().len == roff) {
+                        runs.back().len += len;
+                    } else {
+                        total = (total + 255) / 256 * 256;
+                        own.push_back({i, runs.size(), total});
+                        runs.push_back({roff, len, 0});
+                    }
+                    total += len;
+                }
+            }
+        }
+        sn->arena_bytes = total;
+        if (total) {
+            auto ab = std::make_shared<ArenaBuf>();
+            ab->ctx = ctx;
+            ab->host = host;
+            if (arena_alloc(ctx, host, &ab->p, total, &ab->cap) != cudaSuccess) {
+                cudaGetLastError();
+                ab->p = nullptr;
+                return set_err(ctx, KC_ERR_NOMEM, "kc_capture_%s: cannot allocate a %llu-byte arena",
+                               host ? "host" : "dev", (unsigned long long)total);
+            }
+            sn->arena = ab;
+        }
         std::vector<std::array<uint64_t, 3>> ranges;
-        for (size_t i = 0; i < D.regions.size(); ++i)
-            if (D.regions[i].ok) ranges.push_back({D.regions[i].r.base, (uint64_t)sn->arena + sn->off[i],
-                                                   D.regions[i].r.size});
+        for (const OwnRun& o : own) {
+            kc_snapshot::Run& ru = sn->runs[o.i][o.r];
+            ru.src = (uint64_t)sn->arena->p + o.aoff;
+            ranges.push_back({D.regions[o.i].r.base + ru.roff, ru.src, ru.len});
+        }
+        const double tc = now_s();  // t_d2h_s: the copies only (planning and allocation excluded)
         kc_status s2 = copy_ranges_d2d(ctx, ranges, ctx->copy_stream ? ctx->copy_stream : cs, &rep.dma_calls);
         cudaStreamSynchronize(ctx->copy_stream);
+        t_copy += now_s() - tc;
         return s2;
     };
     st = ensure_pinned(ctx);  // creates the copy stream
     if (st != KC_OK) return fail(st);
-    double t_copy = 0;
     if (mode == KC_MODE_PRE_W) {
-        t = now_s();
-        st = snapshot_regions();
+        st = snapshot_regions(pre_h);
         if (st != KC_OK) return fail(st);
-        t_copy += now_s() - t;
     }
     // ---- forward the dispatch
     t = now_s();
@@ -1602,9 +1705,8 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         }
     }
     D.snapshot_digest = mode == KC_MODE_PRE_W ? pre_snap : post_snap;
-    t = now_s();
     if (mode == KC_MODE_POST) {
-        st = snapshot_regions();
+        st = snapshot_regions(post_h);
         if (st != KC_OK) return fail(st);
     } else if (rep.written_chunks) {
         uint64_t wtot = 0;
@@ -1628,14 +1730,15 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
                 o += len;
             }
         }
+        t = now_s();
         st = copy_ranges_d2d(ctx, ranges, ctx->copy_stream, &rep.dma_calls);
         cudaStreamSynchronize(ctx->copy_stream);
+        t_copy += now_s() - t;
         if (st != KC_OK) return fail(st);
     }
     if (sn->w_off.empty()) sn->w_off.assign(D.regions.size(), 0);
-    t_copy += now_s() - t;
     rep.t_d2h_s = t_copy;  // device-to-device for a device arena
-    if (host) rep.d2h_bytes = sn->arena_bytes + sn->w_bytes;
+    rep.d2h_bytes = sn->arena_bytes + sn->w_bytes;  // bytes moved into the arenas (D2H or D2D)
     for (auto& sr : D.regions)
         if (!sr.ok) rep.n_failed_regions++;
     rep.snapshot_digest = D.snapshot_digest;
@@ -1693,7 +1796,9 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
     const int T = io_threads();
     kc_status st = ensure_io(ctx, T);
     if (st != KC_OK) return st;
-    std::vector<std::pair<size_t, uint64_t>> todo;
+    // work items: 256 MiB pieces of every run, with the address its file offset maps to
+    std::vector<IoItem> items;
+    std::vector<uint64_t> item_base;
     for (size_t i = 0; i < D.regions.size(); ++i) {
         if (!D.regions[i].ok) continue;
         const std::string path = dir + "/memory/region_" + D.regions[i].hx + ".bin";
@@ -1701,9 +1806,12 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
         const bool ok = fd >= 0 && ftruncate(fd, (off_t)D.regions[i].r.size) == 0;
         if (fd >= 0) close(fd);
         if (!ok) return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot create %s", path.c_str());
-        todo.emplace_back(i, D.regions[i].r.size);
+        for (const auto& ru : s->runs[i])
+            for (uint64_t o = 0; o < ru.len; o += 256ull << 20) {
+                items.push_back({i, ru.roff + o, std::min<uint64_t>(256ull << 20, ru.len - o)});
+                item_base.push_back(ru.src - ru.roff);  // base + file offset = source address
+            }
     }
-    const std::vector<IoItem> items = make_items(todo);
     std::atomic<int> bad{0};
     std::atomic<uint64_t> calls{0};
     run_pool(T, items.size(), [&](int t, size_t k) {
@@ -1714,7 +1822,7 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
         int fd = open(path.c_str(), O_WRONLY);
         std::string err;
         // item_d2h copies [base + off, +len) -> file offset off: base = this region's arena slot
-        const bool ok = fd >= 0 && item_d2h(ctx, ctx->io[t], (uint64_t)s->arena + s->off[it.region], it, fd, calls, err);
+        const bool ok = fd >= 0 && item_d2h(ctx, ctx->io[t], item_base[k], it, fd, calls, err);
         if (fd >= 0) close(fd);
         if (!ok) bad = 1;
     });
@@ -1748,26 +1856,17 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
 
 extern "C" uint64_t kc_snapshot_bytes(const kc_snapshot* s) { return s ? s->arena_bytes + s->w_bytes : 0; }
 
+extern "C" uint64_t kc_snapshot_shared_bytes(const kc_snapshot* s) { return s ? s->shared_bytes : 0; }
+
 extern "C" int kc_snapshot_is_host(const kc_snapshot* s) { return s && s->host ? 1 : 0; }
 
 extern "C" void kc_snapshot_free(kc_snapshot* s) {
     if (!s) return;
     if (s->ctx) bind_device(s->ctx);
-    if (s->host) {
-        kc_ctx* ctx = s->ctx;
-        if (s->arena && ctx && s->arena_cap >= ctx->host_arena_bytes) {  // park the larger arena
-            if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
-            ctx->host_arena = s->arena;
-            ctx->host_arena_bytes = s->arena_cap;
-        } else if (s->arena) {
-            cudaFreeHost(s->arena);
-        }
-        if (s->warena) cudaFreeHost(s->warena);
-    } else {
-        if (s->arena) cudaFree(s->arena);
-        if (s->warena) cudaFree(s->warena);
+    if (s->warena) {
+        if (s->host) cudaFreeHost(s->warena); else cudaFree(s->warena);
     }
-    delete s;
+    delete s;  // the arenas go with their last reference (ArenaBuf)
 }
 
 extern "C" kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out) {
@@ -1939,8 +2038,12 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
             if (h->dev_snap) {  // device snapshot: stored bytes from the arena, W's post bytes from the W arena
                 const kc_snapshot* sn = h->dev_snap;
                 const size_t ri = (size_t)(owner - h->regions.data());
-                cudaMemcpy((uint8_t*)typed_ref + off, (const uint8_t*)sn->arena + sn->off[ri] + roff, o.nbytes,
-                           cudaMemcpyDefault);
+                for (const auto& ru : sn->runs[ri]) {  // stored bytes of [roff, roff + nbytes)
+                    const uint64_t lo = std::max(ru.roff, roff), hi = std::min(ru.roff + ru.len, roff + o.nbytes);
+                    if (lo < hi)
+                        cudaMemcpy((uint8_t*)typed_ref + off + (lo - roff), (const uint8_t*)(ru.src + (lo - ru.roff)),
+                                   hi - lo, cudaMemcpyDefault);
+                }
                 if (h->mode == KC_MODE_PRE_W) {
                     uint64_t woff = sn->w_off[ri];
                     for (uint64_t k : owner->written) {

@@ -42,6 +42,7 @@ EXPORTED = [
     "kc_written", "kc_diff_async", "kc_hash_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
+    "kc_capture_incr", "kc_snapshot_shared_bytes",
 ]
 
 
@@ -183,6 +184,9 @@ def lib() -> ctypes.CDLL:
         "kc_capture_host": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
         "kc_host_arena_reserve": (st, [V, U64]),
         "kc_snapshot_is_host": (ctypes.c_int, [V]),
+        "kc_capture_incr": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, V, ctypes.c_int, P(V),
+                                 P(CaptureReport)]),
+        "kc_snapshot_shared_bytes": (U64, [V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -305,6 +309,10 @@ class DevSnapshot:
 
     def is_host(self) -> bool:
         return bool(lib().kc_snapshot_is_host(self.handle))
+
+    def shared_bytes(self) -> int:
+        """Stored bytes referenced from base snapshots (incremental capture)."""
+        return int(lib().kc_snapshot_shared_bytes(self.handle))
 
     def save(self, directory: str) -> None:
         self.ctx._check(lib().kc_snapshot_save(self.ctx.handle, self.handle, directory.encode()), "kc_snapshot_save")
@@ -474,16 +482,24 @@ class Context:
 
     def capture_dev(self, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
                     block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
-                    stream: int = 0, host: bool = False) -> tuple[DevSnapshot, dict]:
-        """kc_capture into a device arena (F1), or a pinned host arena (host=True: kc_capture_host)."""
+                    stream: int = 0, host: bool = False, base: "DevSnapshot | None" = None
+                    ) -> tuple[DevSnapshot, dict]:
+        """kc_capture into a device arena (F1), or a pinned host arena (host=True:
+        kc_capture_host); with base=, only chunks changed against it are copied
+        (kc_capture_incr)."""
         d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream)
         rep = CaptureReport()
         h = ctypes.c_void_p()
         arr = _regions(regions) if regions is not None else None
-        fn = lib().kc_capture_host if host else lib().kc_capture_dev
-        rc = fn(self._h, ctypes.byref(d), arr, len(regions) if regions is not None else 0, mode,
-                ctypes.byref(h), ctypes.byref(rep))
-        self._check(rc, "kc_capture_host" if host else "kc_capture_dev", ok=(KC_OK, KC_PARTIAL))
+        nreg = len(regions) if regions is not None else 0
+        if base is not None:
+            name = "kc_capture_incr"
+            rc = lib().kc_capture_incr(self._h, ctypes.byref(d), arr, nreg, mode, base.handle, int(host),
+                                       ctypes.byref(h), ctypes.byref(rep))
+        else:
+            name = "kc_capture_host" if host else "kc_capture_dev"
+            rc = getattr(lib(), name)(self._h, ctypes.byref(d), arr, nreg, mode, ctypes.byref(h), ctypes.byref(rep))
+        self._check(rc, name, ok=(KC_OK, KC_PARTIAL))
         return DevSnapshot(h.value, self), rep.as_dict()
 
     def capture_host(self, **kw) -> tuple[DevSnapshot, dict]:

@@ -251,6 +251,41 @@ def devsnap(a):
     print(json.dumps(out))
 
 
+def incr(a):
+    """F2 incremental capture: a full capture, then one against it (only the
+    chunks the first dispatch wrote are copied), the base freed, the second
+    persisted for the oracle and restored/replayed/validated."""
+    ctx = kc.Context(0)
+    sizes = [s.size for s in synth.C1_SPECS]
+    vas = [ctx.alloc(sz) for sz in sizes]
+    nodes_va, heads_va, out_va = vas
+    for va, arr in zip(vas, synth.c1_fill(nodes_va)):
+        _upload(va, arr)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    disp = dict(image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
+                kernarg=synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=0), mode=kc.KC_MODE_PRE_W, host=a.host)
+    snap0, rep0 = ctx.capture_dev(**disp)
+    orig_out = _download(out_va, sizes[2])
+    # the second dispatch also mutates the nodes (its W is the 10 node chunks)
+    disp["kernarg"] = synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=1)
+    snap1, rep1 = ctx.capture_dev(base=snap0, **disp)
+    out = {"rep0": rep0, "rep1": rep1, "bytes0": snap0.nbytes(), "bytes1": snap1.nbytes(),
+           "shared1": snap1.shared_bytes(), "sizes": sizes, "vas": vas}
+    snap0.free()  # snap1 keeps the base bytes it references
+    snap1.save(a.dir)
+    for va in vas:
+        ctx.free(va)
+    r, rrep = ctx.restore_dev(snap1)
+    out["restore"] = rrep
+    out["replay"] = ctx.replay(r)
+    out["out_equal"] = bool(np.array_equal(_download(out_va, sizes[2]), orig_out))
+    out["validate"], out["unexpected_chunks"] = ctx.validate(r)
+    out["typed"], _ = ctx.validate(r, outs=[(nodes_va, sizes[0], "u32")])
+    r.release()
+    snap1.free()
+    print(json.dumps(out))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -271,7 +306,7 @@ def main():
     p.add_argument("--cycles", type=int, default=1)
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
-     "inproc": inproc, "devsnap": devsnap}[a.cmd](a)
+     "inproc": inproc, "devsnap": devsnap, "incr": incr}[a.cmd](a)
 
 
 if __name__ == "__main__":

@@ -276,3 +276,28 @@ def test_device_snapshot_capture_restore_replay(tmp_path, mode, mutate, host):
     pred, (heads_va, out_va, nodes_va) = _walker_prediction(d, mutate)
     if mode == "pre_w":   # the PRE_W snapshot holds the inputs: the oracle's walk reproduces the output
         assert np.array_equal(np.load(str(tmp_path / "dev_orig_out.npy")), pred[out_va])
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_incremental_capture_shares_unchanged_chunks(tmp_path, host):
+    """F2 incremental capture: against a full base, only the chunks whose
+    stored-state hash changed are copied (here the 5 chunks of `out` the first
+    dispatch wrote, plus the second capture's own W); the rest reference the base, which is freed before the
+    incremental snapshot is persisted (oracle O1 checks every stored byte
+    against its manifest) and restored at the same VAs."""
+    d = str(tmp_path / "incr")
+    os.makedirs(d, exist_ok=True)
+    res = run("incr", d, *(["--host"] if host else []))
+    nodes, heads, out = res["sizes"]
+    # first capture: every region + W = the 5 out chunks; second: only out (changed by the
+    # first dispatch) + its own W = the 10 node chunks the mutating dispatch rewrites
+    assert res["rep0"]["written_chunks"] == 5 and res["bytes0"] == nodes + heads + out + out
+    assert res["shared1"] == nodes + heads          # unchanged chunks are referenced, not copied
+    assert res["rep1"]["written_chunks"] == 10
+    assert res["bytes1"] == out + nodes and res["rep1"]["d2h_bytes"] == out + nodes
+    from oracle import snapshot
+    summ = snapshot.verify(snapshot.load(d))
+    assert summ["ok"] == 3
+    assert res["restore"]["verify_mismatch_chunks"] == 0 and res["out_equal"]
+    assert all(r["differing_bytes"] == 0 for r in res["validate"]) and res["unexpected_chunks"] == 0
+    assert res["typed"][0]["pass"] == 1
