@@ -37,6 +37,21 @@ double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// KC_TRACE=1: stage times of the in-memory capture on stderr (diagnostics only)
+bool trace_on() {
+    static const bool on = [] {
+        const char* e = getenv("KC_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+void trace(const char* what, double& tl) {
+    if (!trace_on()) return;
+    const double t = now_s();
+    fprintf(stderr, "[kc] %-28s %9.3f ms\n", what, 1e3 * (t - tl));
+    tl = t;
+}
+
 bool mkdir_p(const std::string& path) {
     std::string cur;
     for (size_t i = 0; i < path.size(); ++i) {
@@ -1482,6 +1497,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     kc_capture_report rep;
     memset(&rep, 0, sizeof rep);
     const double t0 = now_s();
+    double tl = t0;
     cudaStream_t cs = (cudaStream_t)d->stream;
     std::vector<kc_region> list;
     if (regions) {
@@ -1542,6 +1558,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     // ---- A3 bracket: quiesce, liveness, K1 pre-manifest
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return fail(cuda_err(ctx, e, "kc_capture_dev: quiesce"));
+    trace("setup + quiesce", tl);
     std::vector<kc_region> live;
     std::vector<uint64_t> pre_off;  // manifest offset per region (ok regions)
     for (auto& r : list) {
@@ -1561,6 +1578,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     kc_status st = hash_regions_sync(ctx, live, pre_h, &pre_dig, &pre_snap, nullptr, cs);
     if (st != KC_OK) return fail(st);
     rep.t_hash_pre_s = now_s() - t;
+    trace("regions + K1 pre", tl);
     rep.n_chunks = pre_h.size();
     for (auto& r : live) rep.total_bytes += r.size;
 
@@ -1625,6 +1643,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
             }
         }
         sn->arena_bytes = total;
+        trace("plan runs", tl);
         if (total) {
             auto ab = std::make_shared<ArenaBuf>();
             ab->ctx = ctx;
@@ -1637,6 +1656,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
             }
             sn->arena = ab;
         }
+        trace("arena alloc", tl);
         std::vector<std::array<uint64_t, 3>> ranges;
         for (const OwnRun& o : own) {
             kc_snapshot::Run& ru = sn->runs[o.i][o.r];
@@ -1647,6 +1667,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         kc_status s2 = copy_ranges_d2d(ctx, ranges, ctx->copy_stream ? ctx->copy_stream : cs, &rep.dma_calls);
         cudaStreamSynchronize(ctx->copy_stream);
         t_copy += now_s() - tc;
+        trace("copy", tl);
         return s2;
     };
     st = ensure_pinned(ctx);  // creates the copy stream
@@ -1673,6 +1694,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         if (r != CUDA_SUCCESS) return fail(cu_err(ctx, r, "kc_capture_dev: target dispatch"));
     }
     rep.t_dispatch_s = now_s() - t;
+    trace("dispatch", tl);
     if (own_mod) {
         KC_DRV(cuModuleUnload)(own_mod);
         own_mod = nullptr;
@@ -1682,6 +1704,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     st = hash_regions_sync(ctx, live, post_h, &post_dig, &post_snap, nullptr, cs);
     if (st != KC_OK) return fail(st);
     rep.t_hash_post_s = now_s() - t;
+    trace("K1 post", tl);
     {
         size_t j = 0;
         for (size_t i = 0; i < D.regions.size(); ++i) {
@@ -1742,6 +1765,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     for (auto& sr : D.regions)
         if (!sr.ok) rep.n_failed_regions++;
     rep.snapshot_digest = D.snapshot_digest;
+    trace("W + finish", tl);
     rep.t_total_s = now_s() - t0;
     sn->rep = rep;
     if (rep_out) *rep_out = rep;
