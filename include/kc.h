@@ -170,7 +170,7 @@ typedef struct {
 
 typedef struct {
     uint32_t iterations;
-    uint32_t _pad;
+    uint32_t module_vars_restored; /* F3: module variables written into the replay module */
     double kernel_ms_mean, kernel_ms_min, kernel_ms_max;
 } kc_replay_report;
 
@@ -343,6 +343,22 @@ void kc_snapshot_free(kc_snapshot* s);
 
 /* ---- A7 replay ------------------------------------ */
 kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts* o, kc_replay_report* rep);
+
+/* ---- F3 module variables -----------------------------
+ * kc_capture / kc_capture_dev / kc_capture_host record every __device__ /
+ * __constant__ variable of the dispatch's code object (ELF .nv.global* /
+ * .nv.constant* symbols other than the kernel parameter banks, resolved with
+ * cuModuleGetGlobal in the dispatch's module) before and after the dispatch
+ * (module_vars.json + module_vars/NNN.{pre,post}.bin).  The code object is
+ * d->image, else (d->func only) the image the CUPTI hook recorded when the
+ * application loaded the module (kc_track_install: cuModuleLoadData,
+ * cuModuleLoadDataEx, cuModuleLoadFatBinary) - PAPER.md:506-516.  kc_replay
+ * writes them into the replay module (pre values in PRE_W, post in POST)
+ * before the launch (and before each iteration when written and recopying),
+ * then compares every variable with its captured post value; this call reads
+ * that comparison of the LAST kc_replay.  KC_NO_MODULE_VARS=1 disables both
+ * sides (ablation). */
+kc_status kc_validate_module_vars(kc_ctx* ctx, const kc_restored* h, uint64_t* n_checked, uint64_t* n_mismatch);
 
 /* ---- A8 validate ---------------------------------- */
 /* outs == NULL: every region with written chunks, compared as bytes against

@@ -77,6 +77,38 @@ def load(d: str) -> Snapshot:
     return Snapshot(d, disp, regs, log)
 
 
+def cubin_module_vars(path: str) -> dict:
+    """{name: size} of the user module variables of a CUDA ELF64 code object:
+    STT_OBJECT symbols with a size, defined in a .nv.global* or .nv.constant*
+    section other than the kernel parameter banks .nv.constant0.* (F3,
+    PAPER.md:728-751).  Plain struct parsing of the ELF64 layout."""
+    import struct
+    b = open(path, "rb").read()
+    assert b[:4] == b"\x7fELF" and b[4] == 2, "not an ELF64 code object"
+    shoff, = struct.unpack_from("<Q", b, 0x28)
+    shentsize, shnum, shstrndx = struct.unpack_from("<HHH", b, 0x3A)
+    secs = [struct.unpack_from("<IIQQQQIIQQ", b, shoff + i * shentsize) for i in range(shnum)]
+    # (name, type, flags, addr, offset, size, link, info, addralign, entsize)
+
+    def cstr(off):
+        return b[off:b.index(b"\0", off)].decode()
+    shstr = secs[shstrndx]
+    names = [cstr(shstr[4] + s[0]) for s in secs]
+    out = {}
+    for s in secs:
+        if s[1] != 2:  # SHT_SYMTAB
+            continue
+        strtab = secs[s[6]]
+        for o in range(0, s[5], s[9]):
+            st_name, st_info, _, st_shndx, _, st_size = struct.unpack_from("<IBBHQQ", b, s[4] + o)
+            if st_info & 0xF != 1 or st_size == 0 or st_shndx == 0 or st_shndx >= shnum:
+                continue
+            sec = names[st_shndx]
+            if sec.startswith(".nv.global") or (sec.startswith(".nv.constant") and not sec.startswith(".nv.constant0")):
+                out[cstr(strtab[4] + st_name)] = st_size
+    return out
+
+
 def verify(snap: Snapshot) -> dict:
     """Recompute and check everything the format promises; returns a summary.
 
@@ -125,4 +157,20 @@ def verify(snap: Snapshot) -> dict:
     S = snapshot_digest(ok_bases, ok_sizes, ok_digs)
     logged = int(snap.log["snapshot_digest"], 16)
     assert S == logged, "snapshot digest mismatch"
-    return {"regions": len(snap.regions), "ok": len(ok_bases), "written_chunks": n_written, "snapshot_digest": S}
+    # F3 module variables: every recorded variable is one the code object declares, with
+    # its declared size, and both value files hold exactly that many bytes
+    n_mv = 0
+    mvp = os.path.join(d, "module_vars.json")
+    if os.path.exists(mvp):
+        mv = json.load(open(mvp))
+        assert mv["format"] == "kc-module-vars/1"
+        declared = cubin_module_vars(cub)
+        for v in mv["vars"]:
+            assert declared.get(v["name"]) == v["size"], f"module variable {v['name']}: not declared with that size"
+            pre = open(os.path.join(d, v["pre"]), "rb").read()
+            post = open(os.path.join(d, v["post"]), "rb").read()
+            assert len(pre) == len(post) == v["size"]
+            assert v["written"] == (pre != post)
+            n_mv += 1
+    return {"regions": len(snap.regions), "ok": len(ok_bases), "written_chunks": n_written, "snapshot_digest": S,
+            "module_vars": n_mv}

@@ -23,7 +23,7 @@ FIXTURE_CUBIN = os.path.join(ROOT, "synth", "kc_fixtures.cubin")
 # (different optimisation level) and a modified kernel (KC_VARIANT_DELTA=1)
 FIXTURE_VARIANTS = {os.path.join(ROOT, "synth", "kc_fixtures_recompiled.cubin"): ["-O1"],
                     os.path.join(ROOT, "synth", "kc_fixtures_modified.cubin"): ["-O3", "-DKC_VARIANT_DELTA=1"]}
-SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu"]
+SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu", "kc_module.cu"]
 HEADERS = ["kc_kernels.cuh", "kc_internal.h", "kc_json.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")

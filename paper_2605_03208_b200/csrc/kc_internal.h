@@ -15,7 +15,7 @@
 // Driver-API entry points resolved through cudart (cudaGetDriverEntryPoint),
 // so libkc.so has no link-time dependency on libcuda and loads on hosts
 // without a GPU driver (calls then fail with KC_ERR_CUDA).
-#define KC_DRV_FUNCS(X) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemFree) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
+#define KC_DRV_FUNCS(X) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemFree) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
 namespace kc {
 struct Drv {
 #define KC_DRV_DECL(f) decltype(&::f) f = nullptr;
@@ -26,6 +26,21 @@ struct Drv {
 const Drv& drv();
 }  // namespace kc
 #define KC_DRV(f) (::kc::drv().f)
+
+// F3 module variables (kc_module.cu): declared in the code object, valued per capture
+namespace kc {
+struct ModVarDecl {
+    std::string name, section;
+    uint64_t size;
+};
+size_t image_size(const void* img, size_t hint);  // ELF64 / fatbin extent (hint wins when nonzero)
+std::vector<ModVarDecl> image_module_vars(const uint8_t* img, size_t n);
+}  // namespace kc
+struct ModVarState {
+    std::string name, section;
+    uint64_t size = 0;
+    std::vector<uint8_t> pre, post;  // bytes before / after the captured dispatch
+};
 
 struct kc_ctx_dev_buf {
     void* p = nullptr;
@@ -84,6 +99,8 @@ struct kc_ctx {
     // driver): freed ranges stay ours, so a same-process restore maps back at
     // the exact VAs (R28d).  heap_free: base -> size of free ranges (mu).
     uint64_t heap_base = 0, heap_size = 0;
+    // F3 code objects seen by the CUPTI hook (cuModuleLoadData*): module -> image bytes (mu)
+    std::map<CUmodule, std::vector<uint8_t>> code_objects;
     // parked pinned host arena for kc_capture_host (kc_host_arena_reserve)
     void* host_arena = nullptr;
     uint64_t host_arena_bytes = 0;
@@ -129,6 +146,8 @@ struct kc_restored {
     CUmodule module = nullptr;
     std::vector<uint8_t> image;  // code object (kernel.cubin or the device snapshot's copy)
     const kc_snapshot* dev_snap = nullptr;  // restored from a device snapshot (kc_restore_dev)
+    std::vector<ModVarState> modvars;       // F3: written into the replay module before each launch
+    uint64_t modvar_checked = 0, modvar_mismatch = 0;  // last replay vs the captured post values
 };
 
 namespace kc {

@@ -804,7 +804,18 @@ const CUpti_CallbackId kTrackedCbids[] = {
     CUPTI_DRIVER_TRACE_CBID_cuMemAllocAsync_ptsz,    CUPTI_DRIVER_TRACE_CBID_cuMemFreeAsync,
     CUPTI_DRIVER_TRACE_CBID_cuMemFreeAsync_ptsz,     CUPTI_DRIVER_TRACE_CBID_cuMemAllocFromPoolAsync,
     CUPTI_DRIVER_TRACE_CBID_cuMemAllocFromPoolAsync_ptsz, CUPTI_DRIVER_TRACE_CBID_cuMemMap,
-    CUPTI_DRIVER_TRACE_CBID_cuMemUnmap};
+    CUPTI_DRIVER_TRACE_CBID_cuMemUnmap,
+    // F3 code-object capture: module loads and unloads
+    CUPTI_DRIVER_TRACE_CBID_cuModuleLoadData, CUPTI_DRIVER_TRACE_CBID_cuModuleLoadDataEx,
+    CUPTI_DRIVER_TRACE_CBID_cuModuleLoadFatBinary, CUPTI_DRIVER_TRACE_CBID_cuModuleUnload};
+
+void record_code_object(kc_ctx* ctx, const CUmodule* mod, const void* image) {
+    if (!mod || !*mod || !image) return;
+    const size_t n = image_size(image, 0);
+    if (!n) return;  // PTX text or an unknown container: not recorded
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->code_objects[*mod].assign((const uint8_t*)image, (const uint8_t*)image + n);
+}
 
 void CUPTIAPI cupti_cb(void* user, CUpti_CallbackDomain domain, CUpti_CallbackId cbid, const void* cbdata) {
     kc_ctx* ctx = (kc_ctx*)user;
@@ -850,6 +861,27 @@ void CUPTIAPI cupti_cb(void* user, CUpti_CallbackDomain domain, CUpti_CallbackId
         case CUPTI_DRIVER_TRACE_CBID_cuMemMap: {
             auto p = (const cuMemMap_params*)d->functionParams;
             kc_track(ctx, KC_EV_MAP, (uint64_t)p->ptr, p->size, dev, KC_KIND_VMM);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuModuleLoadData: {
+            auto p = (const cuModuleLoadData_params*)d->functionParams;
+            record_code_object(ctx, p->module, p->image);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuModuleLoadDataEx: {
+            auto p = (const cuModuleLoadDataEx_params*)d->functionParams;
+            record_code_object(ctx, p->module, p->image);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuModuleLoadFatBinary: {
+            auto p = (const cuModuleLoadFatBinary_params*)d->functionParams;
+            record_code_object(ctx, p->module, p->fatCubin);
+            break;
+        }
+        case CUPTI_DRIVER_TRACE_CBID_cuModuleUnload: {
+            auto p = (const cuModuleUnload_params*)d->functionParams;
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            ctx->code_objects.erase(p->hmod);
             break;
         }
         case CUPTI_DRIVER_TRACE_CBID_cuMemUnmap: {

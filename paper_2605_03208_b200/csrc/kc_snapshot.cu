@@ -295,6 +295,84 @@ bool item_h2d(kc_ctx* ctx, kc_ctx::IoWorker& w, int fd, uint64_t base, const IoI
     return cudaStreamSynchronize(w.stream) == cudaSuccess;
 }
 
+// ------------------------------------------------------------------ F3 module variables + code object
+// (PAPER.md:506-516, 728-751).  The dispatch's module: the one kc loaded from
+// the given image, else the function's own (cuFuncGetModule).  Its code object:
+// the given image, else the bytes the CUPTI hook recorded when the application
+// loaded the module.  Variables: the code object's ELF symbols (kc_module.cu)
+// resolved in that module with cuModuleGetGlobal; read before and after.
+struct ModCapture {
+    CUmodule mod = nullptr;
+    std::vector<uint8_t> image;
+    std::vector<ModVarState> vars;
+    std::vector<CUdeviceptr> addr;
+};
+
+bool modvars_disabled() {
+    const char* e = getenv("KC_NO_MODULE_VARS");
+    return e && *e && *e != '0';
+}
+
+kc_status module_capture_pre(kc_ctx* ctx, const kc_dispatch* d, CUfunction f, CUmodule own_mod, ModCapture& mc) {
+    mc.mod = own_mod;
+    if (!mc.mod && KC_DRV(cuFuncGetModule)(&mc.mod, f) != CUDA_SUCCESS) mc.mod = nullptr;
+    if (d->image) {
+        const size_t n = image_size(d->image, d->image_size);
+        if (n) mc.image.assign((const uint8_t*)d->image, (const uint8_t*)d->image + n);
+    } else if (mc.mod) {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        auto it = ctx->code_objects.find(mc.mod);
+        if (it != ctx->code_objects.end()) mc.image = it->second;
+    }
+    if (!mc.mod || mc.image.empty() || modvars_disabled()) return KC_OK;
+    for (const ModVarDecl& v : image_module_vars(mc.image.data(), mc.image.size())) {
+        CUdeviceptr p = 0;
+        size_t bytes = 0;
+        if (KC_DRV(cuModuleGetGlobal)(&p, &bytes, mc.mod, v.name.c_str()) != CUDA_SUCCESS || !p || !bytes) continue;
+        ModVarState s;
+        s.name = v.name;
+        s.section = v.section;
+        s.size = bytes;
+        s.pre.resize(bytes);
+        KC_CHECK_CUDA(ctx, cudaMemcpy(s.pre.data(), (const void*)p, bytes, cudaMemcpyDeviceToHost), "module variable");
+        mc.vars.push_back(std::move(s));
+        mc.addr.push_back(p);
+    }
+    return KC_OK;
+}
+
+kc_status module_capture_post(kc_ctx* ctx, ModCapture& mc) {
+    for (size_t i = 0; i < mc.vars.size(); ++i) {
+        mc.vars[i].post.resize(mc.vars[i].size);
+        KC_CHECK_CUDA(ctx, cudaMemcpy(mc.vars[i].post.data(), (const void*)mc.addr[i], mc.vars[i].size,
+                                      cudaMemcpyDeviceToHost), "module variable (post)");
+    }
+    return KC_OK;
+}
+
+// module_vars.json + module_vars/NNN.{pre,post}.bin
+bool write_module_vars(const std::string& dir, const std::vector<ModVarState>& vars) {
+    if (vars.empty()) return true;
+    if (!mkdir_p(dir + "/module_vars")) return false;
+    std::string j = "{\n  \"format\": \"kc-module-vars/1\",\n  \"vars\": [";
+    for (size_t i = 0; i < vars.size(); ++i) {
+        char idx[24];
+        snprintf(idx, sizeof idx, "%03zu", i);
+        const std::string pre = std::string("module_vars/") + idx + ".pre.bin";
+        const std::string post = std::string("module_vars/") + idx + ".post.bin";
+        if (!write_file(dir + "/" + pre, vars[i].pre.data(), vars[i].size) ||
+            !write_file(dir + "/" + post, vars[i].post.data(), vars[i].size))
+            return false;
+        char buf[128];
+        snprintf(buf, sizeof buf, "\"size\": %llu, ", (unsigned long long)vars[i].size);
+        j += std::string(i ? "," : "") + "\n    {\"name\": \"" + kcj::esc(vars[i].name) + "\", \"section\": \"" +
+             kcj::esc(vars[i].section) + "\", " + buf + "\"pre\": \"" + pre + "\", \"post\": \"" + post +
+             "\", \"written\": " + (vars[i].pre != vars[i].post ? "true" : "false") + "}";
+    }
+    j += "\n  ]\n}\n";
+    return write_text(dir + "/module_vars.json", j);
+}
+
 // ------------------------------------------------------------------ kc-snapshot/1 writers
 // Shared by kc_capture (file sink) and kc_snapshot_save (device snapshot).
 struct MetaRegion {
@@ -497,6 +575,14 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
             return cuda_err(ctx, e, "kc_capture: quiesce");
         }
     }
+    ModCapture mc;  // F3: the dispatch's code object and module variables (pre values)
+    {
+        kc_status mst = module_capture_pre(ctx, d, f, own_mod, mc);
+        if (mst != KC_OK) {
+            if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+            return mst;
+        }
+    }
     std::vector<RegionState> rs(list.size());
     std::vector<kc_region> live;
     for (size_t i = 0; i < list.size(); ++i) {
@@ -543,10 +629,10 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
 
     auto write_metadata = [&](bool post_digests) -> bool {
         const std::string j = dispatch_json(mode, mangled, d->grid, d->block, d->smem_bytes, d->kernarg_size,
-                                            ctx->device, d->image ? d->image_size : (size_t)0, layout);
+                                            ctx->device, mc.image.size(), layout);
         if (!write_text(dir + "/dispatch.json", j)) return false;
         if (!write_file(dir + "/kernarg.bin", d->kernarg, d->kernarg ? d->kernarg_size : 0)) return false;
-        if (d->image && d->image_size && !write_file(dir + "/kernel.cubin", d->image, d->image_size)) return false;
+        if (!mc.image.empty() && !write_file(dir + "/kernel.cubin", mc.image.data(), mc.image.size())) return false;
         std::vector<MetaRegion> mr;
         for (const RegionState& r : rs)
             mr.push_back({r.r.base, r.r.size, r.n_chunks, post_digests ? r.post_digest : r.pre_digest, r.r.seq,
@@ -643,7 +729,12 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
         }
     }
     rep.t_dispatch_s = now_s() - t;
-    if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+    {
+        kc_status mst = module_capture_post(ctx, mc);
+        if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
+        if (mst != KC_OK) return mst;
+    }
+    if (!write_module_vars(dir, mc.vars)) return set_err(ctx, KC_ERR_IO, "kc_capture: cannot write module_vars");
 
     // test hook: a region freed between completion and snapshot
     if (const char* hook = getenv("KC_TEST_FREE_AFTER_DISPATCH")) {
@@ -910,6 +1001,7 @@ struct SnapDesc {
     std::vector<std::pair<size_t, size_t>> layout;  // kernarg (offset, size)
     std::vector<SnapRegion> regions;                 // ascending base
     uint64_t snapshot_digest = 0;
+    std::vector<ModVarState> modvars;                // F3
 };
 
 struct RestoreSource {
@@ -947,6 +1039,23 @@ kc_status load_desc_files(kc_ctx* ctx, const std::string& dir, SnapDesc& d, kc_r
         return set_err(ctx, KC_ERR_FORMAT, "kernarg.bin has %zu bytes, dispatch.json says %llu", d.kernarg.size(),
                        (unsigned long long)ksz);
     read_bin(dir + "/kernel.cubin", d.image);
+    // F3: module variables (optional file)
+    std::string mtext;
+    if (kcj::read_file(dir + "/module_vars.json", mtext)) {
+        kcj::Value mv;
+        if (!kcj::Parser(mtext).parse(mv) || !mv.get("vars"))
+            return set_err(ctx, KC_ERR_FORMAT, "module_vars.json does not parse");
+        for (auto& e : mv.get("vars")->a) {
+            ModVarState s;
+            s.name = e.get("name") ? e.get("name")->s : "";
+            s.section = e.get("section") ? e.get("section")->s : "";
+            s.size = e.get("size") ? e.get("size")->as_u64() : 0;
+            if (!e.get("pre") || !e.get("post") || !read_bin(dir + "/" + e.get("pre")->s, s.pre) ||
+                !read_bin(dir + "/" + e.get("post")->s, s.post) || s.pre.size() != s.size || s.post.size() != s.size)
+                return set_err(ctx, KC_ERR_FORMAT, "module variable %s: missing or wrong-length files", s.name.c_str());
+            d.modvars.push_back(std::move(s));
+        }
+    }
     for (auto& r : regs) {
         SnapRegion sr;
         sr.r.base = r.base;
@@ -1039,6 +1148,7 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     h->smem = d.smem;
     h->kernarg = d.kernarg;
     h->image = d.image;
+    h->modvars = d.modvars;
     std::vector<ParsedRegion> regs;
     for (auto& sr : d.regions) {
         kc_restored_region rr;
@@ -1553,7 +1663,12 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     D.smem = d->smem_bytes;
     if (d->kernarg && d->kernarg_size)
         D.kernarg.assign((const uint8_t*)d->kernarg, (const uint8_t*)d->kernarg + d->kernarg_size);
-    if (d->image && d->image_size) D.image.assign((const uint8_t*)d->image, (const uint8_t*)d->image + d->image_size);
+    ModCapture mc;  // F3
+    {
+        kc_status mst = module_capture_pre(ctx, d, f, own_mod, mc);
+        if (mst != KC_OK) return fail(mst);
+    }
+    D.image = mc.image;
 
     // ---- A3 bracket: quiesce, liveness, K1 pre-manifest
     cudaError_t e = cudaDeviceSynchronize();
@@ -1695,9 +1810,14 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     }
     rep.t_dispatch_s = now_s() - t;
     trace("dispatch", tl);
-    if (own_mod) {
-        KC_DRV(cuModuleUnload)(own_mod);
-        own_mod = nullptr;
+    {
+        kc_status mst = module_capture_post(ctx, mc);
+        if (own_mod) {
+            KC_DRV(cuModuleUnload)(own_mod);
+            own_mod = nullptr;
+        }
+        if (mst != KC_OK) return fail(mst);
+        D.modvars = std::move(mc.vars);
     }
     // ---- K1 post-manifest + W
     t = now_s();
@@ -1809,7 +1929,8 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
                                                           (uint32_t)D.kernarg.size(), ctx->device, D.image.size(),
                                                           D.layout)) ||
         !write_file(dir + "/kernarg.bin", D.kernarg.data(), D.kernarg.size()) ||
-        (!D.image.empty() && !write_file(dir + "/kernel.cubin", D.image.data(), D.image.size())))
+        (!D.image.empty() && !write_file(dir + "/kernel.cubin", D.image.data(), D.image.size())) ||
+        !write_module_vars(dir, D.modvars))
         return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write metadata in %s", dir_c);
     std::vector<MetaRegion> mr;
     for (auto& sr : D.regions)
@@ -1944,6 +2065,36 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
         if (own) KC_DRV(cuModuleUnload)(mod);
         return set_err(ctx, KC_ERR_ARG, "kc_replay: symbol %s not found in the code object", h->mangled.c_str());
     }
+    // F3: module variables into the replay module, after the memory restore and
+    // before the dispatch; PRE_W restores the pre values,
+    // POST the post values (the same state the region files hold)
+    std::vector<std::pair<CUdeviceptr, const ModVarState*>> mv;
+    uint32_t mv_restored = 0;
+    if (!modvars_disabled())
+        for (const ModVarState& v : h->modvars) {
+            CUdeviceptr p = 0;
+            size_t bytes = 0;
+            if (KC_DRV(cuModuleGetGlobal)(&p, &bytes, mod, v.name.c_str()) != CUDA_SUCCESS || bytes != v.size) continue;
+            mv.emplace_back(p, &v);
+        }
+    auto put_modvars = [&](bool only_written) -> kc_status {
+        for (auto& pv : mv) {
+            const ModVarState& v = *pv.second;
+            if (only_written && v.pre == v.post) continue;
+            const std::vector<uint8_t>& src = h->mode == KC_MODE_PRE_W ? v.pre : v.post;
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync((void*)pv.first, src.data(), v.size, cudaMemcpyHostToDevice, s),
+                          "restore module variable");
+        }
+        return KC_OK;
+    };
+    {
+        kc_status mst = put_modvars(false);
+        if (mst != KC_OK) {
+            if (own) KC_DRV(cuModuleUnload)(mod);
+            return mst;
+        }
+        mv_restored = (uint32_t)mv.size();
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -1958,6 +2109,7 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
                     cudaMemcpyAsync((void*)(rr.r.base + k * kChunk), (uint8_t*)h->stash_pre + rr.stash_off[j], len,
                                     cudaMemcpyDeviceToDevice, s);
                 }
+            if (h->mode == KC_MODE_PRE_W) put_modvars(true);
         }
         cudaEventRecord(e0, s);
         CUresult r;
@@ -1985,9 +2137,19 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    // F3 validation input: every restored variable against its captured post value
+    h->modvar_checked = h->modvar_mismatch = 0;
+    if (res == KC_OK)
+        for (auto& pv : mv) {
+            std::vector<uint8_t> now(pv.second->size);
+            if (cudaMemcpy(now.data(), (const void*)pv.first, now.size(), cudaMemcpyDeviceToHost) != cudaSuccess) break;
+            h->modvar_checked++;
+            h->modvar_mismatch += now != pv.second->post;
+        }
     if (own) KC_DRV(cuModuleUnload)(mod);
     if (res != KC_OK) return res;
     if (rep_out) {
+        rep_out->module_vars_restored = mv_restored;
         rep_out->iterations = iters;
         rep_out->kernel_ms_mean = sum / iters;
         rep_out->kernel_ms_min = mn;
@@ -2007,6 +2169,14 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
             if (!ok) return set_err(ctx, KC_ERR_IO, "dump %s: %s", path.c_str(), err.c_str());
         }
     }
+    return KC_OK;
+}
+
+extern "C" kc_status kc_validate_module_vars(kc_ctx* ctx, const kc_restored* h, uint64_t* n_checked,
+                                             uint64_t* n_mismatch) {
+    if (!ctx || !h) return KC_ERR_ARG;
+    if (n_checked) *n_checked = h->modvar_checked;
+    if (n_mismatch) *n_mismatch = h->modvar_mismatch;
     return KC_OK;
 }
 

@@ -42,7 +42,7 @@ EXPORTED = [
     "kc_written", "kc_diff_async", "kc_hash_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
-    "kc_capture_incr", "kc_snapshot_shared_bytes",
+    "kc_capture_incr", "kc_snapshot_shared_bytes", "kc_validate_module_vars",
 ]
 
 
@@ -116,7 +116,8 @@ class ReplayOpts(ctypes.Structure):
 
 
 class ReplayReport(ctypes.Structure):
-    _fields_ = [("iterations", ctypes.c_uint32), ("_pad", ctypes.c_uint32), ("kernel_ms_mean", ctypes.c_double),
+    _fields_ = [("iterations", ctypes.c_uint32), ("module_vars_restored", ctypes.c_uint32),
+                ("kernel_ms_mean", ctypes.c_double),
                 ("kernel_ms_min", ctypes.c_double), ("kernel_ms_max", ctypes.c_double)]
 
     def as_dict(self):
@@ -187,6 +188,7 @@ def lib() -> ctypes.CDLL:
         "kc_capture_incr": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, V, ctypes.c_int, P(V),
                                  P(CaptureReport)]),
         "kc_snapshot_shared_bytes": (U64, [V]),
+        "kc_validate_module_vars": (st, [V, V, P(U64), P(U64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -457,13 +459,10 @@ class Context:
     # -- closure
     def capture(self, directory: str, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
                 block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
-                stream: int = 0) -> tuple[int, dict]:
-        img = ctypes.create_string_buffer(image, len(image)) if image else None
-        ka = ctypes.create_string_buffer(kernarg, len(kernarg)) if kernarg else None
-        d = Dispatch(None, ctypes.cast(img, ctypes.c_void_p) if img else None, len(image) if image else 0,
-                     mangled.encode() if mangled else None, (ctypes.c_uint32 * 3)(*grid),
-                     (ctypes.c_uint32 * 3)(*block), smem, len(kernarg), ctypes.cast(ka, ctypes.c_void_p) if ka else None,
-                     stream or None)
+                stream: int = 0, func: int = 0) -> tuple[int, dict]:
+        """kc_capture.  func: a CUfunction handle of the application's own module
+        (then image may be omitted when kc_track_install recorded the module's load)."""
+        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func)
         rep = CaptureReport()
         arr = _regions(regions) if regions is not None else None
         rc = lib().kc_capture(self._h, ctypes.byref(d), arr, len(regions) if regions is not None else 0,
@@ -471,10 +470,10 @@ class Context:
         self._check(rc, "kc_capture", ok=(KC_OK, KC_PARTIAL))
         return rc, rep.as_dict()
 
-    def _dispatch(self, image, mangled, grid, block, smem, kernarg, stream):
+    def _dispatch(self, image, mangled, grid, block, smem, kernarg, stream, func=0):
         img = ctypes.create_string_buffer(image, len(image)) if image else None
         ka = ctypes.create_string_buffer(kernarg, len(kernarg)) if kernarg else None
-        d = Dispatch(None, ctypes.cast(img, ctypes.c_void_p) if img else None, len(image) if image else 0,
+        d = Dispatch(func or None, ctypes.cast(img, ctypes.c_void_p) if img else None, len(image) if image else 0,
                      mangled.encode() if mangled else None, (ctypes.c_uint32 * 3)(*grid),
                      (ctypes.c_uint32 * 3)(*block), smem, len(kernarg), ctypes.cast(ka, ctypes.c_void_p) if ka else None,
                      stream or None)
@@ -482,12 +481,12 @@ class Context:
 
     def capture_dev(self, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
                     block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
-                    stream: int = 0, host: bool = False, base: "DevSnapshot | None" = None
+                    stream: int = 0, host: bool = False, base: "DevSnapshot | None" = None, func: int = 0
                     ) -> tuple[DevSnapshot, dict]:
         """kc_capture into a device arena (F1), or a pinned host arena (host=True:
         kc_capture_host); with base=, only chunks changed against it are copied
         (kc_capture_incr)."""
-        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream)
+        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func)
         rep = CaptureReport()
         h = ctypes.c_void_p()
         arr = _regions(regions) if regions is not None else None
@@ -539,6 +538,13 @@ class Context:
         rep = ReplayReport()
         self._check(lib().kc_replay(self._h, restored.handle, ctypes.byref(o), ctypes.byref(rep)), "kc_replay")
         return rep.as_dict()
+
+    def validate_module_vars(self, restored: Restored) -> tuple[int, int]:
+        """F3: (variables checked, variables differing from their captured post value) of the last replay."""
+        n, m = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(lib().kc_validate_module_vars(self._h, restored.handle, ctypes.byref(n), ctypes.byref(m)),
+                    "kc_validate_module_vars")
+        return int(n.value), int(m.value)
 
     def validate(self, restored: Restored, outs=None, atol: float = 1e-8, rtol: float = 1e-5,
                  equal_nan: bool = False) -> tuple[list, int]:

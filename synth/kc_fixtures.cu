@@ -115,3 +115,17 @@ extern "C" __global__ void kc_fixture_moe_gemv(const unsigned long long* __restr
     for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, s);
     if (lane == 0) y[(size_t)t * O + o] = acc;
 }
+
+// F3 (module variables): a kernel whose result depends on
+// module state the tracker cannot see: a __constant__ table and a __device__
+// scale the application sets after loading the module, plus a __device__
+// counter the dispatch itself writes.
+__constant__ unsigned int kc_fixture_cvals[8];
+__device__ float kc_fixture_scale = 2.5f;
+__device__ unsigned long long kc_fixture_hits;
+extern "C" __global__ void kc_fixture_modvar(unsigned long long* out, unsigned int n) {
+    const unsigned int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = (unsigned long long)((float)kc_fixture_cvals[i & 7] * kc_fixture_scale) + i;
+    atomicAdd(&kc_fixture_hits, 1ull);
+}

@@ -164,6 +164,7 @@ def replay(a):
     reps, unexpected = ctx.validate(r)
     out["validate"] = reps
     out["unexpected_chunks"] = unexpected
+    out["modvars"] = ctx.validate_module_vars(r)
     out["dump"] = dump
     r.release()
     print(json.dumps(out))
@@ -286,6 +287,38 @@ def incr(a):
     print(json.dumps(out))
 
 
+def capture_modvar(a):
+    """F3: the application loads the fixture module itself (cuda-python), sets
+    its __constant__ / __device__ variables, and the capture gets only the
+    CUfunction (+ the image unless the CUPTI hook recorded the module load)."""
+    import struct
+    from cuda.bindings import driver as drv
+    ctx = kc.Context(0)
+    if a.cupti:
+        ctx.track_install()
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    err, mod = drv.cuModuleLoadData(image)
+    assert err == drv.CUresult.CUDA_SUCCESS, err
+    err, fn = drv.cuModuleGetFunction(mod, b"kc_fixture_modvar")
+    assert err == drv.CUresult.CUDA_SUCCESS, err
+
+    def put(name, arr):
+        err, p, sz = drv.cuModuleGetGlobal(mod, name)
+        assert err == drv.CUresult.CUDA_SUCCESS and sz == arr.nbytes, (err, sz)
+        drv.cuMemcpyHtoD(p, arr.ctypes.data, arr.nbytes)
+    put(b"kc_fixture_cvals", (np.arange(1, 9, dtype=np.uint32) * 7))
+    put(b"kc_fixture_scale", np.array([3.25], dtype=np.float32))
+    put(b"kc_fixture_hits", np.array([1000], dtype=np.uint64))
+    n = 5000
+    out_va = ctx.alloc(8 * n)
+    _upload(out_va, np.zeros(n, dtype=np.uint64))
+    karg = struct.pack("<QI", out_va, n)
+    rc, rep = ctx.capture(a.dir, func=int(fn), image=None if a.cupti else image, grid=((n + 255) // 256, 1, 1),
+                          block=(256, 1, 1), kernarg=karg, mode=kc.KC_MODE_PRE_W)
+    np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_orig_out.npy"), _download(out_va, 8 * n))
+    print(json.dumps({"rc": rc, "report": rep, "out_va": out_va, "n": n}))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -304,9 +337,10 @@ def main():
     p.add_argument("--typed", default=None)
     p.add_argument("--host", action="store_true")
     p.add_argument("--cycles", type=int, default=1)
+    p.add_argument("--cupti", action="store_true")
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
-     "inproc": inproc, "devsnap": devsnap, "incr": incr}[a.cmd](a)
+     "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar}[a.cmd](a)
 
 
 if __name__ == "__main__":

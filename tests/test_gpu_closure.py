@@ -301,3 +301,37 @@ def test_incremental_capture_shares_unchanged_chunks(tmp_path, host):
     assert res["restore"]["verify_mismatch_chunks"] == 0 and res["out_equal"]
     assert all(r["differing_bytes"] == 0 for r in res["validate"]) and res["unexpected_chunks"] == 0
     assert res["typed"][0]["pass"] == 1
+
+
+@pytest.mark.parametrize("cupti", [False, True])
+def test_module_vars_capture_replay(tmp_path, cupti):
+    """F3: the application sets __constant__ /
+    __device__ variables of its own module; the capture records them (and,
+    with the CUPTI hook, the code object from the module load), a fresh
+    process restores them into the replay module, and the replay reproduces
+    the output; without them (KC_NO_MODULE_VARS=1) it does not."""
+    d = str(tmp_path / "mv")
+    os.makedirs(d, exist_ok=True)
+    cap = run("capture-modvar", d, *(["--cupti"] if cupti else []))
+    assert cap["rc"] == 0
+    mv = json.load(open(os.path.join(d, "module_vars.json")))
+    byname = {v["name"]: v for v in mv["vars"]}
+    assert {"kc_fixture_cvals", "kc_fixture_scale", "kc_fixture_hits"} <= set(byname)
+    assert byname["kc_fixture_cvals"]["size"] == 32 and not byname["kc_fixture_cvals"]["written"]
+    assert byname["kc_fixture_hits"]["written"]  # the dispatch counted itself
+    hits = np.fromfile(os.path.join(d, byname["kc_fixture_hits"]["post"]), dtype=np.uint64)
+    assert int(hits[0]) == 1000 + cap["n"]
+    from oracle import snapshot
+    summ = snapshot.verify(snapshot.load(d))
+    assert summ["ok"] == 1 and summ["module_vars"] >= 3
+    orig = np.load(str(tmp_path / "mv_orig_out.npy"))
+    res = run("replay", d)
+    assert res["replay"]["module_vars_restored"] >= 3
+    assert res["modvars"][0] >= 3 and res["modvars"][1] == 0  # post values reproduced (hits too)
+    assert all(r["differing_bytes"] == 0 for r in res["validate"]) and res["unexpected_chunks"] == 0
+    out_file = os.path.join(res["dump"], "output", "region_%x.bin" % cap["out_va"])
+    # (with the CUPTI hook the tracked region is the whole mapped VMM range, so compare the prefix)
+    assert np.array_equal(np.fromfile(out_file, dtype=np.uint8)[:orig.size], orig)
+    neg = run("replay", d, env={"KC_NO_MODULE_VARS": "1"})
+    assert neg["replay"]["module_vars_restored"] == 0
+    assert any(r["differing_bytes"] > 0 for r in neg["validate"])

@@ -69,3 +69,25 @@ def test_walker_shifted_va_breaks(orc):
     shifted = [(b + (0x100000 if b == NB else 0), m) for b, m in regions]
     with pytest.raises(RuntimeError):
         orc.walk_lists(shifted, HB, 8, NB, OB)
+
+
+def test_cubin_module_vars_matches_readelf():
+    """The oracle's ELF64 module-variable listing (F3) against binutils'
+    readelf on the fixture code object: every defined, sized STT_OBJECT."""
+    import shutil
+    import subprocess
+    from paper_2605_03208_b200 import build
+    from oracle import snapshot
+    import synth
+    if not shutil.which("readelf"):
+        pytest.skip("readelf not available")
+    build.build_fixtures()
+    out = subprocess.run(["readelf", "-s", "-W", synth.FIXTURE_CUBIN], capture_output=True, text=True).stdout
+    exp = {}
+    for line in out.splitlines():
+        f = line.split()
+        if len(f) >= 8 and f[3] == "OBJECT" and f[6] != "UND" and int(f[2]) > 0:
+            exp[f[7]] = int(f[2])
+    got = snapshot.cubin_module_vars(synth.FIXTURE_CUBIN)
+    assert got == exp
+    assert got == {"kc_fixture_cvals": 32, "kc_fixture_scale": 4, "kc_fixture_hits": 8}
