@@ -23,6 +23,10 @@ FIXTURE_CUBIN = os.path.join(ROOT, "synth", "kc_fixtures.cubin")
 # (different optimisation level) and a modified kernel (KC_VARIANT_DELTA=1)
 FIXTURE_VARIANTS = {os.path.join(ROOT, "synth", "kc_fixtures_recompiled.cubin"): ["-O1"],
                     os.path.join(ROOT, "synth", "kc_fixtures_modified.cubin"): ["-O3", "-DKC_VARIANT_DELTA=1"]}
+# F4 workload: one attention-forward code object per "autotune config" BLOCK_N
+ATTN_SRC = os.path.join(ROOT, "synth", "kc_attn_fwd.cu")
+ATTN_BLOCK_N = (32, 64, 128)
+ATTN_CUBINS = {bn: os.path.join(ROOT, "synth", f"kc_attn_fwd_n{bn}.cubin") for bn in ATTN_BLOCK_N}
 SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu", "kc_module.cu"]
 HEADERS = ["kc_kernels.cuh", "kc_internal.h", "kc_json.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,6 +62,12 @@ def build_fixtures(force: bool = False) -> str:
         if force or _stale(out, [FIXTURE_SRC]):
             tmp = out + f".tmp{os.getpid()}"
             subprocess.check_call([NVCC, "-cubin", *ARCH, *flags, "-lineinfo", "-o", tmp, FIXTURE_SRC])
+            os.replace(tmp, out)
+    for bn, out in ATTN_CUBINS.items():
+        if force or _stale(out, [ATTN_SRC]):
+            tmp = out + f".tmp{os.getpid()}"
+            subprocess.check_call([NVCC, "-cubin", *ARCH, "-O3", "-lineinfo", f"-DKC_ATTN_BLOCK_N={bn}",
+                                   "-o", tmp, ATTN_SRC])
             os.replace(tmp, out)
     return FIXTURE_CUBIN
 

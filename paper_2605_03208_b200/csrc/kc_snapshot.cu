@@ -1128,7 +1128,11 @@ struct FileSource : RestoreSource {
         if (!read_bin(dir + "/written/region_" + d.regions[i].hx + ".bin", wb) || wb.size() != bytes)
             return set_err(ctx, KC_ERR_FORMAT, "written/region_%s.bin is missing or has the wrong length",
                            d.regions[i].hx.c_str());
-        KC_CHECK_CUDA(ctx, cudaMemcpy(dst, wb.data(), bytes, cudaMemcpyHostToDevice), "H2D written reference");
+        // on the ctx stream and complete before wb goes away: a legacy-stream
+        // cudaMemcpy would not order the stash against the non-blocking copy_stream
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(dst, wb.data(), bytes, cudaMemcpyHostToDevice, ctx->copy_stream),
+                      "H2D written reference");
+        KC_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream), "H2D written reference");
         return KC_OK;
     }
 };
@@ -1529,7 +1533,8 @@ struct DevSource : RestoreSource {
         return copy_ranges_d2d(ctx, ranges, ctx->copy_stream, nullptr);
     }
     kc_status written_ref(kc_ctx* ctx, const SnapDesc&, size_t i, void* dst, uint64_t bytes) override {
-        KC_CHECK_CUDA(ctx, cudaMemcpy(dst, (const uint8_t*)sn->warena + sn->w_off[i], bytes, cudaMemcpyDefault),
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(dst, (const uint8_t*)sn->warena + sn->w_off[i], bytes, cudaMemcpyDefault,
+                                           ctx->copy_stream),
                       "written reference from the arena");
         return KC_OK;
     }
@@ -2235,8 +2240,8 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
                 for (const auto& ru : sn->runs[ri]) {  // stored bytes of [roff, roff + nbytes)
                     const uint64_t lo = std::max(ru.roff, roff), hi = std::min(ru.roff + ru.len, roff + o.nbytes);
                     if (lo < hi)
-                        cudaMemcpy((uint8_t*)typed_ref + off + (lo - roff), (const uint8_t*)(ru.src + (lo - ru.roff)),
-                                   hi - lo, cudaMemcpyDefault);
+                        cudaMemcpyAsync((uint8_t*)typed_ref + off + (lo - roff),
+                                        (const uint8_t*)(ru.src + (lo - ru.roff)), hi - lo, cudaMemcpyDefault, s);
                 }
                 if (h->mode == KC_MODE_PRE_W) {
                     uint64_t woff = sn->w_off[ri];
@@ -2244,8 +2249,9 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
                         const uint64_t c0 = k * kChunk, len = std::min<uint64_t>(kChunk, owner->r.size - c0);
                         const uint64_t lo = std::max(c0, roff), hi = std::min(c0 + len, roff + o.nbytes);
                         if (lo < hi)
-                            cudaMemcpy((uint8_t*)typed_ref + off + (lo - roff),
-                                       (const uint8_t*)sn->warena + woff + (lo - c0), hi - lo, cudaMemcpyDefault);
+                            cudaMemcpyAsync((uint8_t*)typed_ref + off + (lo - roff),
+                                            (const uint8_t*)sn->warena + woff + (lo - c0), hi - lo, cudaMemcpyDefault,
+                                            s);
                         woff += len;
                     }
                 }
@@ -2269,7 +2275,8 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
                         woff += len;
                     }
                 }
-                cudaMemcpy((uint8_t*)typed_ref + off, host.data(), o.nbytes, cudaMemcpyHostToDevice);
+                cudaMemcpyAsync((uint8_t*)typed_ref + off, host.data(), o.nbytes, cudaMemcpyHostToDevice, s);
+                cudaStreamSynchronize(s);  // host goes out of scope
             }
             kc_buffer b = o;
             b.ref = (uint64_t)typed_ref + off;

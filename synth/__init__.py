@@ -203,6 +203,34 @@ def c5_sizes(S: int, n: int, jitter: bool, s: int | None = None) -> np.ndarray:
     return base
 
 
+# ------------------------------------------------------------------ F4 (drift study)
+# The attn_fwd shape the paper measures: fp16, B=2, H=16,
+# S=4096, D=128.  Inputs N(0, 0.5) as in the Triton attention tutorial's test
+# (reading R32); sm_scale = 1/sqrt(D).  Seed 260503208 + 6 (stream 0/1/2 = Q/K/V).
+F4_B, F4_H, F4_S, F4_D = 2, 16, 4096, 128
+F4_STD = 0.5
+F4_SM_SCALE = 1.0 / math.sqrt(F4_D)
+F4_BLOCK_M = 64
+F4_BYTES = F4_B * F4_H * F4_S * F4_D * 2          # 33,554,432 B per tensor
+F4_SPECS = [RegionSpec(n, F4_BYTES, dtype="f16", fill=("zero" if n == "o" else "normal"), params={"std": F4_STD})
+            for n in ("q", "k", "v", "o")]
+
+
+def f4_cubin(block_n: int) -> str:
+    """Code object of the attn_fwd fixture compiled for one BLOCK_N "autotune config"."""
+    return os.path.join(os.path.dirname(os.path.abspath(__file__)), f"kc_attn_fwd_n{block_n}.cubin")
+
+
+def f4_launch(B: int = F4_B, H: int = F4_H, S: int = F4_S) -> dict:
+    """Grid/block of kc_fixture_attn_fwd: one CTA of 256 threads per 64 query rows and head."""
+    return {"grid": (S // F4_BLOCK_M, B * H, 1), "block": (256, 1, 1)}
+
+
+def f4_kernarg(q_va: int, k_va: int, v_va: int, o_va: int, S: int = F4_S, sm_scale: float = F4_SM_SCALE) -> bytes:
+    """kc_fixture_attn_fwd(Q, K, V, O, int S, float sm_scale): natural alignment 8,8,8,8,4,4."""
+    return struct.pack("<QQQQif", q_va, k_va, v_va, o_va, S, sm_scale)
+
+
 # ------------------------------------------------------------------ torch materialisation
 class _CAI:
     """Expose a raw device range through __cuda_array_interface__ (zero-copy torch view)."""
