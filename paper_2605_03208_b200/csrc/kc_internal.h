@@ -157,7 +157,8 @@ kc_status set_err(kc_ctx* ctx, kc_status st, const char* fmt, ...);
 kc_status cuda_err(kc_ctx* ctx, cudaError_t e, const char* what);
 kc_status cu_err(kc_ctx* ctx, CUresult r, const char* what);
 cudaError_t ensure(kc_ctx_dev_buf& b, size_t bytes);
-kc_status ensure_pinned(kc_ctx* ctx);
+kc_status ensure_stream(kc_ctx* ctx);  // the ctx's non-blocking copy stream
+kc_status ensure_pinned(kc_ctx* ctx);  // + the pinned staging ring (file / PCIe paths only)
 bool bind_device(kc_ctx* ctx);
 
 std::string hex_base(uint64_t base);  // lowercase hex, no 0x

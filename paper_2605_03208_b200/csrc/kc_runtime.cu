@@ -92,10 +92,16 @@ bool bind_device(kc_ctx* ctx) {
     return drv().ok;
 }
 
-kc_status ensure_pinned(kc_ctx* ctx) {
-    if (!ctx->pinned.empty()) return KC_OK;
+kc_status ensure_stream(kc_ctx* ctx) {
     if (!ctx->copy_stream) KC_CHECK_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking),
                                          "cudaStreamCreate(copy)");
+    return KC_OK;
+}
+
+kc_status ensure_pinned(kc_ctx* ctx) {
+    if (!ctx->pinned.empty()) return KC_OK;
+    kc_status st = ensure_stream(ctx);
+    if (st != KC_OK) return st;
     for (uint32_t i = 0; i < ctx->depth; ++i) {
         void* p = nullptr;
         cudaError_t e = cudaHostAlloc(&p, ctx->io_chunk, cudaHostAllocDefault);

@@ -1010,6 +1010,8 @@ struct RestoreSource {
     virtual kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) = 0;
     // PRE_W: the captured post-dispatch bytes of region i's W chunks, concatenated, -> device dst
     virtual kc_status written_ref(kc_ctx* ctx, const SnapDesc& d, size_t i, void* dst, uint64_t bytes) = 0;
+    // the copy-in streams through the pinned staging ring (file sources)
+    virtual bool needs_staging() const { return true; }
 };
 
 namespace {
@@ -1308,15 +1310,35 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
 
     // ---- stage 5a: copy-in (gaps and failed regions zero-filled)
     t = now_s();
-    kc_status st = ensure_pinned(ctx);
+    kc_status st = src.needs_staging() ? ensure_pinned(ctx) : ensure_stream(ctx);
     if (st != KC_OK) {
         rollback(h);
         delete h;
         return st;
     }
-    for (auto& s : h->spans)
-        if (!s.fallback) cudaMemsetAsync((void*)s.base, 0, s.size, ctx->copy_stream);
-    for (auto& rr : h->regions) cudaMemsetAsync((void*)rr.r.base, 0, rr.r.size, ctx->copy_stream);
+    // zero only what the copy-in does not write: span bytes outside every ok
+    // region (granule padding) and failed regions; an ok region's stored bytes
+    // cover it entirely (its region file / arena runs are exactly `size` bytes,
+    // and the K1 verify below checks every chunk)
+    {
+        std::vector<std::pair<uint64_t, uint64_t>> ok_iv;  // ascending (regions are sorted by base)
+        for (auto& rr : h->regions) {
+            if (rr.ok) ok_iv.emplace_back(rr.r.base, rr.r.base + rr.r.size);
+            else cudaMemsetAsync((void*)rr.r.base, 0, rr.r.size, ctx->copy_stream);
+        }
+        size_t j = 0;
+        for (auto& s : h->spans) {
+            if (s.fallback) continue;
+            uint64_t cur = s.base;
+            const uint64_t end = s.base + s.size;
+            while (j < ok_iv.size() && ok_iv[j].second <= cur) ++j;
+            for (size_t k = j; k < ok_iv.size() && ok_iv[k].first < end; ++k) {
+                if (ok_iv[k].first > cur) cudaMemsetAsync((void*)cur, 0, ok_iv[k].first - cur, ctx->copy_stream);
+                cur = std::max(cur, ok_iv[k].second);
+            }
+            if (cur < end) cudaMemsetAsync((void*)cur, 0, end - cur, ctx->copy_stream);
+        }
+    }
     cudaStreamSynchronize(ctx->copy_stream);  // zero-fill before the copy-in streams
     st = src.copy_in(ctx, d, rep);
     cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
@@ -1523,6 +1545,7 @@ kc_status copy_ranges_d2d(kc_ctx* ctx, const std::vector<std::array<uint64_t, 3>
 struct DevSource : RestoreSource {
     const kc_snapshot* sn;
     explicit DevSource(const kc_snapshot* s) : sn(s) {}
+    bool needs_staging() const override { return false; }  // D2D / H2D straight from the arena
     kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) override {
         std::vector<std::array<uint64_t, 3>> ranges;
         for (size_t i = 0; i < d.regions.size(); ++i) {
@@ -1790,7 +1813,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         trace("copy", tl);
         return s2;
     };
-    st = ensure_pinned(ctx);  // creates the copy stream
+    st = ensure_stream(ctx);  // in-memory sinks copy arena <-> device directly: no staging ring
     if (st != KC_OK) return fail(st);
     if (mode == KC_MODE_PRE_W) {
         st = snapshot_regions(pre_h);
