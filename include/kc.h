@@ -375,6 +375,84 @@ kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t
 kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out);
 void kc_release(kc_restored* h);
 
+/* ---- F4 multi-kernel capture -------------------------
+ * PAPER.md:1855-1862 ("capturing a sequence of dependent kernels for joint
+ * replay remains future work") and 1917-1918 ("multi-kernel capture for
+ * dependent kernel sequences with automatic dependency tracking").
+ *
+ * kc_capture_seq forwards the n_disp dispatches ds[0..n_disp) in order (each
+ * one on its kc_dispatch stream, the device synchronised around it as in
+ * kc_capture) and keeps one PRE_W in-memory snapshot per step: step k holds
+ * the state before dispatch k, its post manifest and the post bytes of its
+ * written set W_k.  Step 0 is a full capture (kc_capture_dev / _host), step
+ * k > 0 an incremental one against step k-1 (kc_capture_incr: only chunks
+ * changed since step k-1's stored state are copied).  host: 0 = device
+ * arenas (HBM), 1 = pinned host arenas.  reps: n_disp capture reports or
+ * NULL.  On an error no sequence is returned (steps taken so far are freed),
+ * but the dispatches already forwarded have run.  Ownership of *out passes to
+ * the caller (kc_seq_free).  regions/n as kc_capture (NULL = the tracker).
+ *
+ * Dependency tracking (reading R33): for steps i < j,
+ *   KC_DEP_RAW  a pointer-sized kernarg parameter of dispatch j (layout from
+ *               cuFuncGetParamInfo) holds a VA inside a region of which
+ *               dispatch i wrote a chunk (j may read what i wrote);
+ *   KC_DEP_WAW  W_i and W_j share a chunk;
+ *   KC_DEP_WAR  a pointer parameter of dispatch i lies in a region of which
+ *               dispatch j wrote a chunk (j may overwrite what i read).
+ * Reads through embedded pointers (pointer chasing) are invisible to the
+ * kernarg test; the snapshot still holds them (the closure is whole-heap). */
+typedef struct kc_sequence kc_sequence;
+enum { KC_DEP_RAW = 1, KC_DEP_WAW = 2, KC_DEP_WAR = 4 };
+
+kc_status kc_capture_seq(kc_ctx* ctx, const kc_dispatch* ds, size_t n_disp, const kc_region* regions, size_t n,
+                         int host, kc_sequence** out, kc_capture_report* reps);
+/* Number of steps. */
+size_t kc_seq_length(const kc_sequence* q);
+/* Step k's snapshot (borrowed; owned by the sequence), NULL if k is out of range.
+ * It can be restored (kc_restore_dev) and saved (kc_snapshot_save) on its own. */
+const kc_snapshot* kc_seq_step(const kc_sequence* q, size_t k);
+/* deps[j * n + i] (n = kc_seq_length, caller-allocated n*n bytes): KC_DEP_*
+ * flags of step j on step i < j; every other entry 0.  KC_ERR_ARG if cap < n*n. */
+kc_status kc_seq_deps(const kc_sequence* q, uint8_t* deps, size_t cap);
+/* Persist: dir/step_NNN/ (kc-snapshot/1 each, NNN = 000, 001, ...) and
+ * dir/sequence.json (format "kc-sequence/1", n, per-step symbol and |W|, the
+ * dependency matrix), sentinel dir/sequence_complete written last. */
+kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* dir);
+void kc_seq_free(kc_sequence* q);
+
+typedef struct {
+    size_t first, count;                  /* replay steps [first, first + count) */
+    const void* const* image_overrides;   /* NULL, or `count` code objects (NULL entry = the captured one) */
+    const size_t* image_override_sizes;   /* may be NULL (sizes read from the ELF/fatbin headers) */
+    kc_tolerance tol;                     /* used by each step's report (numpy defaults: 1e-8, 1e-5, 0) */
+    void* stream;
+} kc_seq_replay_opts;
+
+typedef struct {
+    kc_diff_report w;            /* the step's W chunks (every region, as bytes) vs the captured post bytes;
+                                    bitmap-free; w.nbytes = bytes of the regions the step wrote */
+    uint64_t unexpected_chunks;  /* chunks outside W_k whose hash the replayed dispatch changed */
+    uint64_t inherited_chunks;   /* chunks whose state at step entry differs from step k's captured pre-state:
+                                    divergence carried in from earlier replayed steps (0 for the first step,
+                                    which the restore verifies) */
+    uint64_t modvar_mismatch;    /* F3 module variables differing from their captured post values */
+    double kernel_ms;
+    int32_t pass;                /* w.differing_bytes == 0 && unexpected_chunks == 0 && modvar_mismatch == 0
+                                    (a step passes on inherited divergence it does not consume) */
+    int32_t _pad;
+} kc_seq_step_report;
+
+/* Joint replay: restore step `first`'s state at the captured VAs (the live
+ * allocations must be gone, as for kc_restore_dev), then for each step k in
+ * order replay dispatch k (its captured code object or the override) on the
+ * state the previous replays left and validate it -> reps[k - first].  A
+ * divergence in step k therefore shows in k's report and propagates to the
+ * steps that consume its output.  keep != NULL: the restored state after the
+ * last step is returned (kc_release it); else it is released.  Errors of a
+ * step abort the replay (reports of earlier steps are filled). */
+kc_status kc_replay_seq(kc_ctx* ctx, const kc_sequence* q, const kc_seq_replay_opts* o, kc_seq_step_report* reps,
+                        kc_restored** keep);
+
 #ifdef __cplusplus
 }
 #endif

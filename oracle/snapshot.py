@@ -174,3 +174,72 @@ def verify(snap: Snapshot) -> dict:
             n_mv += 1
     return {"regions": len(snap.regions), "ok": len(ok_bases), "written_chunks": n_written, "snapshot_digest": S,
             "module_vars": n_mv}
+
+
+# --------------------------------------------------------------------------- F4 sequences
+DEP_RAW, DEP_WAW, DEP_WAR = 1, 2, 4
+
+
+def _pointer_regions(snap: Snapshot) -> set:
+    """Regions (indices) that a pointer-sized kernarg parameter points into (R33)."""
+    ka = open(os.path.join(snap.dir, "kernarg.bin"), "rb").read()
+    out = set()
+    for p in snap.dispatch.get("kernarg_layout", []):
+        off, sz = int(p["offset"]), int(p["size"])
+        if sz != 8 or off + 8 > len(ka):
+            continue
+        v = int.from_bytes(ka[off:off + 8], "little")
+        for i, r in enumerate(snap.regions):
+            if r.status == "ok" and r.base <= v < r.base + r.size:
+                out.add(i)
+    return out
+
+
+def sequence_deps(steps: list) -> list:
+    """Dependency flags of step j on step i < j, from the step directories
+    alone (R33): RAW = a pointer parameter of j lies in a region i wrote; WAW =
+    W_i and W_j share a chunk; WAR = a pointer parameter of i lies in a region
+    j wrote."""
+    n = len(steps)
+    ptrs = [_pointer_regions(s) for s in steps]
+    wch = [{(i, int(k)) for i, r in enumerate(s.regions) for k in r.written.tolist()} for s in steps]
+    wreg = [{i for i, _ in w} for w in wch]
+    deps = [[0] * n for _ in range(n)]
+    for j in range(n):
+        for i in range(j):
+            f = 0
+            if ptrs[j] & wreg[i]:
+                f |= DEP_RAW
+            if wch[j] & wch[i]:
+                f |= DEP_WAW
+            if ptrs[i] & wreg[j]:
+                f |= DEP_WAR
+            deps[j][i] = f
+    return deps
+
+
+def verify_sequence(d: str) -> dict:
+    """Check a kc-sequence/1 directory (include/kc.h kc_seq_save): sentinel,
+    every step a valid kc-snapshot/1 (verify), the chain identity -- the state
+    before step k+1 is the state after step k, region by region, byte for byte
+    (the dispatches ran back to back) -- and the dependency matrix recomputed
+    from the step files."""
+    assert os.path.exists(os.path.join(d, "sequence_complete")), "no sequence_complete sentinel"
+    meta = json.load(open(os.path.join(d, "sequence.json")))
+    assert meta["format"] == "kc-sequence/1" and meta["n"] == len(meta["steps"])
+    steps = [load(os.path.join(d, s["dir"])) for s in meta["steps"]]
+    sums = [verify(s) for s in steps]
+    for k, (s, m) in enumerate(zip(steps, meta["steps"])):
+        assert s.dispatch["mangled_symbol"] == m["mangled_symbol"]
+        assert sum(int(r.written.size) for r in s.regions) == m["written_chunks"]
+    for k in range(len(steps) - 1):
+        a, b = steps[k], steps[k + 1]
+        assert [(r.base, r.size) for r in a.regions] == [(r.base, r.size) for r in b.regions]
+        for ra, rb in zip(a.regions, b.regions):
+            if ra.status != "ok":
+                continue
+            assert np.array_equal(a.post_state(ra), b.region_bytes(rb)), \
+                f"step {k} -> {k + 1}: region {ra.base:x} after step {k} != before step {k + 1}"
+    deps = sequence_deps(steps)
+    assert deps == meta["deps"], f"dependency matrix {meta['deps']} != recomputed {deps}"
+    return {"n": len(steps), "deps": deps, "written_chunks": [s["written_chunks"] for s in sums]}

@@ -175,6 +175,14 @@ kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std
                             std::vector<uint64_t>* out_digests, uint64_t* out_snapshot, uint64_t* d_hash_out,
                             cudaStream_t s);
 
+// kc_validate with an option to merge every region's W into one report (F4 sequences)
+kc_status validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n, const kc_tolerance* tol,
+                        kc_diff_report* reps, size_t cap_reports, size_t* n_reports_out, uint64_t* unexpected_chunks,
+                        bool merge);
+// re-point a restored handle at another snapshot of the same regions (dispatch,
+// W, post manifest, stashes) without touching the mapped memory (F4 sequences)
+kc_status restored_rebind(kc_ctx* ctx, kc_restored* h, const kc_snapshot* sn);
+
 }  // namespace kc
 
 #define KC_CHECK_CUDA(ctx, expr, what)                                  \

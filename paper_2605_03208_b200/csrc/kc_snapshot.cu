@@ -28,6 +28,7 @@
 
 #include "kc_internal.h"
 #include "kc_json.h"
+#include "kc_snapshot_types.h"
 
 using namespace kc;
 
@@ -979,31 +980,9 @@ static std::string maps_overlapping(uint64_t lo, uint64_t hi) {
 }
 
 // ====================================================================== restore core
-// A snapshot's contents independent of where the bytes live (files or a
-// device arena); restore_core maps the captured VAs and pulls the bytes
+// SnapDesc (kc_snapshot_types.h) is a snapshot's contents independent of where
+// the bytes live; restore_core maps the captured VAs and pulls the bytes
 // through a RestoreSource.
-struct SnapRegion {
-    kc_region r;
-    std::string hx;
-    bool ok = true;
-    uint64_t n_chunks = 0;
-    uint64_t digest = 0, post_digest = 0;
-    std::vector<uint64_t> manifest;       // manifest of the stored bytes
-    std::vector<uint64_t> post_manifest;  // post-dispatch manifest
-    std::vector<uint64_t> written;        // W chunk indices
-};
-
-struct SnapDesc {
-    int mode = KC_MODE_PRE_W;
-    std::string mangled;
-    uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0;
-    std::vector<uint8_t> kernarg, image;
-    std::vector<std::pair<size_t, size_t>> layout;  // kernarg (offset, size)
-    std::vector<SnapRegion> regions;                 // ascending base
-    uint64_t snapshot_digest = 0;
-    std::vector<ModVarState> modvars;                // F3
-};
-
 struct RestoreSource {
     virtual ~RestoreSource() {}
     // stored bytes of every ok region -> its (mapped, zero-filled) VA
@@ -1141,10 +1120,8 @@ struct FileSource : RestoreSource {
 
 }  // namespace
 
-static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src, kc_restored** out,
-                              kc_restore_report* rep_out, kc_restore_report& rep, double t0) {
-    kc_restored* h = new kc_restored();
-    h->ctx = ctx;  // rollback() returns heap spans to this ctx
+// the dispatch a restored handle replays: launch shape, kernarg, code object, F3 variables
+static void bind_dispatch_fields(kc_restored* h, const SnapDesc& d) {
     h->mode = d.mode;
     h->mangled = d.mangled;
     for (int i = 0; i < 3; ++i) {
@@ -1155,6 +1132,53 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     h->kernarg = d.kernarg;
     h->image = d.image;
     h->modvars = d.modvars;
+}
+
+// device stashes of the written chunks: replay recopy (pre-state, from the live
+// memory as it is now) and validation reference (captured post bytes)
+static kc_status build_stash(kc_ctx* ctx, kc_restored* h, const SnapDesc& d, RestoreSource& src) {
+    uint64_t total = 0;
+    for (auto& rr : h->regions) {
+        rr.stash_off.clear();
+        for (uint64_t k : rr.written) {
+            rr.stash_off.push_back(total);
+            total += std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
+        }
+    }
+    h->stash_bytes = total;
+    if (!total) return KC_OK;
+    if (cudaMalloc(&h->stash_pre, total) != cudaSuccess || cudaMalloc(&h->stash_ref, total) != cudaSuccess)
+        return set_err(ctx, KC_ERR_NOMEM, "kc_restore: stash of %llu bytes", (unsigned long long)total);
+    for (size_t i = 0; i < h->regions.size(); ++i) {
+        auto& rr = h->regions[i];
+        if (!rr.ok || rr.written.empty()) continue;
+        uint64_t wbytes = 0;
+        for (size_t j = 0; j < rr.written.size(); ++j) {
+            const uint64_t k = rr.written[j];
+            const uint64_t len = std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
+            cudaMemcpyAsync((uint8_t*)h->stash_pre + rr.stash_off[j], (const void*)(rr.r.base + k * kChunk), len,
+                            cudaMemcpyDeviceToDevice, ctx->copy_stream);
+            if (h->mode != KC_MODE_PRE_W)
+                cudaMemcpyAsync((uint8_t*)h->stash_ref + rr.stash_off[j], (const void*)(rr.r.base + k * kChunk),
+                                len, cudaMemcpyDeviceToDevice, ctx->copy_stream);
+            wbytes += len;
+        }
+        if (h->mode == KC_MODE_PRE_W) {
+            cudaStreamSynchronize(ctx->copy_stream);
+            kc_status st = src.written_ref(ctx, d, i, (uint8_t*)h->stash_ref + rr.stash_off[0], wbytes);
+            if (st != KC_OK) return st;
+        }
+    }
+    cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+    if (ce != cudaSuccess) return cuda_err(ctx, ce, "kc_restore: stash");
+    return KC_OK;
+}
+
+static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src, kc_restored** out,
+                              kc_restore_report* rep_out, kc_restore_report& rep, double t0) {
+    kc_restored* h = new kc_restored();
+    h->ctx = ctx;  // rollback() returns heap spans to this ctx
+    bind_dispatch_fields(h, d);
     std::vector<ParsedRegion> regs;
     for (auto& sr : d.regions) {
         kc_restored_region rr;
@@ -1385,51 +1409,11 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     }
 
     // ---- device stashes of the written chunks: replay recopy (pre) and validation reference (post)
-    uint64_t total = 0;
-    for (auto& rr : h->regions) {
-        rr.stash_off.clear();
-        for (uint64_t k : rr.written) {
-            rr.stash_off.push_back(total);
-            total += std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
-        }
-    }
-    h->stash_bytes = total;
-    if (total) {
-        if (cudaMalloc(&h->stash_pre, total) != cudaSuccess || cudaMalloc(&h->stash_ref, total) != cudaSuccess) {
-            rollback(h);
-            delete h;
-            return set_err(ctx, KC_ERR_NOMEM, "kc_restore: stash of %llu bytes", (unsigned long long)total);
-        }
-        for (size_t i = 0; i < h->regions.size(); ++i) {
-            auto& rr = h->regions[i];
-            if (!rr.ok || rr.written.empty()) continue;
-            uint64_t wbytes = 0;
-            for (size_t j = 0; j < rr.written.size(); ++j) {
-                const uint64_t k = rr.written[j];
-                const uint64_t len = std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
-                cudaMemcpyAsync((uint8_t*)h->stash_pre + rr.stash_off[j], (const void*)(rr.r.base + k * kChunk), len,
-                                cudaMemcpyDeviceToDevice, ctx->copy_stream);
-                if (h->mode != KC_MODE_PRE_W)
-                    cudaMemcpyAsync((uint8_t*)h->stash_ref + rr.stash_off[j], (const void*)(rr.r.base + k * kChunk),
-                                    len, cudaMemcpyDeviceToDevice, ctx->copy_stream);
-                wbytes += len;
-            }
-            if (h->mode == KC_MODE_PRE_W) {
-                cudaStreamSynchronize(ctx->copy_stream);
-                st = src.written_ref(ctx, d, i, (uint8_t*)h->stash_ref + rr.stash_off[0], wbytes);
-                if (st != KC_OK) {
-                    rollback(h);
-                    delete h;
-                    return st;
-                }
-            }
-        }
-        ce = cudaStreamSynchronize(ctx->copy_stream);
-        if (ce != cudaSuccess) {
-            rollback(h);
-            delete h;
-            return cuda_err(ctx, ce, "kc_restore: stash");
-        }
+    st = build_stash(ctx, h, d, src);
+    if (st != KC_OK) {
+        rollback(h);
+        delete h;
+        return st;
     }
     rep.t_total_s = now_s() - t0;
     if (rep_out) *rep_out = rep;
@@ -1463,48 +1447,7 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
 // the new snapshot references the base's bytes (shared ownership of the base
 // arenas, so a base may be freed first).  Hash equality as "unchanged" is the
 // method's own reading: W (A4) declares a chunk unwritten on the same test.
-
-// One arena allocation, freed (or, pinned host, parked in the ctx cache) when
-// the last snapshot referencing it goes.
-struct ArenaBuf {
-    kc_ctx* ctx = nullptr;
-    void* p = nullptr;
-    uint64_t cap = 0;
-    bool host = false;
-    ~ArenaBuf() {
-        if (!p) return;
-        if (ctx) bind_device(ctx);
-        if (!host) {
-            cudaFree(p);
-        } else if (ctx && cap >= ctx->host_arena_bytes) {  // park the larger arena
-            if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
-            ctx->host_arena = p;
-            ctx->host_arena_bytes = cap;
-        } else {
-            cudaFreeHost(p);
-        }
-    }
-};
-
-struct kc_snapshot {
-    kc_ctx* ctx = nullptr;
-    bool host = false;  // arenas in pinned host memory (kc_capture_host)
-    SnapDesc desc;
-    std::shared_ptr<ArenaBuf> arena;                // this snapshot's own stored bytes
-    uint64_t arena_bytes = 0;                       // bytes used in it
-    std::vector<std::shared_ptr<ArenaBuf>> deps;    // base arenas referenced by runs
-    struct Run {
-        uint64_t roff, len;  // region byte range (chunk aligned)
-        uint64_t src;        // where its stored bytes are (own arena or a base's)
-    };
-    std::vector<std::vector<Run>> runs;  // per region, ascending roff, covering ok regions
-    uint64_t shared_bytes = 0;           // stored bytes referenced from base snapshots
-    void* warena = nullptr;              // PRE_W: post bytes of W, region i at w_off[i]
-    uint64_t w_bytes = 0;
-    std::vector<uint64_t> w_off;
-    kc_capture_report rep;
-};
-
+// (ArenaBuf / kc_snapshot: kc_snapshot_types.h.)
 namespace {
 
 // copies of (src, dst, len) ranges between device memory and the device or pinned
@@ -2209,9 +2152,12 @@ extern "C" kc_status kc_validate_module_vars(kc_ctx* ctx, const kc_restored* h, 
 }
 
 // ====================================================================== validate
-extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n,
-                                 const kc_tolerance* tol, kc_diff_report* reps, size_t cap_reports,
-                                 size_t* n_reports_out, uint64_t* unexpected_chunks) {
+// merge: (outs == NULL only) one report over the W chunks of every region, its
+// bitmap indexed by global chunk (regions in order) -- the per-dispatch report
+// of a sequence replay (kc_replay_seq)
+kc_status kc::validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n, const kc_tolerance* tol,
+                            kc_diff_report* reps, size_t cap_reports, size_t* n_reports_out,
+                            uint64_t* unexpected_chunks, bool merge) {
     if (!ctx || !h) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -2222,12 +2168,27 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
     void* typed_ref = nullptr;
     if (!outs) {
         // every region with written chunks, bytes, reference = captured post bytes of W
+        uint64_t gchunk = 0;  // merge: global chunk index of the region's chunk 0
+        if (merge) {
+            uint64_t all = 0, tot = 0;
+            for (auto& rr : h->regions) {
+                all += rr.n_chunks;
+                if (rr.ok && !rr.written.empty()) tot += rr.r.size;
+            }
+            rep_nbytes.push_back(tot);
+            word0.push_back(0);
+            words = (all + 63) / 64;
+        }
         for (auto& rr : h->regions) {
+            const uint64_t c0 = gchunk;
+            gchunk += rr.n_chunks;
             if (!rr.ok || rr.written.empty()) continue;
-            const int rid = (int)rep_nbytes.size();
-            rep_nbytes.push_back(rr.r.size);
-            word0.push_back(words);
-            words += (rr.n_chunks + 63) / 64;
+            const int rid = merge ? 0 : (int)rep_nbytes.size();
+            if (!merge) {
+                rep_nbytes.push_back(rr.r.size);
+                word0.push_back(words);
+                words += (rr.n_chunks + 63) / 64;
+            }
             for (size_t j = 0; j < rr.written.size(); ++j) {
                 const uint64_t k = rr.written[j];
                 kc_buffer b;
@@ -2236,10 +2197,11 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
                 b.nbytes = std::min<uint64_t>(kChunk, rr.r.size - k * kChunk);
                 b.dtype = KC_DT_BYTES;
                 b.report = rid;
-                b.bitmap_chunk0 = k;
+                b.bitmap_chunk0 = merge ? c0 + k : k;
                 segs.push_back(b);
             }
         }
+        if (merge && segs.empty()) rep_nbytes.clear();  // nothing written: no report
     } else {
         // typed sub-ranges: rebuild the captured post-dispatch bytes of each range
         uint64_t total = 0;
@@ -2350,4 +2312,44 @@ extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* o
         *unexpected_chunks = bad;
     }
     return KC_OK;
+}
+
+extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n,
+                                 const kc_tolerance* tol, kc_diff_report* reps, size_t cap_reports,
+                                 size_t* n_reports_out, uint64_t* unexpected_chunks) {
+    return validate_impl(ctx, h, outs, n, tol, reps, cap_reports, n_reports_out, unexpected_chunks, false);
+}
+
+// F4 sequences: point a restored handle at the next dispatch of a sequence
+// whose state the live memory already holds (the replay of the previous
+// dispatches); nothing is remapped or copied in
+kc_status kc::restored_rebind(kc_ctx* ctx, kc_restored* h, const kc_snapshot* sn) {
+    if (!ctx || !h || !sn) return KC_ERR_ARG;
+    const SnapDesc& d = sn->desc;
+    if (d.regions.size() != h->regions.size())
+        return set_err(ctx, KC_ERR_ARG, "rebind: the snapshot has %zu regions, the restored state %zu",
+                       d.regions.size(), h->regions.size());
+    for (size_t i = 0; i < d.regions.size(); ++i)
+        if (d.regions[i].r.base != h->regions[i].r.base || d.regions[i].r.size != h->regions[i].r.size ||
+            d.regions[i].ok != h->regions[i].ok)
+            return set_err(ctx, KC_ERR_ARG, "rebind: region %zu differs from the restored state", i);
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    cudaDeviceSynchronize();
+    if (h->module) KC_DRV(cuModuleUnload)(h->module);
+    h->module = nullptr;
+    if (h->stash_pre) cudaFree(h->stash_pre);
+    if (h->stash_ref) cudaFree(h->stash_ref);
+    h->stash_pre = h->stash_ref = nullptr;
+    h->stash_bytes = 0;
+    bind_dispatch_fields(h, d);
+    for (size_t i = 0; i < d.regions.size(); ++i) {
+        h->regions[i].written = d.regions[i].written;
+        h->regions[i].post_manifest = d.regions[i].post_manifest;
+    }
+    h->dev_snap = sn;
+    h->modvar_checked = h->modvar_mismatch = 0;
+    kc_status st = ensure_stream(ctx);
+    if (st != KC_OK) return st;
+    DevSource src(sn);
+    return build_stash(ctx, h, d, src);
 }

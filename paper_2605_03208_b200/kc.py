@@ -43,7 +43,9 @@ EXPORTED = [
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
     "kc_capture_incr", "kc_snapshot_shared_bytes", "kc_validate_module_vars",
+    "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
 ]
+KC_DEP_RAW, KC_DEP_WAW, KC_DEP_WAR = 1, 2, 4
 
 
 class KcError(RuntimeError):
@@ -133,6 +135,23 @@ class RestoreReport(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class SeqReplayOpts(ctypes.Structure):
+    _fields_ = [("first", ctypes.c_size_t), ("count", ctypes.c_size_t),
+                ("image_overrides", ctypes.POINTER(ctypes.c_void_p)), ("image_override_sizes", ctypes.POINTER(ctypes.c_size_t)),
+                ("tol", Tolerance), ("stream", ctypes.c_void_p)]
+
+
+class SeqStepReport(ctypes.Structure):
+    _fields_ = [("w", DiffReport), ("unexpected_chunks", ctypes.c_uint64), ("inherited_chunks", ctypes.c_uint64),
+                ("modvar_mismatch", ctypes.c_uint64), ("kernel_ms", ctypes.c_double), ("pass_", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {"w": self.w.as_dict(), "unexpected_chunks": self.unexpected_chunks,
+                "inherited_chunks": self.inherited_chunks,
+                "modvar_mismatch": self.modvar_mismatch, "kernel_ms": self.kernel_ms, "pass": self.pass_}
+
+
 # ----------------------------------------------------------------- loading
 _lib = None
 
@@ -189,6 +208,13 @@ def lib() -> ctypes.CDLL:
                                  P(CaptureReport)]),
         "kc_snapshot_shared_bytes": (U64, [V]),
         "kc_validate_module_vars": (st, [V, V, P(U64), P(U64)]),
+        "kc_capture_seq": (st, [V, P(Dispatch), SZ, P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
+        "kc_seq_length": (SZ, [V]),
+        "kc_seq_step": (V, [V, SZ]),
+        "kc_seq_deps": (st, [V, P(ctypes.c_uint8), SZ]),
+        "kc_seq_save": (st, [V, V, ctypes.c_char_p]),
+        "kc_seq_free": (None, [V]),
+        "kc_replay_seq": (st, [V, V, P(SeqReplayOpts), P(SeqStepReport), P(V)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -305,6 +331,7 @@ class DevSnapshot:
     a pinned host arena (capture_host)."""
     handle: int
     ctx: "Context"
+    borrowed: bool = False   # a sequence step: owned by the kc_sequence
 
     def nbytes(self) -> int:
         return int(lib().kc_snapshot_bytes(self.handle))
@@ -320,9 +347,41 @@ class DevSnapshot:
         self.ctx._check(lib().kc_snapshot_save(self.ctx.handle, self.handle, directory.encode()), "kc_snapshot_save")
 
     def free(self):
-        if self.handle:
+        if self.handle and not self.borrowed:
             lib().kc_snapshot_free(self.handle)
-            self.handle = 0
+        self.handle = 0
+
+
+class Sequence:
+    """kc_sequence handle (F4 multi-kernel capture): one in-memory PRE_W snapshot per step."""
+
+    def __init__(self, handle: int, ctx: "Context"):
+        self.handle, self.ctx = handle, ctx
+
+    def __len__(self) -> int:
+        return int(lib().kc_seq_length(self.handle))
+
+    def step(self, k: int) -> "DevSnapshot":
+        """Step k's snapshot, BORROWED (owned by the sequence: do not free it)."""
+        h = lib().kc_seq_step(self.handle, k)
+        if not h:
+            raise IndexError(k)
+        return DevSnapshot(h, self.ctx, borrowed=True)
+
+    def deps(self) -> list:
+        """n x n matrix: deps[j][i] = KC_DEP_* flags of step j on step i < j."""
+        n = len(self)
+        buf = (ctypes.c_uint8 * max(1, n * n))()
+        self.ctx._check(lib().kc_seq_deps(self.handle, buf, n * n), "kc_seq_deps")
+        return [[int(buf[j * n + i]) for i in range(n)] for j in range(n)]
+
+    def save(self, directory: str) -> None:
+        self.ctx._check(lib().kc_seq_save(self.ctx.handle, self.handle, directory.encode()), "kc_seq_save")
+
+    def free(self):
+        if self.handle:
+            lib().kc_seq_free(self.handle)
+            self.handle = None
 
 
 class Context:
@@ -538,6 +597,42 @@ class Context:
         rep = ReplayReport()
         self._check(lib().kc_replay(self._h, restored.handle, ctypes.byref(o), ctypes.byref(rep)), "kc_replay")
         return rep.as_dict()
+
+    def capture_seq(self, dispatches: Sequence[dict], regions=None, host: bool = False
+                    ) -> tuple["Sequence", list]:
+        """kc_capture_seq: dispatches = [dict(image=, mangled=, grid=, block=, smem=, kernarg=, stream=, func=)]."""
+        keep = []
+        arr = (Dispatch * len(dispatches))()
+        for i, d in enumerate(dispatches):
+            arr[i], k = self._dispatch(d.get("image"), d.get("mangled"), d.get("grid", (1, 1, 1)),
+                                       d.get("block", (1, 1, 1)), d.get("smem", 0), d.get("kernarg", b""),
+                                       d.get("stream", 0), d.get("func", 0))
+            keep.append(k)
+        reps = (CaptureReport * len(dispatches))()
+        h = ctypes.c_void_p()
+        rg = _regions(regions) if regions is not None else None
+        rc = lib().kc_capture_seq(self._h, arr, len(dispatches), rg, len(regions) if regions is not None else 0,
+                                  int(host), ctypes.byref(h), reps)
+        self._check(rc, "kc_capture_seq", ok=(KC_OK, KC_PARTIAL))
+        return Sequence(h.value, self), [r.as_dict() for r in reps]
+
+    def replay_seq(self, seq: "Sequence", first: int = 0, count: int | None = None, overrides=None,
+                   atol: float = 1e-8, rtol: float = 1e-5, equal_nan: bool = False, stream: int = 0,
+                   keep: bool = False):
+        """kc_replay_seq: joint replay of steps [first, first+count); overrides = list of code objects
+        (bytes or None) per replayed step.  Returns (step reports, Restored or None)."""
+        n = len(seq)
+        count = n - first if count is None else count
+        bufs = [ctypes.create_string_buffer(b, len(b)) if b else None for b in (overrides or [])]
+        ov = None
+        if overrides is not None:
+            ov = (ctypes.c_void_p * max(1, count))(*[ctypes.cast(b, ctypes.c_void_p) if b else None for b in bufs])
+        o = SeqReplayOpts(first, count, ov, None, Tolerance(atol, rtol, int(bool(equal_nan)), 0), stream or None)
+        reps = (SeqStepReport * max(1, count))()
+        h = ctypes.c_void_p()
+        self._check(lib().kc_replay_seq(self._h, seq.handle, ctypes.byref(o), reps, ctypes.byref(h) if keep else None),
+                    "kc_replay_seq")
+        return [reps[i].as_dict() for i in range(count)], (Restored(h.value, self) if keep else None)
 
     def validate_module_vars(self, restored: Restored) -> tuple[int, int]:
         """F3: (variables checked, variables differing from their captured post value) of the last replay."""

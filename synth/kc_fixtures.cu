@@ -21,7 +21,8 @@ struct KcNode {
 
 // F1 / F1': pointer-chasing linked-list walk (config c1).  Each thread walks
 // one list from heads[i]; out[(va - nodes_base)/16] = running sum; mutate=1
-// also rewrites value <- 3*value + 1 in place (the capture-mode probe).
+// also rewrites value <- 3*value + 1 in place (the capture-mode probe; the
+// KC_VARIANT_DELTA variant adds DELTA to both the sums and the rewrite).
 extern "C" __global__ void kc_fixture_walk(const unsigned long long* __restrict__ heads, unsigned long long* out,
                                            unsigned long long nodes_base, unsigned int n_lists, int mutate) {
     const unsigned int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -33,7 +34,7 @@ extern "C" __global__ void kc_fixture_walk(const unsigned long long* __restrict_
         const unsigned int v = nd->value;
         acc += v + KC_VARIANT_DELTA;
         out[(va - nodes_base) / 16] = acc;
-        if (mutate) nd->value = v * 3u + 1u;
+        if (mutate) nd->value = v * 3u + 1u + KC_VARIANT_DELTA;
         va = nd->next;
     }
 }
@@ -128,4 +129,12 @@ extern "C" __global__ void kc_fixture_modvar(unsigned long long* out, unsigned i
     if (i >= n) return;
     out[i] = (unsigned long long)((float)kc_fixture_cvals[i & 7] * kc_fixture_scale) + i;
     atomicAdd(&kc_fixture_hits, 1ull);
+}
+
+// F4 sequences: an elementwise step independent of the list walk,
+// y[i] = a * x[i] + y[i] (u32, modulo 2^32: exact, so the oracle check is exact).
+extern "C" __global__ void kc_fixture_axpy_u32(const unsigned int* __restrict__ x, unsigned int* __restrict__ y,
+                                               unsigned int n, unsigned int a) {
+    const unsigned int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = a * x[i] + y[i] + KC_VARIANT_DELTA;
 }
