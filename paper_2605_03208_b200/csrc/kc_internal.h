@@ -15,7 +15,7 @@
 // Driver-API entry points resolved through cudart (cudaGetDriverEntryPoint),
 // so libkc.so has no link-time dependency on libcuda and loads on hosts
 // without a GPU driver (calls then fail with KC_ERR_CUDA).
-#define KC_DRV_FUNCS(X) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemFree) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
+#define KC_DRV_FUNCS(X) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemFree) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
 namespace kc {
 struct Drv {
 #define KC_DRV_DECL(f) decltype(&::f) f = nullptr;
@@ -60,7 +60,7 @@ struct kc_ctx {
     uint64_t unknown_frees = 0;
 
     // cached device tables / scratch (stream-ordered; one stream at a time per ctx)
-    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map;
+    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map, dst_tab, gather_tab;
     std::vector<kc::RegionDev> regs_cached;
     kc_ctx_dev_buf pairs, pair_map, dirty;  // F2 (K5) pair table, chunk -> pair map, dirty bitmap
     std::vector<kc::PairDev> pairs_cached;
@@ -171,9 +171,12 @@ uint64_t heap_alloc(kc_ctx* ctx, uint64_t size);
 void heap_put(kc_ctx* ctx, uint64_t base, uint64_t size);
 
 // snapshot format helpers (kc_snapshot.cu)
+// h_dst (one arena address per region): the fused K6 pass, which also copies the bytes there
 kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std::vector<uint64_t>& out_hashes,
                             std::vector<uint64_t>* out_digests, uint64_t* out_snapshot, uint64_t* d_hash_out,
-                            cudaStream_t s);
+                            cudaStream_t s, const uint64_t* h_dst = nullptr);
+kc_status hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_chunk_hash, uint64_t* d_region_digest,
+                    uint64_t* d_snapshot_digest, void* stream, const uint64_t* h_dst);
 
 // kc_validate with an option to merge every region's W into one report (F4 sequences)
 kc_status validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n, const kc_tolerance* tol,

@@ -363,10 +363,20 @@ struct CpCfg {
     static constexpr size_t kSmem = (size_t)WARPS * STAGES * kWStage;
 };
 
-template <class CFG>
+// COPY (K6, the fused capture pass): the staged slices are also written to the
+// snapshot arena (dst[r] = arena address of region r's byte 0) with streaming
+// 16-byte stores, so one HBM read of every region yields both its manifest and
+// its stored copy.  Each 1 KiB slice is written by two warp-wide 512 B rows.
+__device__ __forceinline__ void st_cs16(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+template <class CFG, bool COPY = false>
 __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     k1_hash_cpasync(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out,
-                    const uint32_t* __restrict__ map) {
+                    const uint32_t* __restrict__ map, const unsigned long long* __restrict__ dst = nullptr) {
+    static_assert(!COPY || CFG::kUPC % 32 == 0, "K6 copy-out maps copy unit k to chunk 32k / UPC");
     constexpr int WARPS = CFG::kWarps, STAGES = CFG::kStages, SL = CFG::kSlice, PITCH = CFG::kPitch;
     constexpr int WSTAGE = CFG::kWStage, UPC = CFG::kUPC, UPL = CFG::kUPL;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -442,6 +452,12 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         if (g < C) cr = chunk_ref(regs, nreg, g, map);
         const uint32_t nst = cr.len >= 32 ? cr.len / 32 : 0;
         const uint32_t nsl = __reduce_max_sync(0xFFFFFFFFu, (nst * 32 + SL - 1) / SL);
+        // K6: arena address of this quad's chunk (0 past the end)
+        unsigned long long cdst = 0;
+        if (COPY && g < C) {
+            const int r = map ? (int)__ldg(map + g) : find_region(regs, nreg, g);
+            cdst = dst[r] + (g - regs[r].chunk_off) * kChunk;
+        }
         uint64_t v = lane_seed(ql);
         for (uint32_t s = 0; s < nsl; ++s, ++step) {
             cp_async_wait<STAGES - 2>();
@@ -456,12 +472,28 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             } else {
                 for (uint32_t t = 0; t < n; ++t) v = xround_fast(v, p[4 * t]);
             }
+            if (COPY) {  // the stage's 8 slices -> the arena, before the slot is refilled
+#pragma unroll
+                for (int k = 0; k < UPL; ++k) {
+                    const int qq = (32 * k) / UPC;
+                    const int off = ((32 * k) % UPC + lane) * 16;
+                    const unsigned long long d = __shfl_sync(0xFFFFFFFFu, cdst, 4 * qq);
+                    const uint32_t b = __shfl_sync(0xFFFFFFFFu, nst * 32, 4 * qq);
+                    const uint32_t g_off = s * SL + off;
+                    if (g_off < b)
+                        st_cs16(reinterpret_cast<uint8_t*>(d) + g_off,
+                                *reinterpret_cast<const uint4*>(wring + st * WSTAGE + qq * PITCH + off));
+                }
+            }
             __syncwarp();
             fetch((step + STAGES - 1) % STAGES);
         }
         if (g < C) {
             const uint64_t h = quad_finish<true>(v, ql, qmask, cr.len, cr.src + (size_t)nst * 32);
             if (ql == 0) out[g] = h;
+            if (COPY && ql == 0)  // the sub-32-byte tail is hashed from global, copy it the same way
+                for (uint32_t b = nst * 32; b < cr.len; ++b)
+                    reinterpret_cast<uint8_t*>(cdst)[b] = cr.src[b];
         } else {
             quad_finish<true>(v, ql, qmask, 0, nullptr);
         }
@@ -1363,6 +1395,9 @@ cudaError_t kernels_init() {
     KC_CP_ATTR(CpA) KC_CP_ATTR(CpD)
 #undef KC_CP_ATTR
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k1_hash_cpasync<CpA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)CpA::kSmem);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
     return e;
 }
@@ -1387,10 +1422,14 @@ static void launch_tma(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* 
 
 template <class CFG>
 static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
-                      int num_sms, cudaStream_t s) {
+                      int num_sms, cudaStream_t s, const unsigned long long* d_dst = nullptr) {
     const uint64_t groups = (C + 7) / 8;
     const uint64_t grid = std::min<uint64_t>((groups + CFG::kWarps - 1) / CFG::kWarps, (uint64_t)num_sms);
-    k1_hash_cpasync<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map);
+    if (d_dst)
+        k1_hash_cpasync<CFG, true><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map,
+                                                                                       d_dst);
+    else
+        k1_hash_cpasync<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map);
 }
 
 // K1 variant selection (KC_K1_VARIANT, tuning knob; default = the measured best)
@@ -1418,6 +1457,13 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
         case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         default: launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hash_copy(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out,
+                             const unsigned long long* d_dst, const uint32_t* map, int num_sms, cudaStream_t s) {
+    if (C == 0) return cudaSuccess;
+    launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, d_dst);
     return cudaGetLastError();
 }
 

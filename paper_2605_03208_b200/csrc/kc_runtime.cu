@@ -325,7 +325,7 @@ void kc_destroy(kc_ctx* ctx) {
     if (ctx->heap_base) KC_DRV(cuMemAddressFree)((CUdeviceptr)ctx->heap_base, ctx->heap_size);
     if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch, &ctx->pairs, &ctx->pair_map, &ctx->dirty,
-                              &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map})
+                              &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map, &ctx->dst_tab, &ctx->gather_tab})
         if (b->p) cudaFree(b->p);
     for (auto& w : ctx->io) {
         for (void* p : w.pinned) cudaFreeHost(p);
@@ -508,6 +508,15 @@ static kc_status upload_regions(kc_ctx* ctx, const kc_region* regions, size_t n,
 
 kc_status kc_hash(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_chunk_hash, uint64_t* d_region_digest,
                   uint64_t* d_snapshot_digest, void* stream) {
+    return kc::hash_impl(ctx, regions, n, d_chunk_hash, d_region_digest, d_snapshot_digest, stream, nullptr);
+}
+
+}  // extern "C"
+
+// kc_hash, and with h_dst (host array: arena address per region) the fused
+// capture pass K6 that also copies every region byte to its arena address
+kc_status kc::hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_chunk_hash,
+                        uint64_t* d_region_digest, uint64_t* d_snapshot_digest, void* stream, const uint64_t* h_dst) {
     KC_ENTER(ctx);
     if (n && !regions) return set_err(ctx, KC_ERR_ARG, "kc_hash: regions is NULL");
     for (size_t i = 0; i < n; ++i) {
@@ -520,9 +529,22 @@ kc_status kc_hash(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_c
     kc_status st = upload_regions(ctx, regions, n, s, &C);
     if (st != KC_OK) return st;
     if (C && !d_chunk_hash) return set_err(ctx, KC_ERR_ARG, "kc_hash: d_chunk_hash is NULL");
-    KC_CHECK_CUDA(ctx, launch_hash((const RegionDev*)ctx->regs.p, (int)n, C, ctx->regs_aligned, d_chunk_hash,
-                                   (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s),
-                  "launch K1");
+    if (h_dst) {
+        if (!ctx->regs_aligned) return set_err(ctx, KC_ERR_ARG, "K6: regions must be 16-byte aligned");
+        for (size_t i = 0; i < n; ++i)
+            if (h_dst[i] & 15) return set_err(ctx, KC_ERR_ARG, "K6: arena address %zu not 16-byte aligned", i);
+        KC_CHECK_CUDA(ctx, ensure(ctx->dst_tab, std::max<size_t>(1, n) * 8), "cudaMalloc(arena table)");
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->dst_tab.p, h_dst, n * 8, cudaMemcpyHostToDevice, s),
+                      "upload arena table");
+        KC_CHECK_CUDA(ctx, launch_hash_copy((const RegionDev*)ctx->regs.p, (int)n, C, d_chunk_hash,
+                                            (const unsigned long long*)ctx->dst_tab.p,
+                                            (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s),
+                      "launch K6");
+    } else {
+        KC_CHECK_CUDA(ctx, launch_hash((const RegionDev*)ctx->regs.p, (int)n, C, ctx->regs_aligned, d_chunk_hash,
+                                       (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s),
+                      "launch K1");
+    }
     if (C) ctx->launches += 1;
     if (d_region_digest || d_snapshot_digest) {
         if (d_snapshot_digest)
@@ -536,6 +558,8 @@ kc_status kc_hash(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_c
     }
     return KC_OK;
 }
+
+extern "C" {
 
 // ------------------------------------------------------------------ K3
 kc_status kc_written(kc_ctx* ctx, const uint64_t* d_pre, const uint64_t* d_post, uint64_t n_chunks,

@@ -469,12 +469,23 @@ struct RegionState {
 
 }  // namespace
 
+namespace {
+// A dispatch launched with more than 48 KiB of dynamic shared memory needs the
+// function's opt-in attribute; the application set it on its own CUfunction,
+// a module the closure loads itself (capture from an image, replay) must set it
+// again before launching with the captured smem size.
+CUresult allow_dynamic_smem(CUfunction f, uint32_t smem) {
+    if (smem <= 48u * 1024u) return CUDA_SUCCESS;
+    return KC_DRV(cuFuncSetAttribute)(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+}
+}  // namespace
+
 namespace kc {
 
 // Hash a region list (all must be live) and bring the manifest (and digests) to the host.
 kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std::vector<uint64_t>& out_hashes,
                             std::vector<uint64_t>* out_digests, uint64_t* out_snapshot, uint64_t* d_hash_out,
-                            cudaStream_t s) {
+                            cudaStream_t s, const uint64_t* h_dst) {
     const uint64_t C = kc_count_chunks(regs.data(), regs.size());
     uint64_t* d_h = d_hash_out;
     if (!d_h) {
@@ -489,7 +500,7 @@ kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std
         d_dig = (uint64_t*)dig.p;
         d_snap = d_dig + regs.size();
     }
-    kc_status st = kc_hash(ctx, regs.data(), regs.size(), d_h, d_dig, out_snapshot ? d_snap : nullptr, s);
+    kc_status st = hash_impl(ctx, regs.data(), regs.size(), d_h, d_dig, out_snapshot ? d_snap : nullptr, s, h_dst);
     if (st != KC_OK) {
         if (dig.p) cudaFree(dig.p);
         return st;
@@ -547,6 +558,11 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
         if (r != CUDA_SUCCESS) {
             KC_DRV(cuModuleUnload)(own_mod);
             return set_err(ctx, KC_ERR_ARG, "kc_capture: symbol %s not found in image", d->mangled);
+        }
+        r = allow_dynamic_smem(f, d->smem_bytes);
+        if (r != CUDA_SUCCESS) {
+            KC_DRV(cuModuleUnload)(own_mod);
+            return cu_err(ctx, r, "kc_capture: dynamic shared memory attribute");
         }
     }
     std::string mangled = d->mangled ? d->mangled : "";
@@ -991,6 +1007,14 @@ struct RestoreSource {
     virtual kc_status written_ref(kc_ctx* ctx, const SnapDesc& d, size_t i, void* dst, uint64_t bytes) = 0;
     // the copy-in streams through the pinned staging ring (file sources)
     virtual bool needs_staging() const { return true; }
+    // optional fused copy-in + verify: copies every ok region and returns the
+    // chunk hashes of the bytes it copied (ok regions in order); *done = false
+    // when the source cannot (then copy_in + a K1 pass over the regions run)
+    virtual kc_status copy_in_verify(kc_ctx*, const SnapDesc&, kc_restore_report&, std::vector<uint64_t>&,
+                                     bool& done) {
+        done = false;
+        return KC_OK;
+    }
 };
 
 namespace {
@@ -1364,7 +1388,10 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
         }
     }
     cudaStreamSynchronize(ctx->copy_stream);  // zero-fill before the copy-in streams
-    st = src.copy_in(ctx, d, rep);
+    std::vector<uint64_t> got;
+    bool verified = false;  // the copy-in produced the verify hashes itself (K6)
+    st = src.copy_in_verify(ctx, d, rep, got, verified);
+    if (st == KC_OK && !verified) st = src.copy_in(ctx, d, rep);
     cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
     if (st == KC_OK && ce != cudaSuccess) st = cuda_err(ctx, ce, "kc_restore: copy-in");
     if (st != KC_OK) {
@@ -1379,8 +1406,7 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     std::vector<kc_region> okregs;
     for (auto& rr : h->regions)
         if (rr.ok) okregs.push_back(rr.r);
-    std::vector<uint64_t> got;
-    st = hash_regions_sync(ctx, okregs, got, nullptr, nullptr, nullptr, ctx->copy_stream);
+    if (!verified) st = hash_regions_sync(ctx, okregs, got, nullptr, nullptr, nullptr, ctx->copy_stream);
     if (st != KC_OK) {
         rollback(h);
         delete h;
@@ -1469,9 +1495,8 @@ kc_status copy_ranges_d2d(kc_ctx* ctx, const std::vector<std::array<uint64_t, 3>
     }
     if (!src.empty()) {
         const size_t n = src.size();
-        kc_ctx_dev_buf tab;
-        KC_CHECK_CUDA(ctx, ensure(tab, 3 * 8 * n), "cudaMalloc(gather table)");
-        uint64_t* t = (uint64_t*)tab.p;
+        KC_CHECK_CUDA(ctx, ensure(ctx->gather_tab, 3 * 8 * n), "cudaMalloc(gather table)");  // kept by the ctx
+        uint64_t* t = (uint64_t*)ctx->gather_tab.p;
         cudaMemcpyAsync(t, src.data(), 8 * n, cudaMemcpyHostToDevice, s);
         cudaMemcpyAsync(t + n, dst.data(), 8 * n, cudaMemcpyHostToDevice, s);
         cudaMemcpyAsync(t + 2 * n, len.data(), 8 * n, cudaMemcpyHostToDevice, s);
@@ -1479,7 +1504,6 @@ kc_status copy_ranges_d2d(kc_ctx* ctx, const std::vector<std::array<uint64_t, 3>
         ctx->launches += 1;
         if (calls) ++*calls;
         cudaError_t e = cudaStreamSynchronize(s);
-        cudaFree(tab.p);
         if (e != cudaSuccess) return cuda_err(ctx, e, "K4 gather");
     }
     return KC_OK;
@@ -1489,6 +1513,34 @@ struct DevSource : RestoreSource {
     const kc_snapshot* sn;
     explicit DevSource(const kc_snapshot* s) : sn(s) {}
     bool needs_staging() const override { return false; }  // D2D / H2D straight from the arena
+    // K6 from a device arena: every ok region stored as one run (a full capture)
+    // is read once, hashed and written to its VA.  The hashes are those of the
+    // arena bytes copied; kc_validate's re-hash of every region after the replay
+    // (R31) re-reads what landed at the VAs.
+    kc_status copy_in_verify(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep, std::vector<uint64_t>& got,
+                             bool& done) override {
+        done = false;
+        if (sn->host || getenv("KC_NO_FUSED_RESTORE")) return KC_OK;
+        std::vector<kc_region> srcs;
+        std::vector<uint64_t> dst;
+        for (size_t i = 0; i < d.regions.size(); ++i) {
+            if (!d.regions[i].ok) continue;
+            const auto& runs = sn->runs[i];
+            if (runs.size() != 1 || runs[0].roff != 0 || runs[0].len != d.regions[i].r.size ||
+                (runs[0].src & 15) || (d.regions[i].r.base & 15))
+                return KC_OK;
+            kc_region r = d.regions[i].r;
+            r.base = runs[0].src;
+            srcs.push_back(r);
+            dst.push_back(d.regions[i].r.base);
+        }
+        kc_status st = hash_regions_sync(ctx, srcs, got, nullptr, nullptr, nullptr, ctx->copy_stream,
+                                         dst.empty() ? nullptr : dst.data());
+        if (st != KC_OK) return st;
+        for (const auto& r : srcs) rep.h2d_bytes += r.size;
+        done = true;
+        return KC_OK;
+    }
     kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) override {
         std::vector<std::array<uint64_t, 3>> ranges;
         for (size_t i = 0; i < d.regions.size(); ++i) {
@@ -1603,6 +1655,11 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
             KC_DRV(cuModuleUnload)(own_mod);
             return set_err(ctx, KC_ERR_ARG, "kc_capture_dev: symbol %s not found in image", d->mangled);
         }
+        const CUresult r = allow_dynamic_smem(f, d->smem_bytes);
+        if (r != CUDA_SUCCESS) {
+            KC_DRV(cuModuleUnload)(own_mod);
+            return cu_err(ctx, r, "kc_capture_dev: dynamic shared memory attribute");
+        }
     }
     kc_snapshot* sn = new kc_snapshot();
     sn->ctx = ctx;
@@ -1661,17 +1718,65 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     double t = now_s();
     std::vector<uint64_t> pre_h, pre_dig, post_h, post_dig;
     uint64_t pre_snap = 0, post_snap = 0;
-    kc_status st = hash_regions_sync(ctx, live, pre_h, &pre_dig, &pre_snap, nullptr, cs);
-    if (st != KC_OK) return fail(st);
-    rep.t_hash_pre_s = now_s() - t;
-    trace("regions + K1 pre", tl);
+    double t_copy = 0;
+    // Fused capture pass (K6): a full PRE_W capture into a device arena stores
+    // every live byte, so the plan does not depend on the hashes and one HBM
+    // read yields both the pre-manifest and the stored copy (KC_NO_FUSED_CAPTURE=1:
+    // K1 then copies, for comparison).
+    bool fused = !base && !host && mode == KC_MODE_PRE_W && !getenv("KC_NO_FUSED_CAPTURE");
+    for (auto& r : live) fused = fused && (r.base & 15) == 0;
+    kc_status st = KC_OK;
+    if (fused) {
+        st = ensure_stream(ctx);
+        if (st != KC_OK) return fail(st);
+        sn->runs.assign(D.regions.size(), {});
+        std::vector<uint64_t> aoff(D.regions.size(), 0);
+        uint64_t total = 0;
+        for (size_t i = 0; i < D.regions.size(); ++i) {
+            if (!D.regions[i].ok) continue;
+            total = (total + 255) / 256 * 256;
+            aoff[i] = total;
+            total += D.regions[i].r.size;
+        }
+        sn->arena_bytes = total;
+        std::vector<uint64_t> dst;
+        if (total) {
+            auto ab = std::make_shared<ArenaBuf>();
+            ab->ctx = ctx;
+            if (arena_alloc(ctx, false, &ab->p, total, &ab->cap) != cudaSuccess) {
+                cudaGetLastError();
+                ab->p = nullptr;
+                return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: cannot allocate a %llu-byte arena",
+                                    (unsigned long long)total));
+            }
+            sn->arena = ab;
+            for (size_t i = 0; i < D.regions.size(); ++i) {
+                if (!D.regions[i].ok) continue;
+                const uint64_t src = (uint64_t)ab->p + aoff[i];
+                sn->runs[i].push_back({0, D.regions[i].r.size, src});
+                dst.push_back(src);
+            }
+        }
+        trace("plan + arena alloc", tl);
+        const double tc = now_s();
+        st = hash_regions_sync(ctx, live, pre_h, &pre_dig, &pre_snap, nullptr, cs, dst.empty() ? nullptr : dst.data());
+        t_copy += now_s() - tc;
+        rep.dma_calls += live.empty() ? 0 : 1;
+        if (st != KC_OK) return fail(st);
+        rep.t_hash_pre_s = now_s() - tc;
+        trace("K6 hash + copy", tl);
+    } else {
+        st = hash_regions_sync(ctx, live, pre_h, &pre_dig, &pre_snap, nullptr, cs);
+        if (st != KC_OK) return fail(st);
+        rep.t_hash_pre_s = now_s() - t;
+        trace("regions + K1 pre", tl);
+    }
     rep.n_chunks = pre_h.size();
     for (auto& r : live) rep.total_bytes += r.size;
 
     // ---- the stored bytes: runs per region; chunks whose stored-state hash equals
     // the base's at the same (region, chunk) reference the base, the rest are
     // copied into this snapshot's own arena (256 B aligned runs)
-    double t_copy = 0;
     std::map<uint64_t, size_t> base_idx;
     if (base)
         for (size_t j = 0; j < base->desc.regions.size(); ++j)
@@ -1758,7 +1863,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     };
     st = ensure_stream(ctx);  // in-memory sinks copy arena <-> device directly: no staging ring
     if (st != KC_OK) return fail(st);
-    if (mode == KC_MODE_PRE_W) {
+    if (mode == KC_MODE_PRE_W && !fused) {
         st = snapshot_regions(pre_h);
         if (st != KC_OK) return fail(st);
     }
@@ -1797,19 +1902,19 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     rep.t_hash_post_s = now_s() - t;
     trace("K1 post", tl);
     {
-        size_t j = 0;
+        size_t j = 0;  // (W from the manifests: host loop over the chunks)
         for (size_t i = 0; i < D.regions.size(); ++i) {
             SnapRegion& sr = D.regions[i];
             if (!sr.ok) continue;
-            const uint64_t c0 = pre_off[i];
-            sr.post_manifest.assign(post_h.begin() + c0, post_h.begin() + c0 + sr.n_chunks);
-            std::vector<uint64_t> pm(pre_h.begin() + c0, pre_h.begin() + c0 + sr.n_chunks);
+            const uint64_t* pre = pre_h.data() + pre_off[i];
+            const uint64_t* post = post_h.data() + pre_off[i];
             for (uint64_t k = 0; k < sr.n_chunks; ++k)
-                if (pm[k] != sr.post_manifest[k]) sr.written.push_back(k);
+                if (pre[k] != post[k]) sr.written.push_back(k);
+            sr.post_manifest.assign(post, post + sr.n_chunks);
             rep.written_chunks += sr.written.size();
             sr.post_digest = post_dig[j];
             if (mode == KC_MODE_PRE_W) {
-                sr.manifest = std::move(pm);
+                sr.manifest.assign(pre, pre + sr.n_chunks);
                 sr.digest = pre_dig[j];
             } else {
                 sr.manifest = sr.post_manifest;
@@ -1819,6 +1924,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         }
     }
     D.snapshot_digest = mode == KC_MODE_PRE_W ? pre_snap : post_snap;
+    trace("W sets", tl);
     if (mode == KC_MODE_POST) {
         st = snapshot_regions(post_h);
         if (st != KC_OK) return fail(st);
@@ -1844,6 +1950,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
                 o += len;
             }
         }
+        trace("W plan + W arena", tl);
         t = now_s();
         st = copy_ranges_d2d(ctx, ranges, ctx->copy_stream, &rep.dma_calls);
         cudaStreamSynchronize(ctx->copy_stream);
@@ -2035,6 +2142,13 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
     if (KC_DRV(cuModuleGetFunction)(&f, mod, h->mangled.c_str()) != CUDA_SUCCESS) {
         if (own) KC_DRV(cuModuleUnload)(mod);
         return set_err(ctx, KC_ERR_ARG, "kc_replay: symbol %s not found in the code object", h->mangled.c_str());
+    }
+    {
+        const CUresult r = allow_dynamic_smem(f, h->smem);
+        if (r != CUDA_SUCCESS) {
+            if (own) KC_DRV(cuModuleUnload)(mod);
+            return cu_err(ctx, r, "kc_replay: dynamic shared memory attribute");
+        }
     }
     // F3: module variables into the replay module, after the memory restore and
     // before the dispatch; PRE_W restores the pre values,

@@ -138,3 +138,15 @@ extern "C" __global__ void kc_fixture_axpy_u32(const unsigned int* __restrict__ 
     const unsigned int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) y[i] = a * x[i] + y[i] + KC_VARIANT_DELTA;
 }
+
+// A dispatch with more than 48 KiB of dynamic shared memory (needs the opt-in
+// function attribute on every module it is launched from): each block of 1024
+// threads stages `per_block` u32 through shared memory and writes them reversed.
+extern "C" __global__ void kc_fixture_smem_reverse(const unsigned int* __restrict__ in, unsigned int* __restrict__ out,
+                                                   unsigned int per_block) {
+    extern __shared__ unsigned int stage[];
+    const size_t b0 = (size_t)blockIdx.x * per_block;
+    for (unsigned int i = threadIdx.x; i < per_block; i += blockDim.x) stage[i] = in[b0 + i];
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i < per_block; i += blockDim.x) out[b0 + i] = stage[per_block - 1 - i] ^ blockIdx.x;
+}
