@@ -370,6 +370,8 @@ def run_ours(a, rank, world, device, log):
     e2e = None
     if not a.no_e2e:
         e2e = run_e2e(a, ctx, pool, step, stream, world, log, reps)
+        torch.cuda.synchronize()
+        torch._C._host_emptyCache()   # the 30 GB of pinned e2e staging back to the OS
     lat = None
     if world == 1 and not a.no_latency:
         try:
@@ -539,20 +541,36 @@ def run_latency(a, ctx, pool, log):
                 "copy_out_bytes": cap["d2h_bytes"] or pool.bytes,
                 "copy_in_gbs": rst["h2d_bytes"] / max(rst["t_h2d_s"], 1e-9) / 1e9}
 
-    # ---- device sink (F1)
-    synth.dev_view(pool.va["y"], ys.size).zero_()   # a fresh output buffer: the dispatch writes W != {}
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    snap, cap = ctx.capture_dev(**disp)
-    t1 = time.perf_counter()
-    for s in pool.specs:
-        ctx.free(pool.va[s.name])
-    t2 = time.perf_counter()
-    r_dev, rst = ctx.restore_dev(snap)
-    t3 = time.perf_counter()
-    out["device"] = finish("device", cap, rst, r_dev, (t0, t1, t2, t3))
-    out["device"]["arena_bytes"] = snap.nbytes()
-    snap.free()
+    # ---- device sink (F1): a cold cycle (first in-memory capture and VMM restore
+    # of this process: lazy kernel loading, first arena and physical allocations)
+    # and a warm one on the restored state; both reported, the warm one is the
+    # steady-state latency of a resident tool
+    torch.cuda.empty_cache()          # earlier stages' cached blocks back to the driver
+    cold = None
+    r_dev = None
+    for cycle in ("cold", "warm"):
+        synth.dev_view(pool.va["y"], ys.size).zero_()   # a fresh output buffer: the dispatch writes W != {}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        snap, cap = ctx.capture_dev(**disp)
+        t1 = time.perf_counter()
+        if r_dev is None:
+            for s in pool.specs:
+                ctx.free(pool.va[s.name])
+        else:
+            r_dev.release()
+        t2 = time.perf_counter()
+        r_dev, rst = ctx.restore_dev(snap)
+        t3 = time.perf_counter()
+        res = finish(f"device {cycle}", cap, rst, r_dev, (t0, t1, t2, t3))
+        res["arena_bytes"] = snap.nbytes()
+        snap.free()
+        if cycle == "cold":
+            cold = res
+    out["device"] = res
+    out["device"]["cycle"] = "warm (second capture -> restore in this process)"
+    out["device"]["cold"] = {"latency_s": cold["latency_s"], "stages_s": cold["stages_s"],
+                             "validated_bit_exact": cold["validated_bit_exact"]}
 
     # ---- pinned host sink (the restored memory is now the live state); the arena
     # is pinned ahead of time like the staging ring, its cost reported apart

@@ -60,7 +60,7 @@ struct kc_ctx {
     uint64_t unknown_frees = 0;
 
     // cached device tables / scratch (stream-ordered; one stream at a time per ctx)
-    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map, dst_tab, gather_tab;
+    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map, dst_tab, gather_tab, chunk_order;
     std::vector<kc::RegionDev> regs_cached;
     kc_ctx_dev_buf pairs, pair_map, dirty;  // F2 (K5) pair table, chunk -> pair map, dirty bitmap
     std::vector<kc::PairDev> pairs_cached;
@@ -68,6 +68,7 @@ struct kc_ctx {
     std::vector<kc::DiffGroup> diff_groups;
     uint64_t diff_bitmap_words = 0;
     bool regs_aligned = true;
+    bool has_order = false;  // chunk_order holds a length-sorted chunk order for K1/K6
 
     // pinned staging ring for D2H/H2D (lazily allocated)
     uint64_t io_chunk = 64ull << 20;

@@ -375,7 +375,8 @@ __device__ __forceinline__ void st_cs16(void* p, uint4 v) {
 template <class CFG, bool COPY = false>
 __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     k1_hash_cpasync(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out,
-                    const uint32_t* __restrict__ map, const unsigned long long* __restrict__ dst = nullptr) {
+                    const uint32_t* __restrict__ map, const unsigned long long* __restrict__ dst = nullptr,
+                    const uint32_t* __restrict__ order = nullptr) {
     static_assert(!COPY || CFG::kUPC % 32 == 0, "K6 copy-out maps copy unit k to chunk 32k / UPC");
     constexpr int WARPS = CFG::kWarps, STAGES = CFG::kStages, SL = CFG::kSlice, PITCH = CFG::kPitch;
     constexpr int WSTAGE = CFG::kWStage, UPC = CFG::kUPC, UPL = CFG::kUPL;
@@ -393,8 +394,10 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     uint32_t sf = 0, f_nsl = 0;
     unsigned long long u_src[UPL];
     uint32_t u_bytes[UPL];
+    // position i of the chunk sequence -> chunk index (length-sorted order, or identity)
+    auto chunk_at = [&](uint64_t i) -> uint64_t { return order && i < C ? (uint64_t)__ldg(order + i) : i; };
     auto load_group = [&](uint64_t j) {
-        const uint64_t g = 8 * j + q;
+        const uint64_t g = chunk_at(8 * j + q);
         unsigned long long src = 0;
         uint32_t bytes = 0;
         if (g < C) {
@@ -447,7 +450,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     for (int s = 0; s < STAGES - 1; ++s) fetch(s);
     uint32_t step = 0;
     for (uint64_t j = j0; j < ngroups; j += W) {
-        const uint64_t g = 8 * j + q;
+        const uint64_t g = chunk_at(8 * j + q);
         ChunkRef cr = {nullptr, 0};
         if (g < C) cr = chunk_ref(regs, nreg, g, map);
         const uint32_t nst = cr.len >= 32 ? cr.len / 32 : 0;
@@ -1422,14 +1425,16 @@ static void launch_tma(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* 
 
 template <class CFG>
 static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
-                      int num_sms, cudaStream_t s, const unsigned long long* d_dst = nullptr) {
+                      int num_sms, cudaStream_t s, const unsigned long long* d_dst = nullptr,
+                      const uint32_t* order = nullptr) {
     const uint64_t groups = (C + 7) / 8;
     const uint64_t grid = std::min<uint64_t>((groups + CFG::kWarps - 1) / CFG::kWarps, (uint64_t)num_sms);
     if (d_dst)
         k1_hash_cpasync<CFG, true><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map,
-                                                                                       d_dst);
+                                                                                       d_dst, order);
     else
-        k1_hash_cpasync<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map);
+        k1_hash_cpasync<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map,
+                                                                                 nullptr, order);
 }
 
 // K1 variant selection (KC_K1_VARIANT, tuning knob; default = the measured best)
@@ -1442,7 +1447,7 @@ static int k1_variant() {
 }
 
 cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool aligned, uint64_t* d_out,
-                        const uint32_t* map, int num_sms, cudaStream_t s) {
+                        const uint32_t* map, int num_sms, cudaStream_t s, const uint32_t* order) {
     if (C == 0) return cudaSuccess;
     if (!aligned) {
         uint64_t grid = (C + 63) / 64;
@@ -1454,16 +1459,17 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
     switch (k1_variant()) {
         case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, map, num_sms, s); break;
-        case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s); break;
-        default: launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
+        case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
+        default: launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_hash_copy(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out,
-                             const unsigned long long* d_dst, const uint32_t* map, int num_sms, cudaStream_t s) {
+                             const unsigned long long* d_dst, const uint32_t* map, int num_sms, cudaStream_t s,
+                             const uint32_t* order) {
     if (C == 0) return cudaSuccess;
-    launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, d_dst);
+    launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, d_dst, order);
     return cudaGetLastError();
 }
 

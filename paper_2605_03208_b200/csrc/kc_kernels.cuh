@@ -53,13 +53,15 @@ struct DiffGroup {
 };
 
 // ---- launchers (kc_kernels.cu) ------------------------------------------
+// d_order (may be nullptr = identity): the order in which chunks are assigned to quads
 cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t n_chunks, bool aligned, uint64_t* d_out,
-                        const uint32_t* d_chunk_region /* may be nullptr */, int num_sms, cudaStream_t s);
+                        const uint32_t* d_chunk_region /* may be nullptr */, int num_sms, cudaStream_t s,
+                        const uint32_t* d_order = nullptr);
 // K6 (fused capture): K1 over the regions + copy of every byte to d_dst[r] (arena
 // address of region r, 16-byte aligned; regions 16-byte aligned)
 cudaError_t launch_hash_copy(const RegionDev* d_regs, int nreg, uint64_t n_chunks, uint64_t* d_out,
                              const unsigned long long* d_dst, const uint32_t* d_chunk_region, int num_sms,
-                             cudaStream_t s);
+                             cudaStream_t s, const uint32_t* d_order = nullptr);
 cudaError_t launch_digests(const RegionDev* d_regs, int nreg, const uint64_t* d_chunk_hash, uint64_t* d_region_digest,
                            uint8_t* d_scratch /* 24*nreg */, uint64_t* d_snapshot_digest, cudaStream_t s);
 cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64_t n_chunks, uint64_t* d_bitmap,

@@ -325,7 +325,7 @@ void kc_destroy(kc_ctx* ctx) {
     if (ctx->heap_base) KC_DRV(cuMemAddressFree)((CUdeviceptr)ctx->heap_base, ctx->heap_size);
     if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch, &ctx->pairs, &ctx->pair_map, &ctx->dirty,
-                              &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map, &ctx->dst_tab, &ctx->gather_tab})
+                              &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map, &ctx->dst_tab, &ctx->gather_tab, &ctx->chunk_order})
         if (b->p) cudaFree(b->p);
     for (auto& w : ctx->io) {
         for (void* p : w.pinned) cudaFreeHost(p);
@@ -500,6 +500,35 @@ static kc_status upload_regions(kc_ctx* ctx, const kc_region* regions, size_t n,
         if (!map.empty())
             KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->chunk_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
                           "upload chunk map");
+        // chunk order for K1/K6: full 64 KiB chunks first, then each region's
+        // short last chunk by length, descending, so the 8 chunks a warp hashes
+        // together have similar lengths (a group runs as long as its longest
+        // chunk).  Identity (no table) when every region is a multiple of 64 KiB.
+        std::vector<std::pair<uint32_t, uint32_t>> part;  // (length, chunk)
+        for (size_t i = 0; i < t.size(); ++i) {
+            const uint64_t rem = t[i].size % kChunk;
+            if (rem) part.emplace_back((uint32_t)rem, (uint32_t)(t[i].chunk_off + (t[i].size - 1) / kChunk));
+        }
+        ctx->has_order = !part.empty();
+        if (ctx->has_order) {
+            std::stable_sort(part.begin(), part.end(), [](const std::pair<uint32_t, uint32_t>& a,
+                                                          const std::pair<uint32_t, uint32_t>& b) {
+                return a.first > b.first;
+            });
+            std::vector<uint32_t> order;
+            order.reserve(c);
+            size_t pi = 0;
+            std::vector<uint8_t> is_part(c, 0);
+            for (auto& pr : part) is_part[pr.second] = 1;
+            for (uint64_t g = 0; g < c; ++g)
+                if (!is_part[g]) order.push_back((uint32_t)g);
+            for (; pi < part.size(); ++pi) order.push_back(part[pi].second);
+            KC_CHECK_CUDA(ctx, ensure(ctx->chunk_order, order.size() * 4), "cudaMalloc(chunk order)");
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->chunk_order.p, order.data(), order.size() * 4,
+                                               cudaMemcpyHostToDevice, s),
+                          "upload chunk order");
+            cudaStreamSynchronize(s);  // `order` is pageable and goes out of scope
+        }
         ctx->regs_cached.swap(t);
         ctx->regs_aligned = aligned;
     }
@@ -538,11 +567,13 @@ kc_status kc::hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_
                       "upload arena table");
         KC_CHECK_CUDA(ctx, launch_hash_copy((const RegionDev*)ctx->regs.p, (int)n, C, d_chunk_hash,
                                             (const unsigned long long*)ctx->dst_tab.p,
-                                            (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s),
+                                            (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s,
+                                            ctx->has_order ? (const uint32_t*)ctx->chunk_order.p : nullptr),
                       "launch K6");
     } else {
         KC_CHECK_CUDA(ctx, launch_hash((const RegionDev*)ctx->regs.p, (int)n, C, ctx->regs_aligned, d_chunk_hash,
-                                       (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s),
+                                       (const uint32_t*)ctx->chunk_map.p, ctx->num_sms, s,
+                                       ctx->has_order ? (const uint32_t*)ctx->chunk_order.p : nullptr),
                       "launch K1");
     }
     if (C) ctx->launches += 1;
