@@ -572,6 +572,14 @@ def run_latency(a, ctx, pool, log):
     out["device"]["cold"] = {"latency_s": cold["latency_s"], "stages_s": cold["stages_s"],
                              "validated_bit_exact": cold["validated_bit_exact"]}
 
+    # ---- device arena published to a fresh replay process (CUDA IPC): the
+    # paper's workflow (capture in the application, replay in another process)
+    # without the bytes leaving HBM
+    try:
+        out["device_ipc"] = run_ipc_sink(a, ctx, pool, disp, ys, log)
+    except Exception as ex:  # reported, never hidden
+        out["device_ipc"] = {"error": repr(ex)[:300], "validated_bit_exact": False}
+
     # ---- pinned host sink (the restored memory is now the live state); the arena
     # is pinned ahead of time like the staging ring, its cost reported apart
     tp = time.perf_counter()
@@ -627,8 +635,80 @@ def run_latency(a, ctx, pool, log):
     out["bytes"] = pool.bytes
     out["latency_s"] = out["device"]["latency_s"]
     out["validated_bit_exact"] = all(out[k]["validated_bit_exact"]
-                                     for k in ("device", "host_pinned", "host_pinned_incremental", "files"))
+                                     for k in ("device", "device_ipc", "host_pinned", "host_pinned_incremental",
+                                               "files"))
     return out
+
+
+def run_ipc_sink(a, ctx, pool, disp, ys, log):
+    """kc_capture_dev + kc_snapshot_publish here; kc_restore (CUDA IPC copy-in at
+    the captured VAs) + kc_replay + kc_validate in a fresh process, timed inside
+    it.  latency = capture + the child's restore + replay + validate; the
+    child's interpreter start, CUDA init and exit are reported apart."""
+    import shutil
+    import subprocess
+    import torch
+    import synth
+    d = a.latency_dir + "_ipc"
+    shutil.rmtree(d, ignore_errors=True)
+    synth.dev_view(pool.va["y"], ys.size).zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    snap, cap = ctx.capture_dev(**disp)
+    t1 = time.perf_counter()
+    snap.publish(d)
+    t2 = time.perf_counter()
+    p = subprocess.run([sys.executable, os.path.abspath(__file__), "--replay-child", d], capture_output=True,
+                       text=True, timeout=600, env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get(
+                           "CUDA_VISIBLE_DEVICES", str(torch.cuda.current_device()))))
+    t3 = time.perf_counter()
+    snap.free()
+    shutil.rmtree(d, ignore_errors=True)
+    for x in p.stderr.splitlines():
+        if x.startswith("[kc]"):
+            log("  child " + x)
+    lines = [x for x in p.stdout.splitlines() if x.startswith("{")]
+    if p.returncode != 0 or not lines:
+        raise RuntimeError(f"replay child failed rc={p.returncode}: {p.stderr[-400:]}")
+    ch = json.loads(lines[-1])
+    lat = (t1 - t0) + ch["restore_s"] + ch["replay_s"] + ch["validate_s"]
+    log(f"capture->replay [device_ipc]: capture {t1 - t0:.3f}s (publish {t2 - t1:.3f}s) | fresh process: restore "
+        f"{ch['restore_s']:.3f}s replay {ch['replay_s']:.4f}s validate {ch['validate_s']:.4f}s ok={ch['ok']} "
+        f"(child wall {t3 - t2:.1f}s incl. interpreter + CUDA init)")
+    return {"latency_s": lat, "validated_bit_exact": bool(ch["ok"]), "same_vas": bool(ch["same_vas"]),
+            "written_chunks": cap["written_chunks"],
+            "stages_s": {"capture_total": t1 - t0, "capture_hash_pre": cap["t_hash_pre_s"],
+                         "capture_copy": cap["t_d2h_s"], "capture_hash_post": cap["t_hash_post_s"],
+                         "publish": t2 - t1, "restore_total": ch["restore_s"], **ch["restore_stages"],
+                         "replay": ch["replay_s"], "validate": ch["validate_s"]},
+            "copy_in_gbs": ch["copy_in_gbs"], "child_wall_s": t3 - t2, "child_attempts": ch["attempts"],
+            "note": "restore/replay/validate timed inside the fresh replay process; its startup excluded"}
+
+
+def replay_child(d):
+    """--replay-child DIR: a fresh process restoring a published snapshot."""
+    from paper_2605_03208_b200 import kc
+    kc.exec_replay_process(sys.argv, d)          # pre-CUDA VA collision check (re-exec on collision)
+    ctx = kc.Context(0)
+    t0 = time.perf_counter()
+    r, rst = kc.restore_in_fresh_layout(ctx, d, sys.argv)
+    t1 = time.perf_counter()
+    ctx.replay(r)
+    t2 = time.perf_counter()
+    reps, unexpected = ctx.validate(r)
+    t3 = time.perf_counter()
+    import json as _j
+    regs = json.load(open(os.path.join(d, "memory_regions.json")))
+    same = sorted((x.base, x.size) for x in r.regions()) == sorted((int(e["base"], 16), int(e["size"])) for e in regs)
+    ok = all(x["differing_bytes"] == 0 for x in reps) and unexpected == 0 and rst["verify_mismatch_chunks"] == 0 \
+        and len(reps) > 0
+    print(_j.dumps({"restore_s": t1 - t0, "replay_s": t2 - t1, "validate_s": t3 - t2, "ok": ok, "same_vas": same,
+                    "restore_stages": {"restore_reserve_map": rst["t_reserve_s"], "restore_copy_in": rst["t_h2d_s"],
+                                       "restore_verify": rst["t_verify_s"]},
+                    "copy_in_gbs": rst["h2d_bytes"] / max(rst["t_h2d_s"], 1e-9) / 1e9,
+                    "attempts": int(os.environ.get("KC_REEXEC_ATTEMPT", "0")) + 1}))
+    r.release()
+    ctx.close()
 
 
 def pcie_peak(log, nbytes: int = 1 << 30, reps: int = 5) -> dict:
@@ -745,7 +825,11 @@ def main():
     p.add_argument("--no-latency", action="store_true")
     p.add_argument("--latency-dir", default="/dev/shm/kc_bench_capture")
     p.add_argument("--quiet", action="store_true")
+    p.add_argument("--replay-child", default=None, help=argparse.SUPPRESS)
     a = p.parse_args()
+    if a.replay_child:
+        replay_child(a.replay_child)
+        return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

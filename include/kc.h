@@ -325,12 +325,25 @@ kc_status kc_capture_incr(kc_ctx* ctx, const kc_dispatch* d, const kc_region* re
 /* Pin `bytes` of host memory ahead of time and park it in the ctx's cache (one
  * arena; a larger request replaces a smaller parked one).  0 frees the cache. */
 kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes);
+/* Map `bytes` of device memory (one VMM allocation) ahead of time and park it
+ * in the ctx for kc_capture_dev; a freed device snapshot also parks its arena
+ * there when it is the larger one (never an exported one).  0 releases it. */
+kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes);
 /* Same-VA restore from an in-memory snapshot (device or pinned host arena; the
  * originals must be freed first): VA windows as kc_restore (or the ctx VA
  * heap), then copy-in (D2D or H2D) and the K1 verify. */
 kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep);
 /* Persist an in-memory snapshot as a kc-snapshot/1 directory (parallel). */
 kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
+/* F1 across processes: persist the snapshot's metadata, manifests and W bytes
+ * as a kc-snapshot/1 directory whose region bytes stay in THIS process's
+ * device arena, shared through CUDA IPC (memory/device_arena.json: the
+ * cudaIpcMemHandle_t and each region's arena offset; no memory/region_*.bin).
+ * kc_restore(dir) in another process on the same GPU maps the arena and copies
+ * in at HBM bandwidth (fused with the verify hashes) instead of reading files.
+ * Valid while this process keeps the snapshot alive.  KC_ERR_STATE for host
+ * snapshots and incremental ones (stored bytes not in one own arena). */
+kc_status kc_snapshot_publish(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
 /* Bytes this snapshot copied into its own arenas. */
 uint64_t kc_snapshot_bytes(const kc_snapshot* s);
 /* Stored bytes referenced from base snapshots (kc_capture_incr), not copied. */

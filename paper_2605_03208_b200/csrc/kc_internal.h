@@ -15,7 +15,7 @@
 // Driver-API entry points resolved through cudart (cudaGetDriverEntryPoint),
 // so libkc.so has no link-time dependency on libcuda and loads on hosts
 // without a GPU driver (calls then fail with KC_ERR_CUDA).
-#define KC_DRV_FUNCS(X) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemFree) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
+#define KC_DRV_FUNCS(X) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemExportToShareableHandle) X(cuMemFree) X(cuMemImportFromShareableHandle) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
 namespace kc {
 struct Drv {
 #define KC_DRV_DECL(f) decltype(&::f) f = nullptr;
@@ -102,6 +102,19 @@ struct kc_ctx {
     uint64_t heap_base = 0, heap_size = 0;
     // F3 code objects seen by the CUPTI hook (cuModuleLoadData*): module -> image bytes (mu)
     std::map<CUmodule, std::vector<uint8_t>> code_objects;
+    // parked device arena (a VMM mapping) for kc_capture_dev (kc_dev_arena_reserve)
+    struct ParkedVmm {
+        uint64_t va = 0, size = 0;
+        CUmemGenericAllocationHandle h = 0;
+        void release() {
+            if (!va) return;
+            KC_DRV(cuMemUnmap)((CUdeviceptr)va, size);
+            KC_DRV(cuMemRelease)(h);
+            KC_DRV(cuMemAddressFree)((CUdeviceptr)va, size);
+            va = size = 0;
+            h = 0;
+        }
+    } dev_arena;
     // parked pinned host arena for kc_capture_host (kc_host_arena_reserve)
     void* host_arena = nullptr;
     uint64_t host_arena_bytes = 0;
@@ -147,6 +160,10 @@ struct kc_restored {
     CUmodule module = nullptr;
     std::vector<uint8_t> image;  // code object (kernel.cubin or the device snapshot's copy)
     const kc_snapshot* dev_snap = nullptr;  // restored from a device snapshot (kc_restore_dev)
+    void* ipc_arena = nullptr;              // restored from a published snapshot: its mapped arena
+    uint64_t ipc_vmm_size = 0;              //   imported VMM mapping (0: a legacy CUDA IPC mapping)
+    CUmemGenericAllocationHandle ipc_vmm_h = 0;
+    std::map<uint64_t, uint64_t> ipc_off;   //   region base -> offset in that arena
     std::vector<ModVarState> modvars;       // F3: written into the replay module before each launch
     uint64_t modvar_checked = 0, modvar_mismatch = 0;  // last replay vs the captured post values
 };

@@ -324,6 +324,7 @@ void kc_destroy(kc_ctx* ctx) {
     for (uint64_t b : vm) free_alloc(ctx, b, false);
     if (ctx->heap_base) KC_DRV(cuMemAddressFree)((CUdeviceptr)ctx->heap_base, ctx->heap_size);
     if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+    ctx->dev_arena.release();
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch, &ctx->pairs, &ctx->pair_map, &ctx->dirty,
                               &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map, &ctx->dst_tab, &ctx->gather_tab, &ctx->chunk_order})
         if (b->p) cudaFree(b->p);

@@ -9,8 +9,10 @@
 // Ordering and crash safety: metadata before any D2H copy,
 // per-region copy failures tolerated and logged, the sentinel written last.
 #include <errno.h>
+#include <signal.h>
 #include <fcntl.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
 #include <sys/stat.h>
 #include <sys/types.h>
 #include <unistd.h>
@@ -1171,8 +1173,10 @@ static kc_status build_stash(kc_ctx* ctx, kc_restored* h, const SnapDesc& d, Res
     }
     h->stash_bytes = total;
     if (!total) return KC_OK;
-    if (cudaMalloc(&h->stash_pre, total) != cudaSuccess || cudaMalloc(&h->stash_ref, total) != cudaSuccess)
-        return set_err(ctx, KC_ERR_NOMEM, "kc_restore: stash of %llu bytes", (unsigned long long)total);
+    // one allocation for both stashes (stash_ref = stash_pre + total; kc_release frees stash_pre only)
+    if (cudaMalloc(&h->stash_pre, 2 * total) != cudaSuccess)
+        return set_err(ctx, KC_ERR_NOMEM, "kc_restore: stash of %llu bytes", (unsigned long long)(2 * total));
+    h->stash_ref = (uint8_t*)h->stash_pre + total;
     for (size_t i = 0; i < h->regions.size(); ++i) {
         auto& rr = h->regions[i];
         if (!rr.ok || rr.written.empty()) continue;
@@ -1355,6 +1359,8 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     }
     rep.n_spans = h->spans.size();
     rep.t_reserve_s = now_s() - t;
+    double tl = now_s();
+    trace("restore: reserve + create + map", t);
 
     // ---- stage 5a: copy-in (gaps and failed regions zero-filled)
     t = now_s();
@@ -1388,6 +1394,7 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
         }
     }
     cudaStreamSynchronize(ctx->copy_stream);  // zero-fill before the copy-in streams
+    trace("restore: zero-fill gaps", tl);
     std::vector<uint64_t> got;
     bool verified = false;  // the copy-in produced the verify hashes itself (K6)
     st = src.copy_in_verify(ctx, d, rep, got, verified);
@@ -1400,6 +1407,7 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
         return st;
     }
     rep.t_h2d_s = now_s() - t;
+    trace(verified ? "restore: copy-in + verify (K6)" : "restore: copy-in", tl);
 
     // ---- verify against the captured manifest (K1, O6)
     t = now_s();
@@ -1434,8 +1442,10 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
                        "manifest", (unsigned long long)rep.verify_mismatch_chunks);
     }
 
+    trace("restore: verify", tl);
     // ---- device stashes of the written chunks: replay recopy (pre) and validation reference (post)
     st = build_stash(ctx, h, d, src);
+    trace("restore: W stashes", tl);
     if (st != KC_OK) {
         rollback(h);
         delete h;
@@ -1447,6 +1457,172 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     return KC_OK;
 }
 
+namespace {
+kc_status copy_ranges_d2d(kc_ctx* ctx, const std::vector<std::array<uint64_t, 3>>& ranges, cudaStream_t s,
+                          uint64_t* calls);
+// a published VMM arena mapped into this process: the publisher's fd is
+// duplicated with pidfd_getfd (Linux >= 5.6; a same-user or descendant
+// process), imported and mapped read-write at a fresh VA
+struct ImportedArena {
+    CUdeviceptr va = 0;
+    uint64_t size = 0;
+    CUmemGenericAllocationHandle h = 0;
+    kc_status open(kc_ctx* ctx, int pid, int fd, uint64_t bytes) {
+#if defined(SYS_pidfd_open) && defined(SYS_pidfd_getfd)
+        const int pfd = (int)syscall(SYS_pidfd_open, pid, 0);
+        if (pfd < 0)
+            return set_err(ctx, KC_ERR_STATE, "pidfd_open(%d): %s (is the publishing process alive?)", pid,
+                           strerror(errno));
+        const int myfd = (int)syscall(SYS_pidfd_getfd, pfd, fd, 0);
+        const int gerr = errno;
+        ::close(pfd);
+        if (myfd < 0)
+            return set_err(ctx, KC_ERR_STATE, "pidfd_getfd(%d, fd %d): %s", pid, fd, strerror(gerr));
+        CUresult r = KC_DRV(cuMemImportFromShareableHandle)(&h, (void*)(uintptr_t)myfd,
+                                                            CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+        ::close(myfd);
+        if (r != CUDA_SUCCESS) return cu_err(ctx, r, "cuMemImportFromShareableHandle");
+        size = bytes;
+        r = KC_DRV(cuMemAddressReserve)(&va, size, 0, 0, 0);
+        if (r != CUDA_SUCCESS) {
+            KC_DRV(cuMemRelease)(h);
+            va = 0;
+            return cu_err(ctx, r, "cuMemAddressReserve(published arena)");
+        }
+        CUmemAccessDesc acc;
+        acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc.location.id = ctx->device;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        r = KC_DRV(cuMemMap)(va, size, 0, h, 0);
+        if (r == CUDA_SUCCESS) r = KC_DRV(cuMemSetAccess)(va, size, &acc, 1);
+        if (r != CUDA_SUCCESS) {
+            KC_DRV(cuMemUnmap)(va, size);
+            KC_DRV(cuMemAddressFree)(va, size);
+            KC_DRV(cuMemRelease)(h);
+            va = 0;
+            return cu_err(ctx, r, "cuMemMap(published arena)");
+        }
+        return KC_OK;
+#else
+        (void)pid; (void)fd; (void)bytes;
+        return set_err(ctx, KC_ERR_UNSUPPORTED, "pidfd_getfd is not available on this system");
+#endif
+    }
+    void close() {
+        if (!va) return;
+        cudaDeviceSynchronize();
+        KC_DRV(cuMemUnmap)(va, size);
+        KC_DRV(cuMemAddressFree)(va, size);
+        KC_DRV(cuMemRelease)(h);
+        va = 0;
+    }
+};
+
+// F1 across processes: the region bytes of a published snapshot
+// (kc_snapshot_publish) live in the capturing process's device arena; this
+// process maps it with CUDA IPC and copies in at HBM bandwidth (K6: one read
+// of the arena gives the copy and the verify hashes).  Metadata, manifests
+// and W's post bytes come from the directory.
+struct IpcSource : FileSource {
+    void* arena = nullptr;
+    uint64_t arena_bytes = 0;
+    ImportedArena imp;                 // vmm_fd: the imported mapping
+    std::map<uint64_t, uint64_t> off;  // region base -> arena offset
+    explicit IpcSource(std::string d) : FileSource(std::move(d)) {}
+    ~IpcSource() override {
+        if (imp.va) imp.close();
+        else if (arena) cudaIpcCloseMemHandle(arena);
+    }
+    kc_status open(kc_ctx* ctx) {
+        std::string text;
+        kcj::Value v;
+        if (!kcj::read_file(dir + "/memory/device_arena.json", text) || !kcj::Parser(text).parse(v) ||
+            !v.get("regions"))
+            return set_err(ctx, KC_ERR_FORMAT, "device_arena.json does not parse");
+        if (v.get("format") == nullptr || v.get("format")->s != "kc-device-arena/1")
+            return set_err(ctx, KC_ERR_FORMAT, "device_arena.json: unknown format");
+        if (v.get("pid") && kill((pid_t)v.get("pid")->as_u64(), 0) != 0 && errno == ESRCH)
+            return set_err(ctx, KC_ERR_STATE, "the process that published this snapshot (pid %llu) is gone",
+                           (unsigned long long)v.get("pid")->as_u64());
+        if (v.get("device") && (int)v.get("device")->as_u64() != ctx->device)
+            return set_err(ctx, KC_ERR_ARG, "published snapshot lives on device %d, this ctx is on %d",
+                           (int)v.get("device")->as_u64(), ctx->device);
+        arena_bytes = v.get("arena_bytes") ? v.get("arena_bytes")->as_u64() : 0;
+        for (auto& e : v.get("regions")->a) {
+            if (!e.get("base") || !e.get("offset")) return set_err(ctx, KC_ERR_FORMAT, "device_arena.json: region");
+            off[strtoull(e.get("base")->s.c_str(), nullptr, 16)] = e.get("offset")->as_u64();
+        }
+        if (v.get("kind") && v.get("kind")->s == "vmm_fd") {
+            if (!v.get("fd") || !v.get("mapped_bytes") || !v.get("pid"))
+                return set_err(ctx, KC_ERR_FORMAT, "device_arena.json: vmm_fd needs pid, fd, mapped_bytes");
+            kc_status st = imp.open(ctx, (int)v.get("pid")->as_u64(), (int)v.get("fd")->as_u64(),
+                                    v.get("mapped_bytes")->as_u64());
+            if (st != KC_OK) return st;
+            arena = (void*)imp.va;
+            return KC_OK;
+        }
+        if (!v.get("ipc_handle")) return set_err(ctx, KC_ERR_FORMAT, "device_arena.json: no ipc_handle");
+        cudaIpcMemHandle_t ih;
+        const std::string& hx = v.get("ipc_handle")->s;
+        if (hx.size() != 2 * sizeof ih) return set_err(ctx, KC_ERR_FORMAT, "device_arena.json: bad ipc_handle");
+        for (size_t i = 0; i < sizeof ih; ++i)
+            ((uint8_t*)&ih)[i] = (uint8_t)strtoul(hx.substr(2 * i, 2).c_str(), nullptr, 16);
+        cudaError_t ce = cudaIpcOpenMemHandle(&arena, ih, cudaIpcMemLazyEnablePeerAccess);
+        if (ce != cudaSuccess) {
+            arena = nullptr;
+            return set_err(ctx, KC_ERR_STATE, "cudaIpcOpenMemHandle: %s (is the capturing process alive and the "
+                           "snapshot not freed?)", cudaGetErrorString(ce));
+        }
+        return KC_OK;
+    }
+    bool needs_staging() const override { return false; }
+    // the arena address of every ok region (in order), checked against the arena size
+    kc_status sources(kc_ctx* ctx, const SnapDesc& d, std::vector<kc_region>& srcs, std::vector<uint64_t>& dst) {
+        for (auto& sr : d.regions) {
+            if (!sr.ok) continue;
+            auto it = off.find(sr.r.base);
+            if (it == off.end() || it->second + sr.r.size > arena_bytes)
+                return set_err(ctx, KC_ERR_FORMAT, "device_arena.json: region %s missing or out of the arena",
+                               sr.hx.c_str());
+            kc_region r = sr.r;
+            r.base = (uint64_t)arena + it->second;
+            srcs.push_back(r);
+            dst.push_back(sr.r.base);
+        }
+        return KC_OK;
+    }
+    kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) override {
+        std::vector<kc_region> srcs;
+        std::vector<uint64_t> dst;
+        kc_status st = sources(ctx, d, srcs, dst);
+        if (st != KC_OK) return st;
+        std::vector<std::array<uint64_t, 3>> ranges;
+        for (size_t i = 0; i < srcs.size(); ++i) {
+            ranges.push_back({srcs[i].base, dst[i], srcs[i].size});
+            rep.h2d_bytes += srcs[i].size;
+        }
+        return copy_ranges_d2d(ctx, ranges, ctx->copy_stream, nullptr);
+    }
+    kc_status copy_in_verify(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep, std::vector<uint64_t>& got,
+                             bool& done) override {
+        done = false;
+        if (getenv("KC_NO_FUSED_RESTORE")) return KC_OK;
+        std::vector<kc_region> srcs;
+        std::vector<uint64_t> dst;
+        kc_status st = sources(ctx, d, srcs, dst);
+        if (st != KC_OK) return st;
+        for (size_t i = 0; i < srcs.size(); ++i)
+            if ((srcs[i].base & 15) || (dst[i] & 15)) return KC_OK;
+        st = hash_regions_sync(ctx, srcs, got, nullptr, nullptr, nullptr, ctx->copy_stream,
+                               dst.empty() ? nullptr : dst.data());
+        if (st != KC_OK) return st;
+        for (const auto& r : srcs) rep.h2d_bytes += r.size;
+        done = true;
+        return KC_OK;
+    }
+};
+}  // namespace
+
 extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** out, kc_restore_report* rep_out) {
     if (!ctx || !dir_c || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
@@ -1454,9 +1630,33 @@ extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** ou
     kc_restore_report rep;
     memset(&rep, 0, sizeof rep);
     const double t0 = now_s();
+    struct stat sb;
+    if (stat((std::string(dir_c) + "/memory/device_arena.revoked").c_str(), &sb) == 0)
+        return set_err(ctx, KC_ERR_STATE, "kc_restore: %s was published from a device snapshot that has been freed",
+                       dir_c);
+    double tl = now_s();
     SnapDesc d;
     kc_status st = load_desc_files(ctx, dir_c, d, rep);
     if (st != KC_OK) return st;
+    trace("restore: load metadata", tl);
+    if (stat((std::string(dir_c) + "/memory/device_arena.json").c_str(), &sb) == 0) {
+        if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+        IpcSource src(dir_c);
+        st = src.open(ctx);
+        if (st != KC_OK) return st;
+        trace("restore: open the published arena (CUDA IPC)", tl);
+        st = restore_core(ctx, d, src, out, rep_out, rep, t0);
+        if (st == KC_OK) {  // the mapping stays open for typed validation; kc_release closes it
+            (*out)->dir = dir_c;
+            (*out)->ipc_arena = src.arena;
+            (*out)->ipc_off = src.off;
+            (*out)->ipc_vmm_size = src.imp.va ? src.imp.size : 0;
+            (*out)->ipc_vmm_h = src.imp.h;
+            src.arena = nullptr;
+            src.imp.va = 0;  // ownership moved to the restored handle
+        }
+        return st;
+    }
     FileSource src(dir_c);
     st = restore_core(ctx, d, src, out, rep_out, rep, t0);
     if (st == KC_OK) (*out)->dir = dir_c;
@@ -1563,6 +1763,58 @@ struct DevSource : RestoreSource {
 namespace {
 // arena allocation for in-memory snapshots: device (cudaMalloc) or pinned host,
 // the latter from the ctx's parked arena when it is large enough
+// a device arena as one VMM allocation that can be exported as a POSIX fd
+// (kc_snapshot_publish); false (nothing held) when the device or driver refuses
+bool vmm_arena_alloc(kc_ctx* ctx, ArenaBuf& ab, uint64_t bytes) {
+    if (getenv("KC_NO_VMM_ARENA")) return false;
+    if (ctx->dev_arena.va && ctx->dev_arena.size >= bytes) {  // the parked arena
+        ab.p = (void*)ctx->dev_arena.va;
+        ab.cap = ctx->dev_arena.size;
+        ab.vmm = true;
+        ab.vmm_h = ctx->dev_arena.h;
+        ab.vmm_size = ctx->dev_arena.size;
+        ctx->dev_arena = {};
+        return true;
+    }
+    CUmemAllocationProp prop;
+    memset(&prop, 0, sizeof prop);
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = ctx->device;
+    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    size_t G = 0;
+    if (KC_DRV(cuMemGetAllocationGranularity)(&G, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS || !G)
+        return false;
+    const uint64_t sz = (bytes + G - 1) / G * G;
+    CUmemGenericAllocationHandle h = 0;
+    if (KC_DRV(cuMemCreate)(&h, sz, &prop, 0) != CUDA_SUCCESS) return false;
+    CUdeviceptr va = 0;
+    if (KC_DRV(cuMemAddressReserve)(&va, sz, G, 0, 0) != CUDA_SUCCESS) {
+        KC_DRV(cuMemRelease)(h);
+        return false;
+    }
+    CUmemAccessDesc acc;
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (KC_DRV(cuMemMap)(va, sz, 0, h, 0) != CUDA_SUCCESS) {
+        KC_DRV(cuMemAddressFree)(va, sz);
+        KC_DRV(cuMemRelease)(h);
+        return false;
+    }
+    if (KC_DRV(cuMemSetAccess)(va, sz, &acc, 1) != CUDA_SUCCESS) {
+        KC_DRV(cuMemUnmap)(va, sz);
+        KC_DRV(cuMemAddressFree)(va, sz);
+        KC_DRV(cuMemRelease)(h);
+        return false;
+    }
+    ab.p = (void*)va;
+    ab.cap = bytes;
+    ab.vmm = true;
+    ab.vmm_h = h;
+    ab.vmm_size = sz;
+    return true;
+}
+
 cudaError_t arena_alloc(kc_ctx* ctx, bool host, void** p, uint64_t bytes, uint64_t* cap) {
     *cap = bytes;
     if (!host) return cudaMalloc(p, bytes);
@@ -1595,6 +1847,23 @@ extern "C" kc_status kc_capture_incr(kc_ctx* ctx, const kc_dispatch* d, const kc
                                      kc_capture_report* rep_out) {
     if (base && base->ctx != ctx) return set_err(ctx, KC_ERR_ARG, "kc_capture_incr: base snapshot of another ctx");
     return capture_mem(ctx, d, regions, n, mode, out, rep_out, host != 0, base);
+}
+
+extern "C" kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
+    if (!ctx) return KC_ERR_ARG;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    cudaDeviceSynchronize();
+    if (bytes == 0) {
+        ctx->dev_arena.release();
+        return KC_OK;
+    }
+    if (ctx->dev_arena.size >= bytes) return KC_OK;
+    ArenaBuf ab;  // allocate, then park it through the destructor
+    ab.ctx = ctx;
+    if (!vmm_arena_alloc(ctx, ab, bytes))
+        return set_err(ctx, KC_ERR_NOMEM, "kc_dev_arena_reserve: cannot map a %llu-byte VMM arena",
+                       (unsigned long long)bytes);
+    return KC_OK;
 }
 
 extern "C" kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
@@ -1743,7 +2012,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         if (total) {
             auto ab = std::make_shared<ArenaBuf>();
             ab->ctx = ctx;
-            if (arena_alloc(ctx, false, &ab->p, total, &ab->cap) != cudaSuccess) {
+            if (!vmm_arena_alloc(ctx, *ab, total) && arena_alloc(ctx, false, &ab->p, total, &ab->cap) != cudaSuccess) {
                 cudaGetLastError();
                 ab->p = nullptr;
                 return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: cannot allocate a %llu-byte arena",
@@ -1993,12 +2262,57 @@ extern "C" kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restor
     return st;
 }
 
-extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
+static kc_status save_impl(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c, bool publish) {
     if (!ctx || !s || !dir_c) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
     const std::string dir = dir_c;
     const SnapDesc& D = s->desc;
+    // publish: the region bytes stay in this process's device arena, shared by
+    // CUDA IPC; every ok region must be one run inside the snapshot's own arena
+    std::string arena_json;
+    if (publish) {
+        if (s->host || !s->arena || !s->arena->p)
+            return set_err(ctx, KC_ERR_STATE, "kc_snapshot_publish: needs a device snapshot with its own arena");
+        // VMM arena: export a POSIX fd that the replay process duplicates with
+        // pidfd_getfd and maps (cuMemImportFromShareableHandle); else a legacy
+        // CUDA IPC handle (cudaIpcOpenMemHandle, measured ~160 ms for 30 GB)
+        std::string how;
+        if (s->arena->vmm) {
+            if (s->arena->export_fd < 0) {
+                int fd = -1;
+                KC_CHECK_CU(ctx, KC_DRV(cuMemExportToShareableHandle)(&fd, s->arena->vmm_h,
+                                                                     CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+                            "cuMemExportToShareableHandle");
+                s->arena->export_fd = fd;
+            }
+            how = "\"kind\": \"vmm_fd\",\n  \"fd\": " + std::to_string(s->arena->export_fd) +
+                  ",\n  \"mapped_bytes\": " + std::to_string((unsigned long long)s->arena->vmm_size);
+        } else {
+            cudaIpcMemHandle_t ih;
+            KC_CHECK_CUDA(ctx, cudaIpcGetMemHandle(&ih, s->arena->p), "cudaIpcGetMemHandle");
+            char hx[2 * sizeof ih + 1];
+            for (size_t i = 0; i < sizeof ih; ++i) snprintf(hx + 2 * i, 3, "%02x", (unsigned)((const uint8_t*)&ih)[i]);
+            how = std::string("\"kind\": \"cuda_ipc\",\n  \"ipc_handle\": \"") + hx + "\"";
+        }
+        arena_json = "{\n  \"format\": \"kc-device-arena/1\",\n  \"pid\": " + std::to_string((long long)getpid()) +
+                     ",\n  \"device\": " + std::to_string(ctx->device) + ",\n  \"arena_bytes\": " +
+                     std::to_string((unsigned long long)s->arena_bytes) + ",\n  " + how + ",\n  \"regions\": [";
+        bool first = true;
+        for (size_t i = 0; i < D.regions.size(); ++i) {
+            if (!D.regions[i].ok) continue;
+            const auto& runs = s->runs[i];
+            const uint64_t a0 = (uint64_t)s->arena->p;
+            if (runs.size() != 1 || runs[0].roff != 0 || runs[0].len != D.regions[i].r.size || runs[0].src < a0 ||
+                runs[0].src + runs[0].len > a0 + s->arena_bytes)
+                return set_err(ctx, KC_ERR_STATE, "kc_snapshot_publish: region %s is not one run of the snapshot's "
+                               "own arena (an incremental snapshot)", D.regions[i].hx.c_str());
+            arena_json += std::string(first ? "\n" : ",\n") + "    {\"base\": \"" + D.regions[i].hx +
+                          "\", \"offset\": " + std::to_string((unsigned long long)(runs[0].src - a0)) + "}";
+            first = false;
+        }
+        arena_json += "\n  ]\n}\n";
+    }
     if (!mkdir_p(dir + "/memory") || !mkdir_p(dir + "/post") || !mkdir_p(dir + "/written"))
         return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot create %s", dir_c);
     unlink((dir + "/capture_complete").c_str());
@@ -2015,15 +2329,23 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
         mr.push_back({sr.r.base, sr.r.size, sr.n_chunks, sr.digest, sr.r.seq, sr.r.kind, sr.r.device, sr.ok});
     if (!write_text(dir + "/memory_regions.json", regions_json(mr)))
         return set_err(ctx, KC_ERR_IO, "kc_snapshot_save: cannot write memory_regions.json");
-    // region files from the arena (parallel workers)
+    unlink((dir + "/memory/device_arena.revoked").c_str());
+    if (publish) {
+        if (!write_text(dir + "/memory/device_arena.json", arena_json))
+            return set_err(ctx, KC_ERR_IO, "kc_snapshot_publish: cannot write device_arena.json");
+        s->published.push_back(dir);
+    } else {
+        unlink((dir + "/memory/device_arena.json").c_str());
+    }
+    // region files from the arena (parallel workers; none when publishing)
     const int T = io_threads();
-    kc_status st = ensure_io(ctx, T);
+    kc_status st = publish ? KC_OK : ensure_io(ctx, T);
     if (st != KC_OK) return st;
     // work items: 256 MiB pieces of every run, with the address its file offset maps to
     std::vector<IoItem> items;
     std::vector<uint64_t> item_base;
     for (size_t i = 0; i < D.regions.size(); ++i) {
-        if (!D.regions[i].ok) continue;
+        if (!D.regions[i].ok || publish) continue;
         const std::string path = dir + "/memory/region_" + D.regions[i].hx + ".bin";
         int fd = open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
         const bool ok = fd >= 0 && ftruncate(fd, (off_t)D.regions[i].r.size) == 0;
@@ -2077,6 +2399,14 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
     return KC_OK;
 }
 
+extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
+    return save_impl(ctx, s, dir_c, false);
+}
+
+extern "C" kc_status kc_snapshot_publish(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
+    return save_impl(ctx, s, dir_c, true);
+}
+
 extern "C" uint64_t kc_snapshot_bytes(const kc_snapshot* s) { return s ? s->arena_bytes + s->w_bytes : 0; }
 
 extern "C" uint64_t kc_snapshot_shared_bytes(const kc_snapshot* s) { return s ? s->shared_bytes : 0; }
@@ -2084,6 +2414,13 @@ extern "C" uint64_t kc_snapshot_shared_bytes(const kc_snapshot* s) { return s ? 
 extern "C" int kc_snapshot_is_host(const kc_snapshot* s) { return s && s->host ? 1 : 0; }
 
 extern "C" void kc_snapshot_free(kc_snapshot* s) {
+    // revoke the directories this snapshot published: their bytes go with the arena
+    if (s)
+        for (const std::string& d : s->published) {
+            const std::string j = d + "/memory/device_arena.json";
+            struct stat sb;
+            if (stat(j.c_str(), &sb) == 0) rename(j.c_str(), (d + "/memory/device_arena.revoked").c_str());
+        }
     if (!s) return;
     if (s->ctx) bind_device(s->ctx);
     if (s->warena) {
@@ -2108,8 +2445,14 @@ extern "C" void kc_release(kc_restored* h) {
     if (h->ctx) bind_device(h->ctx);
     cudaDeviceSynchronize();
     if (h->module) KC_DRV(cuModuleUnload)(h->module);
-    if (h->stash_pre) cudaFree(h->stash_pre);
-    if (h->stash_ref) cudaFree(h->stash_ref);
+    if (h->stash_pre) cudaFree(h->stash_pre);  // stash_ref lives in the same allocation
+    if (h->ipc_arena && h->ipc_vmm_size) {
+        KC_DRV(cuMemUnmap)((CUdeviceptr)h->ipc_arena, h->ipc_vmm_size);
+        KC_DRV(cuMemAddressFree)((CUdeviceptr)h->ipc_arena, h->ipc_vmm_size);
+        KC_DRV(cuMemRelease)(h->ipc_vmm_h);
+    } else if (h->ipc_arena) {
+        cudaIpcCloseMemHandle(h->ipc_arena);
+    }
     rollback(h);
     delete h;
 }
@@ -2333,7 +2676,25 @@ kc_status kc::validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, 
                 return set_err(ctx, KC_ERR_OUT_OF_BOUNDS, "kc_validate: output %zu is not inside a restored region", i);
             }
             const uint64_t roff = o.act - owner->r.base;
-            if (h->dev_snap) {  // device snapshot: stored bytes from the arena, W's post bytes from the W arena
+            if (h->ipc_arena) {  // published snapshot: stored bytes from the mapped arena, W's post bytes from the stash
+                auto it = h->ipc_off.find(owner->r.base);
+                if (it == h->ipc_off.end()) {
+                    if (typed_ref) cudaFree(typed_ref);
+                    return set_err(ctx, KC_ERR_FORMAT, "kc_validate: region not in the published arena");
+                }
+                cudaMemcpyAsync((uint8_t*)typed_ref + off, (const uint8_t*)h->ipc_arena + it->second + roff, o.nbytes,
+                                cudaMemcpyDeviceToDevice, s);
+                if (h->mode == KC_MODE_PRE_W)
+                    for (size_t j = 0; j < owner->written.size(); ++j) {
+                        const uint64_t c0 = owner->written[j] * kChunk;
+                        const uint64_t len = std::min<uint64_t>(kChunk, owner->r.size - c0);
+                        const uint64_t lo = std::max(c0, roff), hi = std::min(c0 + len, roff + o.nbytes);
+                        if (lo < hi)
+                            cudaMemcpyAsync((uint8_t*)typed_ref + off + (lo - roff),
+                                            (const uint8_t*)h->stash_ref + owner->stash_off[j] + (lo - c0), hi - lo,
+                                            cudaMemcpyDeviceToDevice, s);
+                    }
+            } else if (h->dev_snap) {  // device snapshot: stored bytes from the arena, W's post bytes from the W arena
                 const kc_snapshot* sn = h->dev_snap;
                 const size_t ri = (size_t)(owner - h->regions.data());
                 for (const auto& ru : sn->runs[ri]) {  // stored bytes of [roff, roff + nbytes)
@@ -2451,8 +2812,7 @@ kc_status kc::restored_rebind(kc_ctx* ctx, kc_restored* h, const kc_snapshot* sn
     cudaDeviceSynchronize();
     if (h->module) KC_DRV(cuModuleUnload)(h->module);
     h->module = nullptr;
-    if (h->stash_pre) cudaFree(h->stash_pre);
-    if (h->stash_ref) cudaFree(h->stash_ref);
+    if (h->stash_pre) cudaFree(h->stash_pre);  // stash_ref lives in the same allocation
     h->stash_pre = h->stash_ref = nullptr;
     h->stash_bytes = 0;
     bind_dispatch_fields(h, d);

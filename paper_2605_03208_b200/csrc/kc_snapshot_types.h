@@ -2,6 +2,8 @@
 // kc_snapshot.cu (capture/restore/replay/validate) and kc_sequence.cu (F4
 // multi-kernel capture).  Not part of the ABI.
 #pragma once
+#include <unistd.h>
+
 #include <memory>
 #include <string>
 #include <vector>
@@ -40,10 +42,32 @@ struct ArenaBuf {
     void* p = nullptr;
     uint64_t cap = 0;
     bool host = false;
+    // device arenas are VMM allocations exportable as a POSIX fd (F1 across
+    // processes); vmm_h/vmm_size describe the mapping at p, export_fd the fd
+    // handed out by kc_snapshot_publish (closed with the arena)
+    bool vmm = false;
+    CUmemGenericAllocationHandle vmm_h = 0;
+    uint64_t vmm_size = 0;
+    int export_fd = -1;
     ~ArenaBuf() {
+        const bool exported = export_fd >= 0;
+        if (exported) close(export_fd);
         if (!p) return;
         if (ctx) kc::bind_device(ctx);
-        if (!host) {
+        if (vmm) {
+            cudaDeviceSynchronize();
+            // park the larger never-exported arena in the ctx for the next capture
+            // (freshly freed device memory is slow to reallocate: measured up to
+            // 40 ms per 30 GB); an exported one may still be mapped elsewhere
+            if (ctx && !exported && vmm_size > ctx->dev_arena.size) {
+                ctx->dev_arena.release();
+                ctx->dev_arena = {(uint64_t)p, vmm_size, vmm_h};
+                return;
+            }
+            KC_DRV(cuMemUnmap)((CUdeviceptr)p, vmm_size);
+            KC_DRV(cuMemRelease)(vmm_h);
+            KC_DRV(cuMemAddressFree)((CUdeviceptr)p, vmm_size);
+        } else if (!host) {
             cudaFree(p);
         } else if (ctx && cap >= ctx->host_arena_bytes) {  // park the larger arena
             if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
@@ -68,6 +92,7 @@ struct kc_snapshot {
     };
     std::vector<std::vector<Run>> runs;  // per region, ascending roff, covering ok regions
     uint64_t shared_bytes = 0;           // stored bytes referenced from base snapshots
+    mutable std::vector<std::string> published;  // kc_snapshot_publish directories, revoked on free
     void* warena = nullptr;              // PRE_W: post bytes of W, region i at w_off[i]
     uint64_t w_bytes = 0;
     std::vector<uint64_t> w_off;

@@ -43,7 +43,7 @@ EXPORTED = [
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
     "kc_capture_incr", "kc_snapshot_shared_bytes", "kc_validate_module_vars",
-    "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
+    "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
 ]
 KC_DEP_RAW, KC_DEP_WAW, KC_DEP_WAR = 1, 2, 4
 
@@ -199,10 +199,12 @@ def lib() -> ctypes.CDLL:
         "kc_capture_dev": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
         "kc_restore_dev": (st, [V, V, P(V), P(RestoreReport)]),
         "kc_snapshot_save": (st, [V, V, ctypes.c_char_p]),
+        "kc_snapshot_publish": (st, [V, V, ctypes.c_char_p]),
         "kc_snapshot_bytes": (U64, [V]),
         "kc_snapshot_free": (None, [V]),
         "kc_capture_host": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
         "kc_host_arena_reserve": (st, [V, U64]),
+        "kc_dev_arena_reserve": (st, [V, U64]),
         "kc_snapshot_is_host": (ctypes.c_int, [V]),
         "kc_capture_incr": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, V, ctypes.c_int, P(V),
                                  P(CaptureReport)]),
@@ -345,6 +347,11 @@ class DevSnapshot:
 
     def save(self, directory: str) -> None:
         self.ctx._check(lib().kc_snapshot_save(self.ctx.handle, self.handle, directory.encode()), "kc_snapshot_save")
+
+    def publish(self, directory: str) -> None:
+        """kc_snapshot_publish: metadata to `directory`, region bytes shared from this process's HBM (CUDA IPC)."""
+        self.ctx._check(lib().kc_snapshot_publish(self.ctx.handle, self.handle, directory.encode()),
+                        "kc_snapshot_publish")
 
     def free(self):
         if self.handle and not self.borrowed:
@@ -563,6 +570,10 @@ class Context:
     def capture_host(self, **kw) -> tuple[DevSnapshot, dict]:
         """kc_capture_host: the capture into a pinned host arena."""
         return self.capture_dev(host=True, **kw)
+
+    def dev_arena_reserve(self, nbytes: int) -> None:
+        """kc_dev_arena_reserve: map a device arena ahead of time and park it (0 releases it)."""
+        self._check(lib().kc_dev_arena_reserve(self._h, nbytes), "kc_dev_arena_reserve")
 
     def host_arena_reserve(self, nbytes: int) -> None:
         """kc_host_arena_reserve: pin a host arena ahead of time (0 frees the parked one)."""

@@ -319,6 +319,46 @@ def capture_modvar(a):
     print(json.dumps({"rc": rc, "report": rep, "out_va": out_va, "n": n}))
 
 
+def publish(a):
+    """F1 across processes: capture c1 into a device arena, persist a normal copy
+    for the oracle (<dir>_files), publish the arena (CUDA IPC) to <dir>, and
+    replay it in a fresh process while this one keeps the snapshot alive."""
+    import subprocess
+    ctx = kc.Context(0)
+    sizes = [s.size for s in synth.C1_SPECS]
+    vas = [ctx.alloc(sz) for sz in sizes]
+    nodes_va, heads_va, out_va = vas
+    for va, arr in zip(vas, synth.c1_fill(nodes_va)):
+        _upload(va, arr)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    disp = dict(image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
+                kernarg=synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=int(a.mutate)), mode=kc.KC_MODE_PRE_W)
+    snap, rep = ctx.capture_dev(**disp)
+    out = {"capture": rep, "vas": vas}
+    snap.save(a.dir + "_files")
+    snap.publish(a.dir)
+    # refused: a host snapshot and an incremental one (bytes not in one own arena)
+    hs, _ = ctx.capture_host(**disp)
+    inc, _ = ctx.capture_dev(base=snap, **disp)
+    out["refused"] = []
+    for s_ in (hs, inc):
+        try:
+            s_.publish(a.dir + "_refused")
+            out["refused"].append(0)
+        except kc.KcError as e:
+            out["refused"].append(e.status)
+        s_.free()
+    p = subprocess.run([sys.executable, __file__, "replay", a.dir], capture_output=True, text=True, timeout=300)
+    out["child_rc"] = p.returncode
+    out["child"] = json.loads(p.stdout.strip().splitlines()[-1]) if p.stdout.strip() else {"stderr": p.stderr[-2000:]}
+    snap.free()
+    # the publisher's arena is gone: a late replay must fail cleanly
+    p = subprocess.run([sys.executable, __file__, "replay", a.dir, "--no-prereserve"], capture_output=True, text=True,
+                       timeout=300)
+    out["late"] = json.loads(p.stdout.strip().splitlines()[-1]) if p.stdout.strip() else {"stderr": p.stderr[-2000:]}
+    print(json.dumps(out))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -340,7 +380,8 @@ def main():
     p.add_argument("--cupti", action="store_true")
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
-     "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar}[a.cmd](a)
+     "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar,
+     "publish": publish}[a.cmd](a)
 
 
 if __name__ == "__main__":

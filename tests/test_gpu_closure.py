@@ -335,3 +335,35 @@ def test_module_vars_capture_replay(tmp_path, cupti):
     neg = run("replay", d, env={"KC_NO_MODULE_VARS": "1"})
     assert neg["replay"]["module_vars_restored"] == 0
     assert any(r["differing_bytes"] > 0 for r in neg["validate"])
+
+
+@pytest.mark.parametrize("mutate", [False, True])
+def test_published_device_snapshot_replays_in_another_process(tmp_path, mutate):
+    """F1 across processes (kc_snapshot_publish): the region bytes stay in the
+    capturing process's HBM and a fresh process restores them through CUDA IPC
+    at the captured VAs (copy-in fused with the verify), replays and validates
+    bit-exactly; its dump equals the oracle's closure walk over the normal
+    (file) copy of the same snapshot.  Host and incremental snapshots are
+    refused; once the publisher frees the snapshot a late restore fails
+    cleanly (KC_ERR_STATE)."""
+    import paper_2605_03208_b200.kc as kc
+    from oracle import snapshot
+    d = str(tmp_path / "pub")
+    res = run("publish", d, *(["--mutate"] if mutate else []))
+    assert res["refused"] == [kc.KC_ERR_STATE, kc.KC_ERR_STATE]
+    # the publisher freed the snapshot at the end: the directory is revoked
+    assert os.path.exists(os.path.join(d, "memory", "device_arena.revoked"))
+    assert not any(f.endswith(".bin") for f in os.listdir(os.path.join(d, "memory")))
+    files = d + "_files"
+    assert snapshot.verify(snapshot.load(files))["ok"] == 3
+    child = res["child"]
+    assert res["child_rc"] == 0 and "restore" in child, child
+    assert child["restore"]["verify_mismatch_chunks"] == 0
+    assert child["restore"]["h2d_bytes"] == sum(s for _, s in child["regions"])
+    assert [tuple(x) for x in child["regions"]] == sorted((r.base, r.size) for r in snapshot.load(files).regions)
+    assert child["validate"] and all(r["differing_bytes"] == 0 and r["pass"] == 1 for r in child["validate"])
+    assert child["unexpected_chunks"] == 0
+    pred, (heads_va, out_va, nodes_va) = _walker_prediction(files, mutate)
+    got = np.fromfile(os.path.join(child["dump"], "output", f"region_{out_va:x}.bin"), dtype=np.uint8)
+    assert np.array_equal(got, pred[out_va])
+    assert res["late"].get("restore_status") == kc.KC_ERR_STATE, res["late"]
