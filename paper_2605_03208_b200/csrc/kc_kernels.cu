@@ -1035,6 +1035,10 @@ __device__ __forceinline__ void vec_slow(const uint32_t (&r)[8], const uint32_t 
 // mask (SIMT runs the longest lane's loop: ~12 of 32 lanes were active at
 // 11% mismatch density).  All accumulations are sums and maxima, so the order
 // in which elements are processed does not change a report bit.
+#ifndef KC_GENERIC_SCAN16
+#define KC_GENERIC_SCAN16 0  // 1: 16-bit floats through the generic packed-mask scan (comparison builds)
+#endif
+constexpr bool kGenericScan16 = KC_GENERIC_SCAN16 != 0;
 template <int DT> struct QT_ { using T = uint32_t; };  // 2-byte types: r | a << 16
 template <> struct QT_<KC_DT_F32> { using T = uint2; };
 template <> struct QT_<KC_DT_F64> { using T = ulonglong2; };
@@ -1060,6 +1064,54 @@ __device__ __forceinline__ void q_push(const uint32_t (&r)[8], const uint32_t (&
                 q[pos++] = make_ulonglong2((unsigned long long)r[i - 1] | ((unsigned long long)r[i] << 32),
                                            (unsigned long long)a[i - 1] | ((unsigned long long)a[i] << 32));
         }
+    }
+}
+
+// ---- 16-bit floats (the c3 case): the element flags stay as bits 15 / 31 of
+// eight words per vector instead of a packed mask.  One byte-nonzero word m8
+// per word feeds the differing-byte count (IDP.4A: 128 per nonzero byte) and
+// the halfword flags ((m8 | m8 << 8) & 0x80008000); flagged halves are counted
+// with IDP.4A as well and pushed by testing the word bits directly.
+template <int DT>
+__device__ __forceinline__ uint32_t vec_scan16(const uint32_t (&r)[8], const uint32_t (&a)[8], uint32_t (&m)[8],
+                                               uint32_t& db128, uint32_t& cnt128, Acc& acc) {
+    uint32_t x[8], anyx = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        x[i] = r[i] ^ a[i];
+        anyx |= x[i];
+    }
+    uint32_t any = 0;
+    if (anyx == 0) {  // bit-equal vector: only Inf/NaN references need the element path
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            m[i] = special_word<DT>(r[i]);
+            any |= m[i];
+        }
+    } else {
+        acc.any = 1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t m8 = (((x[i] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x[i]) & 0x80808080u;
+            db128 = __dp4a(m8, 0x01010101u, db128);
+            m[i] = ((m8 | (m8 << 8)) & 0x80008000u) | special_word<DT>(r[i]);
+            any |= m[i];
+        }
+    }
+    if (any) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cnt128 = __dp4a(m[i], 0x01010101u, cnt128);
+    }
+    return any;
+}
+
+template <int DT>
+__device__ __forceinline__ void q_push16(const uint32_t (&r)[8], const uint32_t (&a)[8], const uint32_t (&m)[8],
+                                         uint32_t* q, uint32_t& pos) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (m[i] & 0x00008000u) q[pos++] = __byte_perm(r[i], a[i], 0x5410);
+        if (m[i] & 0x80000000u) q[pos++] = __byte_perm(r[i], a[i], 0x7632);
     }
 }
 
@@ -1154,6 +1206,29 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
             for (int u = 0; u < U; ++u) {
                 ld256(R + 32 * (size_t)(v + 32 * u), rw[u]);
                 ld256(A + 32 * (size_t)(v + 32 * u), aw[u]);
+            }
+            if constexpr (DT_<DT>::F && S == 2 && !kGenericScan16) {
+                uint32_t mw[U][8];
+                uint32_t any = 0, db128 = 0, cnt128 = 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) any |= vec_scan16<DT>(rw[u], aw[u], mw[u], db128, cnt128, acc);
+                acc.dbytes += db128 >> 7;
+                if (__any_sync(0xFFFFFFFFu, any != 0)) {
+                    const uint32_t c = cnt128 >> 7;
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                        if (lane >= d) incl += t;
+                    }
+                    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    uint32_t pos = qn + incl - c;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) q_push16<DT>(rw[u], aw[u], mw[u], q, pos);
+                    qn += total;
+                    if (qn >= 32) q_drain<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+                }
+                continue;
             }
             uint32_t m[U];
             uint32_t any = 0;
