@@ -244,6 +244,24 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
                         const uint64_t* report_nbytes, const uint64_t* bitmap_word0,
                         const kc_tolerance* tol, kc_diff_report* d_reports, uint64_t* d_bitmaps,
                         void* stream);
+/* F2 hash-filtered validation against a HOST-resident reference (SURVEY.md
+ * 8(f) F2: "validate by manifest compare first and H2D only the references of
+ * mismatching chunks"; the report is O4's).
+ * bufs[i].ref = HOST address of the reference bytes (pinned for full PCIe rate),
+ * bufs[i].act = device VA (16-byte aligned), nbytes, dtype; .report and
+ * .bitmap_chunk0 are ignored (one report per buffer, as kc_diff).
+ * ref_manifest (host) = the reference's XXH64 chunk hashes, buffers in order
+ * (a snapshot's manifest).  One K5 pass reads act once (its manifest and the
+ * chunks holding Inf/NaN), K3 marks the chunks whose hash differs from
+ * ref_manifest, only their reference bytes cross PCIe, and K2 runs over exactly
+ * those chunks plus the Inf/NaN chunks with equal hashes (compared with
+ * themselves: equal hashes are equal bytes, reading R34, the same test as W).
+ * reps: n reports (host); h_bitmaps: optional host bitmaps (as kc_diff);
+ * d_act_manifest: optional device output of act's chunk hashes; *h2d_bytes:
+ * bytes moved host->device (manifest + reference chunks). */
+kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const uint64_t* ref_manifest,
+                               const kc_tolerance* tol, kc_diff_report* reps, uint64_t* h_bitmaps,
+                               uint64_t* d_act_manifest, uint64_t* h2d_bytes, void* stream);
 /* Convenience: one report per buffer, results copied to HOST reps[n] and
  * h_bitmaps (concatenated ceil(n_chunks_i/64) words per buffer, may be NULL).
  * Synchronizes the stream. */

@@ -60,7 +60,7 @@ struct kc_ctx {
     uint64_t unknown_frees = 0;
 
     // cached device tables / scratch (stream-ordered; one stream at a time per ctx)
-    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map, dst_tab, gather_tab, chunk_order;
+    kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map, dst_tab, gather_tab, chunk_order, ref_man, ref_stage;
     std::vector<kc::RegionDev> regs_cached;
     kc_ctx_dev_buf pairs, pair_map, dirty;  // F2 (K5) pair table, chunk -> pair map, dirty bitmap
     std::vector<kc::PairDev> pairs_cached;

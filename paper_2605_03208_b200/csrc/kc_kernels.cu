@@ -536,7 +536,10 @@ __device__ __forceinline__ SpecMask spec_mask(int dt) {
     }
 }
 
-template <class CFG>
+// SELF (every pair has ref == act): only the actual slices are staged and the
+// reference words are the actual ones, so one read gives the manifest and the
+// Inf/NaN chunk flags (the host-reference validation's pass, kc_validate_host_ref)
+template <class CFG, bool SELF = false>
 __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     k5_hash_cmp(const PairDev* __restrict__ pairs, int npair, uint64_t C, uint64_t* __restrict__ out,
                 unsigned long long* __restrict__ dirty, const uint32_t* __restrict__ map) {
@@ -591,7 +594,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
 #pragma unroll
         for (int k = 0; k < UPL; ++k) {
             const int u = lane + 32 * k;
-            if (u < 16 * UPC) {
+            if (u < (SELF ? 8 : 16) * UPC) {
                 const int slot = u / UPC, off = (u % UPC) * 16;  // slot 0-7 actual, 8-15 reference
                 const uint32_t g_off = sf * SL + off;
                 if (g_off < u_bytes[k])
@@ -647,9 +650,9 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const uint32_t done = s * (SL / 32);
             const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
             auto word = [&](int t) {
-                const uint64_t a = pa[4 * t], r = pr[4 * t];
+                const uint64_t a = pa[4 * t], r = SELF ? a : pr[4 * t];
                 v = xround_fast(v, a);
-                x |= a ^ r;
+                if (!SELF) x |= a ^ r;
                 sp_lo |= ((uint32_t)r & sm.m_lo) + sm.a_lo;
                 sp_hi |= ((uint32_t)(r >> 32) & sm.m_hi) + sm.a_hi;
             };
@@ -1477,16 +1480,23 @@ cudaError_t kernels_init() {
                                  (int)CpA::kSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k5_hash_cmp<CmpA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)CmpA::kSmem);
     return e;
 }
 
 cudaError_t launch_hash_cmp(const PairDev* d_pairs, int npair, uint64_t C, uint64_t* d_out, uint64_t* d_dirty,
-                            const uint32_t* map, int num_sms, cudaStream_t s) {
+                            const uint32_t* map, int num_sms, cudaStream_t s, bool self) {
     if (C == 0) return cudaSuccess;
     const uint64_t groups = (C + 7) / 8;
     const uint64_t grid = std::min<uint64_t>((groups + CmpA::kWarps - 1) / CmpA::kWarps, (uint64_t)num_sms);
-    k5_hash_cmp<CmpA><<<(unsigned)grid, CmpA::kWarps * 32, CmpA::kSmem, s>>>(
-        d_pairs, npair, C, d_out, reinterpret_cast<unsigned long long*>(d_dirty), map);
+    if (self)
+        k5_hash_cmp<CmpA, true><<<(unsigned)grid, CmpA::kWarps * 32, CmpA::kSmem, s>>>(
+            d_pairs, npair, C, d_out, reinterpret_cast<unsigned long long*>(d_dirty), map);
+    else
+        k5_hash_cmp<CmpA><<<(unsigned)grid, CmpA::kWarps * 32, CmpA::kSmem, s>>>(
+            d_pairs, npair, C, d_out, reinterpret_cast<unsigned long long*>(d_dirty), map);
     return cudaGetLastError();
 }
 

@@ -72,7 +72,7 @@ cudaError_t launch_diff(const SegDev* d_segs, const DiffGroup* groups, int ngrou
                         int equal_nan, int num_sms, cudaStream_t s, const uint64_t* d_filter = nullptr);
 // K5: chunk hashes of every pair's act bytes + dirty bits (OR-ed into the zeroed d_dirty)
 cudaError_t launch_hash_cmp(const PairDev* d_pairs, int npair, uint64_t n_chunks, uint64_t* d_out, uint64_t* d_dirty,
-                            const uint32_t* d_chunk_pair, int num_sms, cudaStream_t s);
+                            const uint32_t* d_chunk_pair, int num_sms, cudaStream_t s, bool self = false);
 cudaError_t launch_gather(const uint64_t* d_src_ptrs, const uint64_t* d_dst_ptrs, const uint64_t* d_lens, int n,
                           cudaStream_t s);
 

@@ -326,7 +326,8 @@ void kc_destroy(kc_ctx* ctx) {
     if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
     ctx->dev_arena.release();
     for (kc_ctx_dev_buf* b : {&ctx->regs, &ctx->segs, &ctx->meta, &ctx->reps, &ctx->bitmaps, &ctx->digest_scratch, &ctx->pairs, &ctx->pair_map, &ctx->dirty,
-                              &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map, &ctx->dst_tab, &ctx->gather_tab, &ctx->chunk_order})
+                              &ctx->tmp_hash, &ctx->tmp_count, &ctx->chunk_map, &ctx->dst_tab, &ctx->gather_tab, &ctx->chunk_order,
+                              &ctx->ref_man, &ctx->ref_stage})
         if (b->p) cudaFree(b->p);
     for (auto& w : ctx->io) {
         for (void* p : w.pinned) cudaFreeHost(p);
@@ -815,6 +816,140 @@ kc_status kc_hash_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const
     if (C) ctx->launches += 1;
     return diff_launch(ctx, b.data(), n, n, nbytes.data(), word0.data(), tol, d_reports, d_bitmaps, stream,
                        chunk0.data(), dirty);
+}
+
+// ------------------------------------------------------------------ F2: validation against a host-resident reference
+kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const uint64_t* ref_manifest,
+                               const kc_tolerance* tol, kc_diff_report* reps, uint64_t* h_bitmaps,
+                               uint64_t* d_act_manifest, uint64_t* h2d_bytes, void* stream) {
+    KC_ENTER(ctx);
+    if (n && (!bufs || !ref_manifest || !reps)) return set_err(ctx, KC_ERR_ARG, "kc_validate_host_ref: null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<PairDev> t(n);
+    std::vector<uint64_t> nbytes(n), word0(n), chunk0(n);
+    uint64_t C = 0, words = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const int es = elem_size(bufs[i].dtype);
+        if (bufs[i].nbytes == 0 || es == 0 || bufs[i].nbytes % es)
+            return set_err(ctx, KC_ERR_ARG, "kc_validate_host_ref: buffer %zu: empty, bad dtype or ragged", i);
+        if (bufs[i].act & 15)
+            return set_err(ctx, KC_ERR_ARG, "kc_validate_host_ref: buffer %zu: device address not 16-byte aligned", i);
+        nbytes[i] = bufs[i].nbytes;
+        word0[i] = words;
+        chunk0[i] = C;
+        const uint64_t nc = (bufs[i].nbytes + kChunk - 1) / kChunk;
+        words += (nc + 63) / 64;
+        t[i] = PairDev{bufs[i].act, bufs[i].act, bufs[i].nbytes, C, bufs[i].dtype, 0};  // self pairs
+        C += nc;
+    }
+    uint64_t moved = 0;
+    // (1) the reference manifest to the device
+    KC_CHECK_CUDA(ctx, ensure(ctx->ref_man, std::max<uint64_t>(1, C) * 8), "cudaMalloc(reference manifest)");
+    if (C) KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->ref_man.p, ref_manifest, C * 8, cudaMemcpyHostToDevice, s),
+                         "H2D reference manifest");
+    moved += C * 8;
+    // (2) K5 over act alone: act's manifest + chunks holding Inf/NaN (or a ragged tail)
+    const bool same = t.size() == ctx->pairs_cached.size() && ctx->pairs.p &&
+                      (t.empty() || memcmp(t.data(), ctx->pairs_cached.data(), t.size() * sizeof(PairDev)) == 0);
+    if (!same) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->pairs, std::max<size_t>(1, t.size()) * sizeof(PairDev)), "cudaMalloc(pairs)");
+        if (!t.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pairs.p, t.data(), t.size() * sizeof(PairDev),
+                                               cudaMemcpyHostToDevice, s), "upload pairs");
+        std::vector<uint32_t> map(C);
+        for (size_t i = 0; i < n; ++i)
+            std::fill(map.begin() + chunk0[i], map.begin() + chunk0[i] + (bufs[i].nbytes + kChunk - 1) / kChunk,
+                      (uint32_t)i);
+        KC_CHECK_CUDA(ctx, ensure(ctx->pair_map, std::max<size_t>(1, map.size()) * 4), "cudaMalloc(pair map)");
+        if (!map.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pair_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
+                          "upload pair map");
+        cudaStreamSynchronize(s);  // pageable `map`
+        ctx->pairs_cached.swap(t);
+    }
+    uint64_t* act_h = d_act_manifest;
+    if (!act_h) {
+        KC_CHECK_CUDA(ctx, ensure(ctx->tmp_hash, std::max<uint64_t>(1, C) * 8), "cudaMalloc(manifest)");
+        act_h = (uint64_t*)ctx->tmp_hash.p;
+    }
+    const uint64_t nw = (C + 63) / 64;
+    KC_CHECK_CUDA(ctx, ensure(ctx->dirty, std::max<uint64_t>(1, 2 * nw) * 8 + 8), "cudaMalloc(dirty bitmaps)");
+    uint64_t* spec = (uint64_t*)ctx->dirty.p;  // [0, nw): Inf/NaN chunks; [nw, 2nw): hash-dirty chunks
+    if (C) KC_CHECK_CUDA(ctx, cudaMemsetAsync(spec, 0, nw * 8, s), "zero dirty bitmap");
+    KC_CHECK_CUDA(ctx, launch_hash_cmp((const PairDev*)ctx->pairs.p, (int)n, C, act_h, spec,
+                                       (const uint32_t*)ctx->pair_map.p, ctx->num_sms, s, true),
+                  "launch K5 (self)");
+    // (3) K3: chunks whose hash differs from the reference's
+    KC_CHECK_CUDA(ctx, launch_written((const uint64_t*)ctx->ref_man.p, act_h, C, spec + nw, spec + 2 * nw,
+                                      ctx->num_sms, s),
+                  "launch K3");
+    if (C) ctx->launches += 2;
+    std::vector<uint64_t> bm(2 * nw);
+    if (C) KC_CHECK_CUDA(ctx, cudaMemcpyAsync(bm.data(), spec, 2 * nw * 8, cudaMemcpyDeviceToHost, s), "D2H bitmaps");
+    KC_CHECK_CUDA(ctx, cudaStreamSynchronize(s), "kc_validate_host_ref sync");
+    // (4) the reference bytes of hash-dirty chunks, host -> device staging (runs of
+    // consecutive chunks in one copy); K2 segments: those against the staged
+    // reference, Inf/NaN chunks with equal hashes against themselves (R34)
+    std::vector<kc_buffer> segs;
+    for (size_t i = 0; i < n; ++i)  // zero-length segments carry each report's dtype (n_elems, pass rule)
+        segs.push_back(kc_buffer{bufs[i].act, bufs[i].act, 0, bufs[i].dtype, (int32_t)i, 0});
+    // flagged chunks (hash-dirty or Inf/NaN), ascending: scan the bitmap words
+    std::vector<uint64_t> flagged;
+    uint64_t ndirty = 0;
+    for (uint64_t w = 0; w < nw; ++w) {
+        uint64_t m = bm[w] | bm[nw + w];
+        ndirty += __builtin_popcountll(bm[nw + w]);
+        while (m) {
+            flagged.push_back(64 * w + __builtin_ctzll(m));
+            m &= m - 1;
+        }
+    }
+    KC_CHECK_CUDA(ctx, ensure(ctx->ref_stage, std::max<uint64_t>(1, ndirty) * kChunk), "cudaMalloc(reference stage)");
+    auto hdirty = [&](uint64_t g) { return (bm[nw + g / 64] >> (g % 64)) & 1; };
+    uint64_t so = 0;
+    size_t i = 0;  // buffer of the current chunk (chunks ascend, so does i)
+    for (size_t f = 0; f < flagged.size();) {
+        const uint64_t g = flagged[f];
+        while (i + 1 < n && chunk0[i + 1] <= g) ++i;
+        const uint64_t k = g - chunk0[i], nc = (bufs[i].nbytes + kChunk - 1) / kChunk;
+        if (!hdirty(g)) {  // equal hashes, Inf/NaN inside: compared with itself
+            const uint64_t off = k * kChunk, len = std::min<uint64_t>(kChunk, bufs[i].nbytes - off);
+            segs.push_back(kc_buffer{bufs[i].act + off, bufs[i].act + off, len, bufs[i].dtype, (int32_t)i, k});
+            ++f;
+            continue;
+        }
+        uint64_t e = k + 1;  // the run of hash-dirty chunks [k, e) of buffer i
+        size_t fe = f + 1;
+        while (e < nc && fe < flagged.size() && flagged[fe] == chunk0[i] + e && hdirty(flagged[fe])) {
+            ++e;
+            ++fe;
+        }
+        const uint64_t off = k * kChunk, len = std::min<uint64_t>(e * kChunk, bufs[i].nbytes) - off;
+        uint8_t* dst = (uint8_t*)ctx->ref_stage.p + so;
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(dst, (const uint8_t*)bufs[i].ref + off, len, cudaMemcpyHostToDevice, s),
+                      "H2D dirty reference chunks");
+        moved += len;
+        for (uint64_t c = k; c < e; ++c) {
+            const uint64_t co = c * kChunk, cl = std::min<uint64_t>(kChunk, bufs[i].nbytes - co);
+            segs.push_back(kc_buffer{(uint64_t)dst + (co - off), bufs[i].act + co, cl, bufs[i].dtype, (int32_t)i, c});
+        }
+        so += e * kChunk - off;
+        f = fe;
+    }
+    // (5) K2 over exactly those chunks; empty reports for the rest come out of diff_launch's zero-fill
+    KC_CHECK_CUDA(ctx, ensure(ctx->reps, std::max<size_t>(1, n) * sizeof(kc_diff_report)), "cudaMalloc(reports)");
+    KC_CHECK_CUDA(ctx, ensure(ctx->bitmaps, std::max<uint64_t>(1, words) * 8), "cudaMalloc(bitmaps)");
+    kc_status st = diff_launch(ctx, segs.data(), segs.size(), n, nbytes.data(), word0.data(), tol,
+                               (kc_diff_report*)ctx->reps.p, (uint64_t*)ctx->bitmaps.p, stream, nullptr, nullptr);
+    if (st != KC_OK) return st;
+    KC_CHECK_CUDA(ctx, cudaMemcpyAsync(reps, ctx->reps.p, n * sizeof(kc_diff_report), cudaMemcpyDeviceToHost, s),
+                  "D2H reports");
+    if (h_bitmaps && words)
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(h_bitmaps, ctx->bitmaps.p, words * 8, cudaMemcpyDeviceToHost, s),
+                      "D2H bitmaps");
+    KC_CHECK_CUDA(ctx, cudaStreamSynchronize(s), "kc_validate_host_ref sync");
+    if (h2d_bytes) *h2d_bytes = moved;
+    return KC_OK;
 }
 
 kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol, kc_diff_report* reps,

@@ -43,7 +43,7 @@ EXPORTED = [
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
     "kc_capture_incr", "kc_snapshot_shared_bytes", "kc_validate_module_vars",
-    "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
+    "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_validate_host_ref", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
 ]
 KC_DEP_RAW, KC_DEP_WAW, KC_DEP_WAR = 1, 2, 4
 
@@ -189,6 +189,7 @@ def lib() -> ctypes.CDLL:
         "kc_diff_async": (st, [V, P(Buffer), SZ, SZ, P(U64), P(U64), P(Tolerance), V, V, V]),
         "kc_hash_diff_async": (st, [V, P(Buffer), SZ, P(Tolerance), V, V, V, V, V]),
         "kc_diff": (st, [V, P(Buffer), SZ, P(Tolerance), P(DiffReport), P(U64), V]),
+        "kc_validate_host_ref": (st, [V, P(Buffer), SZ, V, P(Tolerance), P(DiffReport), P(U64), V, P(U64), V]),
         "kc_capture": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_char_p, ctypes.c_int, P(CaptureReport)]),
         "kc_restore": (st, [V, ctypes.c_char_p, P(V), P(RestoreReport)]),
         "kc_prereserve": (st, [ctypes.c_char_p, P(U64)]),
@@ -498,6 +499,27 @@ class Context:
             out_b.append([bm[o + k] for k in range(w)])
             o += w
         return [reps[i].as_dict() for i in range(n)], out_b
+
+    def validate_host_ref(self, bufs, ref_manifest_ptr: int, atol: float = 1e-8, rtol: float = 1e-5,
+                          equal_nan: bool = False, stream: int = 0, with_bitmaps: bool = True,
+                          d_act_manifest: int = 0):
+        """kc_validate_host_ref over (host ref address, device act VA, nbytes, dtype) buffers and a host
+        reference manifest (address of the u64 chunk hashes) -> (reports, bitmaps, h2d bytes)."""
+        n = len(bufs)
+        arr = self._buffers(bufs)
+        reps = (DiffReport * max(1, n))()
+        words = [((b.nbytes + KC_CHUNK_BYTES - 1) // KC_CHUNK_BYTES + 63) // 64 for b in arr[:n]]
+        bm = (ctypes.c_uint64 * max(1, sum(words)))()
+        tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
+        moved = ctypes.c_uint64(0)
+        self._check(lib().kc_validate_host_ref(self._h, arr, n, ref_manifest_ptr, ctypes.byref(tol), reps,
+                                               bm if with_bitmaps else None, d_act_manifest or None,
+                                               ctypes.byref(moved), stream or None), "kc_validate_host_ref")
+        out_b, o = [], 0
+        for w in words:
+            out_b.append([bm[o + k] for k in range(w)])
+            o += w
+        return [reps[i].as_dict() for i in range(n)], out_b, int(moved.value)
 
     def diff_async(self, bufs, n_reports: int, report_nbytes: Sequence[int], d_reports: int,
                    bitmap_word0: Sequence[int] | None = None, d_bitmaps: int = 0, atol: float = 1e-8,
