@@ -125,6 +125,9 @@ def verify(snap: Snapshot) -> dict:
     cub = os.path.join(d, "kernel.cubin")
     if snap.dispatch.get("code_object_bytes"):
         assert os.path.getsize(cub) == snap.dispatch["code_object_bytes"]
+    if snap.dispatch.get("code_object_sha256"):   # the code object's identity
+        import hashlib
+        assert hashlib.sha256(open(cub, "rb").read()).hexdigest() == snap.dispatch["code_object_sha256"]
     ok_bases, ok_sizes, ok_digs = [], [], []
     n_written = 0
     for r in snap.regions:

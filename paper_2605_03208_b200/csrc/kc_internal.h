@@ -34,6 +34,7 @@ struct ModVarDecl {
     uint64_t size;
 };
 size_t image_size(const void* img, size_t hint);  // ELF64 / fatbin extent (hint wins when nonzero)
+std::string sha256_hex(const uint8_t* data, size_t n);  // code-object identity (dispatch.json)
 std::vector<ModVarDecl> image_module_vars(const uint8_t* img, size_t n);
 }  // namespace kc
 struct ModVarState {

@@ -390,8 +390,9 @@ struct LogRegion {
 };
 
 std::string dispatch_json(int mode, const std::string& mangled, const uint32_t grid[3], const uint32_t block[3],
-                          uint32_t smem, uint32_t kernarg_size, int device, size_t image_size,
+                          uint32_t smem, uint32_t kernarg_size, int device, const std::vector<uint8_t>& image,
                           const std::vector<std::pair<size_t, size_t>>& layout) {
+    const size_t image_size = image.size();
     int cc_major = 0, cc_minor = 0;
     cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device);
     cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, device);
@@ -412,7 +413,8 @@ std::string dispatch_json(int mode, const std::string& mangled, const uint32_t g
         snprintf(b, sizeof b, "%s{\"offset\": %zu, \"size\": %zu}", i ? ", " : "", layout[i].first, layout[i].second);
         j += b;
     }
-    j += "],\n  \"hash\": {\"algo\": \"xxh64\", \"seed\": 0, \"chunk_bytes\": 65536}\n}\n";
+    j += "],\n  \"code_object_sha256\": \"" + (image.empty() ? std::string() : sha256_hex(image.data(), image.size())) +
+         "\",\n  \"hash\": {\"algo\": \"xxh64\", \"seed\": 0, \"chunk_bytes\": 65536}\n}\n";
     return j;
 }
 
@@ -648,7 +650,7 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
 
     auto write_metadata = [&](bool post_digests) -> bool {
         const std::string j = dispatch_json(mode, mangled, d->grid, d->block, d->smem_bytes, d->kernarg_size,
-                                            ctx->device, mc.image.size(), layout);
+                                            ctx->device, mc.image, layout);
         if (!write_text(dir + "/dispatch.json", j)) return false;
         if (!write_file(dir + "/kernarg.bin", d->kernarg, d->kernarg ? d->kernarg_size : 0)) return false;
         if (!mc.image.empty() && !write_file(dir + "/kernel.cubin", mc.image.data(), mc.image.size())) return false;
@@ -1046,6 +1048,9 @@ kc_status load_desc_files(kc_ctx* ctx, const std::string& dir, SnapDesc& d, kc_r
         return set_err(ctx, KC_ERR_FORMAT, "kernarg.bin has %zu bytes, dispatch.json says %llu", d.kernarg.size(),
                        (unsigned long long)ksz);
     read_bin(dir + "/kernel.cubin", d.image);
+    if (const kcj::Value* sh = dv.get("code_object_sha256"))  // identity of the captured code object
+        if (!sh->s.empty() && (d.image.empty() || sha256_hex(d.image.data(), d.image.size()) != sh->s))
+            return set_err(ctx, KC_ERR_FORMAT, "kernel.cubin does not match dispatch.json code_object_sha256");
     // F3: module variables (optional file)
     std::string mtext;
     if (kcj::read_file(dir + "/module_vars.json", mtext)) {
@@ -2318,7 +2323,7 @@ static kc_status save_impl(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c,
     unlink((dir + "/capture_complete").c_str());
     // metadata first
     if (!write_text(dir + "/dispatch.json", dispatch_json(D.mode, D.mangled, D.grid, D.block, D.smem,
-                                                          (uint32_t)D.kernarg.size(), ctx->device, D.image.size(),
+                                                          (uint32_t)D.kernarg.size(), ctx->device, D.image,
                                                           D.layout)) ||
         !write_file(dir + "/kernarg.bin", D.kernarg.data(), D.kernarg.size()) ||
         (!D.image.empty() && !write_file(dir + "/kernel.cubin", D.image.data(), D.image.size())) ||

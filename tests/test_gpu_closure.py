@@ -367,3 +367,24 @@ def test_published_device_snapshot_replays_in_another_process(tmp_path, mutate):
     got = np.fromfile(os.path.join(child["dump"], "output", f"region_{out_va:x}.bin"), dtype=np.uint8)
     assert np.array_equal(got, pred[out_va])
     assert res["late"].get("restore_status") == kc.KC_ERR_STATE, res["late"]
+
+
+def test_tampered_code_object_is_refused(tmp_path):
+    """dispatch.json records the code object's SHA-256 (the paper matches HSACO
+    blobs by SHA-256); the O1 checker recomputes it with
+    hashlib, and a restore of a snapshot whose kernel.cubin was altered fails
+    with KC_ERR_FORMAT before anything is mapped."""
+    import hashlib
+    import paper_2605_03208_b200.kc as kc
+    from oracle import snapshot
+    d = str(tmp_path / "cap")
+    run("capture-c1", d)
+    disp = json.load(open(os.path.join(d, "dispatch.json")))
+    cub = os.path.join(d, "kernel.cubin")
+    assert disp["code_object_sha256"] == hashlib.sha256(open(cub, "rb").read()).hexdigest()
+    snapshot.verify(snapshot.load(d))
+    b = bytearray(open(cub, "rb").read())
+    b[len(b) // 2] ^= 0x40
+    open(cub, "wb").write(bytes(b))
+    res = run("replay", d)
+    assert res.get("restore_status") == kc.KC_ERR_FORMAT, res
