@@ -1997,12 +1997,14 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     // every live byte, so the plan does not depend on the hashes and one HBM
     // read yields both the pre-manifest and the stored copy (KC_NO_FUSED_CAPTURE=1:
     // K1 then copies, for comparison).
-    bool fused = !base && !host && mode == KC_MODE_PRE_W && !getenv("KC_NO_FUSED_CAPTURE");
-    for (auto& r : live) fused = fused && (r.base & 15) == 0;
-    kc_status st = KC_OK;
-    if (fused) {
-        st = ensure_stream(ctx);
-        if (st != KC_OK) return fail(st);
+    bool full_dev = !base && !host && !getenv("KC_NO_FUSED_CAPTURE");
+    for (auto& r : live) full_dev = full_dev && (r.base & 15) == 0;
+    const bool fused = full_dev && mode == KC_MODE_PRE_W;       // K6 on the pre-state
+    const bool fused_post = full_dev && mode == KC_MODE_POST;   // K6 on the post-state
+    // every ok region one run of this snapshot's own arena; dst = the arena address per live region
+    auto plan_full = [&](std::vector<uint64_t>& dst) -> kc_status {
+        kc_status s2 = ensure_stream(ctx);
+        if (s2 != KC_OK) return s2;
         sn->runs.assign(D.regions.size(), {});
         std::vector<uint64_t> aoff(D.regions.size(), 0);
         uint64_t total = 0;
@@ -2013,15 +2015,14 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
             total += D.regions[i].r.size;
         }
         sn->arena_bytes = total;
-        std::vector<uint64_t> dst;
         if (total) {
             auto ab = std::make_shared<ArenaBuf>();
             ab->ctx = ctx;
             if (!vmm_arena_alloc(ctx, *ab, total) && arena_alloc(ctx, false, &ab->p, total, &ab->cap) != cudaSuccess) {
                 cudaGetLastError();
                 ab->p = nullptr;
-                return fail(set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: cannot allocate a %llu-byte arena",
-                                    (unsigned long long)total));
+                return set_err(ctx, KC_ERR_NOMEM, "kc_capture_dev: cannot allocate a %llu-byte arena",
+                               (unsigned long long)total);
             }
             sn->arena = ab;
             for (size_t i = 0; i < D.regions.size(); ++i) {
@@ -2031,6 +2032,13 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
                 dst.push_back(src);
             }
         }
+        return KC_OK;
+    };
+    kc_status st = KC_OK;
+    if (fused) {
+        std::vector<uint64_t> dst;
+        st = plan_full(dst);
+        if (st != KC_OK) return fail(st);
         trace("plan + arena alloc", tl);
         const double tc = now_s();
         st = hash_regions_sync(ctx, live, pre_h, &pre_dig, &pre_snap, nullptr, cs, dst.empty() ? nullptr : dst.data());
@@ -2169,12 +2177,23 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         if (mst != KC_OK) return fail(mst);
         D.modvars = std::move(mc.vars);
     }
-    // ---- K1 post-manifest + W
+    // ---- K1 post-manifest + W (POST full capture: K6 also stores the post-state)
+    std::vector<uint64_t> post_dst;
+    if (fused_post) {
+        st = plan_full(post_dst);
+        if (st != KC_OK) return fail(st);
+        trace("plan + arena alloc", tl);
+    }
     t = now_s();
-    st = hash_regions_sync(ctx, live, post_h, &post_dig, &post_snap, nullptr, cs);
+    st = hash_regions_sync(ctx, live, post_h, &post_dig, &post_snap, nullptr, cs,
+                           post_dst.empty() ? nullptr : post_dst.data());
     if (st != KC_OK) return fail(st);
     rep.t_hash_post_s = now_s() - t;
-    trace("K1 post", tl);
+    if (fused_post) {
+        t_copy += rep.t_hash_post_s;
+        rep.dma_calls += live.empty() ? 0 : 1;
+    }
+    trace(fused_post ? "K6 post hash + copy" : "K1 post", tl);
     {
         size_t j = 0;  // (W from the manifests: host loop over the chunks)
         for (size_t i = 0; i < D.regions.size(); ++i) {
@@ -2200,8 +2219,10 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     D.snapshot_digest = mode == KC_MODE_PRE_W ? pre_snap : post_snap;
     trace("W sets", tl);
     if (mode == KC_MODE_POST) {
-        st = snapshot_regions(post_h);
-        if (st != KC_OK) return fail(st);
+        if (!fused_post) {
+            st = snapshot_regions(post_h);
+            if (st != KC_OK) return fail(st);
+        }
     } else if (rep.written_chunks) {
         uint64_t wtot = 0;
         for (auto& sr : D.regions) {

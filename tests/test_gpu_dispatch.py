@@ -55,8 +55,9 @@ def test_large_dynamic_smem_capture_replay(env):
     snap.free()
 
 
+@pytest.mark.parametrize("mode", ["pre_w", "post"])
 @pytest.mark.parametrize("fused", [True, False])
-def test_device_capture_ragged_regions(env, tmp_path, fused, monkeypatch):
+def test_device_capture_ragged_regions(env, tmp_path, fused, mode, monkeypatch):
     """K6 (fused hash + copy) on ragged regions: sizes 1 .. 3 chunks + 40 B,
     16-byte aligned inside one allocation, including sub-32-byte tails and
     regions shorter than one hash stripe.  The persisted snapshot is checked
@@ -82,7 +83,10 @@ def test_device_capture_ragged_regions(env, tmp_path, fused, monkeypatch):
     xy = base + offs[-1]
     image = open(synth.FIXTURE_CUBIN, "rb").read()
     snap, rep = ctx.capture_dev(image=image, mangled="kc_fixture_axpy_u32", grid=(4, 1, 1), block=(256, 1, 1),
-                                kernarg=struct.pack("<QQII", xy, xy + 4 * 4096, 1024, 3), regions=regions)
+                                kernarg=struct.pack("<QQII", xy, xy + 4 * 4096, 1024, 3), regions=regions,
+                                mode=kc.KC_MODE_PRE_W if mode == "pre_w" else kc.KC_MODE_POST)
+    if mode == "post":            # the stored state is the post-dispatch one
+        before = buf.cpu().numpy().copy()
     d = str(tmp_path / "snap")
     snap.save(d)
     snap.free()
