@@ -63,6 +63,9 @@ struct kc_ctx {
     // cached device tables / scratch (stream-ordered; one stream at a time per ctx)
     kc_ctx_dev_buf regs, segs, meta, reps, bitmaps, digest_scratch, tmp_hash, tmp_count, chunk_map, dst_tab, gather_tab, chunk_order, ref_man, ref_stage;
     std::vector<kc::RegionDev> regs_cached;
+    std::vector<kc_region> regs_input;  // the kc_region list behind regs_cached (fast same-input check)
+    bool regs_input_sorted = false;
+    uint64_t regs_input_chunks = 0;
     kc_ctx_dev_buf pairs, pair_map, dirty;  // F2 (K5) pair table, chunk -> pair map, dirty bitmap
     std::vector<kc::PairDev> pairs_cached;
     std::vector<uint8_t> diff_key;  // K2 plan cache (raw inputs of the last kc_diff_async)

@@ -550,15 +550,31 @@ kc_status kc::hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_
                         uint64_t* d_region_digest, uint64_t* d_snapshot_digest, void* stream, const uint64_t* h_dst) {
     KC_ENTER(ctx);
     if (n && !regions) return set_err(ctx, KC_ERR_ARG, "kc_hash: regions is NULL");
-    for (size_t i = 0; i < n; ++i) {
-        if (regions[i].size == 0) return set_err(ctx, KC_ERR_ARG, "kc_hash: region %zu has size 0", i);
-        if (d_snapshot_digest && i > 0 && regions[i].base < regions[i - 1].base + regions[i - 1].size)
-            return set_err(ctx, KC_ERR_ARG, "kc_hash: regions not sorted/non-overlapping (snapshot digest, R25)");
-    }
     cudaStream_t s = (cudaStream_t)stream;
     uint64_t C = 0;
-    kc_status st = upload_regions(ctx, regions, n, s, &C);
-    if (st != KC_OK) return st;
+    // the same region list as the previous call (hashing one set again and again:
+    // pre/post manifests, every validation): one memcmp replaces the per-region
+    // checks and the table rebuild (0.5 ms of host time per call at 100k regions)
+    const bool same_input = n == ctx->regs_input.size() && n && ctx->regs.p &&
+                            memcmp(regions, ctx->regs_input.data(), n * sizeof(kc_region)) == 0 &&
+                            (!d_snapshot_digest || ctx->regs_input_sorted);
+    if (same_input) {
+        C = ctx->regs_input_chunks;
+    } else {
+        bool sorted = true;
+        for (size_t i = 0; i < n; ++i) {
+            if (regions[i].size == 0) return set_err(ctx, KC_ERR_ARG, "kc_hash: region %zu has size 0", i);
+            if (i > 0 && regions[i].base < regions[i - 1].base + regions[i - 1].size) sorted = false;
+        }
+        if (d_snapshot_digest && !sorted)
+            return set_err(ctx, KC_ERR_ARG, "kc_hash: regions not sorted/non-overlapping (snapshot digest, R25)");
+        kc_status st0 = upload_regions(ctx, regions, n, s, &C);
+        if (st0 != KC_OK) return st0;
+        ctx->regs_input.assign(regions, regions + n);
+        ctx->regs_input_sorted = sorted;
+        ctx->regs_input_chunks = C;
+    }
+    kc_status st = KC_OK;
     if (C && !d_chunk_hash) return set_err(ctx, KC_ERR_ARG, "kc_hash: d_chunk_hash is NULL");
     if (h_dst) {
         if (!ctx->regs_aligned) return set_err(ctx, KC_ERR_ARG, "K6: regions must be 16-byte aligned");
@@ -640,25 +656,29 @@ static kc_status diff_launch(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, 
     // segment/meta tables (validation of the same buffer set every replay)
     const size_t key_bytes = n_bufs * sizeof(kc_buffer) + n_reports * 8 * (bitmap_word0 ? 2 : 1) + 8 +
                              (filter_chunk0 ? n_bufs * 8 : 0) + 1;
-    std::vector<uint8_t> key(key_bytes);
-    {
-        uint8_t* k = key.data();
-        *k++ = filter_chunk0 ? 1 : 0;
-        if (filter_chunk0 && n_bufs) {
-            memcpy(k, filter_chunk0, n_bufs * 8);
-            k += n_bufs * 8;
+    // the key's pieces in order: filter flag, filter_chunk0, bufs, report_nbytes,
+    // bitmap_word0, n_reports; compared in place first (no copy when it hits)
+    const uint64_t nr = n_reports;
+    struct Piece { const void* p; size_t n; };
+    const uint8_t flag = filter_chunk0 ? 1 : 0;
+    const Piece pieces[] = {{&flag, 1},
+                            {filter_chunk0, filter_chunk0 ? n_bufs * 8 : 0},
+                            {bufs, n_bufs * sizeof(kc_buffer)},
+                            {report_nbytes, n_reports * 8},
+                            {bitmap_word0, bitmap_word0 ? n_reports * 8 : 0},
+                            {&nr, 8}};
+    bool cached = ctx->diff_key.size() == key_bytes && ctx->segs.p && ctx->meta.p;
+    for (size_t i = 0, o = 0; cached && i < sizeof pieces / sizeof pieces[0]; o += pieces[i].n, ++i)
+        cached = pieces[i].n == 0 || memcmp(ctx->diff_key.data() + o, pieces[i].p, pieces[i].n) == 0;
+    std::vector<uint8_t> key;
+    if (!cached) {
+        key.resize(key_bytes);
+        size_t o = 0;
+        for (const Piece& pc : pieces) {
+            if (pc.n) memcpy(key.data() + o, pc.p, pc.n);
+            o += pc.n;
         }
-        if (n_bufs) memcpy(k, bufs, n_bufs * sizeof(kc_buffer));
-        k += n_bufs * sizeof(kc_buffer);
-        if (n_reports) memcpy(k, report_nbytes, n_reports * 8);
-        k += n_reports * 8;
-        if (bitmap_word0 && n_reports) memcpy(k, bitmap_word0, n_reports * 8);
-        k += bitmap_word0 ? n_reports * 8 : 0;
-        const uint64_t nr = n_reports;
-        memcpy(k, &nr, 8);
     }
-    const bool cached = ctx->diff_key.size() == key.size() && ctx->segs.p && ctx->meta.p &&
-                        memcmp(ctx->diff_key.data(), key.data(), key.size()) == 0;
     std::vector<DiffGroup> groups;
     uint64_t bitmap_words = 0;
     if (cached) {
