@@ -406,6 +406,38 @@ kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t
 kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out);
 void kc_release(kc_restored* h);
 
+/* ---- A3 interposed mode ----------------
+ * Capture a dispatch of an application that runs unmodified.  With
+ * kc_track_install active (the tracker sees its allocations and module loads),
+ * arm the capture of launch number `index` (0-based, counting launches whose
+ * kernel name contains `target`; NULL/"" = every kernel).  The CUPTI launch
+ * callback brackets that cuLaunchKernel / cuLaunchKernelEx: at ENTER it takes
+ * the pre-state of every tracked region into an in-memory snapshot (device
+ * arena, or pinned host arena when host != 0), the application's launch then
+ * proceeds (exactly once, even if the capture fails), and at EXIT the post
+ * manifest and W are taken before the application's call returns.  The kernarg
+ * buffer is packed from kernelParams (cuFuncGetParamInfo layout) or copied from
+ * CU_LAUNCH_PARAM_BUFFER_POINTER; the code object is the one the module-load
+ * hook recorded.  dir != NULL/"": the snapshot is also saved there
+ * (kc-snapshot/1).  One capture per arming.  kc_track_install arms from the
+ * environment when KC_CAPTURE_DIR is set (KC_TARGET, KC_DISPATCH_INDEX,
+ * KC_CAPTURE_MODE=pre_w|post).  KC_ERR_STATE if the hook is not installed. */
+kc_status kc_interpose_arm(kc_ctx* ctx, const char* target, uint64_t index, const char* dir, kc_capture_mode mode,
+                           int host);
+/* *state: 0 idle, 1 armed, 2 capturing, 3 captured, -1 failed (the call then
+ * returns the capture's error); *launches_seen: matching launches counted so
+ * far; rep: the capture report once captured.  Any output may be NULL. */
+kc_status kc_interpose_status(kc_ctx* ctx, int* state, uint64_t* launches_seen, kc_capture_report* rep);
+/* The captured in-memory snapshot; ownership passes to the caller (kc_snapshot_free). */
+kc_status kc_interpose_take(kc_ctx* ctx, kc_snapshot** out);
+/* F4 from an unmodified application: capture the `count` consecutive matching
+ * launches [first, first + count) as a sequence (step k = PRE_W state before
+ * launch k, incremental against step k-1, as kc_capture_seq); *state reaches 3
+ * after the last one.  kc_interpose_take_seq hands over the kc_sequence (its
+ * dependency matrix computed; KC_ERR_STATE if the region set changed between
+ * steps or the sequence is incomplete). */
+kc_status kc_interpose_arm_seq(kc_ctx* ctx, const char* target, uint64_t first, uint64_t count, int host);
+
 /* ---- F4 multi-kernel capture -------------------------
  * PAPER.md:1855-1862 ("capturing a sequence of dependent kernels for joint
  * replay remains future work") and 1917-1918 ("multi-kernel capture for
@@ -483,6 +515,8 @@ typedef struct {
  * step abort the replay (reports of earlier steps are filled). */
 kc_status kc_replay_seq(kc_ctx* ctx, const kc_sequence* q, const kc_seq_replay_opts* o, kc_seq_step_report* reps,
                         kc_restored** keep);
+/* The sequence armed with kc_interpose_arm_seq (ownership passes to the caller). */
+kc_status kc_interpose_take_seq(kc_ctx* ctx, kc_sequence** out);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,7 @@ FIXTURE_VARIANTS = {os.path.join(ROOT, "synth", "kc_fixtures_recompiled.cubin"):
 ATTN_SRC = os.path.join(ROOT, "synth", "kc_attn_fwd.cu")
 ATTN_BLOCK_N = (32, 64, 128)
 ATTN_CUBINS = {bn: os.path.join(ROOT, "synth", f"kc_attn_fwd_n{bn}.cubin") for bn in ATTN_BLOCK_N}
-SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu", "kc_module.cu", "kc_sequence.cu"]
+SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu", "kc_module.cu", "kc_sequence.cu", "kc_interpose.cu"]
 HEADERS = ["kc_kernels.cuh", "kc_internal.h", "kc_json.h", "kc_snapshot_types.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")

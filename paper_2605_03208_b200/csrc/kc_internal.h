@@ -5,6 +5,7 @@
 
 #include <cstdarg>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -42,6 +43,8 @@ struct ModVarState {
     uint64_t size = 0;
     std::vector<uint8_t> pre, post;  // bytes before / after the captured dispatch
 };
+
+struct kc_interpose;  // A3 interposed-mode state (kc_interpose.cu)
 
 struct kc_ctx_dev_buf {
     void* p = nullptr;
@@ -124,6 +127,7 @@ struct kc_ctx {
     uint64_t host_arena_bytes = 0;
     std::map<uint64_t, uint64_t> heap_free;
     uint64_t launches = 0;
+    kc_interpose* interpose = nullptr;  // armed / in-flight interposed capture
 };
 
 struct kc_restored_region {
@@ -174,6 +178,17 @@ struct kc_restored {
 
 namespace kc {
 
+// Set on a thread while it runs inside the library: the CUPTI hook ignores the
+// driver calls made then (the library's own scratch, arenas and kernel launches
+// are not application state).  KC_ENTER and the capture/restore entry points hold one.
+extern thread_local int t_internal;
+struct Internal {
+    Internal() { ++t_internal; }
+    ~Internal() { --t_internal; }
+    Internal(const Internal&) = delete;
+    Internal& operator=(const Internal&) = delete;
+};
+
 // error helpers
 kc_status set_err(kc_ctx* ctx, kc_status st, const char* fmt, ...);
 kc_status cuda_err(kc_ctx* ctx, cudaError_t e, const char* what);
@@ -204,6 +219,17 @@ kc_status hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d
 kc_status validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n, const kc_tolerance* tol,
                         kc_diff_report* reps, size_t cap_reports, size_t* n_reports_out, uint64_t* unexpected_chunks,
                         bool merge);
+// A3 interposed mode: the in-memory capture of every tracked region around a
+// dispatch the application launches itself (`forward` returns once it has run)
+kc_status capture_interposed(kc_ctx* ctx, const kc_dispatch* d, kc_capture_mode mode, bool host,
+                             const std::function<CUresult()>& forward, kc_snapshot** out, kc_capture_report* rep,
+                             const kc_snapshot* base = nullptr);
+// F4: a kc_sequence from step snapshots (ownership moves in; deps computed)
+kc_status make_sequence(kc_ctx* ctx, std::vector<kc_snapshot*>& steps, kc_sequence** out);
+// CUPTI launch callbacks (kc_interpose.cu)
+void interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata);
+void interpose_destroy(kc_ctx* ctx);
+void interpose_arm_from_env(kc_ctx* ctx);
 // re-point a restored handle at another snapshot of the same regions (dispatch,
 // W, post manifest, stashes) without touching the mapped memory (F4 sequences)
 kc_status restored_rebind(kc_ctx* ctx, kc_restored* h, const kc_snapshot* sn);

@@ -12,6 +12,10 @@
 #include "kc_internal.h"
 
 namespace kc {
+thread_local int t_internal = 0;
+}  // namespace kc
+
+namespace kc {
 
 // Missing entry points resolve to stubs returning CUDA_ERROR_NOT_INITIALIZED
 // through the ok flag checked in bind_device().
@@ -226,11 +230,11 @@ kc_status free_alloc(kc_ctx* ctx, uint64_t dptr, bool track) {
         KC_CHECK_CU(ctx, KC_DRV(cuMemUnmap)((CUdeviceptr)dptr, va.reserved), "cuMemUnmap");
         KC_DRV(cuMemRelease)(va.h);
         heap_put(ctx, dptr, va.reserved);  // the VA stays in the ctx heap
-        if (track && !ctx->cupti_installed) kc_track(ctx, KC_EV_UNMAP, dptr, 0, ctx->device, KC_KIND_VMM);
+        if (track) kc_track(ctx, KC_EV_UNMAP, dptr, 0, ctx->device, KC_KIND_VMM);
         return KC_OK;
     }
     KC_CHECK_CU(ctx, KC_DRV(cuMemFree)((CUdeviceptr)dptr), "cuMemFree");
-    if (track && !ctx->cupti_installed) kc_track(ctx, KC_EV_FREE, dptr, 0, ctx->device, KC_KIND_MEMALLOC);
+    if (track) kc_track(ctx, KC_EV_FREE, dptr, 0, ctx->device, KC_KIND_MEMALLOC);
     return KC_OK;
 }
 
@@ -245,6 +249,7 @@ std::string hex_base(uint64_t base) {
 using namespace kc;
 
 #define KC_ENTER(ctx)                                                                  \
+    ::kc::Internal _kc_internal_guard;                                                 \
     do {                                                                               \
         if (!(ctx)) return KC_ERR_ARG;                                                 \
         if ((ctx)->poisoned) return KC_ERR_CUDA;                                       \
@@ -318,6 +323,7 @@ kc_status kc_create(kc_ctx** out, const kc_options* opt) {
 void kc_destroy(kc_ctx* ctx) {
     if (!ctx) return;
     if (ctx->cupti_installed) kc_track_uninstall(ctx);
+    interpose_destroy(ctx);
     bind_device(ctx);
     std::vector<uint64_t> vm;
     for (auto& kv : ctx->vmm) vm.push_back(kv.first);
@@ -402,8 +408,8 @@ kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
         if (r == CUDA_ERROR_OUT_OF_MEMORY)
             return set_err(ctx, KC_ERR_NOMEM, "cuMemAlloc(%llu): out of memory", (unsigned long long)size);
         KC_CHECK_CU(ctx, r, "cuMemAlloc");
-        kc_status st = ctx->cupti_installed ? KC_OK
-                                            : kc_track(ctx, KC_EV_ALLOC, (uint64_t)p, size, ctx->device, KC_KIND_MEMALLOC);
+        // tracked explicitly (the CUPTI hook ignores the library's own driver calls)
+        kc_status st = kc_track(ctx, KC_EV_ALLOC, (uint64_t)p, size, ctx->device, KC_KIND_MEMALLOC);
         if (st != KC_OK) {
             KC_DRV(cuMemFree)(p);
             return st;
@@ -447,7 +453,7 @@ kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
         std::lock_guard<std::mutex> lk(ctx->mu);
         ctx->vmm[(uint64_t)va] = kc_ctx::VmmAlloc{rsz, h};
     }
-    if (!ctx->cupti_installed) {
+    {  // tracked explicitly at the requested size (the CUPTI hook ignores the library's own calls)
         kc_status st = kc_track(ctx, KC_EV_MAP, (uint64_t)va, size, ctx->device, KC_KIND_VMM);
         if (st != KC_OK) {
             free_alloc(ctx, (uint64_t)va, false);
@@ -1024,7 +1030,10 @@ const CUpti_CallbackId kTrackedCbids[] = {
     CUPTI_DRIVER_TRACE_CBID_cuMemUnmap,
     // F3 code-object capture: module loads and unloads
     CUPTI_DRIVER_TRACE_CBID_cuModuleLoadData, CUPTI_DRIVER_TRACE_CBID_cuModuleLoadDataEx,
-    CUPTI_DRIVER_TRACE_CBID_cuModuleLoadFatBinary, CUPTI_DRIVER_TRACE_CBID_cuModuleUnload};
+    CUPTI_DRIVER_TRACE_CBID_cuModuleLoadFatBinary, CUPTI_DRIVER_TRACE_CBID_cuModuleUnload,
+    // A3 interposed mode: the launch bracket (kc_interpose.cu)
+    CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel, CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel_ptsz,
+    CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx, CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx_ptsz};
 
 void record_code_object(kc_ctx* ctx, const CUmodule* mod, const void* image) {
     if (!mod || !*mod || !image) return;
@@ -1036,7 +1045,14 @@ void record_code_object(kc_ctx* ctx, const CUmodule* mod, const void* image) {
 
 void CUPTIAPI cupti_cb(void* user, CUpti_CallbackDomain domain, CUpti_CallbackId cbid, const void* cbdata) {
     kc_ctx* ctx = (kc_ctx*)user;
+    if (::kc::t_internal) return;  // the library's own driver calls are not the application's
     const CUpti_CallbackData* d = (const CUpti_CallbackData*)cbdata;
+    if (domain == CUPTI_CB_DOMAIN_DRIVER_API &&
+        (cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel || cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel_ptsz ||
+         cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx || cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx_ptsz)) {
+        ::kc::interpose_launch(ctx, cbid, cbdata);  // ENTER and EXIT
+        return;
+    }
     if (domain != CUPTI_CB_DOMAIN_DRIVER_API || d->callbackSite != CUPTI_API_EXIT) return;
     const CUresult* rv = (const CUresult*)d->functionReturnValue;
     if (rv && *rv != CUDA_SUCCESS) return;
@@ -1141,6 +1157,7 @@ kc_status kc_track_install(kc_ctx* ctx) {
         }
     }
     ctx->cupti_installed = true;
+    interpose_arm_from_env(ctx);  // KC_CAPTURE_DIR (+ KC_TARGET, KC_DISPATCH_INDEX, KC_CAPTURE_MODE)
     return KC_OK;
 }
 

@@ -92,6 +92,7 @@ bool same_regions(const SnapDesc& a, const SnapDesc& b) {
 
 extern "C" kc_status kc_capture_seq(kc_ctx* ctx, const kc_dispatch* ds, size_t n_disp, const kc_region* regions,
                                     size_t n, int host, kc_sequence** out, kc_capture_report* reps) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx || !ds || !n_disp || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     *out = nullptr;
@@ -122,19 +123,35 @@ extern "C" kc_status kc_capture_seq(kc_ctx* ctx, const kc_dispatch* ds, size_t n
     return worst;
 }
 
+kc_status kc::make_sequence(kc_ctx* ctx, std::vector<kc_snapshot*>& steps, kc_sequence** out) {
+    *out = nullptr;
+    for (size_t k = 1; k < steps.size(); ++k)
+        if (!same_regions(steps[0]->desc, steps[k]->desc))
+            return set_err(ctx, KC_ERR_STATE, "sequence: the region set changed between step 0 and step %zu", k);
+    kc_sequence* q = new kc_sequence();
+    q->ctx = ctx;
+    q->steps.swap(steps);
+    q->deps = dependencies(q->steps);
+    *out = q;
+    return KC_OK;
+}
+
 extern "C" size_t kc_seq_length(const kc_sequence* q) { return q ? q->steps.size() : 0; }
 
 extern "C" const kc_snapshot* kc_seq_step(const kc_sequence* q, size_t k) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     return q && k < q->steps.size() ? q->steps[k] : nullptr;
 }
 
 extern "C" kc_status kc_seq_deps(const kc_sequence* q, uint8_t* deps, size_t cap) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!q || !deps || cap < q->deps.size()) return KC_ERR_ARG;
     memcpy(deps, q->deps.data(), q->deps.size());
     return KC_OK;
 }
 
 extern "C" kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* dir_c) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx || !q || !dir_c) return KC_ERR_ARG;
     const std::string dir(dir_c);
     if (mkdir(dir.c_str(), 0755) != 0 && errno != EEXIST)
@@ -171,6 +188,7 @@ extern "C" kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* 
 }
 
 extern "C" void kc_seq_free(kc_sequence* q) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!q) return;
     for (auto it = q->steps.rbegin(); it != q->steps.rend(); ++it) kc_snapshot_free(*it);
     delete q;
@@ -178,6 +196,7 @@ extern "C" void kc_seq_free(kc_sequence* q) {
 
 extern "C" kc_status kc_replay_seq(kc_ctx* ctx, const kc_sequence* q, const kc_seq_replay_opts* o,
                                    kc_seq_step_report* reps, kc_restored** keep) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx || !q || !o || !reps) return KC_ERR_ARG;
     if (keep) *keep = nullptr;
     if (o->count == 0 || o->first >= q->steps.size() || o->count > q->steps.size() - o->first)

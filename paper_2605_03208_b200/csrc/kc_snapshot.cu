@@ -21,6 +21,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <functional>
 #include <map>
 #include <memory>
 #include <thread>
@@ -527,6 +528,7 @@ kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std
 // ====================================================================== capture
 extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                 const char* dir_c, kc_capture_mode mode, kc_capture_report* rep_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -947,6 +949,7 @@ void rollback(kc_restored* h) {
 // captured 32 MiB window, so the caller can re-exec for a fresh ASLR layout.
 // *n_reserved = windows that are free.  No CUDA calls, nothing is mapped.
 extern "C" kc_status kc_prereserve(const char* dir, uint64_t* n_reserved) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!dir) return KC_ERR_ARG;
     std::vector<ParsedRegion> regs;
     kc_status st = parse_regions(nullptr, dir, regs);
@@ -1629,6 +1632,7 @@ struct IpcSource : FileSource {
 }  // namespace
 
 extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** out, kc_restore_report* rep_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx || !dir_c || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     *out = nullptr;
@@ -1834,27 +1838,32 @@ cudaError_t arena_alloc(kc_ctx* ctx, bool host, void** p, uint64_t bytes, uint64
 }
 
 kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
-                      kc_snapshot** out, kc_capture_report* rep_out, bool host, const kc_snapshot* base);
+                      kc_snapshot** out, kc_capture_report* rep_out, bool host, const kc_snapshot* base,
+                      const std::function<CUresult()>* forward = nullptr);
 }  // namespace
 
 extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                     kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     return capture_mem(ctx, d, regions, n, mode, out, rep_out, false, nullptr);
 }
 
 extern "C" kc_status kc_capture_host(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                      kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     return capture_mem(ctx, d, regions, n, mode, out, rep_out, true, nullptr);
 }
 
 extern "C" kc_status kc_capture_incr(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                      kc_capture_mode mode, const kc_snapshot* base, int host, kc_snapshot** out,
                                      kc_capture_report* rep_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (base && base->ctx != ctx) return set_err(ctx, KC_ERR_ARG, "kc_capture_incr: base snapshot of another ctx");
     return capture_mem(ctx, d, regions, n, mode, out, rep_out, host != 0, base);
 }
 
 extern "C" kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx) return KC_ERR_ARG;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
     cudaDeviceSynchronize();
@@ -1872,6 +1881,7 @@ extern "C" kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
 }
 
 extern "C" kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx) return KC_ERR_ARG;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
     if (bytes == 0) {
@@ -1894,7 +1904,8 @@ extern "C" kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
 
 namespace {
 kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n, kc_capture_mode mode,
-                      kc_snapshot** out, kc_capture_report* rep_out, bool host, const kc_snapshot* base) {
+                      kc_snapshot** out, kc_capture_report* rep_out, bool host, const kc_snapshot* base,
+                      const std::function<CUresult()>* forward) {
     if (!ctx) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -2149,9 +2160,12 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         st = snapshot_regions(pre_h);
         if (st != KC_OK) return fail(st);
     }
-    // ---- forward the dispatch
+    // ---- forward the dispatch (interposed mode: the application launches it)
     t = now_s();
-    {
+    if (forward) {
+        const CUresult r = (*forward)();
+        if (r != CUDA_SUCCESS) return fail(cu_err(ctx, r, "kc_capture: intercepted dispatch"));
+    } else {
         CUresult r;
         if (d->kernarg && d->kernarg_size) {
             size_t ksz = d->kernarg_size;
@@ -2272,6 +2286,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
 }  // namespace
 
 extern "C" kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx || !s || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (s->ctx != ctx || ctx->device != s->ctx->device)
@@ -2426,10 +2441,12 @@ static kc_status save_impl(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c,
 }
 
 extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     return save_impl(ctx, s, dir_c, false);
 }
 
 extern "C" kc_status kc_snapshot_publish(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     return save_impl(ctx, s, dir_c, true);
 }
 
@@ -2440,6 +2457,7 @@ extern "C" uint64_t kc_snapshot_shared_bytes(const kc_snapshot* s) { return s ? 
 extern "C" int kc_snapshot_is_host(const kc_snapshot* s) { return s && s->host ? 1 : 0; }
 
 extern "C" void kc_snapshot_free(kc_snapshot* s) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     // revoke the directories this snapshot published: their bytes go with the arena
     if (s)
         for (const std::string& d : s->published) {
@@ -2456,6 +2474,7 @@ extern "C" void kc_snapshot_free(kc_snapshot* s) {
 }
 
 extern "C" kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!h) return KC_ERR_ARG;
     size_t i = 0;
     for (auto& rr : h->regions) {
@@ -2467,6 +2486,7 @@ extern "C" kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t 
 }
 
 extern "C" void kc_release(kc_restored* h) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!h) return;
     if (h->ctx) bind_device(h->ctx);
     cudaDeviceSynchronize();
@@ -2485,6 +2505,7 @@ extern "C" void kc_release(kc_restored* h) {
 
 // ====================================================================== replay
 extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts* o, kc_replay_report* rep_out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx || !h) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -2628,6 +2649,7 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
 
 extern "C" kc_status kc_validate_module_vars(kc_ctx* ctx, const kc_restored* h, uint64_t* n_checked,
                                              uint64_t* n_mismatch) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!ctx || !h) return KC_ERR_ARG;
     if (n_checked) *n_checked = h->modvar_checked;
     if (n_mismatch) *n_mismatch = h->modvar_mismatch;
@@ -2818,6 +2840,7 @@ kc_status kc::validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, 
 extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n,
                                  const kc_tolerance* tol, kc_diff_report* reps, size_t cap_reports,
                                  size_t* n_reports_out, uint64_t* unexpected_chunks) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     return validate_impl(ctx, h, outs, n, tol, reps, cap_reports, n_reports_out, unexpected_chunks, false);
 }
 
@@ -2852,4 +2875,12 @@ kc_status kc::restored_rebind(kc_ctx* ctx, kc_restored* h, const kc_snapshot* sn
     if (st != KC_OK) return st;
     DevSource src(sn);
     return build_stash(ctx, h, d, src);
+}
+
+// interposed mode (kc_interpose.cu): the in-memory capture with the dispatch
+// forwarded by the application itself
+kc_status kc::capture_interposed(kc_ctx* ctx, const kc_dispatch* d, kc_capture_mode mode, bool host,
+                                 const std::function<CUresult()>& forward, kc_snapshot** out, kc_capture_report* rep,
+                                 const kc_snapshot* base) {
+    return capture_mem(ctx, d, nullptr, 0, mode, out, rep, host, base, &forward);
 }

@@ -43,7 +43,8 @@ EXPORTED = [
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
     "kc_capture_incr", "kc_snapshot_shared_bytes", "kc_validate_module_vars",
-    "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_validate_host_ref", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
+    "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_validate_host_ref",
+    "kc_interpose_arm", "kc_interpose_status", "kc_interpose_take", "kc_interpose_arm_seq", "kc_interpose_take_seq", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
 ]
 KC_DEP_RAW, KC_DEP_WAW, KC_DEP_WAR = 1, 2, 4
 
@@ -206,6 +207,11 @@ def lib() -> ctypes.CDLL:
         "kc_capture_host": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
         "kc_host_arena_reserve": (st, [V, U64]),
         "kc_dev_arena_reserve": (st, [V, U64]),
+        "kc_interpose_arm": (st, [V, ctypes.c_char_p, U64, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
+        "kc_interpose_status": (st, [V, P(ctypes.c_int), P(U64), P(CaptureReport)]),
+        "kc_interpose_take": (st, [V, P(V)]),
+        "kc_interpose_arm_seq": (st, [V, ctypes.c_char_p, U64, U64, ctypes.c_int]),
+        "kc_interpose_take_seq": (st, [V, P(V)]),
         "kc_snapshot_is_host": (ctypes.c_int, [V]),
         "kc_capture_incr": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, V, ctypes.c_int, P(V),
                                  P(CaptureReport)]),
@@ -592,6 +598,34 @@ class Context:
     def capture_host(self, **kw) -> tuple[DevSnapshot, dict]:
         """kc_capture_host: the capture into a pinned host arena."""
         return self.capture_dev(host=True, **kw)
+
+    def interpose_arm(self, target: str | None, index: int = 0, directory: str | None = None,
+                      mode: int = KC_MODE_PRE_W, host: bool = False) -> None:
+        """kc_interpose_arm: capture launch `index` of a kernel whose name contains `target` (CUPTI hook)."""
+        self._check(lib().kc_interpose_arm(self._h, target.encode() if target else None, index,
+                                           directory.encode() if directory else None, mode, int(host)),
+                    "kc_interpose_arm")
+
+    def interpose_status(self) -> dict:
+        st, seen, rep = ctypes.c_int(0), ctypes.c_uint64(0), CaptureReport()
+        rc = lib().kc_interpose_status(self._h, ctypes.byref(st), ctypes.byref(seen), ctypes.byref(rep))
+        return {"rc": rc, "state": st.value, "seen": seen.value, "report": rep.as_dict(),
+                "error": self.last_error() if rc < 0 else ""}
+
+    def interpose_arm_seq(self, target: str | None, first: int, count: int, host: bool = False) -> None:
+        """kc_interpose_arm_seq: capture launches [first, first+count) of `target` as a sequence (F4)."""
+        self._check(lib().kc_interpose_arm_seq(self._h, target.encode() if target else None, first, count, int(host)),
+                    "kc_interpose_arm_seq")
+
+    def interpose_take_seq(self) -> "Sequence":
+        h = ctypes.c_void_p()
+        self._check(lib().kc_interpose_take_seq(self._h, ctypes.byref(h)), "kc_interpose_take_seq")
+        return Sequence(h.value, self)
+
+    def interpose_take(self) -> "DevSnapshot":
+        h = ctypes.c_void_p()
+        self._check(lib().kc_interpose_take(self._h, ctypes.byref(h)), "kc_interpose_take")
+        return DevSnapshot(h.value, self)
 
     def dev_arena_reserve(self, nbytes: int) -> None:
         """kc_dev_arena_reserve: map a device arena ahead of time and park it (0 releases it)."""

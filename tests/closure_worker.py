@@ -359,6 +359,87 @@ def publish(a):
     print(json.dumps(out))
 
 
+def interpose(a):
+    """A3 interposed mode: an application drives the CUDA driver API itself
+    (module load, cuMemAlloc, two launches of the list walk); the library only
+    installs its CUPTI hook and arms the capture of launch #1 (the in-place
+    F1' walk).  Reports the capture status and what the application saw."""
+    import ctypes
+    import struct
+    from cuda.bindings import driver as drv
+    ctx = kc.Context(0)
+    ctx.track_install()
+    ctx.interpose_arm("kc_fixture_walk", 1, a.dir, kc.KC_MODE_POST if a.mode == "post" else kc.KC_MODE_PRE_W)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    err, mod = drv.cuModuleLoadData(image)
+    assert err == drv.CUresult.CUDA_SUCCESS, err
+    err, fn = drv.cuModuleGetFunction(mod, b"kc_fixture_walk")
+    sizes = [s.size for s in synth.C1_SPECS]
+    ptrs = []
+    for sz in sizes:
+        err, p_ = drv.cuMemAlloc(sz)
+        assert err == drv.CUresult.CUDA_SUCCESS, err
+        ptrs.append(int(p_))
+    nodes, heads, out = ptrs
+    init = synth.c1_fill(nodes)
+    for p_, arr in zip(ptrs, init):
+        drv.cuMemcpyHtoD(p_, arr.ctypes.data, arr.nbytes)
+    types = (ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int)
+    for mutate in (0, 1):   # launch #0 (not captured), launch #1 (captured, rewrites the nodes)
+        args = ((heads, out, nodes, synth.C1_N_LISTS, mutate), types)
+        err, = drv.cuLaunchKernel(fn, 32, 1, 1, 256, 1, 1, 0, 0, args, 0)
+        assert err == drv.CUresult.CUDA_SUCCESS, err
+    drv.cuCtxSynchronize()
+    st = ctx.interpose_status()
+    got = []
+    for p_, sz in zip(ptrs, sizes):
+        h = np.zeros(sz, dtype=np.uint8)
+        drv.cuMemcpyDtoH(h.ctypes.data, p_, sz)
+        got.append(h)
+    np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_app_nodes.npy"), got[0])
+    np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_app_out.npy"), got[2])
+    np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_init_nodes.npy"), init[0])
+    print(json.dumps({"status": st, "ptrs": ptrs, "tracked": [[r.base, r.size] for r in ctx.regions()]}))
+
+
+def interpose_seq(a):
+    """F4 from an unmodified application: the library arms a 3-launch sequence
+    capture; the application (driver API) runs walk(mutate=1), axpy, walk."""
+    import ctypes
+    from cuda.bindings import driver as drv
+    ctx = kc.Context(0)
+    ctx.track_install()
+    ctx.interpose_arm_seq(None, 0, 3)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    err, mod = drv.cuModuleLoadData(image)
+    err, walk = drv.cuModuleGetFunction(mod, b"kc_fixture_walk")
+    err, axpy = drv.cuModuleGetFunction(mod, b"kc_fixture_axpy_u32")
+    n_y = 100_003
+    sizes = [s.size for s in synth.C1_SPECS] + [4 * n_y, 4 * n_y]
+    ptrs = []
+    for sz in sizes:
+        err, p_ = drv.cuMemAlloc(sz)
+        ptrs.append(int(p_))
+    nodes, heads, out, x, y = ptrs
+    rng = np.random.default_rng(5)
+    init = list(synth.c1_fill(nodes)) + [rng.integers(0, 2**32, n_y, dtype=np.uint64).astype(np.uint32),
+                                         rng.integers(0, 2**32, n_y, dtype=np.uint64).astype(np.uint32)]
+    for p_, arr in zip(ptrs, init):
+        drv.cuMemcpyHtoD(p_, arr.ctypes.data, arr.nbytes)
+    wt = (ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int)
+    drv.cuLaunchKernel(walk, 32, 1, 1, 256, 1, 1, 0, 0, ((heads, out, nodes, synth.C1_N_LISTS, 1), wt), 0)
+    drv.cuLaunchKernel(axpy, (n_y + 255) // 256, 1, 1, 256, 1, 1, 0, 0,
+                       ((x, y, n_y, 7), (ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32)), 0)
+    drv.cuLaunchKernel(walk, 32, 1, 1, 256, 1, 1, 0, 0, ((heads, out, nodes, synth.C1_N_LISTS, 0), wt), 0)
+    drv.cuCtxSynchronize()
+    st = ctx.interpose_status()
+    seq = ctx.interpose_take_seq()
+    deps = seq.deps()
+    seq.save(a.dir)
+    seq.free()
+    print(json.dumps({"status": st, "deps": deps, "ptrs": ptrs}))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -381,7 +462,7 @@ def main():
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
      "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar,
-     "publish": publish}[a.cmd](a)
+     "publish": publish, "interpose": interpose, "interpose-seq": interpose_seq}[a.cmd](a)
 
 
 if __name__ == "__main__":

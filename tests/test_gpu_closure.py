@@ -388,3 +388,60 @@ def test_tampered_code_object_is_refused(tmp_path):
     open(cub, "wb").write(bytes(b))
     res = run("replay", d)
     assert res.get("restore_status") == kc.KC_ERR_FORMAT, res
+
+
+@pytest.mark.parametrize("mode", ["pre_w", "post"])
+def test_interposed_capture_of_an_unmodified_application(tmp_path, mode):
+    """A3 interposed mode: the application
+    loads the module, allocates with cuMemAlloc and launches the list walk twice
+    through the driver API; the CUPTI hook captures launch #1 (F1', in place).
+    The application's launches each ran exactly once (its nodes hold 3v+1, not a
+    double rewrite); the snapshot passes the O1 checker, holds only the three
+    application allocations (none of the library's own), and a fresh process
+    replays it bit-exactly (PRE_W) -- POST starts from the rewritten nodes, so
+    its replay diverges exactly as R7 predicts."""
+    import oracle
+    from oracle import snapshot
+    d = str(tmp_path / "ip")
+    res = run("interpose", d, "--mode", mode)
+    assert res["status"]["state"] == 3, res["status"]
+    assert res["status"]["report"]["n_regions"] == 3 and res["status"]["report"]["written_chunks"] > 0
+    assert sorted(res["ptrs"]) == sorted(b for b, _ in res["tracked"])
+    snap = snapshot.load(d)
+    snapshot.verify(snap)
+    assert sorted(r.base for r in snap.regions) == sorted(res["ptrs"])
+    # what the application saw: plain walk, then the in-place walk, each once
+    init_nodes = np.load(str(tmp_path / "ip_init_nodes.npy"))
+    nodes_dt = np.dtype([("next", "<u8"), ("value", "<u4"), ("pad", "<u4")])
+    v0 = init_nodes.view(nodes_dt)["value"].astype(np.uint64)
+    app_nodes = np.load(str(tmp_path / "ip_app_nodes.npy")).view(nodes_dt)
+    assert np.array_equal(app_nodes["value"], ((3 * v0 + 1) % 2**32).astype(np.uint32))
+    rep = run("replay", d)
+    assert "restore" in rep, rep
+    if mode == "pre_w":
+        assert all(r["differing_bytes"] == 0 for r in rep["validate"]) and rep["unexpected_chunks"] == 0
+    else:
+        assert any(r["differing_bytes"] > 0 for r in rep["validate"])
+
+
+def test_interposed_sequence_capture(tmp_path):
+    """F4 from an unmodified application: kc_interpose_arm_seq captures three
+    consecutive launches (walk with the in-place rewrite, an independent axpy,
+    a walk reading the rewritten nodes).  The saved sequence passes the
+    oracle's sequence checker (O1 per step, chain identity, deps from the
+    files), the dependency matrix is the hand-derived one, and every step
+    replays bit-exactly in a fresh process."""
+    import paper_2605_03208_b200.kc as kc
+    from oracle import snapshot
+    d = str(tmp_path / "seq")
+    res = run("interpose-seq", d)
+    assert res["status"]["state"] == 3, res["status"]
+    RAW, WAW, WAR = kc.KC_DEP_RAW, kc.KC_DEP_WAW, kc.KC_DEP_WAR
+    expect = [[0, 0, 0], [0, 0, 0], [RAW | WAW | WAR, 0, 0]]
+    assert res["deps"] == expect
+    summ = snapshot.verify_sequence(d)
+    assert summ["deps"] == expect and summ["written_chunks"][1] > 0
+    for k in range(3):
+        rep = run("replay", os.path.join(d, f"step_{k:03d}"))
+        assert "restore" in rep, rep
+        assert all(r["differing_bytes"] == 0 for r in rep["validate"]) and rep["unexpected_chunks"] == 0
