@@ -445,3 +445,29 @@ def test_interposed_sequence_capture(tmp_path):
         rep = run("replay", os.path.join(d, f"step_{k:03d}"))
         assert "restore" in rep, rep
         assert all(r["differing_bytes"] == 0 for r in rep["validate"]) and rep["unexpected_chunks"] == 0
+
+
+def test_interposed_capture_of_a_triton_program(tmp_path):
+    """A real JIT framework as the application: an unmodified Triton program
+    (tests/apps/triton_app.py; its module load and cuLaunchKernel(Ex) go through
+    the driver API) has its second `scaled_add` launch captured from the
+    environment (KC_CAPTURE_DIR, KC_TARGET, KC_DISPATCH_INDEX).  The snapshot
+    passes the O1 checker, holds the code object Triton loaded, and a fresh
+    process replays it bit-exactly."""
+    pytest.importorskip("triton")
+    from oracle import snapshot
+    d = str(tmp_path / "tri")
+    env = dict(os.environ, KC_CAPTURE_DIR=d, KC_TARGET="scaled_add", KC_DISPATCH_INDEX="1", KC_REPO=ROOT)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "apps", "triton_app.py")], capture_output=True,
+                       text=True, timeout=600, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    res = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["out_ok"], "the application's own result is wrong: its launch must run exactly once"
+    assert res["status"]["state"] == 3, res["status"]
+    snap = snapshot.load(d)
+    snapshot.verify(snap)
+    assert "scaled_add" in snap.dispatch["mangled_symbol"] and snap.dispatch["code_object_bytes"] > 0
+    rep = run("replay", d)
+    assert "restore" in rep, rep
+    assert rep["validate"] and all(r["differing_bytes"] == 0 for r in rep["validate"])
+    assert rep["unexpected_chunks"] == 0
