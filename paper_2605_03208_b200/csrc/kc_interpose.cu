@@ -137,6 +137,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
             ip->corr = d->correlationId;
             ip->pre_done = ip->go = ip->launched = ip->finished = false;
         }
+        if (ip->worker.joinable()) ip->worker.join();  // a previous capture's worker (already finished)
         auto kernarg = std::make_shared<std::vector<uint8_t>>();
         if (!pack_kernarg(f, kp, extra, *kernarg)) {
             std::lock_guard<std::mutex> lk(ip->mu);
@@ -214,8 +215,9 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
     }
     // EXIT: release the worker, wait for the capture to finish
     {
+        // the bracketed launch (its capture may have failed already: join the worker anyway)
         std::lock_guard<std::mutex> lk(ip->mu);
-        if (ip->state != 2 || ip->corr != d->correlationId || !ip->worker.joinable()) return;
+        if (ip->corr != d->correlationId || !ip->worker.joinable()) return;
     }
     const CUresult* rv = (const CUresult*)d->functionReturnValue;
     {
