@@ -1464,6 +1464,8 @@ using TmaA = HkCfg<256, 3, 1024>;  // 64 slots x 3 x 1 KiB
 using TmaB = HkCfg<128, 3, 2048>;  // 32 slots x 3 x 2 KiB
 using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bound)
 using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
+using CpS = CpCfg<2, 3, 1024>;   // small snapshots: 2-warp CTAs, up to 4 per SM, so < 148 x 64 chunks still
+                                 // spread over every SM (a chunk's hash is a ~25 us serial chain)
 using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
 
 cudaError_t kernels_init() {
@@ -1473,11 +1475,14 @@ cudaError_t kernels_init() {
 #define KC_CP_ATTR(CFG)                                                                                      \
     if (e == cudaSuccess)                                                                                    \
         e = cudaFuncSetAttribute(k1_hash_cpasync<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
-    KC_CP_ATTR(CpA) KC_CP_ATTR(CpD)
+    KC_CP_ATTR(CpA) KC_CP_ATTR(CpD) KC_CP_ATTR(CpS)
 #undef KC_CP_ATTR
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1_hash_cpasync<CpA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)CpA::kSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k1_hash_cpasync<CpS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)CpS::kSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
     if (e == cudaSuccess)
@@ -1513,7 +1518,9 @@ static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d
                       int num_sms, cudaStream_t s, const unsigned long long* d_dst = nullptr,
                       const uint32_t* order = nullptr) {
     const uint64_t groups = (C + 7) / 8;
-    const uint64_t grid = std::min<uint64_t>((groups + CFG::kWarps - 1) / CFG::kWarps, (uint64_t)num_sms);
+    // at most 8 warps' worth of CTAs per SM (one CTA of the 8-warp configs, four of CpS)
+    const uint64_t per_sm = CFG::kWarps >= 8 ? 1 : 8 / CFG::kWarps;
+    const uint64_t grid = std::min<uint64_t>((groups + CFG::kWarps - 1) / CFG::kWarps, (uint64_t)num_sms * per_sm);
     if (d_dst)
         k1_hash_cpasync<CFG, true><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map,
                                                                                        d_dst, order);
@@ -1545,7 +1552,12 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
         case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
-        default: launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
+        default:
+            if ((C + 7) / 8 < (uint64_t)num_sms * 8)  // fewer groups than 8-warp CTAs x SMs: spread them
+                launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
+            else
+                launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
+            break;
     }
     return cudaGetLastError();
 }
@@ -1554,7 +1566,10 @@ cudaError_t launch_hash_copy(const RegionDev* d_regs, int nreg, uint64_t C, uint
                              const unsigned long long* d_dst, const uint32_t* map, int num_sms, cudaStream_t s,
                              const uint32_t* order) {
     if (C == 0) return cudaSuccess;
-    launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, d_dst, order);
+    if ((C + 7) / 8 < (uint64_t)num_sms * 8)
+        launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, d_dst, order);
+    else
+        launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, d_dst, order);
     return cudaGetLastError();
 }
 
