@@ -1464,7 +1464,7 @@ using TmaA = HkCfg<256, 3, 1024>;  // 64 slots x 3 x 1 KiB
 using TmaB = HkCfg<128, 3, 2048>;  // 32 slots x 3 x 2 KiB
 using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bound)
 using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
-using CpS = CpCfg<2, 3, 1024>;   // small snapshots: 2-warp CTAs, up to 4 per SM, so < 148 x 64 chunks still
+using CpS = CpCfg<2, 6, 1024>;   // small snapshots: 2-warp CTAs, 6-deep rings, so < 148 x 64 chunks still
                                  // spread over every SM (a chunk's hash is a ~25 us serial chain)
 using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
 
