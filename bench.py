@@ -705,12 +705,32 @@ def run_latency(a, ctx, pool, log):
     out["files"] = finish("files", cap, rst, r, (t0, t1, t2, t3))
     out["files"]["sink"] = d
     r.release()
+    # capture once, replay many: the file snapshot loaded into HBM once
+    # (kc_snapshot_load, verified), then each edit -> replay -> validate
+    # iteration restores from memory instead of re-reading 30 GB of files
+    try:
+        tl0 = time.perf_counter()
+        snap_l = ctx.load_snapshot(d)
+        tl1 = time.perf_counter()
+        r2, rst2 = ctx.restore_dev(snap_l)
+        tl2 = time.perf_counter()
+        cap_l = dict(cap, t_hash_pre_s=0.0, t_d2h_s=0.0, t_dispatch_s=0.0, t_hash_post_s=0.0, d2h_bytes=0)
+        it = finish("files loaded to HBM", cap_l, rst2, r2, (tl1, tl1, tl1, tl2))
+        out["files_loaded"] = {"load_s": tl1 - tl0, "load_gbs": pool.bytes / (tl1 - tl0) / 1e9,
+                               "iteration_s": it["latency_s"], "validated_bit_exact": it["validated_bit_exact"],
+                               "same_vas": it["same_vas"], "stages_s": it["stages_s"],
+                               "note": "one kc_snapshot_load of the file snapshot, then restore -> replay -> "
+                                       "validate per iteration (the paper's edit-replay loop)"}
+        r2.release()
+        snap_l.free()
+    except Exception as ex:  # reported, never hidden
+        out["files_loaded"] = {"error": repr(ex)[:300], "validated_bit_exact": False}
     shutil.rmtree(d, ignore_errors=True)
     out["bytes"] = pool.bytes
     out["latency_s"] = out["device"]["latency_s"]
     out["validated_bit_exact"] = all(out[k]["validated_bit_exact"]
                                      for k in ("device", "device_ipc", "host_pinned", "host_pinned_incremental",
-                                               "files"))
+                                               "files", "files_loaded"))
     return out
 
 

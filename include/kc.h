@@ -362,6 +362,13 @@ kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
  * Valid while this process keeps the snapshot alive.  KC_ERR_STATE for host
  * snapshots and incremental ones (stored bytes not in one own arena). */
 kc_status kc_snapshot_publish(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
+/* Load a kc-snapshot/1 directory into an in-memory snapshot (device arena, or
+ * pinned host arena when host != 0), verified against its manifests (K1).
+ * The edit -> replay -> validate loop then restores from memory at HBM (or
+ * PCIe) rate each time instead of re-reading the files.  KC_ERR_FORMAT for an
+ * incomplete or malformed directory, KC_ERR_MANIFEST_MISMATCH if a region file
+ * does not match its manifest. */
+kc_status kc_snapshot_load(kc_ctx* ctx, const char* dir, int host, kc_snapshot** out);
 /* Bytes this snapshot copied into its own arenas. */
 uint64_t kc_snapshot_bytes(const kc_snapshot* s);
 /* Stored bytes referenced from base snapshots (kc_capture_incr), not copied. */
@@ -481,6 +488,9 @@ kc_status kc_seq_deps(const kc_sequence* q, uint8_t* deps, size_t cap);
  * dir/sequence.json (format "kc-sequence/1", n, per-step symbol and |W|, the
  * dependency matrix), sentinel dir/sequence_complete written last. */
 kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* dir);
+/* Load a kc-sequence/1 directory (kc_seq_save) back into memory, every step
+ * through kc_snapshot_load: a fresh process can then run kc_replay_seq. */
+kc_status kc_seq_load(kc_ctx* ctx, const char* dir, int host, kc_sequence** out);
 void kc_seq_free(kc_sequence* q);
 
 typedef struct {

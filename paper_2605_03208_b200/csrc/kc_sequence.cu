@@ -187,6 +187,36 @@ extern "C" kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* 
     return KC_OK;
 }
 
+// a kc-sequence/1 directory back into memory (every step fully loaded: the
+// steps' shared bytes are not deduplicated)
+extern "C" kc_status kc_seq_load(kc_ctx* ctx, const char* dir_c, int host, kc_sequence** out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    if (!ctx || !dir_c || !out) return KC_ERR_ARG;
+    *out = nullptr;
+    const std::string dir(dir_c);
+    struct stat sb;
+    if (stat((dir + "/sequence_complete").c_str(), &sb) != 0)
+        return set_err(ctx, KC_ERR_FORMAT, "%s: no sequence_complete sentinel", dir_c);
+    std::vector<kc_snapshot*> steps;
+    for (size_t k = 0;; ++k) {
+        char sub[32];
+        snprintf(sub, sizeof sub, "/step_%03zu", k);
+        if (stat((dir + sub).c_str(), &sb) != 0) break;
+        kc_snapshot* sn = nullptr;
+        kc_status st = kc_snapshot_load(ctx, (dir + sub).c_str(), host, &sn);
+        if (st != KC_OK) {
+            for (auto it = steps.rbegin(); it != steps.rend(); ++it) kc_snapshot_free(*it);
+            return st;
+        }
+        steps.push_back(sn);
+    }
+    if (steps.empty()) return set_err(ctx, KC_ERR_FORMAT, "%s: no step_NNN directories", dir_c);
+    kc_status st = make_sequence(ctx, steps, out);
+    if (st != KC_OK)
+        for (auto it = steps.rbegin(); it != steps.rend(); ++it) kc_snapshot_free(*it);
+    return st;
+}
+
 extern "C" void kc_seq_free(kc_sequence* q) {
     ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     if (!q) return;

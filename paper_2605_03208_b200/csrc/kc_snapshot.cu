@@ -1096,6 +1096,7 @@ kc_status load_desc_files(kc_ctx* ctx, const std::string& dir, SnapDesc& d, kc_r
 
 struct FileSource : RestoreSource {
     std::string dir;
+    std::vector<uint64_t> dst;  // optional: region i's bytes go to dst[i] instead of its VA (kc_snapshot_load)
     explicit FileSource(std::string d) : dir(std::move(d)) {}
     kc_status copy_in(kc_ctx* ctx, const SnapDesc& d, kc_restore_report& rep) override {
         // every region file must exist with exactly `size` bytes (O1)
@@ -1125,7 +1126,8 @@ struct FileSource : RestoreSource {
             const std::string path = dir + "/memory/region_" + sr.hx + ".bin";
             int fd = open(path.c_str(), O_RDONLY);
             std::string err = fd < 0 ? "cannot open" : "";
-            const bool ok = fd >= 0 && item_h2d(ctx, ctx->io[t], fd, sr.r.base, it, err);
+            const uint64_t to = dst.empty() ? sr.r.base : dst[it.region];
+            const bool ok = fd >= 0 && item_h2d(ctx, ctx->io[t], fd, to, it, err);
             if (fd >= 0) close(fd);
             if (ok) {
                 h2d.fetch_add(it.len);
@@ -2448,6 +2450,140 @@ extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const c
 extern "C" kc_status kc_snapshot_publish(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
     ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
     return save_impl(ctx, s, dir_c, true);
+}
+
+// Load a kc-snapshot/1 directory into an in-memory snapshot: the edit -> replay
+// -> validate loop then restores from HBM (or pinned host memory) each time
+// instead of re-reading the files (capture once, replay many).
+extern "C" kc_status kc_snapshot_load(kc_ctx* ctx, const char* dir_c, int host, kc_snapshot** out) {
+    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    if (!ctx || !dir_c || !out) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    *out = nullptr;
+    const double t0 = now_s();
+    kc_restore_report rr;
+    memset(&rr, 0, sizeof rr);
+    kc_snapshot* sn = new kc_snapshot();
+    sn->ctx = ctx;
+    sn->host = host != 0;
+    SnapDesc& D = sn->desc;
+    kc_status st = load_desc_files(ctx, dir_c, D, rr);
+    if (st != KC_OK) {
+        delete sn;
+        return st;
+    }
+    auto fail = [&](kc_status e) {
+        kc_snapshot_free(sn);
+        return e;
+    };
+    st = ensure_stream(ctx);
+    if (st != KC_OK) return fail(st);
+    // the stored bytes: one run per ok region in this snapshot's own arena
+    sn->runs.assign(D.regions.size(), {});
+    uint64_t total = 0;
+    std::vector<uint64_t> aoff(D.regions.size(), 0);
+    for (size_t i = 0; i < D.regions.size(); ++i) {
+        if (!D.regions[i].ok) continue;
+        total = (total + 255) / 256 * 256;
+        aoff[i] = total;
+        total += D.regions[i].r.size;
+    }
+    sn->arena_bytes = total;
+    FileSource src(dir_c);
+    src.dst.assign(D.regions.size(), 0);
+    if (total) {
+        auto ab = std::make_shared<ArenaBuf>();
+        ab->ctx = ctx;
+        ab->host = sn->host;
+        if ((sn->host || !vmm_arena_alloc(ctx, *ab, total)) &&
+            arena_alloc(ctx, sn->host, &ab->p, total, &ab->cap) != cudaSuccess) {
+            cudaGetLastError();
+            ab->p = nullptr;
+            return fail(set_err(ctx, KC_ERR_NOMEM, "kc_snapshot_load: cannot allocate a %llu-byte arena",
+                                (unsigned long long)total));
+        }
+        sn->arena = ab;
+        for (size_t i = 0; i < D.regions.size(); ++i) {
+            if (!D.regions[i].ok) continue;
+            src.dst[i] = (uint64_t)ab->p + aoff[i];
+            sn->runs[i].push_back({0, D.regions[i].r.size, src.dst[i]});
+        }
+    }
+    st = ensure_pinned(ctx);
+    if (st == KC_OK) st = src.copy_in(ctx, D, rr);
+    cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+    if (st == KC_OK && ce != cudaSuccess) st = cuda_err(ctx, ce, "kc_snapshot_load: copy-in");
+    if (st != KC_OK) return fail(st);
+    // verify the loaded bytes against the manifests and recompute the region
+    // digests (K1 over the arena; a pinned host arena is read over PCIe)
+    if (total) {
+        std::vector<kc_region> regs;
+        for (size_t i = 0; i < D.regions.size(); ++i)
+            if (D.regions[i].ok) regs.push_back(kc_region{src.dst[i], D.regions[i].r.size, ctx->device, 0, 0});
+        std::vector<uint64_t> got, digs;
+        st = hash_regions_sync(ctx, regs, got, &digs, nullptr, nullptr, ctx->copy_stream);
+        if (st != KC_OK) return fail(st);
+        for (size_t i = 0, j = 0; i < D.regions.size(); ++i)
+            if (D.regions[i].ok) D.regions[i].digest = digs[j++];
+        uint64_t c = 0, bad = 0;
+        for (auto& sr : D.regions) {
+            if (!sr.ok) continue;
+            for (uint64_t k = 0; k < sr.n_chunks; ++k)
+                bad += sr.manifest.size() != sr.n_chunks || sr.manifest[k] != got[c + k];
+            c += sr.n_chunks;
+        }
+        if (bad)
+            return fail(set_err(ctx, KC_ERR_MANIFEST_MISMATCH, "kc_snapshot_load: %llu chunk(s) do not match the "
+                                "manifest", (unsigned long long)bad));
+    }
+    // W's post bytes (PRE_W) into the W arena
+    uint64_t wtot = 0;
+    for (auto& sr : D.regions) {
+        sn->w_off.push_back(wtot);
+        for (uint64_t k : sr.written) wtot += std::min<uint64_t>(kChunk, sr.r.size - k * kChunk);
+    }
+    sn->w_bytes = D.mode == KC_MODE_PRE_W ? wtot : 0;
+    if (sn->w_bytes) {
+        if ((sn->host ? cudaHostAlloc(&sn->warena, wtot, cudaHostAllocPortable) : cudaMalloc(&sn->warena, wtot)) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            sn->warena = nullptr;
+            return fail(set_err(ctx, KC_ERR_NOMEM, "kc_snapshot_load: W arena of %llu bytes", (unsigned long long)wtot));
+        }
+        for (size_t i = 0; i < D.regions.size(); ++i) {
+            const SnapRegion& sr = D.regions[i];
+            if (!sr.ok || sr.written.empty()) continue;
+            uint64_t wb = 0;
+            for (uint64_t k : sr.written) wb += std::min<uint64_t>(kChunk, sr.r.size - k * kChunk);
+            st = src.written_ref(ctx, D, i, (uint8_t*)sn->warena + sn->w_off[i], wb);
+            if (st != KC_OK) return fail(st);
+        }
+        ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (ce != cudaSuccess) return fail(cuda_err(ctx, ce, "kc_snapshot_load: W bytes"));
+    }
+    memset(&sn->rep, 0, sizeof sn->rep);
+    sn->rep.n_regions = D.regions.size();
+    sn->rep.n_chunks = 0;
+    for (auto& sr : D.regions) {
+        if (!sr.ok) continue;
+        sn->rep.n_chunks += sr.n_chunks;
+        sn->rep.total_bytes += sr.r.size;
+        sn->rep.written_chunks += sr.written.size();
+    }
+    sn->rep.n_failed_regions = rr.n_failed_regions;
+    {  // the snapshot digest as captured (it covers the captured VAs, not the arena's)
+        std::string lt;
+        kcj::Value lv;
+        if (kcj::read_file(std::string(dir_c) + "/capture_log.json", lt) && kcj::Parser(lt).parse(lv) &&
+            lv.get("snapshot_digest"))
+            D.snapshot_digest = strtoull(lv.get("snapshot_digest")->s.c_str(), nullptr, 16);
+    }
+    sn->rep.snapshot_digest = D.snapshot_digest;
+    sn->rep.d2h_bytes = rr.h2d_bytes;
+    sn->rep.t_total_s = now_s() - t0;
+    *out = sn;
+    return KC_OK;
 }
 
 extern "C" uint64_t kc_snapshot_bytes(const kc_snapshot* s) { return s ? s->arena_bytes + s->w_bytes : 0; }

@@ -44,7 +44,8 @@ EXPORTED = [
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
     "kc_capture_incr", "kc_snapshot_shared_bytes", "kc_validate_module_vars",
     "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_validate_host_ref",
-    "kc_interpose_arm", "kc_interpose_status", "kc_interpose_take", "kc_interpose_arm_seq", "kc_interpose_take_seq", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
+    "kc_interpose_arm", "kc_interpose_status", "kc_interpose_take", "kc_interpose_arm_seq", "kc_interpose_take_seq",
+    "kc_snapshot_load", "kc_seq_load", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
 ]
 KC_DEP_RAW, KC_DEP_WAW, KC_DEP_WAR = 1, 2, 4
 
@@ -212,6 +213,8 @@ def lib() -> ctypes.CDLL:
         "kc_interpose_take": (st, [V, P(V)]),
         "kc_interpose_arm_seq": (st, [V, ctypes.c_char_p, U64, U64, ctypes.c_int]),
         "kc_interpose_take_seq": (st, [V, P(V)]),
+        "kc_snapshot_load": (st, [V, ctypes.c_char_p, ctypes.c_int, P(V)]),
+        "kc_seq_load": (st, [V, ctypes.c_char_p, ctypes.c_int, P(V)]),
         "kc_snapshot_is_host": (ctypes.c_int, [V]),
         "kc_capture_incr": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, V, ctypes.c_int, P(V),
                                  P(CaptureReport)]),
@@ -611,6 +614,19 @@ class Context:
         rc = lib().kc_interpose_status(self._h, ctypes.byref(st), ctypes.byref(seen), ctypes.byref(rep))
         return {"rc": rc, "state": st.value, "seen": seen.value, "report": rep.as_dict(),
                 "error": self.last_error() if rc < 0 else ""}
+
+    def load_snapshot(self, directory: str, host: bool = False) -> "DevSnapshot":
+        """kc_snapshot_load: a kc-snapshot/1 directory into device (or pinned host) memory."""
+        h = ctypes.c_void_p()
+        self._check(lib().kc_snapshot_load(self._h, directory.encode(), int(host), ctypes.byref(h)),
+                    "kc_snapshot_load")
+        return DevSnapshot(h.value, self)
+
+    def load_seq(self, directory: str, host: bool = False) -> "Sequence":
+        """kc_seq_load: a kc-sequence/1 directory back into memory."""
+        h = ctypes.c_void_p()
+        self._check(lib().kc_seq_load(self._h, directory.encode(), int(host), ctypes.byref(h)), "kc_seq_load")
+        return Sequence(h.value, self)
 
     def interpose_arm_seq(self, target: str | None, first: int, count: int, host: bool = False) -> None:
         """kc_interpose_arm_seq: capture launches [first, first+count) of `target` as a sequence (F4)."""

@@ -8,6 +8,7 @@ replay / validate in a fresh one).  Prints one JSON line on stdout.
 """
 import argparse
 import json
+import time
 import os
 import sys
 
@@ -440,6 +441,41 @@ def interpose_seq(a):
     print(json.dumps({"status": st, "deps": deps, "ptrs": ptrs}))
 
 
+def load_replay(a):
+    """Capture once, replay many: a fresh process loads a
+    file snapshot into HBM once (kc_snapshot_load), then restores at the
+    captured VAs, replays and validates `cycles` times from memory."""
+    if not a.no_prereserve:
+        kc.exec_replay_process(sys.argv, a.dir)
+    ctx = kc.Context(0)
+    t0 = time.perf_counter()
+    snap = ctx.load_snapshot(a.dir, host=a.host)
+    out = {"load_s": time.perf_counter() - t0, "is_host": snap.is_host(), "cycles": []}
+    for _ in range(a.cycles):
+        t1 = time.perf_counter()
+        r, rst = ctx.restore_dev(snap)
+        t2 = time.perf_counter()
+        ctx.replay(r)
+        reps, unexpected = ctx.validate(r)
+        t3 = time.perf_counter()
+        out["cycles"].append({"restore_s": t2 - t1, "replay_validate_s": t3 - t2, "verify": rst["verify_mismatch_chunks"],
+                              "regions": [[x.base, x.size] for x in r.regions()],
+                              "ok": all(x["differing_bytes"] == 0 for x in reps) and unexpected == 0 and len(reps) > 0})
+        r.release()
+    snap.free()
+    print(json.dumps(out))
+
+
+def load_seq(a):
+    """A saved sequence loaded in a fresh process and replayed jointly."""
+    ctx = kc.Context(0)
+    seq = ctx.load_seq(a.dir)
+    steps, _ = ctx.replay_seq(seq)
+    out = {"n": len(seq), "deps": seq.deps(), "steps": steps}
+    seq.free()
+    print(json.dumps(out))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -462,7 +498,8 @@ def main():
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
      "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar,
-     "publish": publish, "interpose": interpose, "interpose-seq": interpose_seq}[a.cmd](a)
+     "publish": publish, "interpose": interpose, "interpose-seq": interpose_seq, "load-replay": load_replay,
+     "load-seq": load_seq}[a.cmd](a)
 
 
 if __name__ == "__main__":

@@ -471,3 +471,27 @@ def test_interposed_capture_of_a_triton_program(tmp_path):
     assert "restore" in rep, rep
     assert rep["validate"] and all(r["differing_bytes"] == 0 for r in rep["validate"])
     assert rep["unexpected_chunks"] == 0
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_load_once_replay_many(tmp_path, host):
+    """kc_snapshot_load: a fresh process loads the file snapshot into HBM (or
+    pinned host memory) once, verified against its manifests, then restores at
+    the captured VAs, replays and validates three times from memory."""
+    d = str(tmp_path / "cap")
+    run("capture-c1", d, "--mutate")
+    res = run("load-replay", d, "--cycles", "3", *(["--host"] if host else []))
+    assert res["is_host"] == host and len(res["cycles"]) == 3
+    regs = res["cycles"][0]["regions"]
+    for c in res["cycles"]:
+        assert c["ok"] and c["verify"] == 0 and c["regions"] == regs
+
+
+def test_saved_sequence_replays_in_a_fresh_process(tmp_path):
+    """kc_seq_load: the interposed sequence (walk, axpy, walk) saved by one
+    process is loaded and jointly replayed by another, every step bit-exact."""
+    d = str(tmp_path / "seq")
+    run("interpose-seq", d)
+    res = run("load-seq", d)
+    assert res["n"] == 3 and [s["pass"] for s in res["steps"]] == [1, 1, 1], res["steps"]
+    assert [s["inherited_chunks"] for s in res["steps"]] == [0, 0, 0]
