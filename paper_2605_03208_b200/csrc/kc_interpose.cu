@@ -125,6 +125,10 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
         }
         const char* name = nullptr;
         if (KC_DRV(cuFuncGetName)(&name, f) != CUDA_SUCCESS || !name) return;
+        if (ctx->device < 0) {  // injected ctx: the application's current device (the worker has no context)
+            CUdevice dev = 0;
+            if (KC_DRV(cuCtxGetDevice)(&dev) == CUDA_SUCCESS) ctx->device = (int)dev;
+        }
         std::string mangled(name);
         {
             std::lock_guard<std::mutex> lk(ip->mu);

@@ -91,6 +91,18 @@ cudaError_t ensure(kc_ctx_dev_buf& b, size_t bytes) {
 }
 
 bool bind_device(kc_ctx* ctx) {
+    if (!ctx->inited) {  // created by the injection entry point: finish on first use
+        if (ctx->device < 0) {
+            CUdevice dev = 0;  // the calling thread's current context decides (the application's)
+            if (!drv().ok || KC_DRV(cuCtxGetDevice)(&dev) != CUDA_SUCCESS) return false;
+            ctx->device = (int)dev;
+        }
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) == cudaSuccess && sms > 0)
+            ctx->num_sms = sms;
+        if (cudaSetDevice(ctx->device) != cudaSuccess || kernels_init() != cudaSuccess) return false;
+        ctx->inited = true;
+    }
     if (cudaSetDevice(ctx->device) != cudaSuccess) return false;
     if (cudaFree(nullptr) != cudaSuccess) return false;  // make the primary context current
     return drv().ok;
@@ -1127,6 +1139,39 @@ void CUPTIAPI cupti_cb(void* user, CUpti_CallbackDomain domain, CUpti_CallbackId
     }
 }
 }  // namespace
+
+}  // extern "C"
+
+namespace {
+kc_ctx* g_injected = nullptr;  // the ctx of the CUDA_INJECTION64_PATH entry point (lives for the process)
+}
+
+extern "C" {
+
+// CUDA_INJECTION64_PATH=libkc.so: the driver calls this during cuInit of an
+// application that knows nothing about the library (the CUDA counterpart of the
+// paper's HSA_TOOLS_LIB / LD_PRELOAD load).  Only CUPTI may be
+// called here: the ctx is created without touching CUDA and binds to the
+// current context's device at its first capture.  Arms from KC_CAPTURE_DIR,
+// KC_TARGET, KC_DISPATCH_INDEX, KC_CAPTURE_MODE.  Returns 1 (the driver's
+// convention for a loaded injection), 0 on failure (the application runs on).
+int InitializeInjection(void) {
+    if (g_injected) return 1;
+    kc_ctx* ctx = new kc_ctx();
+    ctx->device = -1;  // bound lazily (bind_device)
+    ctx->inited = false;
+    uint64_t io = 0;
+    if (const char* env = getenv("KERNCAP_SNAPSHOT_CHUNK_BYTES")) io = strtoull(env, nullptr, 0);
+    ctx->io_chunk = io ? (io + kChunk - 1) / kChunk * kChunk : 64ull << 20;
+    if (kc_track_install(ctx) != KC_OK) {
+        fprintf(stderr, "[kc] injection: %s\n", ctx->err.c_str());
+        delete ctx;
+        return 0;
+    }
+    g_injected = ctx;
+    if (getenv("KC_TRACE")) fprintf(stderr, "[kc] injected (CUPTI hook installed)\n");
+    return 1;
+}
 
 kc_status kc_track_install(kc_ctx* ctx) {
     if (!ctx) return KC_ERR_ARG;

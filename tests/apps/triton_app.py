@@ -1,12 +1,8 @@
 """An unmodified Triton program used as a capture TARGET (the paper's Triton
 workload class) -- test workload only, not part of the
-library.  Run as a script it does its own work; the capture is armed from the
-environment through kc_track_install (KC_CAPTURE_DIR, KC_TARGET,
-KC_DISPATCH_INDEX), so the program contains no capture calls of its own
-beyond installing the hook before it allocates."""
+library, and it contains no library code: `paper_2605_03208_b200.cli capture`
+runs it with CUDA_INJECTION64_PATH=libkc.so."""
 import json
-import os
-import sys
 
 import torch
 import triton
@@ -24,10 +20,6 @@ def scaled_add(x_ptr, y_ptr, out_ptr, n, alpha, BLOCK: tl.constexpr):
 
 
 def main():
-    sys.path.insert(0, os.environ["KC_REPO"])
-    from paper_2605_03208_b200 import kc
-    ctx = kc.Context(0)
-    ctx.track_install()                       # arms from KC_CAPTURE_DIR / KC_TARGET / KC_DISPATCH_INDEX
     torch.manual_seed(0)
     n = 1_000_003
     x = torch.randn(n, device="cuda")
@@ -37,10 +29,9 @@ def main():
     for alpha in (0.5, 2.0):                  # launch #0 and launch #1
         scaled_add[grid](x, y, out, n, alpha, BLOCK=1024)
     torch.cuda.synchronize()
-    st = ctx.interpose_status()
     expect = (x + 2.0 * y).cpu()
-    print(json.dumps({"status": st, "out_ok": bool(torch.equal(out.cpu(), expect)),
-                      "out_ptr": out.data_ptr(), "nbytes": out.numel() * 4}))
+    print(json.dumps({"out_ok": bool(torch.equal(out.cpu(), expect)), "out_ptr": out.data_ptr(),
+                      "nbytes": out.numel() * 4}))
 
 
 if __name__ == "__main__":

@@ -449,28 +449,30 @@ def test_interposed_sequence_capture(tmp_path):
 
 def test_interposed_capture_of_a_triton_program(tmp_path):
     """A real JIT framework as the application: an unmodified Triton program
-    (tests/apps/triton_app.py; its module load and cuLaunchKernel(Ex) go through
-    the driver API) has its second `scaled_add` launch captured from the
-    environment (KC_CAPTURE_DIR, KC_TARGET, KC_DISPATCH_INDEX).  The snapshot
-    passes the O1 checker, holds the code object Triton loaded, and a fresh
-    process replays it bit-exactly."""
+    (tests/apps/triton_app.py, no library code; its module load and
+    cuLaunchKernel(Ex) go through the driver API) run by `cli capture`, which
+    injects libkc.so with CUDA_INJECTION64_PATH and captures the second
+    `scaled_add` launch.  The program's own result is intact, the snapshot passes
+    the O1 checker and holds the code object Triton loaded, and `cli replay` in a
+    fresh process validates bit-exactly."""
     pytest.importorskip("triton")
     from oracle import snapshot
     d = str(tmp_path / "tri")
-    env = dict(os.environ, KC_CAPTURE_DIR=d, KC_TARGET="scaled_add", KC_DISPATCH_INDEX="1", KC_REPO=ROOT)
-    p = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "apps", "triton_app.py")], capture_output=True,
-                       text=True, timeout=600, env=env)
-    assert p.returncode == 0, p.stderr[-3000:]
-    res = json.loads(p.stdout.strip().splitlines()[-1])
-    assert res["out_ok"], "the application's own result is wrong: its launch must run exactly once"
-    assert res["status"]["state"] == 3, res["status"]
+    cli = [sys.executable, "-m", "paper_2605_03208_b200.cli"]
+    p = subprocess.run(cli + ["capture", "--kernel", "scaled_add", "--index", "1", "--out", d, "--",
+                              sys.executable, os.path.join(ROOT, "tests", "apps", "triton_app.py")],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    lines = [json.loads(x) for x in p.stdout.strip().splitlines() if x.startswith("{")]
+    assert lines[0]["out_ok"], "the application's own result is wrong: its launch must run exactly once"
+    assert lines[-1]["captured"]
     snap = snapshot.load(d)
     snapshot.verify(snap)
     assert "scaled_add" in snap.dispatch["mangled_symbol"] and snap.dispatch["code_object_bytes"] > 0
-    rep = run("replay", d)
-    assert "restore" in rep, rep
-    assert rep["validate"] and all(r["differing_bytes"] == 0 for r in rep["validate"])
-    assert rep["unexpected_chunks"] == 0
+    p = subprocess.run(cli + ["replay", d], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    rep = json.loads(p.stdout.strip().splitlines()[-1])
+    assert rep["pass"] and rep["validate"] and all(r["differing_bytes"] == 0 for r in rep["validate"])
 
 
 @pytest.mark.parametrize("host", [False, True])
@@ -495,3 +497,36 @@ def test_saved_sequence_replays_in_a_fresh_process(tmp_path):
     res = run("load-seq", d)
     assert res["n"] == 3 and [s["pass"] for s in res["steps"]] == [1, 1, 1], res["steps"]
     assert [s["inherited_chunks"] for s in res["steps"]] == [0, 0, 0]
+
+
+def test_cli_capture_of_an_application_without_kc_code(tmp_path):
+    """The paper's workflow on CUDA (`kerncap capture` / `replay`):
+    `python -m paper_2605_03208_b200.cli capture --kernel kc_fixture_walk --index 1
+    --out DIR -- APP` runs a driver-API application that contains no library code.
+    The driver loads libkc.so through CUDA_INJECTION64_PATH (InitializeInjection),
+    whose CUPTI hook tracks the allocations and captures launch #1.  The
+    application's own results are intact (each launch ran once), and `cli replay`
+    in a fresh process validates bit-exactly; `cli info` summarises the snapshot."""
+    from oracle import snapshot
+    d = str(tmp_path / "cli")
+    app_out = str(tmp_path / "app.npz")
+    cli = [sys.executable, "-m", "paper_2605_03208_b200.cli"]
+    p = subprocess.run(cli + ["capture", "--kernel", "kc_fixture_walk", "--index", "1", "--out", d, "--",
+                              sys.executable, os.path.join(ROOT, "tests", "apps", "driver_app.py"), app_out, ROOT],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    assert json.loads(p.stdout.strip().splitlines()[-1])["captured"]
+    app = np.load(app_out)
+    nodes_dt = np.dtype([("next", "<u8"), ("value", "<u4"), ("pad", "<u4")])
+    v0 = app["init_nodes"].view(nodes_dt)["value"].astype(np.uint64)
+    assert np.array_equal(app["nodes"].view(nodes_dt)["value"], ((3 * v0 + 1) % 2**32).astype(np.uint32))
+    snap = snapshot.load(d)
+    snapshot.verify(snap)
+    assert sorted(r.base for r in snap.regions) == sorted(int(x) for x in app["ptrs"])
+    p = subprocess.run(cli + ["replay", d], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    rep = json.loads(p.stdout.strip().splitlines()[-1])
+    assert rep["pass"] and rep["unexpected_chunks"] == 0
+    p = subprocess.run(cli + ["info", d], capture_output=True, text=True, timeout=120, cwd=ROOT)
+    info = json.loads(p.stdout.strip().splitlines()[-1])
+    assert info["kernel"] == "kc_fixture_walk" and info["regions"] == 3
