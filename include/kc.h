@@ -413,6 +413,17 @@ kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t
 kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out);
 void kc_release(kc_restored* h);
 
+/* ---- loading into an unmodified application ------------------------------
+ * CUDA_INJECTION64_PATH=<path>/libkc.so makes the CUDA driver load the library
+ * at cuInit and call this (the CUDA counterpart of the paper's HSA tool-library
+ * load).  It creates a ctx without touching CUDA, installs the
+ * CUPTI hook (kc_track_install) and arms the interposed capture from the
+ * environment (KC_CAPTURE_DIR, KC_TARGET, KC_DISPATCH_INDEX, KC_CAPTURE_MODE);
+ * the ctx binds to the application's device at its first capture and works in
+ * the device's primary context.  Returns 1 when loaded, 0 otherwise (the
+ * application then runs without capture). */
+int InitializeInjection(void);
+
 /* ---- A3 interposed mode ----------------
  * Capture a dispatch of an application that runs unmodified.  With
  * kc_track_install active (the tracker sees its allocations and module loads),
