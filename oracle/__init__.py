@@ -9,7 +9,7 @@ arithmetic).
 
 The arithmetic lives in ``oracle/kc_oracle.c`` (plain C, fp64, no FMA
 contraction), loaded here through ctypes.  Each function cites the passage it
-follows; the readings of the paper are DESIGN.md R1..R26.
+follows; the readings of the paper are DESIGN.md R1..R34.
 
 Pins (what ties this oracle to something other than itself) are the
 ``-m "not gpu"`` tests in ``tests/test_oracle_*.py``.  Every function here is

@@ -1,9 +1,11 @@
 // kc_kernels.cu -- the data-parallel hot path of Kerncap's capture-and-validate
-// loop on B200 (sm_100a): K1 chunked XXH64 content hash (TMA bulk ring, 4 lanes
-// per chunk, shuffle merge), region/snapshot digests, K3 written set, K2 fused
-// diff (bitmap, counts, ULP, fp64 abs/rel, allclose, NaN counters).
+// loop on B200 (sm_100a): K1 chunked XXH64 content hash (cp.async-staged rings,
+// 4 lanes per chunk, shuffle merge; TMA bulk rings as measured alternatives),
+// K6 = K1 + copy into a snapshot arena, region/snapshot digests, K3 written
+// set, K2 fused diff (bitmap, counts, ULP, fp64 abs/rel, allclose, NaN
+// counters), K5 fused hash + compare, K4 gather.
 //
-// Definitions: SURVEY.md 8(c) O2-O4 and DESIGN.md readings R1-R26, restating
+// Definitions: SURVEY.md 8(c) O2-O4 and DESIGN.md readings R1-R34, restating
 // PAPER.md:681-691 (chunked snapshot), 1120-1126 (byte-exact compare),
 // 1128-1135 (allclose + explicit NaN reporting).  Compiled WITHOUT fast-math
 // and with -fmad=false; every fp64 op below is an explicit _rn intrinsic.
