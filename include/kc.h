@@ -258,7 +258,9 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
  * themselves: equal hashes are equal bytes, reading R34, the same test as W).
  * reps: n reports (host); h_bitmaps: optional host bitmaps (as kc_diff);
  * d_act_manifest: optional device output of act's chunk hashes; *h2d_bytes:
- * bytes moved host->device (manifest + reference chunks). */
+ * bytes moved host->device (manifest + reference chunks).  Device scratch: 8 B
+ * per chunk (manifest) plus 64 KiB per chunk whose hash differs (the staged
+ * reference bytes); KC_ERR_NOMEM if that does not fit. */
 kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const uint64_t* ref_manifest,
                                const kc_tolerance* tol, kc_diff_report* reps, uint64_t* h_bitmaps,
                                uint64_t* d_act_manifest, uint64_t* h2d_bytes, void* stream);
