@@ -502,7 +502,9 @@ kc_status kc_seq_deps(const kc_sequence* q, uint8_t* deps, size_t cap);
  * dependency matrix), sentinel dir/sequence_complete written last. */
 kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* dir);
 /* Load a kc-sequence/1 directory (kc_seq_save) back into memory, every step
- * through kc_snapshot_load: a fresh process can then run kc_replay_seq. */
+ * through kc_snapshot_load: a fresh process can then run kc_replay_seq.  As
+ * for kc_restore, run kc_prereserve (on step_000: every step has the same
+ * regions) before CUDA initialises and re-exec on a collision (R28c). */
 kc_status kc_seq_load(kc_ctx* ctx, const char* dir, int host, kc_sequence** out);
 void kc_seq_free(kc_sequence* q);
 

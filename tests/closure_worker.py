@@ -370,7 +370,8 @@ def interpose(a):
     from cuda.bindings import driver as drv
     ctx = kc.Context(0)
     ctx.track_install()
-    ctx.interpose_arm("kc_fixture_walk", 1, a.dir, kc.KC_MODE_POST if a.mode == "post" else kc.KC_MODE_PRE_W)
+    target_dir = "/proc/kc_not_writable/cap" if a.bad_dir else a.dir   # a capture that must fail
+    ctx.interpose_arm("kc_fixture_walk", 1, target_dir, kc.KC_MODE_POST if a.mode == "post" else kc.KC_MODE_PRE_W)
     image = open(synth.FIXTURE_CUBIN, "rb").read()
     err, mod = drv.cuModuleLoadData(image)
     assert err == drv.CUresult.CUDA_SUCCESS, err
@@ -397,6 +398,7 @@ def interpose(a):
         h = np.zeros(sz, dtype=np.uint8)
         drv.cuMemcpyDtoH(h.ctypes.data, p_, sz)
         got.append(h)
+    os.makedirs(a.dir, exist_ok=True)   # (a failed capture never created it)
     np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_app_nodes.npy"), got[0])
     np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_app_out.npy"), got[2])
     np.save(os.path.join(a.dir, "..", os.path.basename(a.dir) + "_init_nodes.npy"), init[0])
@@ -468,6 +470,9 @@ def load_replay(a):
 
 def load_seq(a):
     """A saved sequence loaded in a fresh process and replayed jointly."""
+    # every step covers the same regions: the pre-CUDA collision check of step 0
+    # (re-exec for a fresh ASLR layout, R28c) protects the whole joint replay
+    kc.exec_replay_process(sys.argv, os.path.join(a.dir, "step_000"))
     ctx = kc.Context(0)
     seq = ctx.load_seq(a.dir)
     steps, _ = ctx.replay_seq(seq)
@@ -495,6 +500,7 @@ def main():
     p.add_argument("--host", action="store_true")
     p.add_argument("--cycles", type=int, default=1)
     p.add_argument("--cupti", action="store_true")
+    p.add_argument("--bad-dir", action="store_true")
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
      "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar,

@@ -530,3 +530,18 @@ def test_cli_capture_of_an_application_without_kc_code(tmp_path):
     p = subprocess.run(cli + ["info", d], capture_output=True, text=True, timeout=120, cwd=ROOT)
     info = json.loads(p.stdout.strip().splitlines()[-1])
     assert info["kernel"] == "kc_fixture_walk" and info["regions"] == 3
+
+
+def test_failed_interposed_capture_never_blocks_the_application(tmp_path):
+    """Liveness: when the interposed capture fails (here:
+    its snapshot cannot be written), the state says so with the error, and the
+    application's launch still ran exactly once with correct results."""
+    import paper_2605_03208_b200.kc as kc
+    d = str(tmp_path / "ipbad")
+    res = run("interpose", d, "--bad-dir")
+    assert res["status"]["state"] == -1 and res["status"]["rc"] == kc.KC_ERR_IO, res["status"]
+    init_nodes = np.load(str(tmp_path / "ipbad_init_nodes.npy"))
+    nodes_dt = np.dtype([("next", "<u8"), ("value", "<u4"), ("pad", "<u4")])
+    v0 = init_nodes.view(nodes_dt)["value"].astype(np.uint64)
+    app_nodes = np.load(str(tmp_path / "ipbad_app_nodes.npy")).view(nodes_dt)
+    assert np.array_equal(app_nodes["value"], ((3 * v0 + 1) % 2**32).astype(np.uint32))
