@@ -788,6 +788,29 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
                        nullptr, nullptr);
 }
 
+// K5 pair table + chunk -> pair map (4 B per chunk), uploaded only when the pair
+// list differs from the previous call's (the same buffer set validated again and again)
+static kc_status upload_pairs(kc_ctx* ctx, std::vector<PairDev>& t, uint64_t C, const std::vector<uint64_t>& chunk0,
+                              cudaStream_t s) {
+    const bool same = t.size() == ctx->pairs_cached.size() && ctx->pairs.p &&
+                      (t.empty() || memcmp(t.data(), ctx->pairs_cached.data(), t.size() * sizeof(PairDev)) == 0);
+    if (same) return KC_OK;
+    KC_CHECK_CUDA(ctx, ensure(ctx->pairs, std::max<size_t>(1, t.size()) * sizeof(PairDev)), "cudaMalloc(pairs)");
+    if (!t.empty())
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pairs.p, t.data(), t.size() * sizeof(PairDev), cudaMemcpyHostToDevice,
+                                           s), "upload pairs");
+    std::vector<uint32_t> map(C);
+    for (size_t i = 0; i < t.size(); ++i)
+        std::fill(map.begin() + chunk0[i], map.begin() + chunk0[i] + (t[i].size + kChunk - 1) / kChunk, (uint32_t)i);
+    KC_CHECK_CUDA(ctx, ensure(ctx->pair_map, std::max<size_t>(1, map.size()) * 4), "cudaMalloc(pair map)");
+    if (!map.empty())
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pair_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
+                      "upload pair map");
+    KC_CHECK_CUDA(ctx, cudaStreamSynchronize(s), "upload pair map");  // `map` is pageable and goes away
+    ctx->pairs_cached.swap(t);
+    return KC_OK;
+}
+
 // ------------------------------------------------------------------ F2: K5 fused hash + compare, then filtered K2
 kc_status kc_hash_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
                              uint64_t* d_chunk_hash, kc_diff_report* d_reports, uint64_t* d_bitmaps,
@@ -825,22 +848,9 @@ kc_status kc_hash_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const
                            nullptr, nullptr);
     }
     // pair table + chunk -> pair map, cached like the K1 region table
-    const bool same = t.size() == ctx->pairs_cached.size() && ctx->pairs.p &&
-                      (t.empty() || memcmp(t.data(), ctx->pairs_cached.data(), t.size() * sizeof(PairDev)) == 0);
-    if (!same) {
-        KC_CHECK_CUDA(ctx, ensure(ctx->pairs, std::max<size_t>(1, t.size()) * sizeof(PairDev)), "cudaMalloc(pairs)");
-        if (!t.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pairs.p, t.data(), t.size() * sizeof(PairDev),
-                                               cudaMemcpyHostToDevice, s), "upload pairs");
-        std::vector<uint32_t> map(C);
-        for (size_t i = 0; i < n; ++i)
-            std::fill(map.begin() + chunk0[i], map.begin() + chunk0[i] + (bufs[i].nbytes + kChunk - 1) / kChunk,
-                      (uint32_t)i);
-        KC_CHECK_CUDA(ctx, ensure(ctx->pair_map, std::max<size_t>(1, map.size()) * 4), "cudaMalloc(pair map)");
-        if (!map.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pair_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
-                          "upload pair map");
-        ctx->pairs_cached.swap(t);
+    {
+        kc_status st = upload_pairs(ctx, t, C, chunk0, s);
+        if (st != KC_OK) return st;
     }
     uint64_t* dirty = d_dirty;
     if (!dirty) {
@@ -887,23 +897,9 @@ kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, con
                          "H2D reference manifest");
     moved += C * 8;
     // (2) K5 over act alone: act's manifest + chunks holding Inf/NaN (or a ragged tail)
-    const bool same = t.size() == ctx->pairs_cached.size() && ctx->pairs.p &&
-                      (t.empty() || memcmp(t.data(), ctx->pairs_cached.data(), t.size() * sizeof(PairDev)) == 0);
-    if (!same) {
-        KC_CHECK_CUDA(ctx, ensure(ctx->pairs, std::max<size_t>(1, t.size()) * sizeof(PairDev)), "cudaMalloc(pairs)");
-        if (!t.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pairs.p, t.data(), t.size() * sizeof(PairDev),
-                                               cudaMemcpyHostToDevice, s), "upload pairs");
-        std::vector<uint32_t> map(C);
-        for (size_t i = 0; i < n; ++i)
-            std::fill(map.begin() + chunk0[i], map.begin() + chunk0[i] + (bufs[i].nbytes + kChunk - 1) / kChunk,
-                      (uint32_t)i);
-        KC_CHECK_CUDA(ctx, ensure(ctx->pair_map, std::max<size_t>(1, map.size()) * 4), "cudaMalloc(pair map)");
-        if (!map.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pair_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
-                          "upload pair map");
-        cudaStreamSynchronize(s);  // pageable `map`
-        ctx->pairs_cached.swap(t);
+    {
+        kc_status st = upload_pairs(ctx, t, C, chunk0, s);
+        if (st != KC_OK) return st;
     }
     uint64_t* act_h = d_act_manifest;
     if (!act_h) {
