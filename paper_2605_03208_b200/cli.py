@@ -4,6 +4,8 @@
     python -m paper_2605_03208_b200.cli capture --kernel NAME [--index N] [--mode pre_w|post] --out DIR -- CMD ...
     python -m paper_2605_03208_b200.cli replay DIR [--override CUBIN] [--iterations N] [--no-recopy]
                                                   [--dump] [--typed HEXVA:NBYTES:DTYPE] [--atol A --rtol R]
+    python -m paper_2605_03208_b200.cli capture --kernel NAME --index N --count K --out DIR -- CMD ...   (a sequence)
+    python -m paper_2605_03208_b200.cli replay-seq DIR
     python -m paper_2605_03208_b200.cli info DIR
 
 `capture` runs an unmodified CUDA application with CUDA_INJECTION64_PATH
@@ -34,9 +36,10 @@ def _capture(a, rest) -> int:
         print("capture: missing the application command after --", file=sys.stderr)
         return 2
     env = dict(os.environ, CUDA_INJECTION64_PATH=kc.LIB_PATH, KC_CAPTURE_DIR=os.path.abspath(a.out),
-               KC_TARGET=a.kernel or "", KC_DISPATCH_INDEX=str(a.index), KC_CAPTURE_MODE=a.mode)
+               KC_TARGET=a.kernel or "", KC_DISPATCH_INDEX=str(a.index), KC_CAPTURE_MODE=a.mode,
+               KC_CAPTURE_COUNT=str(a.count))
     p = subprocess.run(rest, env=env)
-    done = os.path.exists(os.path.join(a.out, "capture_complete"))
+    done = os.path.exists(os.path.join(a.out, "capture_complete" if a.count <= 1 else "sequence_complete"))
     print(json.dumps({"app_returncode": p.returncode, "captured": done, "dir": os.path.abspath(a.out)}))
     return 0 if done else 1
 
@@ -60,6 +63,19 @@ def _replay(a) -> int:
     if dump:
         out["dump"] = dump
     r.release()
+    ctx.close()
+    print(json.dumps(out))
+    return 0 if out["pass"] else 3
+
+
+def _replay_seq(a) -> int:
+    from paper_2605_03208_b200 import kc
+    kc.exec_replay_process(sys.argv, os.path.join(a.dir, "step_000"))  # every step has the same regions
+    ctx = kc.Context(0)
+    seq = ctx.load_seq(a.dir)
+    steps, _ = ctx.replay_seq(seq, atol=a.atol, rtol=a.rtol)
+    out = {"n": len(seq), "deps": seq.deps(), "steps": steps, "pass": all(s["pass"] == 1 for s in steps)}
+    seq.free()
     ctx.close()
     print(json.dumps(out))
     return 0 if out["pass"] else 3
@@ -92,6 +108,7 @@ def main(argv=None) -> int:
     c.add_argument("--index", type=int, default=0)
     c.add_argument("--mode", default="pre_w", choices=["pre_w", "post"])
     c.add_argument("--out", required=True)
+    c.add_argument("--count", type=int, default=1, help="consecutive launches to capture as a sequence (F4)")
     r = sub.add_parser("replay")
     r.add_argument("dir")
     r.add_argument("--override", default=None)
@@ -101,6 +118,10 @@ def main(argv=None) -> int:
     r.add_argument("--typed", default=None)
     r.add_argument("--atol", type=float, default=1e-8)
     r.add_argument("--rtol", type=float, default=1e-5)
+    q = sub.add_parser("replay-seq")
+    q.add_argument("dir")
+    q.add_argument("--atol", type=float, default=1e-8)
+    q.add_argument("--rtol", type=float, default=1e-5)
     i_ = sub.add_parser("info")
     i_.add_argument("dir")
     a = p.parse_args(argv)
@@ -108,6 +129,8 @@ def main(argv=None) -> int:
         return _capture(a, rest)
     if a.cmd == "replay":
         return _replay(a)
+    if a.cmd == "replay-seq":
+        return _replay_seq(a)
     return _info(a)
 
 

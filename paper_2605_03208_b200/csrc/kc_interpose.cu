@@ -202,6 +202,17 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
                     ip->steps.push_back(sn);
                     ip->state = ip->steps.size() < ip->count ? 1 : 3;
                     ip->armed = ip->state == 1;  // the next launch of the sequence
+                    if (ip->state == 3 && !dir.empty()) {  // complete and a directory given: persist it
+                        kc_sequence* q = nullptr;
+                        kc_status s2 = make_sequence(ctx, ip->steps, &q);
+                        if (s2 == KC_OK) s2 = kc_seq_save(ctx, q, dir.c_str());
+                        if (s2 != KC_OK) {
+                            ip->state = -1;
+                            ip->status = s2;
+                            ip->err = kc_last_error(ctx);
+                        }
+                        if (q) kc_seq_free(q);  // the steps went into q (or stay in ip->steps on failure)
+                    }
                 } else {
                     ip->state = 3;
                     if (ip->snap) kc_snapshot_free(ip->snap);
@@ -324,6 +335,8 @@ void kc::interpose_arm_from_env(kc_ctx* ctx) {
     const char* t = getenv("KC_TARGET");
     const char* ix = getenv("KC_DISPATCH_INDEX");
     const char* m = getenv("KC_CAPTURE_MODE");
-    kc_interpose_arm(ctx, t, ix ? strtoull(ix, nullptr, 10) : 0, dir,
-                     m && strcmp(m, "post") == 0 ? KC_MODE_POST : KC_MODE_PRE_W, 0);
+    const char* cnt = getenv("KC_CAPTURE_COUNT");
+    const uint64_t count = cnt ? strtoull(cnt, nullptr, 10) : 1;
+    arm(ctx, t, ix ? strtoull(ix, nullptr, 10) : 0, count ? count : 1, dir,
+        m && strcmp(m, "post") == 0 && count <= 1 ? KC_MODE_POST : KC_MODE_PRE_W, 0);
 }

@@ -1045,6 +1045,9 @@ kc_status load_desc_files(kc_ctx* ctx, const std::string& dir, SnapDesc& d, kc_r
     if (const kcj::Value* g = dv.get("block"))
         for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) d.block[i] = (uint32_t)g->a[i].as_u64(1);
     if (const kcj::Value* g = dv.get("shared_mem_bytes")) d.smem = (uint32_t)g->as_u64();
+    if (const kcj::Value* g = dv.get("kernarg_layout"))  // (offset, size) per parameter (R22)
+        for (const auto& e : g->a)
+            if (e.get("offset") && e.get("size")) d.layout.emplace_back(e.get("offset")->as_u64(), e.get("size")->as_u64());
     if (!read_bin(dir + "/kernarg.bin", d.kernarg)) return set_err(ctx, KC_ERR_FORMAT, "cannot read kernarg.bin");
     const uint64_t ksz = dv.get("kernarg_size") ? dv.get("kernarg_size")->as_u64() : d.kernarg.size();
     if (ksz != d.kernarg.size())

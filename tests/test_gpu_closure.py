@@ -496,6 +496,8 @@ def test_saved_sequence_replays_in_a_fresh_process(tmp_path):
     run("interpose-seq", d)
     res = run("load-seq", d)
     assert res["n"] == 3 and [s["pass"] for s in res["steps"]] == [1, 1, 1], res["steps"]
+    import paper_2605_03208_b200.kc as kc   # the loaded steps keep their kernarg layouts: same dependencies
+    assert res["deps"] == [[0, 0, 0], [0, 0, 0], [kc.KC_DEP_RAW | kc.KC_DEP_WAW | kc.KC_DEP_WAR, 0, 0]]
     assert [s["inherited_chunks"] for s in res["steps"]] == [0, 0, 0]
 
 
@@ -545,3 +547,25 @@ def test_failed_interposed_capture_never_blocks_the_application(tmp_path):
     v0 = init_nodes.view(nodes_dt)["value"].astype(np.uint64)
     app_nodes = np.load(str(tmp_path / "ipbad_app_nodes.npy")).view(nodes_dt)
     assert np.array_equal(app_nodes["value"], ((3 * v0 + 1) % 2**32).astype(np.uint32))
+
+
+def test_cli_sequence_capture_and_joint_replay(tmp_path):
+    """`cli capture --count 3` on an application without library code captures
+    its three dependent launches as a sequence (kc-sequence/1, saved when the
+    last step completes); `cli replay-seq` in a fresh process replays them
+    jointly, every step bit-exact, with the hand-derived dependency matrix."""
+    import paper_2605_03208_b200.kc as kc
+    from oracle import snapshot
+    d = str(tmp_path / "cliseq")
+    cli = [sys.executable, "-m", "paper_2605_03208_b200.cli"]
+    p = subprocess.run(cli + ["capture", "--count", "3", "--out", d, "--", sys.executable,
+                              os.path.join(ROOT, "tests", "apps", "driver_seq_app.py"), ROOT],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    RAW, WAW, WAR = kc.KC_DEP_RAW, kc.KC_DEP_WAW, kc.KC_DEP_WAR
+    expect = [[0, 0, 0], [0, 0, 0], [RAW | WAW | WAR, 0, 0]]
+    assert snapshot.verify_sequence(d)["deps"] == expect
+    p = subprocess.run(cli + ["replay-seq", d], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    res = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["pass"] and res["n"] == 3 and res["deps"] == expect
