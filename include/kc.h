@@ -166,7 +166,17 @@ typedef struct {
     const void* image_override; /* variant code object ("--hsaco") */
     size_t image_override_size;
     void* stream;
+    /* launch-shape overrides for a variant whose configuration differs (a
+     * retuned tile: other block size or dynamic shared memory; the paper's
+     * reproducer exposes the launch configuration for editing).  Bits of
+     * `overrides`: 1 grid, 2 block, 4 smem_bytes, 8 symbol; zero = as captured.
+     * The kernarg buffer is always the captured one. */
+    uint32_t overrides;
+    uint32_t grid[3], block[3];
+    uint32_t smem_bytes;
+    const char* symbol;         /* kernel name in the override code object */
 } kc_replay_opts;
+enum { KC_OVR_GRID = 1, KC_OVR_BLOCK = 2, KC_OVR_SMEM = 4, KC_OVR_SYMBOL = 8 };
 
 typedef struct {
     uint32_t iterations;

@@ -27,6 +27,8 @@ FIXTURE_VARIANTS = {os.path.join(ROOT, "synth", "kc_fixtures_recompiled.cubin"):
 ATTN_SRC = os.path.join(ROOT, "synth", "kc_attn_fwd.cu")
 ATTN_BLOCK_N = (32, 64, 128)
 ATTN_CUBINS = {bn: os.path.join(ROOT, "synth", f"kc_attn_fwd_n{bn}.cubin") for bn in ATTN_BLOCK_N}
+# a retuned variant with another launch shape (BLOCK_M = 32: grid x2, 128 threads), same numerics
+ATTN_M32_CUBIN = os.path.join(ROOT, "synth", "kc_attn_fwd_m32n64.cubin")
 SOURCES = ["kc_kernels.cu", "kc_runtime.cu", "kc_snapshot.cu", "kc_module.cu", "kc_sequence.cu", "kc_interpose.cu"]
 HEADERS = ["kc_kernels.cuh", "kc_internal.h", "kc_json.h", "kc_snapshot_types.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -63,11 +65,11 @@ def build_fixtures(force: bool = False) -> str:
             tmp = out + f".tmp{os.getpid()}"
             subprocess.check_call([NVCC, "-cubin", *ARCH, *flags, "-lineinfo", "-o", tmp, FIXTURE_SRC])
             os.replace(tmp, out)
-    for bn, out in ATTN_CUBINS.items():
+    for bn, out in list(ATTN_CUBINS.items()) + [("m32", ATTN_M32_CUBIN)]:
         if force or _stale(out, [ATTN_SRC]):
             tmp = out + f".tmp{os.getpid()}"
-            subprocess.check_call([NVCC, "-cubin", *ARCH, "-O3", "-lineinfo", f"-DKC_ATTN_BLOCK_N={bn}",
-                                   "-o", tmp, ATTN_SRC])
+            flags = ["-DKC_ATTN_BLOCK_M=32", "-DKC_ATTN_BLOCK_N=64"] if bn == "m32" else [f"-DKC_ATTN_BLOCK_N={bn}"]
+            subprocess.check_call([NVCC, "-cubin", *ARCH, "-O3", "-lineinfo", *flags, "-o", tmp, ATTN_SRC])
             os.replace(tmp, out)
     return FIXTURE_CUBIN
 

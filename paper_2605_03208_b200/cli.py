@@ -2,8 +2,9 @@
 1061-1135) over libkc.so.
 
     python -m paper_2605_03208_b200.cli capture --kernel NAME [--index N] [--mode pre_w|post] --out DIR -- CMD ...
-    python -m paper_2605_03208_b200.cli replay DIR [--override CUBIN] [--iterations N] [--no-recopy]
-                                                  [--dump] [--typed HEXVA:NBYTES:DTYPE] [--atol A --rtol R]
+    python -m paper_2605_03208_b200.cli replay DIR [--override CUBIN [--grid X,Y,Z --block X,Y,Z --smem B
+                                                  --symbol NAME]] [--iterations N] [--no-recopy] [--dump]
+                                                  [--typed HEXVA:NBYTES:DTYPE] [--atol A --rtol R]
     python -m paper_2605_03208_b200.cli capture --kernel NAME --index N --count K --out DIR -- CMD ...   (a sequence)
     python -m paper_2605_03208_b200.cli replay-seq DIR
     python -m paper_2605_03208_b200.cli info DIR
@@ -51,7 +52,9 @@ def _replay(a) -> int:
     r, rst = kc.restore_in_fresh_layout(ctx, a.dir, sys.argv)
     override = open(a.override, "rb").read() if a.override else None
     dump = os.path.abspath(a.dir.rstrip("/") + "_replay") if a.dump else None
-    rep = ctx.replay(r, iterations=a.iterations, no_recopy=a.no_recopy, dump_dir=dump, image_override=override)
+    shape = lambda v: tuple(int(x) for x in v.split(",")) if v else None  # noqa: E731
+    rep = ctx.replay(r, iterations=a.iterations, no_recopy=a.no_recopy, dump_dir=dump, image_override=override,
+                     grid=shape(a.grid), block=shape(a.block), smem=a.smem, symbol=a.symbol)
     out = {"restore": rst, "replay": rep}
     if a.typed:
         va, nb, dt = a.typed.split(":")
@@ -73,7 +76,7 @@ def _replay_seq(a) -> int:
     kc.exec_replay_process(sys.argv, os.path.join(a.dir, "step_000"))  # every step has the same regions
     ctx = kc.Context(0)
     seq = ctx.load_seq(a.dir)
-    steps, _ = ctx.replay_seq(seq, atol=a.atol, rtol=a.rtol)
+    steps, _ = kc.replay_seq_in_fresh_layout(ctx, seq, sys.argv, atol=a.atol, rtol=a.rtol)
     out = {"n": len(seq), "deps": seq.deps(), "steps": steps, "pass": all(s["pass"] == 1 for s in steps)}
     seq.free()
     ctx.close()
@@ -114,6 +117,10 @@ def main(argv=None) -> int:
     r.add_argument("--override", default=None)
     r.add_argument("--iterations", type=int, default=1)
     r.add_argument("--no-recopy", action="store_true")
+    r.add_argument("--grid", default=None, help="launch-shape override for a retuned variant, e.g. 128,32")
+    r.add_argument("--block", default=None, help="e.g. 128")
+    r.add_argument("--smem", type=int, default=None, help="dynamic shared memory bytes")
+    r.add_argument("--symbol", default=None, help="kernel name in the override code object")
     r.add_argument("--dump", action="store_true")
     r.add_argument("--typed", default=None)
     r.add_argument("--atol", type=float, default=1e-8)

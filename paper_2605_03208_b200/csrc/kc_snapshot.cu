@@ -2667,13 +2667,21 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
         }
         mod = h->module;
     }
+    // launch shape: as captured unless a variant overrides it
+    const std::string sym = (o->overrides & KC_OVR_SYMBOL) && o->symbol ? std::string(o->symbol) : h->mangled;
+    uint32_t grid[3], block[3];
+    for (int i = 0; i < 3; ++i) {
+        grid[i] = (o->overrides & KC_OVR_GRID) ? o->grid[i] : h->grid[i];
+        block[i] = (o->overrides & KC_OVR_BLOCK) ? o->block[i] : h->block[i];
+    }
+    const uint32_t smem = (o->overrides & KC_OVR_SMEM) ? o->smem_bytes : h->smem;
     CUfunction f = nullptr;
-    if (KC_DRV(cuModuleGetFunction)(&f, mod, h->mangled.c_str()) != CUDA_SUCCESS) {
+    if (KC_DRV(cuModuleGetFunction)(&f, mod, sym.c_str()) != CUDA_SUCCESS) {
         if (own) KC_DRV(cuModuleUnload)(mod);
-        return set_err(ctx, KC_ERR_ARG, "kc_replay: symbol %s not found in the code object", h->mangled.c_str());
+        return set_err(ctx, KC_ERR_ARG, "kc_replay: symbol %s not found in the code object", sym.c_str());
     }
     {
-        const CUresult r = allow_dynamic_smem(f, h->smem);
+        const CUresult r = allow_dynamic_smem(f, smem);
         if (r != CUDA_SUCCESS) {
             if (own) KC_DRV(cuModuleUnload)(mod);
             return cu_err(ctx, r, "kc_replay: dynamic shared memory attribute");
@@ -2731,11 +2739,11 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
             size_t ksz = h->kernarg.size();
             void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, h->kernarg.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
                              CU_LAUNCH_PARAM_END};
-            r = KC_DRV(cuLaunchKernel)(f, h->grid[0], h->grid[1], h->grid[2], h->block[0], h->block[1], h->block[2], h->smem,
-                               (CUstream)s, nullptr, extra);
+            r = KC_DRV(cuLaunchKernel)(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, (CUstream)s,
+                                       nullptr, extra);
         } else {
-            r = KC_DRV(cuLaunchKernel)(f, h->grid[0], h->grid[1], h->grid[2], h->block[0], h->block[1], h->block[2], h->smem,
-                               (CUstream)s, nullptr, nullptr);
+            r = KC_DRV(cuLaunchKernel)(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, (CUstream)s,
+                                       nullptr, nullptr);
         }
         cudaEventRecord(e1, s);
         if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)s);

@@ -116,7 +116,8 @@ class CaptureReport(ctypes.Structure):
 class ReplayOpts(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_uint32), ("no_recopy", ctypes.c_int32), ("dump_dir", ctypes.c_char_p),
                 ("image_override", ctypes.c_void_p), ("image_override_size", ctypes.c_size_t),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("overrides", ctypes.c_uint32), ("grid", ctypes.c_uint32 * 3),
+                ("block", ctypes.c_uint32 * 3), ("smem_bytes", ctypes.c_uint32), ("symbol", ctypes.c_char_p)]
 
 
 class ReplayReport(ctypes.Structure):
@@ -313,6 +314,17 @@ def restore_in_fresh_layout(ctx: "Context", snapshot_dir: str, argv: list, max_a
     The restore itself never relocates: it aborts and rolls back (R21)."""
     try:
         return ctx.restore(snapshot_dir)
+    except KcError as e:
+        if e.status == KC_ERR_VA_UNAVAILABLE:
+            _reexec(argv, max_attempts)
+        raise
+
+
+def replay_seq_in_fresh_layout(ctx: "Context", seq: "Sequence", argv: list, max_attempts: int = 8, **kw):
+    """ctx.replay_seq() with the same policy as restore_in_fresh_layout: a
+    collision of the captured VAs with this process's driver arenas re-execs it."""
+    try:
+        return ctx.replay_seq(seq, **kw)
     except KcError as e:
         if e.status == KC_ERR_VA_UNAVAILABLE:
             _reexec(argv, max_attempts)
@@ -672,11 +684,25 @@ class Context:
         return Restored(h.value, self), rep.as_dict()
 
     def replay(self, restored: Restored, iterations: int = 1, no_recopy: bool = False, dump_dir: str | None = None,
-               image_override: bytes | None = None, stream: int = 0) -> dict:
+               image_override: bytes | None = None, stream: int = 0, grid=None, block=None, smem: int | None = None,
+               symbol: str | None = None) -> dict:
+        """kc_replay; grid/block/smem/symbol override the captured launch shape (a retuned variant)."""
         ov = ctypes.create_string_buffer(image_override, len(image_override)) if image_override else None
         o = ReplayOpts(iterations, int(no_recopy), dump_dir.encode() if dump_dir else None,
                        ctypes.cast(ov, ctypes.c_void_p) if ov else None, len(image_override) if image_override else 0,
                        stream or None)
+        if grid is not None:
+            o.overrides |= 1
+            o.grid[:] = list(grid) + [1] * (3 - len(grid))
+        if block is not None:
+            o.overrides |= 2
+            o.block[:] = list(block) + [1] * (3 - len(block))
+        if smem is not None:
+            o.overrides |= 4
+            o.smem_bytes = smem
+        if symbol is not None:
+            o.overrides |= 8
+            o.symbol = symbol.encode()
         rep = ReplayReport()
         self._check(lib().kc_replay(self._h, restored.handle, ctypes.byref(o), ctypes.byref(rep)), "kc_replay")
         return rep.as_dict()

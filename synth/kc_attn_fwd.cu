@@ -21,8 +21,8 @@
 //   m_i   = m_ij
 // out = fp16(acc / l_i).
 //
-// Layout: Q, K, V, O contiguous [B][H][S][128] fp16; grid (S/64, B*H), block
-// 256: BLOCK_M = 64 query rows per CTA, 4 threads per row.  Thread (r, c4):
+// Layout: Q, K, V, O contiguous [B][H][S][128] fp16; grid (S/BLOCK_M, B*H),
+// block 4*BLOCK_M: BLOCK_M = 64 query rows per CTA by default, 4 threads per row.  Thread (r, c4):
 // score columns n = c4 + 4j of each 32-key sub-tile, output columns
 // c4*32 .. c4*32+31.  Requires S % BLOCK_N == 0 and S % 64 == 0.
 #include <cuda_fp16.h>
@@ -31,9 +31,12 @@
 #ifndef KC_ATTN_BLOCK_N
 #define KC_ATTN_BLOCK_N 64
 #endif
+#ifndef KC_ATTN_BLOCK_M  // query rows per CTA (4 threads each); does not change any row's arithmetic
+#define KC_ATTN_BLOCK_M 64
+#endif
 
 namespace {
-constexpr int D = 128, BM = 64, SUB = 32, PAD = 8, T = 256;
+constexpr int D = 128, BM = KC_ATTN_BLOCK_M, SUB = 32, PAD = 8, T = 4 * BM;
 constexpr int BN = KC_ATTN_BLOCK_N;
 static_assert(BN % SUB == 0, "BLOCK_N must be a multiple of 32");
 constexpr int NSUB = BN / SUB;
@@ -60,7 +63,7 @@ __device__ __forceinline__ void h8_to_f(const __half* p, float* f) {
 }
 }  // namespace
 
-extern "C" __global__ void __launch_bounds__(256) kc_fixture_attn_fwd(const __half* __restrict__ Q,
+extern "C" __global__ void __launch_bounds__(4 * KC_ATTN_BLOCK_M) kc_fixture_attn_fwd(const __half* __restrict__ Q,
                                                                       const __half* __restrict__ K,
                                                                       const __half* __restrict__ V,
                                                                       __half* __restrict__ O, int S, float sm_scale) {

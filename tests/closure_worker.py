@@ -455,7 +455,12 @@ def load_replay(a):
     out = {"load_s": time.perf_counter() - t0, "is_host": snap.is_host(), "cycles": []}
     for _ in range(a.cycles):
         t1 = time.perf_counter()
-        r, rst = ctx.restore_dev(snap)
+        try:
+            r, rst = ctx.restore_dev(snap)
+        except kc.KcError as e:   # the driver's arenas landed on a captured VA: fresh layout (R28c)
+            if e.status == kc.KC_ERR_VA_UNAVAILABLE:
+                kc._reexec(sys.argv, 8)
+            raise
         t2 = time.perf_counter()
         ctx.replay(r)
         reps, unexpected = ctx.validate(r)
@@ -475,7 +480,7 @@ def load_seq(a):
     kc.exec_replay_process(sys.argv, os.path.join(a.dir, "step_000"))
     ctx = kc.Context(0)
     seq = ctx.load_seq(a.dir)
-    steps, _ = ctx.replay_seq(seq)
+    steps, _ = kc.replay_seq_in_fresh_layout(ctx, seq, sys.argv)
     out = {"n": len(seq), "deps": seq.deps(), "steps": steps}
     seq.free()
     print(json.dumps(out))

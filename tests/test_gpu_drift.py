@@ -13,6 +13,8 @@ against the oracle's O4 diff of the same bytes, and every config against the
 fp64 attention definition (oracle.attention) on sampled rows, so the drift is
 shown to be reordering, not error.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -66,15 +68,22 @@ def study():
     for va in vas:
         ctx.free(va)
     runs = {}
-    for name, bn in (("pinned", 64), ("n32", 32), ("n128", 128)):
+    m32 = open(os.path.join(os.path.dirname(synth.f4_cubin(64)), "kc_attn_fwd_m32n64.cubin"), "rb").read()
+    for name, bn in (("pinned", 64), ("n32", 32), ("n128", 128), ("m32", 64)):
         r, _ = ctx.restore_dev(snap)
         assert [x.base for x in r.regions()] == sorted(vas)
-        rep = ctx.replay(r, image_override=None if name == "pinned" else images[bn])
+        if name == "m32":   # BLOCK_M 32: a retuned launch shape, replayed with overrides
+            with pytest.raises(kc.KcError):   # the captured 256-thread block exceeds its launch bounds
+                ctx.replay(r, image_override=m32)
+            rep = ctx.replay(r, image_override=m32, grid=(synth.F4_S // 32, synth.F4_B * synth.F4_H),
+                             block=(128,))
+        else:
+            rep = ctx.replay(r, image_override=None if name == "pinned" else images[bn])
         typed, _ = ctx.validate(r, outs=[(o_va, n, "f16")])
         loose, _ = ctx.validate(r, outs=[(o_va, n, "f16")], atol=1e-3, rtol=1e-3)
         o = synth.dev_view(o_va, n).cpu().numpy().copy()
         runs[name] = {"replay": rep, "typed": typed[0], "loose": loose[0], "out": o}
-        if name != "pinned":
+        if name in ("n32", "n128"):
             outs[bn] = o
         r.release()
     snap.free()
@@ -111,6 +120,16 @@ def test_other_config_drifts_and_k2_matches_oracle(study, name, bn):
     assert 1 <= rep["max_ulp"] <= 64 and rep["nan_act"] == 0 and rep["nan_ref"] == 0
     assert rep["max_abs"] < 1e-2
     assert rep["pass"] == 0                     # strict numpy defaults flag it (the contract is broken)
+
+
+def test_retuned_launch_shape_replays_bit_exact(study):
+    """BLOCK_M does not touch any row's arithmetic: the BLOCK_M = 32 variant,
+    replayed with the launch-shape overrides (grid x2, 128 threads), reproduces
+    the captured BLOCK_M = 64 output bit for bit (the numerical contract is
+    BLOCK_N's, PAPER.md:266-267)."""
+    r = study["runs"]["m32"]
+    assert np.array_equal(r["out"], study["outs"][64])
+    assert r["typed"]["differing_bytes"] == 0 and r["typed"]["pass"] == 1
 
 
 def test_k2_direct_between_configs_matches_oracle(study):
