@@ -154,3 +154,46 @@ def test_each_config_is_attention(study, bn):
         err = np.abs(o[bh, rows].astype(np.float64) - exact).max()
         worst = max(worst, err)
     assert worst < ATTN_ATOL, worst
+
+
+@pytest.mark.slow
+def test_triton_autotune_configs_drift(tmp_path):
+    """The paper's measurement itself on a real Triton kernel:
+    tests/apps/triton_attn.py (fp16, B=2, H=16, S=4096, D=128) runs config a
+    (BLOCK_N 64, 8 warps) unmodified under `cli capture`; config b (BLOCK_N 32,
+    4 warps) is compiled to a code object and replayed on the captured state with
+    the launch-shape overrides (`cli replay --override --block --smem --symbol`).
+    The pinned replay is bit-exact; config b's typed report shows the drift: a
+    visible fraction of elements move by a few fp16 ULPs."""
+    pytest.importorskip("triton")
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    app = os.path.join(root, "tests", "apps", "triton_attn.py")
+    cli = [sys.executable, "-m", "paper_2605_03208_b200.cli"]
+    d = str(tmp_path / "attn")
+    p = subprocess.run(cli + ["capture", "--kernel", "attn_fwd", "--out", d, "--", sys.executable, app],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    app_out = lines[0]
+    assert app_out["max_err_vs_fp32"] < 2e-3
+    cubin = str(tmp_path / "b.cubin")
+    p = subprocess.run([sys.executable, app, "--compile-variant", cubin], capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    var = json.loads(p.stdout.strip().splitlines()[-1])
+    typed = f"{app_out['o_ptr']:x}:{app_out['o_bytes']}:f16"
+    p = subprocess.run(cli + ["replay", d, "--typed", typed], capture_output=True, text=True, timeout=900, cwd=root)
+    assert p.returncode == 0, p.stdout + p.stderr[-3000:]
+    pinned = json.loads(p.stdout.strip().splitlines()[-1])
+    assert pinned["pass"] and pinned["typed"][0]["differing_bytes"] == 0
+    p = subprocess.run(cli + ["replay", d, "--typed", typed, "--override", cubin, "--symbol", var["symbol"],
+                              "--block", str(var["block"]), "--smem", str(var["smem"])],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    rep = json.loads(p.stdout.strip().splitlines()[-1])
+    t = rep["typed"][0]
+    frac = t["differing_elems"] / t["n_elems"]
+    print(f"Triton attn_fwd config b vs captured a: {100 * frac:.2f}% elements changed, max abs {t['max_abs']:.3e}, "
+          f"max ulp {t['max_ulp']}")
+    assert 0.001 < frac < 0.9 and t["max_abs"] < 1e-2 and t["nan_act"] == 0 and t["pass"] == 0
