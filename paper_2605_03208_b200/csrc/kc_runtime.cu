@@ -592,7 +592,6 @@ kc_status kc::hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_
         ctx->regs_input_sorted = sorted;
         ctx->regs_input_chunks = C;
     }
-    kc_status st = KC_OK;
     if (C && !d_chunk_hash) return set_err(ctx, KC_ERR_ARG, "kc_hash: d_chunk_hash is NULL");
     if (h_dst) {
         if (!ctx->regs_aligned) return set_err(ctx, KC_ERR_ARG, "K6: regions must be 16-byte aligned");

@@ -94,7 +94,7 @@ def test_struct_sizes_match_header(kclib):
     assert ctypes.sizeof(kclib.Dispatch) == 80
     assert ctypes.sizeof(kclib.Options) == 24
     assert ctypes.sizeof(kclib.CaptureReport) == 9 * 8 + 5 * 8
-    assert ctypes.sizeof(kclib.ReplayOpts) == 40
+    assert ctypes.sizeof(kclib.ReplayOpts) == 80
     assert ctypes.sizeof(kclib.RestoreReport) == 6 * 8 + 4 * 8
 
 
