@@ -132,6 +132,9 @@ typedef struct {
     uint32_t kernarg_size;
     const void* kernarg;
     void* stream;
+    uint32_t cluster[3];        /* thread-block cluster dims of a cluster launch (cuLaunchKernelEx
+                                   CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION); 0,0,0 or 1,1,1 = none.
+                                   Recorded in dispatch.json and reapplied by kc_replay */
 } kc_dispatch;
 
 /* kc_alloc backing (reading R6/R20): VMM allocations live in free VA space and

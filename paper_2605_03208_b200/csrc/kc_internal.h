@@ -16,7 +16,7 @@
 // Driver-API entry points resolved through cudart (cudaGetDriverEntryPoint),
 // so libkc.so has no link-time dependency on libcuda and loads on hosts
 // without a GPU driver (calls then fail with KC_ERR_CUDA).
-#define KC_DRV_FUNCS(X) X(cuCtxGetDevice) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemExportToShareableHandle) X(cuMemFree) X(cuMemImportFromShareableHandle) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
+#define KC_DRV_FUNCS(X) X(cuCtxGetDevice) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuLaunchKernelEx) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemExportToShareableHandle) X(cuMemFree) X(cuMemImportFromShareableHandle) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
 namespace kc {
 struct Drv {
 #define KC_DRV_DECL(f) decltype(&::f) f = nullptr;
@@ -147,6 +147,7 @@ struct kc_restored {
     int mode = KC_MODE_PRE_W;
     std::string mangled;
     uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0;
+    uint32_t cluster[3] = {1, 1, 1};
     std::vector<uint8_t> kernarg;
     std::vector<kc_restored_region> regions;  // sorted by base
     // VMM spans
@@ -216,6 +217,13 @@ kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std
 kc_status hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_chunk_hash, uint64_t* d_region_digest,
                     uint64_t* d_snapshot_digest, void* stream, const uint64_t* h_dst);
 
+// one launch of a captured dispatch: the packed kernarg buffer, and a cluster
+// launch (cuLaunchKernelEx + CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION) when any
+// cluster dim exceeds 1
+CUresult launch_packed(CUfunction f, const uint32_t grid[3], const uint32_t block[3], uint32_t smem, CUstream s,
+                       const void* kernarg, size_t kernarg_size, const uint32_t cluster[3]);
+// normalised cluster dims of a kc_dispatch (0 -> 1)
+void dispatch_cluster(const kc_dispatch* d, uint32_t out[3]);
 // kc_validate with an option to merge every region's W into one report (F4 sequences)
 kc_status validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n, const kc_tolerance* tol,
                         kc_diff_report* reps, size_t cap_reports, size_t* n_reports_out, uint64_t* unexpected_chunks,

@@ -99,7 +99,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
     const CUpti_CallbackData* d = (const CUpti_CallbackData*)cbdata;
     if (d->callbackSite == CUPTI_API_ENTER) {
         CUfunction f = nullptr;
-        uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0;
+        uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0, cluster[3] = {1, 1, 1};
         CUstream stream = nullptr;
         void** kp = nullptr;
         void** extra = nullptr;
@@ -122,6 +122,12 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
             stream = p->config->hStream;
             kp = p->kernelParams;
             extra = p->extra;
+            for (unsigned a = 0; a < p->config->numAttrs; ++a)  // a cluster launch (thread-block clusters)
+                if (p->config->attrs[a].id == CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION) {
+                    cluster[0] = p->config->attrs[a].value.clusterDim.x;
+                    cluster[1] = p->config->attrs[a].value.clusterDim.y;
+                    cluster[2] = p->config->attrs[a].value.clusterDim.z;
+                }
         }
         const char* name = nullptr;
         if (KC_DRV(cuFuncGetName)(&name, f) != CUDA_SUCCESS || !name) return;
@@ -151,7 +157,8 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
             return;
         }
         ip->worker = std::thread([ctx, ip, f, grid0 = grid[0], grid1 = grid[1], grid2 = grid[2], block0 = block[0],
-                                  block1 = block[1], block2 = block[2], smem, stream, mangled, kernarg]() {
+                                  block1 = block[1], block2 = block[2], smem, stream, mangled, kernarg,
+                                  cl0 = cluster[0], cl1 = cluster[1], cl2 = cluster[2]]() {
             Internal guard;  // the capture's own driver calls are not the application's
             kc_dispatch disp;
             memset(&disp, 0, sizeof disp);
@@ -163,6 +170,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
             disp.kernarg_size = (uint32_t)kernarg->size();
             disp.kernarg = kernarg->empty() ? nullptr : kernarg->data();
             disp.stream = (void*)stream;
+            disp.cluster[0] = cl0, disp.cluster[1] = cl1, disp.cluster[2] = cl2;
             // the application's launch happens between the two halves of the capture
             std::function<CUresult()> forward = [ip, stream]() -> CUresult {
                 std::unique_lock<std::mutex> lk(ip->hm);

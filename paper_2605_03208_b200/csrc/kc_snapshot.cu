@@ -392,7 +392,7 @@ struct LogRegion {
 
 std::string dispatch_json(int mode, const std::string& mangled, const uint32_t grid[3], const uint32_t block[3],
                           uint32_t smem, uint32_t kernarg_size, int device, const std::vector<uint8_t>& image,
-                          const std::vector<std::pair<size_t, size_t>>& layout) {
+                          const std::vector<std::pair<size_t, size_t>>& layout, const uint32_t cluster[3]) {
     const size_t image_size = image.size();
     int cc_major = 0, cc_minor = 0;
     cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device);
@@ -403,11 +403,11 @@ std::string dispatch_json(int mode, const std::string& mangled, const uint32_t g
     j += "  \"mangled_symbol\": \"" + kcj::esc(mangled) + "\",\n";
     char b[512];
     snprintf(b, sizeof b,
-             "  \"grid\": [%u, %u, %u],\n  \"block\": [%u, %u, %u],\n  \"cluster\": [1, 1, 1],\n"
+             "  \"grid\": [%u, %u, %u],\n  \"block\": [%u, %u, %u],\n  \"cluster\": [%u, %u, %u],\n"
              "  \"shared_mem_bytes\": %u,\n  \"kernarg_size\": %u,\n  \"device_ordinal\": %d,\n"
              "  \"compute_capability\": \"%d.%d\",\n  \"code_object_bytes\": %zu,\n",
-             grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, kernarg_size, device, cc_major, cc_minor,
-             image_size);
+             grid[0], grid[1], grid[2], block[0], block[1], block[2], cluster[0], cluster[1], cluster[2], smem,
+             kernarg_size, device, cc_major, cc_minor, image_size);
     j += b;
     j += "  \"kernarg_layout\": [";
     for (size_t i = 0; i < layout.size(); ++i) {
@@ -479,6 +479,39 @@ namespace {
 // function's opt-in attribute; the application set it on its own CUfunction,
 // a module the closure loads itself (capture from an image, replay) must set it
 // again before launching with the captured smem size.
+}  // namespace
+
+CUresult kc::launch_packed(CUfunction f, const uint32_t grid[3], const uint32_t block[3], uint32_t smem, CUstream s,
+                           const void* kernarg, size_t kernarg_size, const uint32_t cluster[3]) {
+    size_t ksz = kernarg_size;
+    void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, (void*)kernarg, CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
+                     CU_LAUNCH_PARAM_END};
+    void** ex = kernarg && kernarg_size ? extra : nullptr;
+    if (cluster && cluster[0] * cluster[1] * cluster[2] > 1) {
+        CUlaunchAttribute attr;
+        memset(&attr, 0, sizeof attr);
+        attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+        attr.value.clusterDim.x = cluster[0];
+        attr.value.clusterDim.y = cluster[1];
+        attr.value.clusterDim.z = cluster[2];
+        CUlaunchConfig cfg;
+        memset(&cfg, 0, sizeof cfg);
+        cfg.gridDimX = grid[0], cfg.gridDimY = grid[1], cfg.gridDimZ = grid[2];
+        cfg.blockDimX = block[0], cfg.blockDimY = block[1], cfg.blockDimZ = block[2];
+        cfg.sharedMemBytes = smem;
+        cfg.hStream = s;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        return KC_DRV(cuLaunchKernelEx)(&cfg, f, nullptr, ex);
+    }
+    return KC_DRV(cuLaunchKernel)(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, s, nullptr, ex);
+}
+
+void kc::dispatch_cluster(const kc_dispatch* d, uint32_t out[3]) {
+    for (int i = 0; i < 3; ++i) out[i] = d->cluster[i] ? d->cluster[i] : 1;
+}
+
+namespace {
 CUresult allow_dynamic_smem(CUfunction f, uint32_t smem) {
     if (smem <= 48u * 1024u) return CUDA_SUCCESS;
     return KC_DRV(cuFuncSetAttribute)(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
@@ -651,8 +684,10 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
     }
 
     auto write_metadata = [&](bool post_digests) -> bool {
+        uint32_t cl[3];
+        dispatch_cluster(d, cl);
         const std::string j = dispatch_json(mode, mangled, d->grid, d->block, d->smem_bytes, d->kernarg_size,
-                                            ctx->device, mc.image, layout);
+                                            ctx->device, mc.image, layout, cl);
         if (!write_text(dir + "/dispatch.json", j)) return false;
         if (!write_file(dir + "/kernarg.bin", d->kernarg, d->kernarg ? d->kernarg_size : 0)) return false;
         if (!mc.image.empty() && !write_file(dir + "/kernel.cubin", mc.image.data(), mc.image.size())) return false;
@@ -734,17 +769,9 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
     // ---- A3: forward the target dispatch, then wait for it
     t = now_s();
     {
-        CUresult r;
-        if (d->kernarg && d->kernarg_size) {
-            size_t ksz = d->kernarg_size;
-            void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, (void*)d->kernarg, CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
-                             CU_LAUNCH_PARAM_END};
-            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
-                               d->smem_bytes, (CUstream)cs, nullptr, extra);
-        } else {
-            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
-                               d->smem_bytes, (CUstream)cs, nullptr, nullptr);
-        }
+        uint32_t cl[3];
+        dispatch_cluster(d, cl);
+        CUresult r = launch_packed(f, d->grid, d->block, d->smem_bytes, (CUstream)cs, d->kernarg, d->kernarg_size, cl);
         if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)cs);
         if (r != CUDA_SUCCESS) {
             if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
@@ -1045,6 +1072,8 @@ kc_status load_desc_files(kc_ctx* ctx, const std::string& dir, SnapDesc& d, kc_r
     if (const kcj::Value* g = dv.get("block"))
         for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) d.block[i] = (uint32_t)g->a[i].as_u64(1);
     if (const kcj::Value* g = dv.get("shared_mem_bytes")) d.smem = (uint32_t)g->as_u64();
+    if (const kcj::Value* g = dv.get("cluster"))
+        for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) d.cluster[i] = std::max<uint32_t>(1, (uint32_t)g->a[i].as_u64(1));
     if (const kcj::Value* g = dv.get("kernarg_layout"))  // (offset, size) per parameter (R22)
         for (const auto& e : g->a)
             if (e.get("offset") && e.get("size")) d.layout.emplace_back(e.get("offset")->as_u64(), e.get("size")->as_u64());
@@ -1168,6 +1197,7 @@ static void bind_dispatch_fields(kc_restored* h, const SnapDesc& d) {
         h->block[i] = d.block[i];
     }
     h->smem = d.smem;
+    for (int i = 0; i < 3; ++i) h->cluster[i] = d.cluster[i];
     h->kernarg = d.kernarg;
     h->image = d.image;
     h->modvars = d.modvars;
@@ -1979,6 +2009,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         D.block[i] = d->block[i];
     }
     D.smem = d->smem_bytes;
+    dispatch_cluster(d, D.cluster);
     if (d->kernarg && d->kernarg_size)
         D.kernarg.assign((const uint8_t*)d->kernarg, (const uint8_t*)d->kernarg + d->kernarg_size);
     ModCapture mc;  // F3
@@ -2171,17 +2202,9 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
         const CUresult r = (*forward)();
         if (r != CUDA_SUCCESS) return fail(cu_err(ctx, r, "kc_capture: intercepted dispatch"));
     } else {
-        CUresult r;
-        if (d->kernarg && d->kernarg_size) {
-            size_t ksz = d->kernarg_size;
-            void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, (void*)d->kernarg, CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
-                             CU_LAUNCH_PARAM_END};
-            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
-                                       d->smem_bytes, (CUstream)cs, nullptr, extra);
-        } else {
-            r = KC_DRV(cuLaunchKernel)(f, d->grid[0], d->grid[1], d->grid[2], d->block[0], d->block[1], d->block[2],
-                                       d->smem_bytes, (CUstream)cs, nullptr, nullptr);
-        }
+        uint32_t cl[3];
+        dispatch_cluster(d, cl);
+        CUresult r = launch_packed(f, d->grid, d->block, d->smem_bytes, (CUstream)cs, d->kernarg, d->kernarg_size, cl);
         if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)cs);
         if (r != CUDA_SUCCESS) return fail(cu_err(ctx, r, "kc_capture_dev: target dispatch"));
     }
@@ -2365,7 +2388,7 @@ static kc_status save_impl(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c,
     // metadata first
     if (!write_text(dir + "/dispatch.json", dispatch_json(D.mode, D.mangled, D.grid, D.block, D.smem,
                                                           (uint32_t)D.kernarg.size(), ctx->device, D.image,
-                                                          D.layout)) ||
+                                                          D.layout, D.cluster)) ||
         !write_file(dir + "/kernarg.bin", D.kernarg.data(), D.kernarg.size()) ||
         (!D.image.empty() && !write_file(dir + "/kernel.cubin", D.image.data(), D.image.size())) ||
         !write_module_vars(dir, D.modvars))
@@ -2734,17 +2757,8 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
             if (h->mode == KC_MODE_PRE_W) put_modvars(true);
         }
         cudaEventRecord(e0, s);
-        CUresult r;
-        if (!h->kernarg.empty()) {
-            size_t ksz = h->kernarg.size();
-            void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, h->kernarg.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
-                             CU_LAUNCH_PARAM_END};
-            r = KC_DRV(cuLaunchKernel)(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, (CUstream)s,
-                                       nullptr, extra);
-        } else {
-            r = KC_DRV(cuLaunchKernel)(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, (CUstream)s,
-                                       nullptr, nullptr);
-        }
+        CUresult r = launch_packed(f, grid, block, smem, (CUstream)s, h->kernarg.empty() ? nullptr : h->kernarg.data(),
+                                   h->kernarg.size(), h->cluster);
         cudaEventRecord(e1, s);
         if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)s);
         if (r != CUDA_SUCCESS) {

@@ -95,7 +95,7 @@ class Dispatch(ctypes.Structure):
     _fields_ = [("func", ctypes.c_void_p), ("image", ctypes.c_void_p), ("image_size", ctypes.c_size_t),
                 ("mangled", ctypes.c_char_p), ("grid", ctypes.c_uint32 * 3), ("block", ctypes.c_uint32 * 3),
                 ("smem_bytes", ctypes.c_uint32), ("kernarg_size", ctypes.c_uint32), ("kernarg", ctypes.c_void_p),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("cluster", ctypes.c_uint32 * 3)]
 
 
 class Options(ctypes.Structure):
@@ -568,10 +568,10 @@ class Context:
     # -- closure
     def capture(self, directory: str, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
                 block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
-                stream: int = 0, func: int = 0) -> tuple[int, dict]:
+                stream: int = 0, func: int = 0, cluster=None) -> tuple[int, dict]:
         """kc_capture.  func: a CUfunction handle of the application's own module
         (then image may be omitted when kc_track_install recorded the module's load)."""
-        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func)
+        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func, cluster)
         rep = CaptureReport()
         arr = _regions(regions) if regions is not None else None
         rc = lib().kc_capture(self._h, ctypes.byref(d), arr, len(regions) if regions is not None else 0,
@@ -579,23 +579,24 @@ class Context:
         self._check(rc, "kc_capture", ok=(KC_OK, KC_PARTIAL))
         return rc, rep.as_dict()
 
-    def _dispatch(self, image, mangled, grid, block, smem, kernarg, stream, func=0):
+    def _dispatch(self, image, mangled, grid, block, smem, kernarg, stream, func=0, cluster=None):
         img = ctypes.create_string_buffer(image, len(image)) if image else None
         ka = ctypes.create_string_buffer(kernarg, len(kernarg)) if kernarg else None
         d = Dispatch(func or None, ctypes.cast(img, ctypes.c_void_p) if img else None, len(image) if image else 0,
                      mangled.encode() if mangled else None, (ctypes.c_uint32 * 3)(*grid),
                      (ctypes.c_uint32 * 3)(*block), smem, len(kernarg), ctypes.cast(ka, ctypes.c_void_p) if ka else None,
-                     stream or None)
+                     stream or None, (ctypes.c_uint32 * 3)(*(tuple(cluster) + (1,) * (3 - len(cluster))))
+                     if cluster else (ctypes.c_uint32 * 3)(0, 0, 0))
         return d, (img, ka)
 
     def capture_dev(self, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
                     block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
-                    stream: int = 0, host: bool = False, base: "DevSnapshot | None" = None, func: int = 0
-                    ) -> tuple[DevSnapshot, dict]:
+                    stream: int = 0, host: bool = False, base: "DevSnapshot | None" = None, func: int = 0,
+                    cluster=None) -> tuple[DevSnapshot, dict]:
         """kc_capture into a device arena (F1), or a pinned host arena (host=True:
         kc_capture_host); with base=, only chunks changed against it are copied
-        (kc_capture_incr)."""
-        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func)
+        (kc_capture_incr); cluster = thread-block cluster dims of a cluster launch."""
+        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func, cluster)
         rep = CaptureReport()
         h = ctypes.c_void_p()
         arr = _regions(regions) if regions is not None else None
@@ -715,7 +716,7 @@ class Context:
         for i, d in enumerate(dispatches):
             arr[i], k = self._dispatch(d.get("image"), d.get("mangled"), d.get("grid", (1, 1, 1)),
                                        d.get("block", (1, 1, 1)), d.get("smem", 0), d.get("kernarg", b""),
-                                       d.get("stream", 0), d.get("func", 0))
+                                       d.get("stream", 0), d.get("func", 0), d.get("cluster"))
             keep.append(k)
         reps = (CaptureReport * len(dispatches))()
         h = ctypes.c_void_p()

@@ -3,6 +3,7 @@
 // path: compiled to synth/kc_fixtures.cubin and loaded through kc_capture's
 // (image, mangled) dispatch description, exactly like a captured code object.
 // Every kernel accumulates in a fixed order, so a replay is bit-reproducible.
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -149,4 +150,20 @@ extern "C" __global__ void kc_fixture_smem_reverse(const unsigned int* __restric
     for (unsigned int i = threadIdx.x; i < per_block; i += blockDim.x) stage[i] = in[b0 + i];
     __syncthreads();
     for (unsigned int i = threadIdx.x; i < per_block; i += blockDim.x) out[b0 + i] = stage[per_block - 1 - i] ^ blockIdx.x;
+}
+
+// A dispatch launched with runtime thread-block clusters (cuLaunchKernelEx +
+// CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION): each block records its rank in the
+// cluster, the cluster size, and its neighbour's value read through
+// distributed shared memory -- all different without the cluster launch.
+extern "C" __global__ void kc_fixture_cluster(unsigned int* out) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ unsigned int v;
+    if (threadIdx.x == 0) v = blockIdx.x * 7u + 1u;
+    cl.sync();
+    const unsigned int rank = cl.block_rank(), nb = cl.num_blocks();
+    const unsigned int* peer = cl.map_shared_rank(&v, (rank + 1) % nb);
+    if (threadIdx.x == 0) out[blockIdx.x] = (rank << 24) | (nb << 16) | (*peer & 0xFFFFu);
+    cl.sync();
 }

@@ -96,3 +96,39 @@ def test_device_capture_ragged_regions(env, tmp_path, fused, mode, monkeypatch):
     for r, of, sz in zip(sorted(s.regions, key=lambda r: r.base), offs, sizes):
         assert np.array_equal(s.region_bytes(r), before[of:of + sz]), f"stored bytes of region +{of} differ"
     assert rep["written_chunks"] == 1
+
+
+def test_cluster_launch_capture_replay(env, tmp_path):
+    """A dispatch launched with thread-block clusters (Blackwell cluster launch,
+    CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION = 2): the cluster dims are part of the
+    dispatch state.  They are recorded (dispatch.json "cluster"), the replay
+    launches with them again, and the output -- cluster rank, cluster size and a
+    neighbour's value read through distributed shared memory -- matches the
+    definition and validates bit-exactly."""
+    import json
+    import os
+    ctx, kc, synth = env
+    n = 64
+    vout = ctx.alloc(4 * n)
+    synth.dev_view(vout, 4 * n).zero_()
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    disp = dict(image=image, mangled="kc_fixture_cluster", grid=(n, 1, 1), block=(32, 1, 1),
+                kernarg=struct.pack("<Q", vout), regions=[(vout, 4 * n)], cluster=(2, 1, 1))
+    snap, rep = ctx.capture_dev(**disp)
+    b = np.arange(n, dtype=np.uint32)
+    rank = b % 2
+    peer = (b - rank + (rank + 1) % 2) * 7 + 1
+    expect = (rank << 24) | (2 << 16) | (peer & 0xFFFF)
+    got = synth.dev_view(vout, 4 * n).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, expect), "the cluster launch did not run as defined"
+    d = str(tmp_path / "cl")
+    snap.save(d)
+    assert json.load(open(os.path.join(d, "dispatch.json")))["cluster"] == [2, 1, 1]
+    ctx.free(vout)
+    r, _ = ctx.restore_dev(snap)
+    ctx.replay(r)
+    reps, unexpected = ctx.validate(r)
+    assert reps and reps[0]["differing_bytes"] == 0 and unexpected == 0
+    assert np.array_equal(synth.dev_view(vout, 4 * n).cpu().numpy().view(np.uint32), expect)
+    r.release()
+    snap.free()

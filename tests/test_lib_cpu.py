@@ -91,7 +91,7 @@ def test_struct_sizes_match_header(kclib):
     assert ctypes.sizeof(kclib.Buffer) == 40
     assert ctypes.sizeof(kclib.Tolerance) == 24
     assert ctypes.sizeof(kclib.DiffReport) == 14 * 8 + 8
-    assert ctypes.sizeof(kclib.Dispatch) == 80
+    assert ctypes.sizeof(kclib.Dispatch) == 96
     assert ctypes.sizeof(kclib.Options) == 24
     assert ctypes.sizeof(kclib.CaptureReport) == 9 * 8 + 5 * 8
     assert ctypes.sizeof(kclib.ReplayOpts) == 80
