@@ -135,7 +135,9 @@ typedef struct {
     uint32_t cluster[3];        /* thread-block cluster dims of a cluster launch (cuLaunchKernelEx
                                    CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION); 0,0,0 or 1,1,1 = none.
                                    Recorded in dispatch.json and reapplied by kc_replay */
+    uint32_t flags;             /* KC_LAUNCH_COOPERATIVE: a cooperative launch (grid-wide sync) */
 } kc_dispatch;
+enum { KC_LAUNCH_COOPERATIVE = 1 };
 
 /* kc_alloc backing (reading R6/R20): VMM allocations live in free VA space and
  * can be re-reserved at the same VA by a fresh process; plain cuMemAlloc

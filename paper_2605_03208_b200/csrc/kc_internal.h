@@ -148,6 +148,7 @@ struct kc_restored {
     std::string mangled;
     uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0;
     uint32_t cluster[3] = {1, 1, 1};
+    uint32_t flags = 0;  // KC_LAUNCH_COOPERATIVE
     std::vector<uint8_t> kernarg;
     std::vector<kc_restored_region> regions;  // sorted by base
     // VMM spans
@@ -221,7 +222,7 @@ kc_status hash_impl(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d
 // launch (cuLaunchKernelEx + CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION) when any
 // cluster dim exceeds 1
 CUresult launch_packed(CUfunction f, const uint32_t grid[3], const uint32_t block[3], uint32_t smem, CUstream s,
-                       const void* kernarg, size_t kernarg_size, const uint32_t cluster[3]);
+                       const void* kernarg, size_t kernarg_size, const uint32_t cluster[3], uint32_t flags = 0);
 // normalised cluster dims of a kc_dispatch (0 -> 1)
 void dispatch_cluster(const kc_dispatch* d, uint32_t out[3]);
 // kc_validate with an option to merge every region's W into one report (F4 sequences)

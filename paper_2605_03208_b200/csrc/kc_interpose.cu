@@ -99,7 +99,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
     const CUpti_CallbackData* d = (const CUpti_CallbackData*)cbdata;
     if (d->callbackSite == CUPTI_API_ENTER) {
         CUfunction f = nullptr;
-        uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0, cluster[3] = {1, 1, 1};
+        uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0, cluster[3] = {1, 1, 1}, flags = 0;
         CUstream stream = nullptr;
         void** kp = nullptr;
         void** extra = nullptr;
@@ -112,6 +112,16 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
             stream = p->hStream;
             kp = p->kernelParams;
             extra = p->extra;
+        } else if (cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchCooperativeKernel ||
+                   cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchCooperativeKernel_ptsz) {
+            auto p = (const cuLaunchCooperativeKernel_params*)d->functionParams;  // same layout as _ptsz
+            f = p->f;
+            grid[0] = p->gridDimX, grid[1] = p->gridDimY, grid[2] = p->gridDimZ;
+            block[0] = p->blockDimX, block[1] = p->blockDimY, block[2] = p->blockDimZ;
+            smem = p->sharedMemBytes;
+            stream = p->hStream;
+            kp = p->kernelParams;
+            flags |= KC_LAUNCH_COOPERATIVE;
         } else {
             auto p = (const cuLaunchKernelEx_params*)d->functionParams;
             if (!p->config) return;
@@ -127,6 +137,9 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
                     cluster[0] = p->config->attrs[a].value.clusterDim.x;
                     cluster[1] = p->config->attrs[a].value.clusterDim.y;
                     cluster[2] = p->config->attrs[a].value.clusterDim.z;
+                } else if (p->config->attrs[a].id == CU_LAUNCH_ATTRIBUTE_COOPERATIVE &&
+                           p->config->attrs[a].value.cooperative) {
+                    flags |= KC_LAUNCH_COOPERATIVE;
                 }
         }
         const char* name = nullptr;
@@ -158,7 +171,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
         }
         ip->worker = std::thread([ctx, ip, f, grid0 = grid[0], grid1 = grid[1], grid2 = grid[2], block0 = block[0],
                                   block1 = block[1], block2 = block[2], smem, stream, mangled, kernarg,
-                                  cl0 = cluster[0], cl1 = cluster[1], cl2 = cluster[2]]() {
+                                  cl0 = cluster[0], cl1 = cluster[1], cl2 = cluster[2], flags]() {
             Internal guard;  // the capture's own driver calls are not the application's
             kc_dispatch disp;
             memset(&disp, 0, sizeof disp);
@@ -171,6 +184,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
             disp.kernarg = kernarg->empty() ? nullptr : kernarg->data();
             disp.stream = (void*)stream;
             disp.cluster[0] = cl0, disp.cluster[1] = cl1, disp.cluster[2] = cl2;
+            disp.flags = flags;
             // the application's launch happens between the two halves of the capture
             std::function<CUresult()> forward = [ip, stream]() -> CUresult {
                 std::unique_lock<std::mutex> lk(ip->hm);

@@ -1040,7 +1040,8 @@ const CUpti_CallbackId kTrackedCbids[] = {
     CUPTI_DRIVER_TRACE_CBID_cuModuleLoadFatBinary, CUPTI_DRIVER_TRACE_CBID_cuModuleUnload,
     // A3 interposed mode: the launch bracket (kc_interpose.cu)
     CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel, CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel_ptsz,
-    CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx, CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx_ptsz};
+    CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx, CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx_ptsz,
+    CUPTI_DRIVER_TRACE_CBID_cuLaunchCooperativeKernel, CUPTI_DRIVER_TRACE_CBID_cuLaunchCooperativeKernel_ptsz};
 
 void record_code_object(kc_ctx* ctx, const CUmodule* mod, const void* image) {
     if (!mod || !*mod || !image) return;
@@ -1056,7 +1057,9 @@ void CUPTIAPI cupti_cb(void* user, CUpti_CallbackDomain domain, CUpti_CallbackId
     const CUpti_CallbackData* d = (const CUpti_CallbackData*)cbdata;
     if (domain == CUPTI_CB_DOMAIN_DRIVER_API &&
         (cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel || cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernel_ptsz ||
-         cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx || cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx_ptsz)) {
+         cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx || cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchKernelEx_ptsz ||
+         cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchCooperativeKernel ||
+         cbid == CUPTI_DRIVER_TRACE_CBID_cuLaunchCooperativeKernel_ptsz)) {
         ::kc::interpose_launch(ctx, cbid, cbdata);  // ENTER and EXIT
         return;
     }

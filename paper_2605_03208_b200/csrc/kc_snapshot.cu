@@ -392,7 +392,8 @@ struct LogRegion {
 
 std::string dispatch_json(int mode, const std::string& mangled, const uint32_t grid[3], const uint32_t block[3],
                           uint32_t smem, uint32_t kernarg_size, int device, const std::vector<uint8_t>& image,
-                          const std::vector<std::pair<size_t, size_t>>& layout, const uint32_t cluster[3]) {
+                          const std::vector<std::pair<size_t, size_t>>& layout, const uint32_t cluster[3],
+                          uint32_t flags) {
     const size_t image_size = image.size();
     int cc_major = 0, cc_minor = 0;
     cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device);
@@ -401,6 +402,7 @@ std::string dispatch_json(int mode, const std::string& mangled, const uint32_t g
     j += "  \"format\": \"kc-snapshot/1\",\n";
     j += std::string("  \"mode\": \"") + (mode == KC_MODE_PRE_W ? "pre_w" : "post") + "\",\n";
     j += "  \"mangled_symbol\": \"" + kcj::esc(mangled) + "\",\n";
+    j += std::string("  \"cooperative\": ") + ((flags & KC_LAUNCH_COOPERATIVE) ? "true" : "false") + ",\n";
     char b[512];
     snprintf(b, sizeof b,
              "  \"grid\": [%u, %u, %u],\n  \"block\": [%u, %u, %u],\n  \"cluster\": [%u, %u, %u],\n"
@@ -482,26 +484,35 @@ namespace {
 }  // namespace
 
 CUresult kc::launch_packed(CUfunction f, const uint32_t grid[3], const uint32_t block[3], uint32_t smem, CUstream s,
-                           const void* kernarg, size_t kernarg_size, const uint32_t cluster[3]) {
+                           const void* kernarg, size_t kernarg_size, const uint32_t cluster[3], uint32_t flags) {
     size_t ksz = kernarg_size;
     void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, (void*)kernarg, CU_LAUNCH_PARAM_BUFFER_SIZE, &ksz,
                      CU_LAUNCH_PARAM_END};
     void** ex = kernarg && kernarg_size ? extra : nullptr;
+    CUlaunchAttribute attrs[2];
+    memset(attrs, 0, sizeof attrs);
+    unsigned na = 0;
     if (cluster && cluster[0] * cluster[1] * cluster[2] > 1) {
-        CUlaunchAttribute attr;
-        memset(&attr, 0, sizeof attr);
-        attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-        attr.value.clusterDim.x = cluster[0];
-        attr.value.clusterDim.y = cluster[1];
-        attr.value.clusterDim.z = cluster[2];
+        attrs[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+        attrs[na].value.clusterDim.x = cluster[0];
+        attrs[na].value.clusterDim.y = cluster[1];
+        attrs[na].value.clusterDim.z = cluster[2];
+        ++na;
+    }
+    if (flags & KC_LAUNCH_COOPERATIVE) {
+        attrs[na].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+        attrs[na].value.cooperative = 1;
+        ++na;
+    }
+    if (na) {
         CUlaunchConfig cfg;
         memset(&cfg, 0, sizeof cfg);
         cfg.gridDimX = grid[0], cfg.gridDimY = grid[1], cfg.gridDimZ = grid[2];
         cfg.blockDimX = block[0], cfg.blockDimY = block[1], cfg.blockDimZ = block[2];
         cfg.sharedMemBytes = smem;
         cfg.hStream = s;
-        cfg.attrs = &attr;
-        cfg.numAttrs = 1;
+        cfg.attrs = attrs;
+        cfg.numAttrs = na;
         return KC_DRV(cuLaunchKernelEx)(&cfg, f, nullptr, ex);
     }
     return KC_DRV(cuLaunchKernel)(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, s, nullptr, ex);
@@ -687,7 +698,7 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
         uint32_t cl[3];
         dispatch_cluster(d, cl);
         const std::string j = dispatch_json(mode, mangled, d->grid, d->block, d->smem_bytes, d->kernarg_size,
-                                            ctx->device, mc.image, layout, cl);
+                                            ctx->device, mc.image, layout, cl, d->flags);
         if (!write_text(dir + "/dispatch.json", j)) return false;
         if (!write_file(dir + "/kernarg.bin", d->kernarg, d->kernarg ? d->kernarg_size : 0)) return false;
         if (!mc.image.empty() && !write_file(dir + "/kernel.cubin", mc.image.data(), mc.image.size())) return false;
@@ -771,7 +782,8 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
     {
         uint32_t cl[3];
         dispatch_cluster(d, cl);
-        CUresult r = launch_packed(f, d->grid, d->block, d->smem_bytes, (CUstream)cs, d->kernarg, d->kernarg_size, cl);
+        CUresult r = launch_packed(f, d->grid, d->block, d->smem_bytes, (CUstream)cs, d->kernarg, d->kernarg_size, cl,
+                                   d->flags);
         if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)cs);
         if (r != CUDA_SUCCESS) {
             if (own_mod) KC_DRV(cuModuleUnload)(own_mod);
@@ -1072,6 +1084,8 @@ kc_status load_desc_files(kc_ctx* ctx, const std::string& dir, SnapDesc& d, kc_r
     if (const kcj::Value* g = dv.get("block"))
         for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) d.block[i] = (uint32_t)g->a[i].as_u64(1);
     if (const kcj::Value* g = dv.get("shared_mem_bytes")) d.smem = (uint32_t)g->as_u64();
+    if (const kcj::Value* g = dv.get("cooperative"))
+        if (g->s == "true" || g->b) d.flags |= KC_LAUNCH_COOPERATIVE;
     if (const kcj::Value* g = dv.get("cluster"))
         for (int i = 0; i < 3 && i < (int)g->a.size(); ++i) d.cluster[i] = std::max<uint32_t>(1, (uint32_t)g->a[i].as_u64(1));
     if (const kcj::Value* g = dv.get("kernarg_layout"))  // (offset, size) per parameter (R22)
@@ -1198,6 +1212,7 @@ static void bind_dispatch_fields(kc_restored* h, const SnapDesc& d) {
     }
     h->smem = d.smem;
     for (int i = 0; i < 3; ++i) h->cluster[i] = d.cluster[i];
+    h->flags = d.flags;
     h->kernarg = d.kernarg;
     h->image = d.image;
     h->modvars = d.modvars;
@@ -2010,6 +2025,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     }
     D.smem = d->smem_bytes;
     dispatch_cluster(d, D.cluster);
+    D.flags = d->flags;
     if (d->kernarg && d->kernarg_size)
         D.kernarg.assign((const uint8_t*)d->kernarg, (const uint8_t*)d->kernarg + d->kernarg_size);
     ModCapture mc;  // F3
@@ -2204,7 +2220,8 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
     } else {
         uint32_t cl[3];
         dispatch_cluster(d, cl);
-        CUresult r = launch_packed(f, d->grid, d->block, d->smem_bytes, (CUstream)cs, d->kernarg, d->kernarg_size, cl);
+        CUresult r = launch_packed(f, d->grid, d->block, d->smem_bytes, (CUstream)cs, d->kernarg, d->kernarg_size, cl,
+                                   d->flags);
         if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)cs);
         if (r != CUDA_SUCCESS) return fail(cu_err(ctx, r, "kc_capture_dev: target dispatch"));
     }
@@ -2388,7 +2405,7 @@ static kc_status save_impl(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c,
     // metadata first
     if (!write_text(dir + "/dispatch.json", dispatch_json(D.mode, D.mangled, D.grid, D.block, D.smem,
                                                           (uint32_t)D.kernarg.size(), ctx->device, D.image,
-                                                          D.layout, D.cluster)) ||
+                                                          D.layout, D.cluster, D.flags)) ||
         !write_file(dir + "/kernarg.bin", D.kernarg.data(), D.kernarg.size()) ||
         (!D.image.empty() && !write_file(dir + "/kernel.cubin", D.image.data(), D.image.size())) ||
         !write_module_vars(dir, D.modvars))
@@ -2758,7 +2775,7 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
         }
         cudaEventRecord(e0, s);
         CUresult r = launch_packed(f, grid, block, smem, (CUstream)s, h->kernarg.empty() ? nullptr : h->kernarg.data(),
-                                   h->kernarg.size(), h->cluster);
+                                   h->kernarg.size(), h->cluster, h->flags);
         cudaEventRecord(e1, s);
         if (r == CUDA_SUCCESS) r = KC_DRV(cuStreamSynchronize)((CUstream)s);
         if (r != CUDA_SUCCESS) {

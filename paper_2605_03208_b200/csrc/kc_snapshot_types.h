@@ -29,6 +29,7 @@ struct SnapDesc {
     std::string mangled;
     uint32_t grid[3] = {1, 1, 1}, block[3] = {1, 1, 1}, smem = 0;
     uint32_t cluster[3] = {1, 1, 1};                 // thread-block cluster dims (1,1,1 = no cluster launch)
+    uint32_t flags = 0;                              // KC_LAUNCH_COOPERATIVE
     std::vector<uint8_t> kernarg, image;
     std::vector<std::pair<size_t, size_t>> layout;  // kernarg (offset, size)
     std::vector<SnapRegion> regions;                 // ascending base

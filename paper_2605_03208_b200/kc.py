@@ -95,7 +95,7 @@ class Dispatch(ctypes.Structure):
     _fields_ = [("func", ctypes.c_void_p), ("image", ctypes.c_void_p), ("image_size", ctypes.c_size_t),
                 ("mangled", ctypes.c_char_p), ("grid", ctypes.c_uint32 * 3), ("block", ctypes.c_uint32 * 3),
                 ("smem_bytes", ctypes.c_uint32), ("kernarg_size", ctypes.c_uint32), ("kernarg", ctypes.c_void_p),
-                ("stream", ctypes.c_void_p), ("cluster", ctypes.c_uint32 * 3)]
+                ("stream", ctypes.c_void_p), ("cluster", ctypes.c_uint32 * 3), ("flags", ctypes.c_uint32)]
 
 
 class Options(ctypes.Structure):
@@ -579,24 +579,25 @@ class Context:
         self._check(rc, "kc_capture", ok=(KC_OK, KC_PARTIAL))
         return rc, rep.as_dict()
 
-    def _dispatch(self, image, mangled, grid, block, smem, kernarg, stream, func=0, cluster=None):
+    def _dispatch(self, image, mangled, grid, block, smem, kernarg, stream, func=0, cluster=None,
+                  cooperative=False):
         img = ctypes.create_string_buffer(image, len(image)) if image else None
         ka = ctypes.create_string_buffer(kernarg, len(kernarg)) if kernarg else None
         d = Dispatch(func or None, ctypes.cast(img, ctypes.c_void_p) if img else None, len(image) if image else 0,
                      mangled.encode() if mangled else None, (ctypes.c_uint32 * 3)(*grid),
                      (ctypes.c_uint32 * 3)(*block), smem, len(kernarg), ctypes.cast(ka, ctypes.c_void_p) if ka else None,
                      stream or None, (ctypes.c_uint32 * 3)(*(tuple(cluster) + (1,) * (3 - len(cluster))))
-                     if cluster else (ctypes.c_uint32 * 3)(0, 0, 0))
+                     if cluster else (ctypes.c_uint32 * 3)(0, 0, 0), 1 if cooperative else 0)
         return d, (img, ka)
 
     def capture_dev(self, *, image: bytes | None = None, mangled: str | None = None, grid=(1, 1, 1),
                     block=(1, 1, 1), smem: int = 0, kernarg: bytes = b"", regions=None, mode: int = KC_MODE_PRE_W,
                     stream: int = 0, host: bool = False, base: "DevSnapshot | None" = None, func: int = 0,
-                    cluster=None) -> tuple[DevSnapshot, dict]:
+                    cluster=None, cooperative: bool = False) -> tuple[DevSnapshot, dict]:
         """kc_capture into a device arena (F1), or a pinned host arena (host=True:
         kc_capture_host); with base=, only chunks changed against it are copied
         (kc_capture_incr); cluster = thread-block cluster dims of a cluster launch."""
-        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func, cluster)
+        d, keep = self._dispatch(image, mangled, grid, block, smem, kernarg, stream, func, cluster, cooperative)
         rep = CaptureReport()
         h = ctypes.c_void_p()
         arr = _regions(regions) if regions is not None else None

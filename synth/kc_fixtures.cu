@@ -167,3 +167,14 @@ extern "C" __global__ void kc_fixture_cluster(unsigned int* out) {
     if (threadIdx.x == 0) out[blockIdx.x] = (rank << 24) | (nb << 16) | (*peer & 0xFFFFu);
     cl.sync();
 }
+
+// A cooperative launch (grid-wide synchronisation): every block publishes a
+// value, the whole grid synchronises, then each block reads its neighbour's.
+// Launched without the cooperative attribute, grid.sync() is not allowed.
+extern "C" __global__ void kc_fixture_coop(unsigned int* stage, unsigned int* out) {
+    namespace cg = cooperative_groups;
+    cg::grid_group g = cg::this_grid();
+    if (threadIdx.x == 0) stage[blockIdx.x] = blockIdx.x * 13u + 5u;
+    g.sync();
+    if (threadIdx.x == 0) out[blockIdx.x] = stage[(blockIdx.x + 1) % gridDim.x] ^ 0xA5A5u;
+}

@@ -132,3 +132,31 @@ def test_cluster_launch_capture_replay(env, tmp_path):
     assert np.array_equal(synth.dev_view(vout, 4 * n).cpu().numpy().view(np.uint32), expect)
     r.release()
     snap.free()
+
+
+def test_cooperative_launch_capture_replay(env):
+    """A cooperative launch (grid-wide sync) is dispatch state too: recorded
+    (kc_dispatch.flags, dispatch.json "cooperative") and replayed with
+    CU_LAUNCH_ATTRIBUTE_COOPERATIVE; the neighbour values read after grid.sync()
+    match the definition and validate bit-exactly."""
+    ctx, kc, synth = env
+    n = 96
+    vstage, vout = ctx.alloc(4 * n), ctx.alloc(4 * n)
+    synth.dev_view(vstage, 4 * n).zero_()
+    synth.dev_view(vout, 4 * n).zero_()
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    snap, _ = ctx.capture_dev(image=image, mangled="kc_fixture_coop", grid=(n, 1, 1), block=(64, 1, 1),
+                              kernarg=struct.pack("<QQ", vstage, vout),
+                              regions=sorted([(vstage, 4 * n), (vout, 4 * n)]), cooperative=True)
+    b = np.arange(n, dtype=np.uint32)
+    expect = (((b + 1) % n) * 13 + 5) ^ 0xA5A5
+    assert np.array_equal(synth.dev_view(vout, 4 * n).cpu().numpy().view(np.uint32), expect)
+    ctx.free(vstage)
+    ctx.free(vout)
+    r, _ = ctx.restore_dev(snap)
+    ctx.replay(r)
+    reps, unexpected = ctx.validate(r)
+    assert reps and all(x["differing_bytes"] == 0 for x in reps) and unexpected == 0
+    assert np.array_equal(synth.dev_view(vout, 4 * n).cpu().numpy().view(np.uint32), expect)
+    r.release()
+    snap.free()
