@@ -4,8 +4,8 @@ The attn_fwd fixture (fp16, B=2, H=16, S=4096, D=128; synth/kc_attn_fwd.cu) is
 captured under BLOCK_N = 64 into a device snapshot, restored at the same VAs and
 replayed with each config's code object (kc_replay image_override).  For each
 pair the K2 report (kc_validate / kc_diff) gives % elements changed, max abs,
-max ULP; every config is also compared with the fp64 definition (oracle, test
-infrastructure) on sampled rows, and timed (kc_replay kernel events).
+max ULP; every config is also compared with an fp64 PyTorch attention on sampled
+rows, and timed (kc_replay kernel events).
 
     python tools/drift_study.py [--out profiles/r1_f4_drift.txt]
 """
@@ -29,7 +29,12 @@ def main():
     p.add_argument("--iters", type=int, default=10)
     p.add_argument("--seeds", type=int, default=3)
     a = p.parse_args()
-    from oracle.attention import attention_rows   # fp64 definition (test infrastructure)
+    def attention_rows(q, k, v, rows, sm_scale):
+        """fp64 softmax(sm_scale q k^T) v on sampled rows, plain PyTorch (the oracle's
+        copy lives in oracle/ and is for tests only)."""
+        q64 = torch.from_numpy(q[rows]).double()
+        k64, v64 = torch.from_numpy(k).double(), torch.from_numpy(v).double()
+        return (torch.softmax(q64 @ k64.T * sm_scale, dim=1) @ v64).numpy()
     torch.cuda.set_device(0)
     ctx = kc.Context(0)
     n = synth.F4_BYTES
