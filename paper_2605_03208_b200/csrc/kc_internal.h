@@ -16,7 +16,7 @@
 // Driver-API entry points resolved through cudart (cudaGetDriverEntryPoint),
 // so libkc.so has no link-time dependency on libcuda and loads on hosts
 // without a GPU driver (calls then fail with KC_ERR_CUDA).
-#define KC_DRV_FUNCS(X) X(cuCtxGetDevice) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuLaunchKernelEx) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemExportToShareableHandle) X(cuMemFree) X(cuMemImportFromShareableHandle) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamSynchronize)
+#define KC_DRV_FUNCS(X) X(cuCtxGetDevice) X(cuFuncGetModule) X(cuFuncGetName) X(cuFuncGetParamInfo) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuLaunchKernel) X(cuLaunchKernelEx) X(cuMemAddressFree) X(cuMemAddressReserve) X(cuMemAlloc) X(cuMemCreate) X(cuMemExportToShareableHandle) X(cuMemFree) X(cuMemImportFromShareableHandle) X(cuMemGetAllocationGranularity) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap) X(cuModuleGetFunction) X(cuModuleGetGlobal) X(cuModuleLoadData) X(cuModuleUnload) X(cuPointerGetAttribute) X(cuStreamIsCapturing) X(cuStreamSynchronize)
 namespace kc {
 struct Drv {
 #define KC_DRV_DECL(f) decltype(&::f) f = nullptr;

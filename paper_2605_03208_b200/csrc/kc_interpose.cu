@@ -142,6 +142,10 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
                     flags |= KC_LAUNCH_COOPERATIVE;
                 }
         }
+        // a launch recorded into a CUDA graph (stream capture) does not run now: it is
+        // neither counted nor captured (and syncing would invalidate the graph capture)
+        CUstreamCaptureStatus cap = CU_STREAM_CAPTURE_STATUS_NONE;
+        if (KC_DRV(cuStreamIsCapturing)(stream, &cap) == CUDA_SUCCESS && cap != CU_STREAM_CAPTURE_STATUS_NONE) return;
         const char* name = nullptr;
         if (KC_DRV(cuFuncGetName)(&name, f) != CUDA_SUCCESS || !name) return;
         if (ctx->device < 0) {  // injected ctx: the application's current device (the worker has no context)

@@ -486,6 +486,44 @@ def load_seq(a):
     print(json.dumps(out))
 
 
+def interpose_graph(a):
+    """A launch recorded by stream capture (CUDA graph) is not a dispatch that runs:
+    the hook skips it; the graph replays, then the direct launch is captured."""
+    import ctypes
+    from cuda.bindings import driver as drv
+    ctx = kc.Context(0)
+    ctx.track_install()
+    ctx.interpose_arm("kc_fixture_walk", 0, a.dir, kc.KC_MODE_PRE_W)
+    err, mod = drv.cuModuleLoadData(open(synth.FIXTURE_CUBIN, "rb").read())
+    err, fn = drv.cuModuleGetFunction(mod, b"kc_fixture_walk")
+    sizes = [s.size for s in synth.C1_SPECS]
+    ptrs = [int(drv.cuMemAlloc(sz)[1]) for sz in sizes]
+    nodes, heads, out = ptrs
+    init = synth.c1_fill(nodes)
+    for p_, arr in zip(ptrs, init):
+        drv.cuMemcpyHtoD(p_, arr.ctypes.data, arr.nbytes)
+    err, stream = drv.cuStreamCreate(0)
+    types = (ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int)
+    drv.cuStreamBeginCapture(stream, drv.CUstreamCaptureMode.CU_STREAM_CAPTURE_MODE_RELAXED)
+    drv.cuLaunchKernel(fn, 32, 1, 1, 256, 1, 1, 0, stream, ((heads, out, nodes, synth.C1_N_LISTS, 0), types), 0)
+    err, graph = drv.cuStreamEndCapture(stream)
+    assert err == drv.CUresult.CUDA_SUCCESS, err
+    err, gexec = drv.cuGraphInstantiate(graph, 0)
+    assert err == drv.CUresult.CUDA_SUCCESS, err
+    seen_after_capture = ctx.interpose_status()["seen"]
+    drv.cuGraphLaunch(gexec, stream)
+    drv.cuStreamSynchronize(stream)
+    drv.cuLaunchKernel(fn, 32, 1, 1, 256, 1, 1, 0, stream, ((heads, out, nodes, synth.C1_N_LISTS, 1), types), 0)
+    drv.cuStreamSynchronize(stream)
+    st = ctx.interpose_status()
+    h = np.zeros(sizes[0], dtype=np.uint8)
+    drv.cuMemcpyDtoH(h.ctypes.data, nodes, sizes[0])
+    dt = np.dtype([("next", "<u8"), ("value", "<u4"), ("pad", "<u4")])
+    v0 = init[0].view(dt)["value"].astype(np.uint64)
+    once = bool(np.array_equal(h.view(dt)["value"], ((3 * v0 + 1) % 2**32).astype(np.uint32)))
+    print(json.dumps({"status": st, "seen_after_capture": seen_after_capture, "mutated_once": once}))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -510,7 +548,7 @@ def main():
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
      "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar,
      "publish": publish, "interpose": interpose, "interpose-seq": interpose_seq, "load-replay": load_replay,
-     "load-seq": load_seq}[a.cmd](a)
+     "load-seq": load_seq, "interpose-graph": interpose_graph}[a.cmd](a)
 
 
 if __name__ == "__main__":

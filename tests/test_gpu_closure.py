@@ -569,3 +569,20 @@ def test_cli_sequence_capture_and_joint_replay(tmp_path):
     assert p.returncode == 0, p.stdout + p.stderr[-3000:]
     res = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["pass"] and res["n"] == 3 and res["deps"] == expect
+
+
+def test_interposition_skips_launches_recorded_into_a_cuda_graph(tmp_path):
+    """Stream capture records launches without running them: the hook neither
+    counts nor captures them (a device sync would also invalidate the graph
+    capture).  The graph still replays for the application, and launch #0 of
+    the kernel is the first one that actually runs directly (mutate = 1)."""
+    import struct
+    from oracle import snapshot
+    d = str(tmp_path / "graph")
+    res = run("interpose-graph", d)
+    assert res["seen_after_capture"] == 0 and res["status"]["state"] == 3, res
+    assert res["mutated_once"]
+    snap = snapshot.load(d)
+    snapshot.verify(snap)
+    ka = open(os.path.join(d, "kernarg.bin"), "rb").read()
+    assert struct.unpack("<QQQIi", ka)[4] == 1      # the captured dispatch is the direct, mutating launch
