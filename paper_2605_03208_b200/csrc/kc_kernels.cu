@@ -809,6 +809,11 @@ struct Acc {
     unsigned long long max_ulp;
     double max_abs, max_rel;
     uint32_t any;  // this lane saw a differing byte in the current unit
+    // 16-bit float fast path (elem16): an fp32 running max of exact |a - r|
+    // (merged into max_abs at flush), RD32 of a value <= max_rel, and directed
+    // fp32 roundings of atol / rtol (set once per launch, not by acc_zero)
+    float mabs32, mrel32;
+    float alo, ahi, rlo, rhi;
 };
 constexpr uint64_t kFlushUnits = 65536;
 
@@ -817,6 +822,7 @@ __device__ __forceinline__ void acc_zero(Acc& a) {
     a.max_abs = 0.0;
     a.max_rel = 0.0;
     a.any = 0;
+    a.mabs32 = a.mrel32 = 0.f;
 }
 
 // number of nonzero bytes of x
@@ -916,6 +922,75 @@ __device__ __forceinline__ void elem_float(typename std::conditional<DT_<DT>::S 
             // implies d/|r| <= M, and RN is monotonic
             const double rel = __ddiv_rn(d, ar);
             if (rel > acc.max_rel) acc.max_rel = rel;
+        }
+    }
+}
+
+// ---- 16-bit floats, fp32 fast path (DESIGN.md §7 K2, "16-bit fp32 path").  For finite f16/bf16 values
+// whose exponent fields differ by at most KMAX, a - r is an integer below 2^24
+// times a power of two inside fp32's range, so __fsub_rn returns it exactly and
+// |a - r| equals the fp64 difference the oracle takes.  The two decisions
+// that need fp64 are bracketed in fp32 with directed rounding:
+//   isclose: L = RD(alo + RD(rlo*|r|)) <= RN64(atol + RN64(rtol*|r|)) <= U = RU(ahi + RU(rhi*|r|)),
+//            so d <= L (or d <= alo) means close, d > U (and d > ahi) means not
+//            close; in between the fp64 formula decides;
+//   max_rel: d <= RD(mrel32*|r|) <= max_rel*|r| means RN64(d/|r|) <= max_rel, so
+//            the fp64 division runs only when it can raise the running max.
+// Everything else (Inf/NaN, exponents far apart, bf16 near overflow, equal bits
+// with a special reference) takes elem_float unchanged.
+#ifndef KC_K2_FAST16
+#define KC_K2_FAST16 1
+#endif
+template <int DT>
+__device__ __forceinline__ float f16bits_to_f32(uint32_t b) {
+    if (DT == KC_DT_F16) return __half2float(__ushort_as_half((unsigned short)b));
+    return __uint_as_float(b << 16);
+}
+
+template <int DT>
+__device__ __forceinline__ void elem16(uint32_t r, uint32_t a, Acc& acc, double atol, double rtol, int equal_nan) {
+    if constexpr (!KC_K2_FAST16) {
+        elem_float<DT>(r, a, acc, atol, rtol, equal_nan);
+        return;
+    } else {
+        constexpr int EB = DT == KC_DT_F16 ? 10 : 7;               // exponent field position
+        constexpr uint32_t EM = DT == KC_DT_F16 ? 0x1Fu : 0xFFu;    // field mask
+        constexpr uint32_t EFAST = DT == KC_DT_F16 ? 0x1Eu : 0xFDu; // largest field on the fast path
+        constexpr uint32_t KMAX = DT == KC_DT_F16 ? 13u : 16u;      // (2^11-1)(2^13+1), (2^8-1)(2^16+1) < 2^24
+        const uint32_t er = (r >> EB) & EM, ea = (a >> EB) & EM;
+        const uint32_t de = er > ea ? er - ea : ea - er;  // raw fields: subnormals count one too far (conservative)
+        if (er > EFAST || ea > EFAST || de > KMAX || r == a) {
+            elem_float<DT>(r, a, acc, atol, rtol, equal_nan);
+            return;
+        }
+        acc.delems += 1;
+        const int oa = (a & 0x8000u) ? -(int)(a & 0x7FFFu) : (int)a;
+        const int orr = (r & 0x8000u) ? -(int)(r & 0x7FFFu) : (int)r;
+        const unsigned long long ulp = (unsigned long long)(oa >= orr ? oa - orr : orr - oa);
+        if (ulp > acc.max_ulp) acc.max_ulp = ulp;
+        const float av = f16bits_to_f32<DT>(a), rv = f16bits_to_f32<DT>(r);
+        const float d = fabsf(__fsub_rn(av, rv));  // exact
+        acc.mabs32 = fmaxf(acc.mabs32, d);
+        if (d == 0.f) return;  // +0 vs -0: close, no relative error
+        const float ar = fabsf(rv);
+        bool close;
+        if (d <= acc.alo || d <= __fadd_rd(acc.alo, __fmul_rd(acc.rlo, ar))) {
+            close = true;
+        } else if (d > acc.ahi && d > __fadd_ru(acc.ahi, __fmul_ru(acc.rhi, ar))) {
+            close = false;
+        } else {
+            const double dd = (double)d;
+            close = (dd <= atol) || (dd <= __dadd_rn(atol, __dmul_rn(rtol, (double)ar)));
+        }
+        acc.fail += !close;
+        if (rv == 0.f) {
+            acc.rel_undef += 1;
+        } else if (d > __fmul_rd(acc.mrel32, ar)) {
+            const double rel = __ddiv_rn((double)d, (double)ar);
+            if (rel > acc.max_rel) {
+                acc.max_rel = rel;
+                acc.mrel32 = __double2float_rd(rel);
+            }
         }
     }
 }
@@ -1073,13 +1148,15 @@ __device__ __forceinline__ void q_push(const uint32_t (&r)[8], const uint32_t (&
 }
 
 // ---- 16-bit floats (the c3 case): the element flags stay as bits 15 / 31 of
-// eight words per vector instead of a packed mask.  One byte-nonzero word m8
-// per word feeds the differing-byte count (IDP.4A: 128 per nonzero byte) and
-// the halfword flags ((m8 | m8 << 8) & 0x80008000); flagged halves are counted
-// with IDP.4A as well and pushed by testing the word bits directly.
+// eight words per vector instead of a packed mask.  A half is flagged when its
+// bits differ or the reference half has an all-ones exponent: both tests are
+// "add a constant below the sign bit, look at bit 15 / 31", merged into one
+// LOP3 per word.  The flagged halves are counted with IDP.4A and pushed by
+// testing the word bits directly.  Differing bytes are not counted here: every
+// element with a differing byte is flagged, so q_item counts its bytes.
 template <int DT>
 __device__ __forceinline__ uint32_t vec_scan16(const uint32_t (&r)[8], const uint32_t (&a)[8], uint32_t (&m)[8],
-                                               uint32_t& db128, uint32_t& cnt128, Acc& acc) {
+                                               uint32_t& cnt128, Acc& acc) {
     uint32_t x[8], anyx = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -1095,11 +1172,13 @@ __device__ __forceinline__ uint32_t vec_scan16(const uint32_t (&r)[8], const uin
         }
     } else {
         acc.any = 1;
+        constexpr uint32_t EX = DT == KC_DT_F16 ? 0x7C007C00u : 0x7F807F80u;
+        constexpr uint32_t EI = DT == KC_DT_F16 ? 0x04000400u : 0x00800080u;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const uint32_t m8 = (((x[i] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x[i]) & 0x80808080u;
-            db128 = __dp4a(m8, 0x01010101u, db128);
-            m[i] = ((m8 | (m8 << 8)) & 0x80008000u) | special_word<DT>(r[i]);
+            const uint32_t nz = ((x[i] & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x[i];  // bit 15/31: half differs
+            const uint32_t sp = (r[i] & EX) + EI;                               // bit 15/31: Inf/NaN ref
+            m[i] = (nz | sp) & 0x80008000u;
             any |= m[i];
         }
     }
@@ -1122,9 +1201,13 @@ __device__ __forceinline__ void q_push16(const uint32_t (&r)[8], const uint32_t 
 
 template <int DT>
 __device__ __forceinline__ void q_item(typename QT_<DT>::T t, Acc& acc, double atol, double rtol, int equal_nan) {
-    if constexpr (DT_<DT>::S == 2)
-        elem_float<DT>(t & 0xFFFFu, t >> 16, acc, atol, rtol, equal_nan);
-    else
+    if constexpr (DT_<DT>::S == 2) {
+        if constexpr (!kGenericScan16) {  // vec_scan16 leaves the differing bytes to the element
+            const uint32_t x = (t ^ (t >> 16)) & 0xFFFFu;
+            acc.dbytes += (uint32_t)((x & 0xFFu) != 0) + (uint32_t)(x > 0xFFu);
+        }
+        elem16<DT>(t & 0xFFFFu, t >> 16, acc, atol, rtol, equal_nan);
+    } else
         elem_float<DT>(t.x, t.y, acc, atol, rtol, equal_nan);
 }
 
@@ -1214,10 +1297,9 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
             }
             if constexpr (DT_<DT>::F && S == 2 && !kGenericScan16) {
                 uint32_t mw[U][8];
-                uint32_t any = 0, db128 = 0, cnt128 = 0;
+                uint32_t any = 0, cnt128 = 0;
 #pragma unroll
-                for (int u = 0; u < U; ++u) any |= vec_scan16<DT>(rw[u], aw[u], mw[u], db128, cnt128, acc);
-                acc.dbytes += db128 >> 7;
+                for (int u = 0; u < U; ++u) any |= vec_scan16<DT>(rw[u], aw[u], mw[u], cnt128, acc);
                 if (__any_sync(0xFFFFFFFFu, any != 0)) {
                     const uint32_t c = cnt128 >> 7;
                     uint32_t incl = c;
@@ -1313,6 +1395,7 @@ __device__ __forceinline__ unsigned long long warp_maxu(unsigned long long v) {
 
 __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
     const unsigned FULL = 0xFFFFFFFFu;
+    acc.max_abs = fmax(acc.max_abs, (double)acc.mabs32);  // both exact values
     const unsigned long long mabs = (unsigned long long)__double_as_longlong(acc.max_abs);
     const unsigned long long mrel = (unsigned long long)__double_as_longlong(acc.max_rel);
     // one ballot per field: only fields nonzero somewhere in the warp are reduced
@@ -1377,6 +1460,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
     Acc acc;
     acc_zero(acc);
+    acc.alo = __double2float_rd(atol);
+    acc.ahi = __double2float_ru(atol);
+    acc.rlo = __double2float_rd(rtol);
+    acc.rhi = __double2float_ru(rtol);
     extern __shared__ __align__(16) uint8_t k2_smem[];
     typename QT_<DT>::T* q =
         reinterpret_cast<typename QT_<DT>::T*>(k2_smem + (size_t)(threadIdx.x >> 5) * KQ<DT, VU>::kBytes);
@@ -1616,7 +1703,9 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
 // Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per
 // SM with 2 vectors of each operand in flight keeps the float paths free of
 // spills and reaches 6.9 TB/s on identical bf16 pairs; 512 x 2 CTAs (64
-// registers) spilled segment state into the inner loop (3.6 TB/s).
+// registers) spilled segment state into the inner loop (3.6 TB/s).  For the
+// planted 16-bit case 640 / 768 threads (1 or 2 vectors) were no faster
+// (profiles/r1_k2_bench_fast16_configs.txt).
 template <int DT>
 static void launch_k2(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps, unsigned long long* bm,
                       double atol, double rtol, int equal_nan, int num_sms, cudaStream_t s,

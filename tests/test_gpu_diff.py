@@ -110,6 +110,70 @@ def test_k2_misaligned_scalar_path(env, dtname):
     assert [int(w) for w in bms[0]] == [int(w) for w in exp.bitmap]
 
 
+def _spread16(dt, n, spread, rng, orc, flip=0.3, density=0.4):
+    """16-bit float pair: finite references over the whole exponent range, and
+    actuals whose exponent field moves by up to `spread` (the fp32 fast path
+    holds up to 13 / 16; beyond it elem_float decides), random signs and
+    mantissas, zeros and subnormals."""
+    eb, em = (10, 0x1F) if dt == orc.DT_F16 else (7, 0xFF)
+    mant = (1 << eb) - 1
+    er = rng.integers(0, em, size=n)                       # finite fields only
+    r = (rng.integers(0, 2, size=n) << 15) | (er << eb) | rng.integers(0, mant + 1, size=n)
+    ea = np.clip(er + rng.integers(-spread, spread + 1, size=n), 0, em - 1)
+    sa = (r >> 15) ^ (rng.random(n) < flip)
+    a = (sa << 15) | (ea << eb) | rng.integers(0, mant + 1, size=n)
+    a = np.where(rng.random(n) < density, a, r)
+    z = rng.random(n) < 0.02                               # +-0 references and actuals
+    r = np.where(z, rng.integers(0, 2, size=n) << 15, r)
+    return r.astype(np.uint16).view(np.uint8), a.astype(np.uint16).view(np.uint8)
+
+
+@pytest.mark.parametrize("dtname", ["f16", "bf16"])
+def test_k2_16bit_exponent_spread_and_tolerance_edges(env, dtname):
+    """16-bit float elements take an fp32 path (DESIGN.md §7 K2) when their exponents are
+    close.  Many 4 KiB buffers (one report each, so per-buffer maxima are seen),
+    exponent spreads from 0 to 20 fields around the 13 / 16 limits, bf16 fields
+    up to 254 (fp32 overflow of a - r), Inf/NaN in a few, and tolerances that sit
+    exactly on elements' |a - r| (atol = d, or rtol = d/|r| in fp64)."""
+    torch, kc, ctx, orc = env
+    dt = orc.DTYPE_NAMES.index(dtname)
+    rng = np.random.default_rng(35 + dt)
+    n = 2048
+    pairs = []
+    for j in range(84):
+        r, a = _spread16(dt, n, j % 21, rng, orc, flip=0.0 if j % 3 == 0 else 0.3)
+        if j % 7 == 6:   # a few specials on both sides
+            rv, av = r.view(np.uint16), a.view(np.uint16)
+            ex = 0x7C00 if dt == orc.DT_F16 else 0x7F80
+            av[5], rv[9], av[9], rv[13] = ex | 1, ex, ex, ex | 3
+        pairs.append((r, a))
+    # tolerances on an element's exact |a - r| (fp64, like the oracle)
+    f = np.float16 if dt == orc.DT_F16 else None
+
+    def vals(u8):
+        u = u8.view(np.uint16)
+        if f is not None:
+            return u.view(np.float16).astype(np.float64)
+        return (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    r0, a0 = vals(pairs[4][0]), vals(pairs[4][1])
+    k = int(np.nonzero((r0 != a0) & (r0 != 0) & np.isfinite(r0) & np.isfinite(a0))[0][7])
+    d = abs(a0[k] - r0[k])
+    tols = [(1e-8, 1e-5, False), (0.0, 0.0, False), (1e-3, 1e-3, True), (d, 0.0, False), (0.0, d / abs(r0[k]), False),
+            (1e-2, 0.0, False), (1e-30, 1e-30, False), (float(np.nextafter(d, 0)), 0.0, False)]
+    hold, bufs = [], []
+    for r, a in pairs:
+        tr, pr = _dev(torch, r)
+        ta, pa = _dev(torch, a)
+        hold += [tr, ta]
+        bufs.append((pr, pa, r.size, dtname))
+    for tol in tols:
+        reps, bms = ctx.diff(bufs, atol=tol[0], rtol=tol[1], equal_nan=tol[2])
+        for j, (r, a) in enumerate(pairs):
+            exp = orc.diff(r, a, dt, atol=tol[0], rtol=tol[1], equal_nan=tol[2])
+            _same(reps[j], exp.report, f"{dtname} buffer {j} tol {tol}")
+            assert [int(w) for w in bms[j]] == [int(w) for w in exp.bitmap]
+
+
 def test_k2_identical_and_empty(env):
     torch, kc, ctx, orc = env
     r, _ = _pair_host(orc.DT_F32, 100000, 1, orc, specials=False)
