@@ -1580,11 +1580,24 @@ cudaError_t kernels_init() {
     return e;
 }
 
+// Grid for the group-interleaved ring kernels (K1/K5/K6): warp w hashes groups
+// j0, j0 + W, ... (W = warps in the grid).  With groups = 3.5 x the warps that
+// fit, half the warps would run a 4th group alone, a latency-bound tail (2 GiB
+// went at 6.0 TB/s).  With few groups per warp the grid shrinks until every
+// warp gets the same count (6.3 TB/s); large snapshots keep the full grid.
+static uint64_t balanced_grid(uint64_t groups, uint64_t max_ctas, int warps_per_cta) {
+    const uint64_t max_warps = max_ctas * (uint64_t)warps_per_cta;
+    uint64_t warps = std::min(groups, max_warps);
+    const uint64_t per_warp = (groups + max_warps - 1) / max_warps;
+    if (per_warp > 1 && per_warp <= 16) warps = (groups + per_warp - 1) / per_warp;
+    return (warps + warps_per_cta - 1) / warps_per_cta;
+}
+
 cudaError_t launch_hash_cmp(const PairDev* d_pairs, int npair, uint64_t C, uint64_t* d_out, uint64_t* d_dirty,
                             const uint32_t* map, int num_sms, cudaStream_t s, bool self) {
     if (C == 0) return cudaSuccess;
     const uint64_t groups = (C + 7) / 8;
-    const uint64_t grid = std::min<uint64_t>((groups + CmpA::kWarps - 1) / CmpA::kWarps, (uint64_t)num_sms);
+    const uint64_t grid = balanced_grid(groups, (uint64_t)num_sms, CmpA::kWarps);
     if (self)
         k5_hash_cmp<CmpA, true><<<(unsigned)grid, CmpA::kWarps * 32, CmpA::kSmem, s>>>(
             d_pairs, npair, C, d_out, reinterpret_cast<unsigned long long*>(d_dirty), map);
@@ -1609,7 +1622,7 @@ static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d
     const uint64_t groups = (C + 7) / 8;
     // at most 8 warps' worth of CTAs per SM (one CTA of the 8-warp configs, four of CpS)
     const uint64_t per_sm = CFG::kWarps >= 8 ? 1 : 8 / CFG::kWarps;
-    const uint64_t grid = std::min<uint64_t>((groups + CFG::kWarps - 1) / CFG::kWarps, (uint64_t)num_sms * per_sm);
+    const uint64_t grid = balanced_grid(groups, (uint64_t)num_sms * per_sm, CFG::kWarps);
     if (d_dst)
         k1_hash_cpasync<CFG, true><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map,
                                                                                        d_dst, order);
