@@ -1432,9 +1432,11 @@ __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
 
 // One launch per dtype group: segments [seg0, seg0+nseg) own the global units
 // [unit0, unit0+U).
-// Unfiltered: each warp takes a contiguous block of units.  Filtered (K5 ran
-// first): units are interleaved over warps (u = unit0 + w + k*W) so the dirty
-// chunks, wherever they cluster, spread evenly; a unit whose chunk is clean is
+// Units are interleaved over warps (u = unit0 + w + k*W), so work that
+// clusters (one planted buffer among identical ones, the dirty chunks of a
+// filtered launch) spreads evenly over the warps; contiguous blocks per warp
+// (KC_K2_BLOCKED builds) left c3's Q/K/V warps idle while the O warps ran the
+// element path.  Filtered (K5 ran first): a unit whose chunk is clean is
 // skipped without reading it.
 template <int DT, int THREADS, int MINB, int VU>
 __global__ void __launch_bounds__(THREADS, MINB)
@@ -1445,9 +1447,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
     segs += seg0;
     const uint64_t W = (uint64_t)gridDim.x * (THREADS / 32);
     const uint64_t w = (uint64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
-    const uint64_t u0 = filter ? unit0 + w : unit0 + (U * w) / W;
-    const uint64_t u1 = filter ? unit0 + U : unit0 + (U * (w + 1)) / W;
-    const uint64_t ustep = filter ? W : 1;
+#ifndef KC_K2_BLOCKED
+#define KC_K2_BLOCKED 0
+#endif
+    const bool inter = filter || !KC_K2_BLOCKED;
+    const uint64_t u0 = inter ? unit0 + w : unit0 + (U * w) / W;
+    const uint64_t u1 = inter ? unit0 + U : unit0 + (U * (w + 1)) / W;
+    const uint64_t ustep = inter ? W : 1;
     if (u0 >= u1) return;
     int s = 0;
     {
