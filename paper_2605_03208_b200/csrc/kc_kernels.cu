@@ -1435,22 +1435,19 @@ __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
 // Units are interleaved over warps (u = unit0 + w + k*W), so work that
 // clusters (one planted buffer among identical ones, the dirty chunks of a
 // filtered launch) spreads evenly over the warps; contiguous blocks per warp
-// (KC_K2_BLOCKED builds) left c3's Q/K/V warps idle while the O warps ran the
+// (KC_K2_BLOCKED=1, a measurement knob) left c3's Q/K/V warps idle while the O warps ran the
 // element path.  Filtered (K5 ran first): a unit whose chunk is clean is
 // skipped without reading it.
 template <int DT, int THREADS, int MINB, int VU>
 __global__ void __launch_bounds__(THREADS, MINB)
     k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
             kc_diff_report* __restrict__ reps, unsigned long long* __restrict__ bitmaps, double atol, double rtol,
-            int equal_nan, const unsigned long long* __restrict__ filter) {
+            int equal_nan, const unsigned long long* __restrict__ filter, int blocked) {
     const int lane = threadIdx.x & 31;
     segs += seg0;
     const uint64_t W = (uint64_t)gridDim.x * (THREADS / 32);
     const uint64_t w = (uint64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
-#ifndef KC_K2_BLOCKED
-#define KC_K2_BLOCKED 0
-#endif
-    const bool inter = filter || !KC_K2_BLOCKED;
+    const bool inter = filter || !blocked;
     const uint64_t u0 = inter ? unit0 + w : unit0 + (U * w) / W;
     const uint64_t u1 = inter ? unit0 + U : unit0 + (U * (w + 1)) / W;
     const uint64_t ustep = inter ? W : 1;
@@ -1702,6 +1699,14 @@ cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64
 
 // K2 launch configurations (KC_K2_VARIANT, tuning knob): threads per CTA,
 // min CTAs per SM (register budget), vectors of each operand in flight per lane
+static int k2_blocked() {
+    static const int b = [] {
+        const char* e = getenv("KC_K2_BLOCKED");
+        return e && *e ? atoi(e) : 0;
+    }();
+    return b;
+}
+
 template <int DT, int THREADS, int MINB, int U>
 static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps,
                           unsigned long long* bm, double atol, double rtol, int equal_nan, int num_sms,
@@ -1716,7 +1721,8 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
     }();
     (void)attr;
     k2_diff<DT, THREADS, MINB, U><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
-                                                                         d_reps, bm, atol, rtol, equal_nan, filter);
+                                                                         d_reps, bm, atol, rtol, equal_nan, filter,
+                                                                         k2_blocked());
 }
 
 // Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per
