@@ -1432,12 +1432,16 @@ __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
 
 // One launch per dtype group: segments [seg0, seg0+nseg) own the global units
 // [unit0, unit0+U).
-// Units are interleaved over warps (u = unit0 + w + k*W), so work that
-// clusters (one planted buffer among identical ones, the dirty chunks of a
-// filtered launch) spreads evenly over the warps; contiguous blocks per warp
-// (KC_K2_BLOCKED=1, a measurement knob) left c3's Q/K/V warps idle while the O warps ran the
-// element path.  Filtered (K5 ran first): a unit whose chunk is clean is
-// skipped without reading it.
+// Unit order.  Segments of >= 4 MiB on average (and filtered launches): units
+// are interleaved over warps (u = unit0 + w + k*W), so work that clusters (one
+// planted buffer among identical ones, the dirty chunks of a filtered launch)
+// spreads evenly; one contiguous block per warp left c3's Q/K/V warps idle
+// while the O warps ran the element path (3.56 vs 5.27 TB/s), and the
+// interleaved order also streams large pairs faster.  Smaller segments: one
+// contiguous block per warp, walked segment by segment (interleaving made
+// every unit a segment change, 1 MiB x 10k pairs 7.0 -> 6.2 TB/s).
+// KC_K2_BLOCKED=0/1 forces either (measurement knob).  Filtered (K5 ran
+// first): a unit whose chunk is clean is skipped without reading it.
 template <int DT, int THREADS, int MINB, int VU>
 __global__ void __launch_bounds__(THREADS, MINB)
     k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
@@ -1447,11 +1451,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
     segs += seg0;
     const uint64_t W = (uint64_t)gridDim.x * (THREADS / 32);
     const uint64_t w = (uint64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
-    const bool inter = filter || !blocked;
-    const uint64_t u0 = inter ? unit0 + w : unit0 + (U * w) / W;
-    const uint64_t u1 = inter ? unit0 + U : unit0 + (U * (w + 1)) / W;
-    const uint64_t ustep = inter ? W : 1;
-    if (u0 >= u1) return;
+    // blocks of B units, block b to warp b mod W: single units (interleaved)
+    // when filtered or when segments are large; one contiguous block per warp
+    // when the host chose `blocked` (small segments: a warp walks them in order)
+    const uint64_t B = (filter || !blocked) ? 1 : (U + W - 1) / W;
+    const uint64_t nblk = (U + B - 1) / B;
+    if (w >= nblk) return;
+    const uint64_t u0 = unit0 + w * B;
     int s = 0;
     {
         int lo = 0, hi = nseg;
@@ -1472,11 +1478,23 @@ __global__ void __launch_bounds__(THREADS, MINB)
         reinterpret_cast<typename QT_<DT>::T*>(k2_smem + (size_t)(threadIdx.x >> 5) * KQ<DT, VU>::kBytes);
     uint32_t qn = 0;  // warp-uniform queue length
     uint64_t since_flush = 0;
-    for (uint64_t u = u0; u < u1; u += ustep) {
-        while (s + 1 < nseg && segs[s + 1].unit_off <= u) {
+    for (uint64_t b = w; b < nblk; b += W)
+    for (uint64_t u = unit0 + b * B, ue = min(unit0 + (b + 1) * B, unit0 + U); u < ue; ++u) {
+        if (s + 1 < nseg && segs[s + 1].unit_off <= u) {
+            // leaving segment s: flush what this warp accumulated for it, then
+            // jump (binary search) to u's segment -- with units W apart a warp
+            // can pass thousands of small segments it never touches
             q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
             acc_flush(acc, reps + segs[s].report, lane);
-            ++s;
+            ++s;  // contiguous blocks: the next segment
+            if (s + 1 < nseg && segs[s + 1].unit_off <= u) {
+                int lo = s + 1, hi = nseg;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (segs[mid].unit_off <= u) lo = mid + 1; else hi = mid;
+                }
+                s = lo - 1;
+            }
         }
         const SegDev sg = segs[s];
         const uint32_t s_rep = sg.report;
@@ -1699,12 +1717,14 @@ cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64
 
 // K2 launch configurations (KC_K2_VARIANT, tuning knob): threads per CTA,
 // min CTAs per SM (register budget), vectors of each operand in flight per lane
-static int k2_blocked() {
-    static const int b = [] {
+// contiguous unit blocks for groups of small segments (see k2_diff)
+static int k2_blocked(const DiffGroup& G) {
+    static const int forced = [] {
         const char* e = getenv("KC_K2_BLOCKED");
-        return e && *e ? atoi(e) : 0;
+        return e && *e ? atoi(e) : -1;
     }();
-    return b;
+    if (forced >= 0) return forced;
+    return G.n_units < 256 * (uint64_t)G.n_segs;  // average segment < 4 MiB
 }
 
 template <int DT, int THREADS, int MINB, int U>
@@ -1722,7 +1742,7 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
     (void)attr;
     k2_diff<DT, THREADS, MINB, U><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
                                                                          d_reps, bm, atol, rtol, equal_nan, filter,
-                                                                         k2_blocked());
+                                                                         k2_blocked(G));
 }
 
 // Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per
