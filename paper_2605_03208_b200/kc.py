@@ -300,7 +300,7 @@ def _reexec(argv: list, max_attempts: int) -> None:
         os.execv(sys.executable, [sys.executable] + list(argv))
 
 
-def exec_replay_process(argv: list, snapshot_dir: str, max_attempts: int = 8) -> None:
+def exec_replay_process(argv: list, snapshot_dir: str, max_attempts: int = 16) -> None:
     """Call first thing in a replay process, before CUDA initialises: if a host
     mapping already sits on a captured VA window, re-exec for a new layout."""
     _, ok = prereserve(snapshot_dir)
@@ -308,7 +308,7 @@ def exec_replay_process(argv: list, snapshot_dir: str, max_attempts: int = 8) ->
         _reexec(argv, max_attempts)
 
 
-def restore_in_fresh_layout(ctx: "Context", snapshot_dir: str, argv: list, max_attempts: int = 8):
+def restore_in_fresh_layout(ctx: "Context", snapshot_dir: str, argv: list, max_attempts: int = 16):
     """ctx.restore(); on KC_ERR_VA_UNAVAILABLE re-exec this process (ASLR gives
     the driver's VA arenas a new random placement) up to max_attempts times.
     The restore itself never relocates: it aborts and rolls back (R21)."""
@@ -317,10 +317,11 @@ def restore_in_fresh_layout(ctx: "Context", snapshot_dir: str, argv: list, max_a
     except KcError as e:
         if e.status == KC_ERR_VA_UNAVAILABLE:
             _reexec(argv, max_attempts)
+            e.args = (f"{e.args[0] if e.args else ''} (after {max_attempts} process layouts)",)
         raise
 
 
-def replay_seq_in_fresh_layout(ctx: "Context", seq: "Sequence", argv: list, max_attempts: int = 8, **kw):
+def replay_seq_in_fresh_layout(ctx: "Context", seq: "Sequence", argv: list, max_attempts: int = 16, **kw):
     """ctx.replay_seq() with the same policy as restore_in_fresh_layout: a
     collision of the captured VAs with this process's driver arenas re-execs it."""
     try:
