@@ -55,7 +55,7 @@ def _replay(a) -> int:
     shape = lambda v: tuple(int(x) for x in v.split(",")) if v else None  # noqa: E731
     rep = ctx.replay(r, iterations=a.iterations, no_recopy=a.no_recopy, dump_dir=dump, image_override=override,
                      grid=shape(a.grid), block=shape(a.block), smem=a.smem, symbol=a.symbol)
-    out = {"restore": rst, "replay": rep}
+    out = {"restore": rst, "replay": rep, "process_layouts": int(os.environ.get("KC_REEXEC_ATTEMPT", "0")) + 1}
     if a.typed:
         va, nb, dt = a.typed.split(":")
         out["typed"], _ = ctx.validate(r, outs=[(int(va, 16), int(nb), dt)], atol=a.atol, rtol=a.rtol)

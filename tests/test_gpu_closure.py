@@ -528,6 +528,7 @@ def test_cli_capture_of_an_application_without_kc_code(tmp_path):
     p = subprocess.run(cli + ["replay", d], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert p.returncode == 0, p.stdout + p.stderr[-3000:]
     rep = json.loads(p.stdout.strip().splitlines()[-1])
+    print(f"cli replay: {rep.get('process_layouts')} process layout(s)")
     assert rep["pass"] and rep["unexpected_chunks"] == 0
     p = subprocess.run(cli + ["info", d], capture_output=True, text=True, timeout=120, cwd=ROOT)
     info = json.loads(p.stdout.strip().splitlines()[-1])
