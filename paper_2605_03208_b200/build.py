@@ -44,17 +44,33 @@ def _stale(target, deps):
 
 
 def build_lib(force: bool = False, verbose: bool = False) -> str:
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "kc.h"), __file__]
-    if not force and not _stale(LIB, deps):
+    """One object per translation unit, compiled in parallel (objects under
+    build/, rebuilt when their source or any header changed), then linked."""
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "kc.h"), __file__]
+    objdir = os.path.join(ROOT, "build", "kc_obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+    todo = [(s, o) for s, o in zip(SOURCES, objs) if force or _stale(o, [os.path.join(CSRC, s)] + hdrs)]
+    if not todo and not _stale(LIB, objs):
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
-           "-shared", "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES],
-           "-ldl"]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd, cwd=CSRC)
+        flags.insert(0, "-Xptxas=-v")
+
+    def compile_one(so):
+        src, obj = so
+        tmp = obj + f".tmp{os.getpid()}"
+        cmd = [NVCC, *flags, "-c", "-o", tmp, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd, cwd=CSRC)
+        os.replace(tmp, obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        list(ex.map(compile_one, todo))
+    tmp = LIB + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"], cwd=CSRC)
     os.replace(tmp, LIB)
     return LIB
 

@@ -1705,6 +1705,11 @@ cudaError_t launch_digests(const RegionDev* d_regs, int nreg, const uint64_t* d_
     return cudaGetLastError();
 }
 
+cudaError_t launch_snapshot_digest(const uint8_t* d_triples, int nreg, uint64_t* d_out, cudaStream_t s) {
+    k1_snapshot_digest<<<1, 4, 0, s>>>(d_triples, nreg, d_out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64_t C, uint64_t* d_bitmap,
                            uint64_t* d_count, int num_sms, cudaStream_t s) {
     if (C == 0) return cudaSuccess;

@@ -64,6 +64,8 @@ cudaError_t launch_hash_copy(const RegionDev* d_regs, int nreg, uint64_t n_chunk
                              cudaStream_t s, const uint32_t* d_order = nullptr);
 cudaError_t launch_digests(const RegionDev* d_regs, int nreg, const uint64_t* d_chunk_hash, uint64_t* d_region_digest,
                            uint8_t* d_scratch /* 24*nreg */, uint64_t* d_snapshot_digest, cudaStream_t s);
+// S over an explicit (base, size, digest) u64 triple list (24 B per region, ascending base)
+cudaError_t launch_snapshot_digest(const uint8_t* d_triples, int nreg, uint64_t* d_out, cudaStream_t s);
 cudaError_t launch_written(const uint64_t* d_pre, const uint64_t* d_post, uint64_t n_chunks, uint64_t* d_bitmap,
                            uint64_t* d_count, int num_sms, cudaStream_t s);
 // d_filter (may be nullptr): dirty-chunk bitmap; units of clean chunks are skipped

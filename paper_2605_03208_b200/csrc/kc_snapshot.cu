@@ -467,6 +467,7 @@ std::string capture_log_json(const std::vector<LogRegion>& rs, const kc_capture_
 struct RegionState {
     kc_region r;
     bool ok = true;
+    bool failed_pre = false;  // not live before the dispatch: never in any S
     std::string error;
     uint64_t chunk0 = 0;  // index into the manifest arrays (ok regions only)
     uint64_t n_chunks = 0;
@@ -530,6 +531,23 @@ CUresult allow_dynamic_smem(CUfunction f, uint32_t smem) {
 }  // namespace
 
 namespace kc {
+
+// Snapshot digest S (O2, R4) over the regions whose FINAL status is ok: a region
+// can fail after the pre/post pass that produced the first S (a D2H or
+// written-chunk copy failure, or a buffer freed after the dispatch,
+// PAPER.md:753-761), and S must describe exactly the region files written.
+kc_status final_snapshot_digest(kc_ctx* ctx, const std::vector<std::array<uint64_t, 3>>& triples, cudaStream_t s,
+                                uint64_t* out) {
+    const size_t n = triples.size();
+    KC_CHECK_CUDA(ctx, ensure(ctx->digest_scratch, 24 * n + 8), "cudaMalloc(digest scratch)");
+    uint8_t* d = (uint8_t*)ctx->digest_scratch.p;
+    if (n) KC_CHECK_CUDA(ctx, cudaMemcpyAsync(d, triples.data(), 24 * n, cudaMemcpyHostToDevice, s), "upload triples");
+    KC_CHECK_CUDA(ctx, launch_snapshot_digest(d, (int)n, (uint64_t*)(d + 24 * n), s), "launch snapshot digest");
+    ctx->launches += 1;
+    KC_CHECK_CUDA(ctx, cudaMemcpyAsync(out, d + 24 * n, 8, cudaMemcpyDeviceToHost, s), "D2H snapshot digest");
+    KC_CHECK_CUDA(ctx, cudaStreamSynchronize(s), "snapshot digest");
+    return KC_OK;
+}
 
 // Hash a region list (all must be live) and bring the manifest (and digests) to the host.
 kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std::vector<uint64_t>& out_hashes,
@@ -657,6 +675,7 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
         rs[i].n_chunks = (list[i].size + kChunk - 1) / kChunk;
         if (!region_live(ctx, list[i].base, list[i].size)) {
             rs[i].ok = false;
+            rs[i].failed_pre = true;
             rs[i].error = "not inside a live CUDA allocation before the dispatch";
         } else {
             rs[i].chunk0 = kc_count_chunks(live.data(), live.size());
@@ -884,6 +903,19 @@ extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_regi
 
     // ---- capture_log.json, then the sentinel LAST
     rep.snapshot_digest = mode == KC_MODE_PRE_W ? pre_snap : post_snap;  // S of the region files written
+    {
+        // recomputed over the final ok regions when any region failed after that pass
+        std::vector<std::array<uint64_t, 3>> tri;
+        bool changed = false;
+        for (const RegionState& r : rs) {
+            if (r.ok) tri.push_back({r.r.base, r.r.size, mode == KC_MODE_PRE_W ? r.pre_digest : r.post_digest});
+            else if (!r.failed_pre) changed = true;
+        }
+        if (changed) {
+            st = final_snapshot_digest(ctx, tri, cs, &rep.snapshot_digest);
+            if (st != KC_OK) return st;
+        }
+    }
     std::vector<LogRegion> lr;
     for (const RegionState& r : rs) {
         if (!r.ok) rep.n_failed_regions++;
