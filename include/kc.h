@@ -285,6 +285,22 @@ kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, con
 kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
                   kc_diff_report* reps, uint64_t* h_bitmaps, void* stream);
 
+/* ---- A9 combine: finalize reports merged across ranks ------------------
+ * a buffer's report is split over the ranks that hold its
+ * chunks; their counters are SUMmed and their maxima MAXed (exact, order-free)
+ * by the caller's collective.  This recomputes the derived fields of each
+ * merged report from nbytes[i] and dtypes[i] (kc_dtype) with the rules K2
+ * applies at the end of kc_diff (O4, readings R9, R18):
+ * nbytes, n_elems = nbytes / element size, n_chunks = ceil(nbytes / 65536),
+ * percent_bytes = RN(RN(100 * differing_bytes) / nbytes) (0 when nbytes = 0),
+ * differing_elems = differing_bytes for KC_DT_BYTES, and pass (floats:
+ * allclose_fail == 0; integers: differing_elems == 0; bytes: differing_bytes
+ * == 0).  reps, nbytes, dtypes: HOST arrays of n entries (borrowed; reps is
+ * updated in place).  No CUDA call: usable on any host.  KC_ERR_ARG on a NULL
+ * array with n > 0, an unknown dtype, or nbytes not a multiple of the
+ * element size. */
+kc_status kc_report_finalize(kc_diff_report* reps, const uint64_t* nbytes, const int32_t* dtypes, size_t n);
+
 /* ---- F2 fused hash + validate ----------------------
  * One pass (K5) over every buffer pair hashes the ACTUAL bytes (the chunk
  * manifest of the regions {act, nbytes} in the given order: bit-identical to

@@ -49,7 +49,8 @@ struct kc_interpose {
     // the capture in flight
     uint64_t corr = 0;
     std::thread worker;
-    std::mutex hm;
+    bool busy = false;  // ENTER started a worker that EXIT has not joined yet (guarded by mu)
+    std::mutex hm;      // guards the handshake flags below
     std::condition_variable cv;
     bool pre_done = false, go = false, launched = false, finished = false;
 };
@@ -160,17 +161,27 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
             const uint64_t k = ip->seen++;
             if (k < ip->index || k >= ip->index + ip->count) return;
             ip->armed = false;
+            if (ip->busy) {  // (defensive: re-arming waits for the previous worker's join)
+                ip->state = -1;
+                ip->status = KC_ERR_STATE;
+                ip->err = "launch " + std::to_string(k) + " arrived while the previous capture was in flight";
+                return;
+            }
             ip->state = 2;
             ip->corr = d->correlationId;
+            ip->busy = true;
+        }
+        {
+            std::lock_guard<std::mutex> lk(ip->hm);
             ip->pre_done = ip->go = ip->launched = ip->finished = false;
         }
-        if (ip->worker.joinable()) ip->worker.join();  // a previous capture's worker (already finished)
         auto kernarg = std::make_shared<std::vector<uint8_t>>();
         if (!pack_kernarg(f, kp, extra, *kernarg)) {
             std::lock_guard<std::mutex> lk(ip->mu);
             ip->state = -1;
             ip->status = KC_ERR_UNSUPPORTED;
             ip->err = "launch parameters neither in kernelParams nor in a CU_LAUNCH_PARAM_BUFFER_POINTER";
+            ip->busy = false;
             return;
         }
         ip->worker = std::thread([ctx, ip, f, grid0 = grid[0], grid1 = grid[1], grid2 = grid[2], block0 = block[0],
@@ -226,8 +237,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
                     if (sn) kc_snapshot_free(sn);
                 } else if (seq) {
                     ip->steps.push_back(sn);
-                    ip->state = ip->steps.size() < ip->count ? 1 : 3;
-                    ip->armed = ip->state == 1;  // the next launch of the sequence
+                    ip->state = ip->steps.size() < ip->count ? 1 : 3;  // re-armed by EXIT after the join
                     if (ip->state == 3 && !dir.empty()) {  // complete and a directory given: persist it
                         kc_sequence* q = nullptr;
                         kc_status s2 = make_sequence(ctx, ip->steps, &q);
@@ -258,7 +268,7 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
     {
         // the bracketed launch (its capture may have failed already: join the worker anyway)
         std::lock_guard<std::mutex> lk(ip->mu);
-        if (ip->corr != d->correlationId || !ip->worker.joinable()) return;
+        if (ip->corr != d->correlationId || !ip->busy) return;
     }
     const CUresult* rv = (const CUresult*)d->functionReturnValue;
     {
@@ -268,6 +278,11 @@ void kc::interpose_launch(kc_ctx* ctx, uint32_t cbid, const void* cbdata) {
         ip->cv.notify_all();
     }
     ip->worker.join();
+    // only now may the next launch of a sequence start a capture: a new ENTER can no
+    // longer race this join or move-assign a joinable worker
+    std::lock_guard<std::mutex> lk(ip->mu);
+    ip->busy = false;
+    if (ip->count > 1 && ip->state == 1) ip->armed = true;
 }
 
 static kc_status arm(kc_ctx* ctx, const char* target, uint64_t index, uint64_t count, const char* dir,
@@ -306,7 +321,7 @@ static kc_status arm(kc_ctx* ctx, const char* target, uint64_t index, uint64_t c
         return set_err(ctx, KC_ERR_STATE, "kc_interpose_arm: kc_track_install first (the launch hook is CUPTI's)");
     kc_interpose* ip = state_of(ctx);
     std::lock_guard<std::mutex> lk(ip->mu);
-    if (ip->state == 2) return set_err(ctx, KC_ERR_STATE, "kc_interpose_arm: a capture is in flight");
+    if (ip->state == 2 || ip->busy) return set_err(ctx, KC_ERR_STATE, "kc_interpose_arm: a capture is in flight");
     ip->armed = true;
     ip->target = target ? target : "";
     ip->dir = dir ? dir : "";

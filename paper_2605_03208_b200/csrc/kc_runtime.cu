@@ -985,6 +985,35 @@ kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, con
     return KC_OK;
 }
 
+// A9 (C3): derived fields of reports merged across ranks, K2's finalize rules on the host
+kc_status kc_report_finalize(kc_diff_report* reps, const uint64_t* nbytes, const int32_t* dtypes, size_t n) {
+    if (n && (!reps || !nbytes || !dtypes)) return KC_ERR_ARG;
+    for (size_t j = 0; j < n; ++j) {
+        const int dt = dtypes[j];
+        if (dt < KC_DT_BYTES || dt > KC_DT_F64) return KC_ERR_ARG;
+        const uint64_t es = (dt == KC_DT_BYTES || dt == KC_DT_U8 || dt == KC_DT_I8) ? 1
+                            : (dt == KC_DT_U16 || dt == KC_DT_I16 || dt == KC_DT_F16 || dt == KC_DT_BF16) ? 2
+                            : (dt == KC_DT_U32 || dt == KC_DT_I32 || dt == KC_DT_F32) ? 4 : 8;
+        const uint64_t nb = nbytes[j];
+        if (nb % es) return KC_ERR_ARG;
+        kc_diff_report& r = reps[j];
+        r.nbytes = nb;
+        r.n_elems = nb / es;
+        r.n_chunks = (nb + kChunk - 1) / kChunk;
+        volatile double hundred_db = 100.0 * (double)r.differing_bytes;  // two RN steps, no contraction
+        r.percent_bytes = nb ? hundred_db / (double)nb : 0.0;
+        if (dt == KC_DT_BYTES) {
+            r.differing_elems = r.differing_bytes;
+            r.pass = r.differing_bytes == 0;
+        } else if (dt == KC_DT_F16 || dt == KC_DT_BF16 || dt == KC_DT_F32 || dt == KC_DT_F64) {
+            r.pass = r.allclose_fail == 0;
+        } else {
+            r.pass = r.differing_elems == 0;
+        }
+    }
+    return KC_OK;
+}
+
 kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol, kc_diff_report* reps,
                   uint64_t* h_bitmaps, void* stream) {
     KC_ENTER(ctx);

@@ -1357,24 +1357,55 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
             if (w.first <= s.base && s.base + s.size <= w.first + w.second) covered = true;
         if (!covered) {
             const uint64_t prev_end = h->windows.empty() ? 0 : h->windows.back().first + h->windows.back().second;
+            bool lost = false;  // a window released for a merge could not be taken back
             for (uint64_t W : kWindows) {
                 const uint64_t A = W ? W : G;
                 uint64_t lo = s.base / A * A;
                 const uint64_t hi = (s.base + s.size + A - 1) / A * A;
+                // A span that starts inside the window we hold but ends past it (two
+                // regions less than a window apart): the exact span would overlap that
+                // window, so the window is released and one window covering both is
+                // reserved instead (and the old one taken back if that fails).
+                bool merge = false;
                 if (lo < prev_end) {
-                    if (W) continue;  // would overlap a window we already hold
-                    lo = s.base;
+                    if (!W) continue;
+                    lo = std::min(lo, h->windows.back().first) / A * A;
+                    if (h->windows.size() >= 2 &&
+                        lo < h->windows[h->windows.size() - 2].first + h->windows[h->windows.size() - 2].second)
+                        continue;  // would overlap an earlier window
+                    merge = true;
                 }
+                const std::pair<uint64_t, uint64_t> old = merge ? h->windows.back() : std::pair<uint64_t, uint64_t>(0, 0);
+                if (merge) KC_DRV(cuMemAddressFree)((CUdeviceptr)old.first, old.second);
                 CUdeviceptr p = 0;
                 cr = KC_DRV(cuMemAddressReserve)(&p, hi - lo, A, (CUdeviceptr)lo, 0);
                 if (cr == CUDA_SUCCESS && (uint64_t)p == lo) {
-                    h->windows.emplace_back(lo, hi - lo);
+                    if (merge) h->windows.back() = {lo, hi - lo};
+                    else h->windows.emplace_back(lo, hi - lo);
                     covered = true;
                     break;
                 }
                 if (cr == CUDA_SUCCESS) KC_DRV(cuMemAddressFree)(p, hi - lo);
                 s.reserve_got = (uint64_t)p;
                 s.reserve_cr = (int)cr;
+                if (merge) {
+                    CUdeviceptr q = 0;
+                    const CUresult r2 = KC_DRV(cuMemAddressReserve)(&q, old.second, 0, (CUdeviceptr)old.first, 0);
+                    if (r2 != CUDA_SUCCESS || (uint64_t)q != old.first) {
+                        if (r2 == CUDA_SUCCESS) KC_DRV(cuMemAddressFree)(q, old.second);
+                        h->windows.pop_back();
+                        lost = true;
+                        break;
+                    }
+                }
+            }
+            if (lost) {
+                rollback(h);
+                delete h;
+                return set_err(ctx, KC_ERR_VA_UNAVAILABLE,
+                               "kc_restore: the VA window ending at 0x%llx, released to merge span [0x%llx, +%llu) could not be "
+                               "reserved again; VA faithfulness is a hard requirement (PAPER.md:1080-1082)",
+                               (unsigned long long)prev_end, (unsigned long long)s.base, (unsigned long long)s.size);
             }
         }
         if (covered) {

@@ -33,6 +33,10 @@ def _nchunks(size: int) -> int:
     return (size + CHUNK - 1) // CHUNK
 
 
+def _bitmap_words(size: int) -> int:
+    return (_nchunks(size) + 63) // 64
+
+
 def _host_staged(group) -> bool:
     """gloo cannot run these collectives on CUDA tensors: stage through host memory."""
     return dist.get_backend(group) == "gloo"
@@ -98,6 +102,22 @@ class Plan:
     def global_chunks(self) -> int:
         return sum(_nchunks(s) for s in self.sizes)
 
+    def bitmap_words(self, r=None) -> int:
+        """Bitmap words of rank r's regions (one ceil(n_chunks/64)-word bitmap per region)."""
+        return sum(_bitmap_words(s) for _, s in self.local_regions(r))
+
+    def bitmap_permutation(self) -> torch.Tensor:
+        """Index into the gathered [world, max_local_words] bitmap words that yields
+        every region's bitmap in global (ascending base) order."""
+        pad = max(1, max(self.bitmap_words(r) for r in range(self.world)))
+        offs = [0] * self.world
+        idx = []
+        for s, o in zip(self.sizes, self.owner):
+            n = _bitmap_words(s)
+            idx.extend(range(o * pad + offs[o], o * pad + offs[o] + n))
+            offs[o] += n
+        return torch.tensor(idx, dtype=torch.int64)
+
     def manifest_permutation(self) -> torch.Tensor:
         """Index into the gathered [world, max_local] manifest that yields global chunk order."""
         pad = self.max_local_chunks()
@@ -142,34 +162,12 @@ def combine_reports(reps: torch.Tensor, group=None) -> torch.Tensor:
     return out
 
 
-_ELEM = {"bytes": 1, "u8": 1, "i8": 1, "u16": 2, "i16": 2, "u32": 4, "i32": 4, "u64": 8, "i64": 8,
-         "f16": 2, "bf16": 2, "f32": 4, "f64": 8}
-_FLOATS = ("f16", "bf16", "f32", "f64")
-
-
 def finalize(combined: torch.Tensor, nbytes: list, dtypes: list) -> list:
-    """Host-side report dicts of a combined report table (same rules as K2's finalize)."""
-    rows = combined.cpu()
-    out = []
-    for i, (n, dt) in enumerate(zip(nbytes, dtypes)):
-        r = rows[i]
-        u = lambda k: int(r[k].item()) & 0xFFFFFFFFFFFFFFFF
-        d = lambda k: float(torch.tensor([int(r[k].item())], dtype=torch.int64).view(torch.float64).item())
-        db = u(DIFF_BYTES)
-        rep = {"nbytes": n, "n_elems": n // _ELEM[dt], "n_chunks": _nchunks(n), "differing_bytes": db,
-               "differing_elems": db if dt == "bytes" else u(DIFF_ELEMS), "max_ulp": u(MAX_ULP),
-               "max_abs": d(MAX_ABS), "max_rel": d(MAX_REL),
-               "percent_bytes": (100.0 * float(db)) / float(n) if n else 0.0,
-               "nan_ref": u(NAN_REF), "nan_act": u(NAN_ACT), "nan_pos_mismatch": u(NAN_POS),
-               "rel_undefined": u(REL_UNDEF), "allclose_fail": u(ALLCLOSE_FAIL)}
-        if dt == "bytes":
-            rep["pass"] = int(db == 0)
-        elif dt in _FLOATS:
-            rep["pass"] = int(rep["allclose_fail"] == 0)
-        else:
-            rep["pass"] = int(rep["differing_elems"] == 0)
-        out.append(rep)
-    return out
+    """Report dicts of a combined report table: the derived fields (n_elems,
+    n_chunks, percent_bytes, pass) are recomputed by the library
+    (kc_report_finalize, K2's finalize rules), not here."""
+    from . import kc
+    return kc.report_finalize(combined.cpu().numpy(), nbytes, dtypes)
 
 
 # ------------------------------------------------------------------ C4
@@ -183,3 +181,19 @@ def gather_bitmaps(local_words: torch.Tensor, group=None) -> torch.Tensor:
     for r in range(1, world):
         acc |= out.view(world, -1)[r]
     return acc
+
+
+def gather_region_bitmaps(plan: Plan, local_words: torch.Tensor, perm: torch.Tensor | None = None,
+                          group=None) -> torch.Tensor:
+    """C4 for per-region bitmaps under E1 (each region wholly on one rank): all-gather
+    every rank's words (its regions in ascending base, ceil(n_chunks/64) words each)
+    and return them in global region order -- the 1-GPU kc_diff bitmap layout."""
+    pad = max(1, max(plan.bitmap_words(r) for r in range(plan.world)))
+    mine = torch.zeros(pad, dtype=torch.int64, device=local_words.device)
+    n = plan.bitmap_words()
+    mine[:n].copy_(local_words[:n])
+    out = torch.empty(plan.world * pad, dtype=torch.int64, device=local_words.device)
+    _all_gather_into(out, mine, group)
+    if perm is None:
+        perm = plan.bitmap_permutation()
+    return out.index_select(0, perm.to(local_words.device))

@@ -46,6 +46,7 @@ EXPORTED = [
     "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_validate_host_ref",
     "kc_interpose_arm", "kc_interpose_status", "kc_interpose_take", "kc_interpose_arm_seq", "kc_interpose_take_seq",
     "kc_snapshot_load", "kc_seq_load", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
+    "kc_report_finalize",
 ]
 KC_DEP_RAW, KC_DEP_WAW, KC_DEP_WAR = 1, 2, 4
 
@@ -228,6 +229,7 @@ def lib() -> ctypes.CDLL:
         "kc_seq_save": (st, [V, V, ctypes.c_char_p]),
         "kc_seq_free": (None, [V]),
         "kc_replay_seq": (st, [V, V, P(SeqReplayOpts), P(SeqStepReport), P(V)]),
+        "kc_report_finalize": (st, [P(DiffReport), P(U64), P(I32), SZ]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -255,6 +257,23 @@ def build_info() -> str:
 def count_chunks(regions: Sequence[Region]) -> int:
     arr = _regions(regions)
     return int(lib().kc_count_chunks(arr, len(regions)))
+
+
+def report_finalize(rows, nbytes: Sequence[int], dtypes: Sequence[str]) -> list:
+    """kc_report_finalize over reports merged across ranks (A9, C3).  ``rows``:
+    an [R, 15] int64 array/tensor view of kc_diff_report structs (or raw
+    bytes).  Returns the finalized reports as dicts (host only, no CUDA)."""
+    import numpy as np
+    raw = np.ascontiguousarray(np.asarray(rows, dtype=np.int64)).reshape(-1)
+    n = len(nbytes)
+    arr = (DiffReport * max(1, n))()
+    ctypes.memmove(arr, raw.ctypes.data, min(raw.nbytes, ctypes.sizeof(DiffReport) * n))
+    nb = (ctypes.c_uint64 * max(1, n))(*nbytes)
+    dt = (ctypes.c_int32 * max(1, n))(*[DT[d] if isinstance(d, str) else int(d) for d in dtypes])
+    rc = lib().kc_report_finalize(arr, nb, dt, n)
+    if rc != KC_OK:
+        raise KcError(rc, "kc_report_finalize: bad dtype or nbytes")
+    return [arr[i].as_dict() for i in range(n)]
 
 
 def region_array(regions) -> ctypes.Array:

@@ -524,6 +524,34 @@ def interpose_graph(a):
     print(json.dumps({"status": st, "seen_after_capture": seen_after_capture, "mutated_once": once}))
 
 
+def capture_gap(a):
+    """Two regions less than one 32 MiB VA window apart, the second starting
+    inside the first one's window and ending past it (the restore's
+    window merge).  A: 2 MiB at w + 2 MiB, B: 8 MiB at w + 28 MiB (w 32 MiB
+    aligned); the pad and the 24 MiB filler between them are freed before
+    the capture."""
+    M = 1 << 20
+    ctx = kc.Context(0)
+    probe = ctx.alloc(2 * M)
+    ctx.free(probe)
+    pad_sz = ((2 * M - probe) % (32 * M)) or 32 * M
+    pad = ctx.alloc(pad_sz)
+    A = ctx.alloc(2 * M)
+    filler = ctx.alloc(24 * M)
+    B = ctx.alloc(8 * M)
+    ctx.free(filler)
+    ctx.free(pad)
+    geom = {"A": A, "B": B, "a_off": A % (32 * M), "b_off": B - A // (32 * M) * (32 * M)}
+    rng = np.random.default_rng(7)
+    _upload(A, rng.integers(0, 256, 2 * M, dtype=np.uint8))
+    _upload(B, rng.integers(0, 256, 8 * M, dtype=np.uint8))
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    rc, rep = ctx.capture(a.dir, image=image, mangled="kc_fixture_walk", grid=(1, 1, 1), block=(32, 1, 1),
+                          kernarg=synth.c1_kernarg(0, 0, 0, n_lists=0), regions=[(A, 2 * M), (B, 8 * M)],
+                          mode=kc.KC_MODE_PRE_W)
+    print(json.dumps({"rc": rc, "geom": geom, "report": rep}))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("cmd")
@@ -548,7 +576,8 @@ def main():
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
      "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar,
      "publish": publish, "interpose": interpose, "interpose-seq": interpose_seq, "load-replay": load_replay,
-     "load-seq": load_seq, "interpose-graph": interpose_graph}[a.cmd](a)
+     "load-seq": load_seq, "interpose-graph": interpose_graph,
+     "capture-gap": capture_gap}[a.cmd](a)
 
 
 if __name__ == "__main__":

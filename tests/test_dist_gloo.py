@@ -51,6 +51,19 @@ def _worker(rank, world, port, errq):
         whole = np.concatenate([oracle.chunk_hashes(data[i]) for i in order])
         assert np.array_equal(got, whole), "gathered manifest != 1-process manifest"
 
+        # ---- C4 per-region bitmaps (E1: each region on one rank): gathered in global order
+        def act_of(b, d):
+            a = d.copy()
+            a[(b >> 20) % d.size] ^= 0x10                  # one flipped byte per region, VA-seeded
+            if d.size > 70 * CH:
+                a[66 * CH + 3] ^= 1
+            return a
+        lw = [oracle.diff(by_base[b], act_of(b, by_base[b])).bitmap for b, _ in plan.local_regions()]
+        local_w = torch.from_numpy(np.concatenate(lw).view(np.int64)) if lw else torch.zeros(0, dtype=torch.int64)
+        got_bm = kd.gather_region_bitmaps(plan, local_w).numpy().view(np.uint64)
+        whole_bm = np.concatenate([oracle.diff(data[i], act_of(bases[i], data[i])).bitmap for i in order])
+        assert np.array_equal(got_bm, whole_bm), "gathered per-region bitmaps != 1-process bitmaps"
+
         # ---- C3/C4 on a buffer split across the ranks (chunk-aligned halves)
         rng = np.random.default_rng(7)
         n_el = 2 * (128 * CH) // 2  # bf16 elements of a 2 x 4 MiB buffer
@@ -129,3 +142,34 @@ def test_plan_permutation_single_rank_is_identity():
     p2 = Plan([0, 1 << 30, 2 << 30], [CH * 3, 5, CH], [1, 0, 1], 2, 0)
     # rank 0 holds region 1 (1 chunk), rank 1 holds regions 0 and 2 (3 + 1 chunks); pad = 4
     assert p2.manifest_permutation().tolist() == [4, 5, 6, 0, 7]
+
+
+def test_plan_bitmap_permutation():
+    from paper_2605_03208_b200.dist import Plan
+    # sizes: 130 chunks (3 words), 1 chunk (1 word), 64 chunks (1 word); owners 1, 0, 1
+    p = Plan([0, 1 << 30, 2 << 30], [CH * 130, 5, CH * 64], [1, 0, 1], 2, 0)
+    # rank 0 words: [r1]; rank 1 words: [r0 x3, r2]; pad = 4
+    assert p.bitmap_words(0) == 1 and p.bitmap_words(1) == 4
+    assert p.bitmap_permutation().tolist() == [4, 5, 6, 0, 7]
+
+
+def test_report_finalize_in_the_library_matches_the_oracle_rules():
+    """kc_report_finalize (host, no CUDA) on counters the oracle produced: the derived
+    fields equal the oracle's own report (1 of 1024 bytes -> 0.09765625)."""
+    import oracle
+    from paper_2605_03208_b200 import kc
+    ref = np.zeros(1024, dtype=np.uint8)
+    act = ref.copy()
+    act[5] = 1
+    for dt, name in ((oracle.DT_BYTES, "bytes"), (oracle.DT_U32, "u32"), (oracle.DT_F32, "f32")):
+        exp = oracle.diff(ref, act, dt).report
+        row = np.zeros(15, dtype=np.int64)
+        row[3], row[4], row[5] = exp["differing_bytes"], exp["differing_elems"], exp["max_ulp"]
+        row[9:14] = [exp[k] for k in ("nan_ref", "nan_act", "nan_pos_mismatch", "rel_undefined", "allclose_fail")]
+        row[6] = np.array([exp["max_abs"]]).view(np.int64)[0]
+        row[7] = np.array([exp["max_rel"]]).view(np.int64)[0]
+        got = kc.report_finalize(row.reshape(1, 15), [1024], [name])[0]
+        assert got == exp, (name, got, exp)
+        assert got["percent_bytes"] == 0.09765625
+    with pytest.raises(kc.KcError):
+        kc.report_finalize(np.zeros((1, 15), dtype=np.int64), [1023], ["u32"])

@@ -169,6 +169,22 @@ def test_region_freed_after_dispatch_is_tolerated(tmp_path, mode):
     assert json.load(open(os.path.join(d, "memory_regions.json")))  # written first, still parses
 
 
+def test_restore_merges_a_window_straddling_span(tmp_path):
+    """Two captured regions 24 MiB apart, the second starting inside the first's
+    32 MiB VA window and ending past it: a fresh process restores both at their
+    VAs (the window is released and one covering both reserved; R28a)."""
+    d = str(tmp_path / "gap")
+    cap = run("capture-gap", d)
+    assert cap["rc"] == 0, cap
+    g = cap["geom"]
+    M = 1 << 20
+    assert g["a_off"] == 2 * M and g["b_off"] == 28 * M      # B starts inside A's window, ends past it
+    res = run("replay", d)
+    assert "restore" in res, res
+    assert [tuple(x) for x in res["regions"]] == [(g["A"], 2 * M), (g["B"], 8 * M)]
+    assert all(r["differing_bytes"] == 0 for r in res["validate"])
+
+
 def test_staging_pieces_follow_io_chunk(tmp_path):
     """the number of D2H copies follows KERNCAP_SNAPSHOT_CHUNK_BYTES."""
     d = str(tmp_path / "st")
