@@ -102,13 +102,14 @@ class ClockSampler:
 class Pool:
     """This rank's shard of the c4 pool: live regions, the captured reference copy, the F3 dispatch."""
 
-    def __init__(self, ctx, rank, world, device, log):
+    def __init__(self, ctx, rank, world, device, log, plant=False, placement="e1"):
         import numpy as np
         import torch
         import synth
         self.torch = torch
+        self.placement = placement
         specs = synth.c4_specs()
-        owner = synth.c4_placement(specs, world)
+        owner = synth.c4_placement(specs, world) if placement == "e1" else [0] * len(specs)
         # the F3 activations/output sit with layer 0 on rank 0 (its closure is local)
         for i, s in enumerate(specs):
             if s.name in ("x", "topk", "y"):
@@ -165,7 +166,74 @@ class Pool:
             self.ref[s.name] = ctx.alloc(s.size)
             synth.dev_view(self.ref[s.name], s.size, device).copy_(synth.dev_view(self.va[s.name], s.size, device))
         torch.cuda.synchronize()
+        self.n_plants = 0
+        if plant:
+            self.n_plants = self.plant(device)
         self.C = None
+        if placement == "e2":
+            self.share_e2(ctx, rank, world, log)
+
+    def share_e2(self, ctx, rank, world, log):
+        """E2: the whole pool lives in rank 0's HBM; every rank maps
+        rank 0's live and reference regions (kc_peer_export -> kc_peer_import: NVLink
+        peer access from the other GPUs) and hashes/diffs a contiguous, 64-chunk
+        aligned share of the global chunk range (global spec order), so bitmap words
+        of different ranks are disjoint."""
+        import torch.distributed as dist
+        objs = [None]
+        if rank == 0:
+            objs[0] = {"pid": os.getpid(),
+                       "va": {n: (va,) + ctx.peer_export(va) for n, va in self.va.items()},
+                       "ref": {n: (va,) + ctx.peer_export(va) for n, va in self.ref.items()}}
+        dist.broadcast_object_list(objs, src=0)
+        ex = objs[0]
+        t0 = time.time()
+        if rank != 0:
+            self.va = {n: ctx.peer_import(ex["pid"], fd, sz, va) for n, (va, fd, sz) in ex["va"].items()}
+            self.ref = {n: ctx.peer_import(ex["pid"], fd, sz, va) for n, (va, fd, sz) in ex["ref"].items()}
+        dist.barrier()
+        specs = self.all_specs
+        nck = [(sp.size + 65535) // 65536 for sp in specs]
+        C = sum(nck)
+        bnd = [min(C, (C * r // world) // 64 * 64) for r in range(world)] + [C]
+        lo, hi = bnd[rank], bnd[rank + 1]
+        self.e2_counts = [bnd[r + 1] - bnd[r] for r in range(world)]
+        self.sub = []   # (global idx, chunk offset in the region, nbytes) of this rank's share
+        off = 0
+        for g, sp in enumerate(specs):
+            a, b = max(lo, off), min(hi, off + nck[g])
+            if a < b:
+                k0 = a - off
+                self.sub.append((g, k0, min(sp.size, b * 65536 - off * 65536) - k0 * 65536))
+            off += nck[g]
+        self.regions = [(self.va[specs[g].name] + 65536 * k0, n) for g, k0, n in self.sub]
+        self.bytes = sum(n for _, _, n in self.sub)
+        log(f"rank {rank}: E2 share chunks [{lo}, {hi}) of {C} over {len(self.sub)} sub-regions, "
+            f"{self.bytes / 1e9:.3f} GB of rank 0's pool ({'own HBM' if rank == 0 else 'peer-mapped'}; "
+            f"mapped in {time.time() - t0:.2f}s)")
+
+    def plant(self, device) -> int:
+        """--plant: XOR single bytes of the reference copy at offsets fixed by the
+        region's global index (the same at every N): a 1-ULP step, a sign flip and
+        an exponent-bit flip in one of every 7 bf16 regions.  Each plant changes
+        exactly one byte."""
+        import synth
+        n = 0
+        for s in self.specs:
+            g = self.gidx[s.name]
+            if s.dtype != "bf16" or g % 7 != 3:
+                continue
+            v = synth.dev_view(self.ref[s.name], s.size, device)
+            ne = s.size // 2
+            offs = {}
+            for k, (lohi, mask) in enumerate(((0, 0x01), (1, 0x80), (1, 0x01))):
+                e = (g * 2654435761 + k * 40503 * 32768 + 17) % ne
+                offs[2 * e + lohi] = mask
+            for off, mask in offs.items():
+                v[off] ^= mask
+                n += 1
+        self.torch.cuda.synchronize()
+        return n
 
     def launch_f3(self, stream):
         if self.fn is None:
@@ -182,11 +250,27 @@ class Pool:
         return 1
 
     def diff_buffers(self):
+        """(buffers, report sizes, report bitmap word offsets).  E1: one report per
+        local region.  E2: one report per GLOBAL region (185), each rank's share a
+        segment of it starting at its chunk offset (bitmap_chunk0)."""
         from paper_2605_03208_b200 import kc
         out = []
-        for i, s in enumerate(self.specs):
-            out.append(kc.Buffer(self.ref[s.name], self.va[s.name], s.size, kc.DT[s.dtype], i, 0))
-        return out
+        if self.placement == "e2":
+            specs = self.all_specs
+            for g, k0, n in self.sub:
+                s = specs[g]
+                out.append(kc.Buffer(self.ref[s.name] + 65536 * k0, self.va[s.name] + 65536 * k0, n, kc.DT[s.dtype],
+                                     g, k0))
+            sizes = [s.size for s in specs]
+        else:
+            for i, s in enumerate(self.specs):
+                out.append(kc.Buffer(self.ref[s.name], self.va[s.name], s.size, kc.DT[s.dtype], i, 0))
+            sizes = [s.size for s in self.specs]
+        word0, acc = [], 0
+        for n in sizes:
+            word0.append(acc)
+            acc += ((n + 65535) // 65536 + 63) // 64
+        return out, sizes, word0, acc
 
 
 def run_ours(a, rank, world, device, log):
@@ -197,7 +281,7 @@ def run_ours(a, rank, world, device, log):
 
     torch.cuda.set_device(device)
     ctx = kc.Context(device)
-    pool = Pool(ctx, rank, world, device, log)
+    pool = Pool(ctx, rank, world, device, log, plant=a.plant, placement=a.placement)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     C = kc.count_chunks(pool.regions)
@@ -208,14 +292,10 @@ def run_ours(a, rank, world, device, log):
     words = (C + 63) // 64
     wbm = torch.zeros(max(1, words), dtype=torch.int64, device="cuda")
     wcnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    bufs = pool.diff_buffers()
-    rep_nbytes = [b.nbytes for b in bufs]
-    word0, acc = [], 0
-    for b in bufs:
-        word0.append(acc)
-        acc += ((b.nbytes + 65535) // 65536 + 63) // 64
+    bufs, rep_nbytes, word0, acc = pool.diff_buffers()
+    n_rep = len(rep_nbytes)
     REP_WORDS = 15  # sizeof(kc_diff_report) / 8
-    reps = torch.zeros(max(1, len(bufs)) * REP_WORDS, dtype=torch.int64, device="cuda")
+    reps = torch.zeros(max(1, n_rep) * REP_WORDS, dtype=torch.int64, device="cuda")
     bms = torch.zeros(max(1, acc), dtype=torch.int64, device="cuda")
     KEYS = ("hash_pre", "dispatch", "hash_post", "written", "diff", "combine")
     evs = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in KEYS}
@@ -224,6 +304,7 @@ def run_ours(a, rank, world, device, log):
     # A9 combine (N > 1): C1 plan broadcast once; per step C2 manifests all-gather, C3 reports all-reduce
     plan = perm = None
     glob_reps = None
+    e2 = pool.placement == "e2"
     if world > 1:
         from paper_2605_03208_b200 import dist as kd
         specs_all = pool.all_specs
@@ -231,8 +312,10 @@ def run_ours(a, rank, world, device, log):
                                   [s.size for s in specs_all] if rank == 0 else None,
                                   pool.owner if rank == 0 else None, device="cuda")
         perm = plan.manifest_permutation().cuda()
+        bperm = plan.bitmap_permutation().cuda()
         rows = torch.tensor([pool.gidx[s.name] for s in pool.specs], dtype=torch.int64, device="cuda")
         glob_reps = torch.zeros(len(specs_all), REP_WORDS, dtype=torch.int64, device="cuda")
+        glob = {}
 
     def step(ev):
         launches = 0
@@ -254,14 +337,20 @@ def run_ours(a, rank, world, device, log):
         ctx.written(pre.data_ptr(), post.data_ptr(), C, wbm.data_ptr(), wcnt.data_ptr(), stream=sh)
         rec("written", 1)
         rec("diff", 0)
-        ctx.diff_async(bufs, len(bufs), rep_nbytes, reps.data_ptr(), word0, bms.data_ptr(), stream=sh)
+        ctx.diff_async(bufs, n_rep, rep_nbytes, reps.data_ptr(), word0, bms.data_ptr(), stream=sh)
         rec("diff", 1)
         if world > 1:
             rec("combine", 0)
-            kd.Plan.gather_manifest(plan, post, perm)
-            glob_reps.zero_()
-            glob_reps.index_copy_(0, rows, reps.view(-1, REP_WORDS))
-            kd.combine_reports(glob_reps)
+            if e2:   # contiguous chunk ranges; every rank reports all 185 regions (its segments)
+                glob["manifest"] = kd.gather_ranges(post, pool.e2_counts)              # C2
+                glob["reports"] = kd.combine_reports(reps.view(-1, REP_WORDS))          # C3
+                glob["bitmaps"] = kd.gather_bitmaps(bms)                                # C4 (disjoint words)
+            else:
+                glob["manifest"] = kd.Plan.gather_manifest(plan, post, perm)            # C2
+                glob_reps.zero_()
+                glob_reps.index_copy_(0, rows, reps.view(-1, REP_WORDS))
+                glob["reports"] = kd.combine_reports(glob_reps)                         # C3
+                glob["bitmaps"] = kd.gather_region_bitmaps(plan, bms, bperm)            # C4
             rec("combine", 1)
         return launches
 
@@ -270,7 +359,11 @@ def run_ours(a, rank, world, device, log):
     torch.cuda.synchronize()
     # correctness gate before timing: the replayed pool must validate bit-exactly
     rh = reps.view(-1, REP_WORDS).cpu().numpy()
-    assert int(rh[:, 3].sum()) == 0, "pool pair differs: validation failed"
+    chk = torch.tensor([int(rh[:, 3].sum()), pool.n_plants], dtype=torch.int64, device="cuda")
+    if world > 1:   # (E2: a region's plants may lie in another rank's share)
+        kd._all_reduce(chk, dist.ReduceOp.SUM)
+    assert int(chk[0]) == int(chk[1]), \
+        f"pool pair: {int(chk[0])} differing bytes, {int(chk[1])} planted: validation failed"
 
     l0 = ctx.kernel_launches()
     clocks = ClockSampler(device)
@@ -307,33 +400,47 @@ def run_ours(a, rank, world, device, log):
 
     # cross-N fingerprint (O7: N-GPU results equal the 1-GPU ones bit for bit): SHA-256 of the
     # post-manifest in global spec order (pointer tables excluded: they hold this process's
-    # VAs) and the combined report counters
+    # VAs), of the finalized reports (kc_report_finalize) and of the per-region bitmaps, all in
+    # global spec order -- at N > 1 the C2/C3/C4 results of the last timed step
     import hashlib
     import numpy as np
     specs_all = pool.all_specs
+    nck = [(s.size + 65535) // 65536 for s in specs_all]
+    nwd = [(c + 63) // 64 for c in nck]
     if world > 1:
-        gm = kd.Plan.gather_manifest(plan, post, perm).cpu().numpy()
-        cr = kd.combine_reports(torch.zeros_like(glob_reps).index_copy_(0, rows, reps.view(-1, REP_WORDS)))
-        counters = cr.cpu().numpy()[:, [3, 4, 9, 10, 13]].sum(axis=0)
-        starts, o = [], 0
-        for s in specs_all:
-            starts.append(o)
-            o += (s.size + 65535) // 65536
-        pieces = [gm[starts[g]:starts[g] + (s.size + 65535) // 65536] for g, s in enumerate(specs_all)]
+        gm = glob["manifest"].cpu().numpy()
+        rep_rows = glob["reports"].cpu().numpy()
+        gb = glob["bitmaps"].cpu().numpy()
+        starts = np.cumsum([0] + nck[:-1])
+        wst = np.cumsum([0] + nwd[:-1])
+        pieces = [gm[starts[g]:starts[g] + nck[g]] for g in range(len(specs_all))]
+        bm_pieces = [gb[wst[g]:wst[g] + nwd[g]] for g in range(len(specs_all))]
     else:
-        hp = post.cpu().numpy()
-        byg, o = {}, 0
-        for s in pool.specs:
-            n = (s.size + 65535) // 65536
-            byg[pool.gidx[s.name]] = hp[o:o + n]
-            o += n
+        hp, bh = post.cpu().numpy(), bms.cpu().numpy()
+        rl = reps.view(-1, REP_WORDS).cpu().numpy()
+        byg, bmg, o = {}, {}, 0
+        rep_rows = np.zeros((len(specs_all), REP_WORDS), dtype=np.int64)
+        for i, s in enumerate(pool.specs):
+            g = pool.gidx[s.name]
+            byg[g] = hp[o:o + nck[g]]
+            o += nck[g]
+            bmg[g] = bh[word0[i]:word0[i] + nwd[g]]
+            rep_rows[g] = rl[i]
         pieces = [byg[g] for g in range(len(specs_all))]
-        counters = reps.view(-1, REP_WORDS).cpu().numpy()[:, [3, 4, 9, 10, 13]].sum(axis=0)
+        bm_pieces = [bmg[g] for g in range(len(specs_all))]
+    fin = kc.report_finalize(rep_rows, [s.size for s in specs_all], [s.dtype for s in specs_all])
+    counters = [sum(r[k] for r in fin) for k in ("differing_bytes", "differing_elems", "nan_ref", "nan_act",
+                                                 "allclose_fail")]
     fp = hashlib.sha256()
     for s, pc in zip(specs_all, pieces):
         if not s.name.startswith("ptr_"):
             fp.update(pc.tobytes())
     fingerprint = {"post_manifest_sha256_excl_ptr_tables": fp.hexdigest(),
+                   "reports_sha256": hashlib.sha256(json.dumps(fin, sort_keys=True).encode()).hexdigest(),
+                   "bitmaps_sha256": hashlib.sha256(b"".join(b.tobytes() for b in bm_pieces)).hexdigest(),
+                   "bitmap_bits": int(sum(bin(int(w) & 0xFFFFFFFFFFFFFFFF).count("1") for b in bm_pieces for w in b)),
+                   "max_ulp": max(r["max_ulp"] for r in fin), "max_abs": max(r["max_abs"] for r in fin),
+                   "max_rel": max(r["max_rel"] for r in fin),
                    "chunks": int(sum(p.size for p in pieces)), "report_counter_sums": [int(x) for x in counters]}
 
     # per-kernel roofline: the dominant kernel by time share
@@ -365,12 +472,12 @@ def run_ours(a, rank, world, device, log):
 
     # ------------------------------------------------------------------ F2 fused step
     fused = None
-    if not a.no_fused:
+    if not a.no_fused and not e2:
         fused = run_fused(a, ctx, pool, stream, pre, post, dig, wbm, wcnt, bufs, reps, C, nreg, world, log)
 
     # ------------------------------------------------------------------ e2e
     e2e = e2e_host_ref = None
-    if not a.no_e2e:
+    if not a.no_e2e and not e2:
         e2e_host_ref = run_e2e_host_ref(a, ctx, pool, stream, world, log, pre, post, dig, wbm, wcnt, C, nreg)
         torch.cuda.synchronize()
         torch._C._host_emptyCache()   # pinned e2e staging back to the OS
@@ -919,14 +1026,36 @@ def main():
     p.add_argument("--no-latency", action="store_true")
     p.add_argument("--latency-dir", default="/dev/shm/kc_bench_capture")
     p.add_argument("--quiet", action="store_true")
+    p.add_argument("--plant", action="store_true",
+                   help="plant 1-byte mismatches in the reference pool (deterministic by region, so the N-GPU "
+                        "reports and bitmaps can be compared with the 1-GPU ones); never a headline number")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--placement", default="e1", choices=["e1", "e2"],
+                   help="e1: residency-first shards (each rank reads its own HBM; the headline); e2: the pool "
+                        "resident on rank 0, every rank reading a 1/N share of it over NVLink peer mappings "
+                        "(bounded by rank 0's HBM, SURVEY.md 8(e))")
     p.add_argument("--replay-child", default=None, help=argparse.SUPPRESS)
     a = p.parse_args()
     if a.replay_child:
         replay_child(a.replay_child)
         return
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        # one process per GPU: launch the ranks ourselves (the driver's torchrun line,
+        # run from here), rendezvous on 127.0.0.1; rank 0 prints the JSON line
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print(json.dumps({"error": f"--gpus {a.gpus} but WORLD_SIZE {world}: launch one rank per GPU"}), flush=True)
+        sys.exit(2)
     log = (lambda m: None) if a.quiet else (lambda m: print(m, file=sys.stderr, flush=True))
 
     if a.impl == "reference":
@@ -947,10 +1076,19 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
         else:
             dist.init_process_group(backend)
+    if world == 1:
+        a.placement = "e1"   # one rank: the pool is resident and local either way
     res, pool = run_ours(a, rank, world, device, log)
+    if world > 1:
+        res["config"]["collectives"] = {"backend": torch.distributed.get_backend(),
+                                        "nccl": ".".join(map(str, torch.cuda.nccl.version())),
+                                        "step": "C2 all_gather manifests, C3 all_reduce SUM/MAX reports, "
+                                                "C4 all_gather per-region bitmaps"}
     if os.environ.get("KC_BENCH_ONE_GPU") and world > 1:
         res["config"]["functional_check_only"] = "all ranks on cuda:0 (KC_BENCH_ONE_GPU)"
-    if rank == 0:
+    if a.plant:
+        res["config"]["planted"] = "reference pool planted with 1-byte mismatches (--plant): a parity run"
+    if rank == 0 and not a.no_cpu_baseline:
         threads = os.cpu_count() or 1
         sample = oracle_sample(pool, a.cpu_sample_mb)
         v, dt, nb = time_oracle(sample, threads, a.cpu_seconds)
@@ -959,6 +1097,7 @@ def main():
                                          f"({sum(x.size for _, x in sample) / 1e6:.1f} MB) repeated to "
                                          f"{nb / 1e9:.2f} GB: 2 oracle manifests + oracle diff per pass; "
                                          f"{dt:.1f} s on {threads} threads"}
+    if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:
         torch.distributed.barrier()

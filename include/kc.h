@@ -285,6 +285,33 @@ kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, con
 kc_status kc_diff(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
                   kc_diff_report* reps, uint64_t* h_bitmaps, void* stream);
 
+/* ---- E2 peer mappings ------------------------------
+ * The north star's "each GPU hashes and diffs its shard (reading peer memory
+ * over NVLink)": a pool resident on one GPU is read by the kernels of other
+ * GPUs, one process per GPU.  The paper is single-GPU.
+ *
+ * kc_peer_export: the physical allocation behind a VMM kc_alloc allocation
+ * (base = the address kc_alloc returned) as a POSIX file descriptor of this
+ * process (*fd_out, owned by the ctx: closed by kc_free(base) or kc_destroy)
+ * and its mapped size (*size_out, granularity-rounded).  The fd number is only
+ * meaningful together with this process's pid.  KC_ERR_NOT_TRACKED if base is
+ * not such an allocation (KC_ALLOC_MEMALLOC memory cannot be exported). */
+kc_status kc_peer_export(kc_ctx* ctx, uint64_t base, int32_t* fd_out, uint64_t* size_out);
+/* kc_peer_import: duplicate the owner's fd (pid, fd from kc_peer_export) with
+ * pidfd_getfd (Linux >= 5.6; same user or CAP_SYS_PTRACE), import it and map
+ * size bytes read-write for THIS ctx's device: peer access over NVLink when the
+ * owner is another GPU, a second mapping when it is the same GPU.  The mapping
+ * is placed at want_va when that range is free in this process (0 = anywhere),
+ * else at a fresh VA; *va_out receives it.  Chunk hashes and diff reports do
+ * not depend on the VA, so the manifests equal the owner's.  The owner must
+ * keep the allocation alive while it is mapped here.  KC_ERR_STATE when the
+ * owner process or its fd is gone; KC_ERR_CUDA on an import/map failure
+ * (nothing is left mapped). */
+kc_status kc_peer_import(kc_ctx* ctx, int32_t pid, int32_t fd, uint64_t size, uint64_t want_va, uint64_t* va_out);
+/* kc_peer_release: unmap an imported mapping (after the device is idle) and
+ * drop the imported handle.  KC_ERR_NOT_TRACKED if va is not one. */
+kc_status kc_peer_release(kc_ctx* ctx, uint64_t va);
+
 /* ---- A9 combine: finalize reports merged across ranks ------------------
  * a buffer's report is split over the ranks that hold its
  * chunks; their counters are SUMmed and their maxima MAXed (exact, order-free)

@@ -102,6 +102,7 @@ struct kc_ctx {
     struct VmmAlloc {
         uint64_t reserved;
         CUmemGenericAllocationHandle h;
+        int export_fd = -1;  // E2: POSIX fd of the physical allocation once exported (closed on free)
     };
     std::map<uint64_t, VmmAlloc> vmm;  // base -> reservation (guarded by mu)
     // ctx-owned VA heap for KC_ALLOC_VMM (reserved once, never returned to the
@@ -129,6 +130,13 @@ struct kc_ctx {
     std::map<uint64_t, uint64_t> heap_free;
     uint64_t launches = 0;
     kc_interpose* interpose = nullptr;  // armed / in-flight interposed capture
+    // E2: peer allocations imported from other processes (kc_peer_import): va -> mapping (mu)
+    struct PeerMap {
+        uint64_t size;
+        CUmemGenericAllocationHandle h;
+        bool own_va;  // the VA range was reserved by the import (else: inside the ctx heap)
+    };
+    std::map<uint64_t, PeerMap> peers;
 };
 
 struct kc_restored_region {

@@ -3,6 +3,9 @@
 // interposition), and the asynchronous K1/K2/K3 entry points of include/kc.h.
 #include <cupti.h>
 #include <dlfcn.h>
+#include <errno.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -239,6 +242,7 @@ kc_status free_alloc(kc_ctx* ctx, uint64_t dptr, bool track) {
         }
     }
     if (is_vmm) {
+        if (va.export_fd >= 0) close(va.export_fd);
         KC_CHECK_CU(ctx, KC_DRV(cuMemUnmap)((CUdeviceptr)dptr, va.reserved), "cuMemUnmap");
         KC_DRV(cuMemRelease)(va.h);
         heap_put(ctx, dptr, va.reserved);  // the VA stays in the ctx heap
@@ -337,6 +341,11 @@ void kc_destroy(kc_ctx* ctx) {
     if (ctx->cupti_installed) kc_track_uninstall(ctx);
     interpose_destroy(ctx);
     bind_device(ctx);
+    {
+        std::vector<uint64_t> pv;
+        for (auto& kv : ctx->peers) pv.push_back(kv.first);
+        for (uint64_t v : pv) kc_peer_release(ctx, v);
+    }
     std::vector<uint64_t> vm;
     for (auto& kv : ctx->vmm) vm.push_back(kv.first);
     for (uint64_t b : vm) free_alloc(ctx, b, false);
@@ -437,6 +446,7 @@ kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = ctx->device;
+    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // exportable to peers (E2)
     if (!heap_init(ctx)) return set_err(ctx, KC_ERR_CUDA, "kc_alloc: cannot reserve the VA heap");
     const CUdeviceptr va = (CUdeviceptr)heap_alloc(ctx, rsz);
     if (!va) return set_err(ctx, KC_ERR_NOMEM, "kc_alloc: VA heap exhausted (KC_VA_HEAP_GB)");
@@ -463,7 +473,7 @@ kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
     }
     {
         std::lock_guard<std::mutex> lk(ctx->mu);
-        ctx->vmm[(uint64_t)va] = kc_ctx::VmmAlloc{rsz, h};
+        ctx->vmm[(uint64_t)va] = kc_ctx::VmmAlloc{rsz, h, -1};
     }
     {  // tracked explicitly at the requested size (the CUPTI hook ignores the library's own calls)
         kc_status st = kc_track(ctx, KC_EV_MAP, (uint64_t)va, size, ctx->device, KC_KIND_VMM);
@@ -479,6 +489,103 @@ kc_status kc_alloc(kc_ctx* ctx, uint64_t size, uint64_t* dptr_out) {
 kc_status kc_free(kc_ctx* ctx, uint64_t dptr) {
     KC_ENTER(ctx);
     return free_alloc(ctx, dptr, true);
+}
+
+// ------------------------------------------------------------------ E2 peer mappings
+// SURVEY.md 8(e) E2 / north star "each GPU hashes and diffs its shard (reading
+// peer memory over NVLink)": the owner exports the physical allocation behind a
+// kc_alloc'd region as a POSIX fd; a peer process (one per GPU) duplicates it
+// with pidfd_getfd, imports it and maps it with access for its own device, so
+// K1/K2 launched there read the owner's HBM over NVLink (same GPU: plain HBM).
+kc_status kc_peer_export(kc_ctx* ctx, uint64_t base, int32_t* fd_out, uint64_t* size_out) {
+    KC_ENTER(ctx);
+    if (!fd_out || !size_out) return set_err(ctx, KC_ERR_ARG, "kc_peer_export: NULL output");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    auto it = ctx->vmm.find(base);
+    if (it == ctx->vmm.end())
+        return set_err(ctx, KC_ERR_NOT_TRACKED, "kc_peer_export: 0x%llx is not the base of a VMM kc_alloc allocation",
+                       (unsigned long long)base);
+    if (it->second.export_fd < 0) {
+        int fd = -1;
+        KC_CHECK_CU(ctx, KC_DRV(cuMemExportToShareableHandle)(&fd, it->second.h,
+                                                               CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+                    "cuMemExportToShareableHandle");
+        it->second.export_fd = fd;
+    }
+    *fd_out = it->second.export_fd;
+    *size_out = it->second.reserved;
+    return KC_OK;
+}
+
+kc_status kc_peer_import(kc_ctx* ctx, int32_t pid, int32_t fd, uint64_t size, uint64_t want_va, uint64_t* va_out) {
+    KC_ENTER(ctx);
+    if (!va_out || size == 0 || fd < 0) return set_err(ctx, KC_ERR_ARG, "kc_peer_import: bad args");
+#if defined(SYS_pidfd_open) && defined(SYS_pidfd_getfd)
+    const int pfd = (int)syscall(SYS_pidfd_open, pid, 0);
+    if (pfd < 0) return set_err(ctx, KC_ERR_STATE, "kc_peer_import: pidfd_open(%d): %s", pid, strerror(errno));
+    const int myfd = (int)syscall(SYS_pidfd_getfd, pfd, fd, 0);
+    const int gerr = errno;
+    close(pfd);
+    if (myfd < 0) return set_err(ctx, KC_ERR_STATE, "kc_peer_import: pidfd_getfd(%d, %d): %s", pid, fd, strerror(gerr));
+    CUmemGenericAllocationHandle h;
+    CUresult r = KC_DRV(cuMemImportFromShareableHandle)(&h, (void*)(uintptr_t)myfd,
+                                                        CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(myfd);
+    if (r != CUDA_SUCCESS) return cu_err(ctx, r, "kc_peer_import: cuMemImportFromShareableHandle");
+    // the owner's VA when it is free here (the region keeps its address), else any VA
+    CUdeviceptr va = 0;
+    r = KC_DRV(cuMemAddressReserve)(&va, size, 0, (CUdeviceptr)want_va, 0);
+    if (r == CUDA_SUCCESS && want_va && (uint64_t)va != want_va) {
+        KC_DRV(cuMemAddressFree)(va, size);
+        r = KC_DRV(cuMemAddressReserve)(&va, size, 0, 0, 0);
+    }
+    if (r != CUDA_SUCCESS) {
+        KC_DRV(cuMemRelease)(h);
+        return cu_err(ctx, r, "kc_peer_import: cuMemAddressReserve");
+    }
+    r = KC_DRV(cuMemMap)(va, size, 0, h, 0);
+    if (r == CUDA_SUCCESS) {
+        CUmemAccessDesc acc;
+        acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc.location.id = ctx->device;  // peer access from this GPU (NVLink when the owner is another GPU)
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        r = KC_DRV(cuMemSetAccess)(va, size, &acc, 1);
+        if (r != CUDA_SUCCESS) KC_DRV(cuMemUnmap)(va, size);
+    }
+    if (r != CUDA_SUCCESS) {
+        KC_DRV(cuMemAddressFree)(va, size);
+        KC_DRV(cuMemRelease)(h);
+        return cu_err(ctx, r, "kc_peer_import: cuMemMap/cuMemSetAccess");
+    }
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        ctx->peers[(uint64_t)va] = kc_ctx::PeerMap{size, h, true};
+    }
+    *va_out = (uint64_t)va;
+    return KC_OK;
+#else
+    (void)pid; (void)fd; (void)size; (void)want_va;
+    return set_err(ctx, KC_ERR_UNSUPPORTED, "kc_peer_import: pidfd_getfd is not available on this system");
+#endif
+}
+
+kc_status kc_peer_release(kc_ctx* ctx, uint64_t va) {
+    KC_ENTER(ctx);
+    kc_ctx::PeerMap m;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        auto it = ctx->peers.find(va);
+        if (it == ctx->peers.end())
+            return set_err(ctx, KC_ERR_NOT_TRACKED, "kc_peer_release: 0x%llx is not an imported mapping",
+                           (unsigned long long)va);
+        m = it->second;
+        ctx->peers.erase(it);
+    }
+    cudaDeviceSynchronize();  // no kernel may still read the mapping
+    KC_DRV(cuMemUnmap)((CUdeviceptr)va, m.size);
+    KC_DRV(cuMemAddressFree)((CUdeviceptr)va, m.size);
+    KC_DRV(cuMemRelease)(m.h);
+    return KC_OK;
 }
 
 uint64_t kc_kernel_launches(const kc_ctx* ctx) { return ctx ? ctx->launches : 0; }

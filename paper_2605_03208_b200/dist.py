@@ -197,3 +197,17 @@ def gather_region_bitmaps(plan: Plan, local_words: torch.Tensor, perm: torch.Ten
     if perm is None:
         perm = plan.bitmap_permutation()
     return out.index_select(0, perm.to(local_words.device))
+
+
+def gather_ranges(local: torch.Tensor, counts: list, group=None) -> torch.Tensor:
+    """C2 under E2 (contiguous chunk ranges per rank, in rank order): all-gather
+    the per-rank manifests, padded to the largest count, and concatenate the
+    valid prefixes -- the global manifest."""
+    world = len(counts)
+    pad = max(1, max(counts))
+    mine = torch.zeros(pad, dtype=local.dtype, device=local.device)
+    r = dist.get_rank(group)
+    mine[:counts[r]].copy_(local[:counts[r]])
+    out = torch.empty(world * pad, dtype=local.dtype, device=local.device)
+    _all_gather_into(out, mine, group)
+    return torch.cat([out[i * pad:i * pad + counts[i]] for i in range(world)])

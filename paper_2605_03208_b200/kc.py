@@ -46,7 +46,7 @@ EXPORTED = [
     "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_validate_host_ref",
     "kc_interpose_arm", "kc_interpose_status", "kc_interpose_take", "kc_interpose_arm_seq", "kc_interpose_take_seq",
     "kc_snapshot_load", "kc_seq_load", "kc_capture_seq", "kc_seq_length", "kc_seq_step", "kc_seq_deps", "kc_seq_save", "kc_seq_free", "kc_replay_seq",
-    "kc_report_finalize",
+    "kc_report_finalize", "kc_peer_export", "kc_peer_import", "kc_peer_release",
 ]
 KC_DEP_RAW, KC_DEP_WAW, KC_DEP_WAR = 1, 2, 4
 
@@ -230,6 +230,9 @@ def lib() -> ctypes.CDLL:
         "kc_seq_free": (None, [V]),
         "kc_replay_seq": (st, [V, V, P(SeqReplayOpts), P(SeqStepReport), P(V)]),
         "kc_report_finalize": (st, [P(DiffReport), P(U64), P(I32), SZ]),
+        "kc_peer_export": (st, [V, U64, P(I32), P(U64)]),
+        "kc_peer_import": (st, [V, I32, I32, U64, U64, P(U64)]),
+        "kc_peer_release": (st, [V, U64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -488,6 +491,21 @@ class Context:
         p = ctypes.c_uint64(0)
         self._check(lib().kc_alloc(self._h, size, ctypes.byref(p)), "kc_alloc")
         return p.value
+
+    def peer_export(self, base: int) -> tuple[int, int]:
+        """kc_peer_export: (fd, mapped size) of a kc_alloc'd region, for kc_peer_import elsewhere."""
+        fd, sz = ctypes.c_int32(-1), ctypes.c_uint64(0)
+        self._check(lib().kc_peer_export(self._h, base, ctypes.byref(fd), ctypes.byref(sz)), "kc_peer_export")
+        return fd.value, sz.value
+
+    def peer_import(self, pid: int, fd: int, size: int, want_va: int = 0) -> int:
+        """kc_peer_import: map another process's exported allocation here; returns its VA."""
+        va = ctypes.c_uint64(0)
+        self._check(lib().kc_peer_import(self._h, pid, fd, size, want_va, ctypes.byref(va)), "kc_peer_import")
+        return va.value
+
+    def peer_release(self, va: int) -> None:
+        self._check(lib().kc_peer_release(self._h, va), "kc_peer_release")
 
     def free(self, dptr: int):
         self._check(lib().kc_free(self._h, dptr), "kc_free")
