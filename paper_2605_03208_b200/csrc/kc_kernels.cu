@@ -814,6 +814,7 @@ struct Acc {
     // fp32 roundings of atol / rtol (set once per launch, not by acc_zero)
     float mabs32, mrel32;
     float alo, ahi, rlo, rhi;
+    uint32_t mulp16;  // running max ULP of the 16-bit common path (merged into max_ulp at flush)
 };
 constexpr uint64_t kFlushUnits = 65536;
 
@@ -823,6 +824,7 @@ __device__ __forceinline__ void acc_zero(Acc& a) {
     a.max_rel = 0.0;
     a.any = 0;
     a.mabs32 = a.mrel32 = 0.f;
+    a.mulp16 = 0;
 }
 
 // number of nonzero bytes of x
@@ -993,6 +995,46 @@ __device__ __forceinline__ void elem16(uint32_t r, uint32_t a, Acc& acc, double 
             }
         }
     }
+}
+
+// ---- 16-bit common case, branch-free (the drain rounds of the element queue).
+// An element is handled here, with exactly elem16's result, when it is a
+// same-sign pair of finite nonzero values whose magnitudes are within a factor
+// 2^KMAX of each other (so their exponents differ by at most KMAX, 13 for f16
+// and 16 for bf16, and a - r is exact in fp32: |a - r| <= max(|a|, |r|) is an
+// integer below (2^p - 1)(2^KMAX + 1) < 2^24 times the smaller ulp, and same
+// signs cannot overflow), that differ (d != 0), whose isclose decision lies
+// outside the directed-rounding bracket, and which cannot raise the running
+// max_rel (d <= RD(mrel32 * |r|)).  Then: delems += 1, ULP = |bits(a) - bits(r)|
+// (same sign), |a - r| into the fp32 max, fail += !close.  Anything else
+// (Inf/NaN, zeros, far exponents, opposite signs, equal bits, an ambiguous
+// isclose, a max_rel candidate) returns true: the rare queue runs elem16 on it.
+template <int DT>
+__device__ __forceinline__ bool elem16_rare(uint32_t t, Acc& acc) {
+    const uint32_t hi = t >> 16, lo = t & 0xFFFFu;
+    float av, rv;
+    if constexpr (DT == KC_DT_BF16) {
+        av = __uint_as_float(t & 0xFFFF0000u);
+        rv = __uint_as_float(t << 16);
+    } else {
+        av = __half2float(__ushort_as_half((unsigned short)hi));
+        rv = __half2float(__ushort_as_half((unsigned short)lo));
+    }
+    constexpr float RATIO = DT == KC_DT_F16 ? 8192.f : 65536.f;  // 2^KMAX
+    const float d = fabsf(__fsub_rn(av, rv));
+    const float ar = fabsf(rv), aa = fabsf(av);
+    const bool close_lo = d <= __fadd_rd(acc.alo, __fmul_rd(acc.rlo, ar));
+    const bool far_hi = d > __fadd_ru(acc.ahi, __fmul_ru(acc.rhi, ar));
+    const bool common = (ar < __fmul_rn(RATIO, aa)) & (aa < __fmul_rn(RATIO, ar)) &
+                        (((t ^ (t << 16)) & 0x80000000u) == 0) & (d != 0.f) & (close_lo != far_hi) &
+                        (d <= __fmul_rd(acc.mrel32, ar));
+    if (common) {
+        acc.delems += 1;
+        acc.mulp16 = max(acc.mulp16, (uint32_t)abs((int)hi - (int)lo));
+        acc.mabs32 = fmaxf(acc.mabs32, d);
+        acc.fail += far_hi;
+    }
+    return !common;
 }
 
 template <int DT>
@@ -1199,6 +1241,21 @@ __device__ __forceinline__ void q_push16(const uint32_t (&r)[8], const uint32_t 
     }
 }
 
+// the same push as one shared-memory byte address bumped by the flag bits
+// (no serial increment/move chain per element)
+__device__ __forceinline__ void q_push16_addr(const uint32_t (&r)[8], const uint32_t (&a)[8], const uint32_t (&m)[8],
+                                              uint32_t& sa) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (m[i] & 0x00008000u)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(__byte_perm(r[i], a[i], 0x5410)) : "memory");
+        sa += (m[i] >> 13) & 4u;
+        if (m[i] & 0x80000000u)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(__byte_perm(r[i], a[i], 0x7632)) : "memory");
+        sa += (m[i] >> 29) & 4u;
+    }
+}
+
 template <int DT>
 __device__ __forceinline__ void q_item(typename QT_<DT>::T t, Acc& acc, double atol, double rtol, int equal_nan) {
     if constexpr (DT_<DT>::S == 2) {
@@ -1239,6 +1296,69 @@ __device__ __forceinline__ void q_finish(typename QT_<DT>::T* q, uint32_t& qn, A
     }
 }
 
+// 16-bit floats with the rare queue (Q2): each drain round runs the branch-free
+// common case (elem16_rare) on 32 queued elements; the elements it declines are
+// appended to a second per-warp queue (rq, < 64 entries, ballot slots) and
+// processed 32 at a time by elem16 when that queue fills.  Every element is
+// handled exactly once by exactly one of the two, so the report is unchanged.
+constexpr int kRareBytes = 64 * 4;  // rare queue per warp
+
+template <int DT>
+__device__ __forceinline__ void rq_round(uint32_t* rq, uint32_t& rn, Acc& acc, double atol, double rtol,
+                                         int equal_nan, int lane) {
+    __syncwarp();
+    const uint32_t t = rq[lane];
+    elem16<DT>(t & 0xFFFFu, t >> 16, acc, atol, rtol, equal_nan);
+    const uint32_t left = rn - 32;
+    uint32_t u = 0;
+    if (lane < left) u = rq[32 + lane];
+    __syncwarp();
+    if (lane < left) rq[lane] = u;
+    __syncwarp();
+    rn = left;
+}
+
+template <int DT>
+__device__ __forceinline__ void q_drain16(uint32_t* q, uint32_t& qn, uint32_t* rq, uint32_t& rn, Acc& acc,
+                                          double atol, double rtol, int equal_nan, int lane) {
+    __syncwarp();
+    const uint32_t full = qn & ~31u, rem = qn - full;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t i = lane; i < full; i += 32) {
+        const uint32_t t = q[i];
+        const uint32_t x = (t ^ (t >> 16)) & 0xFFFFu;  // bytes differ: every queued element is counted here
+        acc.dbytes += (uint32_t)((x & 0xFFu) != 0) + (uint32_t)(x > 0xFFu);
+        const bool rare = elem16_rare<DT>(t, acc);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, rare);
+        if (rare) rq[rn + __popc(bal & lt)] = t;
+        rn += __popc(bal);
+        if (rn >= 32) rq_round<DT>(rq, rn, acc, atol, rtol, equal_nan, lane);
+    }
+    uint32_t t = 0;
+    if (lane < rem) t = q[full + lane];
+    __syncwarp();
+    if (lane < rem) q[lane] = t;
+    __syncwarp();
+    qn = rem;
+}
+
+// everything left in both queues (before a report flush)
+template <int DT>
+__device__ __forceinline__ void q_finish16(uint32_t* q, uint32_t& qn, uint32_t* rq, uint32_t& rn, Acc& acc,
+                                           double atol, double rtol, int equal_nan, int lane) {
+    if (qn) {
+        __syncwarp();
+        if (lane < qn) q_item<DT>(q[lane], acc, atol, rtol, equal_nan);
+        qn = 0;
+    }
+    if (rn) {
+        __syncwarp();
+        if (lane < rn) elem16<DT>(rq[lane] & 0xFFFFu, rq[lane] >> 16, acc, atol, rtol, equal_nan);
+        rn = 0;
+    }
+    __syncwarp();
+}
+
 // scalar path: one element at byte offset o (element-size aligned within the buffer)
 template <int DT>
 __device__ __forceinline__ void elem_scalar(const uint8_t* R, const uint8_t* A, Acc& acc, double atol, double rtol,
@@ -1277,15 +1397,60 @@ __device__ __forceinline__ void ld256(const void* p, uint32_t* w) {
 
 // one unit [off, off+len) of a segment, whole warp: U vectors of each stream
 // in flight per lane; the per-element path runs once per vector that needs it.
-template <int DT, int U>
+template <int DT, int U, int Q2>
 __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, uint32_t len, bool vec_ok, Acc& acc,
                                           double atol, double rtol, int equal_nan, int lane,
-                                          typename QT_<DT>::T* q, uint32_t& qn) {
+                                          typename QT_<DT>::T* q, uint32_t& qn, uint32_t* rq, uint32_t& rn) {
     constexpr int S = DT_<DT>::S;
     uint32_t done = 0;
     if (vec_ok) {
         const uint32_t nvec = len / 32;
         uint32_t v = lane;
+        if constexpr (DT_<DT>::F && S == 2 && !kGenericScan16 && Q2) {
+            // 16-bit floats, software-pipelined: step k+1's vectors are loaded into
+            // the registers step k's push has just finished with, BEFORE step k's
+            // queue drain, so the drain's ALU work covers the load latency (ncu:
+            // the first use of each step's loads was the top stall, ~27% of samples)
+            const uint32_t nsteps = nvec / (32 * U);  // warp-uniform
+            if (nsteps) {
+                uint32_t rw[U][8], aw[U][8];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    ld256(R + 32 * (size_t)(v + 32 * u), rw[u]);
+                    ld256(A + 32 * (size_t)(v + 32 * u), aw[u]);
+                }
+                for (uint32_t k = 0; k < nsteps; ++k) {
+                    uint32_t mw[U][8];
+                    uint32_t any = 0, cnt128 = 0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) any |= vec_scan16<DT>(rw[u], aw[u], mw[u], cnt128, acc);
+                    const bool push = __any_sync(0xFFFFFFFFu, any != 0);
+                    if (push) {
+                        const uint32_t c = cnt128 >> 7;
+                        uint32_t incl = c;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                            if (lane >= d) incl += t;
+                        }
+                        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                        uint32_t sa = (uint32_t)__cvta_generic_to_shared(q) + 4 * (qn + incl - c);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) q_push16_addr(rw[u], aw[u], mw[u], sa);
+                        qn += total;
+                    }
+                    v += 32 * U;
+                    if (k + 1 < nsteps) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            ld256(R + 32 * (size_t)(v + 32 * u), rw[u]);
+                            ld256(A + 32 * (size_t)(v + 32 * u), aw[u]);
+                        }
+                    }
+                    if (qn >= 32) q_drain16<DT>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
+                }
+            }
+        }
         // every lane runs the same number of U-steps (nvec is warp-uniform), so
         // the warp-wide queue operations below see all 32 lanes
         for (; v - lane + 32 * U <= nvec; v += 32 * U) {
@@ -1310,10 +1475,18 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
                     }
                     const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
                     uint32_t pos = qn + incl - c;
+                    if constexpr (Q2) {
+                        uint32_t sa = (uint32_t)__cvta_generic_to_shared(q) + 4 * pos;
 #pragma unroll
-                    for (int u = 0; u < U; ++u) q_push16<DT>(rw[u], aw[u], mw[u], q, pos);
-                    qn += total;
-                    if (qn >= 32) q_drain<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+                        for (int u = 0; u < U; ++u) q_push16_addr(rw[u], aw[u], mw[u], sa);
+                        qn += total;
+                        if (qn >= 32) q_drain16<DT>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) q_push16<DT>(rw[u], aw[u], mw[u], q, pos);
+                        qn += total;
+                        if (qn >= 32) q_drain<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+                    }
                 }
                 continue;
             }
@@ -1396,6 +1569,7 @@ __device__ __forceinline__ unsigned long long warp_maxu(unsigned long long v) {
 __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
     const unsigned FULL = 0xFFFFFFFFu;
     acc.max_abs = fmax(acc.max_abs, (double)acc.mabs32);  // both exact values
+    if (acc.mulp16 > acc.max_ulp) acc.max_ulp = acc.mulp16;
     const unsigned long long mabs = (unsigned long long)__double_as_longlong(acc.max_abs);
     const unsigned long long mrel = (unsigned long long)__double_as_longlong(acc.max_rel);
     // one ballot per field: only fields nonzero somewhere in the warp are reduced
@@ -1442,7 +1616,16 @@ __device__ void acc_flush(Acc& acc, kc_diff_report* rep, int lane) {
 // every unit a segment change, 1 MiB x 10k pairs 7.0 -> 6.2 TB/s).
 // KC_K2_BLOCKED=0/1 forces either (measurement knob).  Filtered (K5 ran
 // first): a unit whose chunk is clean is skipped without reading it.
-template <int DT, int THREADS, int MINB, int VU>
+template <int DT, int U, int Q2>
+__device__ __forceinline__ void q_fin(typename QT_<DT>::T* q, uint32_t& qn, uint32_t* rq, uint32_t& rn, Acc& acc,
+                                      double atol, double rtol, int equal_nan, int lane) {
+    if constexpr (DT_<DT>::F && DT_<DT>::S == 2 && Q2 && !kGenericScan16)
+        q_finish16<DT>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
+    else
+        q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+}
+
+template <int DT, int THREADS, int MINB, int VU, int Q2>
 __global__ void __launch_bounds__(THREADS, MINB)
     k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
             kc_diff_report* __restrict__ reps, unsigned long long* __restrict__ bitmaps, double atol, double rtol,
@@ -1477,6 +1660,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
     typename QT_<DT>::T* q =
         reinterpret_cast<typename QT_<DT>::T*>(k2_smem + (size_t)(threadIdx.x >> 5) * KQ<DT, VU>::kBytes);
     uint32_t qn = 0;  // warp-uniform queue length
+    uint32_t* rq = reinterpret_cast<uint32_t*>(k2_smem + (size_t)(THREADS / 32) * KQ<DT, VU>::kBytes +
+                                               (size_t)(threadIdx.x >> 5) * kRareBytes);
+    uint32_t rn = 0;  // warp-uniform rare-queue length (16-bit floats, Q2)
     uint64_t since_flush = 0;
     for (uint64_t b = w; b < nblk; b += W)
     for (uint64_t u = unit0 + b * B, ue = min(unit0 + (b + 1) * B, unit0 + U); u < ue; ++u) {
@@ -1484,7 +1670,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             // leaving segment s: flush what this warp accumulated for it, then
             // jump (binary search) to u's segment -- with units W apart a warp
             // can pass thousands of small segments it never touches
-            q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+            q_fin<DT, VU, Q2>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
             acc_flush(acc, reps + segs[s].report, lane);
             ++s;  // contiguous blocks: the next segment
             if (s + 1 < nseg && segs[s + 1].unit_off <= u) {
@@ -1508,18 +1694,18 @@ __global__ void __launch_bounds__(THREADS, MINB)
         const uint8_t* A = reinterpret_cast<const uint8_t*>(sg.act) + off;
         const bool vec_ok = ((sg.ref | sg.act) & 31) == 0;
         acc.any = 0;
-        diff_unit<DT, VU>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane, q, qn);
+        diff_unit<DT, VU, Q2>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane, q, qn, rq, rn);
         if (__any_sync(0xFFFFFFFFu, acc.any) && lane == 0 && bitmaps) {
             const uint64_t k = sg.bitmap_chunk0 + off / kChunk;
             atomicOr(bitmaps + sg.bitmap_word0 + k / 64, 1ULL << (k % 64));
         }
         if (++since_flush == kFlushUnits) {  // keeps the 32-bit lane counters in range
             since_flush = 0;
-            q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+            q_fin<DT, VU, Q2>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
             acc_flush(acc, reps + s_rep, lane);
         }
     }
-    q_finish<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
+    q_fin<DT, VU, Q2>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
     acc_flush(acc, reps + segs[s].report, lane);
 }
 
@@ -1732,20 +1918,20 @@ static int k2_blocked(const DiffGroup& G) {
     return G.n_units < 256 * (uint64_t)G.n_segs;  // average segment < 4 MiB
 }
 
-template <int DT, int THREADS, int MINB, int U>
+template <int DT, int THREADS, int MINB, int U, int Q2 = 1>
 static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps,
                           unsigned long long* bm, double atol, double rtol, int equal_nan, int num_sms,
                           cudaStream_t s, const unsigned long long* filter) {
     constexpr int WPB = THREADS / 32;
     uint64_t grid = (G.n_units + WPB - 1) / WPB;
     if (grid > (uint64_t)num_sms * MINB) grid = (uint64_t)num_sms * MINB;
-    const int smem = DT_<DT>::F ? WPB * KQ<DT, U>::kBytes : 0;
+    constexpr int smem = DT_<DT>::F ? WPB * (KQ<DT, U>::kBytes + (DT_<DT>::S == 2 ? kRareBytes : 0)) : 0;
     static bool attr = [] {
-        return cudaFuncSetAttribute(k2_diff<DT, THREADS, MINB, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    DT_<DT>::F ? WPB * KQ<DT, U>::kBytes : 0) == cudaSuccess;
+        return cudaFuncSetAttribute(k2_diff<DT, THREADS, MINB, U, Q2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem) == cudaSuccess;
     }();
     (void)attr;
-    k2_diff<DT, THREADS, MINB, U><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
+    k2_diff<DT, THREADS, MINB, U, Q2><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
                                                                          d_reps, bm, atol, rtol, equal_nan, filter,
                                                                          k2_blocked(G));
 }
@@ -1760,7 +1946,18 @@ template <int DT>
 static void launch_k2(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps, unsigned long long* bm,
                       double atol, double rtol, int equal_nan, int num_sms, cudaStream_t s,
                       const unsigned long long* filter) {
-    launch_k2_cfg<DT, 512, 1, 2>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
+    if constexpr (DT_<DT>::F && DT_<DT>::S == 2) {
+        // KC_K2_Q2=0: the round-1 16-bit element path (A/B measurement knob)
+        static const int q2 = [] {
+            const char* e = getenv("KC_K2_Q2");
+            return e && *e ? atoi(e) : 1;
+        }();
+        if (!q2) {
+            launch_k2_cfg<DT, 512, 1, 2, 0>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
+            return;
+        }
+    }
+    launch_k2_cfg<DT, 512, 1, 2, 1>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
 }
 
 cudaError_t launch_diff(const SegDev* d_segs, const DiffGroup* groups, int ngroups, const ReportMeta* d_meta,
