@@ -107,6 +107,7 @@ class Pool:
         import torch
         import synth
         self.torch = torch
+        self.ctx = ctx
         self.placement = placement
         specs = synth.c4_specs()
         owner = synth.c4_placement(specs, world) if placement == "e1" else [0] * len(specs)
@@ -271,6 +272,17 @@ class Pool:
             word0.append(acc)
             acc += ((n + 65535) // 65536 + 63) // 64
         return out, sizes, word0, acc
+
+
+def workload_config(world: int) -> dict:
+    """The `config` both arms print (the reference arm times a bounded sample of it)."""
+    import synth
+    return {"workload": "c4: vLLM-style MoE weight pool, 30,074,000,000 B, 185 regions, E1 placement",
+            "step": "K1 pre-manifest + F3 dispatch + K1 post-manifest + K3 written set + K2 pool-pair validate"
+                    + (" + NCCL combine" if world > 1 else ""),
+            "alg_bytes_per_step": 4 * synth.C4_TOTAL, "pool_bytes": synth.C4_TOTAL, "regions": 185,
+            "l2": "inputs (30 GB) >> L2 (126 MB); no flush needed",
+            "parallelism": f"E1 residency-first shards over {world} GPU(s)"}
 
 
 def run_ours(a, rank, world, device, log):
@@ -481,7 +493,7 @@ def run_ours(a, rank, world, device, log):
         e2e_host_ref = run_e2e_host_ref(a, ctx, pool, stream, world, log, pre, post, dig, wbm, wcnt, C, nreg)
         torch.cuda.synchronize()
         torch._C._host_emptyCache()   # pinned e2e staging back to the OS
-        e2e = run_e2e(a, ctx, pool, step, stream, world, log, reps)
+        e2e = run_e2e(a, ctx, pool, stream, world, log, pre, post, dig, wbm, wcnt, C, nreg)
         torch.cuda.synchronize()
         torch._C._host_emptyCache()
     lat = None
@@ -491,18 +503,30 @@ def run_ours(a, rank, world, device, log):
         except Exception as ex:  # reported, never hidden
             lat = {"error": repr(ex)[:300]}
 
+    # PCIe roofline (A5 D2H capture, A6 H2D restore, the e2e H2D): rates over the in-run
+    # measured pinned peak (best of 5 x 1 GiB) and the 64 GB/s Gen5 x16 spec
+    pcie = None
+    if lat and "host_pinned" in lat and "pcie" in lat["host_pinned"]:
+        pk = lat["host_pinned"]["pcie"]
+
+        def prow(gbs, peak_key):
+            return {"achieved": gbs, "peak_measured": pk[peak_key], "frac": gbs / pk[peak_key],
+                    "frac_of_spec_64": gbs / 64.0}
+        pcie = {"unit": "GB/s", "measured": pk,
+                "d2h_capture_host_pinned": prow(lat["host_pinned"]["copy_out_gbs"], "d2h_gbs"),
+                "h2d_restore_host_pinned": prow(lat["host_pinned"]["copy_in_gbs"], "h2d_gbs")}
+        if e2e:
+            pcie["h2d_e2e_byte_exact"] = prow(e2e["h2d_gbs"], "h2d_gbs")
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded; bf16 N(0,0.02) expert weights, bf16 misc, device-pointer tables)",
-        "config": {"workload": "c4: vLLM-style MoE weight pool, 30,074,000,000 B, 185 regions, E1 placement",
-                   "step": "K1 pre-manifest + F3 dispatch + K1 post-manifest + K3 written set + K2 pool-pair "
-                           "validate" + (" + NCCL combine" if world > 1 else ""),
-                   "alg_bytes_per_step": int(float(alg.item())), "regions_this_rank": len(pool.regions),
-                   "bytes_this_rank": pool.bytes, "l2": "inputs (30 GB) >> L2 (126 MB); no flush needed",
-                   "parallelism": f"E1 residency-first shards over {world} GPU(s)"},
+        "config": workload_config(world),
+        "shard": {"regions_this_rank": len(pool.regions), "bytes_this_rank": pool.bytes,
+                  "alg_bytes_per_step_all_ranks": int(float(alg.item()))},
         "roofline": roof, "kernels": kern, "clocks": clk, "gpu_launches": launches,
-        "e2e": e2e, "e2e_host_ref": e2e_host_ref, "capture_replay": lat, "fingerprint": fingerprint, "fused_step": fused,
+        "e2e": e2e, "e2e_host_ref": e2e_host_ref, "capture_replay": lat, "pcie": pcie, "fingerprint": fingerprint,
+        "fused_step": fused,
     }
     return res, pool
 
@@ -633,10 +657,14 @@ def run_e2e_host_ref(a, ctx, pool, stream, world, log, pre, post, dig, wbm, wcnt
                     "headline e2e; `e2e` copies every reference byte and compares all of them"}
 
 
-def run_e2e(a, ctx, pool, step, stream, world, log, reps):
-    """Same metric through the public API with the snapshot in pinned HOST memory:
-    every step copies the snapshot host->device (restore) before the device hot
-    path and reads the reports back."""
+def run_e2e(a, ctx, pool, stream, world, log, pre, post, dig, wbm, wcnt, C, nreg):
+    """The metric end to end through the public C ABI with the captured snapshot in
+    pinned HOST memory (what kc_capture_host leaves behind): every step runs the K1
+    pre-manifest, the F3 dispatch, kc_validate_host_ref in BYTE-EXACT mode (every
+    reference byte crosses PCIe through the library's 3 x 256 MiB staging ring on its
+    copy stream, K2 diffs each piece as it lands, K1 gives the post-manifest; the
+    reports and bitmaps come back to the host) and K3.  Same algorithmic work as
+    the device step (2 hashes of N, a diff reading 2N) plus N bytes host->device."""
     import torch
     import synth
     host = {}
@@ -645,8 +673,23 @@ def run_e2e(a, ctx, pool, step, stream, world, log, reps):
         h.copy_(synth.dev_view(pool.ref[s.name], s.size, torch.cuda.current_device()))
         host[s.name] = h
     torch.cuda.synchronize()
-    steps = max(1, min(a.steps, a.e2e_steps))
-    out = torch.empty(reps.numel(), dtype=torch.int64, pin_memory=True)
+    hbufs = [(host[s.name].data_ptr(), pool.va[s.name], s.size, s.dtype) for s in pool.specs]
+    sh = stream.cuda_stream
+    out = {}
+
+    def step():
+        ctx.hash(pool.regions, pre.data_ptr(), dig.data_ptr(), dig.data_ptr() + 8 * nreg if world == 1 else 0,
+                 stream=sh)
+        pool.launch_f3(sh)
+        reps, bms, moved = ctx.validate_host_ref(hbufs, 0, d_act_manifest=post.data_ptr(), stream=sh)
+        ctx.written(pre.data_ptr(), post.data_ptr(), C, wbm.data_ptr(), wcnt.data_ptr(), stream=sh)
+        out["reps"], out["moved"], out["bm_words"] = reps, moved, sum(len(b) for b in bms)
+    step()   # warm-up: plan caches, the staging ring, its events
+    torch.cuda.synchronize()
+    diffs = sum(r["differing_bytes"] for r in out["reps"])
+    ok = diffs == pool.n_plants if pool.n_plants else all(r["differing_bytes"] == 0 and r["pass"] == 1
+                                                          for r in out["reps"])
+    steps = max(1, a.e2e_steps)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -654,13 +697,10 @@ def run_e2e(a, ctx, pool, step, stream, world, log, reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
-        for s in pool.specs:
-            synth.dev_view(pool.ref[s.name], s.size, torch.cuda.current_device()).copy_(host[s.name],
-                                                                                         non_blocking=True)
-        step(None)
-        out.copy_(reps, non_blocking=True)  # the step's result: every validation report
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
     ms = e0.elapsed_time(e1) / steps
     tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -668,9 +708,15 @@ def run_e2e(a, ctx, pool, step, stream, world, log, reps):
     ms = float(tm.item())
     host.clear()
     total = 4 * pool.total_bytes
-    return {"value": total / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": pool.total_bytes,
-            "d2h_bytes_per_step": 8 * reps.numel(), "ms_per_step": ms, "steps": steps,
-            "h2d_gbs": pool.total_bytes / world / (ms * 1e-3) / 1e9}
+    d2h = 120 * len(hbufs) + 8 * out["bm_words"]
+    log(f"e2e (byte-exact kc_validate_host_ref): {ms:.2f} ms/step, h2d {out['moved'] / 1e9:.2f} GB/step "
+        f"({out['moved'] / (ms * 1e-3) / 1e9:.1f} GB/s), validated {ok}")
+    return {"value": total / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": out["moved"],
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "wall_ms_per_step": 1e3 * wall, "steps": steps,
+            "h2d_gbs": out["moved"] / (ms * 1e-3) / 1e9, "validated_bit_exact": bool(ok),
+            "path": "kc_hash (pre) + F3 dispatch + kc_validate_host_ref(ref_manifest=NULL: byte-exact, every "
+                    "reference byte H2D through the library's staging ring overlapped with K2; K1 post-manifest) "
+                    "+ kc_written; reports and bitmaps read back every step"}
 
 
 def run_latency(a, ctx, pool, log):
@@ -935,79 +981,134 @@ def pcie_peak(log, nbytes: int = 1 << 30, reps: int = 5) -> dict:
     return out
 
 
-# ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
-def oracle_sample(pool_or_none, sample_mb: int):
-    """A bounded sample of the c4 workload as host bytes: real pool regions (copied
-    back) when a pool exists, else regenerated on the host with the same recipes."""
-    import numpy as np
+# ------------------------------------------------------------------ BASELINE.json configs c1, c2, c3, c5
+def run_configs(a, ctx, log, peak):
+    """Per-config GPU numbers (kc_* calls, CUDA events, L2 flushed) beside the oracle's
+    CPU rates on a bounded sample of each config's bytes (bench_configs.py)."""
+    import torch
+    import bench_configs as bc
     import synth
-    specs = synth.c4_specs()
-    chosen, total = [], 0
-    for s in sorted(specs, key=lambda s: s.size):
-        if s.name in ("x", "topk", "y") or total + s.size > sample_mb * 2**20:
-            continue
-        chosen.append(s)
-        total += s.size
-    # add a slice of one expert stack so the sample mixes big and small regions
-    out = []
-    rng = np.random.default_rng(synth.seed(4, 999))
-    for s in chosen:
-        if pool_or_none is not None and s.name in pool_or_none.ref:
-            v = synth.dev_view(pool_or_none.ref[s.name], s.size).cpu().numpy()
-        elif s.fill == "zero":
-            v = np.zeros(s.size, dtype=np.uint8)
-        else:
-            v = (rng.standard_normal(s.size // 2).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
-            v = v.view(np.uint8)
-        out.append((s, v))
+    timer = bc.Timer(torch, a.config_iters)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    osec = a.config_oracle_seconds
+    out = {}
+    t_all = time.perf_counter()
+
+    def fill_c1(vas):
+        for spec, arr in zip(synth.C1_SPECS, synth.c1_fill(vas["nodes"])):
+            synth.dev_view(vas[spec.name], arr.size).copy_(torch.from_numpy(arr))
+    res, pairs, live = bc.closure(
+        torch, ctx, timer, synth.C1_SPECS, fill_c1,
+        lambda v: dict(image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
+                       kernarg=synth.c1_kernarg(v["heads"], v["out"], v["nodes"])), "c1", peak, outputs=("out",))
+    res["oracle"] = bc.oracle_both(bc.sample_pairs(torch, [(b, b, n, DTC[d]) for b, _, n, d in pairs], 1 << 20), osec)
+    live.release()
+    out["c1"] = res
+    c2s = synth.c2_specs()
+
+    def fill_c2(vas):
+        gen = torch.Generator(device="cuda").manual_seed(synth.seed(2))
+        for sp in c2s:
+            synth.fill_device(synth.dev_view(vas[sp.name], sp.size), sp, gen)
+    res, pairs, live = bc.closure(
+        torch, ctx, timer, c2s, fill_c2,
+        lambda v: dict(image=image, mangled="kc_fixture_decode_attn", grid=(32, 1, 1), block=(128, 1, 1),
+                       kernarg=synth.c2_kernarg(v)), "c2", peak, host=True, outputs=("attn_out",))
+    res["oracle"] = bc.oracle_both(bc.sample_pairs(torch, [(b, b, n, DTC[d]) for b, _, n, d in pairs], 64 << 20),
+                                   osec)
+    live.release()
+    out["c2"] = res
+    for kind in ("f16", "bf16"):
+        res, pairs, keep = bc.c3(torch, ctx, timer, kind, peak)
+        res["oracle"] = bc.oracle_both(bc.sample_pairs(torch, pairs[3:] + pairs[:3], 64 << 20), osec)
+        del keep
+        torch.cuda.empty_cache()
+        out[f"c3_{kind}"] = res
+    cells = []
+    g = torch.Generator(device="cuda").manual_seed(synth.seed(5))
+    for S, n in bc.C5_BENCH_CELLS:
+        res, pairs, keep = bc.c5_cell(torch, ctx, timer, S, n, peak, g)
+        res["oracle_all_cores"] = bc.oracle_rates(bc.sample_pairs(torch, pairs, 32 << 20), os.cpu_count() or 1,
+                                                  osec / 2)
+        del keep
+        torch.cuda.empty_cache()
+        cells.append(res)
+    out["c5"] = cells
+    out["method"] = (f"GPU: CUDA events around each kc_* call, best of {a.config_iters} after one warm-up call, "
+                     "L2 flushed (512 MiB write) before each; closure stages wall-clock around each call. Oracle: "
+                     "oracle/ as it stands on a bounded sample of the config's bytes copied back from the device, "
+                     "1 thread (first 32 MiB) and every host core")
+    out["seconds"] = time.perf_counter() - t_all
+    k = out
+    log("configs: c2 K1 {:.0f} GB/s ({:.2f}); c3 f16 K2 {:.0f} GB/s ({:.2f}), bf16 K2 {:.0f} GB/s ({:.2f}); "
+        "{:.1f} s".format(k["c2"]["K1"]["gbs"], k["c2"]["K1"]["frac"], k["c3_f16"]["K2"]["gbs"],
+                          k["c3_f16"]["K2"]["frac"], k["c3_bf16"]["K2"]["gbs"], k["c3_bf16"]["K2"]["frac"],
+                          out["seconds"]))
     return out
 
 
-def time_oracle(sample, threads: int, min_seconds: float = 0.0):
-    """The oracle as it stands on the host cores: per pass, two manifests (A2, A4)
-    and the diff of every sampled region against its reference copy (A8); passes
-    repeat until min_seconds of work.  Returns (GB/s in the metric's unit, s, bytes)."""
-    import oracle
-    from concurrent.futures import ThreadPoolExecutor
-    oracle.build()
-    dts = {"bf16": oracle.DT_BF16, "u64": oracle.DT_U64, "i32": oracle.DT_I32, "f32": oracle.DT_F32}
-    refs = [(s, v, v.copy()) for s, v in sample]
-    nbytes = sum(v.size for _, v in sample)
-    passes = 0
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        while True:
-            list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), refs))
-            list(ex.map(lambda sv: oracle.chunk_hashes(sv[1]), refs))
-            list(ex.map(lambda sv: oracle.diff(sv[2], sv[1], dts.get(sv[0].dtype, oracle.DT_BYTES)), refs))
-            passes += 1
-            if time.perf_counter() - t0 >= min_seconds:
-                break
-    dt = time.perf_counter() - t0
-    return 4 * nbytes * passes / dt / 1e9, dt, nbytes * passes
+# oracle dtype codes by the synth dtype names (the kc_dtype numbering)
+DTC = {"bytes": 0, "u8": 1, "i8": 2, "u16": 3, "i16": 4, "u32": 5, "i32": 6, "u64": 7, "i64": 8, "f16": 9,
+       "bf16": 10, "f32": 11, "f64": 12}
+
+
+# ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
+def c4_sample(pool_or_none, sample_mb: int):
+    """A bounded, stratified sample of the c4 workload: the head (whole 64 KiB chunks) of
+    EVERY region, sized so the sample is about sample_mb, as (ref, act, dtype) host pairs.
+    With a pool: this run's reference bytes copied back (the pool pair is bit-identical,
+    so act = ref).  Without (the reference arm, no GPU): regenerated on the host with the
+    c4 recipes (bf16 N(0, 0.02) experts, bf16 misc, 10% zero misc, u64 pointer tables)."""
+    import numpy as np
+    import synth
+    specs = synth.c4_specs()
+    per = max(65536, (sample_mb * 2**20 // len(specs)) // 65536 * 65536)
+    rng = np.random.default_rng(synth.seed(4, 999))
+    out = []
+    for s in specs:
+        k = min(s.size, per)
+        if pool_or_none is not None and s.name in pool_or_none.ref:
+            v = synth.dev_view(pool_or_none.ref[s.name], k).cpu().numpy().copy()
+        elif s.fill == "zero":
+            v = np.zeros(k, dtype=np.uint8)
+        elif s.fill in ("ptr_table", "topk"):
+            v = rng.integers(0, 2**63, size=k // 8, dtype=np.uint64).view(np.uint8)
+        else:
+            std = s.params.get("std", 1.0)
+            v = ((rng.standard_normal(k // 2).astype(np.float32) * np.float32(std)).view(np.uint32) >> 16)
+            v = v.astype(np.uint16).view(np.uint8)
+        out.append((v, v.copy(), DTC.get(s.dtype, 0)))
+    return out
 
 
 def run_reference(a, rank, world):
+    """The reference arm: the CPU oracle as it stands, on every host core, timing the
+    metric's step mix (2 manifests of N + the O4 diff reading 2N) over a bounded sample
+    of the c4 workload per step; same config/metric/unit as our arm."""
     if rank != 0:
         return None
+    import bench_configs as bc
     threads = os.cpu_count() or 1
-    sample = oracle_sample(None, a.cpu_sample_mb)
+    sample = c4_sample(None, a.cpu_sample_mb)
+    nb = sum(v.size for v, _, _ in sample)
     for _ in range(min(a.warmup, 1)):
-        time_oracle(sample[:2], threads)
-    vals, secs = [], 0.0
+        bc.oracle_rates(sample[:4], threads, 0.0)
+    steps = []
     for _ in range(a.steps):
-        v, dt, nb = time_oracle(sample, threads, a.ref_step_seconds)
-        vals.append(v)
-        secs += dt
-    value = sum(vals) / len(vals)
-    desc = (f"{len(sample)} smallest c4 regions ({sum(v.size for _, v in sample) / 1e6:.1f} MB, regenerated on the "
-            f"host with the c4 recipes), repeated for >= {a.ref_step_seconds:.0f} s per step: 2 oracle manifests + "
-            f"oracle diff of each region vs its reference per pass")
+        r = bc.oracle_rates(sample, threads, a.ref_step_seconds / 2)
+        steps.append(r)
+    secs = sum(r["hash_s"] + r["diff_s"] for r in steps)
+    value = sum(r["step_mix_gbs"] for r in steps) / len(steps)
+    desc = (f"the first {nb // 185 // 1024} KiB of every one of the 185 c4 regions ({nb / 1e6:.1f} MB, regenerated "
+            f"on the host with the c4 recipes); per step: O2 manifests repeated >= {a.ref_step_seconds / 2:.1f} s, "
+            f"the O4 diff repeated >= {a.ref_step_seconds / 2:.1f} s; value = 4N / (2N/hash + 2N/diff)")
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "c4 sample (bounded) on host cores", "threads": threads},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": workload_config(world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+                             "hash_gbs": sum(r["hash_gbs"] for r in steps) / len(steps),
+                             "diff_gbs": sum(r["diff_gbs"] for r in steps) / len(steps),
+                             "host": bc.host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -1019,9 +1120,9 @@ def main():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-fused", action="store_true", help="skip the F2 fused-step measurement")
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--cpu-sample-mb", type=int, default=384)
-    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--ref-step-seconds", type=float, default=5.0)
     p.add_argument("--no-latency", action="store_true")
     p.add_argument("--latency-dir", default="/dev/shm/kc_bench_capture")
@@ -1030,6 +1131,9 @@ def main():
                    help="plant 1-byte mismatches in the reference pool (deterministic by region, so the N-GPU "
                         "reports and bitmaps can be compared with the 1-GPU ones); never a headline number")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-configs", action="store_true", help="skip the c1/c2/c3/c5 per-config measurements")
+    p.add_argument("--config-iters", type=int, default=5)
+    p.add_argument("--config-oracle-seconds", type=float, default=1.0)
     p.add_argument("--placement", default="e1", choices=["e1", "e2"],
                    help="e1: residency-first shards (each rank reads its own HBM; the headline); e2: the pool "
                         "resident on rank 0, every rank reading a 1/N share of it over NVLink peer mappings "
@@ -1080,23 +1184,32 @@ def main():
         a.placement = "e1"   # one rank: the pool is resident and local either way
     res, pool = run_ours(a, rank, world, device, log)
     if world > 1:
-        res["config"]["collectives"] = {"backend": torch.distributed.get_backend(),
+        res["collectives"] = {"backend": torch.distributed.get_backend(),
                                         "nccl": ".".join(map(str, torch.cuda.nccl.version())),
                                         "step": "C2 all_gather manifests, C3 all_reduce SUM/MAX reports, "
                                                 "C4 all_gather per-region bitmaps"}
     if os.environ.get("KC_BENCH_ONE_GPU") and world > 1:
-        res["config"]["functional_check_only"] = "all ranks on cuda:0 (KC_BENCH_ONE_GPU)"
+        res["functional_check_only"] = "all ranks on cuda:0 (KC_BENCH_ONE_GPU)"
     if a.plant:
-        res["config"]["planted"] = "reference pool planted with 1-byte mismatches (--plant): a parity run"
+        res["planted"] = "reference pool planted with 1-byte mismatches (--plant): a parity run"
+    if rank == 0 and world == 1 and not a.no_configs:
+        res["configs"] = run_configs(a, pool.ctx, log, res["roofline"]["peak"])
     if rank == 0 and not a.no_cpu_baseline:
+        import bench_configs as bc
         threads = os.cpu_count() or 1
-        sample = oracle_sample(pool, a.cpu_sample_mb)
-        v, dt, nb = time_oracle(sample, threads, a.cpu_seconds)
-        res["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                               "sample": f"{len(sample)} smallest regions of this run's c4 pool "
-                                         f"({sum(x.size for _, x in sample) / 1e6:.1f} MB) repeated to "
-                                         f"{nb / 1e9:.2f} GB: 2 oracle manifests + oracle diff per pass; "
-                                         f"{dt:.1f} s on {threads} threads"}
+        sample = c4_sample(pool, a.cpu_sample_mb)
+        nb = sum(v.size for v, _, _ in sample)
+        rates = bc.oracle_both(sample, a.cpu_seconds / 4, threads)
+        res["cpu_baseline"] = {"value": rates["all_cores"]["step_mix_gbs"], "unit": UNIT, "cores": threads,
+                               "kind": "oracle",
+                               "sample": f"this run's c4 pool: the first {nb // 185 // 1024} KiB of every one of "
+                                         f"the 185 regions ({nb / 1e6:.1f} MB, copied back from HBM); O2 manifests "
+                                         f"and the O4 diff each repeated >= {a.cpu_seconds / 4:.1f} s at 1 thread "
+                                         f"(first 32 MiB) and at {threads} threads; value = the metric's step mix "
+                                         f"4N / (2N/hash + 2N/diff) at {threads} threads",
+                               "hash_gbs": {"t1": rates["t1"]["hash_gbs"], "all_cores": rates["all_cores"]["hash_gbs"]},
+                               "diff_gbs": {"t1": rates["t1"]["diff_gbs"], "all_cores": rates["all_cores"]["diff_gbs"]},
+                               "step_mix_gbs_t1": rates["t1"]["step_mix_gbs"], "host": bc.host_info()}
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

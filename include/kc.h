@@ -275,7 +275,14 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
  * d_act_manifest: optional device output of act's chunk hashes; *h2d_bytes:
  * bytes moved host->device (manifest + reference chunks).  Device scratch: 8 B
  * per chunk (manifest) plus 64 KiB per chunk whose hash differs (the staged
- * reference bytes); KC_ERR_NOMEM if that does not fit. */
+ * reference bytes); KC_ERR_NOMEM if that does not fit.
+ * ref_manifest == NULL selects BYTE-EXACT mode (the paper's strict compare,
+ * PAPER.md:1120-1126, with no hash trusted): every reference byte crosses
+ * PCIe, streamed through a 3 x 256 MiB device staging ring on the context's
+ * copy stream while K2 diffs the previous piece on `stream`; *h2d_bytes = the
+ * total reference bytes; d_act_manifest (optional) is then filled by K1 over
+ * the act buffers in order.  Reports and bitmaps equal kc_diff's over the same
+ * (reference, actual) pairs.  Blocks until the reports are on the host. */
 kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const uint64_t* ref_manifest,
                                const kc_tolerance* tol, kc_diff_report* reps, uint64_t* h_bitmaps,
                                uint64_t* d_act_manifest, uint64_t* h2d_bytes, void* stream);

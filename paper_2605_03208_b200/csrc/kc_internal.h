@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys/ncu) injects
 
 #include <cstdarg>
 #include <cstdint>
@@ -84,6 +85,7 @@ struct kc_ctx {
     std::vector<void*> pinned;
     std::vector<cudaEvent_t> pin_ev;
     cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> full_ev;  // byte-exact host-reference validation: per staging slot copied / freed
     // parallel snapshot file I/O workers (stream + `depth` pinned buffers each)
     struct IoWorker {
         cudaStream_t stream = nullptr;
@@ -193,9 +195,20 @@ namespace kc {
 // driver calls made then (the library's own scratch, arenas and kernel launches
 // are not application state).  KC_ENTER and the capture/restore entry points hold one.
 extern thread_local int t_internal;
+// With a name (every C-ABI entry point passes __func__) it also spans the call
+// with an NVTX range, so a timeline tool shows each kc_* call; the stages
+// inside capture/restore are NVTX marks (trace() in kc_snapshot.cu).
 struct Internal {
-    Internal() { ++t_internal; }
-    ~Internal() { --t_internal; }
+    Internal() : named(false) { ++t_internal; }
+    explicit Internal(const char* name) : named(true) {
+        ++t_internal;
+        nvtxRangePushA(name);
+    }
+    ~Internal() {
+        if (named) nvtxRangePop();
+        --t_internal;
+    }
+    const bool named;
     Internal(const Internal&) = delete;
     Internal& operator=(const Internal&) = delete;
 };

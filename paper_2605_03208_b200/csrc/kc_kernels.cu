@@ -39,21 +39,31 @@ __device__ __forceinline__ uint64_t xround(uint64_t acc, uint64_t x) {
     return acc * P1;
 }
 
-// Same round with an explicit 32-bit schedule: acc + x*P2 as one mad.wide plus
-// two off-chain IMADs, the 64-bit rotate as two funnel shifts, *P1 as one
-// mad.wide + two IMADs (10 SASS instead of 13; the chain is what bounds K1).
-__device__ __forceinline__ uint64_t xround_fast(uint64_t acc, uint64_t x) {
-    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+// The accumulator chain in "y form".  With y = acc + x*P2 (the pre-rotation
+// sum) the round is  y' = rotl(y, 31)*P1 + x'*P2,  and the 64-bit multiply's
+// low product absorbs the next word's x'*P2 as its 64-bit addend (one
+// mad.wide.u32).  x'*P2 is off the chain, so the chain per 32-byte stripe is
+// funnel shift -> {mad.wide, 2 IMAD in parallel} -> IADD3: 3 dependent SASS
+// instead of 6 (the per-chunk latency floor that bounds sub-wave snapshots).
+// A lane starts from y0 = rotr(seed * P1^-1, 31), so that rotl(y0, 31)*P1 is
+// the XXH64 lane seed, and ends with yfinal(y) = rotl(y, 31)*P1 = the lane's
+// accumulator.  Same arithmetic mod 2^64, reordered: results are identical.
+__device__ __forceinline__ uint64_t ystep(uint64_t y, uint64_t x) {
+    const uint64_t p = x * P2;  // off the chain
+    const uint32_t yl = (uint32_t)y, yh = (uint32_t)(y >> 32);
+    const uint32_t rh = __funnelshift_l(yl, yh, 31), rl = __funnelshift_l(yh, yl, 31);
     uint64_t w;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(xl), "r"((uint32_t)P2), "l"(acc));
-    const uint32_t t = xl * (uint32_t)(P2 >> 32) + xh * (uint32_t)P2;
-    const uint32_t sl = (uint32_t)w, sh = (uint32_t)(w >> 32) + t;
-    const uint32_t rh = __funnelshift_l(sl, sh, 31), rl = __funnelshift_l(sh, sl, 31);
-    uint64_t w2;
-    asm("mul.wide.u32 %0, %1, %2;" : "=l"(w2) : "r"(rl), "r"((uint32_t)P1));
-    const uint32_t t2 = rl * (uint32_t)(P1 >> 32) + rh * (uint32_t)P1;
-    return (w2 & 0xFFFFFFFFull) | ((uint64_t)((uint32_t)(w2 >> 32) + t2) << 32);
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(rl), "r"((uint32_t)P1), "l"(p));
+    uint32_t hi;
+    asm("{\n\t.reg .u32 a, b;\n\t"
+        "mul.lo.u32 a, %1, %3;\n\t"
+        "mul.lo.u32 b, %2, %4;\n\t"
+        "add.u32 a, a, b;\n\t"
+        "add.u32 %0, a, %5;\n\t}"
+        : "=r"(hi) : "r"(rl), "r"(rh), "r"((uint32_t)(P1 >> 32)), "r"((uint32_t)P1), "r"((uint32_t)(w >> 32)));
+    return ((uint64_t)hi << 32) | (uint32_t)w;
 }
+__device__ __forceinline__ uint64_t yfinal(uint64_t y) { return ystep(y, 0); }
 
 __device__ __forceinline__ uint64_t xavalanche(uint64_t h) {
     h ^= h >> 33;
@@ -128,9 +138,10 @@ __device__ __forceinline__ uint64_t quad_finish(uint64_t v, int ql, unsigned qma
     return xavalanche(h);
 }
 
-__device__ __forceinline__ uint64_t lane_seed(int ql) {
-    // v1 = P1+P2, v2 = P2, v3 = 0, v4 = -P1 (seed 0)
-    return ql == 0 ? (P1 + P2) : (ql == 1 ? P2 : (ql == 2 ? 0ULL : (0ULL - P1)));
+__device__ __forceinline__ uint64_t lane_yseed(int ql) {
+    // y0 = rotr(v * P1^-1, 31) for the seed-0 lane seeds v1 = P1+P2, v2 = P2,
+    // v3 = 0, v4 = -P1 (P1^-1 = 0x0887493432BADB37 mod 2^64)
+    return ql == 0 ? 0x32E245F52D5533D6ULL : (ql == 1 ? 0x32E245F32D5533D6ULL : (ql == 2 ? 0ULL : ~0ULL));
 }
 
 // XXH64 of one contiguous global byte range by a quad, direct loads (16
@@ -138,7 +149,7 @@ __device__ __forceinline__ uint64_t lane_seed(int ql) {
 // manifests of up to ~84 KB serially, so load latency must not be exposed).
 template <bool ALIGNED>
 __device__ uint64_t quad_xxh64_global(const uint8_t* p, uint64_t len, int ql, unsigned qmask) {
-    uint64_t v = lane_seed(ql);
+    uint64_t v = lane_yseed(ql);  // y form
     const uint64_t nst = len >= 32 ? len / 32 : 0;
     const uint8_t* q = p + 8 * ql;
     uint64_t t = 0;
@@ -154,17 +165,17 @@ __device__ uint64_t quad_xxh64_global(const uint8_t* p, uint64_t len, int ql, un
 #pragma unroll
                 for (int u = 0; u < U; ++u) xb[u] = __ldg(g + 4 * (t + U + u));
 #pragma unroll
-                for (int u = 0; u < U; ++u) v = xround_fast(v, xa[u]);
+                for (int u = 0; u < U; ++u) v = ystep(v, xa[u]);
                 if (t + 3 * U <= nst) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) xa[u] = __ldg(g + 4 * (t + 2 * U + u));
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) v = xround_fast(v, xb[u]);
+                for (int u = 0; u < U; ++u) v = ystep(v, xb[u]);
             }
             if (t + U <= nst) {  // xa already holds batch t when fewer than 2U stripes remain
 #pragma unroll
-                for (int u = 0; u < U; ++u) v = xround_fast(v, xa[u]);
+                for (int u = 0; u < U; ++u) v = ystep(v, xa[u]);
                 t += U;
             }
         }
@@ -172,9 +183,9 @@ __device__ uint64_t quad_xxh64_global(const uint8_t* p, uint64_t len, int ql, un
     for (; t < nst; ++t) {
         const uint64_t x =
             ALIGNED ? __ldg(reinterpret_cast<const unsigned long long*>(q + 32 * t)) : ldg_u64_bytes(q + 32 * t);
-        v = xround_fast(v, x);
+        v = ystep(v, x);
     }
-    return quad_finish<ALIGNED>(v, ql, qmask, len, p + 32 * nst);
+    return quad_finish<ALIGNED>(yfinal(v), ql, qmask, len, p + 32 * nst);
 }
 
 __device__ __forceinline__ int find_region(const RegionDev* __restrict__ r, int n, uint64_t g) {
@@ -316,7 +327,7 @@ __global__ void __launch_bounds__(CFG::kThreads, 1)
     for (uint64_t g = g0; g < C; g += Q) {
         const ChunkRef cr = chunk_ref(regs, nreg, g, map);
         const uint32_t nst = cr.len >= 32 ? cr.len / 32 : 0;
-        uint64_t v = lane_seed(ql);
+        uint64_t v = lane_yseed(ql);  // y form
         uint32_t remaining = nst * 32;
         while (remaining > 0) {
             const int st = consumed % CFG::kStages;
@@ -324,11 +335,11 @@ __global__ void __launch_bounds__(CFG::kThreads, 1)
             const uint64_t* p = reinterpret_cast<const uint64_t*>(ring + st * CFG::kPitch) + ql;
             if (remaining >= (uint32_t)CFG::kSlice) {
 #pragma unroll
-                for (int t = 0; t < CFG::kSlice / 32; ++t) v = xround_fast(v, p[4 * t]);
+                for (int t = 0; t < CFG::kSlice / 32; ++t) v = ystep(v, p[4 * t]);
                 remaining -= CFG::kSlice;
             } else {
                 const uint32_t n = remaining / 32;
-                for (uint32_t t = 0; t < n; ++t) v = xround_fast(v, p[4 * t]);
+                for (uint32_t t = 0; t < n; ++t) v = ystep(v, p[4 * t]);
                 remaining = 0;
             }
             ++consumed;
@@ -338,7 +349,7 @@ __global__ void __launch_bounds__(CFG::kThreads, 1)
                 issue_next();
             }
         }
-        const uint64_t h = quad_finish<true>(v, ql, qmask, cr.len, cr.src + (size_t)nst * 32);
+        const uint64_t h = quad_finish<true>(yfinal(v), ql, qmask, cr.len, cr.src + (size_t)nst * 32);
         if (ql == 0) out[g] = h;
     }
 }
@@ -463,7 +474,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const int r = map ? (int)__ldg(map + g) : find_region(regs, nreg, g);
             cdst = dst[r] + (g - regs[r].chunk_off) * kChunk;
         }
-        uint64_t v = lane_seed(ql);
+        uint64_t v = lane_yseed(ql);  // y form
         for (uint32_t s = 0; s < nsl; ++s, ++step) {
             cp_async_wait<STAGES - 2>();
             __syncwarp();
@@ -473,9 +484,9 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
             if (n == SL / 32) {
 #pragma unroll
-                for (int t = 0; t < SL / 32; ++t) v = xround_fast(v, p[4 * t]);
+                for (int t = 0; t < SL / 32; ++t) v = ystep(v, p[4 * t]);
             } else {
-                for (uint32_t t = 0; t < n; ++t) v = xround_fast(v, p[4 * t]);
+                for (uint32_t t = 0; t < n; ++t) v = ystep(v, p[4 * t]);
             }
             if (COPY) {  // the stage's 8 slices -> the arena, before the slot is refilled
 #pragma unroll
@@ -494,13 +505,13 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             fetch((step + STAGES - 1) % STAGES);
         }
         if (g < C) {
-            const uint64_t h = quad_finish<true>(v, ql, qmask, cr.len, cr.src + (size_t)nst * 32);
+            const uint64_t h = quad_finish<true>(yfinal(v), ql, qmask, cr.len, cr.src + (size_t)nst * 32);
             if (ql == 0) out[g] = h;
             if (COPY && ql == 0)  // the sub-32-byte tail is hashed from global, copy it the same way
                 for (uint32_t b = nst * 32; b < cr.len; ++b)
                     reinterpret_cast<uint8_t*>(cdst)[b] = cr.src[b];
         } else {
-            quad_finish<true>(v, ql, qmask, 0, nullptr);
+            quad_finish<true>(yfinal(v), ql, qmask, 0, nullptr);
         }
     }
     cp_async_wait<0>();
@@ -640,7 +651,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         }
         const uint32_t nst = len >= 32 ? len / 32 : 0;
         const uint32_t nsl = __reduce_max_sync(0xFFFFFFFFu, (nst * 32 + SL - 1) / SL);
-        uint64_t v = lane_seed(ql);
+        uint64_t v = lane_yseed(ql);  // y form
         unsigned long long x = 0;
         uint32_t sp_lo = 0, sp_hi = 0;
         for (uint32_t s = 0; s < nsl; ++s, ++step) {
@@ -653,7 +664,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
             auto word = [&](int t) {
                 const uint64_t a = pa[4 * t], r = SELF ? a : pr[4 * t];
-                v = xround_fast(v, a);
+                v = ystep(v, a);
                 if (!SELF) x |= a ^ r;
                 sp_lo |= ((uint32_t)r & sm.m_lo) + sm.a_lo;
                 sp_hi |= ((uint32_t)(r >> 32) & sm.m_hi) + sm.a_hi;
@@ -670,13 +681,13 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         const bool mine = x != 0 || ((sp_lo & sm.h_lo) | (sp_hi & sm.h_hi)) != 0 || (len & 31u) != 0;
         const bool d = __ballot_sync(0xFFFFFFFFu, mine) & qmask;
         if (g < C) {
-            const uint64_t h = quad_finish<true>(v, ql, qmask, len, src + (size_t)nst * 32);
+            const uint64_t h = quad_finish<true>(yfinal(v), ql, qmask, len, src + (size_t)nst * 32);
             if (ql == 0) {
                 out[g] = h;
                 if (d) atomicOr(dirty + (g >> 6), 1ULL << (g & 63));
             }
         } else {
-            quad_finish<true>(v, ql, qmask, 0, nullptr);
+            quad_finish<true>(yfinal(v), ql, qmask, 0, nullptr);
         }
     }
     cp_async_wait<0>();
@@ -727,7 +738,7 @@ __global__ void __launch_bounds__(32)
             for (uint32_t o = 8 * lane; o < b; o += 256) cp_async8(&buf[k & 1][o], p + off + o);
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        uint64_t v = lane_seed(ql);
+        uint64_t v = lane_yseed(ql);  // y form
         if (nstage > 0) issue(0);
         for (uint32_t k = 0; k < nstage; ++k) {
             if (k + 1 < nstage) {
@@ -744,14 +755,14 @@ __global__ void __launch_bounds__(32)
                 uint32_t t = 0;
                 for (; t + 8 <= n; t += 8) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) v = xround_fast(v, q[4 * (t + u)]);
+                    for (int u = 0; u < 8; ++u) v = ystep(v, q[4 * (t + u)]);
                 }
-                for (; t < n; ++t) v = xround_fast(v, q[4 * t]);
+                for (; t < n; ++t) v = ystep(v, q[4 * t]);
             }
             __syncwarp();  // stage k & 1 is rewritten by issue(k + 2)
         }
         if (lane < 4) {
-            const uint64_t d = quad_finish<true>(v, ql, 0xFu, len, p + body);
+            const uint64_t d = quad_finish<true>(yfinal(v), ql, 0xFu, len, p + body);
             if (lane == 0) {
                 if (dig) dig[r] = d;
                 if (scratch) {
@@ -1629,7 +1640,7 @@ template <int DT, int THREADS, int MINB, int VU, int Q2>
 __global__ void __launch_bounds__(THREADS, MINB)
     k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
             kc_diff_report* __restrict__ reps, unsigned long long* __restrict__ bitmaps, double atol, double rtol,
-            int equal_nan, const unsigned long long* __restrict__ filter, int blocked) {
+            int equal_nan, const unsigned long long* __restrict__ filter, int blocked, uint32_t flush_units) {
     const int lane = threadIdx.x & 31;
     segs += seg0;
     const uint64_t W = (uint64_t)gridDim.x * (THREADS / 32);
@@ -1699,7 +1710,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             const uint64_t k = sg.bitmap_chunk0 + off / kChunk;
             atomicOr(bitmaps + sg.bitmap_word0 + k / 64, 1ULL << (k % 64));
         }
-        if (++since_flush == kFlushUnits) {  // keeps the 32-bit lane counters in range
+        if (++since_flush == flush_units) {  // keeps the 32-bit lane counters in range
             since_flush = 0;
             q_fin<DT, VU, Q2>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
             acc_flush(acc, reps + s_rep, lane);
@@ -1925,15 +1936,31 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
     constexpr int WPB = THREADS / 32;
     uint64_t grid = (G.n_units + WPB - 1) / WPB;
     if (grid > (uint64_t)num_sms * MINB) grid = (uint64_t)num_sms * MINB;
+    // KC_K2_MAX_CTAS (tests only): fewer CTAs, so each warp walks many units and
+    // segment boundaries (with KC_K2_FLUSH_UNITS: many periodic flushes)
+    static const uint64_t max_ctas = [] {
+        const char* e = getenv("KC_K2_MAX_CTAS");
+        const long v = e && *e ? strtol(e, nullptr, 10) : 0;
+        return v > 0 ? (uint64_t)v : ~0ull;
+    }();
+    if (grid > max_ctas) grid = max_ctas;
     constexpr int smem = DT_<DT>::F ? WPB * (KQ<DT, U>::kBytes + (DT_<DT>::S == 2 ? kRareBytes : 0)) : 0;
     static bool attr = [] {
         return cudaFuncSetAttribute(k2_diff<DT, THREADS, MINB, U, Q2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem) == cudaSuccess;
     }();
     (void)attr;
+    // KC_K2_FLUSH_UNITS (tests only): flush the lane accumulators every n units
+    // instead of every kFlushUnits (1 GiB per warp, which no test-sized launch
+    // reaches), so the periodic-flush path is exercised
+    static const uint32_t flush_units = [] {
+        const char* e = getenv("KC_K2_FLUSH_UNITS");
+        const long v = e && *e ? strtol(e, nullptr, 10) : 0;
+        return v > 0 && v <= (long)kFlushUnits ? (uint32_t)v : (uint32_t)kFlushUnits;
+    }();
     k2_diff<DT, THREADS, MINB, U, Q2><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
                                                                          d_reps, bm, atol, rtol, equal_nan, filter,
-                                                                         k2_blocked(G));
+                                                                         k2_blocked(G), flush_units);
 }
 
 // Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per

@@ -265,7 +265,7 @@ std::string hex_base(uint64_t base) {
 using namespace kc;
 
 #define KC_ENTER(ctx)                                                                  \
-    ::kc::Internal _kc_internal_guard;                                                 \
+    ::kc::Internal _kc_internal_guard(__func__);                                                 \
     do {                                                                               \
         if (!(ctx)) return KC_ERR_ARG;                                                 \
         if ((ctx)->poisoned) return KC_ERR_CUDA;                                       \
@@ -363,6 +363,7 @@ void kc_destroy(kc_ctx* ctx) {
     }
     for (void* p : ctx->pinned) cudaFreeHost(p);
     for (cudaEvent_t e : ctx->pin_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->full_ev) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
 }
@@ -767,7 +768,7 @@ static int elem_size(int dt) {
 static kc_status diff_launch(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
                              const uint64_t* report_nbytes, const uint64_t* bitmap_word0, const kc_tolerance* tol,
                              kc_diff_report* d_reports, uint64_t* d_bitmaps, void* stream,
-                             const uint64_t* filter_chunk0, const uint64_t* d_filter) {
+                             const uint64_t* filter_chunk0, const uint64_t* d_filter, bool accumulate = false) {
     if ((n_bufs && !bufs) || (n_reports && (!d_reports || !report_nbytes)))
         return set_err(ctx, KC_ERR_ARG, "kc_diff_async: null pointer");
     if (d_bitmaps && !bitmap_word0) return set_err(ctx, KC_ERR_ARG, "kc_diff_async: bitmaps need bitmap_word0");
@@ -873,9 +874,11 @@ static kc_status diff_launch(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, 
         ctx->diff_groups = groups;
         ctx->diff_bitmap_words = bitmap_words;
     }
-    if (n_reports)
+    // accumulate: the caller zeroed reports and bitmaps once and streams pieces
+    // through several launches (counts add, maxima max, finalize is idempotent)
+    if (n_reports && !accumulate)
         KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_reports, 0, n_reports * sizeof(kc_diff_report), s), "zero reports");
-    if (d_bitmaps && bitmap_words)
+    if (d_bitmaps && bitmap_words && !accumulate)
         KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_bitmaps, 0, bitmap_words * 8, s), "zero bitmaps");
     KC_CHECK_CUDA(ctx, launch_diff((const SegDev*)ctx->segs.p, groups.data(), (int)groups.size(),
                                    (const ReportMeta*)ctx->meta.p, (int)n_reports, d_reports, d_bitmaps, tol->atol,
@@ -972,12 +975,111 @@ kc_status kc_hash_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const
                        chunk0.data(), dirty);
 }
 
+// Byte-exact validation against a HOST reference (ref_manifest == NULL): every
+// reference byte crosses PCIe (the paper's strict compare),
+// streamed through a device staging ring of kFullSlots pieces.  The ctx copy
+// stream fills slot k while K2 runs on the caller's stream over slot k-1, so
+// the diff hides under the H2D and the call runs at the PCIe rate.  Pieces cut
+// buffers at 64 KiB chunk boundaries (bitmap_chunk0 = the piece's first chunk)
+// and pack small buffers together; every piece's K2 launch accumulates into
+// the same reports (zeroed once; counts add, maxima max; the finalize is
+// idempotent), each launch carrying a zero-length segment per report so that
+// every report keeps its dtype.
+constexpr uint64_t kFullPiece = 256ull << 20;
+constexpr int kFullSlots = 3;
+
+static kc_status validate_host_full(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const kc_tolerance* tol,
+                                    kc_diff_report* reps, uint64_t* h_bitmaps, uint64_t* d_act_manifest,
+                                    uint64_t* h2d_bytes, cudaStream_t s, const std::vector<uint64_t>& nbytes,
+                                    const std::vector<uint64_t>& word0, uint64_t words) {
+    kc_status st = ensure_stream(ctx);
+    if (st != KC_OK) return st;
+    cudaStream_t cs = ctx->copy_stream;
+    if (ctx->full_ev.empty()) {
+        for (int k = 0; k < 2 * kFullSlots; ++k) {
+            cudaEvent_t e;
+            KC_CHECK_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(stage)");
+            ctx->full_ev.push_back(e);
+        }
+    }
+    cudaEvent_t* copied = ctx->full_ev.data();
+    cudaEvent_t* freed = ctx->full_ev.data() + kFullSlots;
+    KC_CHECK_CUDA(ctx, ensure(ctx->ref_stage, kFullSlots * kFullPiece), "cudaMalloc(reference stage ring)");
+    KC_CHECK_CUDA(ctx, ensure(ctx->reps, std::max<size_t>(1, n) * sizeof(kc_diff_report)), "cudaMalloc(reports)");
+    KC_CHECK_CUDA(ctx, ensure(ctx->bitmaps, std::max<uint64_t>(1, words) * 8), "cudaMalloc(bitmaps)");
+    kc_diff_report* d_reps = (kc_diff_report*)ctx->reps.p;
+    uint64_t* d_bm = (uint64_t*)ctx->bitmaps.p;
+    if (n) KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_reps, 0, n * sizeof(kc_diff_report), s), "zero reports");
+    if (words) KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_bm, 0, words * 8, s), "zero bitmaps");
+    if (d_act_manifest) {  // the actual buffers' manifest (K1), as the filtered mode's K5 gives it
+        std::vector<kc_region> regs(n);
+        for (size_t i = 0; i < n; ++i) regs[i] = kc_region{bufs[i].act, bufs[i].nbytes, ctx->device, KC_KIND_MEMALLOC, 0};
+        st = hash_impl(ctx, regs.data(), n, d_act_manifest, nullptr, nullptr, s, nullptr);
+        if (st != KC_OK) return st;
+    }
+    // the copy stream starts after the caller's earlier work (a previous call's K2 may still read the ring)
+    KC_CHECK_CUDA(ctx, cudaEventRecord(freed[0], s), "event record");
+    KC_CHECK_CUDA(ctx, cudaStreamWaitEvent(cs, freed[0], 0), "stream wait");
+    uint8_t* ring = (uint8_t*)ctx->ref_stage.p;
+    std::vector<kc_buffer> segs;
+    auto reset_segs = [&]() {
+        segs.clear();
+        for (size_t i = 0; i < n; ++i) segs.push_back(kc_buffer{bufs[i].act, bufs[i].act, 0, bufs[i].dtype, (int32_t)i, 0});
+    };
+    reset_segs();
+    int slot = 0;
+    uint64_t used = 0, moved = 0, pieces = 0;
+    auto flush = [&]() -> kc_status {
+        if (segs.size() == n) return KC_OK;
+        KC_CHECK_CUDA(ctx, cudaEventRecord(copied[slot], cs), "event record");
+        KC_CHECK_CUDA(ctx, cudaStreamWaitEvent(s, copied[slot], 0), "stream wait");
+        kc_status r = diff_launch(ctx, segs.data(), segs.size(), n, nbytes.data(), word0.data(), tol, d_reps,
+                                  words ? d_bm : nullptr, s, nullptr, nullptr, true);
+        if (r != KC_OK) return r;
+        KC_CHECK_CUDA(ctx, cudaEventRecord(freed[slot], s), "event record");
+        slot = (slot + 1) % kFullSlots;
+        ++pieces;
+        if (pieces >= (uint64_t)kFullSlots)  // the next slot's previous piece must be diffed before it is refilled
+            KC_CHECK_CUDA(ctx, cudaStreamWaitEvent(cs, freed[slot], 0), "stream wait");
+        used = 0;
+        reset_segs();
+        return KC_OK;
+    };
+    for (size_t i = 0; i < n; ++i) {
+        uint64_t off = 0;
+        while (off < bufs[i].nbytes) {
+            if (kFullPiece - used < kChunk) {
+                st = flush();
+                if (st != KC_OK) return st;
+            }
+            const uint64_t room = (kFullPiece - used) / kChunk * kChunk;  // whole chunks: pieces cut at chunk bounds
+            const uint64_t len = std::min<uint64_t>(room, bufs[i].nbytes - off);
+            uint8_t* dst = ring + (uint64_t)slot * kFullPiece + used;
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(dst, (const uint8_t*)bufs[i].ref + off, len, cudaMemcpyHostToDevice, cs),
+                          "H2D reference piece");
+            segs.push_back(kc_buffer{(uint64_t)dst, bufs[i].act + off, len, bufs[i].dtype, (int32_t)i, off / kChunk});
+            moved += len;
+            off += len;
+            used += (len + 255) & ~255ull;  // the next piece starts 256-byte aligned
+        }
+    }
+    st = flush();
+    if (st != KC_OK) return st;
+    KC_CHECK_CUDA(ctx, cudaMemcpyAsync(reps, d_reps, n * sizeof(kc_diff_report), cudaMemcpyDeviceToHost, s),
+                  "D2H reports");
+    if (h_bitmaps && words)
+        KC_CHECK_CUDA(ctx, cudaMemcpyAsync(h_bitmaps, d_bm, words * 8, cudaMemcpyDeviceToHost, s), "D2H bitmaps");
+    KC_CHECK_CUDA(ctx, cudaStreamSynchronize(s), "kc_validate_host_ref sync");
+    if (h2d_bytes) *h2d_bytes = moved;
+    return KC_OK;
+}
+
 // ------------------------------------------------------------------ F2: validation against a host-resident reference
 kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, const uint64_t* ref_manifest,
                                const kc_tolerance* tol, kc_diff_report* reps, uint64_t* h_bitmaps,
                                uint64_t* d_act_manifest, uint64_t* h2d_bytes, void* stream) {
     KC_ENTER(ctx);
-    if (n && (!bufs || !ref_manifest || !reps)) return set_err(ctx, KC_ERR_ARG, "kc_validate_host_ref: null pointer");
+    if (n && (!bufs || !reps)) return set_err(ctx, KC_ERR_ARG, "kc_validate_host_ref: null pointer");
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<PairDev> t(n);
     std::vector<uint64_t> nbytes(n), word0(n), chunk0(n);
@@ -996,6 +1098,9 @@ kc_status kc_validate_host_ref(kc_ctx* ctx, const kc_buffer* bufs, size_t n, con
         t[i] = PairDev{bufs[i].act, bufs[i].act, bufs[i].nbytes, C, bufs[i].dtype, 0};  // self pairs
         C += nc;
     }
+    if (!ref_manifest)
+        return validate_host_full(ctx, bufs, n, tol, reps, h_bitmaps, d_act_manifest, h2d_bytes, s, nbytes, word0,
+                                  words);
     uint64_t moved = 0;
     // (1) the reference manifest to the device
     KC_CHECK_CUDA(ctx, ensure(ctx->ref_man, std::max<uint64_t>(1, C) * 8), "cudaMalloc(reference manifest)");

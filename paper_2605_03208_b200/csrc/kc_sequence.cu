@@ -92,7 +92,7 @@ bool same_regions(const SnapDesc& a, const SnapDesc& b) {
 
 extern "C" kc_status kc_capture_seq(kc_ctx* ctx, const kc_dispatch* ds, size_t n_disp, const kc_region* regions,
                                     size_t n, int host, kc_sequence** out, kc_capture_report* reps) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !ds || !n_disp || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     *out = nullptr;
@@ -139,19 +139,19 @@ kc_status kc::make_sequence(kc_ctx* ctx, std::vector<kc_snapshot*>& steps, kc_se
 extern "C" size_t kc_seq_length(const kc_sequence* q) { return q ? q->steps.size() : 0; }
 
 extern "C" const kc_snapshot* kc_seq_step(const kc_sequence* q, size_t k) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     return q && k < q->steps.size() ? q->steps[k] : nullptr;
 }
 
 extern "C" kc_status kc_seq_deps(const kc_sequence* q, uint8_t* deps, size_t cap) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!q || !deps || cap < q->deps.size()) return KC_ERR_ARG;
     memcpy(deps, q->deps.data(), q->deps.size());
     return KC_OK;
 }
 
 extern "C" kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* dir_c) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !q || !dir_c) return KC_ERR_ARG;
     const std::string dir(dir_c);
     if (mkdir(dir.c_str(), 0755) != 0 && errno != EEXIST)
@@ -190,7 +190,7 @@ extern "C" kc_status kc_seq_save(kc_ctx* ctx, const kc_sequence* q, const char* 
 // a kc-sequence/1 directory back into memory (every step fully loaded: the
 // steps' shared bytes are not deduplicated)
 extern "C" kc_status kc_seq_load(kc_ctx* ctx, const char* dir_c, int host, kc_sequence** out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !dir_c || !out) return KC_ERR_ARG;
     *out = nullptr;
     const std::string dir(dir_c);
@@ -218,7 +218,7 @@ extern "C" kc_status kc_seq_load(kc_ctx* ctx, const char* dir_c, int host, kc_se
 }
 
 extern "C" void kc_seq_free(kc_sequence* q) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!q) return;
     for (auto it = q->steps.rbegin(); it != q->steps.rend(); ++it) kc_snapshot_free(*it);
     delete q;
@@ -226,7 +226,7 @@ extern "C" void kc_seq_free(kc_sequence* q) {
 
 extern "C" kc_status kc_replay_seq(kc_ctx* ctx, const kc_sequence* q, const kc_seq_replay_opts* o,
                                    kc_seq_step_report* reps, kc_restored** keep) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !q || !o || !reps) return KC_ERR_ARG;
     if (keep) *keep = nullptr;
     if (o->count == 0 || o->first >= q->steps.size() || o->count > q->steps.size() - o->first)

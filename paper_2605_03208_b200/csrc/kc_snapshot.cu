@@ -50,6 +50,7 @@ bool trace_on() {
     return on;
 }
 void trace(const char* what, double& tl) {
+    nvtxMarkA(what);  // stage boundary on the timeline (the stage named ends here)
     if (!trace_on()) return;
     const double t = now_s();
     fprintf(stderr, "[kc] %-28s %9.3f ms\n", what, 1e3 * (t - tl));
@@ -590,7 +591,7 @@ kc_status hash_regions_sync(kc_ctx* ctx, const std::vector<kc_region>& regs, std
 // ====================================================================== capture
 extern "C" kc_status kc_capture(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                 const char* dir_c, kc_capture_mode mode, kc_capture_report* rep_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -1020,7 +1021,7 @@ void rollback(kc_restored* h) {
 // captured 32 MiB window, so the caller can re-exec for a fresh ASLR layout.
 // *n_reserved = windows that are free.  No CUDA calls, nothing is mapped.
 extern "C" kc_status kc_prereserve(const char* dir, uint64_t* n_reserved) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!dir) return KC_ERR_ARG;
     std::vector<ParsedRegion> regs;
     kc_status st = parse_regions(nullptr, dir, regs);
@@ -1745,7 +1746,7 @@ struct IpcSource : FileSource {
 }  // namespace
 
 extern "C" kc_status kc_restore(kc_ctx* ctx, const char* dir_c, kc_restored** out, kc_restore_report* rep_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !dir_c || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     *out = nullptr;
@@ -1957,26 +1958,26 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
 
 extern "C" kc_status kc_capture_dev(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                     kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     return capture_mem(ctx, d, regions, n, mode, out, rep_out, false, nullptr);
 }
 
 extern "C" kc_status kc_capture_host(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                      kc_capture_mode mode, kc_snapshot** out, kc_capture_report* rep_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     return capture_mem(ctx, d, regions, n, mode, out, rep_out, true, nullptr);
 }
 
 extern "C" kc_status kc_capture_incr(kc_ctx* ctx, const kc_dispatch* d, const kc_region* regions, size_t n,
                                      kc_capture_mode mode, const kc_snapshot* base, int host, kc_snapshot** out,
                                      kc_capture_report* rep_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (base && base->ctx != ctx) return set_err(ctx, KC_ERR_ARG, "kc_capture_incr: base snapshot of another ctx");
     return capture_mem(ctx, d, regions, n, mode, out, rep_out, host != 0, base);
 }
 
 extern "C" kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx) return KC_ERR_ARG;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
     cudaDeviceSynchronize();
@@ -1994,7 +1995,7 @@ extern "C" kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
 }
 
 extern "C" kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx) return KC_ERR_ARG;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
     if (bytes == 0) {
@@ -2394,7 +2395,7 @@ kc_status capture_mem(kc_ctx* ctx, const kc_dispatch* d, const kc_region* region
 }  // namespace
 
 extern "C" kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !s || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (s->ctx != ctx || ctx->device != s->ctx->device)
@@ -2549,12 +2550,12 @@ static kc_status save_impl(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c,
 }
 
 extern "C" kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     return save_impl(ctx, s, dir_c, false);
 }
 
 extern "C" kc_status kc_snapshot_publish(kc_ctx* ctx, const kc_snapshot* s, const char* dir_c) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     return save_impl(ctx, s, dir_c, true);
 }
 
@@ -2562,7 +2563,7 @@ extern "C" kc_status kc_snapshot_publish(kc_ctx* ctx, const kc_snapshot* s, cons
 // -> validate loop then restores from HBM (or pinned host memory) each time
 // instead of re-reading the files (capture once, replay many).
 extern "C" kc_status kc_snapshot_load(kc_ctx* ctx, const char* dir_c, int host, kc_snapshot** out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !dir_c || !out) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -2699,7 +2700,7 @@ extern "C" uint64_t kc_snapshot_shared_bytes(const kc_snapshot* s) { return s ? 
 extern "C" int kc_snapshot_is_host(const kc_snapshot* s) { return s && s->host ? 1 : 0; }
 
 extern "C" void kc_snapshot_free(kc_snapshot* s) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     // revoke the directories this snapshot published: their bytes go with the arena
     if (s)
         for (const std::string& d : s->published) {
@@ -2716,7 +2717,7 @@ extern "C" void kc_snapshot_free(kc_snapshot* s) {
 }
 
 extern "C" kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t cap, size_t* n_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!h) return KC_ERR_ARG;
     size_t i = 0;
     for (auto& rr : h->regions) {
@@ -2728,7 +2729,7 @@ extern "C" kc_status kc_restored_regions(kc_restored* h, kc_region* out, size_t 
 }
 
 extern "C" void kc_release(kc_restored* h) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!h) return;
     if (h->ctx) bind_device(h->ctx);
     cudaDeviceSynchronize();
@@ -2747,7 +2748,7 @@ extern "C" void kc_release(kc_restored* h) {
 
 // ====================================================================== replay
 extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts* o, kc_replay_report* rep_out) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !h) return KC_ERR_ARG;
     if (ctx->poisoned) return KC_ERR_CUDA;
     if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
@@ -2890,7 +2891,7 @@ extern "C" kc_status kc_replay(kc_ctx* ctx, kc_restored* h, const kc_replay_opts
 
 extern "C" kc_status kc_validate_module_vars(kc_ctx* ctx, const kc_restored* h, uint64_t* n_checked,
                                              uint64_t* n_mismatch) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     if (!ctx || !h) return KC_ERR_ARG;
     if (n_checked) *n_checked = h->modvar_checked;
     if (n_mismatch) *n_mismatch = h->modvar_mismatch;
@@ -3081,7 +3082,7 @@ kc_status kc::validate_impl(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, 
 extern "C" kc_status kc_validate(kc_ctx* ctx, kc_restored* h, const kc_buffer* outs, size_t n,
                                  const kc_tolerance* tol, kc_diff_report* reps, size_t cap_reports,
                                  size_t* n_reports_out, uint64_t* unexpected_chunks) {
-    ::kc::Internal _kc_internal_guard;  // the CUPTI hook ignores our own driver calls
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
     return validate_impl(ctx, h, outs, n, tol, reps, cap_reports, n_reports_out, unexpected_chunks, false);
 }
 

@@ -563,7 +563,8 @@ class Context:
                           equal_nan: bool = False, stream: int = 0, with_bitmaps: bool = True,
                           d_act_manifest: int = 0):
         """kc_validate_host_ref over (host ref address, device act VA, nbytes, dtype) buffers and a host
-        reference manifest (address of the u64 chunk hashes) -> (reports, bitmaps, h2d bytes)."""
+        reference manifest (address of the u64 chunk hashes; 0 = byte-exact mode, every reference byte
+        crosses PCIe) -> (reports, bitmaps, h2d bytes)."""
         n = len(bufs)
         arr = self._buffers(bufs)
         reps = (DiffReport * max(1, n))()
@@ -571,7 +572,7 @@ class Context:
         bm = (ctypes.c_uint64 * max(1, sum(words)))()
         tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
         moved = ctypes.c_uint64(0)
-        self._check(lib().kc_validate_host_ref(self._h, arr, n, ref_manifest_ptr, ctypes.byref(tol), reps,
+        self._check(lib().kc_validate_host_ref(self._h, arr, n, ref_manifest_ptr or None, ctypes.byref(tol), reps,
                                                bm if with_bitmaps else None, d_act_manifest or None,
                                                ctypes.byref(moved), stream or None), "kc_validate_host_ref")
         out_b, o = [], 0

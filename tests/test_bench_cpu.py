@@ -15,3 +15,33 @@ def test_world_mismatch_fails_fast():
                        capture_output=True, text=True, timeout=300, env=e, cwd=ROOT)
     assert p.returncode == 2
     assert "WORLD_SIZE" in json.loads(p.stdout.strip().splitlines()[-1])["error"]
+
+
+def test_reference_arm_runs_on_cpu_with_our_config():
+    """--impl reference times the CPU oracle (no GPU needed) and prints the same metric,
+    unit and config as our arm, with a cpu_baseline describing the run and an e2e object."""
+    sys.path.insert(0, ROOT)
+    import bench
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
+                        "--warmup", "1", "--ref-step-seconds", "0.1", "--cpu-sample-mb", "12"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    r = json.loads(p.stdout.strip().splitlines()[-1])
+    assert r["impl"] == "reference" and r["metric"] == bench.METRIC and r["unit"] == bench.UNIT
+    assert r["config"] == bench.workload_config(1)
+    cb = r["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == (os.cpu_count() or 1) and cb["value"] == r["value"] > 0
+    assert cb["hash_gbs"] > 0 and cb["diff_gbs"] > 0 and cb["host"]["nproc"] == os.cpu_count()
+    assert r["e2e"] == {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_c4_host_sample_is_stratified_and_bounded():
+    """The oracle's c4 sample takes the head of every one of the 185 regions (every region
+    kind), in whole chunks, within the requested size."""
+    sys.path.insert(0, ROOT)
+    import bench
+    s = bench.c4_sample(None, 24)
+    assert len(s) == 185
+    assert all(r.size == a.size and r.size % 2 == 0 for r, a, _ in s)
+    assert sum(r.size for r, _, _ in s) <= 24 * 2**20 + 185 * 65536
+    assert {dt for _, _, dt in s} == {bench.DTC["bf16"], bench.DTC["u64"], bench.DTC["i32"], bench.DTC["f32"]}

@@ -2,9 +2,16 @@
 pool, 185 regions) in the launch configuration bench.py times: the same Pool,
 the same kc_hash / kc_diff_async / kc_hash_diff_async calls.
 
-The oracle cannot hash or diff 60 GB in a test, so (task rule ③) it checks
-sampled outputs it can compute one by one, plus properties that hold at any
-size:
+Full size, every output:
+* K1: all 458,973 chunk hashes of the 30 GB manifest recomputed by the
+  oracle (O2) from the chunk bytes, region by region (each region copied to
+  pinned host memory, hashed on every host core); every region digest and
+  the snapshot digest recomputed from the oracle's own manifest;
+* K2 / K5: every region's report and bitmap against oracle.diff (O4) over
+  the region's full reference and actual bytes (the reference copy carries
+  seeded plants: bf16 +-k ULP, a NaN, a pointer-table entry).
+
+Sampled (fast, kept as a first failure signal):
 * K1: ~600 chunk hashes (the first and last chunk of every region, plus a
   seeded sample) recomputed from the chunk bytes; region digests and the
   snapshot digest recomputed from the manifest;
@@ -14,6 +21,9 @@ size:
   report over its planted chunks (sums and maxima), with the size-derived
   fields recomputed from the region size; bitmaps likewise.
 """
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import pytest
 
@@ -78,6 +88,62 @@ def test_c4_manifest_and_digests_sampled(pool):
     assert S == int(dig[nreg])
 
 
+def _host_regions(torch, vas_sizes, depth: int = 3):
+    """Yield (index, host uint8 array) for each (va, size), copying region i+1..i+depth
+    device->host on a side stream while the caller works on region i."""
+    import synth
+    stream = torch.cuda.Stream()
+    pend = []
+    it = iter(enumerate(vas_sizes))
+
+    def issue():
+        try:
+            i, (va, n) = next(it)
+        except StopIteration:
+            return
+        h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        with torch.cuda.stream(stream):
+            h.copy_(synth.dev_view(va, n), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        pend.append((i, h, ev))
+    for _ in range(depth):
+        issue()
+    while pend:
+        i, h, ev = pend.pop(0)
+        ev.synchronize()
+        issue()
+        yield i, h.numpy()
+
+
+def test_c4_full_manifest_every_chunk_vs_oracle(pool):
+    """All 458,973 chunk hashes of the 30 GB snapshot equal the oracle's (O2), and the
+    region digests and snapshot digest equal the oracle's computed from its OWN manifest."""
+    torch, kc, ctx, orc, p = pool
+    C = kc.count_chunks(p.regions)
+    nreg = len(p.regions)
+    d_h = torch.zeros(C, dtype=torch.int64, device="cuda")
+    d_dig = torch.zeros(nreg + 1, dtype=torch.int64, device="cuda")
+    ctx.hash(p.regions, d_h.data_ptr(), d_dig.data_ptr(), d_dig.data_ptr() + 8 * nreg)
+    torch.cuda.synchronize()
+    h = d_h.cpu().numpy().view(np.uint64)
+    dig = d_dig.cpu().numpy().view(np.uint64)
+    threads = max(1, os.cpu_count() or 1)
+    starts = np.cumsum([0] + [(s + CH - 1) // CH for _, s in p.regions])
+    odig, checked = [], 0
+    for j, data in _host_regions(torch, p.regions):
+        eh = orc.chunk_hashes(data, threads=threads)
+        got = h[starts[j]:starts[j + 1]]
+        bad = np.nonzero(eh != got)[0]
+        assert bad.size == 0, f"region {j}: {bad.size} chunk hashes differ, first chunk {int(bad[0])}"
+        checked += eh.size
+        odig.append(orc.region_digest(eh))
+    assert checked == C == 458973
+    assert odig == [int(x) for x in dig[:nreg]], "region digests != oracle"
+    S = orc.snapshot_digest([b for b, _ in p.regions], [s for _, s in p.regions], odig)
+    assert S == int(dig[nreg]), "snapshot digest != oracle"
+
+
 def _plant(torch, p, rng):
     """Seeded plants in the REFERENCE copy; returns {region index: sorted planted chunk list}."""
     import synth
@@ -135,6 +201,35 @@ def _expected(torch, orc, kc, p, planted):
     return out
 
 
+def _expected_full(torch, orc, kc, p):
+    """Per-region report and bitmap bit set from oracle.diff over the WHOLE region (O4):
+    reference and actual bytes streamed to the host, regions diffed in parallel."""
+    out = {}
+    refs = _host_regions(torch, [(p.ref[s.name], s.size) for s in p.specs], depth=2)
+    acts = _host_regions(torch, [(p.va[s.name], s.size) for s in p.specs], depth=2)
+
+    def one(j, r, a):
+        s = p.specs[j]
+        ex = orc.diff(r, a, kc.DT[s.dtype])
+        nc = (s.size + CH - 1) // CH
+        bits = {k for k in range(nc) if (int(ex.bitmap[k // 64]) >> (k % 64)) & 1}
+        return j, (dict(ex.report), bits)
+    with ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1))) as ex:
+        futs = []
+        for (j, r), (j2, a) in zip(refs, acts):
+            assert j == j2
+            futs.append(ex.submit(one, j, r.copy(), a.copy()))
+            if len(futs) >= 16:     # bound host memory: at most ~16 regions in flight
+                for f in futs[:8]:
+                    jj, v = f.result()
+                    out[jj] = v
+                futs = futs[8:]
+        for f in futs:
+            jj, v = f.result()
+            out[jj] = v
+    return out
+
+
 def _check(kc, reps_raw, bms, word0, exp, p, label):
     for j, s in enumerate(p.specs):
         got = kc.DiffReport.from_buffer_copy(reps_raw[120 * j:120 * (j + 1)]).as_dict()
@@ -154,12 +249,8 @@ def test_c4_k2_and_k5_reports_full_size(pool):
     rng = np.random.default_rng(260503208 + 4)
     planted = _plant(torch, p, rng)
     exp = _expected(torch, orc, kc, p, planted)
-    bufs = p.diff_buffers()
-    nb = [b.nbytes for b in bufs]
-    word0, acc = [], 0
-    for b in bufs:
-        word0.append(acc)
-        acc += ((b.nbytes + CH - 1) // CH + 63) // 64
+    bufs, nb, word0, acc = p.diff_buffers()   # bench.py's buffers, report sizes and bitmap offsets
+    assert [b.nbytes for b in bufs] == nb
     reps = torch.zeros(len(bufs) * 15, dtype=torch.int64, device="cuda")
     bms = torch.zeros(acc, dtype=torch.int64, device="cuda")
     # bench.py's K2 call
@@ -178,6 +269,11 @@ def test_c4_k2_and_k5_reports_full_size(pool):
     torch.cuda.synchronize()
     _check(kc, reps.cpu().numpy().tobytes(), bms.cpu().numpy().view(np.uint64), word0, exp, p, "K5+K2")
     assert torch.equal(d_h5, d_h1)
+    # every field of every region's report, and every bitmap bit, against the oracle over
+    # the full 2 x 30 GB (not only the planted chunks)
+    full = _expected_full(torch, orc, kc, p)
+    assert len(full) == len(p.specs)
+    _check(kc, reps.cpu().numpy().tobytes(), bms.cpu().numpy().view(np.uint64), word0, full, p, "K5+K2 full")
     # every planted chunk is dirty; the dirty set stays small (tails + plants)
     starts = np.cumsum([0] + [(s.size + CH - 1) // CH for s in p.specs])
     dw = dirty.cpu().numpy().view(np.uint64)

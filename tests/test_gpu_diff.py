@@ -281,3 +281,22 @@ def test_k2_plan_cache_sees_new_contents_and_new_sets(env):
     _same(second[0], orc.diff(r, a2, orc.DT_F16).report, "second")
     third, _ = ctx.diff([(pr, pa, r.size // 2, "f16")])   # a different set
     _same(third[0], orc.diff(r[:r.size // 2], a2[:a2.size // 2], orc.DT_F16).report, "third")
+
+
+@pytest.mark.parametrize("every,ctas", [("1", ""), ("3", "1"), ("5", "2")])
+def test_periodic_flush_path(every, ctas):
+    """K2's periodic flush of the 32-bit lane counters (every kFlushUnits = 1 GiB per
+    warp in production, which no test-sized launch reaches) forced to every 1 / 3 / 5
+    units in a fresh process, with the grid cut to 1 or 2 CTAs so each warp walks
+    ~20 units across segment boundaries: reports and bitmaps still equal the oracle's."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "tests", "k2_flush_worker.py")], capture_output=True,
+                       text=True, timeout=600, env=dict(os.environ, KC_K2_FLUSH_UNITS=every, KC_K2_MAX_CTAS=ctas))
+    assert p.returncode == 0, p.stderr[-3000:]
+    r = json.loads(p.stdout.strip().splitlines()[-1])
+    assert r["flush_units"] == every and r["bad"] == [], r["bad"][:10]
+    assert all(d > 0 for d in r["differing_elems"])

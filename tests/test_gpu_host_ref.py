@@ -119,3 +119,48 @@ def test_host_ref_clean_copy_moves_only_the_manifest(env):
     man = np.ascontiguousarray(orc.chunk_hashes(ref))
     reps, _, moved = ctx.validate_host_ref([(h.data_ptr(), d.data_ptr(), ref.size, "bytes")], man.ctypes.data)
     assert moved == man.nbytes and reps[0]["differing_bytes"] == 0 and reps[0]["pass"] == 1
+
+
+def test_host_ref_byte_exact_mode_streams_every_byte(env):
+    """ref_manifest == NULL: every reference byte crosses PCIe through the 3 x 256 MiB
+    staging ring (a 1 GiB + 2 MiB buffer wraps the ring: 5 pieces), mixed with the small
+    CASES packed into shared pieces.  Reports, bitmaps and the act manifest equal the
+    oracle's O4 / O2 over the full buffers; h2d bytes = every reference byte."""
+    torch, kc, ctx, orc = env
+    dts = {"bf16": orc.DT_BF16, "f16": orc.DT_F16, "f32": orc.DT_F32, "bytes": orc.DT_BYTES}
+    refs, acts, bufs, names = [], [], [], []
+    for k, (name, nch, tail, dirty, nanc, infc) in enumerate(CASES):
+        ref, act = _case(orc, dts[name], nch, tail, 260503208 + 77 * k, dirty, nanc, infc)
+        refs.append(ref)
+        acts.append(act)
+        names.append(name)
+    # the big one: bf16 N(0,1) with +-1 ULP plants at piece boundaries, a NaN and a ragged tail
+    rng = np.random.default_rng(260503208 + 99)
+    nb = (1 << 30) + (2 << 20) + 6
+    big = (rng.standard_normal(nb // 2).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    bact = big.copy()
+    P = (256 << 20) // 2
+    for e in (0, P - 1, P, 2 * P + 5, 3 * P - 1, 4 * P + 3, nb // 2 - 1):
+        bact[e] ^= 1
+    bact[3 * P + 11] = 0x7FC1
+    refs.insert(2, big.view(np.uint8))
+    acts.insert(2, bact.view(np.uint8))
+    names.insert(2, "bf16")
+    h_refs = [torch.from_numpy(r).pin_memory() for r in refs]
+    d_acts = [torch.from_numpy(a).cuda() for a in acts]
+    bufs = [(h.data_ptr(), d.data_ptr(), r.size, nm) for h, d, r, nm in zip(h_refs, d_acts, refs, names)]
+    C = sum(orc.n_chunks(r.size) for r in refs)
+    d_man = torch.zeros(C, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(2):   # a second call reuses the ring (the copy stream waits for the previous K2)
+        reps, bms, moved = ctx.validate_host_ref(bufs, 0, d_act_manifest=d_man.data_ptr())
+        assert moved == sum(r.size for r in refs)
+        for k, nm in enumerate(names):
+            exp = orc.diff(refs[k], acts[k], dts[nm])
+            for f in FIELDS:
+                g, e = reps[k][f], exp.report[f]
+                assert g == e or (isinstance(e, float) and np.isnan(g) and np.isnan(e)), f"{k} {nm} {f}: {g} vs {e}"
+            assert [int(x) for x in bms[k]] == [int(x) for x in exp.bitmap], f"{k} {nm} bitmap"
+    want = np.concatenate([orc.chunk_hashes(a, threads=8) for a in acts])
+    assert np.array_equal(d_man.cpu().numpy().view(np.uint64), want)
+    assert reps[2]["differing_elems"] == 8 and reps[2]["nan_act"] == 1

@@ -20,7 +20,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
-ARGS = ["--steps", "2", "--warmup", "1", "--no-e2e", "--no-fused", "--no-latency", "--no-cpu-baseline", "--plant",
+ARGS = ["--steps", "2", "--warmup", "1", "--no-e2e", "--no-fused", "--no-latency", "--no-cpu-baseline", "--no-configs", "--plant",
         "--quiet"]
 
 
@@ -51,7 +51,7 @@ def test_n2_one_gpu_combine_equals_n1(one, placement):
     allocations (on one GPU a second mapping of the same HBM; over NVLink on two)."""
     two = _bench(2, {"KC_BENCH_ONE_GPU": "1", "KC_BENCH_BACKEND": "gloo"}, ["--placement", placement])
     assert one["n_gpus"] == 1 and two["n_gpus"] == 2
-    assert two["config"]["collectives"]["backend"] == "gloo"
+    assert two["collectives"]["backend"] == "gloo"
     f1, f2 = one["fingerprint"], two["fingerprint"]
     assert f1["report_counter_sums"][0] > 0 and f1["bitmap_bits"] > 0 and f1["max_ulp"] > 0   # planted
     for k in KEYS:
@@ -64,6 +64,6 @@ def test_n2_one_gpu_combine_equals_n1(one, placement):
 @pytest.mark.parametrize("placement", ["e1", "e2"])
 def test_n2_nccl_two_gpus_equals_n1(one, placement):
     two = _bench(2, extra=["--placement", placement])
-    assert two["n_gpus"] == 2 and two["config"]["collectives"]["backend"] == "nccl"
+    assert two["n_gpus"] == 2 and two["collectives"]["backend"] == "nccl"
     for k in KEYS:
         assert one["fingerprint"][k] == two["fingerprint"][k], k

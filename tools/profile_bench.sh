@@ -6,7 +6,7 @@
 set -u
 O=${1:-gpurun_out}
 mkdir -p "$O"
-B="python bench.py --steps 2 --warmup 1 --no-e2e --no-latency"
+B="python bench.py --steps 2 --warmup 1 --no-e2e --no-latency --no-configs --no-cpu-baseline"
 [ "${SKIP_LIST:-0}" = 1 ] || ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k1_|k2_|k3_|k5_|kc_fixture" --csv \
     --log-file "$O/launches.csv" $B --no-fused > "$O/launch_run.log" 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k2_diff<.int.10," \
