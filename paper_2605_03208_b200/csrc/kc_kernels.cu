@@ -42,9 +42,9 @@ __device__ __forceinline__ uint64_t xround(uint64_t acc, uint64_t x) {
 // The accumulator chain in "y form".  With y = acc + x*P2 (the pre-rotation
 // sum) the round is  y' = rotl(y, 31)*P1 + x'*P2,  and the 64-bit multiply's
 // low product absorbs the next word's x'*P2 as its 64-bit addend (one
-// mad.wide.u32).  x'*P2 is off the chain, so the chain per 32-byte stripe is
-// funnel shift -> {mad.wide, 2 IMAD in parallel} -> IADD3: 3 dependent SASS
-// instead of 6 (the per-chunk latency floor that bounds sub-wave snapshots).
+// mad.wide.u32).  x'*P2 is off the chain (tools/probes/k1_round_probe.cu:
+// ~30 cycles per round for one chain per thread at one warp per SMSP, every
+// formulation within 15%; this one is the fastest measured).
 // A lane starts from y0 = rotr(seed * P1^-1, 31), so that rotl(y0, 31)*P1 is
 // the XXH64 lane seed, and ends with yfinal(y) = rotl(y, 31)*P1 = the lane's
 // accumulator.  Same arithmetic mod 2^64, reordered: results are identical.
@@ -52,16 +52,15 @@ __device__ __forceinline__ uint64_t ystep(uint64_t y, uint64_t x) {
     const uint64_t p = x * P2;  // off the chain
     const uint32_t yl = (uint32_t)y, yh = (uint32_t)(y >> 32);
     const uint32_t rh = __funnelshift_l(yl, yh, 31), rl = __funnelshift_l(yh, yl, 31);
-    uint64_t w;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(rl), "r"((uint32_t)P1), "l"(p));
-    uint32_t hi;
-    asm("{\n\t.reg .u32 a, b;\n\t"
-        "mul.lo.u32 a, %1, %3;\n\t"
-        "mul.lo.u32 b, %2, %4;\n\t"
-        "add.u32 a, a, b;\n\t"
-        "add.u32 %0, a, %5;\n\t}"
-        : "=r"(hi) : "r"(rl), "r"(rh), "r"((uint32_t)(P1 >> 32)), "r"((uint32_t)P1), "r"((uint32_t)(w >> 32)));
-    return ((uint64_t)hi << 32) | (uint32_t)w;
+    // the cross products go into the high addend; the low product's carry
+    // chain (mad.lo.cc / madc.hi) keeps ptxas from splitting the 64-bit add
+    // back out: SASS is SHF -> IMAD -> IMAD -> IMAD.WIDE.U32 (64-bit addend)
+    const uint32_t c = rl * (uint32_t)(P1 >> 32) + rh * (uint32_t)P1 + (uint32_t)(p >> 32);
+    uint32_t lo, hi;
+    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;"
+        : "=r"(lo), "=r"(hi)
+        : "r"(rl), "r"((uint32_t)P1), "r"((uint32_t)p), "r"(c));
+    return ((uint64_t)hi << 32) | lo;
 }
 __device__ __forceinline__ uint64_t yfinal(uint64_t y) { return ystep(y, 0); }
 
@@ -1873,10 +1872,13 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
         case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
         default:
-            if ((C + 7) / 8 < (uint64_t)num_sms * 8)  // fewer groups than 8-warp CTAs x SMs: spread them
+            // fewer groups than 8-warp CTAs x SMs: spread them (a per-quad TMA bulk ring of
+            // 16 slots x 3 x 2 KiB measured 92-129 us on c2 against CpS's 53 us, round 2)
+            if ((C + 7) / 8 < (uint64_t)num_sms * 8) {
                 launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
-            else
+            } else {
                 launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
+            }
             break;
     }
     return cudaGetLastError();

@@ -1,0 +1,8 @@
+set -u
+./build/k1_round_probe > gpurun_out/r2c_k1_round_probe.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_diff.py -m gpu -q -p no:cacheprovider -k "flush" > gpurun_out/r2c_flush.log 2>&1; echo "rc=$?" >> gpurun_out/r2c_flush.log
+python tools/k2_bench.py > gpurun_out/r2c_k2_bench.txt 2>&1
+export KC_K2_CASES=c3_planted_bf16
+ncu --set full --clock-control none --import-source on -k regex:k2_diff --launch-skip 3 -c 1 -o gpurun_out/r2c_k2_planted python tools/k2_bench.py one > gpurun_out/r2c_k2ncu.log 2>&1
+python tools/ncu_summary.py gpurun_out/r2c_k2_planted.ncu-rep > gpurun_out/r2c_k2_planted_summary.txt 2>&1
+python tools/ncu_sass_hist.py gpurun_out/r2c_k2_planted.ncu-rep >> gpurun_out/r2c_k2_planted_summary.txt 2>&1
