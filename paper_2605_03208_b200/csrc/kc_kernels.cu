@@ -11,6 +11,7 @@
 // and with -fmad=false; every fp64 op below is an explicit _rn intrinsic.
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
+#include <cuda_bf16.h>
 #include <math_constants.h>
 
 #include <algorithm>
@@ -1241,6 +1242,48 @@ __device__ __forceinline__ uint32_t vec_scan16(const uint32_t (&r)[8], const uin
     return any;
 }
 
+// Round 2: the same flags with the half-precision compare unit doing most of
+// the work (the ALU pipe binds the planted case, ncu: ALU 78%, FMA 20%).  A
+// half needs the element path iff its bits differ or a side is NaN:
+//   HSET2.NEU(r, a) is true for every pair of unequal values and for every NaN
+//   (unordered), and false only for equal values; equal values with unequal
+//   bits are exactly +0 / -0 (f16 and bf16 have no other duplicate encodings,
+//   subnormals are compared as values: set.*.f16x2 / bf16x2 honour them), whose
+//   sign bits differ.  So flag = NEU(r, a) | ((r ^ a) & sign): one HSET2 and
+//   one LOP3 per word.  An Inf reference with equal bits contributes nothing to
+//   any report field (elem_float returns at once), so it is no longer flagged.
+// acc.any (a differing byte in this unit, for the bitmap) still needs the raw
+// XOR, taken only for vectors with a flag.
+template <int DT>
+__device__ __forceinline__ uint32_t ne_mask16(uint32_t r, uint32_t a) {
+    if constexpr (DT == KC_DT_F16) {
+        return __hneu2_mask(*reinterpret_cast<const __half2*>(&r), *reinterpret_cast<const __half2*>(&a));
+    } else {
+        return __hneu2_mask(*reinterpret_cast<const __nv_bfloat162*>(&r),
+                            *reinterpret_cast<const __nv_bfloat162*>(&a));
+    }
+}
+
+template <int DT>
+__device__ __forceinline__ uint32_t vec_scan16h(const uint32_t (&r)[8], const uint32_t (&a)[8], uint32_t (&m)[8],
+                                                uint32_t& cnt128, Acc& acc) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        m[i] = (ne_mask16<DT>(r[i], a[i]) | (r[i] ^ a[i])) & 0x80008000u;
+        any |= m[i];
+    }
+    if (any) {
+        uint32_t anyx = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) anyx |= r[i] ^ a[i];
+        acc.any |= (uint32_t)(anyx != 0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cnt128 = __dp4a(m[i], 0x01010101u, cnt128);
+    }
+    return any;
+}
+
 template <int DT>
 __device__ __forceinline__ void q_push16(const uint32_t (&r)[8], const uint32_t (&a)[8], const uint32_t (&m)[8],
                                          uint32_t* q, uint32_t& pos) {
@@ -1263,6 +1306,32 @@ __device__ __forceinline__ void q_push16_addr(const uint32_t (&r)[8], const uint
         if (m[i] & 0x80000000u)
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(__byte_perm(r[i], a[i], 0x7632)) : "memory");
         sa += (m[i] >> 29) & 4u;
+    }
+}
+
+// Q2 = 3 push (default): one ALU op per address bump instead of three (the ALU
+// pipe binds this path, ncu: ALU 79%).  m is masked to bits 15 / 31; f = m &
+// 0x8000 (the LOP3 that also sets the store predicate) gives 4 * bit15 =
+// hi32(f * 2^19) and 4 * bit31 = hi32(m * 8) (bit 15 does not reach), each a
+// mad.hi.u32 by a power of two, which ptxas emits as one LEA.HI.  (The same
+// bumps as IMAD.HI on the FMA pipe, with multipliers hidden from ptxas, were
+// slower: a serial chain of 4-cycle IMADs, 5.2 vs 5.8 TB/s.)
+__device__ __forceinline__ uint32_t bump_hi(uint32_t v, uint32_t mul, uint32_t sa) {
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(v), "r"(mul), "r"(sa));
+    return d;
+}
+__device__ __forceinline__ void q_push16_lea(const uint32_t (&r)[8], const uint32_t (&a)[8], const uint32_t (&m)[8],
+                                             uint32_t& sa) {
+    constexpr uint32_t k19 = 1u << 19, k3 = 8u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t f = m[i] & 0x00008000u;
+        if (f) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(__byte_perm(r[i], a[i], 0x5410)) : "memory");
+        sa = bump_hi(f, k19, sa);
+        if ((int)m[i] < 0)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(__byte_perm(r[i], a[i], 0x7632)) : "memory");
+        sa = bump_hi(m[i], k3, sa);
     }
 }
 
@@ -1433,7 +1502,9 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
                     uint32_t mw[U][8];
                     uint32_t any = 0, cnt128 = 0;
 #pragma unroll
-                    for (int u = 0; u < U; ++u) any |= vec_scan16<DT>(rw[u], aw[u], mw[u], cnt128, acc);
+                    for (int u = 0; u < U; ++u)
+                        any |= Q2 >= 2 ? vec_scan16h<DT>(rw[u], aw[u], mw[u], cnt128, acc)
+                                       : vec_scan16<DT>(rw[u], aw[u], mw[u], cnt128, acc);
                     const bool push = __any_sync(0xFFFFFFFFu, any != 0);
                     if (push) {
                         const uint32_t c = cnt128 >> 7;
@@ -1446,7 +1517,10 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
                         const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
                         uint32_t sa = (uint32_t)__cvta_generic_to_shared(q) + 4 * (qn + incl - c);
 #pragma unroll
-                        for (int u = 0; u < U; ++u) q_push16_addr(rw[u], aw[u], mw[u], sa);
+                        for (int u = 0; u < U; ++u) {
+                            if constexpr (Q2 == 3) q_push16_lea(rw[u], aw[u], mw[u], sa);
+                            else q_push16_addr(rw[u], aw[u], mw[u], sa);
+                        }
                         qn += total;
                     }
                     v += 32 * U;
@@ -1474,7 +1548,9 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
                 uint32_t mw[U][8];
                 uint32_t any = 0, cnt128 = 0;
 #pragma unroll
-                for (int u = 0; u < U; ++u) any |= vec_scan16<DT>(rw[u], aw[u], mw[u], cnt128, acc);
+                for (int u = 0; u < U; ++u)
+                    any |= Q2 >= 2 ? vec_scan16h<DT>(rw[u], aw[u], mw[u], cnt128, acc)
+                                   : vec_scan16<DT>(rw[u], aw[u], mw[u], cnt128, acc);
                 if (__any_sync(0xFFFFFFFFu, any != 0)) {
                     const uint32_t c = cnt128 >> 7;
                     uint32_t incl = c;
@@ -1488,7 +1564,10 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
                     if constexpr (Q2) {
                         uint32_t sa = (uint32_t)__cvta_generic_to_shared(q) + 4 * pos;
 #pragma unroll
-                        for (int u = 0; u < U; ++u) q_push16_addr(rw[u], aw[u], mw[u], sa);
+                        for (int u = 0; u < U; ++u) {
+                            if constexpr (Q2 == 3) q_push16_lea(rw[u], aw[u], mw[u], sa);
+                            else q_push16_addr(rw[u], aw[u], mw[u], sa);
+                        }
                         qn += total;
                         if (qn >= 32) q_drain16<DT>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
                     } else {
@@ -1976,13 +2055,23 @@ static void launch_k2(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* 
                       double atol, double rtol, int equal_nan, int num_sms, cudaStream_t s,
                       const unsigned long long* filter) {
     if constexpr (DT_<DT>::F && DT_<DT>::S == 2) {
-        // KC_K2_Q2=0: the round-1 16-bit element path (A/B measurement knob)
+        // KC_K2_Q2 (A/B measurement knob; profiles/r2_k2_bench.txt): 0 = the round-1
+        // 16-bit element path, 1 = the rare queue with the integer flag scan,
+        // 2 = + the HSET2 flag scan (vec_scan16h), 3 (default) = + LEA.HI pushes
         static const int q2 = [] {
             const char* e = getenv("KC_K2_Q2");
-            return e && *e ? atoi(e) : 1;
+            return e && *e ? atoi(e) : 3;
         }();
-        if (!q2) {
+        if (q2 == 0) {
             launch_k2_cfg<DT, 512, 1, 2, 0>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
+            return;
+        }
+        if (q2 == 2) {
+            launch_k2_cfg<DT, 512, 1, 2, 2>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
+            return;
+        }
+        if (q2 == 3) {
+            launch_k2_cfg<DT, 512, 1, 2, 3>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
             return;
         }
     }

@@ -300,3 +300,30 @@ def test_periodic_flush_path(every, ctas):
     r = json.loads(p.stdout.strip().splitlines()[-1])
     assert r["flush_units"] == every and r["bad"] == [], r["bad"][:10]
     assert all(d > 0 for d in r["differing_elems"])
+
+
+@pytest.mark.parametrize("name", ["f16", "bf16"])
+@pytest.mark.parametrize("equal_nan", [False, True])
+def test_k2_16bit_every_pattern_against_neighbours(env, name, equal_nan):
+    """Every one of the 65,536 16-bit patterns as the reference, against itself, its sign
+    flip, its LSB flip, +0, -0, the smallest subnormal and a quiet NaN: the K2 flag scan
+    (HSET2-based by default) must send exactly the elements the oracle counts -- equal
+    NaNs, +0/-0, subnormal vs zero, Inf vs NaN -- so every report field and bitmap bit
+    equals the oracle's."""
+    torch, kc, ctx, orc = env
+    dt = kc.DT[name]
+    pat = np.arange(65536, dtype=np.uint16)
+    qnan = np.uint16(0x7E00 if name == "f16" else 0x7FC0)
+    partners = [pat, pat ^ np.uint16(0x8000), pat ^ np.uint16(1), np.zeros_like(pat), np.full_like(pat, 0x8000),
+                np.full_like(pat, 1), np.full_like(pat, qnan)]
+    ref = np.tile(pat, len(partners))
+    act = np.concatenate(partners)
+    rb, ab = ref.view(np.uint8), act.view(np.uint8)
+    dr, pr = _dev(torch, rb)
+    da, pa = _dev(torch, ab)
+    torch.cuda.synchronize()
+    for tol in ((1e-8, 1e-5), (1e-3, 1e-3), (0.0, 0.0)):
+        reps, bms = ctx.diff([(pr, pa, rb.size, name)], atol=tol[0], rtol=tol[1], equal_nan=equal_nan)
+        exp = orc.diff(rb, ab, dt, atol=tol[0], rtol=tol[1], equal_nan=equal_nan)
+        _same(reps[0], exp.report, f"{name} tol={tol} equal_nan={equal_nan}")
+        assert [int(x) for x in bms[0]] == [int(x) for x in exp.bitmap]
