@@ -242,6 +242,33 @@ kc_status kc_hash(kc_ctx* ctx, const kc_region* regions, size_t n, uint64_t* d_c
 /* Total chunk count of a region list (host helper). */
 uint64_t kc_count_chunks(const kc_region* regions, size_t n);
 
+/* ---- prepared plans (K1 / K2 without per-call host work) ---------------- */
+/* The paper's loop hashes and validates the SAME region and buffer sets again
+ * and again (pre/post manifests, every replay's validation).
+ * A plan validates and uploads the set once; each run is the kernel launches
+ * alone, bit-identical to kc_hash / kc_diff_async on the same inputs.
+ * kc_hash_plan_create: regions as kc_hash (copied; the memory they describe
+ * must stay mapped while the plan is run).  kc_hash_plan_run: as kc_hash
+ * (asynchronous on stream); KC_ERR_ARG when the snapshot digest is requested
+ * for an unsorted/overlapping set.  kc_diff_plan_create: bufs, report_nbytes
+ * and bitmap_word0 as kc_diff_async (copied; bitmap_word0 may be NULL, then
+ * runs take no bitmaps).  kc_diff_plan_run: as kc_diff_async with the plan's
+ * buffers (reports zeroed and finalized; asynchronous).  A plan belongs to the
+ * ctx that created it (KC_ERR_ARG elsewhere) and must be destroyed before it;
+ * destroy(NULL) is a no-op. */
+typedef struct kc_hash_plan kc_hash_plan;
+typedef struct kc_diff_plan kc_diff_plan;
+kc_status kc_hash_plan_create(kc_ctx* ctx, const kc_region* regions, size_t n, kc_hash_plan** out);
+kc_status kc_hash_plan_run(kc_ctx* ctx, const kc_hash_plan* p, uint64_t* d_chunk_hash, uint64_t* d_region_digest,
+                           uint64_t* d_snapshot_digest, void* stream);
+uint64_t kc_hash_plan_chunks(const kc_hash_plan* p);
+kc_status kc_hash_plan_destroy(kc_hash_plan* p);
+kc_status kc_diff_plan_create(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
+                              const uint64_t* report_nbytes, const uint64_t* bitmap_word0, kc_diff_plan** out);
+kc_status kc_diff_plan_run(kc_ctx* ctx, const kc_diff_plan* p, const kc_tolerance* tol, kc_diff_report* d_reports,
+                           uint64_t* d_bitmaps, void* stream);
+kc_status kc_diff_plan_destroy(kc_diff_plan* p);
+
 /* ---- K3 written set (A4) ---------------------------------------------- */
 /* W[k] = (pre[k] != post[k]) for k < n_chunks: d_w_bitmap (device,
  * ceil(C/64) u64, LSB-first) and d_written_count (device, 1 u64).  Async. */

@@ -362,6 +362,12 @@ __global__ void __launch_bounds__(CFG::kThreads, 1)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
+// the same with a shared-window address computed once per thread: cvta per
+// copy cost S2R SR_CgaCtaId + MOV + LEA under each copy's predicate (K1's
+// staging was 8 SASS per 16-byte copy, 17% of the sub-wave K1's samples)
+__device__ __forceinline__ void cp_async16_s(uint32_t saddr, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -397,6 +403,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q = lane >> 2, ql = lane & 3;
     const unsigned qmask = 0xFu << (lane & 28);
     uint8_t* wring = smem + (size_t)w * STAGES * WSTAGE;
+    const uint32_t wring_s = smem_u32(wring);
     const uint64_t ngroups = (C + 7) / 8;
     const uint64_t W = (uint64_t)gridDim.x * WARPS;
     const uint64_t j0 = (uint64_t)w * gridDim.x + blockIdx.x;  // interleaved over CTAs
@@ -428,7 +435,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         }
     };
     auto issue = [&](int stage) {
-        uint8_t* dst = wring + stage * WSTAGE;
+        const uint32_t dst = wring_s + stage * WSTAGE;
 #pragma unroll
         for (int k = 0; k < UPL; ++k) {
             const int u = lane + 32 * k;
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
                 const int qq = u / UPC, off = (u % UPC) * 16;
                 const uint32_t g_off = sf * SL + off;
                 if (g_off < u_bytes[k])
-                    cp_async16(dst + qq * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                    cp_async16_s(dst + qq * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
             }
         }
     };
@@ -562,6 +569,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q = lane >> 2, ql = lane & 3;
     const unsigned qmask = 0xFu << (lane & 28);
     uint8_t* wring = smem + (size_t)w * STAGES * WSTAGE;
+    const uint32_t wring_s = smem_u32(wring);
     const uint64_t ngroups = (C + 7) / 8;
     const uint64_t W = (uint64_t)gridDim.x * WARPS;
     const uint64_t j0 = (uint64_t)w * gridDim.x + blockIdx.x;
@@ -603,7 +611,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         }
     };
     auto issue = [&](int stage) {
-        uint8_t* dst = wring + stage * WSTAGE;
+        const uint32_t dst = wring_s + stage * WSTAGE;
 #pragma unroll
         for (int k = 0; k < UPL; ++k) {
             const int u = lane + 32 * k;
@@ -611,7 +619,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
                 const int slot = u / UPC, off = (u % UPC) * 16;  // slot 0-7 actual, 8-15 reference
                 const uint32_t g_off = sf * SL + off;
                 if (g_off < u_bytes[k])
-                    cp_async16(dst + slot * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                    cp_async16_s(dst + slot * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
             }
         }
     };

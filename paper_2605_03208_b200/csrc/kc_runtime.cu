@@ -598,67 +598,85 @@ uint64_t kc_count_chunks(const kc_region* regions, size_t n) {
 }
 
 // ------------------------------------------------------------------ K1
-static kc_status upload_regions(kc_ctx* ctx, const kc_region* regions, size_t n, cudaStream_t s, uint64_t* C_out) {
-    std::vector<RegionDev> t(n);
-    uint64_t c = 0;
+// Host-side K1 tables of a region list: the device region table, the chunk ->
+// region map (4 B per 64 KiB chunk: one load instead of a binary search per
+// chunk) and, when some region ends in a short chunk, the chunk order (full
+// 64 KiB chunks first, then each region's short last chunk by length,
+// descending, so the 8 chunks a warp hashes together have similar lengths: a
+// group runs as long as its longest chunk).
+struct RegionTables {
+    std::vector<RegionDev> regs;
+    std::vector<uint32_t> map, order;  // order empty = identity
+    uint64_t C = 0;
     bool aligned = true;
+};
+
+static void build_region_tables(const kc_region* regions, size_t n, RegionTables& T) {
+    T.regs.resize(n);
+    uint64_t c = 0;
     for (size_t i = 0; i < n; ++i) {
-        t[i].base = regions[i].base;
-        t[i].size = regions[i].size;
-        t[i].chunk_off = c;
+        T.regs[i].base = regions[i].base;
+        T.regs[i].size = regions[i].size;
+        T.regs[i].chunk_off = c;
         c += (regions[i].size + kChunk - 1) / kChunk;
-        if (regions[i].base & 15) aligned = false;
+        if (regions[i].base & 15) T.aligned = false;
     }
-    *C_out = c;
-    bool same = t.size() == ctx->regs_cached.size() && ctx->regs.p &&
-                (t.empty() || memcmp(t.data(), ctx->regs_cached.data(), t.size() * sizeof(RegionDev)) == 0);
+    T.C = c;
+}
+
+static void build_chunk_tables(RegionTables& T) {
+    const uint64_t c = T.C;
+    const std::vector<RegionDev>& t = T.regs;
+    T.map.assign(c, 0);
+    for (size_t i = 0; i < t.size(); ++i) {
+        const uint64_t n_i = (i + 1 < t.size() ? t[i + 1].chunk_off : c) - t[i].chunk_off;
+        std::fill(T.map.begin() + t[i].chunk_off, T.map.begin() + t[i].chunk_off + n_i, (uint32_t)i);
+    }
+    std::vector<std::pair<uint32_t, uint32_t>> part;  // (length, chunk)
+    for (size_t i = 0; i < t.size(); ++i) {
+        const uint64_t rem = t[i].size % kChunk;
+        if (rem) part.emplace_back((uint32_t)rem, (uint32_t)(t[i].chunk_off + (t[i].size - 1) / kChunk));
+    }
+    T.order.clear();
+    if (part.empty()) return;
+    std::stable_sort(part.begin(), part.end(), [](const std::pair<uint32_t, uint32_t>& a,
+                                                  const std::pair<uint32_t, uint32_t>& b) { return a.first > b.first; });
+    T.order.reserve(c);
+    std::vector<uint8_t> is_part(c, 0);
+    for (auto& pr : part) is_part[pr.second] = 1;
+    for (uint64_t g = 0; g < c; ++g)
+        if (!is_part[g]) T.order.push_back((uint32_t)g);
+    for (auto& pr : part) T.order.push_back(pr.second);
+}
+
+static kc_status upload_regions(kc_ctx* ctx, const kc_region* regions, size_t n, cudaStream_t s, uint64_t* C_out) {
+    RegionTables T;
+    build_region_tables(regions, n, T);
+    *C_out = T.C;
+    bool same = T.regs.size() == ctx->regs_cached.size() && ctx->regs.p &&
+                (T.regs.empty() || memcmp(T.regs.data(), ctx->regs_cached.data(), T.regs.size() * sizeof(RegionDev)) == 0);
     if (!same) {
-        KC_CHECK_CUDA(ctx, ensure(ctx->regs, t.size() * sizeof(RegionDev)), "cudaMalloc(region table)");
-        if (!t.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->regs.p, t.data(), t.size() * sizeof(RegionDev),
+        build_chunk_tables(T);
+        KC_CHECK_CUDA(ctx, ensure(ctx->regs, T.regs.size() * sizeof(RegionDev)), "cudaMalloc(region table)");
+        if (!T.regs.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->regs.p, T.regs.data(), T.regs.size() * sizeof(RegionDev),
                                                cudaMemcpyHostToDevice, s),
                           "upload region table");
-        // chunk -> region map (4 B per 64 KiB chunk): one load instead of a binary search per chunk
-        std::vector<uint32_t> map(c);
-        for (size_t i = 0; i < t.size(); ++i) {
-            const uint64_t n_i = (i + 1 < t.size() ? t[i + 1].chunk_off : c) - t[i].chunk_off;
-            std::fill(map.begin() + t[i].chunk_off, map.begin() + t[i].chunk_off + n_i, (uint32_t)i);
-        }
-        KC_CHECK_CUDA(ctx, ensure(ctx->chunk_map, std::max<size_t>(1, map.size()) * 4), "cudaMalloc(chunk map)");
-        if (!map.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->chunk_map.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, s),
+        KC_CHECK_CUDA(ctx, ensure(ctx->chunk_map, std::max<size_t>(1, T.map.size()) * 4), "cudaMalloc(chunk map)");
+        if (!T.map.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->chunk_map.p, T.map.data(), T.map.size() * 4, cudaMemcpyHostToDevice,
+                                               s),
                           "upload chunk map");
-        // chunk order for K1/K6: full 64 KiB chunks first, then each region's
-        // short last chunk by length, descending, so the 8 chunks a warp hashes
-        // together have similar lengths (a group runs as long as its longest
-        // chunk).  Identity (no table) when every region is a multiple of 64 KiB.
-        std::vector<std::pair<uint32_t, uint32_t>> part;  // (length, chunk)
-        for (size_t i = 0; i < t.size(); ++i) {
-            const uint64_t rem = t[i].size % kChunk;
-            if (rem) part.emplace_back((uint32_t)rem, (uint32_t)(t[i].chunk_off + (t[i].size - 1) / kChunk));
-        }
-        ctx->has_order = !part.empty();
+        ctx->has_order = !T.order.empty();
         if (ctx->has_order) {
-            std::stable_sort(part.begin(), part.end(), [](const std::pair<uint32_t, uint32_t>& a,
-                                                          const std::pair<uint32_t, uint32_t>& b) {
-                return a.first > b.first;
-            });
-            std::vector<uint32_t> order;
-            order.reserve(c);
-            size_t pi = 0;
-            std::vector<uint8_t> is_part(c, 0);
-            for (auto& pr : part) is_part[pr.second] = 1;
-            for (uint64_t g = 0; g < c; ++g)
-                if (!is_part[g]) order.push_back((uint32_t)g);
-            for (; pi < part.size(); ++pi) order.push_back(part[pi].second);
-            KC_CHECK_CUDA(ctx, ensure(ctx->chunk_order, order.size() * 4), "cudaMalloc(chunk order)");
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->chunk_order.p, order.data(), order.size() * 4,
+            KC_CHECK_CUDA(ctx, ensure(ctx->chunk_order, T.order.size() * 4), "cudaMalloc(chunk order)");
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->chunk_order.p, T.order.data(), T.order.size() * 4,
                                                cudaMemcpyHostToDevice, s),
                           "upload chunk order");
-            cudaStreamSynchronize(s);  // `order` is pageable and goes out of scope
         }
-        ctx->regs_cached.swap(t);
-        ctx->regs_aligned = aligned;
+        cudaStreamSynchronize(s);  // the tables are pageable and go out of scope
+        ctx->regs_cached.swap(T.regs);
+        ctx->regs_aligned = T.aligned;
     }
     return KC_OK;
 }
@@ -765,6 +783,71 @@ static int elem_size(int dt) {
 
 // K2 planning + launch.  filter_chunk0 (host, per buffer) and d_filter (device
 // dirty bitmap) select the filtered mode that skips clean chunks (F2).
+// K2 plan: validate the buffers, order segments by dtype (stable) so each dtype
+// is one launch, number the 16 KiB units, and build the per-report metadata.
+struct DiffTables {
+    std::vector<SegDev> segs;
+    std::vector<ReportMeta> meta;
+    std::vector<DiffGroup> groups;
+    uint64_t bitmap_words = 0;
+};
+
+static kc_status build_diff_tables(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
+                                   const uint64_t* report_nbytes, const uint64_t* bitmap_word0,
+                                   const uint64_t* filter_chunk0, DiffTables& T) {
+    T.meta.resize(n_reports);
+    std::vector<int> rep_dt(n_reports, -1);
+    std::vector<size_t> order;
+    order.reserve(n_bufs);
+    for (size_t i = 0; i < n_bufs; ++i) {
+        const kc_buffer& b = bufs[i];
+        const int es = elem_size(b.dtype);
+        if (es == 0) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: bad dtype %d", i, b.dtype);
+        if (b.nbytes % es) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: %llu bytes is not a multiple of "
+                                          "the element size %d", i, (unsigned long long)b.nbytes, es);
+        if (b.report < 0 || (size_t)b.report >= n_reports)
+            return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: report index %d out of range", i, b.report);
+        if (rep_dt[b.report] >= 0 && rep_dt[b.report] != b.dtype)
+            return set_err(ctx, KC_ERR_ARG, "kc_diff: report %d mixes dtypes", b.report);
+        rep_dt[b.report] = b.dtype;
+        if (b.nbytes == 0) continue;
+        if (!b.ref || !b.act) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: null VA", i);
+        order.push_back(i);
+    }
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return bufs[a].dtype < bufs[b].dtype; });
+    T.segs.reserve(order.size());
+    uint64_t U = 0;
+    for (size_t i : order) {
+        const kc_buffer& b = bufs[i];
+        SegDev d;
+        d.ref = b.ref;
+        d.act = b.act;
+        d.nbytes = b.nbytes;
+        d.bitmap_word0 = bitmap_word0 ? bitmap_word0[b.report] : 0;
+        d.bitmap_chunk0 = b.bitmap_chunk0;
+        d.unit_off = U;
+        d.filter_chunk0 = filter_chunk0 ? filter_chunk0[i] : 0;
+        d.dtype = b.dtype;
+        d.report = b.report;
+        const uint64_t nu = (b.nbytes + kDiffUnit - 1) / kDiffUnit;
+        if (T.groups.empty() || T.groups.back().dtype != b.dtype)
+            T.groups.push_back(DiffGroup{b.dtype, (int32_t)T.segs.size(), 0, U, 0});
+        T.groups.back().n_segs += 1;
+        T.groups.back().n_units += nu;
+        U += nu;
+        T.segs.push_back(d);
+    }
+    for (size_t j = 0; j < n_reports; ++j) {
+        T.meta[j].nbytes = report_nbytes[j];
+        T.meta[j].dtype = rep_dt[j] < 0 ? KC_DT_BYTES : rep_dt[j];
+        if (bitmap_word0) {
+            const uint64_t w = (report_nbytes[j] + kChunk - 1) / kChunk;
+            T.bitmap_words = std::max(T.bitmap_words, bitmap_word0[j] + (w + 63) / 64);
+        }
+    }
+    return KC_OK;
+}
+
 static kc_status diff_launch(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
                              const uint64_t* report_nbytes, const uint64_t* bitmap_word0, const kc_tolerance* tol,
                              kc_diff_report* d_reports, uint64_t* d_bitmaps, void* stream,
@@ -810,66 +893,19 @@ static kc_status diff_launch(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, 
         groups = ctx->diff_groups;
         bitmap_words = ctx->diff_bitmap_words;
     } else {
-        std::vector<ReportMeta> meta(n_reports);
-        std::vector<int> rep_dt(n_reports, -1);
-        // validate, then order segments by dtype (stable) so each dtype is one launch
-        std::vector<size_t> order;
-        order.reserve(n_bufs);
-        for (size_t i = 0; i < n_bufs; ++i) {
-            const kc_buffer& b = bufs[i];
-            const int es = elem_size(b.dtype);
-            if (es == 0) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: bad dtype %d", i, b.dtype);
-            if (b.nbytes % es) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: %llu bytes is not a multiple of "
-                                              "the element size %d", i, (unsigned long long)b.nbytes, es);
-            if (b.report < 0 || (size_t)b.report >= n_reports)
-                return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: report index %d out of range", i, b.report);
-            if (rep_dt[b.report] >= 0 && rep_dt[b.report] != b.dtype)
-                return set_err(ctx, KC_ERR_ARG, "kc_diff: report %d mixes dtypes", b.report);
-            rep_dt[b.report] = b.dtype;
-            if (b.nbytes == 0) continue;
-            if (!b.ref || !b.act) return set_err(ctx, KC_ERR_ARG, "kc_diff: buffer %zu: null VA", i);
-            order.push_back(i);
-        }
-        std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return bufs[a].dtype < bufs[b].dtype; });
-        std::vector<SegDev> segs;
-        segs.reserve(order.size());
-        uint64_t U = 0;
-        for (size_t i : order) {
-            const kc_buffer& b = bufs[i];
-            SegDev d;
-            d.ref = b.ref;
-            d.act = b.act;
-            d.nbytes = b.nbytes;
-            d.bitmap_word0 = bitmap_word0 ? bitmap_word0[b.report] : 0;
-            d.bitmap_chunk0 = b.bitmap_chunk0;
-            d.unit_off = U;
-            d.filter_chunk0 = filter_chunk0 ? filter_chunk0[i] : 0;
-            d.dtype = b.dtype;
-            d.report = b.report;
-            const uint64_t nu = (b.nbytes + kDiffUnit - 1) / kDiffUnit;
-            if (groups.empty() || groups.back().dtype != b.dtype)
-                groups.push_back(DiffGroup{b.dtype, (int32_t)segs.size(), 0, U, 0});
-            groups.back().n_segs += 1;
-            groups.back().n_units += nu;
-            U += nu;
-            segs.push_back(d);
-        }
-        for (size_t j = 0; j < n_reports; ++j) {
-            meta[j].nbytes = report_nbytes[j];
-            meta[j].dtype = rep_dt[j] < 0 ? KC_DT_BYTES : rep_dt[j];
-            if (bitmap_word0) {
-                const uint64_t w = (report_nbytes[j] + kChunk - 1) / kChunk;
-                bitmap_words = std::max(bitmap_words, bitmap_word0[j] + (w + 63) / 64);
-            }
-        }
-        KC_CHECK_CUDA(ctx, ensure(ctx->segs, segs.size() * sizeof(SegDev)), "cudaMalloc(segments)");
-        KC_CHECK_CUDA(ctx, ensure(ctx->meta, meta.size() * sizeof(ReportMeta)), "cudaMalloc(meta)");
-        if (!segs.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(SegDev),
+        DiffTables T;
+        kc_status st = build_diff_tables(ctx, bufs, n_bufs, n_reports, report_nbytes, bitmap_word0, filter_chunk0, T);
+        if (st != KC_OK) return st;
+        KC_CHECK_CUDA(ctx, ensure(ctx->segs, T.segs.size() * sizeof(SegDev)), "cudaMalloc(segments)");
+        KC_CHECK_CUDA(ctx, ensure(ctx->meta, T.meta.size() * sizeof(ReportMeta)), "cudaMalloc(meta)");
+        if (!T.segs.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->segs.p, T.segs.data(), T.segs.size() * sizeof(SegDev),
                                                cudaMemcpyHostToDevice, s), "upload segments");
-        if (!meta.empty())
-            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->meta.p, meta.data(), meta.size() * sizeof(ReportMeta),
+        if (!T.meta.empty())
+            KC_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->meta.p, T.meta.data(), T.meta.size() * sizeof(ReportMeta),
                                                cudaMemcpyHostToDevice, s), "upload meta");
+        groups = T.groups;
+        bitmap_words = T.bitmap_words;
         ctx->diff_key.swap(key);
         ctx->diff_groups = groups;
         ctx->diff_bitmap_words = bitmap_words;
@@ -895,6 +931,158 @@ kc_status kc_diff_async(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_
     KC_ENTER(ctx);
     return diff_launch(ctx, bufs, n_bufs, n_reports, report_nbytes, bitmap_word0, tol, d_reports, d_bitmaps, stream,
                        nullptr, nullptr);
+}
+
+// ------------------------------------------------------------------ prepared plans (K1, K2)
+// A region / buffer set validated and uploaded once, owned by the plan: every
+// later run is the launches alone, with no per-call host work (the memcmp of
+// the same-input cache is 0.19 ms at 100k regions, as long as the kernel).
+struct kc_hash_plan {
+    kc_ctx* ctx = nullptr;
+    size_t n = 0;
+    uint64_t C = 0;
+    bool aligned = true, sorted = true;
+    void *regs = nullptr, *map = nullptr, *order = nullptr, *scratch = nullptr;
+};
+
+struct kc_diff_plan {
+    kc_ctx* ctx = nullptr;
+    size_t n_reports = 0;
+    bool has_bitmaps = false;
+    std::vector<DiffGroup> groups;
+    uint64_t bitmap_words = 0;
+    void *segs = nullptr, *meta = nullptr;
+};
+
+static cudaError_t plan_upload(void** dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess && bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    return e;
+}
+
+kc_status kc_hash_plan_destroy(kc_hash_plan* p) {
+    if (!p) return KC_OK;
+    if (p->ctx) bind_device(p->ctx);
+    for (void* d : {p->regs, p->map, p->order, p->scratch})
+        if (d) cudaFree(d);
+    delete p;
+    return KC_OK;
+}
+
+kc_status kc_hash_plan_create(kc_ctx* ctx, const kc_region* regions, size_t n, kc_hash_plan** out) {
+    KC_ENTER(ctx);
+    if (!out || (n && !regions)) return set_err(ctx, KC_ERR_ARG, "kc_hash_plan_create: null pointer");
+    *out = nullptr;
+    auto* p = new kc_hash_plan;
+    p->ctx = ctx;
+    p->n = n;
+    for (size_t i = 0; i < n; ++i) {
+        if (regions[i].size == 0) {
+            delete p;
+            return set_err(ctx, KC_ERR_ARG, "kc_hash_plan_create: region %zu has size 0", i);
+        }
+        if (i > 0 && regions[i].base < regions[i - 1].base + regions[i - 1].size) p->sorted = false;
+    }
+    RegionTables T;
+    build_region_tables(regions, n, T);
+    build_chunk_tables(T);
+    p->C = T.C;
+    p->aligned = T.aligned;
+    cudaError_t e = plan_upload(&p->regs, T.regs.data(), T.regs.size() * sizeof(RegionDev));
+    if (e == cudaSuccess) e = plan_upload(&p->map, T.map.data(), T.map.size() * 4);
+    if (e == cudaSuccess && !T.order.empty()) e = plan_upload(&p->order, T.order.data(), T.order.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&p->scratch, 24 * n + 8);
+    if (e != cudaSuccess) {
+        kc_hash_plan_destroy(p);
+        return cuda_err(ctx, e, "kc_hash_plan_create: device tables");
+    }
+    *out = p;
+    return KC_OK;
+}
+
+uint64_t kc_hash_plan_chunks(const kc_hash_plan* p) { return p ? p->C : 0; }
+
+kc_status kc_hash_plan_run(kc_ctx* ctx, const kc_hash_plan* p, uint64_t* d_chunk_hash, uint64_t* d_region_digest,
+                           uint64_t* d_snapshot_digest, void* stream) {
+    KC_ENTER(ctx);
+    if (!p || p->ctx != ctx) return set_err(ctx, KC_ERR_ARG, "kc_hash_plan_run: plan of another context");
+    if (p->C && !d_chunk_hash) return set_err(ctx, KC_ERR_ARG, "kc_hash_plan_run: d_chunk_hash is NULL");
+    if (d_snapshot_digest && !p->sorted)
+        return set_err(ctx, KC_ERR_ARG, "kc_hash_plan_run: regions not sorted/non-overlapping (snapshot digest, R25)");
+    cudaStream_t s = (cudaStream_t)stream;
+    KC_CHECK_CUDA(ctx, launch_hash((const RegionDev*)p->regs, (int)p->n, p->C, p->aligned, d_chunk_hash,
+                                   (const uint32_t*)p->map, ctx->num_sms, s, (const uint32_t*)p->order),
+                  "launch K1 (plan)");
+    if (p->C) ctx->launches += 1;
+    if (d_region_digest || d_snapshot_digest) {
+        KC_CHECK_CUDA(ctx, launch_digests((const RegionDev*)p->regs, (int)p->n, d_chunk_hash, d_region_digest,
+                                          (uint8_t*)p->scratch, d_snapshot_digest, s),
+                      "launch digests (plan)");
+        if (p->n) ctx->launches += d_snapshot_digest ? 2 : 1;
+        if (d_snapshot_digest && p->n == 0)
+            KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_snapshot_digest, 0, 8, s), "snapshot digest of nothing");
+    }
+    return KC_OK;
+}
+
+kc_status kc_diff_plan_destroy(kc_diff_plan* p) {
+    if (!p) return KC_OK;
+    if (p->ctx) bind_device(p->ctx);
+    if (p->segs) cudaFree(p->segs);
+    if (p->meta) cudaFree(p->meta);
+    delete p;
+    return KC_OK;
+}
+
+kc_status kc_diff_plan_create(kc_ctx* ctx, const kc_buffer* bufs, size_t n_bufs, size_t n_reports,
+                              const uint64_t* report_nbytes, const uint64_t* bitmap_word0, kc_diff_plan** out) {
+    KC_ENTER(ctx);
+    if (!out || (n_bufs && !bufs) || (n_reports && !report_nbytes))
+        return set_err(ctx, KC_ERR_ARG, "kc_diff_plan_create: null pointer");
+    *out = nullptr;
+    DiffTables T;
+    kc_status st = build_diff_tables(ctx, bufs, n_bufs, n_reports, report_nbytes, bitmap_word0, nullptr, T);
+    if (st != KC_OK) return st;
+    auto* p = new kc_diff_plan;
+    p->ctx = ctx;
+    p->n_reports = n_reports;
+    p->has_bitmaps = bitmap_word0 != nullptr;
+    p->groups = T.groups;
+    p->bitmap_words = T.bitmap_words;
+    cudaError_t e = plan_upload(&p->segs, T.segs.data(), T.segs.size() * sizeof(SegDev));
+    if (e == cudaSuccess) e = plan_upload(&p->meta, T.meta.data(), T.meta.size() * sizeof(ReportMeta));
+    if (e != cudaSuccess) {
+        kc_diff_plan_destroy(p);
+        return cuda_err(ctx, e, "kc_diff_plan_create: device tables");
+    }
+    *out = p;
+    return KC_OK;
+}
+
+kc_status kc_diff_plan_run(kc_ctx* ctx, const kc_diff_plan* p, const kc_tolerance* tol, kc_diff_report* d_reports,
+                           uint64_t* d_bitmaps, void* stream) {
+    KC_ENTER(ctx);
+    if (!p || p->ctx != ctx) return set_err(ctx, KC_ERR_ARG, "kc_diff_plan_run: plan of another context");
+    if (p->n_reports && !d_reports) return set_err(ctx, KC_ERR_ARG, "kc_diff_plan_run: d_reports is NULL");
+    if (d_bitmaps && !p->has_bitmaps)
+        return set_err(ctx, KC_ERR_ARG, "kc_diff_plan_run: plan was created without bitmap_word0");
+    const kc_tolerance deft = {1e-8, 1e-5, 0, 0};  // numpy defaults (reading R14)
+    if (!tol) tol = &deft;
+    if (!(tol->atol >= 0.0) || !(tol->rtol >= 0.0))
+        return set_err(ctx, KC_ERR_ARG, "kc_diff_plan_run: tolerances must be >= 0 (atol %g, rtol %g)", tol->atol,
+                       tol->rtol);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->n_reports)
+        KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_reports, 0, p->n_reports * sizeof(kc_diff_report), s), "zero reports");
+    if (d_bitmaps && p->bitmap_words)
+        KC_CHECK_CUDA(ctx, cudaMemsetAsync(d_bitmaps, 0, p->bitmap_words * 8, s), "zero bitmaps");
+    KC_CHECK_CUDA(ctx, launch_diff((const SegDev*)p->segs, p->groups.data(), (int)p->groups.size(),
+                                   (const ReportMeta*)p->meta, (int)p->n_reports, d_reports, d_bitmaps, tol->atol,
+                                   tol->rtol, tol->equal_nan, ctx->num_sms, s, nullptr),
+                  "launch K2 (plan)");
+    for (auto& g : p->groups) ctx->launches += g.n_units ? 1 : 0;
+    if (p->n_reports) ctx->launches += 1;
+    return KC_OK;
 }
 
 // K5 pair table + chunk -> pair map (4 B per chunk), uploaded only when the pair

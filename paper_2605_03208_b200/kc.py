@@ -39,6 +39,8 @@ EXPORTED = [
     "kc_create", "kc_destroy", "kc_last_error", "kc_abi_version", "kc_build_info", "kc_status_str",
     "kc_kernel_launches", "kc_track",
     "kc_regions", "kc_alloc", "kc_free", "kc_track_install", "kc_track_uninstall", "kc_hash", "kc_count_chunks",
+    "kc_hash_plan_create", "kc_hash_plan_run", "kc_hash_plan_chunks", "kc_hash_plan_destroy",
+    "kc_diff_plan_create", "kc_diff_plan_run", "kc_diff_plan_destroy",
     "kc_written", "kc_diff_async", "kc_hash_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
     "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
@@ -233,6 +235,13 @@ def lib() -> ctypes.CDLL:
         "kc_peer_export": (st, [V, U64, P(I32), P(U64)]),
         "kc_peer_import": (st, [V, I32, I32, U64, U64, P(U64)]),
         "kc_peer_release": (st, [V, U64]),
+        "kc_hash_plan_create": (st, [V, P(Region), SZ, P(V)]),
+        "kc_hash_plan_run": (st, [V, V, V, V, V, V]),
+        "kc_hash_plan_chunks": (U64, [V]),
+        "kc_hash_plan_destroy": (st, [V]),
+        "kc_diff_plan_create": (st, [V, P(Buffer), SZ, SZ, P(U64), P(U64), P(V)]),
+        "kc_diff_plan_run": (st, [V, V, P(Tolerance), V, V, V]),
+        "kc_diff_plan_destroy": (st, [V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -240,6 +249,44 @@ def lib() -> ctypes.CDLL:
         fn.argtypes = args
     _lib = L
     return L
+
+
+class HashPlan:
+    """A prepared K1 region set (kc_hash_plan_*): run() is the launches alone."""
+
+    def __init__(self, ctx: "Context", h: ctypes.c_void_p):
+        self.ctx, self._h = ctx, h
+
+    @property
+    def chunks(self) -> int:
+        return int(lib().kc_hash_plan_chunks(self._h))
+
+    def run(self, d_chunk_hash: int, d_region_digest: int = 0, d_snapshot_digest: int = 0, stream: int = 0):
+        self.ctx._check(lib().kc_hash_plan_run(self.ctx._h, self._h, d_chunk_hash or None, d_region_digest or None,
+                                               d_snapshot_digest or None, stream or None), "kc_hash_plan_run")
+
+    def close(self):
+        if self._h:
+            lib().kc_hash_plan_destroy(self._h)
+            self._h = None
+
+
+class DiffPlan:
+    """A prepared K2 buffer set (kc_diff_plan_*): run() is the launches alone."""
+
+    def __init__(self, ctx: "Context", h: ctypes.c_void_p):
+        self.ctx, self._h = ctx, h
+
+    def run(self, d_reports: int, d_bitmaps: int = 0, atol: float = 1e-8, rtol: float = 1e-5,
+            equal_nan: bool = False, stream: int = 0):
+        tol = Tolerance(atol, rtol, int(bool(equal_nan)), 0)
+        self.ctx._check(lib().kc_diff_plan_run(self.ctx._h, self._h, ctypes.byref(tol), d_reports, d_bitmaps or None,
+                                               stream or None), "kc_diff_plan_run")
+
+    def close(self):
+        if self._h:
+            lib().kc_diff_plan_destroy(self._h)
+            self._h = None
 
 
 def status_name(s: int) -> str:
@@ -523,6 +570,24 @@ class Context:
         n = len(regions) if n is None else n
         self._check(lib().kc_hash(self._h, arr, n, d_chunk_hash or None, d_region_digest or None,
                                   d_snapshot_digest or None, stream or None), "kc_hash")
+
+    def hash_plan(self, regions) -> "HashPlan":
+        """kc_hash_plan_create: the region set validated and uploaded once (run it many times)."""
+        arr = _regions(regions)
+        h = ctypes.c_void_p()
+        self._check(lib().kc_hash_plan_create(self._h, arr, len(regions), ctypes.byref(h)), "kc_hash_plan_create")
+        return HashPlan(self, h)
+
+    def diff_plan(self, bufs, n_reports: int, report_nbytes: Sequence[int],
+                  bitmap_word0: Sequence[int] | None = None) -> "DiffPlan":
+        """kc_diff_plan_create: the buffer set (as kc_diff_async) validated and uploaded once."""
+        arr = self._buffers(bufs)
+        rn = (ctypes.c_uint64 * max(1, n_reports))(*report_nbytes)
+        w0 = (ctypes.c_uint64 * max(1, n_reports))(*bitmap_word0) if bitmap_word0 is not None else None
+        h = ctypes.c_void_p()
+        self._check(lib().kc_diff_plan_create(self._h, arr, len(bufs), n_reports, rn, w0, ctypes.byref(h)),
+                    "kc_diff_plan_create")
+        return DiffPlan(self, h)
 
     def written(self, d_pre: int, d_post: int, n_chunks: int, d_bitmap: int, d_count: int = 0, stream: int = 0):
         self._check(lib().kc_written(self._h, d_pre, d_post, n_chunks, d_bitmap, d_count or None, stream or None),
