@@ -45,3 +45,22 @@ def test_c4_host_sample_is_stratified_and_bounded():
     assert all(r.size == a.size and r.size % 2 == 0 for r, a, _ in s)
     assert sum(r.size for r, _, _ in s) <= 24 * 2**20 + 185 * 65536
     assert {dt for _, _, dt in s} == {bench.DTC["bf16"], bench.DTC["u64"], bench.DTC["i32"], bench.DTC["f32"]}
+
+
+def test_oracle_rates_are_bounded_and_consistent():
+    """bench_configs.oracle_rates: the oracle on host threads over (ref, act, dtype) pairs;
+    max_bytes keeps only the first pieces, and the step mix is 4N / (2N/H + 2N/D)."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import bench_configs as bc
+    rng = np.random.default_rng(0)
+    pairs = [(rng.integers(0, 256, 6 << 20, dtype=np.uint8), None, 0)]
+    pairs = [(r, r.copy(), 0) for r, _, _ in pairs]
+    r1 = bc.oracle_rates(pairs, 2, 0.0)
+    assert r1["bytes"] == 6 << 20 and r1["hash_gbs"] > 0 and r1["diff_gbs"] > 0
+    H, D = r1["hash_gbs"], r1["diff_gbs"]
+    assert abs(r1["step_mix_gbs"] - 4 / (2 / H + 2 / D)) < 1e-9 * r1["step_mix_gbs"]
+    r2 = bc.oracle_rates(pairs, 1, 0.0, max_bytes=bc.PIECE)
+    assert r2["bytes"] == bc.PIECE
+    info = bc.host_info()
+    assert info["nproc"] == (os.cpu_count() or 1)

@@ -16,3 +16,6 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
     > "$O/k1_ncu.log" 2>&1
 [ "${SKIP_K5:-0}" = 1 ] || ncu --set full --clock-control none --import-source on -k regex:k5_hash_cmp -c 1 -o "$O/k5_bench" $B \
     > "$O/k5_ncu.log" 2>&1
+for r in k2_bench k1_bench k5_bench; do
+    [ -f "$O/$r.ncu-rep" ] && python tools/ncu_summary.py "$O/$r.ncu-rep" > "$O/${r}_summary.txt" 2>&1
+done
