@@ -1029,27 +1029,29 @@ __device__ __forceinline__ void elem16(uint32_t r, uint32_t a, Acc& acc, double 
 // (Inf/NaN, zeros, far exponents, opposite signs, equal bits, an ambiguous
 // isclose, a max_rel candidate) returns true: the rare queue runs elem16 on it.
 template <int DT>
-__device__ __forceinline__ bool elem16_rare(uint32_t t, Acc& acc) {
-    const uint32_t hi = t >> 16, lo = t & 0xFFFFu;
+__device__ __forceinline__ bool elem16_rare(uint32_t t, uint32_t xs, Acc& acc) {
+    // tl / th: the reference / actual bits in the high half; xs = t ^ tl, whose high
+    // half is a ^ r (bit 31: the signs differ); computed once by the caller
+    const uint32_t tl = t << 16, th = t & 0xFFFF0000u;
     float av, rv;
     if constexpr (DT == KC_DT_BF16) {
-        av = __uint_as_float(t & 0xFFFF0000u);
-        rv = __uint_as_float(t << 16);
+        av = __uint_as_float(th);
+        rv = __uint_as_float(tl);
     } else {
-        av = __half2float(__ushort_as_half((unsigned short)hi));
-        rv = __half2float(__ushort_as_half((unsigned short)lo));
+        av = __half2float(__ushort_as_half((unsigned short)(t >> 16)));
+        rv = __half2float(__ushort_as_half((unsigned short)(t & 0xFFFFu)));
     }
     constexpr float RATIO = DT == KC_DT_F16 ? 8192.f : 65536.f;  // 2^KMAX
     const float d = fabsf(__fsub_rn(av, rv));
     const float ar = fabsf(rv), aa = fabsf(av);
     const bool close_lo = d <= __fadd_rd(acc.alo, __fmul_rd(acc.rlo, ar));
     const bool far_hi = d > __fadd_ru(acc.ahi, __fmul_ru(acc.rhi, ar));
-    const bool common = (ar < __fmul_rn(RATIO, aa)) & (aa < __fmul_rn(RATIO, ar)) &
-                        (((t ^ (t << 16)) & 0x80000000u) == 0) & (d != 0.f) & (close_lo != far_hi) &
-                        (d <= __fmul_rd(acc.mrel32, ar));
+    const bool common = (ar < __fmul_rn(RATIO, aa)) & (aa < __fmul_rn(RATIO, ar)) & ((int)xs >= 0) &
+                        (d != 0.f) & (close_lo != far_hi) & (d <= __fmul_rd(acc.mrel32, ar));
     if (common) {
         acc.delems += 1;
-        acc.mulp16 = max(acc.mulp16, (uint32_t)abs((int)hi - (int)lo));
+        // same signs: |bits(a) - bits(r)| < 2^15, so (th - tl) = (a - r) * 2^16 fits an int
+        acc.mulp16 = max(acc.mulp16, (uint32_t)abs((int)th - (int)tl) >> 16);
         acc.mabs32 = fmaxf(acc.mabs32, d);
         acc.fail += far_hi;
     }
@@ -1410,12 +1412,13 @@ __device__ __forceinline__ void q_drain16(uint32_t* q, uint32_t& qn, uint32_t* r
                                           double atol, double rtol, int equal_nan, int lane) {
     __syncwarp();
     const uint32_t full = qn & ~31u, rem = qn - full;
-    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t lt;  // lanes below this one (a special register: not re-derived inside the loop)
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
     for (uint32_t i = lane; i < full; i += 32) {
         const uint32_t t = q[i];
-        const uint32_t x = (t ^ (t >> 16)) & 0xFFFFu;  // bytes differ: every queued element is counted here
-        acc.dbytes += (uint32_t)((x & 0xFFu) != 0) + (uint32_t)(x > 0xFFu);
-        const bool rare = elem16_rare<DT>(t, acc);
+        const uint32_t xs = t ^ (t << 16);  // high half: a ^ r; every queued element's bytes are counted here
+        acc.dbytes += (uint32_t)((xs & 0x00FF0000u) != 0) + (uint32_t)(xs >= 0x01000000u);
+        const bool rare = elem16_rare<DT>(t, xs, acc);
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, rare);
         if (rare) rq[rn + __popc(bal & lt)] = t;
         rn += __popc(bal);
