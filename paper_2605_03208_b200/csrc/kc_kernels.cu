@@ -365,8 +365,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // the same with a shared-window address computed once per thread: cvta per
 // copy cost S2R SR_CgaCtaId + MOV + LEA under each copy's predicate (K1's
 // staging was 8 SASS per 16-byte copy, 17% of the sub-wave K1's samples)
+// KC_CP_L2_PREFETCH=1 adds the .L2::256B prefetch qualifier: measured neutral
+// on B200 (K1 over 2 GiB 6,394 vs 6,357 GB/s; the 30 GB pool 6,633 vs 6,623;
+// K5 6,264 vs 6,282), so off by default
+#ifndef KC_CP_L2_PREFETCH
+#define KC_CP_L2_PREFETCH 0
+#endif
 __device__ __forceinline__ void cp_async16_s(uint32_t saddr, const void* gmem) {
+#if KC_CP_L2_PREFETCH
+    // L2::256B: the L2 fetches whole 256-byte blocks (a warp's copy instruction
+    // covers 512 contiguous bytes of one chunk)
+    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(saddr), "l"(gmem) : "memory");
+#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gmem) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>

@@ -104,6 +104,34 @@ def main():
         c0, w0 = c0 + nch[j], w0 + words[j]
     print("K5 + filtered K2 ok", flush=True)
 
+    # prepared plans (K1 / K2 from plan-owned tables) and the byte-exact host-reference
+    # validation (staging ring on the copy stream, K2 accumulating over pieces)
+    hp = ctx.hash_plan(regions)
+    hp.run(h.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(u64(h), exp), "K1 plan != oracle"
+    hp.close()
+    nbs = [r.size for _, r, _ in pairs]
+    w0s = list(np.cumsum([0] + words[:-1]))
+    dp = ctx.diff_plan(kb, len(kb), nbs, w0s)
+    dp.run(d_rep.data_ptr(), d_bm.data_ptr())
+    torch.cuda.synchronize()
+    raw = d_rep.cpu().numpy().tobytes()
+    for j, (dtname, r, a) in enumerate(pairs):
+        e = oracle.diff(r, a, oracle.DTYPE_NAMES.index(dtname))
+        _same(kc.DiffReport.from_buffer_copy(raw[120 * j:120 * (j + 1)]).as_dict(), e.report, f"K2 plan {dtname}")
+    dp.close()
+    hostb, hb = [], []
+    for (dtname, r, a), (pr, pa, nb, _) in zip(pairs, kb):
+        hr = torch.from_numpy(r).pin_memory()
+        hostb.append(hr)
+        hb.append((hr.data_ptr(), pa, nb, dtname))
+    reps, bms, moved = ctx.validate_host_ref(hb, 0)
+    assert moved == sum(nbs)
+    for j, (dtname, r, a) in enumerate(pairs):
+        _same(reps[j], oracle.diff(r, a, oracle.DTYPE_NAMES.index(dtname)).report, f"byte-exact host ref {dtname}")
+    print("plans + byte-exact host-reference validation ok", flush=True)
+
     # K6 on the CpA ring: a 640 MiB region next to the c1 closure, captured into HBM,
     # restored at the same VAs (fused restore), replayed and validated
     sizes = [s.size for s in synth.C1_SPECS] + [640 * 2**20]

@@ -164,3 +164,36 @@ def test_host_ref_byte_exact_mode_streams_every_byte(env):
     want = np.concatenate([orc.chunk_hashes(a, threads=8) for a in acts])
     assert np.array_equal(d_man.cpu().numpy().view(np.uint64), want)
     assert reps[2]["differing_elems"] == 8 and reps[2]["nan_act"] == 1
+
+
+def test_host_ref_byte_exact_packing_and_edges(env):
+    """Byte-exact mode: many small buffers packed into shared staging pieces, one buffer
+    exactly one piece long (256 MiB) right after them (so it starts mid-piece and is cut),
+    a 1-byte buffer, an empty call.  Every report and bitmap equals the oracle's."""
+    torch, kc, ctx, orc = env
+    reps, bms, moved = ctx.validate_host_ref([], 0)
+    assert reps == [] and moved == 0
+    rng = np.random.default_rng(11)
+    sizes = [int(x) for x in rng.integers(1, 3 * CH, size=300)] + [256 << 20, 1, 5 * CH + 3]
+    refs, acts, bufs, keep = [], [], [], []
+    for i, n in enumerate(sizes):
+        r = rng.integers(0, 256, n, dtype=np.uint8)
+        a = r.copy()
+        if i % 3 == 0:
+            a[rng.integers(0, n)] ^= 0x40
+        if n == 256 << 20:
+            a[[0, CH - 1, (128 << 20) + 5, n - 1]] ^= 1
+        h = torch.from_numpy(r).pin_memory()
+        d = torch.from_numpy(a).cuda()
+        keep += [h, d]
+        refs.append(r)
+        acts.append(a)
+        bufs.append((h.data_ptr(), d.data_ptr(), n, "bytes"))
+    torch.cuda.synchronize()
+    reps, bms, moved = ctx.validate_host_ref(bufs, 0)
+    assert moved == sum(sizes)
+    for k, (r, a) in enumerate(zip(refs, acts)):
+        exp = orc.diff(r, a, orc.DT_BYTES)
+        for f in FIELDS:
+            assert reps[k][f] == exp.report[f], (k, sizes[k], f, reps[k][f], exp.report[f])
+        assert [int(x) for x in bms[k]] == [int(x) for x in exp.bitmap], (k, sizes[k])
