@@ -50,17 +50,26 @@ __device__ __forceinline__ uint64_t xround(uint64_t acc, uint64_t x) {
 // the XXH64 lane seed, and ends with yfinal(y) = rotl(y, 31)*P1 = the lane's
 // accumulator.  Same arithmetic mod 2^64, reordered: results are identical.
 __device__ __forceinline__ uint64_t ystep(uint64_t y, uint64_t x) {
-    const uint64_t p = x * P2;  // off the chain
-    const uint32_t yl = (uint32_t)y, yh = (uint32_t)(y >> 32);
-    const uint32_t rh = __funnelshift_l(yl, yh, 31), rl = __funnelshift_l(yh, yl, 31);
-    // the cross products go into the high addend; the low product's carry
-    // chain (mad.lo.cc / madc.hi) keeps ptxas from splitting the 64-bit add
-    // back out: SASS is SHF -> IMAD -> IMAD -> IMAD.WIDE.U32 (64-bit addend)
-    const uint32_t c = rl * (uint32_t)(P1 >> 32) + rh * (uint32_t)P1 + (uint32_t)(p >> 32);
+    // one PTX block: x*P2 is formed completely off the chain (plo, phi), and the
+    // chain is  funnel shifts -> mad (rh*P1lo + phi) -> mad (rl*P1hi + .) ->
+    // mad.lo.cc / madc.hi (rl*P1lo + {plo, .}): four dependent SASS per stripe
     uint32_t lo, hi;
-    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;"
+    asm("{\n\t.reg .u32 xl, xh, yl, yh, plo, phi, rl, rh, t;\n\t"
+        "mov.b64 {xl, xh}, %2;\n\t"
+        "mov.b64 {yl, yh}, %3;\n\t"
+        "mul.lo.u32 plo, xl, %4;\n\t"
+        "mul.hi.u32 phi, xl, %4;\n\t"
+        "mad.lo.u32 phi, xl, %5, phi;\n\t"
+        "mad.lo.u32 phi, xh, %4, phi;\n\t"
+        "shf.l.wrap.b32 rh, yl, yh, 31;\n\t"
+        "shf.l.wrap.b32 rl, yh, yl, 31;\n\t"
+        "mad.lo.u32 t, rh, %6, phi;\n\t"
+        "mad.lo.u32 t, rl, %7, t;\n\t"
+        "mad.lo.cc.u32 %0, rl, %6, plo;\n\t"
+        "madc.hi.u32 %1, rl, %6, t;\n\t}"
         : "=r"(lo), "=r"(hi)
-        : "r"(rl), "r"((uint32_t)P1), "r"((uint32_t)p), "r"(c));
+        : "l"(x), "l"(y), "r"((uint32_t)P2), "r"((uint32_t)(P2 >> 32)), "r"((uint32_t)P1),
+          "r"((uint32_t)(P1 >> 32)));
     return ((uint64_t)hi << 32) | lo;
 }
 __device__ __forceinline__ uint64_t yfinal(uint64_t y) { return ystep(y, 0); }
