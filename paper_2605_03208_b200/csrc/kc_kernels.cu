@@ -2108,6 +2108,20 @@ static void launch_k2(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* 
             return;
         }
     }
+    if constexpr (!DT_<DT>::F) {
+        // sub-wave launches (at most ~4 units per warp of the full grid) are bound by
+        // load round trips, not bandwidth: 4 vectors of each operand in flight per lane
+        // instead of 2 halves the trips per unit (integer and byte dtypes: no element
+        // queue, so the registers are there)
+        static const bool small_u4 = [] {
+            const char* e = getenv("KC_K2_SMALL_U4");
+            return !(e && *e == '0');
+        }();
+        if (small_u4 && !filter && G.n_units <= (uint64_t)num_sms * 16 * 4) {
+            launch_k2_cfg<DT, 512, 1, 4, 1>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
+            return;
+        }
+    }
     launch_k2_cfg<DT, 512, 1, 2, 1>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
 }
 
