@@ -1881,7 +1881,6 @@ using TmaA = HkCfg<256, 3, 1024>;  // 64 slots x 3 x 1 KiB
 using TmaB = HkCfg<128, 3, 2048>;  // 32 slots x 3 x 2 KiB
 using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bound)
 using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
-using CpE = CpCfg<8, 6, 512>;    // 64 chunks/SM x 6 x 512 B: 5/6 of the ring in flight instead of 2/3
 using CpS = CpCfg<2, 6, 1024>;   // small snapshots: 2-warp CTAs, 6-deep rings, so < 148 x 64 chunks still
                                  // spread over every SM (a chunk's hash is a ~25 us serial chain)
 using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
@@ -1893,7 +1892,7 @@ cudaError_t kernels_init() {
 #define KC_CP_ATTR(CFG)                                                                                      \
     if (e == cudaSuccess)                                                                                    \
         e = cudaFuncSetAttribute(k1_hash_cpasync<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
-    KC_CP_ATTR(CpA) KC_CP_ATTR(CpD) KC_CP_ATTR(CpS) KC_CP_ATTR(CpE)
+    KC_CP_ATTR(CpA) KC_CP_ATTR(CpD) KC_CP_ATTR(CpS)
 #undef KC_CP_ATTR
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1_hash_cpasync<CpA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1983,7 +1982,6 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
         case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
-        case 6: launch_cp<CpE>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
         default:
             // fewer groups than 8-warp CTAs x SMs: spread them (round 2 A/B on c2: a per-quad
             // TMA bulk ring of 16 slots x 3 x 2 KiB 92-129 us; CpS with 3 x 2 KiB slices, the
