@@ -1194,7 +1194,7 @@ def main():
         res["planted"] = "reference pool planted with 1-byte mismatches (--plant): a parity run"
     if rank == 0 and world == 1 and not a.no_configs:
         res["configs"] = run_configs(a, pool.ctx, log, res["roofline"]["peak"])
-    if rank == 0 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:   # the oracle baseline: rank 0 at N = 1 only
         import bench_configs as bc
         threads = os.cpu_count() or 1
         sample = c4_sample(pool, a.cpu_sample_mb)
