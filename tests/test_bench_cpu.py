@@ -64,3 +64,16 @@ def test_oracle_rates_are_bounded_and_consistent():
     assert r2["bytes"] == bc.PIECE
     info = bc.host_info()
     assert info["nproc"] == (os.cpu_count() or 1)
+
+
+def test_profile_renderers_on_committed_evidence():
+    """tools/baseline_table.py and tools/pcie_trace.py --summarize re-derive BASELINE.md's
+    table and the PCIe summary from the committed round-2 evidence (no GPU)."""
+    b = os.path.join(ROOT, "profiles", "r2_bench_n1.json")
+    t = os.path.join(ROOT, "profiles", "r2_pcie_trace.json")
+    out = subprocess.check_output([sys.executable, os.path.join(ROOT, "tools", "baseline_table.py"), b], text=True)
+    assert "| c4 30 GB MoE pool, N = 1 |" in out and out.count("| c5 ") == 6
+    out = subprocess.check_output([sys.executable, os.path.join(ROOT, "tools", "pcie_trace.py"), "--summarize", t,
+                                   "57.2", "55.6"], text=True)
+    rows = {ln.split()[0]: ln.split() for ln in out.splitlines() if ln[:3] in ("D2H", "H2D")}
+    assert int(rows["D2H"][6].replace(",", "")) == int(rows["H2D"][6].replace(",", "")) > 29_000_000_000
