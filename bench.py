@@ -328,6 +328,36 @@ def run_ours(a, rank, world, device, log):
         rows = torch.tensor([pool.gidx[s.name] for s in pool.specs], dtype=torch.int64, device="cuda")
         glob_reps = torch.zeros(len(specs_all), REP_WORDS, dtype=torch.int64, device="cuda")
         glob = {}
+        peer = None
+        if a.combine == "peer" and not e2:
+            # the combine fused into the producing kernels over peer memory: rank 0 owns the
+            # global manifest, report rows and bitmap words ([world, pad] layouts); every rank
+            # maps them (kc_peer_export -> kc_peer_import) and its K1 stores the post-manifest,
+            # and its K2 accumulates reports and sets bitmap bits, straight into its slice of
+            # rank 0's HBM (NVLink on a multi-GPU node).  The exchange is then a barrier.
+            import synth
+            pad = max(1, plan.max_local_chunks())
+            maxrows = max(1, max(sum(1 for o in plan.owner if o == r) for r in range(world)))
+            padw = max(1, max(plan.bitmap_words(r) for r in range(world)))
+            sizes = {"man": world * pad * 8, "reps": world * maxrows * 8 * REP_WORDS, "bms": world * padw * 8}
+            objs = [None]
+            if rank == 0:
+                bases = {k: ctx.alloc(n) for k, n in sizes.items()}
+                objs[0] = {"pid": os.getpid(), "buf": {k: (va,) + ctx.peer_export(va) for k, va in bases.items()}}
+            dist.broadcast_object_list(objs, src=0)
+            if rank == 0:
+                peer_va = bases
+            else:
+                peer_va = {k: ctx.peer_import(objs[0]["pid"], fd, sz, va) for k, (va, fd, sz) in objs[0]["buf"].items()}
+            dist.barrier()
+            peer = {"va": peer_va, "pad": pad, "maxrows": maxrows, "padw": padw}
+            # this rank's slices, as tensors aliasing rank 0's memory (the step code is unchanged)
+            post = synth.dev_view(peer_va["man"] + 8 * rank * pad, 8 * max(1, C), device).view(torch.int64)
+            reps = synth.dev_view(peer_va["reps"] + 8 * REP_WORDS * rank * maxrows,
+                                  8 * REP_WORDS * max(1, n_rep), device).view(torch.int64)
+            bms = synth.dev_view(peer_va["bms"] + 8 * rank * padw, 8 * max(1, acc), device).view(torch.int64)
+            log(f"rank {rank}: peer combine: manifest, reports and bitmaps written into rank 0's HBM "
+                f"({'own' if rank == 0 else 'peer-mapped'})")
 
     def step(ev):
         launches = 0
@@ -353,7 +383,10 @@ def run_ours(a, rank, world, device, log):
         rec("diff", 1)
         if world > 1:
             rec("combine", 0)
-            if e2:   # contiguous chunk ranges; every rank reports all 185 regions (its segments)
+            if peer is not None:   # the results are already in rank 0's HBM: make them visible
+                stream.synchronize()
+                dist.barrier()
+            elif e2:   # contiguous chunk ranges; every rank reports all 185 regions (its segments)
                 glob["manifest"] = kd.gather_ranges(post, pool.e2_counts)              # C2
                 glob["reports"] = kd.combine_reports(reps.view(-1, REP_WORDS))          # C3
                 glob["bitmaps"] = kd.gather_bitmaps(bms)                                # C4 (disjoint words)
@@ -419,6 +452,21 @@ def run_ours(a, rank, world, device, log):
     specs_all = pool.all_specs
     nck = [(s.size + 65535) // 65536 for s in specs_all]
     nwd = [(c + 63) // 64 for c in nck]
+    if world > 1 and peer is not None:   # rank 0 reads the combined results from its own HBM
+        gman = synth.dev_view(peer["va"]["man"], 8 * world * peer["pad"], device).view(torch.int64)
+        glob["manifest"] = gman[perm]
+        grep = synth.dev_view(peer["va"]["reps"], 8 * REP_WORDS * world * peer["maxrows"],
+                              device).view(torch.int64).view(world * peer["maxrows"], REP_WORDS)
+        ridx = []
+        seen = [0] * world
+        for o in plan.owner:   # global spec order -> (owner, its local row)
+            ridx.append(o * peer["maxrows"] + seen[o])
+            seen[o] += 1
+        glob["reports"] = grep[torch.tensor(ridx, dtype=torch.int64, device="cuda")]
+        gbm = synth.dev_view(peer["va"]["bms"], 8 * world * peer["padw"], device).view(torch.int64)
+        pw = max(1, max(plan.bitmap_words(r) for r in range(world)))
+        assert pw == peer["padw"]
+        glob["bitmaps"] = gbm[bperm]
     if world > 1:
         gm = glob["manifest"].cpu().numpy()
         rep_rows = glob["reports"].cpu().numpy()
@@ -1134,6 +1182,9 @@ def main():
     p.add_argument("--no-configs", action="store_true", help="skip the c1/c2/c3/c5 per-config measurements")
     p.add_argument("--config-iters", type=int, default=5)
     p.add_argument("--config-oracle-seconds", type=float, default=1.0)
+    p.add_argument("--combine", default="nccl", choices=["nccl", "peer"],
+                   help="N > 1, E1: nccl = C2/C3/C4 collectives; peer = K1/K2 write the post-manifest, reports "
+                        "and bitmaps straight into rank 0's HBM through peer mappings, the exchange a barrier")
     p.add_argument("--placement", default="e1", choices=["e1", "e2"],
                    help="e1: residency-first shards (each rank reads its own HBM; the headline); e2: the pool "
                         "resident on rank 0, every rank reading a 1/N share of it over NVLink peer mappings "

@@ -44,12 +44,16 @@ KEYS = ("post_manifest_sha256_excl_ptr_tables", "reports_sha256", "bitmaps_sha25
         "report_counter_sums", "max_ulp", "max_abs", "max_rel")
 
 
-@pytest.mark.parametrize("placement", ["e1", "e2"])
-def test_n2_one_gpu_combine_equals_n1(one, placement):
+@pytest.mark.parametrize("placement,combine", [("e1", "nccl"), ("e2", "nccl"), ("e1", "peer")])
+def test_n2_one_gpu_combine_equals_n1(one, placement, combine):
     """E1: each rank its own regions.  E2: rank 0 owns the whole pool and rank 1
     hashes/diffs half of its chunks through a kc_peer_import mapping of rank 0's
-    allocations (on one GPU a second mapping of the same HBM; over NVLink on two)."""
-    two = _bench(2, {"KC_BENCH_ONE_GPU": "1", "KC_BENCH_BACKEND": "gloo"}, ["--placement", placement])
+    allocations (on one GPU a second mapping of the same HBM; over NVLink on two).
+    combine=peer: no data collective -- each rank's K1 stores its post-manifest, and
+    its K2 its reports and bitmap bits, into its slice of rank 0's buffers through
+    peer mappings; rank 0 reads the combined results from its own HBM."""
+    two = _bench(2, {"KC_BENCH_ONE_GPU": "1", "KC_BENCH_BACKEND": "gloo"},
+                 ["--placement", placement, "--combine", combine])
     assert one["n_gpus"] == 1 and two["n_gpus"] == 2
     assert two["collectives"]["backend"] == "gloo"
     f1, f2 = one["fingerprint"], two["fingerprint"]
