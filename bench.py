@@ -1237,8 +1237,11 @@ def main():
     if world > 1:
         res["collectives"] = {"backend": torch.distributed.get_backend(),
                                         "nccl": ".".join(map(str, torch.cuda.nccl.version())),
-                                        "step": "C2 all_gather manifests, C3 all_reduce SUM/MAX reports, "
-                                                "C4 all_gather per-region bitmaps"}
+                                        "step": ("peer combine: K1's post-manifest, K2's reports and bitmaps "
+                                                 "written into rank 0's HBM through peer mappings, then a barrier"
+                                                 if a.combine == "peer" and a.placement == "e1" else
+                                                 "C2 all_gather manifests, C3 all_reduce SUM/MAX reports, "
+                                                 "C4 all_gather per-region bitmaps")}
     if os.environ.get("KC_BENCH_ONE_GPU") and world > 1:
         res["functional_check_only"] = "all ranks on cuda:0 (KC_BENCH_ONE_GPU)"
     if a.plant:
