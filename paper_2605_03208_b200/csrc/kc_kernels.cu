@@ -2117,7 +2117,10 @@ static void launch_k2(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* 
             const char* e = getenv("KC_K2_SMALL_U4");
             return !(e && *e == '0');
         }();
-        if (small_u4 && !filter && G.n_units <= (uint64_t)num_sms * 16 * 4) {
+        // (likewise many short segments: a warp walks them one by one, a few round
+        // trips each, when at least half the segments are a single 16 KiB unit)
+        if (small_u4 && !filter &&
+            (G.n_units <= (uint64_t)num_sms * 16 * 4 || 2 * (uint64_t)G.n_segs >= G.n_units)) {
             launch_k2_cfg<DT, 512, 1, 4, 1>(d_segs, G, d_reps, bm, atol, rtol, equal_nan, num_sms, s, filter);
             return;
         }
