@@ -1984,8 +1984,9 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
         case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
         default:
             // fewer groups than 8-warp CTAs x SMs: spread them (round 2 A/B on c2: a per-quad
-            // TMA bulk ring of 16 slots x 3 x 2 KiB 92-129 us; CpS with 3 x 2 KiB slices, the
-            // same smem, 50.2-51.2 us; CpS 50.2 us)
+            // TMA bulk ring of 16 slots x 3 x 2 KiB 92-129 us; this warp ring filled by one
+            // bulk copy per chunk slice from the quad leaders, 66 us; CpS with 3 x 2 KiB
+            // slices, the same smem, 50.2-51.2 us; CpS 48-50 us)
             if ((C + 7) / 8 < (uint64_t)num_sms * 8) {
                 launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
             } else {
