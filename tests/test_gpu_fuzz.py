@@ -99,3 +99,41 @@ def test_k5_and_plan_random_sets_match_oracle(env):
             torch.cuda.synchronize()
             check("plan")
         plan.close()
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_k1_random_region_sets_match_oracle(env, block):
+    """Random region sets (1 to 2,000 regions of 1 B to ~4 chunks, 16-byte aligned or not,
+    so both the cp.async rings (large and sub-wave) and the generic path run) through
+    kc_hash and a prepared plan: every chunk hash, region digest and the snapshot digest
+    equal the oracle's."""
+    torch, kc, ctx, orc = env
+    for t in range(block * 6, block * 6 + 6):
+        rng = np.random.default_rng(77 + t)
+        nreg = int(rng.choice([1, 3, 40, 700, 2000]))
+        sizes = [int(x) for x in rng.choice([1, 31, 32, 33, 4096, 65535, 65536, 65537, 200_000, 262_144], size=nreg)]
+        sizes = [s + int(rng.integers(0, 64)) for s in sizes]
+        align = 16 if rng.integers(0, 3) else 8
+        offs = np.concatenate([[0], np.cumsum([(s + 255) // 256 * 256 for s in sizes])])
+        buf = torch.randint(0, 256, (int(offs[-1]) + 64,), dtype=torch.uint8, device="cuda")
+        shift = 0 if align == 16 else 8
+        regions = [(buf.data_ptr() + int(o) + shift, s) for o, s in zip(offs[:-1], sizes)]
+        C = kc.count_chunks(regions)
+        h = torch.zeros(C, dtype=torch.int64, device="cuda")
+        dg = torch.zeros(nreg + 1, dtype=torch.int64, device="cuda")
+        ctx.hash(regions, h.data_ptr(), dg.data_ptr(), dg.data_ptr() + 8 * nreg)
+        torch.cuda.synchronize()
+        host = buf.cpu().numpy()
+        base = buf.data_ptr()
+        man = [orc.chunk_hashes(host[b - base:b - base + s]) for b, s in regions]
+        assert np.array_equal(h.cpu().numpy().view(np.uint64), np.concatenate(man)), f"set {t} manifest"
+        digs = [orc.region_digest(m) for m in man]
+        assert [int(x) for x in dg.cpu().numpy().view(np.uint64)[:nreg]] == digs, f"set {t} digests"
+        assert int(dg.cpu().numpy().view(np.uint64)[nreg]) == orc.snapshot_digest(
+            [b for b, _ in regions], sizes, digs), f"set {t} snapshot digest"
+        plan = ctx.hash_plan(regions)
+        h2 = torch.zeros_like(h)
+        plan.run(h2.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(h, h2), f"set {t} plan"
+        plan.close()
