@@ -1192,7 +1192,12 @@ static kc_status validate_host_full(kc_ctx* ctx, const kc_buffer* bufs, size_t n
     }
     cudaEvent_t* copied = ctx->full_ev.data();
     cudaEvent_t* freed = ctx->full_ev.data() + kFullSlots;
-    KC_CHECK_CUDA(ctx, ensure(ctx->ref_stage, kFullSlots * kFullPiece), "cudaMalloc(reference stage ring)");
+    // piece size: 256 MiB, or less when everything fits in one piece (a small call
+    // does not grow the ctx's staging ring to 768 MiB)
+    uint64_t total = kChunk;
+    for (size_t i = 0; i < n; ++i) total += (bufs[i].nbytes + 255) & ~255ull;
+    const uint64_t piece = std::min<uint64_t>(kFullPiece, (total + kChunk - 1) / kChunk * kChunk);
+    KC_CHECK_CUDA(ctx, ensure(ctx->ref_stage, kFullSlots * piece), "cudaMalloc(reference stage ring)");
     KC_CHECK_CUDA(ctx, ensure(ctx->reps, std::max<size_t>(1, n) * sizeof(kc_diff_report)), "cudaMalloc(reports)");
     KC_CHECK_CUDA(ctx, ensure(ctx->bitmaps, std::max<uint64_t>(1, words) * 8), "cudaMalloc(bitmaps)");
     kc_diff_report* d_reps = (kc_diff_report*)ctx->reps.p;
@@ -1236,13 +1241,13 @@ static kc_status validate_host_full(kc_ctx* ctx, const kc_buffer* bufs, size_t n
     for (size_t i = 0; i < n; ++i) {
         uint64_t off = 0;
         while (off < bufs[i].nbytes) {
-            if (kFullPiece - used < kChunk) {
+            if (piece - used < kChunk) {
                 st = flush();
                 if (st != KC_OK) return st;
             }
-            const uint64_t room = (kFullPiece - used) / kChunk * kChunk;  // whole chunks: pieces cut at chunk bounds
+            const uint64_t room = (piece - used) / kChunk * kChunk;  // whole chunks: pieces cut at chunk bounds
             const uint64_t len = std::min<uint64_t>(room, bufs[i].nbytes - off);
-            uint8_t* dst = ring + (uint64_t)slot * kFullPiece + used;
+            uint8_t* dst = ring + (uint64_t)slot * piece + used;
             KC_CHECK_CUDA(ctx, cudaMemcpyAsync(dst, (const uint8_t*)bufs[i].ref + off, len, cudaMemcpyHostToDevice, cs),
                           "H2D reference piece");
             segs.push_back(kc_buffer{(uint64_t)dst, bufs[i].act + off, len, bufs[i].dtype, (int32_t)i, off / kChunk});
