@@ -31,3 +31,14 @@ for i in range(20):
     best = min(best, e0.elapsed_time(e1))
 n = sum(sizes)
 print(f"{cfg}: {n} B, {C} chunks: K1 {best * 1e3:.1f} us = {n / (best * 1e-3) / 1e9:.0f} GB/s")
+if "--b2b" in sys.argv:  # back to back, no flush kernel between calls (c2 > L2, so still HBM reads)
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for k in range(2):
+        e0.record()
+        for i in range(reps):
+            ctx.hash(rarr, h.data_ptr(), stream=torch.cuda.current_stream().cuda_stream)
+        e1.record()
+        torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps
+    print(f"{cfg}: back to back x{reps}: K1 {t * 1e3:.1f} us per call = {n / (t * 1e-3) / 1e9:.0f} GB/s")
