@@ -1083,7 +1083,7 @@ def run_configs(a, ctx, log, peak):
         cells.append(res)
     out["c5"] = cells
     out["method"] = (f"GPU: CUDA events around each kc_* call, best of {a.config_iters} after one warm-up call, "
-                     "L2 flushed (512 MiB write) before each; closure stages wall-clock around each call. Oracle: "
+                     "L2 flushed before each (512 MiB write, then 512 MiB read: no input line and no dirty line left in L2); closure stages wall-clock around each call. Oracle: "
                      "oracle/ as it stands on a bounded sample of the config's bytes copied back from the device, "
                      "1 thread (first 32 MiB) and every host core")
     out["seconds"] = time.perf_counter() - t_all

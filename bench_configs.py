@@ -3,7 +3,10 @@ bench.py's headline step) and the oracle's CPU rates.
 
 Every GPU number is a CUDA-event time around the public C-ABI call (kc_hash,
 kc_diff_async, kc_capture_dev/host, kc_restore_dev, kc_replay, kc_validate),
-best of `iters`, with L2 flushed (a 512 MiB write) before each timed call.
+best of `iters`, with L2 flushed before each timed call: a 512 MiB write, then a
+512 MiB read, so the timed call finds none of its inputs in L2 AND no dirty lines
+(after the write alone, the first ~126 MB the call touches also pay the write-back
+of the flush's dirty lines: c2 K1 40 -> 47 us, tools/c2_k1_probe.py --flushes).
 Each config's result carries GB/s and its fraction of the measured HBM peak
 (MEASURED_PEAKS.json) and of the 8 TB/s spec, and -- beside it -- the CPU
 oracle's hash and diff rates on a bounded sample of the same config's bytes
@@ -123,12 +126,18 @@ class Timer:
     def __init__(self, torch, iters: int):
         self.torch, self.iters = torch, iters
         self.flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        self.flush_r = torch.zeros(64 << 20, dtype=torch.int64, device="cuda")  # 512 MiB, read back
+        self.acc = torch.zeros((), dtype=torch.int64, device="cuda")
+
+    def flush_l2(self, i: int) -> None:
+        self.flush.fill_(i & 0xFF)                                 # write > L2: evicts every input line
+        self.torch.sum(self.flush_r, dim=0, out=self.acc)          # read > L2: evicts the dirty flush lines
 
     def best_ms(self, fn) -> float:
         torch = self.torch
         best = 1e30
         for i in range(self.iters + 1):
-            self.flush.fill_(i & 0xFF)
+            self.flush_l2(i)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()

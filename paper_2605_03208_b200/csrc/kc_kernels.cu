@@ -74,37 +74,6 @@ __device__ __forceinline__ uint64_t ystep(uint64_t y, uint64_t x) {
 }
 __device__ __forceinline__ uint64_t yfinal(uint64_t y) { return ystep(y, 0); }
 
-// The same round with the 64-bit multiply's wide product off the chain: IMAD.WIDE's
-// result is ~12.5 / ~16.75 cycles away (low / high word, tools/probes/op_latency.cu)
-// against ~4.4 for IMAD and ~9.7 for IMAD.HI, so the low word is a plain mad.lo
-// (rl*P1lo + plo), its carry a compare (lo < plo), and the high word
-// mul.hi(rl, P1lo) + t + carry: SHF -> IMAD -> ISETP -> IADD beside SHF -> IMAD.HI.
-__device__ __forceinline__ uint64_t ystep_h(uint64_t y, uint64_t x) {
-    uint32_t lo, hi;
-    asm("{\n\t.reg .u32 xl, xh, yl, yh, plo, phi, rl, rh, a, b, h0;\n\t"
-        "mov.b64 {xl, xh}, %2;\n\t"
-        "mov.b64 {yl, yh}, %3;\n\t"
-        "mul.lo.u32 plo, xl, %4;\n\t"
-        "mul.hi.u32 phi, xl, %4;\n\t"
-        "mad.lo.u32 phi, xl, %5, phi;\n\t"
-        "mad.lo.u32 phi, xh, %4, phi;\n\t"
-        "shf.l.wrap.b32 rh, yl, yh, 31;\n\t"
-        "shf.l.wrap.b32 rl, yh, yl, 31;\n\t"
-        "mad.lo.cc.u32 %0, rl, %6, plo;\n\t"
-        "madc.hi.u32 h0, rl, %6, phi;\n\t"
-        "mul.lo.u32 a, rh, %6;\n\t"
-        "mad.lo.u32 b, rl, %7, a;\n\t"
-        "add.u32 %1, h0, b;\n\t}"
-        : "=r"(lo), "=r"(hi)
-        : "l"(x), "l"(y), "r"((uint32_t)P2), "r"((uint32_t)(P2 >> 32)), "r"((uint32_t)P1),
-          "r"((uint32_t)(P1 >> 32)));
-    return ((uint64_t)hi << 32) | lo;
-}
-template <int YF>
-__device__ __forceinline__ uint64_t ystep_f(uint64_t y, uint64_t x) {
-    return YF ? ystep_h(y, x) : ystep(y, x);
-}
-
 __device__ __forceinline__ uint64_t xavalanche(uint64_t h) {
     h ^= h >> 33;
     h *= P2;
@@ -578,21 +547,22 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
 
 // ========================================================================== //
 // K1, warp-specialized ring (sub-wave snapshots).  Below one wave a chunk's  //
-// 2,048-round chain sets the time, and in k1_hash_cpasync the hashing warp   //
-// also issues its own staging (~142 SASS per 32-round slice, in order with   //
-// the chain): ~49.5 cycles per round against ~30 for the bare chain.  Here   //
-// each hashing warp (8 chunks, one per quad, as above) has a partner         //
-// producer warp on another SMSP that runs the same group/slice sequence and  //
-// fills the ring with the same coalesced 16-byte cp.async rows; a stage is   //
-// handed over through two mbarriers: full[st] (32 producer arrivals, each    //
-// fired by cp.async.mbarrier.arrive.noinc when that lane's copies landed)   //
-// and empty[st] (one arrival from the hashing warp's lane 0 once the warp is //
-// done reading the slot).  The hashing warp issues only the wait, the 32     //
-// shared loads and the 32 rounds per slice.                                  //
+// 2,048-round chain sets the time.  In k1_hash_cpasync the hashing warp also //
+// issues its own staging, in order with the chain (~49.5 cycles per round    //
+// against ~28-30 for the bare chain, tools/probes/k1_round_probe.cu), and    //
+// two chain-bound warps on one SMSP share its FMA pipe (45-50 cycles each).  //
+// Here each hashing warp (8 chunks, one per quad) runs alone on its SMSP and //
+// a partner producer warp runs the same group/slice sequence, filling the    //
+// ring with the same coalesced 16-byte cp.async rows.  A stage is handed     //
+// over through two mbarriers: full[st] (32 producer arrivals, each fired by  //
+// cp.async.mbarrier.arrive.noinc when that lane's copies have landed) and    //
+// empty[st] (one arrival from the hashing warp's lane 0 once the warp is     //
+// done reading the slot).  Per 2 KiB slice the hashing warp issues only the  //
+// wait, 64 shared loads, 64 rounds and the release.                          //
 // ========================================================================== //
-// SPREAD: warp w runs on SMSP w % 4; the hashing warps take slots 0..HW-1 (HW <= 3) and their
-// producers slots 3, 7, 11 (all on SMSP 3), the other slots exit at once, so no hashing warp
-// shares its SMSP with anything
+// SPREAD (HW <= 3): warp w runs on SMSP w % 4; the hashing warps take slots 0..HW-1 and their
+// producers slots 3, 7, 11 (all on SMSP 3); the other slots exit at once, so no hashing warp
+// shares its SMSP.  Without SPREAD the producers are warps HW..2HW-1.
 template <int HW, int STAGES, int SL, bool SPREAD = false>
 struct WsCfg {
     static_assert(!SPREAD || HW <= 3, "SPREAD leaves SMSP 3 to the producers");
@@ -628,7 +598,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <class CFG, int YF = 0>
+template <class CFG>
 __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     k1_hash_ws(const RegionDev* __restrict__ regs, int nreg, uint64_t C, uint64_t* __restrict__ out,
                const uint32_t* __restrict__ map, const uint32_t* __restrict__ order = nullptr) {
@@ -721,10 +691,10 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const uint64_t* xp = xp0 + st * (WSTAGE / 8);
             if (left >= (uint32_t)(SL / 32)) {
 #pragma unroll
-                for (int t = 0; t < SL / 32; ++t) v = ystep_f<YF>(v, xp[4 * t]);
+                for (int t = 0; t < SL / 32; ++t) v = ystep(v, xp[4 * t]);
                 left -= SL / 32;
             } else {
-                for (uint32_t t = 0; t < left; ++t) v = ystep_f<YF>(v, xp[4 * t]);
+                for (uint32_t t = 0; t < left; ++t) v = ystep(v, xp[4 * t]);
                 left = 0;
             }
             __syncwarp();
@@ -2078,13 +2048,10 @@ using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bou
 using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
 using CpS = CpCfg<2, 6, 1024>;   // small snapshots: 2-warp CTAs, 6-deep rings, so < 148 x 64 chunks still
                                  // spread over every SM (a chunk's hash is a ~25 us serial chain)
-using WsS = WsCfg<2, 6, 1024>;   // sub-wave, warp-specialized: 2 hashing + 2 producer warps, 6-deep rings
 using Ws1 = WsCfg<1, 4, 2048, true>;  // one CTA per SM, HW hashing warps (one per SMSP) + HW producers
 using Ws2 = WsCfg<2, 4, 2048, true>;  // on SMSP 3, 2 KiB slices (64 rounds between ring hand-overs)
 using Ws3 = WsCfg<3, 4, 2048, true>;
 using Ws4 = WsCfg<4, 3, 2048>;
-using WsA = WsCfg<8, 3, 1024>;   // full waves: 8 hashing + 8 producer warps, the CpA ring
-using WsB = WsCfg<6, 4, 1024>;   // full waves: 6 hashing + 6 producer warps, 4-deep rings
 using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
 
 cudaError_t kernels_init() {
@@ -2102,22 +2069,11 @@ cudaError_t kernels_init() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1_hash_cpasync<CpS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)CpS::kSmem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k1_hash_ws<WsS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsS::kSmem);
 #define KC_WS_ATTR(CFG)                                                                                      \
     if (e == cudaSuccess)                                                                                    \
-        e = cudaFuncSetAttribute(k1_hash_ws<CFG, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
+        e = cudaFuncSetAttribute(k1_hash_ws<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
     KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3) KC_WS_ATTR(Ws4)
 #undef KC_WS_ATTR
-#define KC_WS_ATTR(CFG)                                                                                      \
-    if (e == cudaSuccess)                                                                                    \
-        e = cudaFuncSetAttribute(k1_hash_ws<CFG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
-    KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3) KC_WS_ATTR(Ws4)
-#undef KC_WS_ATTR
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k1_hash_ws<WsA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsA::kSmem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k1_hash_ws<WsB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsB::kSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
     if (e == cudaSuccess)
@@ -2177,20 +2133,10 @@ static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d
                                                                                  nullptr, order);
 }
 
-template <class CFG>
-static void launch_ws(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
-                      int num_sms, cudaStream_t s, const uint32_t* order) {
-    const uint64_t groups = (C + 7) / 8;
-    const uint64_t per_sm = 228 * 1024 / (CFG::kSmem + 1024);  // CTAs resident per SM (shared memory)
-    const uint64_t grid = balanced_grid(groups, (uint64_t)num_sms * per_sm, CFG::kHashWarps);
-    k1_hash_ws<CFG><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map, order);
-}
-
 // Sub-wave K1 with at most one hashing warp per SMSP: a second chain-bound warp on the same
 // SMSP shares its FMA pipe (~17 pipe cycles per round each) and stretches the ~30-cycle round
 // to 45-50 (tools/probes/k1_round_probe.cu at 256 threads/CTA).  One CTA per SM with HW =
 // ceil(groups / SMs) hashing warps (slots 0..HW-1, SMSPs 0..HW-1) and their HW producers.
-template <int YF>
 static bool launch_ws_subwave(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
                               int num_sms, cudaStream_t s, const uint32_t* order) {
     const uint64_t groups = (C + 7) / 8;
@@ -2198,10 +2144,10 @@ static bool launch_ws_subwave(const RegionDev* d_regs, int nreg, uint64_t C, uin
     if (hw > 4) return false;
     const unsigned grid = (unsigned)((groups + hw - 1) / hw);
     switch (hw) {
-        case 1: k1_hash_ws<Ws1, YF><<<grid, Ws1::kWarps * 32, Ws1::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
-        case 2: k1_hash_ws<Ws2, YF><<<grid, Ws2::kWarps * 32, Ws2::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
-        case 3: k1_hash_ws<Ws3, YF><<<grid, Ws3::kWarps * 32, Ws3::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
-        default: k1_hash_ws<Ws4, YF><<<grid, Ws4::kWarps * 32, Ws4::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        case 1: k1_hash_ws<Ws1><<<grid, Ws1::kWarps * 32, Ws1::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        case 2: k1_hash_ws<Ws2><<<grid, Ws2::kWarps * 32, Ws2::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        case 3: k1_hash_ws<Ws3><<<grid, Ws3::kWarps * 32, Ws3::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        default: k1_hash_ws<Ws4><<<grid, Ws4::kWarps * 32, Ws4::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
     }
     return true;
 }
@@ -2229,41 +2175,23 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
         case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
-        case 4:  // warp-specialized ring below one wave, CpA above
-            if ((C + 7) / 8 < (uint64_t)num_sms * 8)
-                launch_ws<WsS>(d_regs, nreg, C, d_out, map, num_sms, s, order);
-            else
-                launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
-            break;
-        case 7:  // one hashing warp per SMSP up to 4 x SMs groups, then as the default
-        case 8:  // the same with the IMAD.HI round
-            if (k1_variant() == 7 ? launch_ws_subwave<0>(d_regs, nreg, C, d_out, map, num_sms, s, order)
-                                  : launch_ws_subwave<1>(d_regs, nreg, C, d_out, map, num_sms, s, order))
-                break;
+        case 4:  // round 2's sub-wave path (CpS below one wave), for A/B
             if ((C + 7) / 8 < (uint64_t)num_sms * 8)
                 launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
             else
                 launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
-            break;
-        case 5:
-        case 6:  // warp-specialized rings at every size
-            if ((C + 7) / 8 < (uint64_t)num_sms * 8)
-                launch_ws<WsS>(d_regs, nreg, C, d_out, map, num_sms, s, order);
-            else if (k1_variant() == 5)
-                launch_ws<WsA>(d_regs, nreg, C, d_out, map, num_sms, s, order);
-            else
-                launch_ws<WsB>(d_regs, nreg, C, d_out, map, num_sms, s, order);
             break;
         default:
-            // fewer groups than 8-warp CTAs x SMs: spread them (round 2 A/B on c2: a per-quad
-            // TMA bulk ring of 16 slots x 3 x 2 KiB 92-129 us; this warp ring filled by one
-            // bulk copy per chunk slice from the quad leaders, 66 us; CpS with 3 x 2 KiB
-            // slices, the same smem, 50.2-51.2 us; CpS 48-50 us)
-            if ((C + 7) / 8 < (uint64_t)num_sms * 8) {
+            // up to 4 x SMs groups: one hashing warp per SMSP fed by producer warps (c2 45.3 ->
+            // 38.7 us back to back, 64 KiB x 1k 49.2 -> 41.0 us; K1); then, below one
+            // wave of 8-warp CTAs, CpS spread over every SM (round 2 A/B on c2: a per-quad TMA
+            // bulk ring of 16 slots x 3 x 2 KiB 92-129 us; a warp ring filled by one bulk copy per
+            // chunk slice from the quad leaders, 66 us; CpS 48-50 us); above, CpA
+            if (launch_ws_subwave(d_regs, nreg, C, d_out, map, num_sms, s, order)) break;
+            if ((C + 7) / 8 < (uint64_t)num_sms * 8)
                 launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
-            } else {
+            else
                 launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
-            }
             break;
     }
     return cudaGetLastError();

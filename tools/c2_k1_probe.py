@@ -31,6 +31,23 @@ for i in range(20):
     best = min(best, e0.elapsed_time(e1))
 n = sum(sizes)
 print(f"{cfg}: {n} B, {C} chunks: K1 {best * 1e3:.1f} us = {n / (best * 1e-3) / 1e9:.0f} GB/s")
+if "--flushes" in sys.argv:  # the same best-of-20 with other flushes before each call
+    src = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda").fill_(3)
+    acc = torch.empty(1, dtype=torch.int64, device="cuda")
+    for name, fl in [("write 256 MiB", lambda: flush.fill_(1)),
+                     ("read 512 MiB", lambda: torch.sum(src.view(torch.int64), dim=0, out=acc)),
+                     ("write 256 MiB + read 512 MiB", lambda: (flush.fill_(1), torch.sum(src.view(torch.int64), dim=0, out=acc))),
+                     ("none (L2 holds the tail of the last call)", lambda: None)]:
+        best = 1e30
+        for i in range(20):
+            fl()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ctx.hash(rarr, h.data_ptr(), stream=torch.cuda.current_stream().cuda_stream)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        print(f"{cfg}: flush {name}: K1 {best * 1e3:.1f} us")
 if "--b2b" in sys.argv:  # back to back, no flush kernel between calls (c2 > L2, so still HBM reads)
     reps = 50
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
