@@ -560,14 +560,12 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
 // done reading the slot).  Per 2 KiB slice the hashing warp issues only the  //
 // wait, 64 shared loads, 64 rounds and the release.                          //
 // ========================================================================== //
-// SPREAD (HW <= 3): warp w runs on SMSP w % 4; the hashing warps take slots 0..HW-1 and their
-// producers slots 3, 7, 11 (all on SMSP 3); the other slots exit at once, so no hashing warp
-// shares its SMSP.  Without SPREAD the producers are warps HW..2HW-1.
-template <int HW, int STAGES, int SL, bool SPREAD = false>
+// Warp w runs on SMSP w % 4: the hashing warps take slots 0..HW-1 (HW <= 3) and their producers
+// slots 3, 7, 11 (all on SMSP 3); the other slots exit at once, so no hashing warp shares its SMSP.
+template <int HW, int STAGES, int SL>
 struct WsCfg {
-    static_assert(!SPREAD || HW <= 3, "SPREAD leaves SMSP 3 to the producers");
-    static constexpr bool kSpread = SPREAD;
-    static constexpr int kHashWarps = HW, kWarps = SPREAD ? 4 * HW : 2 * HW, kStages = STAGES, kSlice = SL;
+    static_assert(HW >= 1 && HW <= 3, "SMSP 3 is left to the producers");
+    static constexpr int kHashWarps = HW, kWarps = 4 * HW, kStages = STAGES, kSlice = SL;
     static constexpr int kPitch = SL + 32;
     static constexpr int kWStage = 8 * kPitch;
     static constexpr int kUPC = SL / 16;
@@ -606,8 +604,8 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     constexpr int WSTAGE = CFG::kWStage, UPC = CFG::kUPC, UPL = CFG::kUPL;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q = lane >> 2, ql = lane & 3;
-    const bool producer = CFG::kSpread ? (w & 3) == 3 : w >= HW;
-    const int hw = CFG::kSpread ? (producer ? w >> 2 : w) : (producer ? w - HW : w);  // hashing warp served
+    const bool producer = (w & 3) == 3;
+    const int hw = producer ? w >> 2 : w;  // the hashing warp this warp is (or serves)
     uint8_t* wring = smem + (size_t)hw * STAGES * WSTAGE;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + CFG::kRing) + hw * 2 * STAGES;
     uint64_t* empty = full + STAGES;
@@ -621,7 +619,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (CFG::kSpread && !producer && w >= HW) return;  // placeholder slot
+    if (!producer && w >= HW) return;  // placeholder slot
     const uint64_t ngroups = (C + 7) / 8;
     const uint64_t W = (uint64_t)gridDim.x * HW;
     const uint64_t j0 = (uint64_t)hw * gridDim.x + blockIdx.x;
@@ -2048,10 +2046,9 @@ using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bou
 using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
 using CpS = CpCfg<2, 6, 1024>;   // small snapshots: 2-warp CTAs, 6-deep rings, so < 148 x 64 chunks still
                                  // spread over every SM (a chunk's hash is a ~25 us serial chain)
-using Ws1 = WsCfg<1, 4, 2048, true>;  // one CTA per SM, HW hashing warps (one per SMSP) + HW producers
-using Ws2 = WsCfg<2, 4, 2048, true>;  // on SMSP 3, 2 KiB slices (64 rounds between ring hand-overs)
-using Ws3 = WsCfg<3, 4, 2048, true>;
-using Ws4 = WsCfg<4, 3, 2048>;
+using Ws1 = WsCfg<1, 4, 2048>;  // one CTA per SM, HW hashing warps (one per SMSP) + HW producers
+using Ws2 = WsCfg<2, 4, 2048>;  // on SMSP 3, 4 x 2 KiB slices (64 rounds between ring hand-overs)
+using Ws3 = WsCfg<3, 4, 2048>;
 using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
 
 cudaError_t kernels_init() {
@@ -2072,7 +2069,7 @@ cudaError_t kernels_init() {
 #define KC_WS_ATTR(CFG)                                                                                      \
     if (e == cudaSuccess)                                                                                    \
         e = cudaFuncSetAttribute(k1_hash_ws<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
-    KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3) KC_WS_ATTR(Ws4)
+    KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3)
 #undef KC_WS_ATTR
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
@@ -2133,21 +2130,22 @@ static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d
                                                                                  nullptr, order);
 }
 
-// Sub-wave K1 with at most one hashing warp per SMSP: a second chain-bound warp on the same
+// Sub-wave K1 with one hashing warp alone on each SMSP: a second chain-bound warp on the same
 // SMSP shares its FMA pipe (~17 pipe cycles per round each) and stretches the ~30-cycle round
 // to 45-50 (tools/probes/k1_round_probe.cu at 256 threads/CTA).  One CTA per SM with HW =
-// ceil(groups / SMs) hashing warps (slots 0..HW-1, SMSPs 0..HW-1) and their HW producers.
+// ceil(groups / SMs) <= 3 hashing warps on SMSPs 0..HW-1 and their producers on SMSP 3.  With
+// HW = 4 the producers must share SMSPs with hashing warps, and CpS (2-warp CTAs staging their
+// own rings, one warp per SMSP at that size) measured faster (1 MiB x 256: 49.2 vs 52.2 us).
 static bool launch_ws_subwave(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
                               int num_sms, cudaStream_t s, const uint32_t* order) {
     const uint64_t groups = (C + 7) / 8;
     const uint64_t hw = (groups + num_sms - 1) / num_sms;
-    if (hw > 4) return false;
+    if (hw > 3) return false;
     const unsigned grid = (unsigned)((groups + hw - 1) / hw);
     switch (hw) {
         case 1: k1_hash_ws<Ws1><<<grid, Ws1::kWarps * 32, Ws1::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
         case 2: k1_hash_ws<Ws2><<<grid, Ws2::kWarps * 32, Ws2::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
-        case 3: k1_hash_ws<Ws3><<<grid, Ws3::kWarps * 32, Ws3::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
-        default: k1_hash_ws<Ws4><<<grid, Ws4::kWarps * 32, Ws4::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        default: k1_hash_ws<Ws3><<<grid, Ws3::kWarps * 32, Ws3::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
     }
     return true;
 }
@@ -2182,8 +2180,8 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
                 launch_cp<CpA>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
             break;
         default:
-            // up to 4 x SMs groups: one hashing warp per SMSP fed by producer warps (c2 45.3 ->
-            // 38.7 us back to back, 64 KiB x 1k 49.2 -> 41.0 us; K1); then, below one
+            // up to 3 x SMs groups: one hashing warp per SMSP fed by producer warps (c2 45.3 ->
+            // 38.7 us back to back, 64 KiB x 1k 48.0 -> 38.9 us; K1); then, below one
             // wave of 8-warp CTAs, CpS spread over every SM (round 2 A/B on c2: a per-quad TMA
             // bulk ring of 16 slots x 3 x 2 KiB 92-129 us; a warp ring filled by one bulk copy per
             // chunk slice from the quad leaders, 66 us; CpS 48-50 us); above, CpA
