@@ -116,6 +116,31 @@ def test_k1_zero_chunks_and_empty(env):
     assert h.size == 0
 
 
+@pytest.mark.parametrize("groups_per_sm", [None, 1.0, 1.01, 2.5, 3.0, 3.02])
+def test_k1_subwave_ring_boundaries(env, groups_per_sm):
+    """The sub-wave warp-specialized ring (k1_hash_ws: 1-3 hashing warps per SM, 8 chunks per
+    warp) and the switch to CpS above 3 x SMs chunk groups: chunk counts on each side of the
+    HW = 1 / 2 / 3 boundaries, with ragged region tails (a 17-byte sub-stripe tail, a 20-byte
+    region, a 100-byte one) that put the chunks in length-sorted order."""
+    torch, kc, ctx, orc = env
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    C = 1 if groups_per_sm is None else int(round(groups_per_sm * sms)) * 8 + (5 if groups_per_sm % 1 else 0)
+    tail = [CH + 17, 20, 100] if C >= 4 else []
+    full = C - (2 + 1 + 1 if tail else 0)
+    sizes = ([full * CH] if full else []) + tail
+    offs = np.concatenate([[0], np.cumsum([(x + 255) // 256 * 256 for x in sizes])])
+    big = _rand_dev(torch, int(offs[-1]), 4242 + C)
+    regions = [(big.data_ptr() + int(o), int(x)) for o, x in zip(offs[:-1], sizes)]
+    assert kc.count_chunks(regions) == C
+    h, d, s = _hash(torch, ctx, regions)
+    host = big.cpu().numpy()
+    exp = [orc.chunk_hashes(host[int(o):int(o) + int(x)], threads=16) for o, x in zip(offs[:-1], sizes)]
+    assert np.array_equal(h, np.concatenate(exp))
+    dig = [orc.region_digest(e) for e in exp]
+    assert [int(x) for x in d] == dig
+    assert s == orc.snapshot_digest([r[0] for r in regions], [r[1] for r in regions], dig)
+
+
 def test_k1_deterministic_across_calls(env):
     torch, kc, ctx, orc = env
     buf = _rand_dev(torch, 37 * CH + 5, 99)
