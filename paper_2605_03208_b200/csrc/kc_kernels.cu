@@ -393,10 +393,22 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int WARPS, int STAGES, int SL>
+// Slice layout in the ring.  SWZ = 0 (round 2): quad q's slice at q * (SL + 32), so the 8 quads
+// of a warp read distinct bank groups; but then a 128-byte global line lands across two
+// 128-byte shared rows for 3 quads in 4, and L1TEX splits its cp.async into two L2 requests
+// that touch 3 sectors each (ncu: 7 requests and 22 sectors per 512-byte LDGSTS instead of 4
+// and 16; 1.375 x the L2 sector traffic, 20% L2 hits).  SWZ = 1: slices at q * SL, 128-byte
+// aligned, and within every 128-byte row stripe t of quad q sits at position (t ^ q) & 3
+// (byte offset ^ (q & 3) << 5): each global line fills exactly one shared row, and the quads'
+// words of one round spread over 4 bank groups (quads q and q + 4 share one: 2 wavefronts for
+// the warp's 256 bytes, the minimum).
+__host__ __device__ constexpr int swz_off(bool swz, int q, int off) { return swz ? off ^ ((q & 3) << 5) : off; }
+
+template <int WARPS, int STAGES, int SL, bool SWZ = true>
 struct CpCfg {
     static constexpr int kWarps = WARPS, kStages = STAGES, kSlice = SL;
-    static constexpr int kPitch = SL + 32;      // quads of a warp on distinct bank groups
+    static constexpr bool kSwz = SWZ;
+    static constexpr int kPitch = SWZ ? SL : SL + 32;  // see swz_off
     static constexpr int kWStage = 8 * kPitch;  // one warp's stage: 8 chunk slices
     static constexpr int kUPC = SL / 16;        // 16-byte copy units per chunk slice
     static constexpr int kUPL = (8 * kUPC + 31) / 32;  // copy units per lane per step
@@ -461,10 +473,11 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         for (int k = 0; k < UPL; ++k) {
             const int u = lane + 32 * k;
             if (u < 8 * UPC) {
-                const int qq = u / UPC, off = (u % UPC) * 16;
+                const int qq = u / UPC, off = (u % UPC) * 16;  // qq is k * 32 / UPC: compile-time
                 const uint32_t g_off = sf * SL + off;
                 if (g_off < u_bytes[k])
-                    cp_async16_s(dst + qq * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                    cp_async16_s(dst + qq * PITCH + swz_off(CFG::kSwz, qq, off),
+                                 reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
             }
         }
     };
@@ -510,11 +523,13 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const uint64_t* p = reinterpret_cast<const uint64_t*>(wring + st * WSTAGE + q * PITCH) + ql;
             const uint32_t done = s * (SL / 32);
             const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
+            const int sq = CFG::kSwz ? (q & 3) : 0;  // stripe t of this quad at row position t ^ sq
             if (n == SL / 32) {
+                const uint64_t* pb[4] = {p + 4 * (0 ^ sq), p + 4 * (1 ^ sq), p + 4 * (2 ^ sq), p + 4 * (3 ^ sq)};
 #pragma unroll
-                for (int t = 0; t < SL / 32; ++t) v = ystep(v, p[4 * t]);
+                for (int t = 0; t < SL / 32; ++t) v = ystep(v, pb[t & 3][4 * (t & ~3)]);
             } else {
-                for (uint32_t t = 0; t < n; ++t) v = ystep(v, p[4 * t]);
+                for (uint32_t t = 0; t < n; ++t) v = ystep(v, p[4 * (t ^ sq)]);
             }
             if (COPY) {  // the stage's 8 slices -> the arena, before the slot is refilled
 #pragma unroll
@@ -526,7 +541,8 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
                     const uint32_t g_off = s * SL + off;
                     if (g_off < b)
                         st_cs16(reinterpret_cast<uint8_t*>(d) + g_off,
-                                *reinterpret_cast<const uint4*>(wring + st * WSTAGE + qq * PITCH + off));
+                                *reinterpret_cast<const uint4*>(wring + st * WSTAGE + qq * PITCH +
+                                                                swz_off(CFG::kSwz, qq, off)));
                 }
             }
             __syncwarp();
@@ -566,7 +582,8 @@ template <int HW, int STAGES, int SL>
 struct WsCfg {
     static_assert(HW >= 1 && HW <= 3, "SMSP 3 is left to the producers");
     static constexpr int kHashWarps = HW, kWarps = 4 * HW, kStages = STAGES, kSlice = SL;
-    static constexpr int kPitch = SL + 32;
+    static constexpr bool kSwz = true;
+    static constexpr int kPitch = SL;  // swizzled rows (swz_off)
     static constexpr int kWStage = 8 * kPitch;
     static constexpr int kUPC = SL / 16;
     static constexpr int kUPL = (8 * kUPC + 31) / 32;
@@ -660,7 +677,8 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
                         const int qq = u / UPC, off = (u % UPC) * 16;
                         const uint32_t g_off = sf * SL + off;
                         if (g_off < u_bytes[k])
-                            cp_async16_s(dst + qq * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                            cp_async16_s(dst + qq * PITCH + swz_off(CFG::kSwz, qq, off),
+                                         reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
                     }
                 }
                 cp_async_mbar_arrive_noinc_s(full_s + 8 * st);
@@ -674,6 +692,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
     const unsigned qmask = 0xFu << (lane & 28);
     // shared addresses computed once: this lane's word of stage 0, the stage's barriers
     const uint64_t* xp0 = reinterpret_cast<const uint64_t*>(wring + q * PITCH) + ql;
+    const int sq = CFG::kSwz ? (q & 3) : 0;  // stripe t of this quad at row position t ^ sq
     const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
     uint32_t st = 0, ph = 0;
     for (uint64_t j = j0; j < ngroups; j += W) {
@@ -688,11 +707,12 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             mbar_wait_s(full_s + 8 * st, ph);
             const uint64_t* xp = xp0 + st * (WSTAGE / 8);
             if (left >= (uint32_t)(SL / 32)) {
+                const uint64_t* pb[4] = {xp + 4 * (0 ^ sq), xp + 4 * (1 ^ sq), xp + 4 * (2 ^ sq), xp + 4 * (3 ^ sq)};
 #pragma unroll
-                for (int t = 0; t < SL / 32; ++t) v = ystep(v, xp[4 * t]);
+                for (int t = 0; t < SL / 32; ++t) v = ystep(v, pb[t & 3][4 * (t & ~3)]);
                 left -= SL / 32;
             } else {
-                for (uint32_t t = 0; t < left; ++t) v = ystep(v, xp[4 * t]);
+                for (uint32_t t = 0; t < left; ++t) v = ystep(v, xp[4 * (t ^ sq)]);
                 left = 0;
             }
             __syncwarp();
@@ -720,7 +740,8 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
 template <int WARPS, int STAGES, int SL>
 struct CmpCfg {
     static constexpr int kWarps = WARPS, kStages = STAGES, kSlice = SL;
-    static constexpr int kPitch = SL + 32;
+    static constexpr bool kSwz = true;
+    static constexpr int kPitch = SL;  // swizzled rows (swz_off)
     static constexpr int kWStage = 16 * kPitch;          // 8 actual + 8 reference slices
     static constexpr int kUPC = SL / 16;                 // 16-byte units per slice
     static constexpr int kUPL = (16 * kUPC + 31) / 32;   // units per lane per step
@@ -803,7 +824,8 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
                 const int slot = u / UPC, off = (u % UPC) * 16;  // slot 0-7 actual, 8-15 reference
                 const uint32_t g_off = sf * SL + off;
                 if (g_off < u_bytes[k])
-                    cp_async16_s(dst + slot * PITCH + off, reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                    cp_async16_s(dst + slot * PITCH + swz_off(CFG::kSwz, slot, off),
+                                 reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
             }
         }
     };
@@ -854,18 +876,25 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const uint64_t* pr = reinterpret_cast<const uint64_t*>(wring + st * WSTAGE + (8 + q) * PITCH) + ql;
             const uint32_t done = s * (SL / 32);
             const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
-            auto word = [&](int t) {
-                const uint64_t a = pa[4 * t], r = SELF ? a : pr[4 * t];
+            const int sq = CFG::kSwz ? (q & 3) : 0;  // stripe t of this quad at row position t ^ sq
+            auto word = [&](uint64_t a, uint64_t r) {
                 v = ystep(v, a);
                 if (!SELF) x |= a ^ r;
                 sp_lo |= ((uint32_t)r & sm.m_lo) + sm.a_lo;
                 sp_hi |= ((uint32_t)(r >> 32) & sm.m_hi) + sm.a_hi;
             };
             if (n == SL / 32) {
+                const int o[4] = {4 * (0 ^ sq), 4 * (1 ^ sq), 4 * (2 ^ sq), 4 * (3 ^ sq)};
 #pragma unroll
-                for (int t = 0; t < SL / 32; ++t) word(t);
+                for (int t = 0; t < SL / 32; ++t) {
+                    const uint64_t a = pa[o[t & 3] + 4 * (t & ~3)];
+                    word(a, SELF ? a : pr[o[t & 3] + 4 * (t & ~3)]);
+                }
             } else {
-                for (uint32_t t = 0; t < n; ++t) word(t);
+                for (uint32_t t = 0; t < n; ++t) {
+                    const uint64_t a = pa[4 * (t ^ sq)];
+                    word(a, SELF ? a : pr[4 * (t ^ sq)]);
+                }
             }
             __syncwarp();
             fetch((step + STAGES - 1) % STAGES);
@@ -2043,6 +2072,7 @@ __global__ void k4_gather(const uint64_t* __restrict__ src, const uint64_t* __re
 using TmaA = HkCfg<256, 3, 1024>;  // 64 slots x 3 x 1 KiB
 using TmaB = HkCfg<128, 3, 2048>;  // 32 slots x 3 x 2 KiB
 using CpA = CpCfg<8, 3, 1024>;   // 64 chunks/SM x 3 x 1 KiB   (default: HBM-bound)
+using CpA0 = CpCfg<8, 3, 1024, false>;  // round 2's padded (unswizzled) slices, for A/B
 using CpD = CpCfg<16, 3, 512>;   // 128 chunks/SM x 3 x 512 B
 using CpS = CpCfg<2, 6, 1024>;   // small snapshots: 2-warp CTAs, 6-deep rings, so < 148 x 64 chunks still
                                  // spread over every SM (a chunk's hash is a ~25 us serial chain)
@@ -2058,7 +2088,7 @@ cudaError_t kernels_init() {
 #define KC_CP_ATTR(CFG)                                                                                      \
     if (e == cudaSuccess)                                                                                    \
         e = cudaFuncSetAttribute(k1_hash_cpasync<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
-    KC_CP_ATTR(CpA) KC_CP_ATTR(CpD) KC_CP_ATTR(CpS)
+    KC_CP_ATTR(CpA) KC_CP_ATTR(CpD) KC_CP_ATTR(CpS) KC_CP_ATTR(CpA0)
 #undef KC_CP_ATTR
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1_hash_cpasync<CpA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2173,6 +2203,7 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
         case 1: launch_tma<TmaA>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 2: launch_tma<TmaB>(d_regs, nreg, C, d_out, map, num_sms, s); break;
         case 3: launch_cp<CpD>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
+        case 9: launch_cp<CpA0>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order); break;
         case 4:  // round 2's sub-wave path (CpS below one wave), for A/B
             if ((C + 7) / 8 < (uint64_t)num_sms * 8)
                 launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
