@@ -12,7 +12,7 @@ B="python bench.py --steps 2 --warmup 1 --no-e2e --no-latency --no-configs --no-
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k2_diff<.int.10," \
     --launch-skip 1 -c 1 -o "$O/k2_bench" $B --no-fused > "$O/k2_ncu.log" 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k regex:"CpCfg<.int.8, .int.3, .int.1024>, .bool.0>" --launch-skip 3 -c 1 -o "$O/k1_bench" $B --no-fused \
+    -k regex:"CpCfg<.int.8, .int.3, .int.1024, .bool.1>, .bool.0>" --launch-skip 3 -c 1 -o "$O/k1_bench" $B --no-fused \
     > "$O/k1_ncu.log" 2>&1
 [ "${SKIP_K5:-0}" = 1 ] || ncu --set full --clock-control none --import-source on -k regex:k5_hash_cmp -c 1 -o "$O/k5_bench" $B \
     > "$O/k5_ncu.log" 2>&1
