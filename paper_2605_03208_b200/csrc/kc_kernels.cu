@@ -1942,8 +1942,7 @@ template <int DT, int THREADS, int MINB, int VU, int Q2>
 __global__ void __launch_bounds__(THREADS, MINB)
     k2_diff(const SegDev* __restrict__ segs, int seg0, int nseg, uint64_t unit0, uint64_t U,
             kc_diff_report* __restrict__ reps, unsigned long long* __restrict__ bitmaps, double atol, double rtol,
-            int equal_nan, const unsigned long long* __restrict__ filter, int blocked, uint32_t flush_units,
-            int l2_prefetch) {
+            int equal_nan, const unsigned long long* __restrict__ filter, int blocked, uint32_t flush_units) {
     const int lane = threadIdx.x & 31;
     segs += seg0;
     const uint64_t W = (uint64_t)gridDim.x * (THREADS / 32);
@@ -2007,18 +2006,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
         const uint8_t* R = reinterpret_cast<const uint8_t*>(sg.ref) + off;
         const uint8_t* A = reinterpret_cast<const uint8_t*>(sg.act) + off;
         const bool vec_ok = ((sg.ref | sg.act) & 31) == 0;
-        if (l2_prefetch && !filter && lane == 0 && vec_ok) {
-            // this warp's next unit of the same segment, pulled into L2 by one bulk prefetch per
-            // operand while this unit streams (KC_K2_L2_PREFETCH, A/B knob)
-            const uint64_t noff = off + (B == 1 ? W : 1) * (uint64_t)kDiffUnit;
-            if (noff < sg.nbytes) {
-                const uint32_t nl = (uint32_t)min((uint64_t)kDiffUnit, sg.nbytes - noff) & ~15u;
-                if (nl) {
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sg.ref + noff), "r"(nl) : "memory");
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sg.act + noff), "r"(nl) : "memory");
-                }
-            }
-        }
         acc.any = 0;
         diff_unit<DT, VU, Q2>(R, A, len, vec_ok, acc, atol, rtol, equal_nan, lane, q, qn, rq, rn);
         if (__any_sync(0xFFFFFFFFu, acc.any) && lane == 0 && bitmaps) {
@@ -2286,14 +2273,6 @@ static int k2_blocked(const DiffGroup& G) {
     return G.n_units < 256 * (uint64_t)G.n_segs;  // average segment < 4 MiB
 }
 
-static int k2_l2_prefetch() {
-    static const int v = [] {
-        const char* e = getenv("KC_K2_L2_PREFETCH");
-        return e && *e ? atoi(e) : 0;
-    }();
-    return v;
-}
-
 template <int DT, int THREADS, int MINB, int U, int Q2 = 1>
 static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_report* d_reps,
                           unsigned long long* bm, double atol, double rtol, int equal_nan, int num_sms,
@@ -2325,7 +2304,7 @@ static void launch_k2_cfg(const SegDev* d_segs, const DiffGroup& G, kc_diff_repo
     }();
     k2_diff<DT, THREADS, MINB, U, Q2><<<(unsigned)grid, THREADS, smem, s>>>(d_segs, G.seg0, G.n_segs, G.unit0, G.n_units,
                                                                          d_reps, bm, atol, rtol, equal_nan, filter,
-                                                                         k2_blocked(G), flush_units, k2_l2_prefetch());
+                                                                         k2_blocked(G), flush_units);
 }
 
 // Measured on B200 (tools/k2_bench.py): 512 threads x 1 CTA per
