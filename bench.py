@@ -515,7 +515,7 @@ def run_ours(a, rank, world, device, log):
     }
     if world > 1:
         kern["A9_combine_ms"] = per["combine"]
-    dom = "K2_diff" if 2 * k2_ms >= 2 * k1_ms else "K1_hash"
+    dom = "K2_diff" if k2_ms >= 2 * k1_ms else "K1_hash"   # K1 runs twice per step (pre and post)
     dom_ms = k2_ms if dom == "K2_diff" else 2 * k1_ms
     share = dom_ms / ms if ms else None
     traffic, traffic_src = None, None
