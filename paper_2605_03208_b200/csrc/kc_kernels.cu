@@ -707,9 +707,14 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             mbar_wait_s(full_s + 8 * st, ph);
             const uint64_t* xp = xp0 + st * (WSTAGE / 8);
             if (left >= (uint32_t)(SL / 32)) {
-                const uint64_t* pb[4] = {xp + 4 * (0 ^ sq), xp + 4 * (1 ^ sq), xp + 4 * (2 ^ sq), xp + 4 * (3 ^ sq)};
+                constexpr int UR = SL / 32 < 64 ? SL / 32 : 64;  // rounds unrolled per block (i-cache)
+#pragma unroll 1
+                for (int b = 0; b < SL / 32; b += UR) {
+                    const uint64_t* xb = xp + 4 * b;
+                    const uint64_t* pb[4] = {xb + 4 * (0 ^ sq), xb + 4 * (1 ^ sq), xb + 4 * (2 ^ sq), xb + 4 * (3 ^ sq)};
 #pragma unroll
-                for (int t = 0; t < SL / 32; ++t) v = ystep(v, pb[t & 3][4 * (t & ~3)]);
+                    for (int t = 0; t < UR; ++t) v = ystep(v, pb[t & 3][4 * (t & ~3)]);
+                }
                 left -= SL / 32;
             } else {
                 for (uint32_t t = 0; t < left; ++t) v = ystep(v, xp[4 * (t ^ sq)]);
@@ -2079,6 +2084,9 @@ using CpS = CpCfg<2, 6, 1024>;   // small snapshots: 2-warp CTAs, 6-deep rings, 
 using Ws1 = WsCfg<1, 4, 2048>;  // one CTA per SM, HW hashing warps (one per SMSP) + HW producers
 using Ws2 = WsCfg<2, 4, 2048>;  // on SMSP 3, 4 x 2 KiB slices (64 rounds between ring hand-overs)
 using Ws3 = WsCfg<3, 4, 2048>;
+using Ws1b = WsCfg<1, 2, 4096>;  // A/B: 2 x 4 KiB slices (half the ring hand-overs)
+using Ws2b = WsCfg<2, 2, 4096>;
+using Ws3b = WsCfg<3, 2, 4096>;
 using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
 
 cudaError_t kernels_init() {
@@ -2099,7 +2107,7 @@ cudaError_t kernels_init() {
 #define KC_WS_ATTR(CFG)                                                                                      \
     if (e == cudaSuccess)                                                                                    \
         e = cudaFuncSetAttribute(k1_hash_ws<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
-    KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3)
+    KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3) KC_WS_ATTR(Ws1b) KC_WS_ATTR(Ws2b) KC_WS_ATTR(Ws3b)
 #undef KC_WS_ATTR
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
@@ -2150,7 +2158,8 @@ static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d
                       const uint32_t* order = nullptr) {
     const uint64_t groups = (C + 7) / 8;
     // at most 8 warps' worth of CTAs per SM (one CTA of the 8-warp configs, four of CpS)
-    const uint64_t per_sm = CFG::kWarps >= 8 ? 1 : 8 / CFG::kWarps;
+    const uint64_t per_sm = std::min<uint64_t>(CFG::kWarps >= 8 ? 1 : 8 / CFG::kWarps,
+                                               std::max<uint64_t>(1, 232448 / (CFG::kSmem + 1024)));  // + smem fit
     const uint64_t grid = balanced_grid(groups, (uint64_t)num_sms * per_sm, CFG::kWarps);
     if (d_dst)
         k1_hash_cpasync<CFG, true><<<(unsigned)grid, CFG::kWarps * 32, CFG::kSmem, s>>>(d_regs, nreg, C, d_out, map,
@@ -2166,6 +2175,7 @@ static void launch_cp(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d
 // ceil(groups / SMs) <= 3 hashing warps on SMSPs 0..HW-1 and their producers on SMSP 3.  With
 // HW = 4 the producers must share SMSPs with hashing warps, and CpS (2-warp CTAs staging their
 // own rings, one warp per SMSP at that size) measured faster (1 MiB x 256: 49.2 vs 52.2 us).
+template <class W1, class W2, class W3>
 static bool launch_ws_subwave(const RegionDev* d_regs, int nreg, uint64_t C, uint64_t* d_out, const uint32_t* map,
                               int num_sms, cudaStream_t s, const uint32_t* order) {
     const uint64_t groups = (C + 7) / 8;
@@ -2173,9 +2183,9 @@ static bool launch_ws_subwave(const RegionDev* d_regs, int nreg, uint64_t C, uin
     if (hw > 3) return false;
     const unsigned grid = (unsigned)((groups + hw - 1) / hw);
     switch (hw) {
-        case 1: k1_hash_ws<Ws1><<<grid, Ws1::kWarps * 32, Ws1::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
-        case 2: k1_hash_ws<Ws2><<<grid, Ws2::kWarps * 32, Ws2::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
-        default: k1_hash_ws<Ws3><<<grid, Ws3::kWarps * 32, Ws3::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        case 1: k1_hash_ws<W1><<<grid, W1::kWarps * 32, W1::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        case 2: k1_hash_ws<W2><<<grid, W2::kWarps * 32, W2::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
+        default: k1_hash_ws<W3><<<grid, W3::kWarps * 32, W3::kSmem, s>>>(d_regs, nreg, C, d_out, map, order); break;
     }
     return true;
 }
@@ -2216,7 +2226,9 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
             // wave of 8-warp CTAs, CpS spread over every SM (round 2 A/B on c2: a per-quad TMA
             // bulk ring of 16 slots x 3 x 2 KiB 92-129 us; a warp ring filled by one bulk copy per
             // chunk slice from the quad leaders, 66 us; CpS 48-50 us); above, CpA
-            if (launch_ws_subwave(d_regs, nreg, C, d_out, map, num_sms, s, order)) break;
+            if (k1_variant() == 12 ? launch_ws_subwave<Ws1b, Ws2b, Ws3b>(d_regs, nreg, C, d_out, map, num_sms, s, order)
+                                   : launch_ws_subwave<Ws1, Ws2, Ws3>(d_regs, nreg, C, d_out, map, num_sms, s, order))
+                break;
             if ((C + 7) / 8 < (uint64_t)num_sms * 8)
                 launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
             else
