@@ -2084,9 +2084,6 @@ using CpS = CpCfg<2, 6, 1024>;   // small snapshots: 2-warp CTAs, 6-deep rings, 
 using Ws1 = WsCfg<1, 4, 2048>;  // one CTA per SM, HW hashing warps (one per SMSP) + HW producers
 using Ws2 = WsCfg<2, 4, 2048>;  // on SMSP 3, 4 x 2 KiB slices (64 rounds between ring hand-overs)
 using Ws3 = WsCfg<3, 4, 2048>;
-using Ws1b = WsCfg<1, 2, 4096>;  // A/B: 2 x 4 KiB slices (half the ring hand-overs)
-using Ws2b = WsCfg<2, 2, 4096>;
-using Ws3b = WsCfg<3, 2, 4096>;
 using CmpA = CmpCfg<8, 3, 512>;  // K5: 64 chunk pairs/SM x 3 x (512 B act + 512 B ref)
 
 cudaError_t kernels_init() {
@@ -2107,7 +2104,7 @@ cudaError_t kernels_init() {
 #define KC_WS_ATTR(CFG)                                                                                      \
     if (e == cudaSuccess)                                                                                    \
         e = cudaFuncSetAttribute(k1_hash_ws<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFG::kSmem);
-    KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3) KC_WS_ATTR(Ws1b) KC_WS_ATTR(Ws2b) KC_WS_ATTR(Ws3b)
+    KC_WS_ATTR(Ws1) KC_WS_ATTR(Ws2) KC_WS_ATTR(Ws3)
 #undef KC_WS_ATTR
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k5_hash_cmp<CmpA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CmpA::kSmem);
@@ -2226,9 +2223,7 @@ cudaError_t launch_hash(const RegionDev* d_regs, int nreg, uint64_t C, bool alig
             // wave of 8-warp CTAs, CpS spread over every SM (round 2 A/B on c2: a per-quad TMA
             // bulk ring of 16 slots x 3 x 2 KiB 92-129 us; a warp ring filled by one bulk copy per
             // chunk slice from the quad leaders, 66 us; CpS 48-50 us); above, CpA
-            if (k1_variant() == 12 ? launch_ws_subwave<Ws1b, Ws2b, Ws3b>(d_regs, nreg, C, d_out, map, num_sms, s, order)
-                                   : launch_ws_subwave<Ws1, Ws2, Ws3>(d_regs, nreg, C, d_out, map, num_sms, s, order))
-                break;
+            if (launch_ws_subwave<Ws1, Ws2, Ws3>(d_regs, nreg, C, d_out, map, num_sms, s, order)) break;
             if ((C + 7) / 8 < (uint64_t)num_sms * 8)
                 launch_cp<CpS>(d_regs, nreg, C, d_out, map, num_sms, s, nullptr, order);
             else
