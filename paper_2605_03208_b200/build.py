@@ -43,17 +43,25 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> str:
+LIB_CHECKED = os.path.join(PKG, "libkc_checked.so")
+
+
+def build_lib(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
     """One object per translation unit, compiled in parallel (objects under
-    build/, rebuilt when their source or any header changed), then linked."""
+    build/, rebuilt when their source or any header changed), then linked.
+    checked=True builds libkc_checked.so with -DKC_CHECKS=1 (device bounds checks
+    on the rings, queues and chunk lookups; loaded when KC_LIB=checked)."""
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "kc.h"), __file__]
-    objdir = os.path.join(ROOT, "build", "kc_obj")
+    objdir = os.path.join(ROOT, "build", "kc_obj_checked" if checked else "kc_obj")
+    LIB = LIB_CHECKED if checked else globals()["LIB"]
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
     todo = [(s, o) for s, o in zip(SOURCES, objs) if force or _stale(o, [os.path.join(CSRC, s)] + hdrs)]
     if not todo and not _stale(LIB, objs):
         return LIB
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2"]
+    if checked:
+        flags.append("-DKC_CHECKS=1")
     if verbose:
         flags.insert(0, "-Xptxas=-v")
 
@@ -96,5 +104,8 @@ def build(force: bool = False, verbose: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--checked" in sys.argv:
+        print(build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv, checked=True))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

@@ -20,6 +20,27 @@
 
 #include "kc_kernels.cuh"
 
+// KC_CHECKS=1 (libkc_checked.so, `python -m paper_2605_03208_b200.build --checked`): device-side
+// bounds checks on every shared-memory ring slot, queue push and chunk lookup of the hot path,
+// trapping with the failing condition.  The GPU pool has compute-sanitizer disabled, so the
+// checked build run under the parity tests stands in for memcheck on these kernels.
+#ifndef KC_CHECKS
+#define KC_CHECKS 0
+#endif
+#if KC_CHECKS
+#include <cstdio>
+#define KC_DCHECK(c)                                                                                    \
+    do {                                                                                                \
+        if (!(c)) {                                                                                     \
+            printf("KC_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #c, __FILE__, __LINE__,       \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                  \
+            __trap();                                                                                   \
+        }                                                                                               \
+    } while (0)
+#else
+#define KC_DCHECK(c) ((void)0)
+#endif
+
 namespace kc {
 
 // ========================================================================== //
@@ -270,7 +291,9 @@ struct ChunkRef {
 __device__ __forceinline__ ChunkRef chunk_ref(const RegionDev* __restrict__ regs, int nreg, uint64_t g,
                                              const uint32_t* __restrict__ map) {
     const int r = map ? (int)__ldg(map + g) : find_region(regs, nreg, g);
+    KC_DCHECK(r >= 0 && r < nreg && regs[r].chunk_off <= g);
     const uint64_t off = (g - regs[r].chunk_off) * kChunk;
+    KC_DCHECK(off < regs[r].size);
     const uint64_t rem = regs[r].size - off;
     return {reinterpret_cast<const uint8_t*>(regs[r].base + off), rem < kChunk ? (uint32_t)rem : (uint32_t)kChunk};
 }
@@ -475,9 +498,13 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             if (u < 8 * UPC) {
                 const int qq = u / UPC, off = (u % UPC) * 16;  // qq is k * 32 / UPC: compile-time
                 const uint32_t g_off = sf * SL + off;
-                if (g_off < u_bytes[k])
+                if (g_off < u_bytes[k]) {
+                    KC_DCHECK(dst + qq * PITCH + swz_off(CFG::kSwz, qq, off) + 16 <= wring_s - w * STAGES * WSTAGE +
+                                                                                       CFG::kSmem);
+                    KC_DCHECK(g_off + 16 <= u_bytes[k]);
                     cp_async16_s(dst + qq * PITCH + swz_off(CFG::kSwz, qq, off),
                                  reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                }
             }
         }
     };
@@ -524,6 +551,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             const uint32_t done = s * (SL / 32);
             const uint32_t n = nst > done ? min((uint32_t)(SL / 32), nst - done) : 0u;
             const int sq = CFG::kSwz ? (q & 3) : 0;  // stripe t of this quad at row position t ^ sq
+            KC_DCHECK(reinterpret_cast<const uint8_t*>(p) - smem + 32 * (SL / 32 - 1) + 8 <= (long)CFG::kSmem);
             if (n == SL / 32) {
                 const uint64_t* pb[4] = {p + 4 * (0 ^ sq), p + 4 * (1 ^ sq), p + 4 * (2 ^ sq), p + 4 * (3 ^ sq)};
 #pragma unroll
@@ -676,9 +704,13 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
                     if (u < 8 * UPC) {
                         const int qq = u / UPC, off = (u % UPC) * 16;
                         const uint32_t g_off = sf * SL + off;
-                        if (g_off < u_bytes[k])
+                        if (g_off < u_bytes[k]) {
+                            KC_DCHECK(dst + qq * PITCH + swz_off(CFG::kSwz, qq, off) + 16 <=
+                                      smem_u32(smem) + CFG::kRing);
+                            KC_DCHECK(g_off + 16 <= u_bytes[k]);
                             cp_async16_s(dst + qq * PITCH + swz_off(CFG::kSwz, qq, off),
                                          reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                        }
                     }
                 }
                 cp_async_mbar_arrive_noinc_s(full_s + 8 * st);
@@ -706,6 +738,8 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
         for (uint32_t s = 0; s < nsl; ++s) {
             mbar_wait_s(full_s + 8 * st, ph);
             const uint64_t* xp = xp0 + st * (WSTAGE / 8);
+            KC_DCHECK(st < (uint32_t)STAGES &&
+                      reinterpret_cast<const uint8_t*>(xp) - smem + 32 * (SL / 32 - 1) + 8 <= (long)CFG::kRing);
             if (left >= (uint32_t)(SL / 32)) {
                 constexpr int UR = SL / 32 < 64 ? SL / 32 : 64;  // rounds unrolled per block (i-cache)
 #pragma unroll 1
@@ -828,9 +862,13 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
             if (u < (SELF ? 8 : 16) * UPC) {
                 const int slot = u / UPC, off = (u % UPC) * 16;  // slot 0-7 actual, 8-15 reference
                 const uint32_t g_off = sf * SL + off;
-                if (g_off < u_bytes[k])
+                if (g_off < u_bytes[k]) {
+                    KC_DCHECK(dst + slot * PITCH + swz_off(CFG::kSwz, slot, off) + 16 <=
+                              wring_s - w * STAGES * WSTAGE + CFG::kSmem);
+                    KC_DCHECK(g_off + 16 <= u_bytes[k]);
                     cp_async16_s(dst + slot * PITCH + swz_off(CFG::kSwz, slot, off),
                                  reinterpret_cast<const uint8_t*>(u_src[k]) + g_off);
+                }
             }
         }
     };
@@ -888,6 +926,7 @@ __global__ void __launch_bounds__(CFG::kWarps * 32, 1)
                 sp_lo |= ((uint32_t)r & sm.m_lo) + sm.a_lo;
                 sp_hi |= ((uint32_t)(r >> 32) & sm.m_hi) + sm.a_hi;
             };
+            KC_DCHECK(reinterpret_cast<const uint8_t*>(pr) - smem + 32 * (SL / 32 - 1) + 8 <= (long)CFG::kSmem);
             if (n == SL / 32) {
                 const int o[4] = {4 * (0 ^ sq), 4 * (1 ^ sq), 4 * (2 ^ sq), 4 * (3 ^ sq)};
 #pragma unroll
@@ -1638,6 +1677,7 @@ __device__ __forceinline__ void q_drain16(uint32_t* q, uint32_t& qn, uint32_t* r
         acc.dbytes += (uint32_t)((xs & 0x00FF0000u) != 0) + (uint32_t)(xs >= 0x01000000u);
         const bool rare = elem16_rare<DT>(t, xs, acc);
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, rare);
+        KC_DCHECK(rn + __popc(bal) <= (uint32_t)(kRareBytes / 4));
         if (rare) rq[rn + __popc(bal & lt)] = t;
         rn += __popc(bal);
         if (rn >= 32) rq_round<DT>(rq, rn, acc, atol, rtol, equal_nan, lane);
@@ -1751,6 +1791,7 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
                             else q_push16_addr(rw[u], aw[u], mw[u], sa);
                         }
                         qn += total;
+                        KC_DCHECK((qn <= (uint32_t)KQ<DT, U>::kCap));
                     }
                     v += 32 * U;
                     if (k + 1 < nsteps) {
@@ -1798,11 +1839,13 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
                             else q_push16_addr(rw[u], aw[u], mw[u], sa);
                         }
                         qn += total;
+                        KC_DCHECK((qn <= (uint32_t)KQ<DT, U>::kCap));
                         if (qn >= 32) q_drain16<DT>(q, qn, rq, rn, acc, atol, rtol, equal_nan, lane);
                     } else {
 #pragma unroll
                         for (int u = 0; u < U; ++u) q_push16<DT>(rw[u], aw[u], mw[u], q, pos);
                         qn += total;
+                        KC_DCHECK((qn <= (uint32_t)KQ<DT, U>::kCap));
                         if (qn >= 32) q_drain<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
                     }
                 }
@@ -1831,6 +1874,7 @@ __device__ __forceinline__ void diff_unit(const uint8_t* R, const uint8_t* A, ui
 #pragma unroll
                     for (int u = 0; u < U; ++u) q_push<DT>(rw[u], aw[u], m[u], q, pos);
                     qn += total;
+                        KC_DCHECK((qn <= (uint32_t)KQ<DT, U>::kCap));
                     if (qn >= 32) q_drain<DT>(q, qn, acc, atol, rtol, equal_nan, lane);
                 }
                 continue;

@@ -16,7 +16,8 @@ from dataclasses import dataclass
 from typing import Iterable, Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libkc.so")
+# KC_LIB=checked loads the bounds-checked build (libkc_checked.so, -DKC_CHECKS=1)
+LIB_PATH = os.path.join(_PKG, "libkc_checked.so" if os.environ.get("KC_LIB") == "checked" else "libkc.so")
 
 KC_CHUNK_BYTES = 65536
 
