@@ -439,7 +439,11 @@ kc_status kc_capture_incr(kc_ctx* ctx, const kc_dispatch* d, const kc_region* re
 kc_status kc_host_arena_reserve(kc_ctx* ctx, uint64_t bytes);
 /* Map `bytes` of device memory (one VMM allocation) ahead of time and park it
  * in the ctx for kc_capture_dev; a freed device snapshot also parks its arena
- * there when it is the larger one (never an exported one).  0 releases it. */
+ * there when it is the larger one (never an exported one).  0 releases it, and
+ * with it the physical allocations parked by released restores (a released
+ * kc_restored parks each span's physical allocation in the ctx, up to
+ * KC_PHYS_PARK_MAX bytes, default 96 GiB; the next restore takes a parked one of
+ * the same size instead of cuMemCreate; KC_PHYS_PARK=0 releases them at once). */
 kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes);
 /* Same-VA restore from an in-memory snapshot (device or pinned host arena; the
  * originals must be freed first): VA windows as kc_restore (or the ctx VA

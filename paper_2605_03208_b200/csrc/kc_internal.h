@@ -126,6 +126,12 @@ struct kc_ctx {
             h = 0;
         }
     } dev_arena;
+    // physical VMM allocations of released restores, parked by size and reused by the next
+    // restore of the same span sizes (no cuMemCreate / scrub of freshly released memory on a
+    // resident tool's repeated capture -> restore cycles); KC_PHYS_PARK=0 disables, and
+    // kc_dev_arena_reserve(ctx, 0) or kc_destroy releases them
+    std::multimap<uint64_t, CUmemGenericAllocationHandle> phys_park;
+    uint64_t phys_park_bytes = 0;
     // parked pinned host arena for kc_capture_host (kc_host_arena_reserve)
     void* host_arena = nullptr;
     uint64_t host_arena_bytes = 0;

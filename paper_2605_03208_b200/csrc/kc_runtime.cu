@@ -349,6 +349,8 @@ void kc_destroy(kc_ctx* ctx) {
     std::vector<uint64_t> vm;
     for (auto& kv : ctx->vmm) vm.push_back(kv.first);
     for (uint64_t b : vm) free_alloc(ctx, b, false);
+    for (auto& kv : ctx->phys_park) KC_DRV(cuMemRelease)(kv.second);
+    ctx->phys_park.clear();
     if (ctx->heap_base) KC_DRV(cuMemAddressFree)((CUdeviceptr)ctx->heap_base, ctx->heap_size);
     if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
     ctx->dev_arena.release();

@@ -999,12 +999,45 @@ std::vector<std::pair<uint64_t, uint64_t>> make_spans(const std::vector<ParsedRe
     return spans;
 }
 
+// physical allocations of released restores (kc_ctx::phys_park): parked up to
+// KC_PHYS_PARK_MAX bytes (default 96 GiB) unless KC_PHYS_PARK=0
+bool phys_park_on() {
+    static const bool on = [] {
+        const char* e = getenv("KC_PHYS_PARK");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+uint64_t phys_park_max() {
+    static const uint64_t m = [] {
+        const char* e = getenv("KC_PHYS_PARK_MAX");
+        return e && *e ? strtoull(e, nullptr, 10) : (96ull << 30);
+    }();
+    return m;
+}
+void phys_release(kc_ctx* ctx, CUmemGenericAllocationHandle h, uint64_t size) {
+    if (ctx && phys_park_on() && ctx->phys_park_bytes + size <= phys_park_max()) {
+        ctx->phys_park.emplace(size, h);
+        ctx->phys_park_bytes += size;
+        return;
+    }
+    KC_DRV(cuMemRelease)(h);
+}
+bool phys_take(kc_ctx* ctx, uint64_t size, CUmemGenericAllocationHandle* h) {
+    auto it = ctx->phys_park.find(size);
+    if (it == ctx->phys_park.end()) return false;
+    *h = it->second;
+    ctx->phys_park.erase(it);
+    ctx->phys_park_bytes -= size;
+    return true;
+}
+
 void rollback(kc_restored* h) {
     for (auto it = h->spans.rbegin(); it != h->spans.rend(); ++it) {
         for (uint64_t p : it->memalloc) KC_DRV(cuMemFree)((CUdeviceptr)p);
         it->memalloc.clear();
         if (it->mapped) KC_DRV(cuMemUnmap)((CUdeviceptr)it->base, it->size);
-        if (it->created) KC_DRV(cuMemRelease)(it->h);
+        if (it->created) phys_release(h->ctx, it->h, it->size);
         if (it->heap) heap_put(h->ctx, it->base, it->size);
     }
     h->spans.clear();
@@ -1420,7 +1453,7 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     }
     for (auto& s : h->spans) {
         if (s.fallback) continue;
-        cr = KC_DRV(cuMemCreate)(&s.h, s.size, &prop, 0);
+        cr = phys_take(ctx, s.size, &s.h) ? CUDA_SUCCESS : KC_DRV(cuMemCreate)(&s.h, s.size, &prop, 0);
         if (cr == CUDA_SUCCESS) {
             s.created = true;
             cr = KC_DRV(cuMemMap)((CUdeviceptr)s.base, s.size, 0, s.h, 0);
@@ -1983,6 +2016,9 @@ extern "C" kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes) {
     cudaDeviceSynchronize();
     if (bytes == 0) {
         ctx->dev_arena.release();
+        for (auto& kv : ctx->phys_park) KC_DRV(cuMemRelease)(kv.second);
+        ctx->phys_park.clear();
+        ctx->phys_park_bytes = 0;
         return KC_OK;
     }
     if (ctx->dev_arena.size >= bytes) return KC_OK;
