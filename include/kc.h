@@ -449,6 +449,17 @@ kc_status kc_dev_arena_reserve(kc_ctx* ctx, uint64_t bytes);
  * originals must be freed first): VA windows as kc_restore (or the ctx VA
  * heap), then copy-in (D2D or H2D) and the K1 verify. */
 kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restored** out, kc_restore_report* rep);
+/* Restore an in-memory snapshot into a LIVE restore of the same regions (the same
+ * bases, sizes and ok flags, in order): the VA windows and mappings of `r` are kept
+ * (no reservation, no cuMemCreate / cuMemMap), and stages 5-6 of kc_restore_dev run
+ * on them: zero-fill, copy-in fused with the verify hashes (K6), verify, W stashes.
+ * `r` takes the snapshot's dispatch, written sets and post manifests, so kc_replay /
+ * kc_validate then act on the new capture.  This is the repeated-replay fast path of
+ * a resident tool (capture from the restored state, restore over it, replay again;
+ * PAPER.md:1100-1108's stage 5 without stages 2-4).  KC_ERR_ARG when the region
+ * lists differ; on a copy-in or verify failure `r` stays mapped with undefined
+ * contents (release it, or restore into it again). */
+kc_status kc_restore_dev_into(kc_ctx* ctx, const kc_snapshot* s, kc_restored* r, kc_restore_report* rep);
 /* Persist an in-memory snapshot as a kc-snapshot/1 directory (parallel). */
 kc_status kc_snapshot_save(kc_ctx* ctx, const kc_snapshot* s, const char* dir);
 /* F1 across processes: persist the snapshot's metadata, manifests and W bytes

@@ -1326,6 +1326,86 @@ static kc_status build_stash(kc_ctx* ctx, kc_restored* h, const SnapDesc& d, Res
     return KC_OK;
 }
 
+// Stages 5-6 of a restore into mapped spans: zero-fill what the copy-in does not write,
+// copy in (fused with the verify hashes when the source allows), verify against the
+// captured manifest, and build the W stashes.  Shared by kc_restore / kc_restore_dev
+// (fresh mappings) and kc_restore_dev_into (the mappings of a live restore).
+static kc_status restore_fill(kc_ctx* ctx, kc_restored* h, const SnapDesc& d, RestoreSource& src,
+                              kc_restore_report& rep) {
+    double t, tl = now_s();
+    // ---- stage 5a: copy-in (gaps and failed regions zero-filled, SPEC.md:628)
+    t = now_s();
+    kc_status st = src.needs_staging() ? ensure_pinned(ctx) : ensure_stream(ctx);
+    if (st != KC_OK) return st;
+    // zero only what the copy-in does not write: span bytes outside every ok
+    // region (granule padding) and failed regions; an ok region's stored bytes
+    // cover it entirely (its region file / arena runs are exactly `size` bytes,
+    // and the K1 verify below checks every chunk)
+    {
+        std::vector<std::pair<uint64_t, uint64_t>> ok_iv;  // ascending (regions are sorted by base)
+        for (auto& rr : h->regions) {
+            if (rr.ok) ok_iv.emplace_back(rr.r.base, rr.r.base + rr.r.size);
+            else cudaMemsetAsync((void*)rr.r.base, 0, rr.r.size, ctx->copy_stream);
+        }
+        size_t j = 0;
+        for (auto& s : h->spans) {
+            if (s.fallback) continue;
+            uint64_t cur = s.base;
+            const uint64_t end = s.base + s.size;
+            while (j < ok_iv.size() && ok_iv[j].second <= cur) ++j;
+            for (size_t k = j; k < ok_iv.size() && ok_iv[k].first < end; ++k) {
+                if (ok_iv[k].first > cur) cudaMemsetAsync((void*)cur, 0, ok_iv[k].first - cur, ctx->copy_stream);
+                cur = std::max(cur, ok_iv[k].second);
+            }
+            if (cur < end) cudaMemsetAsync((void*)cur, 0, end - cur, ctx->copy_stream);
+        }
+    }
+    cudaStreamSynchronize(ctx->copy_stream);  // zero-fill before the copy-in streams
+    trace("restore: zero-fill gaps", tl);
+    std::vector<uint64_t> got;
+    bool verified = false;  // the copy-in produced the verify hashes itself (K6)
+    st = src.copy_in_verify(ctx, d, rep, got, verified);
+    if (st == KC_OK && !verified) st = src.copy_in(ctx, d, rep);
+    cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+    if (st == KC_OK && ce != cudaSuccess) st = cuda_err(ctx, ce, "kc_restore: copy-in");
+    if (st != KC_OK) return st;
+    rep.t_h2d_s = now_s() - t;
+    trace(verified ? "restore: copy-in + verify (K6)" : "restore: copy-in", tl);
+
+    // ---- verify against the captured manifest (K1, O6)
+    t = now_s();
+    std::vector<kc_region> okregs;
+    for (auto& rr : h->regions)
+        if (rr.ok) okregs.push_back(rr.r);
+    if (!verified) st = hash_regions_sync(ctx, okregs, got, nullptr, nullptr, nullptr, ctx->copy_stream);
+    if (st != KC_OK) return st;
+    {
+        uint64_t c = 0, mism = 0;
+        for (auto& sr : d.regions) {
+            if (!sr.ok) continue;
+            if (sr.manifest.size() != sr.n_chunks) {
+                mism += sr.n_chunks;
+            } else {
+                for (uint64_t k = 0; k < sr.n_chunks; ++k) mism += sr.manifest[k] != got[c + k];
+            }
+            c += sr.n_chunks;
+        }
+        rep.verify_mismatch_chunks = mism;
+    }
+    rep.t_verify_s = now_s() - t;
+    if (rep.verify_mismatch_chunks) {
+        return set_err(ctx, KC_ERR_MANIFEST_MISMATCH, "kc_restore: %llu restored chunk(s) do not match the captured "
+                       "manifest", (unsigned long long)rep.verify_mismatch_chunks);
+    }
+
+    trace("restore: verify", tl);
+    // ---- device stashes of the written chunks: replay recopy (pre) and validation reference (post)
+    st = build_stash(ctx, h, d, src);
+    trace("restore: W stashes", tl);
+    if (st != KC_OK) return st;
+    return KC_OK;
+}
+
 static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src, kc_restored** out,
                               kc_restore_report* rep_out, kc_restore_report& rep, double t0) {
     kc_restored* h = new kc_restored();
@@ -1514,97 +1594,14 @@ static kc_status restore_core(kc_ctx* ctx, const SnapDesc& d, RestoreSource& src
     }
     rep.n_spans = h->spans.size();
     rep.t_reserve_s = now_s() - t;
-    double tl = now_s();
     trace("restore: reserve + create + map", t);
 
-    // ---- stage 5a: copy-in (gaps and failed regions zero-filled, SPEC.md:628)
-    t = now_s();
-    kc_status st = src.needs_staging() ? ensure_pinned(ctx) : ensure_stream(ctx);
-    if (st != KC_OK) {
-        rollback(h);
-        delete h;
-        return st;
-    }
-    // zero only what the copy-in does not write: span bytes outside every ok
-    // region (granule padding) and failed regions; an ok region's stored bytes
-    // cover it entirely (its region file / arena runs are exactly `size` bytes,
-    // and the K1 verify below checks every chunk)
-    {
-        std::vector<std::pair<uint64_t, uint64_t>> ok_iv;  // ascending (regions are sorted by base)
-        for (auto& rr : h->regions) {
-            if (rr.ok) ok_iv.emplace_back(rr.r.base, rr.r.base + rr.r.size);
-            else cudaMemsetAsync((void*)rr.r.base, 0, rr.r.size, ctx->copy_stream);
-        }
-        size_t j = 0;
-        for (auto& s : h->spans) {
-            if (s.fallback) continue;
-            uint64_t cur = s.base;
-            const uint64_t end = s.base + s.size;
-            while (j < ok_iv.size() && ok_iv[j].second <= cur) ++j;
-            for (size_t k = j; k < ok_iv.size() && ok_iv[k].first < end; ++k) {
-                if (ok_iv[k].first > cur) cudaMemsetAsync((void*)cur, 0, ok_iv[k].first - cur, ctx->copy_stream);
-                cur = std::max(cur, ok_iv[k].second);
-            }
-            if (cur < end) cudaMemsetAsync((void*)cur, 0, end - cur, ctx->copy_stream);
-        }
-    }
-    cudaStreamSynchronize(ctx->copy_stream);  // zero-fill before the copy-in streams
-    trace("restore: zero-fill gaps", tl);
-    std::vector<uint64_t> got;
-    bool verified = false;  // the copy-in produced the verify hashes itself (K6)
-    st = src.copy_in_verify(ctx, d, rep, got, verified);
-    if (st == KC_OK && !verified) st = src.copy_in(ctx, d, rep);
-    cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
-    if (st == KC_OK && ce != cudaSuccess) st = cuda_err(ctx, ce, "kc_restore: copy-in");
-    if (st != KC_OK) {
-        rollback(h);
-        delete h;
-        return st;
-    }
-    rep.t_h2d_s = now_s() - t;
-    trace(verified ? "restore: copy-in + verify (K6)" : "restore: copy-in", tl);
-
-    // ---- verify against the captured manifest (K1, O6)
-    t = now_s();
-    std::vector<kc_region> okregs;
-    for (auto& rr : h->regions)
-        if (rr.ok) okregs.push_back(rr.r);
-    if (!verified) st = hash_regions_sync(ctx, okregs, got, nullptr, nullptr, nullptr, ctx->copy_stream);
-    if (st != KC_OK) {
-        rollback(h);
-        delete h;
-        return st;
-    }
-    {
-        uint64_t c = 0, mism = 0;
-        for (auto& sr : d.regions) {
-            if (!sr.ok) continue;
-            if (sr.manifest.size() != sr.n_chunks) {
-                mism += sr.n_chunks;
-            } else {
-                for (uint64_t k = 0; k < sr.n_chunks; ++k) mism += sr.manifest[k] != got[c + k];
-            }
-            c += sr.n_chunks;
-        }
-        rep.verify_mismatch_chunks = mism;
-    }
-    rep.t_verify_s = now_s() - t;
-    if (rep.verify_mismatch_chunks) {
+    const kc_status st0 = restore_fill(ctx, h, d, src, rep);
+    if (st0 != KC_OK) {
         if (rep_out) *rep_out = rep;
         rollback(h);
         delete h;
-        return set_err(ctx, KC_ERR_MANIFEST_MISMATCH, "kc_restore: %llu restored chunk(s) do not match the captured "
-                       "manifest", (unsigned long long)rep.verify_mismatch_chunks);
-    }
-
-    trace("restore: verify", tl);
-    // ---- device stashes of the written chunks: replay recopy (pre) and validation reference (post)
-    st = build_stash(ctx, h, d, src);
-    trace("restore: W stashes", tl);
-    if (st != KC_OK) {
-        rollback(h);
-        delete h;
-        return st;
+        return st0;
     }
     rep.t_total_s = now_s() - t0;
     if (rep_out) *rep_out = rep;
@@ -2445,6 +2442,57 @@ extern "C" kc_status kc_restore_dev(kc_ctx* ctx, const kc_snapshot* s, kc_restor
     DevSource src(s);
     kc_status st = restore_core(ctx, s->desc, src, out, rep_out, rep, t0);
     if (st == KC_OK) (*out)->dev_snap = s;
+    return st;
+}
+
+extern "C" kc_status kc_restore_dev_into(kc_ctx* ctx, const kc_snapshot* s, kc_restored* h,
+                                        kc_restore_report* rep_out) {
+    ::kc::Internal _kc_internal_guard(__func__);  // the CUPTI hook ignores our own driver calls
+    if (!ctx || !s || !h) return KC_ERR_ARG;
+    if (ctx->poisoned) return KC_ERR_CUDA;
+    if (s->ctx != ctx || h->ctx != ctx)
+        return set_err(ctx, KC_ERR_ARG, "kc_restore_dev_into: snapshot and restore must live on this ctx");
+    const SnapDesc& d = s->desc;
+    if (d.regions.size() != h->regions.size())
+        return set_err(ctx, KC_ERR_ARG, "kc_restore_dev_into: %zu regions in the snapshot, %zu in the restore",
+                       d.regions.size(), h->regions.size());
+    for (size_t i = 0; i < d.regions.size(); ++i) {
+        const auto& sr = d.regions[i];
+        const auto& rr = h->regions[i];
+        if (sr.r.base != rr.r.base || sr.r.size != rr.r.size || sr.ok != rr.ok)
+            return set_err(ctx, KC_ERR_ARG, "kc_restore_dev_into: region %zu (%#llx, %llu B) is not the live "
+                           "restore's", i, (unsigned long long)sr.r.base, (unsigned long long)sr.r.size);
+    }
+    if (!bind_device(ctx)) return set_err(ctx, KC_ERR_CUDA, "cannot bind device");
+    kc_restore_report rep;
+    memset(&rep, 0, sizeof rep);
+    const double t0 = now_s();
+    rep.n_regions = d.regions.size();
+    for (auto& sr : d.regions)
+        if (!sr.ok) rep.n_failed_regions++;
+    rep.n_spans = h->spans.size();
+    // the live restore takes this snapshot's dispatch, written sets and post manifests
+    if (h->stash_pre) cudaFree(h->stash_pre);
+    h->stash_pre = h->stash_ref = nullptr;
+    h->stash_bytes = 0;
+    if (h->module && h->image != d.image) {  // another code object: the next replay reloads it
+        KC_DRV(cuModuleUnload)(h->module);
+        h->module = nullptr;
+    }
+    h->modvar_checked = h->modvar_mismatch = 0;
+    bind_dispatch_fields(h, d);
+    for (size_t i = 0; i < d.regions.size(); ++i) {
+        auto& rr = h->regions[i];
+        rr.hexbase = d.regions[i].hx;
+        rr.n_chunks = d.regions[i].n_chunks;
+        rr.written = d.regions[i].written;
+        rr.post_manifest = d.regions[i].post_manifest;
+    }
+    DevSource src(s);
+    const kc_status st = restore_fill(ctx, h, d, src, rep);
+    rep.t_total_s = now_s() - t0;
+    if (rep_out) *rep_out = rep;
+    if (st == KC_OK) h->dev_snap = s;
     return st;
 }
 

@@ -43,7 +43,8 @@ EXPORTED = [
     "kc_hash_plan_create", "kc_hash_plan_run", "kc_hash_plan_chunks", "kc_hash_plan_destroy",
     "kc_diff_plan_create", "kc_diff_plan_run", "kc_diff_plan_destroy",
     "kc_written", "kc_diff_async", "kc_hash_diff_async", "kc_diff", "kc_capture", "kc_restore", "kc_prereserve", "kc_replay",
-    "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_snapshot_save",
+    "kc_validate", "kc_restored_regions", "kc_release", "kc_capture_dev", "kc_restore_dev", "kc_restore_dev_into",
+    "kc_snapshot_save",
     "kc_snapshot_bytes", "kc_snapshot_free", "kc_capture_host", "kc_host_arena_reserve", "kc_snapshot_is_host",
     "kc_capture_incr", "kc_snapshot_shared_bytes", "kc_validate_module_vars",
     "kc_snapshot_publish", "kc_dev_arena_reserve", "kc_validate_host_ref",
@@ -206,6 +207,7 @@ def lib() -> ctypes.CDLL:
         "kc_release": (None, [V]),
         "kc_capture_dev": (st, [V, P(Dispatch), P(Region), SZ, ctypes.c_int, P(V), P(CaptureReport)]),
         "kc_restore_dev": (st, [V, V, P(V), P(RestoreReport)]),
+        "kc_restore_dev_into": (st, [V, V, V, P(RestoreReport)]),
         "kc_snapshot_save": (st, [V, V, ctypes.c_char_p]),
         "kc_snapshot_publish": (st, [V, V, ctypes.c_char_p]),
         "kc_snapshot_bytes": (U64, [V]),
@@ -779,6 +781,16 @@ class Context:
             e.report = rep.as_dict()
             raise e
         return Restored(h.value, self), rep.as_dict()
+
+    def restore_dev_into(self, snap: DevSnapshot, restored: Restored) -> dict:
+        """kc_restore_dev_into: the snapshot restored over a live restore of the same regions."""
+        rep = RestoreReport()
+        rc = lib().kc_restore_dev_into(self._h, snap.handle, restored.handle, ctypes.byref(rep))
+        if rc != KC_OK:
+            e = KcError(rc, f"kc_restore_dev_into: {self.last_error()}")
+            e.report = rep.as_dict()
+            raise e
+        return rep.as_dict()
 
     def restore(self, directory: str) -> tuple[Restored, dict]:
         h = ctypes.c_void_p()

@@ -253,6 +253,57 @@ def devsnap(a):
     print(json.dumps(out))
 
 
+def devsnap_inplace(a):
+    """kc_restore_dev_into: restore c1 once (kc_restore_dev), then `cycles` times capture
+    from the restored state and restore the new snapshot over the live restore (no VA or
+    physical operations); every replay must reproduce the output its capture observed, and
+    a snapshot of other regions is refused."""
+    ctx = kc.Context(0)
+    sizes = [s.size for s in synth.C1_SPECS]
+    vas = [ctx.alloc(sz) for sz in sizes]
+    nodes_va, heads_va, out_va = vas
+    for va, arr in zip(vas, synth.c1_fill(nodes_va)):
+        _upload(va, arr)
+    image = open(synth.FIXTURE_CUBIN, "rb").read()
+    disp = dict(image=image, mangled="kc_fixture_walk", grid=(32, 1, 1), block=(256, 1, 1),
+                kernarg=synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=int(a.mutate)), mode=kc.KC_MODE_PRE_W,
+                regions=sorted(zip(vas, sizes)))
+    snap, rep = ctx.capture_dev(**disp)
+    for va in vas:
+        ctx.free(va)
+    r, rrep = ctx.restore_dev(snap)
+    snap.free()
+    out = {"cycles": []}
+    for c in range(a.cycles):
+        _upload(out_va, np.zeros(sizes[2], dtype=np.uint8))  # a fresh output buffer: W != {}
+        snap, rep = ctx.capture_dev(**disp)
+        seen = _download(out_va, sizes[2])
+        rrep = ctx.restore_dev_into(snap, r)
+        after_restore = _download(out_va, sizes[2])
+        cyc = {"capture": rep, "restore": rrep, "regions": [[x.base, x.size] for x in r.regions()],
+               "restored_pre": bool(np.array_equal(after_restore, np.zeros(sizes[2], dtype=np.uint8))),
+               "replay": ctx.replay(r)}
+        cyc["out_equal"] = bool(np.array_equal(_download(out_va, sizes[2]), seen))
+        cyc["validate"], cyc["unexpected_chunks"] = ctx.validate(r)
+        out["cycles"].append(cyc)
+        snap.free()
+    # a snapshot of other regions is refused
+    other = ctx.alloc(65536)
+    _upload(other, np.ones(65536, dtype=np.uint8))
+    snap_o, _ = ctx.capture_dev(image=image, mangled="kc_fixture_walk", grid=(1, 1, 1), block=(32, 1, 1),
+                                kernarg=synth.c1_kernarg(heads_va, out_va, nodes_va, mutate=0),
+                                mode=kc.KC_MODE_PRE_W, regions=[(other, 65536)])
+    try:
+        ctx.restore_dev_into(snap_o, r)
+        out["refused"] = False
+    except kc.KcError as e:
+        out["refused"] = e.status == kc.KC_ERR_ARG
+    snap_o.free()
+    r.release()
+    out["vas"] = vas
+    print(json.dumps(out))
+
+
 def incr(a):
     """F2 incremental capture: a full capture, then one against it (only the
     chunks the first dispatch wrote are copied), the base freed, the second
@@ -574,7 +625,7 @@ def main():
     p.add_argument("--bad-dir", action="store_true")
     a = p.parse_args()
     {"capture-c1": capture_c1, "capture-c2": capture_c2, "replay": replay, "recapture": recapture,
-     "inproc": inproc, "devsnap": devsnap, "incr": incr, "capture-modvar": capture_modvar,
+     "inproc": inproc, "devsnap": devsnap, "devsnap-inplace": devsnap_inplace, "incr": incr, "capture-modvar": capture_modvar,
      "publish": publish, "interpose": interpose, "interpose-seq": interpose_seq, "load-replay": load_replay,
      "load-seq": load_seq, "interpose-graph": interpose_graph,
      "capture-gap": capture_gap}[a.cmd](a)

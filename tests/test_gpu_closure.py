@@ -300,6 +300,25 @@ def test_device_snapshot_capture_restore_replay(tmp_path, mode, mutate, host):
         assert np.array_equal(np.load(str(tmp_path / "dev_orig_out.npy")), pred[out_va])
 
 
+@pytest.mark.parametrize("mutate", [False, True])
+def test_device_snapshot_restored_into_the_live_restore(tmp_path, mutate):
+    """kc_restore_dev_into (the repeated-replay fast path): each cycle captures from the
+    restored state and restores the new snapshot over the live restore's mappings; the
+    restore puts back the pre-state (the zeroed output), the replay reproduces the output
+    the capture observed (with the mutating walk the state moves on every cycle), validate
+    is clean, and a snapshot of other regions is refused with KC_ERR_ARG."""
+    d = str(tmp_path / "inplace")
+    os.makedirs(d, exist_ok=True)
+    res = run("devsnap-inplace", d, "--cycles", "3", *(["--mutate"] if mutate else []))
+    assert len(res["cycles"]) == 3 and res["refused"]
+    for cyc in res["cycles"]:
+        assert cyc["regions"] == res["cycles"][0]["regions"]
+        assert cyc["capture"]["written_chunks"] > 0
+        assert cyc["restore"]["verify_mismatch_chunks"] == 0 and cyc["restore"]["mapped_bytes"] == 0
+        assert cyc["restored_pre"] and cyc["out_equal"]
+        assert all(r["differing_bytes"] == 0 for r in cyc["validate"]) and cyc["unexpected_chunks"] == 0
+
+
 @pytest.mark.parametrize("host", [False, True])
 def test_incremental_capture_shares_unchanged_chunks(tmp_path, host):
     """F2 incremental capture: against a full base, only the chunks whose
