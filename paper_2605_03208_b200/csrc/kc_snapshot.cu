@@ -1015,8 +1015,15 @@ uint64_t phys_park_max() {
     }();
     return m;
 }
+uint64_t phys_park_min() {  // spans below this size are released, not parked
+    static const uint64_t m = [] {
+        const char* e = getenv("KC_PHYS_PARK_MIN");
+        return e && *e ? strtoull(e, nullptr, 10) : 0ull;
+    }();
+    return m;
+}
 void phys_release(kc_ctx* ctx, CUmemGenericAllocationHandle h, uint64_t size) {
-    if (ctx && phys_park_on() && ctx->phys_park_bytes + size <= phys_park_max()) {
+    if (ctx && phys_park_on() && size >= phys_park_min() && ctx->phys_park_bytes + size <= phys_park_max()) {
         ctx->phys_park.emplace(size, h);
         ctx->phys_park_bytes += size;
         return;
